@@ -1,0 +1,324 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.
+
+Plain CPU reference of the GS-SLAM RGB-D splatting renderer (arXiv 2311.11700). Only
+`tests/`, `__graft_entry__.smoke()` and `bench.py`'s cpu_baseline / `--impl reference` legs may
+import this package. It shares no code with `paper_2311_11700_b200` (neither imports the other).
+
+  * projection, binning, forward, backward: `oracle.cpp` (C++17 + OpenMP, ctypes), O1-O4
+  * loss, Adam, pose step, densify/prune/select: numpy fp64 below, O5
+
+Parity unpinned: none of the functions here (each is pinned by tests/test_oracle_*.py; see
+DESIGN.md §4 for the pin of every function).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = os.path.join(_HERE, "oracle.cpp")
+
+GFLAGS = ["-O2", "-std=c++17", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC"]
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so (plain g++; no CUDA)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        subprocess.check_call(["g++", *GFLAGS, _SRC, "-o", _SO])
+    return _SO
+
+
+class OracleCam(ctypes.Structure):
+    _fields_ = [("fx", ctypes.c_double), ("fy", ctypes.c_double), ("cx", ctypes.c_double),
+                ("cy", ctypes.c_double), ("width", ctypes.c_int32), ("height", ctypes.c_int32),
+                ("znear", ctypes.c_double), ("bg", ctypes.c_double * 3), ("dil", ctypes.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+    return _lib
+
+
+def _cam(cam) -> OracleCam:
+    c = OracleCam()
+    c.fx, c.fy, c.cx, c.cy = cam.fx, cam.fy, cam.cx, cam.cy
+    c.width, c.height = cam.width, cam.height
+    c.znear = cam.znear
+    for k in range(3):
+        c.bg[k] = cam.bg[k]
+    c.dil = cam.cov2d_dilation
+    return c
+
+
+def _p(a):
+    return ctypes.c_void_p(a.ctypes.data) if a is not None else None
+
+
+def _dtype(precision: str):
+    return {"f32": np.float32, "f64": np.float64}[precision]
+
+
+def set_threads(n: int) -> None:
+    lib().oracle_set_threads(ctypes.c_int(n))
+
+
+def num_threads() -> int:
+    return int(lib().oracle_num_threads())
+
+
+def grid(cam) -> tuple[int, int]:
+    return (cam.width + 15) // 16, (cam.height + 15) // 16
+
+
+# ------------------------------------------------------------------------------------ O1
+def project(params, view, cam, precision="f32") -> dict:
+    """O1 (Eq. 2-3): per-Gaussian projection. params [14][n], view [3][4]."""
+    dt = _dtype(precision)
+    params = np.ascontiguousarray(params, dt)
+    view = np.ascontiguousarray(view, dt)
+    n = params.shape[1]
+    out = dict(mean2d=np.zeros((2, n), dt), conic=np.zeros((3, n), dt), depth=np.zeros(n, dt),
+               radius=np.zeros(n, np.int32), rect=np.zeros((4, n), np.int32), tiles=np.zeros(n, np.uint32),
+               depth_bits=np.zeros(n, np.uint32), cov2d=np.zeros((3, n), dt))
+    c = _cam(cam)
+    fn = getattr(lib(), f"oracle_project_{precision}")
+    fn(_p(params), ctypes.c_int64(n), ctypes.c_int64(n), _p(view), ctypes.byref(c), _p(out["mean2d"]),
+       _p(out["conic"]), _p(out["depth"]), _p(out["radius"]), _p(out["rect"]), _p(out["tiles"]),
+       _p(out["depth_bits"]), _p(out["cov2d"]))
+    return out
+
+
+# ------------------------------------------------------------------------------------ O2
+def bin_sort(depth_bits, rect, tiles, cam) -> dict:
+    """O2: keys (tile<<32 | depth bits) emitted in index order, stable-sorted; per-tile ranges."""
+    gx, gy = grid(cam)
+    depth_bits = np.ascontiguousarray(depth_bits, np.uint32)
+    rect = np.ascontiguousarray(rect, np.int32)
+    tiles = np.ascontiguousarray(tiles, np.uint32)
+    n = depth_bits.shape[0]
+    k = int(tiles.astype(np.int64).sum())
+    keys = np.zeros(k, np.uint64)
+    vals = np.zeros(k, np.uint32)
+    ranges = np.zeros((gx * gy, 2), np.uint32)
+    got = lib().oracle_bin
+    got.restype = ctypes.c_int64
+    kk = got(_p(depth_bits), _p(rect), _p(tiles), ctypes.c_int64(n), ctypes.c_int32(gx), ctypes.c_int32(gy),
+             _p(keys), _p(vals), _p(ranges), ctypes.c_int64(k))
+    assert kk == k
+    return dict(keys=keys, vals=vals, ranges=ranges, n_keys=k)
+
+
+# ------------------------------------------------------------------------------------ O3
+def forward(params, view, cam, precision="f32", pixels=None, replay_nlast=None, accum_weight=False) -> dict:
+    """O3 (Eq. 4-5, cumulative opacity P:118). Full images unless `pixels` (linear ids) given."""
+    dt = _dtype(precision)
+    params = np.ascontiguousarray(params, dt)
+    view = np.ascontiguousarray(view, dt)
+    n = params.shape[1]
+    if pixels is not None:
+        pixels = np.ascontiguousarray(pixels, np.int64)
+        npx = pixels.shape[0]
+        shape = (npx,)
+    else:
+        npx = cam.width * cam.height
+        shape = (cam.height, cam.width)
+    color = np.zeros((3, npx), np.float64)
+    depth = np.zeros(npx, np.float64)
+    alpha = np.zeros(npx, np.float64)
+    n_last = np.zeros(npx, np.uint32)
+    examined = np.zeros(npx, np.uint32)
+    amb = np.zeros(npx, np.uint8)
+    h = np.zeros(1, np.uint64)
+    aw = np.zeros(n, np.float64) if accum_weight else None
+    rp = np.ascontiguousarray(replay_nlast, np.uint32).reshape(-1) if replay_nlast is not None else None
+    c = _cam(cam)
+    getattr(lib(), f"oracle_forward_{precision}")(
+        _p(params), ctypes.c_int64(n), ctypes.c_int64(n), _p(view), ctypes.byref(c), _p(pixels),
+        ctypes.c_int64(npx), _p(rp), _p(color), _p(depth), _p(alpha), _p(n_last), _p(examined), _p(amb),
+        _p(h), _p(aw))
+    out = dict(color=color.reshape((3,) + shape), depth=depth.reshape(shape), alpha=alpha.reshape(shape),
+               n_last=n_last.reshape(shape), examined=examined.reshape(shape), ambiguous=amb.reshape(shape),
+               hash=int(h[0]))
+    if accum_weight:
+        out["accum_weight"] = aw
+    return out
+
+
+# ------------------------------------------------------------------------------------ O4
+def backward(params, view, cam, dL_dcolor, dL_ddepth, precision="f32", replay_nlast=None, qt_cov=True) -> dict:
+    """O4 (Eq. 11, S1-S6): fp64 gradients for the 14 params, screen grads, and the pose.
+
+    pose_twist: (rho, phi) left-perturbation twist, covariance path included (reading C7);
+    pose_twist_paper: same without the Sigma'-through-pose term (paper mode);
+    pose_qt: dL/d(q_r,q_i,q_j,q_k,t) via Eq. S1/S3 (independent path), plus the pose quaternion.
+    """
+    dt = _dtype(precision)
+    params = np.ascontiguousarray(params, dt)
+    view = np.ascontiguousarray(view, dt)
+    n = params.shape[1]
+    dc = np.ascontiguousarray(dL_dcolor, np.float32).reshape(-1)
+    dd = np.ascontiguousarray(dL_ddepth, np.float32).reshape(-1)
+    gp = np.zeros((14, n), np.float64)
+    gs = np.zeros((10, n), np.float64)
+    tw = np.zeros(6, np.float64)
+    twp = np.zeros(6, np.float64)
+    qt = np.zeros(11, np.float64)
+    rp = np.ascontiguousarray(replay_nlast, np.uint32).reshape(-1) if replay_nlast is not None else None
+    c = _cam(cam)
+    getattr(lib(), f"oracle_backward_{precision}")(
+        _p(params), ctypes.c_int64(n), ctypes.c_int64(n), _p(view), ctypes.byref(c), _p(dc), _p(dd), _p(rp),
+        _p(gp), _p(gs), _p(tw), _p(twp), _p(qt), ctypes.c_int32(1 if qt_cov else 0))
+    return dict(grad_params=gp, grad_screen=gs, pose_twist=tw, pose_twist_paper=twp,
+                pose_q=qt[0:4], pose_t=qt[4:7], pose_quat=qt[7:11])
+
+
+# ------------------------------------------------------------------------------------ O5 (numpy fp64)
+def loss_l1(color, depth, tgt_color, tgt_depth, w_color=0.9, w_depth=0.1) -> dict:
+    """Eq. 6 as means (reading C20): L = w_c/(3HW) sum|C-C*| + w_d/#valid sum_valid|D-D*|.
+    dL/dC = w_c/(3HW) sign(C-C*), sign(0)=0; dL/dD likewise over valid pixels (D* > 0)."""
+    c = np.asarray(color, np.float64)
+    d = np.asarray(depth, np.float64)
+    tc = np.asarray(tgt_color, np.float64)
+    td = np.asarray(tgt_depth, np.float64)
+    h, w = d.shape
+    valid = td > 0
+    nvalid = int(valid.sum())
+    sc = w_color / (3.0 * h * w)
+    sd = w_depth / nvalid if nvalid > 0 else 0.0
+    loss = sc * np.abs(c - tc).sum() + sd * np.abs(d - td)[valid].sum()
+    return dict(loss=loss, dL_dcolor=sc * np.sign(c - tc), dL_ddepth=sd * np.sign(d - td) * valid, n_valid=nvalid)
+
+
+RAW_ACT = ("id",) * 3 + ("exp",) * 3 + ("id",) * 4 + ("sigmoid",) + ("id",) * 3
+
+
+def activate(raw) -> np.ndarray:
+    """Raw (log-scale, logit-opacity) -> activated parameters (reading C18)."""
+    raw = np.asarray(raw, np.float64)
+    act = raw.copy()
+    act[3:6] = np.exp(raw[3:6])
+    act[10] = 1.0 / (1.0 + np.exp(-raw[10]))
+    return act
+
+
+def adam_step(raw, grad_act, m, v, lr, step, b1=0.9, b2=0.999, eps=1e-8) -> dict:
+    """Textbook Adam (betas/eps unstated -> 0.9/0.999/1e-8) in raw space with the
+    activation chain rule: d/dlog s = s d/ds, d/dlogit o = o(1-o) d/do. lr: 14 per-row rates."""
+    raw = np.asarray(raw, np.float64)
+    g = np.asarray(grad_act, np.float64).copy()
+    act = activate(raw)
+    g[3:6] *= act[3:6]
+    g[10] *= act[10] * (1.0 - act[10])
+    m = b1 * np.asarray(m, np.float64) + (1 - b1) * g
+    v = b2 * np.asarray(v, np.float64) + (1 - b2) * g * g
+    mh = m / (1 - b1 ** step)
+    vh = v / (1 - b2 ** step)
+    lr = np.asarray(lr, np.float64).reshape(14, 1)
+    new_raw = raw - lr * mh / (np.sqrt(vh) + eps)
+    return dict(raw=new_raw, act=activate(new_raw), m=m, v=v)
+
+
+def skew(w):
+    return np.array([[0.0, -w[2], w[1]], [w[2], 0.0, -w[0]], [-w[1], w[0], 0.0]])
+
+
+def se3_exp(delta) -> np.ndarray:
+    """exp of the twist (rho, phi) as a 3x4 [R | t] (Rodrigues; V(phi) rho)."""
+    rho = np.asarray(delta[:3], np.float64)
+    phi = np.asarray(delta[3:], np.float64)
+    th = float(np.linalg.norm(phi))
+    K = skew(phi)
+    if th < 1e-12:
+        R = np.eye(3) + K
+        V = np.eye(3) + 0.5 * K
+    else:
+        R = np.eye(3) + math.sin(th) / th * K + (1 - math.cos(th)) / th ** 2 * K @ K
+        V = np.eye(3) + (1 - math.cos(th)) / th ** 2 * K + (th - math.sin(th)) / th ** 3 * K @ K
+    out = np.empty((3, 4))
+    out[:, :3] = R
+    out[:, 3] = V @ rho
+    return out
+
+
+def apply_twist(delta, view) -> np.ndarray:
+    """Left perturbation T <- exp(delta^) T of a world->camera 3x4 (DESIGN.md pose convention)."""
+    e = se3_exp(delta)
+    v = np.asarray(view, np.float64)
+    out = np.empty((3, 4))
+    out[:, :3] = e[:, :3] @ v[:, :3]
+    out[:, 3] = e[:, :3] @ v[:, 3] + e[:, 3]
+    return out
+
+
+def pose_adam_step(view, grad_twist, m6, v6, step, lr_rho, lr_phi, b1=0.9, b2=0.999, eps=1e-8) -> dict:
+    """Adam on the twist (reading C23), then T <- exp(delta^) T ("FusedAdam" on the pose)."""
+    g = np.asarray(grad_twist, np.float64)
+    m6 = b1 * np.asarray(m6, np.float64) + (1 - b1) * g
+    v6 = b2 * np.asarray(v6, np.float64) + (1 - b2) * g * g
+    mh = m6 / (1 - b1 ** step)
+    vh = v6 / (1 - b2 ** step)
+    lr = np.array([lr_rho] * 3 + [lr_phi] * 3)
+    delta = -lr * mh / (np.sqrt(vh) + eps)
+    return dict(view=apply_twist(delta, view), m=m6, v=v6, delta=delta)
+
+
+def densify_add(alpha, depth, tgt_color, tgt_depth, view, cam, tau_alpha=0.5, tau_depth=0.10, stride=2,
+                init_opacity=0.5, max_add=None) -> np.ndarray:
+    """Eq. 8: unreliable iff T < tau_T or |D - D_hat| > tau_D (T = alpha image);
+    restricted to valid target depth and the stride-2 checkerboard ((u+v) % 2 == 0, the HW/2 of
+    Eq. 7), ordered by pixel index; back-projected from the target depth through the inverse
+    pose; init per reading C22. Returns activated params [14][n_add]."""
+    a = np.asarray(alpha, np.float64)
+    d = np.asarray(depth, np.float64)
+    td = np.asarray(tgt_depth, np.float64)
+    tc = np.asarray(tgt_color, np.float64)
+    h, w = a.shape
+    vv, uu = np.mgrid[0:h, 0:w]
+    flag = (td > 0) & ((a < tau_alpha) | (np.abs(td - d) > tau_depth)) & (((uu + vv) % stride) == 0)
+    idx = np.flatnonzero(flag.reshape(-1))
+    if max_add is not None:
+        idx = idx[:max_add]
+    u = (idx % w).astype(np.float64)
+    v = (idx // w).astype(np.float64)
+    z = td.reshape(-1)[idx]
+    xc = np.stack([(u - cam.cx) / cam.fx * z, (v - cam.cy) / cam.fy * z, z])
+    V = np.asarray(view, np.float64)
+    X = V[:, :3].T @ (xc - V[:, 3:4])
+    out = np.zeros((14, idx.size))
+    out[0:3] = X
+    out[3:6] = z * stride / (cam.fx + cam.fy)
+    out[6] = 1.0
+    out[10] = init_opacity
+    out[11:14] = tc.reshape(3, -1)[:, idx]
+    return out
+
+
+def densify_prune_mask(opacity, min_opacity=0.005) -> np.ndarray:
+    """Keep mask of the opacity prune (BASELINE config 4; not in the paper): keep o >= min."""
+    return np.asarray(opacity, np.float64) >= min_opacity
+
+
+def select_mask(mean2d, depth, tiles, accum_weight, tgt_depth, sel_weight=0.5, sel_depth=0.05) -> np.ndarray:
+    """Eq. 12, reading C24: keep iff accumulated alpha*T > sel_weight and
+    |D*(round m) - d| < sel_depth at pixel round(m) = floor(m + 0.5) inside the image, D* > 0."""
+    td = np.asarray(tgt_depth, np.float64)
+    h, w = td.shape
+    m = np.asarray(mean2d, np.float64)
+    u = np.floor(m[0] + 0.5)
+    v = np.floor(m[1] + 0.5)
+    inside = (u >= 0) & (u < w) & (v >= 0) & (v < h) & (np.asarray(tiles) > 0)
+    ui = np.where(inside, u, 0).astype(np.int64)
+    vi = np.where(inside, v, 0).astype(np.int64)
+    dstar = td[vi, ui]
+    return inside & (dstar > 0) & (np.asarray(accum_weight) > sel_weight) & \
+        (np.abs(dstar - np.asarray(depth, np.float64)) < sel_depth)
