@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark of the GS-SLAM hot path on B200 (BASELINE.json metric):
+   fwd+bwd RGB-D render iters/s at 1200x680 with 500k Gaussians (config 2), and Gaussian-px evals/s.
+
+One step = gs_project + gs_bin_sort + gs_render_fwd + gs_loss_l1 + gs_render_bwd over one synthetic
+Replica-shaped frame, inputs resident in HBM. N > 1 (torchrun): independent
+replicas, one frame per rank ("replicas only" for single-frame rendering), time =
+max over ranks. `--impl reference` times the CPU oracle (the reference arm of this tier).
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# algorithmic work per unit (SURVEY.md §8(d) per-unit figures)
+FWD_OPS_PER_EVAL = 20      # FP32 lane-ops per forward Gaussian-pixel evaluation
+BWD_OPS_PER_EVAL = 50      # FP32 lane-ops per backward Gaussian-pixel evaluation
+SORT_BYTES_PER_KEY = 24    # one onesweep pass: read + write (u64 key, u32 value)
+
+
+def load_json(path, default=None):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return default
+
+
+BASELINE = load_json(os.path.join(ROOT, "BASELINE.json"), {})
+METRIC = BASELINE.get("metric", "fwd+bwd RGB-D render iters/s (1200x680, 500k Gaussians); Gaussian-px evals/s")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--binsort", default="bucket", choices=["bucket", "keys"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="timed loop only (for ncu launch lists)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.lines: list[str] = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.15)
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------------- dist
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def init_dist(world, backend):
+    import torch.distributed as dist
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group(backend)
+    return dist if world > 1 else None
+
+
+# ----------------------------------------------------------------------------------- reference arm
+def cpu_sample(cfg, frac_rows=16):
+    """Bounded oracle sample of one config-`cfg` iteration: every `frac_rows`-th pixel row."""
+    import numpy as np
+    import gs_inputs as gi
+    import oracle
+    cam = cfg.cam
+    rows = np.arange(0, cam.height, frac_rows)
+    px = (rows[:, None] * cam.width + np.arange(cam.width)[None, :]).reshape(-1)
+    p, v = cfg.scene(), cfg.view()
+    tc, td = gi.random_images(cam.width, cam.height, 77)
+
+    def run():
+        f = oracle.forward(p, v, cam, "f32", pixels=px)
+        L = oracle.loss_l1(f["color"].reshape(3, 1, -1), f["depth"].reshape(1, -1), tc.reshape(3, -1)[:, px][:, None],
+                           td.reshape(-1)[px][None], cfg.w_color, cfg.w_depth)
+        dc = np.zeros((3, cam.height * cam.width), np.float32)
+        dd = np.zeros(cam.height * cam.width, np.float32)
+        dc[:, px] = L["dL_dcolor"].reshape(3, -1)
+        dd[px] = L["dL_ddepth"].reshape(-1)
+        oracle.backward(p, v, cam, dc, dd, "f32", pixels=px)
+    return run, px.size / (cam.width * cam.height), f"every {frac_rows}th pixel row ({px.size} px) of one " \
+        f"config-{2} fwd+bwd iteration; value scaled to whole iterations"
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import gs_inputs as gi
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    oracle.set_threads(cores)
+    cfg = gi.CONFIGS[args.config]
+    run, frac, desc = cpu_sample(cfg)
+    for _ in range(max(args.warmup, 0)):
+        run()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run()
+    dt = (time.perf_counter() - t0) / max(args.steps, 1)
+    value = frac / dt
+    line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3 / frac, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"config {args.config}: {cfg.name} {cfg.cam.width}x{cfg.cam.height}, {cfg.n} Gaussians"},
+            "cpu_baseline": {"value": value, "unit": "iters/s", "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------------- our arm
+def main_ours(args):
+    import numpy as np
+    import torch
+
+    import gs_inputs as gi
+    import paper_2311_11700_b200 as g
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = init_dist(world, "nccl")
+    dev = torch.device("cuda", local)
+    cfg = gi.CONFIGS[args.config]
+    cam = cfg.cam
+    n = cfg.n
+    p = cfg.scene()
+    v = cfg.view()
+    P = torch.as_tensor(p, device=dev)
+    V = torch.as_tensor(v, device=dev)
+    bin_flags = g.GS_FLAG_BINSORT_KEYS if args.binsort == "keys" else 0
+
+    # ---- setup (untimed): target = render of a second seeded scene at the same pose (config 2)
+    probe = g.RenderPipeline(n, 1 << 26, cam.width, cam.height, dev)
+    tgt_seed = cfg.target_seed if cfg.target_seed is not None else cfg.scene_seed + 1
+    Pt = torch.as_tensor(gi.gaussians(n, tgt_seed, cfg.lo, cfg.hi), device=dev)
+    fr_t = probe.forward(Pt, n, V, cam, bin_flags=bin_flags)
+    tc, td = fr_t.color.clone(), fr_t.depth.clone()
+    fr = probe.forward(P, n, V, cam, bin_flags=bin_flags, fwd_flags=g.GS_FLAG_EXAMINED)
+    a = probe.arrays(n)
+    K = fr.n_keys
+    E_f = int(a["examined"].to(torch.int64).sum().item())
+    E_b = int(a["n_last"].to(torch.int64).sum().item())
+    V_s = int((a["tiles"] > 0).sum().item())
+    V_front = int((a["radius"] > 0).sum().item())
+    del probe
+    torch.cuda.empty_cache()
+    key_cap = int(max(K, fr_t.n_keys) * 1.1) + 65536
+    pipe = g.RenderPipeline(n, key_cap, cam.width, cam.height, dev)
+    grad = torch.zeros_like(P)
+    gpose = torch.zeros(6, dtype=torch.float64, device=dev)
+    flags = bin_flags | g.GS_FLAG_NO_HOST_SYNC
+
+    def step():
+        grad.zero_()
+        gpose.zero_()
+        pipe.iteration(P, n, V, cam, tc, td, grad, gpose, bin_flags=flags, fwd_flags=0)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    def timed(fn, steps):
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1) / steps
+        if dist:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    l0 = pipe.ws.launches()
+    with ClockSampler(local) as clk:
+        ms = timed(step, args.steps)
+    launches = (pipe.ws.launches() - l0) // args.steps
+    err = int(pipe.arrays()["error_flag"].item())
+    assert err == 0, "device-side key capacity overflow during the timed region"
+    clocks = clk.summary()
+    value = world * 1000.0 / ms
+    out = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Replica-shaped room scene, SURVEY.md §8(d))",
+           "config": {"workload": f"config {args.config}: {cfg.name} {cam.width}x{cam.height}, {n} Gaussians, "
+                                  f"fwd+bwd L1 (0.9/0.1) iteration", "n_gaussians": n, "width": cam.width,
+                      "height": cam.height, "keys": K, "visible": V_front, "on_screen": V_s, "E_f": E_f, "E_b": E_b,
+                      "binsort": args.binsort, "l2": "per-iteration working set > L2 (keys+values ~"
+                      f"{K * 24 / 1e9:.2f} GB); no flush", "parallelism": f"replicas x{world}"},
+           "evals_per_s": world * (E_f + E_b) * 1000.0 / ms, "clocks": clocks, "gpu_launches": int(launches)}
+
+    if not args.quick:
+        # ---- per-kernel times over a second timed region (event log on the launching stream)
+        steps2 = min(args.steps, 20)
+        log = g.EventLog(pipe.ws, steps2 * 64)
+        with log:
+            ms_logged = timed(step, steps2)
+        kern = {}
+        for name, t in log.read():
+            d = kern.setdefault(name, [0.0, 0])
+            d[0] += t
+            d[1] += 1
+        log.close()
+        per_step = {k: (v_[0] / steps2, v_[1] / steps2) for k, v_ in kern.items()}
+        out["kernels_ms_per_step"] = {k: round(v_[0], 4) for k, v_ in sorted(per_step.items(), key=lambda x: -x[1][0])}
+        out["kernels_launches_per_step"] = {k: v_[1] for k, v_ in per_step.items()}
+        out["ms_per_step_with_event_log"] = ms_logged
+        out["roofline"] = roofline(per_step, clocks, K=K, n=n, V_s=V_s, E_f=E_f, E_b=E_b,
+                                   npx=cam.width * cam.height)
+        # ---- e2e through the public API with host buffers (pinned) and a loss readback
+        if not args.no_e2e:
+            hp = torch.empty_like(P, device="cpu").pin_memory()
+            hp.copy_(P.cpu())
+            hv = V.cpu().pin_memory()
+            htc, htd = tc.cpu().pin_memory(), td.cpu().pin_memory()
+            hloss = torch.empty(1, dtype=torch.float64).pin_memory()
+            Pd, Vd, tcd, tdd = torch.empty_like(P), torch.empty_like(V), torch.empty_like(tc), torch.empty_like(td)
+
+            def e2e_step():
+                Pd.copy_(hp, non_blocking=True)
+                Vd.copy_(hv, non_blocking=True)
+                tcd.copy_(htc, non_blocking=True)
+                tdd.copy_(htd, non_blocking=True)
+                grad.zero_()
+                gpose.zero_()
+                pipe.iteration(Pd, n, Vd, cam, tcd, tdd, grad, gpose, bin_flags=flags, fwd_flags=0)
+                hloss.copy_(pipe.loss, non_blocking=True)
+            for _ in range(3):
+                e2e_step()
+            ms_e2e = timed(e2e_step, args.steps)
+            h2d = P.numel() * 4 + V.numel() * 4 + tc.numel() * 4 + td.numel() * 4
+            out["e2e"] = {"value": world * 1000.0 / ms_e2e, "unit": "iters/s", "h2d_bytes_per_step": int(h2d),
+                          "d2h_bytes_per_step": 8}
+        # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            try:
+                import oracle
+                cores = len(os.sched_getaffinity(0))
+                oracle.set_threads(cores)
+                run, frac, desc = cpu_sample(cfg)
+                t0 = time.perf_counter()
+                run()
+                dt = time.perf_counter() - t0
+                out["cpu_baseline"] = {"value": frac / dt, "unit": "iters/s", "cores": oracle.num_threads(),
+                                       "kind": "oracle", "sample": desc}
+            except Exception as exc:   # the baseline is reported, never required for our number
+                out["cpu_baseline"] = {"value": None, "unit": "iters/s", "cores": None, "kind": "oracle",
+                                       "sample": f"failed: {exc!r}"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def roofline(per_step, clocks, K, n, V_s, E_f, E_b, npx):
+    peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json"), {}) or {}
+    hbm_peak = peaks.get("hbm_gbs")
+    hbm_src = "measured" if hbm_peak else "fallback"
+    hbm_peak = hbm_peak or 6650.0
+    sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz") or 1965.0
+    alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e12   # FP32 lane-ops/s, T
+    work = {   # (bound, algorithmic amount per step, unit)
+        "render_bwd_tiles": ("alu", E_b * BWD_OPS_PER_EVAL / 1e12, "TFLOP/s"),
+        "render_fwd": ("alu", E_f * FWD_OPS_PER_EVAL / 1e12, "TFLOP/s"),
+        "sort_pass": ("hbm", K * SORT_BYTES_PER_KEY / 1e9, "GB/s"),
+        "emit_keys": ("hbm", (K * 12 + n * 20) / 1e9, "GB/s"),
+        "project": ("hbm", n * (56 + 72) / 1e9, "GB/s"),
+        "gaussian_bwd": ("hbm", (n * 4 + V_s * 244) / 1e9, "GB/s"),
+        "loss_l1": ("hbm", npx * 48 / 1e9, "GB/s"),
+    }
+    dom = max((k for k in per_step if k in work), key=lambda k: per_step[k][0])
+    bound, amount, unit = work[dom]
+    t_ms, launches = per_step[dom]
+    per_launch_amount = amount / max(launches, 1)
+    per_launch_s = t_ms / 1e3 / max(launches, 1)
+    achieved = per_launch_amount / per_launch_s
+    peak = alu_peak if bound == "alu" else hbm_peak
+    traffic = None
+    prof = load_json(os.path.join(ROOT, "profiles", "ncu_traffic.json"), {}) or {}
+    if dom in prof:
+        traffic = prof[dom]
+    return {"kernel": dom, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": achieved / peak, "traffic": traffic,
+            "peak_source": ("FP32 148 SMs x 128 lanes x measured median SM clock %.0f MHz" % sm_mhz)
+            if bound == "alu" else f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})",
+            "share_of_step": t_ms / sum(v[0] for v in per_step.values())}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return main_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

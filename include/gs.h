@@ -1,0 +1,214 @@
+/* gs.h — C ABI of the B200 differentiable RGB-D Gaussian-splatting renderer (GS-SLAM hot path,
+ * arXiv 2311.11700). Library: paper_2311_11700_b200/libgs.so (sm_100a).
+ *
+ * Conventions (all entry points)
+ *  - Pointers are CUDA DEVICE pointers unless marked (host).
+ *  - Every call is asynchronous on `stream` (a cudaStream_t passed as void*; NULL = legacy default
+ *    stream) and never allocates device memory. The caller owns every buffer, including the
+ *    device workspace and the host workspace state `gs_ws` (see gs_ws_init).
+ *  - The library holds no global state; calls on distinct workspaces are independent.
+ *  - Argument errors are detected on the host before any launch (GS_ERR_INVALID_ARG);
+ *    a failed launch returns GS_ERR_CUDA (gs_last_cuda_error() gives the CUDA error string).
+ *  - Gaussian parameters are ACTIVATED values in a structure-of-arrays float32 buffer
+ *    params[14][ld] (row k at params + k*ld), columns 0..n-1:
+ *      rows 0-2  mean X (world, metres)                    Eq. 1 "position X_i"
+ *      rows 3-5  scale s (linear, > 0)                      Eq. 2 "S"
+ *      rows 6-9  rotation quaternion (r,i,j,k), raw; normalised inside gs_project
+ *      row  10   opacity Lambda in (0,1)                    Eq. 1
+ *      rows 11-13 RGB colour (SH degree 0, "light" model)
+ *    Gradients are returned with respect to these 14 activated values.
+ *  - viewmat: float[12] row-major 3x4 WORLD->CAMERA [W | t] (reading C1: X^c = W X + t,
+ *    PAPER.md:626). It is a device pointer so CUDA graphs can update the pose in place.
+ *  - Images are planar float32: colour [3][H][W], depth / alpha [H][W]; pixel (u,v) has its
+ *    centre at integer coordinates (reading C12).
+ *  - Pose gradients are a left-perturbation twist (rho, phi): T <- exp(delta^) T (reading C1/C7).
+ */
+#ifndef GS_H_
+#define GS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GS_OK = 0,
+    GS_ERR_INVALID_ARG = 1,
+    GS_ERR_CAPACITY = 2,     /* key or Gaussian capacity exceeded; required size reported */
+    GS_ERR_STALE = 3,        /* backward on a workspace whose last forward does not match */
+    GS_ERR_CUDA = 4,
+    GS_ERR_UNSUPPORTED = 5
+} gs_status;
+
+/* Pinhole camera + render settings (host struct). */
+typedef struct {
+    float fx, fy, cx, cy;    /* intrinsics K */
+    int32_t width, height;   /* image size; width*height <= the workspace's W*H */
+    float znear;             /* near-plane cull, metres (reading C13: 0.2) */
+    float bg[3];             /* background colour (reading C15: black) */
+    float cov2d_dilation;    /* added to the diagonal of Sigma' (reading C11: 0.3 px^2) */
+} gs_camera;
+
+/* Host-side workspace state: opaque, caller-allocated, initialised by gs_ws_init. */
+typedef struct { uint64_t opaque[128]; } gs_ws;
+
+enum {
+    GS_FLAG_POSE_COV_PATH = 1u,   /* include dSigma'/dpose in pose gradients (reading C7; exact, FD-parity
+                                     default). Off = the paper's approximation */
+    GS_FLAG_NO_HOST_SYNC = 2u,    /* gs_bin_sort: do not read K back; grids sized from key_cap, K stays on
+                                     the device; overflow sets the device error flag (CUDA-graph mode) */
+    GS_FLAG_ACCUM_WEIGHT = 4u,    /* gs_render_fwd: accumulate per-Gaussian sum_px alpha*T (Eq. 12 select) */
+    GS_FLAG_EXAMINED = 8u,        /* gs_render_fwd: write the per-pixel examined count (for E_f) */
+    GS_FLAG_BINSORT_KEYS = 16u    /* gs_bin_sort: emit 64-bit (tile|depth) keys and onesweep-sort them
+                                     (north_star literal path); default = depth-presort + tile bucketing
+                                     (bit-identical lists, fewer HBM bytes) */
+};
+
+/* ---------------------------------------------------------------------------------------------
+ * Workspace. Device bytes needed for up to n_cap Gaussians, key_cap (tile, Gaussian) keys and
+ * images up to W x H pixels. gs_ws_init carves `dev` (>= gs_workspace_bytes, 256-B aligned) and
+ * fills the host state. Ownership stays with the caller; the library never frees.
+ * Errors: GS_ERR_INVALID_ARG on non-positive sizes, misalignment or too few bytes.
+ * ------------------------------------------------------------------------------------------- */
+size_t gs_workspace_bytes(int64_t n_cap, int64_t key_cap, int32_t W, int32_t H);
+gs_status gs_ws_init(gs_ws* ws /*(host)*/, void* dev, size_t dev_bytes, int64_t n_cap, int64_t key_cap,
+                     int32_t W, int32_t H);
+
+/* gs_project — Eq. 2-3, O1: per Gaussian i < n
+ *   X^c = W X + t; cull unless z^c > znear; q_hat = q/|q|; R(q_hat) by Eq. S1;
+ *   Sigma = R diag(s)^2 R^T; Sigma' = (J W) Sigma (J W)^T + dil I with the affine-projection
+ *   Jacobian J; conic = Sigma'^-1; radius r = ceil(3 sqrt(lambda_max)); mean m = (fx x/z + cx,
+ *   fy y/z + cy); 16x16-tile rect of the 3-sigma box; depth d = z^c (Eq. 5 text).
+ * mask: optional u8[n]; mask[i] == 0 culls Gaussian i (coarse-to-fine selection, Eq. 12).
+ * Writes the projected records into the workspace (consumed by gs_bin_sort / gs_render_*).
+ * Culling is a value, not an error (radius 0, no tiles). Bit-exact with the oracle on depth key,
+ * radius, rect and tile count (fixed fp32 operation order, no FMA contraction). */
+gs_status gs_project(const float* params, int64_t n, int64_t ld, const uint8_t* mask /*nullable*/,
+                     const float* viewmat, const gs_camera* cam /*(host)*/, gs_ws* ws, void* stream);
+
+/* gs_bin_sort — tile binning + depth sort ("sorting the Gaussians in depth order", PAPER.md:83;
+ * north_star: 64-bit (tile << 32 | depth-bits) keys, 16x16 tiles). Produces, per tile t, the list
+ * of Gaussian indices whose rect contains t, ordered by (depth bits, index) — the stable ascending
+ * sort of keys emitted in index order (O2) — and ranges[t] = [start, end).
+ * n_keys (host, nullable): receives K. If K > key_cap: returns GS_ERR_CAPACITY with the required K
+ * in *n_keys (host-sync mode) or sets the device error flag (GS_FLAG_NO_HOST_SYNC). */
+gs_status gs_bin_sort(gs_ws* ws, int64_t* n_keys /*(host) out, nullable*/, uint32_t flags, void* stream);
+
+/* gs_render_fwd — Eq. 4-5 and the cumulative opacity of Eq. 8:
+ * per pixel, front to back over its tile's list: alpha = min(0.99, o exp(-1/2 d^T Sigma'^-1 d)),
+ * skip alpha < 1/255, stop before the Gaussian that would take T below 1e-4 (reading C9);
+ * colour = sum c_i alpha_i T_i + T_final bg, depth = sum d_i alpha_i T_i, alpha = 1 - T_final.
+ * accum_weight: float[n] (+=) per-Gaussian sum of alpha_i T_i, written iff GS_FLAG_ACCUM_WEIGHT.
+ * Keeps T_final and the last-contributor position per pixel in the workspace for the backward. */
+gs_status gs_render_fwd(gs_ws* ws, const gs_camera* cam /*(host)*/, float* color, float* depth, float* alpha,
+                        float* accum_weight /*nullable*/, uint32_t flags, void* stream);
+
+/* gs_render_bwd — analytic backward of the last gs_render_fwd on this workspace (Eq. 11,
+ * PAPER.md:155-168; Supplement A, PAPER.md:608-749 incl. Eq. S6): given dL/dcolor [3][H][W] and
+ * dL/ddepth [H][W], ACCUMULATES (+=) dL/dparams into grad_params[14][ld] and, if grad_pose is
+ * non-NULL, dL/d(rho, phi) into grad_pose[6] (fp64). params/viewmat must be those of the forward.
+ * Returns GS_ERR_STALE if gs_project ran after the last gs_render_fwd or n changed. */
+gs_status gs_render_bwd(const float* params, int64_t n, int64_t ld, const float* viewmat, gs_ws* ws,
+                        const gs_camera* cam /*(host)*/, const float* dL_dcolor, const float* dL_ddepth,
+                        float* grad_params /*[14][ld], +=*/, double* grad_pose /*nullable [6], +=*/,
+                        uint32_t flags, void* stream);
+
+/* gs_pose_grad — pose-only backward (Eq. 11; tracking, Alg. 1): same inputs as
+ * gs_render_bwd, ACCUMULATES dL/d(rho, phi) into grad_pose[6]; no per-Gaussian outputs. */
+gs_status gs_pose_grad(const float* params, int64_t n, int64_t ld, const float* viewmat, gs_ws* ws,
+                       const gs_camera* cam /*(host)*/, const float* dL_dcolor, const float* dL_ddepth,
+                       double* grad_pose /*[6] (rho_xyz, phi_xyz), +=*/, uint32_t flags, void* stream);
+
+/* gs_loss_l1 — Eq. 6 as means (reading C20):
+ *   L = w_c/(3HW) sum|C - C*| + w_d/#valid sum_{D*>0}|D - D*|
+ * writes dL/dC = w_c/(3HW) sign(C - C*) (sign(0) = 0), dL/dD likewise on valid pixels, and
+ * loss[0] = L (fp64, device). */
+gs_status gs_loss_l1(const float* color, const float* depth, const float* tgt_color, const float* tgt_depth,
+                     int32_t W, int32_t H, float w_color, float w_depth, float* dL_dcolor, float* dL_ddepth,
+                     double* loss /*[1]*/, gs_ws* ws, void* stream);
+
+/* gs_adam_step — Adam (betas/eps = b1,b2,eps) over params_raw[14][ld] (raw space:
+ * rows 3-5 log-scale, row 10 logit-opacity, others identity) with per-row learning rates lr[14]
+ * (host), using gradients w.r.t. the ACTIVATED values (chain rule fused) and bias correction at
+ * `step` (1-based). Also writes the activated copy params_act[14][ld]. m, v: [14][ld]. */
+gs_status gs_adam_step(float* params_raw, float* params_act, const float* grad_act, float* m, float* v,
+                       int64_t n, int64_t ld, const float lr[14] /*(host)*/, int32_t step, float b1, float b2,
+                       float eps, void* stream);
+
+/* gs_pose_step — Adam on the pose twist (reading C23; "FusedAdam" PAPER.md:954) then
+ * T <- exp(delta^) T applied to viewmat in place (device-only, no host sync). m6, v6: float[6]. */
+gs_status gs_pose_step(float* viewmat, const double* grad_pose, float* m6, float* v6, int32_t step,
+                       float lr_rho, float lr_phi, void* stream);
+
+/* gs_densify_prune — adaptive expansion (Sec. 3.2) and selection (Eq. 12):
+ *  GS_DENSIFY_ADD    Eq. 8: pixel unreliable iff alpha < tau_alpha or |D* - D| > tau_depth, with
+ *                    D* > 0 and (u+v) % stride == 0, in pixel order; back-projected at D* through
+ *                    the inverse pose; init rgb = C*, opacity = init_opacity, quat (1,0,0,0),
+ *                    scale = D* stride/(fx+fy) (reading C22). Appended at columns [n, n+added) of
+ *                    params (and logit/log in params_raw, zero moments); n_dev updated; at most
+ *                    max_add and capacity - n. If add_out != NULL the candidates are (also) written
+ *                    to add_out[14][max_add] and *n_dev is NOT changed (multi-GPU gather mode).
+ *  GS_DENSIFY_PRUNE  drop Gaussians with opacity < min_opacity by stable compaction of params,
+ *                    params_raw, adam_m, adam_v (any of the last three may be NULL); n_dev updated.
+ *  GS_DENSIFY_SELECT Eq. 12 (reading C24): select_mask[i] = accum_weight[i] > sel_weight and
+ *                    |D*(round m_i) - d_i| < sel_depth, using the last gs_project on this ws.
+ * n_dev: device int64 [1] (in/out). All compaction is deterministic. */
+enum { GS_DENSIFY_ADD = 1, GS_DENSIFY_PRUNE = 2, GS_DENSIFY_SELECT = 3 };
+typedef struct {
+    int32_t mode;
+    float tau_alpha, tau_depth, min_opacity, sel_weight, sel_depth, init_opacity;
+    int32_t stride;
+    int64_t max_add;
+} gs_densify_cfg;
+gs_status gs_densify_prune(float* params, float* params_raw /*nullable*/, int64_t* n_dev, int64_t capacity,
+                           int64_t ld, float* adam_m /*nullable*/, float* adam_v /*nullable*/, const float* alpha,
+                           const float* depth, const float* target_rgb, const float* target_depth,
+                           const float* accum_weight, const float* viewmat, const gs_camera* cam /*(host)*/,
+                           const gs_densify_cfg* cfg /*(host)*/, uint8_t* select_mask, float* add_out,
+                           gs_ws* ws, void* stream);
+
+/* Introspection for tests and benchmarks (host struct of device pointers into the workspace). */
+typedef struct {
+    const float* records;        /* [n][12]: mx, my, conic a, b | conic c, opacity, depth, pad | r, g, b, pad */
+    const uint32_t* depth_key;   /* [n] float bits of z^c */
+    const int16_t* rect;         /* [n][4] xlo, xhi, ylo, yhi */
+    const int32_t* radius;       /* [n] */
+    const uint32_t* tiles;       /* [n] tiles touched */
+    const uint64_t* keys;        /* [K] sorted (tile << 32 | depth key); valid after gs_bin_sort */
+    const uint32_t* vals;        /* [K] sorted Gaussian indices */
+    const uint32_t* ranges;      /* [GX*GY][2] */
+    const float* t_final;        /* [H*W] */
+    const uint32_t* n_last;      /* [H*W] 1-based position of the last blended Gaussian (0: none) */
+    const uint32_t* examined;    /* [H*W] (GS_FLAG_EXAMINED) */
+    const uint64_t* n_keys_dev;  /* [1] K on the device */
+    const uint32_t* error_flag;  /* [1] nonzero after a device-side capacity overflow */
+    int64_t n, key_cap, n_cap;
+    int32_t grid_x, grid_y, width, height;
+} gs_ws_view;
+gs_status gs_ws_get_view(const gs_ws* ws, gs_ws_view* out /*(host)*/);
+
+/* Per-launch accounting: number of kernels this library launched on the workspace since init
+ * (host counter; bench.py reports it as gpu_launches). */
+int64_t gs_ws_launch_count(const gs_ws* ws);
+
+/* Optional per-kernel timing (bench.py roofline). While attached, every kernel launch issued on
+ * `ws` is bracketed by cudaEventRecord(events[2k]) / (events[2k+1]) on its stream and its kernel id
+ * is stored in ids[k], for k < capacity (later launches are not logged). events: 2*capacity
+ * cudaEvent_t (host array, e.g. from gs_events_create); capacity 0 detaches. The caller owns both
+ * arrays; read the times with gs_events_elapsed after synchronising. */
+gs_status gs_ws_set_event_log(gs_ws* ws, void** events /*(host)*/, int32_t* ids /*(host)*/, int32_t capacity);
+int32_t gs_ws_event_log_count(const gs_ws* ws);
+gs_status gs_events_create(void** events /*(host) out*/, int32_t count);
+gs_status gs_events_destroy(void** events /*(host)*/, int32_t count);
+gs_status gs_events_elapsed(void* const* events /*(host)*/, int32_t pairs, float* ms /*(host) out [pairs]*/);
+const char* gs_kernel_name(int32_t id);
+
+const char* gs_status_string(gs_status s);
+const char* gs_last_cuda_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GS_H_ */

@@ -155,7 +155,8 @@ def forward(params, view, cam, precision="f32", pixels=None, replay_nlast=None, 
 
 
 # ------------------------------------------------------------------------------------ O4
-def backward(params, view, cam, dL_dcolor, dL_ddepth, precision="f32", replay_nlast=None, qt_cov=True) -> dict:
+def backward(params, view, cam, dL_dcolor, dL_ddepth, precision="f32", replay_nlast=None, qt_cov=True,
+             pixels=None) -> dict:
     """O4 (Eq. 11, S1-S6): fp64 gradients for the 14 params, screen grads, and the pose.
 
     pose_twist: (rho, phi) left-perturbation twist, covariance path included (reading C7);
@@ -174,10 +175,12 @@ def backward(params, view, cam, dL_dcolor, dL_ddepth, precision="f32", replay_nl
     twp = np.zeros(6, np.float64)
     qt = np.zeros(11, np.float64)
     rp = np.ascontiguousarray(replay_nlast, np.uint32).reshape(-1) if replay_nlast is not None else None
+    px = np.ascontiguousarray(pixels, np.int64) if pixels is not None else None
     c = _cam(cam)
     getattr(lib(), f"oracle_backward_{precision}")(
         _p(params), ctypes.c_int64(n), ctypes.c_int64(n), _p(view), ctypes.byref(c), _p(dc), _p(dd), _p(rp),
-        _p(gp), _p(gs), _p(tw), _p(twp), _p(qt), ctypes.c_int32(1 if qt_cov else 0))
+        _p(gp), _p(gs), _p(tw), _p(twp), _p(qt), ctypes.c_int32(1 if qt_cov else 0), _p(px),
+        ctypes.c_int64(0 if px is None else px.shape[0]))
     return dict(grad_params=gp, grad_screen=gs, pose_twist=tw, pose_twist_paper=twp,
                 pose_q=qt[0:4], pose_t=qt[4:7], pose_quat=qt[7:11])
 

@@ -594,14 +594,17 @@ ORACLE_FORWARD(f64, double)
     int oracle_backward_##SUF(const R* params, int64_t n, int64_t ld, const R* view, const OracleCam* oc,      \
                               const float* dLdC, const float* dLdD, const uint32_t* replay_nlast,              \
                               double* grad_params, double* grad_screen, double* pose_twist,                    \
-                              double* pose_twist_paper, double* pose_qt, int32_t qt_cov) {                     \
+                              double* pose_twist_paper, double* pose_qt, int32_t qt_cov,                       \
+                              const int64_t* pixels, int64_t n_pix) {                                          \
         Cam<R> cam(*oc);                                                                                       \
         auto pj = project_all<R>(params, n, ld, view, cam);                                                    \
         auto order = depth_order(pj);                                                                          \
         const int64_t P = int64_t(cam.W) * cam.H;                                                              \
+        const int64_t NQ = pixels ? n_pix : P; /* optional pixel subset (bounded CPU-baseline sample) */       \
         std::vector<ScreenGrad> sg(size_t(n), ScreenGrad{0, 0, 0, 0, 0, 0, 0, 0, 0, 0});                       \
         _Pragma("omp parallel for schedule(dynamic, 64)")                                                     \
-        for (int64_t q = 0; q < P; ++q) {                                                                      \
+        for (int64_t qi = 0; qi < NQ; ++qi) {                                                                  \
+            const int64_t q = pixels ? pixels[qi] : qi;                                                        \
             const int u = int(q % cam.W), v = int(q / cam.W);                                                  \
             PixelResult r;                                                                                     \
             blend_pixel<R>(u, v, pj, order, params, ld, cam, replay_nlast ? int64_t(replay_nlast[q]) : -1,     \

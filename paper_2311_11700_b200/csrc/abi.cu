@@ -1,0 +1,348 @@
+// C ABI entry points of libgs (include/gs.h): argument checks on the host, workspace carving,
+// generation tracking, and dispatch to the kernels. No allocation, no global device state.
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "gs_internal.cuh"
+#include "onesweep.cuh"
+
+namespace gs {
+
+static thread_local std::string g_last_cuda_error;
+
+void set_cuda_error(cudaError_t e, const char* what) {
+    g_last_cuda_error = std::string(what) + ": " + cudaGetErrorString(e);
+}
+
+gs_status check_launch(WsState*, const char* what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_cuda_error(e, what);
+        return GS_ERR_CUDA;
+    }
+    return GS_OK;
+}
+
+struct Carver {
+    uint64_t off = 0;
+    Region take(uint64_t bytes) {
+        Region r{off, bytes};
+        off += (bytes + 255) & ~uint64_t(255);
+        return r;
+    }
+};
+
+static int64_t sort_parts(int64_t key_cap) { return (std::max<int64_t>(key_cap, 1) + kSortTile - 1) / kSortTile; }
+
+static void carve(WsState* s, Carver& c) {
+    const int64_t n = std::max<int64_t>(s->n_cap, 1), K = std::max<int64_t>(s->key_cap, 1);
+    const int64_t px = int64_t(s->W) * s->H;
+    const int64_t tiles = int64_t(s->GX) * s->GY;
+    const int64_t scan_items = std::max(n, px);
+    s->rec = c.take(uint64_t(n) * 48);
+    s->depth_key = c.take(uint64_t(n) * 4);
+    s->rect = c.take(uint64_t(n) * 8);
+    s->radius = c.take(uint64_t(n) * 4);
+    s->tiles = c.take(uint64_t(n) * 4);
+    s->offsets = c.take(uint64_t(n) * 4);
+    s->sgrad = c.take(uint64_t(n) * 4 * 10);
+    s->scan_state = c.take(uint64_t((scan_items + 2047) / 2048 + 1) * 8);
+    s->keys0 = c.take(uint64_t(K) * 8);
+    s->keys1 = c.take(uint64_t(K) * 8);
+    s->vals0 = c.take(uint64_t(K) * 4);
+    s->vals1 = c.take(uint64_t(K) * 4);
+    s->ranges = c.take(uint64_t(tiles) * 8);
+    s->t_final = c.take(uint64_t(px) * 4);
+    s->n_last = c.take(uint64_t(px) * 4);
+    s->examined = c.take(uint64_t(px) * 4);
+    s->sort_hist = c.take(8 * 256 * 4);
+    s->max_parts = std::max(sort_parts(s->key_cap), sort_parts(s->n_cap));
+    s->sort_look = c.take(uint64_t(s->max_parts) * 256 * 8);
+    s->misc = c.take(sizeof(Misc));
+    s->scratch = c.take(uint64_t(px) * 4 * 4);
+    s->scratch14 = c.take(uint64_t(n) * 4 * 14);
+    s->dkey_sorted = c.take(uint64_t(n) * 4 * 2);
+    s->dval_sorted = c.take(uint64_t(n) * 4 * 2);
+    s->chunk_hist = c.take(uint64_t(std::max<int64_t>((n + 2047) / 2048, (px + 2047) / 2048) + 1) * 4 +
+                           uint64_t((n + 1023) / 1024 + 1) * tiles * 4);
+}
+
+static bool ws_ok(const gs_ws* ws) { return ws && state(ws)->magic == kMagic; }
+
+}  // namespace gs
+
+using namespace gs;
+
+extern "C" {
+
+size_t gs_workspace_bytes(int64_t n_cap, int64_t key_cap, int32_t W, int32_t H) {
+    if (n_cap < 0 || key_cap < 0 || W <= 0 || H <= 0) return 0;
+    WsState s{};
+    s.n_cap = n_cap;
+    s.key_cap = key_cap;
+    s.W = W;
+    s.H = H;
+    s.GX = (W + kTile - 1) / kTile;
+    s.GY = (H + kTile - 1) / kTile;
+    Carver c;
+    carve(&s, c);
+    return size_t(c.off);
+}
+
+gs_status gs_ws_init(gs_ws* ws, void* dev, size_t dev_bytes, int64_t n_cap, int64_t key_cap, int32_t W, int32_t H) {
+    if (!ws || !dev || n_cap < 0 || key_cap < 0 || key_cap >= (int64_t(1) << 30) || n_cap >= (int64_t(1) << 31) ||
+        W <= 0 || H <= 0 || (reinterpret_cast<uintptr_t>(dev) & 255))
+        return GS_ERR_INVALID_ARG;
+    if (dev_bytes < gs_workspace_bytes(n_cap, key_cap, W, H)) return GS_ERR_INVALID_ARG;
+    std::memset(ws, 0, sizeof(gs_ws));
+    WsState* s = state(ws);
+    s->magic = kMagic;
+    s->dev = static_cast<char*>(dev);
+    s->dev_bytes = dev_bytes;
+    s->n_cap = n_cap;
+    s->key_cap = key_cap;
+    s->W = W;
+    s->H = H;
+    s->GX = (W + kTile - 1) / kTile;
+    s->GY = (H + kTile - 1) / kTile;
+    Carver c;
+    carve(s, c);
+    s->n_keys_host = -1;
+    s->epoch = 1;
+    // look-back words must not carry a live epoch: clear them once (legacy stream, synchronous)
+    if (cudaMemset(s->dev + s->scan_state.off, 0, s->scan_state.bytes) != cudaSuccess ||
+        cudaMemset(s->dev + s->sort_look.off, 0, s->sort_look.bytes) != cudaSuccess ||
+        cudaMemset(s->dev + s->misc.off, 0, s->misc.bytes) != cudaSuccess) {
+        set_cuda_error(cudaGetLastError(), "gs_ws_init memset");
+        return GS_ERR_CUDA;
+    }
+    return GS_OK;
+}
+
+static bool cam_ok(const WsState* s, const gs_camera* cam) {
+    return cam && cam->width > 0 && cam->height > 0 && cam->width <= s->W * 1 && cam->height <= s->H &&
+           int64_t(cam->width) * cam->height <= int64_t(s->W) * s->H && cam->fx > 0 && cam->fy > 0 &&
+           ((cam->width + kTile - 1) / kTile) * ((cam->height + kTile - 1) / kTile) <= s->GX * s->GY;
+}
+
+gs_status gs_project(const float* params, int64_t n, int64_t ld, const uint8_t* mask, const float* viewmat,
+                     const gs_camera* cam, gs_ws* ws, void* stream) {
+    if (!ws_ok(ws)) return GS_ERR_INVALID_ARG;
+    WsState* s = state(ws);
+    if (n < 0 || n > s->n_cap || ld < n || (n > 0 && !params) || !viewmat || !cam_ok(s, cam)) return GS_ERR_INVALID_ARG;
+    s->n = n;
+    s->cam_w = cam->width;
+    s->cam_h = cam->height;
+    s->cam_gx = (cam->width + kTile - 1) / kTile;
+    s->cam_gy = (cam->height + kTile - 1) / kTile;
+    s->gen_project += 1;
+    launch_project(s, params, n, ld, mask, viewmat, *cam, static_cast<cudaStream_t>(stream));
+    return check_launch(s, "gs_project");
+}
+
+gs_status gs_bin_sort(gs_ws* ws, int64_t* n_keys, uint32_t flags, void* stream) {
+    if (!ws_ok(ws)) return GS_ERR_INVALID_ARG;
+    WsState* s = state(ws);
+    if (s->gen_project == 0) return GS_ERR_STALE;
+    if (flags & GS_FLAG_BINSORT_KEYS) return run_bin_sort_keys(s, n_keys, flags, static_cast<cudaStream_t>(stream));
+    return run_bin_sort_bucket(s, n_keys, flags, static_cast<cudaStream_t>(stream));
+}
+
+gs_status gs_render_fwd(gs_ws* ws, const gs_camera* cam, float* color, float* depth, float* alpha, float* accum_weight,
+                        uint32_t flags, void* stream) {
+    if (!ws_ok(ws)) return GS_ERR_INVALID_ARG;
+    WsState* s = state(ws);
+    if (!cam_ok(s, cam) || !color || !depth || !alpha) return GS_ERR_INVALID_ARG;
+    if (cam->width != s->cam_w || cam->height != s->cam_h) return GS_ERR_INVALID_ARG;
+    if (s->gen_project == 0) return GS_ERR_STALE;
+    launch_render_fwd(s, *cam, color, depth, alpha, accum_weight, flags, static_cast<cudaStream_t>(stream));
+    s->gen_fwd = s->gen_project;
+    return check_launch(s, "gs_render_fwd");
+}
+
+static gs_status backward_common(const float* params, int64_t n, int64_t ld, const float* viewmat, gs_ws* ws,
+                                 const gs_camera* cam, const float* dLdC, const float* dLdD, float* grad,
+                                 double* grad_pose, uint32_t flags, void* stream) {
+    if (!ws_ok(ws)) return GS_ERR_INVALID_ARG;
+    WsState* s = state(ws);
+    if (!cam_ok(s, cam) || !dLdC || !dLdD || !viewmat || (n > 0 && !params) || ld < n) return GS_ERR_INVALID_ARG;
+    if (s->gen_fwd == 0 || s->gen_fwd != s->gen_project || n != s->n || cam->width != s->cam_w ||
+        cam->height != s->cam_h)
+        return GS_ERR_STALE;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaMemsetAsync(s->dev + s->sgrad.off, 0, size_t(s->n_cap) * 4 * 10, st);
+    launch_render_bwd_tiles(s, *cam, nullptr, dLdC, dLdD, st);
+    launch_gaussian_bwd(s, params, n, ld, viewmat, *cam, grad, grad_pose, flags, st);
+    return check_launch(s, "gs_render_bwd");
+}
+
+gs_status gs_render_bwd(const float* params, int64_t n, int64_t ld, const float* viewmat, gs_ws* ws,
+                        const gs_camera* cam, const float* dL_dcolor, const float* dL_ddepth, float* grad_params,
+                        double* grad_pose, uint32_t flags, void* stream) {
+    if (!grad_params) return GS_ERR_INVALID_ARG;
+    return backward_common(params, n, ld, viewmat, ws, cam, dL_dcolor, dL_ddepth, grad_params, grad_pose, flags,
+                           stream);
+}
+
+gs_status gs_pose_grad(const float* params, int64_t n, int64_t ld, const float* viewmat, gs_ws* ws,
+                       const gs_camera* cam, const float* dL_dcolor, const float* dL_ddepth, double* grad_pose,
+                       uint32_t flags, void* stream) {
+    if (!grad_pose) return GS_ERR_INVALID_ARG;
+    return backward_common(params, n, ld, viewmat, ws, cam, dL_dcolor, dL_ddepth, nullptr, grad_pose, flags, stream);
+}
+
+gs_status gs_loss_l1(const float* color, const float* depth, const float* tgt_color, const float* tgt_depth, int32_t W,
+                     int32_t H, float w_color, float w_depth, float* dL_dcolor, float* dL_ddepth, double* loss,
+                     gs_ws* ws, void* stream) {
+    if (!ws_ok(ws) || !color || !depth || !tgt_color || !tgt_depth || !dL_dcolor || !dL_ddepth || W <= 0 || H <= 0)
+        return GS_ERR_INVALID_ARG;
+    WsState* s = state(ws);
+    launch_loss_l1(s, color, depth, tgt_color, tgt_depth, W, H, w_color, w_depth, dL_dcolor, dL_ddepth, loss,
+                   static_cast<cudaStream_t>(stream));
+    return check_launch(s, "gs_loss_l1");
+}
+
+gs_status gs_adam_step(float* params_raw, float* params_act, const float* grad_act, float* m, float* v, int64_t n,
+                       int64_t ld, const float lr[14], int32_t step, float b1, float b2, float eps, void* stream) {
+    if ((n > 0 && (!params_raw || !params_act || !grad_act || !m || !v)) || !lr || n < 0 || ld < n || step < 1)
+        return GS_ERR_INVALID_ARG;
+    launch_adam(params_raw, params_act, grad_act, m, v, n, ld, lr, step, b1, b2, eps, static_cast<cudaStream_t>(stream));
+    return check_launch(nullptr, "gs_adam_step");
+}
+
+gs_status gs_pose_step(float* viewmat, const double* grad_pose, float* m6, float* v6, int32_t step, float lr_rho,
+                       float lr_phi, void* stream) {
+    if (!viewmat || !grad_pose || !m6 || !v6 || step < 1) return GS_ERR_INVALID_ARG;
+    launch_pose_step(viewmat, grad_pose, m6, v6, step, lr_rho, lr_phi, static_cast<cudaStream_t>(stream));
+    return check_launch(nullptr, "gs_pose_step");
+}
+
+gs_status gs_densify_prune(float* params, float* params_raw, int64_t* n_dev, int64_t capacity, int64_t ld,
+                           float* adam_m, float* adam_v, const float* alpha, const float* depth,
+                           const float* target_rgb, const float* target_depth, const float* accum_weight,
+                           const float* viewmat, const gs_camera* cam, const gs_densify_cfg* cfg,
+                           uint8_t* select_mask, float* add_out, gs_ws* ws, void* stream) {
+    if (!ws_ok(ws) || !cfg || !n_dev || capacity < 0 || ld < capacity) return GS_ERR_INVALID_ARG;
+    WsState* s = state(ws);
+    switch (cfg->mode) {
+        case GS_DENSIFY_ADD:
+            if (!params || !alpha || !depth || !target_rgb || !target_depth || !viewmat || !cam_ok(s, cam) ||
+                cfg->stride < 1 || cfg->max_add < 0)
+                return GS_ERR_INVALID_ARG;
+            break;
+        case GS_DENSIFY_PRUNE:
+            if (!params || capacity > s->n_cap) return GS_ERR_INVALID_ARG;
+            break;
+        case GS_DENSIFY_SELECT:
+            if (!select_mask || !accum_weight || !target_depth || !cam_ok(s, cam) || capacity > s->n_cap)
+                return GS_ERR_INVALID_ARG;
+            if (s->gen_project == 0) return GS_ERR_STALE;
+            break;
+        default:
+            return GS_ERR_INVALID_ARG;
+    }
+    const gs_camera dummy{};
+    return run_densify(s, params, params_raw, n_dev, capacity, ld, adam_m, adam_v, alpha, depth, target_rgb,
+                       target_depth, accum_weight, viewmat, cam ? *cam : dummy, *cfg, select_mask, add_out,
+                       static_cast<cudaStream_t>(stream));
+}
+
+gs_status gs_ws_get_view(const gs_ws* ws, gs_ws_view* out) {
+    if (!ws_ok(ws) || !out) return GS_ERR_INVALID_ARG;
+    const WsState* s = state(ws);
+    Misc* misc = at<Misc>(s, s->misc);
+    out->records = at<float>(s, s->rec);
+    out->depth_key = at<uint32_t>(s, s->depth_key);
+    out->rect = at<int16_t>(s, s->rect);
+    out->radius = at<int32_t>(s, s->radius);
+    out->tiles = at<uint32_t>(s, s->tiles);
+    out->keys = s->sorted_in_1 ? at<uint64_t>(s, s->keys1) : at<uint64_t>(s, s->keys0);
+    out->vals = s->sorted_in_1 ? at<uint32_t>(s, s->vals1) : at<uint32_t>(s, s->vals0);
+    out->ranges = at<uint32_t>(s, s->ranges);
+    out->t_final = at<float>(s, s->t_final);
+    out->n_last = at<uint32_t>(s, s->n_last);
+    out->examined = at<uint32_t>(s, s->examined);
+    out->n_keys_dev = reinterpret_cast<const uint64_t*>(&misc->n_keys);
+    out->error_flag = &misc->error_flag;
+    out->n = s->n;
+    out->key_cap = s->key_cap;
+    out->n_cap = s->n_cap;
+    out->grid_x = s->cam_gx;
+    out->grid_y = s->cam_gy;
+    out->width = s->cam_w;
+    out->height = s->cam_h;
+    return GS_OK;
+}
+
+int64_t gs_ws_launch_count(const gs_ws* ws) { return ws_ok(ws) ? state(ws)->launches : -1; }
+
+gs_status gs_ws_set_event_log(gs_ws* ws, void** events, int32_t* ids, int32_t capacity) {
+    if (!ws_ok(ws) || capacity < 0 || (capacity > 0 && (!events || !ids))) return GS_ERR_INVALID_ARG;
+    WsState* s = state(ws);
+    s->ev = capacity > 0 ? events : nullptr;
+    s->ev_ids = capacity > 0 ? ids : nullptr;
+    s->ev_cap = capacity;
+    s->ev_n = 0;
+    return GS_OK;
+}
+
+int32_t gs_ws_event_log_count(const gs_ws* ws) { return ws_ok(ws) ? state(ws)->ev_n : -1; }
+
+gs_status gs_events_create(void** events, int32_t count) {
+    if (!events || count < 0) return GS_ERR_INVALID_ARG;
+    for (int32_t i = 0; i < count; ++i) {
+        cudaEvent_t e;
+        const cudaError_t err = cudaEventCreate(&e);
+        if (err != cudaSuccess) {
+            set_cuda_error(err, "cudaEventCreate");
+            return GS_ERR_CUDA;
+        }
+        events[i] = e;
+    }
+    return GS_OK;
+}
+
+gs_status gs_events_destroy(void** events, int32_t count) {
+    if (!events || count < 0) return GS_ERR_INVALID_ARG;
+    for (int32_t i = 0; i < count; ++i)
+        if (events[i]) cudaEventDestroy(static_cast<cudaEvent_t>(events[i]));
+    return GS_OK;
+}
+
+gs_status gs_events_elapsed(void* const* events, int32_t pairs, float* ms) {
+    if (!events || !ms || pairs < 0) return GS_ERR_INVALID_ARG;
+    for (int32_t i = 0; i < pairs; ++i) {
+        const cudaError_t err = cudaEventElapsedTime(ms + i, static_cast<cudaEvent_t>(events[2 * i]),
+                                                     static_cast<cudaEvent_t>(events[2 * i + 1]));
+        if (err != cudaSuccess) {
+            set_cuda_error(err, "cudaEventElapsedTime");
+            return GS_ERR_CUDA;
+        }
+    }
+    return GS_OK;
+}
+
+const char* gs_kernel_name(int32_t id) {
+    static const char* names[KID_COUNT] = {"project", "chained_scan", "emit_keys", "sort_hist", "sort_digit_scan",
+                                           "sort_pass", "tile_ranges", "render_fwd", "render_bwd_tiles",
+                                           "gaussian_bwd", "pose_finalize", "loss_l1", "densify", "depth_sort",
+                                           "chunk_hist", "chunk_scan", "bucket_emit"};
+    return (id >= 0 && id < KID_COUNT) ? names[id] : "unknown";
+}
+
+const char* gs_status_string(gs_status st) {
+    switch (st) {
+        case GS_OK: return "GS_OK";
+        case GS_ERR_INVALID_ARG: return "GS_ERR_INVALID_ARG";
+        case GS_ERR_CAPACITY: return "GS_ERR_CAPACITY";
+        case GS_ERR_STALE: return "GS_ERR_STALE";
+        case GS_ERR_CUDA: return "GS_ERR_CUDA";
+        case GS_ERR_UNSUPPORTED: return "GS_ERR_UNSUPPORTED";
+    }
+    return "GS_ERR_UNKNOWN";
+}
+
+const char* gs_last_cuda_error(void) { return g_last_cuda_error.c_str(); }
+
+}  // extern "C"

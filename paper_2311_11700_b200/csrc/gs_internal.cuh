@@ -1,0 +1,151 @@
+// Internal declarations of libgs (B200 / sm_100a). Not part of the ABI; see include/gs.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gs.h"
+
+namespace gs {
+
+constexpr int kTile = 16;                 // 16x16 pixel tiles (north_star)
+constexpr int kTilePx = kTile * kTile;    // 256 pixels = 256 threads per tile CTA
+constexpr int kRecFloats = 12;            // projected record: 3 x float4 (48 B)
+
+// ------------------------------------------------------------------ workspace (host state)
+struct Region { uint64_t off, bytes; };
+
+struct WsState {
+    uint64_t magic;
+    char* dev;
+    uint64_t dev_bytes;
+    int64_t n_cap, key_cap;
+    int32_t W, H, GX, GY;          // capacity image size and tile grid
+    // carve
+    Region rec, depth_key, rect, radius, tiles, offsets, sgrad, scan_state,
+        keys0, keys1, vals0, vals1, ranges, t_final, n_last, examined, sort_hist, sort_look,
+        misc, scratch, scratch14, dkey_sorted, dval_sorted, chunk_hist;
+    // run state
+    int64_t n;                     // Gaussians of the last gs_project
+    int32_t cam_w, cam_h, cam_gx, cam_gy;   // image of the last gs_project
+    uint64_t gen_project, gen_fwd; // generation counters (GS_ERR_STALE)
+    int32_t sorted_in_1;           // final sorted keys/vals live in buffer 1
+    int32_t pad0;
+    int64_t n_keys_host;           // K of the last host-synced gs_bin_sort (-1 unknown)
+    int64_t launches;              // kernels launched (gs_ws_launch_count)
+    int64_t max_parts;             // sort lookback partitions per pass
+    uint64_t epoch;                // look-back epoch (scan and sort status words)
+    // optional per-kernel event log (gs_ws_set_event_log)
+    void** ev;                     // 2*ev_cap caller-created cudaEvent_t
+    int32_t* ev_ids;               // kernel id per logged launch
+    int32_t ev_cap, ev_n;
+};
+static_assert(sizeof(WsState) <= sizeof(gs_ws), "WsState must fit in gs_ws");
+constexpr uint64_t kMagic = 0x67735F62323030ull;   // "gs_b200"
+
+inline WsState* state(gs_ws* ws) { return reinterpret_cast<WsState*>(ws); }
+inline const WsState* state(const gs_ws* ws) { return reinterpret_cast<const WsState*>(ws); }
+template <class T> inline T* at(const WsState* s, const Region& r) { return reinterpret_cast<T*>(s->dev + r.off); }
+
+// misc region layout (device scalars)
+struct Misc {
+    unsigned long long n_keys;     // K
+    unsigned long long n_keys_eff; // K if K <= key_cap else 0 (what sort / ranges / render consume)
+    unsigned int error_flag;
+    unsigned int scan_counter;
+    unsigned int sort_counter[8];  // per-pass partition counters
+    double loss_acc[4];            // |C-C*| sum, |D-D*| valid sum, valid count, spare
+    double pose_acc[16];
+    unsigned long long add_count;  // densify
+    unsigned long long keep_count;
+    unsigned int chunk_counter;
+    unsigned int pad[3];
+};
+
+// ------------------------------------------------------------------ launch helpers
+// Kernel ids for the event log; names in gs_kernel_name (abi.cu). Keep in sync.
+enum KernelId {
+    KID_PROJECT = 0, KID_SCAN, KID_EMIT, KID_SORT_HIST, KID_SORT_DSCAN, KID_SORT_PASS, KID_RANGES,
+    KID_FWD, KID_BWD_TILE, KID_BWD_GAUSS, KID_POSE_FIN, KID_LOSS, KID_DENSIFY,
+    KID_DEPTH_SORT, KID_CHUNK_HIST, KID_CHUNK_SCAN, KID_BUCKET_EMIT, KID_COUNT
+};
+
+// RAII bracket around one kernel launch: counts it and, when an event log is attached, records
+// an event before and after it on the launching stream.
+struct KTimer {
+    WsState* s;
+    cudaStream_t st;
+    bool on;
+    KTimer(WsState* s_, int kid, cudaStream_t st_) : s(s_), st(st_), on(false) {
+        if (s && s->ev && s->ev_n < s->ev_cap) {
+            on = true;
+            s->ev_ids[s->ev_n] = kid;
+            cudaEventRecord(static_cast<cudaEvent_t>(s->ev[2 * s->ev_n]), st);
+        }
+    }
+    ~KTimer() {
+        if (!s) return;
+        s->launches += 1;
+        if (on) {
+            cudaEventRecord(static_cast<cudaEvent_t>(s->ev[2 * s->ev_n + 1]), st);
+            s->ev_n += 1;
+        }
+    }
+};
+
+gs_status check_launch(WsState* s, const char* what);
+void set_cuda_error(cudaError_t e, const char* what);
+
+// kernels-side entry points (defined in the .cu files; host wrappers)
+void launch_project(WsState* s, const float* params, int64_t n, int64_t ld, const uint8_t* mask,
+                    const float* viewmat, const gs_camera& cam, cudaStream_t st);
+gs_status run_bin_sort_keys(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t st);
+gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t st);
+void launch_render_fwd(WsState* s, const gs_camera& cam, float* color, float* depth, float* alpha,
+                       float* accum_weight, uint32_t flags, cudaStream_t st);
+void launch_render_bwd_tiles(WsState* s, const gs_camera& cam, const float* color_unused,
+                             const float* dL_dcolor, const float* dL_ddepth, cudaStream_t st);
+void launch_gaussian_bwd(WsState* s, const float* params, int64_t n, int64_t ld, const float* viewmat,
+                         const gs_camera& cam, float* grad_params, double* grad_pose, uint32_t flags,
+                         cudaStream_t st);
+void launch_loss_l1(WsState* s, const float* color, const float* depth, const float* tc, const float* td,
+                    int32_t W, int32_t H, float wc, float wd, float* dc, float* dd, double* loss, cudaStream_t st);
+void launch_adam(float* raw, float* act, const float* g, float* m, float* v, int64_t n, int64_t ld,
+                 const float lr[14], int32_t step, float b1, float b2, float eps, cudaStream_t st);
+void launch_pose_step(float* viewmat, const double* gp, float* m6, float* v6, int32_t step, float lr_rho,
+                      float lr_phi, cudaStream_t st);
+gs_status run_densify(WsState* s, float* params, float* raw, int64_t* n_dev, int64_t capacity, int64_t ld,
+                      float* m, float* v, const float* alpha, const float* depth, const float* trgb,
+                      const float* tdepth, const float* accum, const float* viewmat, const gs_camera& cam,
+                      const gs_densify_cfg& cfg, uint8_t* select_mask, float* add_out, cudaStream_t st);
+
+// ------------------------------------------------------------------ device helpers
+__device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
+
+// alpha of Gaussian record (r0 = {mx, my, a, b}, r1 = {c, o, d, -}) at pixel (px, py).
+// Shared by the forward and both backward kernels so every decision is bit-identical between
+// them. Written with explicit round-to-nearest intrinsics so no contraction choice of the
+// compiler can differ between call sites. Returns alpha (0 when skipped) and G, and whether the
+// 0.99 clamp is active.
+struct AlphaEval { float alpha, G, dx, dy; bool clamped; };
+
+__device__ __forceinline__ AlphaEval eval_alpha(float4 r0, float4 r1, float px, float py) {
+    AlphaEval e;
+    e.dx = __fsub_rn(r0.x, px);
+    e.dy = __fsub_rn(r0.y, py);
+    // power = -0.5 (a dx^2 + c dy^2) - b dx dy
+    const float q = __fmaf_rn(__fmul_rn(r1.x, e.dy), e.dy, __fmul_rn(__fmul_rn(r0.z, e.dx), e.dx));
+    const float power = __fmaf_rn(-0.5f, q, -__fmul_rn(__fmul_rn(r0.w, e.dx), e.dy));
+    // G = exp(power) via ex2.approx (MUFU): power * log2(e)
+    float G;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(G) : "f"(__fmul_rn(power, 1.4426950408889634f)));
+    const float og = __fmul_rn(r1.y, G);
+    e.G = G;
+    e.clamped = og > 0.99f;
+    float a = fminf(0.99f, og);
+    if (power > 0.f || a < (1.0f / 255.0f)) a = 0.f;   // skipped: contributes nothing
+    e.alpha = a;
+    return e;
+}
+
+}  // namespace gs

@@ -1,0 +1,384 @@
+// gs_loss_l1, gs_adam_step, gs_pose_step, gs_densify_prune kernels (sm_100a).
+// All elementwise / compaction work is HBM-bound; no host synchronisation (device counts).
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include "gs_internal.cuh"
+
+namespace gs {
+
+// ------------------------------------------------------------------ L1 loss, Eq. 6 (reading C20)
+__global__ void __launch_bounds__(256) loss_reduce_kernel(const float* __restrict__ c, const float* __restrict__ d,
+                                                          const float* __restrict__ tc, const float* __restrict__ td,
+                                                          int64_t npx, double* __restrict__ acc) {
+    double sc = 0.0, sd = 0.0, nv = 0.0;
+    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < npx; p += int64_t(gridDim.x) * blockDim.x) {
+        sc += double(fabsf(c[p] - tc[p])) + double(fabsf(c[npx + p] - tc[npx + p])) +
+              double(fabsf(c[2 * npx + p] - tc[2 * npx + p]));
+        const float t = td[p];
+        if (t > 0.f) {
+            sd += double(fabsf(d[p] - t));
+            nv += 1.0;
+        }
+    }
+    using BR = cub::BlockReduce<double, 256>;
+    __shared__ typename BR::TempStorage tmp;
+    const double a = BR(tmp).Sum(sc);
+    __syncthreads();
+    const double b = BR(tmp).Sum(sd);
+    __syncthreads();
+    const double e = BR(tmp).Sum(nv);
+    if (threadIdx.x == 0) {
+        atomicAdd(acc + 0, a);
+        atomicAdd(acc + 1, b);
+        atomicAdd(acc + 2, e);
+    }
+}
+
+__device__ __forceinline__ float sgnf(float x) { return float((x > 0.f) - (x < 0.f)); }
+
+__global__ void __launch_bounds__(256) loss_grad_kernel(const float* __restrict__ c, const float* __restrict__ d,
+                                                        const float* __restrict__ tc, const float* __restrict__ td,
+                                                        int64_t npx, float wc, float wd, const double* __restrict__ acc,
+                                                        float* __restrict__ dc, float* __restrict__ dd,
+                                                        double* __restrict__ loss) {
+    const double nvalid = acc[2];
+    const float sc = float(double(wc) / (3.0 * double(npx)));
+    const float sd = nvalid > 0 ? float(double(wd) / nvalid) : 0.f;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && loss)
+        *loss = double(sc) * acc[0] + (nvalid > 0 ? double(sd) * acc[1] : 0.0);
+    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < npx; p += int64_t(gridDim.x) * blockDim.x) {
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) dc[ch * npx + p] = sc * sgnf(c[ch * npx + p] - tc[ch * npx + p]);
+        const float t = td[p];
+        dd[p] = t > 0.f ? sd * sgnf(d[p] - t) : 0.f;
+    }
+}
+
+void launch_loss_l1(WsState* s, const float* color, const float* depth, const float* tc, const float* td, int32_t W,
+                    int32_t H, float wc, float wd, float* dc, float* dd, double* loss, cudaStream_t st) {
+    Misc* misc = at<Misc>(s, s->misc);
+    const int64_t npx = int64_t(W) * H;
+    cudaMemsetAsync(misc->loss_acc, 0, sizeof(misc->loss_acc), st);
+    const int blocks = int(std::min<int64_t>((npx + 255) / 256, 148 * 4));
+    {
+        KTimer kt(s, KID_LOSS, st);
+        loss_reduce_kernel<<<blocks, 256, 0, st>>>(color, depth, tc, td, npx, misc->loss_acc);
+    }
+    KTimer kt(s, KID_LOSS, st);
+    loss_grad_kernel<<<blocks, 256, 0, st>>>(color, depth, tc, td, npx, wc, wd, misc->loss_acc, dc, dd, loss);
+}
+
+// ------------------------------------------------------------------ Adam
+struct Lr14 { float v[14]; };
+
+__global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ raw, float* __restrict__ act,
+                                                   const float* __restrict__ g, float* __restrict__ m,
+                                                   float* __restrict__ v, int64_t n, int64_t ld, Lr14 lr, float b1,
+                                                   float b2, float eps, float bc1, float bc2) {
+    const int k = blockIdx.y;
+    const float lrk = lr.v[k];
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t o = k * ld + i;
+        const float r = raw[o];
+        float gr = g[o];
+        if (k >= 3 && k < 6) gr *= expf(r);                       // d/dlog s = s d/ds
+        else if (k == 10) { const float s = 1.f / (1.f + expf(-r)); gr *= s * (1.f - s); }   // d/dlogit o
+        const float mm = b1 * m[o] + (1.f - b1) * gr;
+        const float vv = b2 * v[o] + (1.f - b2) * gr * gr;
+        m[o] = mm;
+        v[o] = vv;
+        const float nr = r - lrk * (mm / bc1) / (sqrtf(vv / bc2) + eps);
+        raw[o] = nr;
+        act[o] = (k >= 3 && k < 6) ? expf(nr) : (k == 10 ? 1.f / (1.f + expf(-nr)) : nr);
+    }
+}
+
+void launch_adam(float* raw, float* act, const float* g, float* m, float* v, int64_t n, int64_t ld, const float lr[14],
+                 int32_t step, float b1, float b2, float eps, cudaStream_t st) {
+    if (n == 0) return;
+    Lr14 l;
+    for (int k = 0; k < 14; ++k) l.v[k] = lr[k];
+    const float bc1 = float(1.0 - std::pow(double(b1), step)), bc2 = float(1.0 - std::pow(double(b2), step));
+    dim3 grid(unsigned(std::min<int64_t>((n + 255) / 256, 148 * 2)), 14);
+    adam_kernel<<<grid, 256, 0, st>>>(raw, act, g, m, v, n, ld, l, b1, b2, eps, bc1, bc2);
+}
+
+// ------------------------------------------------------------------ pose step (reading C23)
+__global__ void pose_step_kernel(float* viewmat, const double* gp, float* m6, float* v6, int32_t step, float lr_rho,
+                                 float lr_phi) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+    const double bc1 = 1.0 - pow(b1, step), bc2 = 1.0 - pow(b2, step);
+    double d[6];
+    for (int k = 0; k < 6; ++k) {
+        const double g = gp[k];
+        const double mm = b1 * m6[k] + (1 - b1) * g, vv = b2 * v6[k] + (1 - b2) * g * g;
+        m6[k] = float(mm);
+        v6[k] = float(vv);
+        d[k] = -double(k < 3 ? lr_rho : lr_phi) * (mm / bc1) / (sqrt(vv / bc2) + eps);
+    }
+    // exp(delta^): Rodrigues + V(phi) rho
+    const double px = d[3], py = d[4], pz = d[5];
+    const double th2 = px * px + py * py + pz * pz, th = sqrt(th2);
+    const double K[3][3] = {{0, -pz, py}, {pz, 0, -px}, {-py, px, 0}};
+    double K2[3][3];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) K2[a][b] = K[a][0] * K[0][b] + K[a][1] * K[1][b] + K[a][2] * K[2][b];
+    double A, B, C;
+    if (th < 1e-8) { A = 1.0; B = 0.5; C = 1.0 / 6.0; }
+    else { A = sin(th) / th; B = (1 - cos(th)) / th2; C = (th - sin(th)) / (th2 * th); }
+    double R[3][3], Vm[3][3];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) {
+            const double I = a == b ? 1.0 : 0.0;
+            R[a][b] = I + A * K[a][b] + B * K2[a][b];
+            Vm[a][b] = I + B * K[a][b] + C * K2[a][b];
+        }
+    double W[3][3], t[3];
+    for (int a = 0; a < 3; ++a) {
+        for (int b = 0; b < 3; ++b) W[a][b] = viewmat[4 * a + b];
+        t[a] = viewmat[4 * a + 3];
+    }
+    for (int a = 0; a < 3; ++a) {
+        for (int b = 0; b < 3; ++b) viewmat[4 * a + b] = float(R[a][0] * W[0][b] + R[a][1] * W[1][b] + R[a][2] * W[2][b]);
+        viewmat[4 * a + 3] = float(R[a][0] * t[0] + R[a][1] * t[1] + R[a][2] * t[2] + Vm[a][0] * d[0] +
+                                   Vm[a][1] * d[1] + Vm[a][2] * d[2]);
+    }
+}
+
+void launch_pose_step(float* viewmat, const double* gp, float* m6, float* v6, int32_t step, float lr_rho, float lr_phi,
+                      cudaStream_t st) {
+    pose_step_kernel<<<1, 32, 0, st>>>(viewmat, gp, m6, v6, step, lr_rho, lr_phi);
+}
+
+// ------------------------------------------------------------------ densify / prune / select
+// Ordered compaction: a block-local scan + one look-back per block would do; counts here are
+// small (pixels / Gaussians), so a two-level scan is used: per-block counts -> exclusive scan
+// of the block counts in one block -> scatter. Deterministic (order-preserving).
+constexpr int kCmpThreads = 256, kCmpItems = 8, kCmpTile = kCmpThreads * kCmpItems;
+
+template <class Pred>
+__global__ void __launch_bounds__(kCmpThreads) count_kernel(int64_t n, const int64_t* n_dev, Pred pred,
+                                                            uint32_t* __restrict__ block_counts) {
+    using BR = cub::BlockReduce<uint32_t, kCmpThreads>;
+    __shared__ typename BR::TempStorage tmp;
+    const int64_t nn = n_dev ? *n_dev : n;
+    const int64_t base = int64_t(blockIdx.x) * kCmpTile;
+    uint32_t c = 0;
+    for (int k = 0; k < kCmpItems; ++k) {
+        const int64_t i = base + int64_t(threadIdx.x) * kCmpItems + k;
+        if (i < nn && pred(i)) ++c;
+    }
+    const uint32_t tot = BR(tmp).Sum(c);
+    if (threadIdx.x == 0) block_counts[blockIdx.x] = tot;
+}
+
+// exclusive scan of nb block counts (single block, sequential chunks of 1024)
+__global__ void scan_blocks_kernel(uint32_t* __restrict__ counts, int nb, unsigned long long* __restrict__ total) {
+    using BS = cub::BlockScan<uint32_t, 1024>;
+    __shared__ typename BS::TempStorage tmp;
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < nb; base += 1024) {
+        const int i = base + threadIdx.x;
+        const uint32_t v = i < nb ? counts[i] : 0u;
+        uint32_t ex, agg;
+        BS(tmp).ExclusiveSum(v, ex, agg);
+        if (i < nb) counts[i] = carry + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += agg;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+
+template <class Pred, class Emit>
+__global__ void __launch_bounds__(kCmpThreads) scatter_kernel(int64_t n, const int64_t* n_dev, Pred pred, Emit emit,
+                                                              const uint32_t* __restrict__ block_offsets) {
+    using BS = cub::BlockScan<uint32_t, kCmpThreads>;
+    __shared__ typename BS::TempStorage tmp;
+    const int64_t nn = n_dev ? *n_dev : n;
+    const int64_t base = int64_t(blockIdx.x) * kCmpTile + int64_t(threadIdx.x) * kCmpItems;
+    bool f[kCmpItems];
+    uint32_t c = 0;
+    for (int k = 0; k < kCmpItems; ++k) {
+        f[k] = (base + k < nn) && pred(base + k);
+        c += f[k];
+    }
+    uint32_t ex;
+    BS(tmp).ExclusiveSum(c, ex);
+    uint32_t o = block_offsets[blockIdx.x] + ex;
+    for (int k = 0; k < kCmpItems; ++k)
+        if (f[k]) emit(base + k, o++);
+}
+
+struct AddPred {
+    const float *alpha, *depth, *td;
+    int W;
+    float tau_a, tau_d;
+    int stride;
+    __device__ bool operator()(int64_t p) const {
+        const int u = int(p % W), v = int(p / W);
+        const float t = td[p];
+        return t > 0.f && (alpha[p] < tau_a || fabsf(t - depth[p]) > tau_d) && ((u + v) % stride) == 0;
+    }
+};
+
+struct AddEmit {
+    const float *td, *trgb;
+    const float* viewmat;
+    int W;
+    int64_t npx;
+    float fx, fy, cx, cy, init_o;
+    int stride;
+    float* params;   // [14][ld] (activated), columns n + o
+    float* raw;      // nullable
+    float *m, *v;    // nullable
+    float* out;      // nullable: [14][max_add] candidate records
+    int64_t ld, capacity, max_add;
+    const int64_t* n_dev;
+    __device__ void operator()(int64_t p, uint32_t o) const {
+        if (int64_t(o) >= max_add) return;
+        const int64_t n = *n_dev;
+        const float z = td[p];
+        const float u = float(p % W), v_ = float(p / W);
+        const float xc = (u - cx) / fx * z, yc = (v_ - cy) / fy * z, zc = z;
+        const float* V = viewmat;
+        // X = W^T (X^c - t)
+        const float a0 = xc - V[3], a1 = yc - V[7], a2 = zc - V[11];
+        float rec[14];
+        rec[0] = V[0] * a0 + V[4] * a1 + V[8] * a2;
+        rec[1] = V[1] * a0 + V[5] * a1 + V[9] * a2;
+        rec[2] = V[2] * a0 + V[6] * a1 + V[10] * a2;
+        const float s = z * float(stride) / (fx + fy);
+        rec[3] = rec[4] = rec[5] = s;
+        rec[6] = 1.f;
+        rec[7] = rec[8] = rec[9] = 0.f;
+        rec[10] = init_o;
+        rec[11] = trgb[p];
+        rec[12] = trgb[npx + p];
+        rec[13] = trgb[2 * npx + p];
+        if (out) {
+            for (int k = 0; k < 14; ++k) out[k * max_add + o] = rec[k];
+            return;
+        }
+        const int64_t col = n + o;
+        if (col >= capacity) return;
+        for (int k = 0; k < 14; ++k) params[k * ld + col] = rec[k];
+        if (raw) {
+            for (int k = 0; k < 14; ++k) raw[k * ld + col] = rec[k];
+            for (int k = 3; k < 6; ++k) raw[k * ld + col] = logf(s);
+            raw[10 * ld + col] = logf(init_o / (1.f - init_o));
+        }
+        if (m) for (int k = 0; k < 14; ++k) m[k * ld + col] = 0.f;
+        if (v) for (int k = 0; k < 14; ++k) v[k * ld + col] = 0.f;
+    }
+};
+
+__global__ void add_commit_kernel(int64_t* n_dev, const unsigned long long* count, int64_t max_add, int64_t capacity) {
+    const int64_t n = *n_dev;
+    int64_t a = int64_t(*count);
+    if (a > max_add) a = max_add;
+    if (n + a > capacity) a = capacity - n;
+    *n_dev = n + a;
+}
+
+struct KeepPred {
+    const float* opacity;   // row 10 of params
+    float min_o;
+    __device__ bool operator()(int64_t i) const { return opacity[i] >= min_o; }
+};
+
+struct GatherEmit {
+    const float* src;
+    float* dst;
+    int64_t src_ld, dst_ld;
+    __device__ void operator()(int64_t i, uint32_t o) const {
+        for (int k = 0; k < 14; ++k) dst[k * dst_ld + o] = src[k * src_ld + i];
+    }
+};
+
+__global__ void copy_rows_kernel(const float* __restrict__ src, int64_t src_ld, float* __restrict__ dst, int64_t dst_ld,
+                                 const unsigned long long* __restrict__ count) {
+    const int64_t n = int64_t(*count);
+    const int k = blockIdx.y;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        dst[k * dst_ld + i] = src[k * src_ld + i];
+}
+
+__global__ void set_n_kernel(int64_t* n_dev, const unsigned long long* count) { *n_dev = int64_t(*count); }
+
+__global__ void select_kernel(int64_t n, const int64_t* n_dev, const float4* __restrict__ rec,
+                              const uint32_t* __restrict__ tiles, const float* __restrict__ accum,
+                              const float* __restrict__ td, int W, int H, float sel_w, float sel_d,
+                              uint8_t* __restrict__ mask) {
+    const int64_t nn = n_dev ? *n_dev : n;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nn; i += int64_t(gridDim.x) * blockDim.x) {
+        uint8_t keep = 0;
+        if (tiles[i] > 0) {
+            const float4 r0 = rec[3 * i], r1 = rec[3 * i + 1];
+            const float u = floorf(r0.x + 0.5f), v = floorf(r0.y + 0.5f);
+            if (u >= 0.f && u < float(W) && v >= 0.f && v < float(H)) {
+                const float t = td[int64_t(v) * W + int64_t(u)];
+                keep = (t > 0.f && accum[i] > sel_w && fabsf(t - r1.z) < sel_d) ? 1 : 0;
+            }
+        }
+        mask[i] = keep;
+    }
+}
+
+#define GS_K(call)                              \
+    do {                                        \
+        KTimer kt_(s, KID_DENSIFY, st);         \
+        call;                                   \
+    } while (0)
+
+gs_status run_densify(WsState* s, float* params, float* raw, int64_t* n_dev, int64_t capacity, int64_t ld, float* m,
+                      float* v, const float* alpha, const float* depth, const float* trgb, const float* tdepth,
+                      const float* accum, const float* viewmat, const gs_camera& cam, const gs_densify_cfg& cfg,
+                      uint8_t* select_mask, float* add_out, cudaStream_t st) {
+    Misc* misc = at<Misc>(s, s->misc);
+    uint32_t* bcounts = at<uint32_t>(s, s->chunk_hist);
+    if (cfg.mode == GS_DENSIFY_SELECT) {
+        const int blocks = int(std::min<int64_t>((capacity + 255) / 256, 148 * 8));
+        GS_K((select_kernel<<<blocks, 256, 0, st>>>(capacity, n_dev, at<float4>(s, s->rec), at<uint32_t>(s, s->tiles),
+                                                    accum, tdepth, cam.width, cam.height, cfg.sel_weight,
+                                                    cfg.sel_depth, select_mask)));
+        return check_launch(s, "densify_select");
+    }
+    if (cfg.mode == GS_DENSIFY_ADD) {
+        const int64_t npx = int64_t(cam.width) * cam.height;
+        const int nb = int((npx + kCmpTile - 1) / kCmpTile);
+        AddPred pred{alpha, depth, tdepth, cam.width, cfg.tau_alpha, cfg.tau_depth, cfg.stride};
+        AddEmit emit{tdepth, trgb, viewmat, cam.width, npx, cam.fx, cam.fy, cam.cx, cam.cy, cfg.init_opacity,
+                     cfg.stride, params, raw, m, v, add_out, ld, capacity, cfg.max_add, n_dev};
+        GS_K((count_kernel<<<nb, kCmpThreads, 0, st>>>(npx, nullptr, pred, bcounts)));
+        GS_K((scan_blocks_kernel<<<1, 1024, 0, st>>>(bcounts, nb, &misc->add_count)));
+        GS_K((scatter_kernel<<<nb, kCmpThreads, 0, st>>>(npx, nullptr, pred, emit, bcounts)));
+        if (!add_out) GS_K((add_commit_kernel<<<1, 1, 0, st>>>(n_dev, &misc->add_count, cfg.max_add, capacity)));
+        return check_launch(s, "densify_add");
+    }
+    if (cfg.mode == GS_DENSIFY_PRUNE) {
+        const int nb = int((capacity + kCmpTile - 1) / kCmpTile);
+        KeepPred pred{params + 10 * ld, cfg.min_opacity};
+        GS_K((count_kernel<<<nb, kCmpThreads, 0, st>>>(capacity, n_dev, pred, bcounts)));
+        GS_K((scan_blocks_kernel<<<1, 1024, 0, st>>>(bcounts, nb, &misc->keep_count)));
+        float* scratch = at<float>(s, s->scratch14);
+        float* arrays[4] = {raw, m, v, params};   // params last: the predicate reads its opacity row
+        for (float* a : arrays) {
+            if (!a) continue;
+            GS_K((scatter_kernel<<<nb, kCmpThreads, 0, st>>>(capacity, n_dev, pred,
+                                                             GatherEmit{a, scratch, ld, s->n_cap}, bcounts)));
+            dim3 g(unsigned(std::min<int64_t>((capacity + 255) / 256, 148 * 4)), 14);
+            GS_K((copy_rows_kernel<<<g, 256, 0, st>>>(scratch, s->n_cap, a, ld, &misc->keep_count)));
+        }
+        GS_K((set_n_kernel<<<1, 1, 0, st>>>(n_dev, &misc->keep_count)));
+        return check_launch(s, "densify_prune");
+    }
+    return GS_ERR_INVALID_ARG;
+}
+#undef GS_K
+
+}  // namespace gs

@@ -1,0 +1,67 @@
+"""Shared helpers for the -m gpu parity tests: run the CUDA path through the C ABI and the oracle
+on the same seeded inputs, and compare with the tolerances of BASELINE.json north_star."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import gs_inputs as gi
+import oracle
+
+ATOL_IMG = 1e-4                 # north_star: fp32 colour/depth/alpha within 1e-4 absolute
+RTOL_GRAD, ATOL_GRAD = 2e-3, 1e-6   # north_star: gradients 2e-3 relative, 1e-6 absolute floor
+
+
+def to_dev(a, dtype=torch.float32):
+    return torch.as_tensor(np.ascontiguousarray(a)).to(device="cuda", dtype=dtype)
+
+
+def key_cap_for(params, view, cam, slack=1.05):
+    pr = oracle.project(params, view, cam, "f32")
+    k = int(pr["tiles"].astype(np.int64).sum())
+    return max(int(k * slack) + 1024, 4096), pr
+
+
+def run_forward(params, view, cam, flags_bin=0, key_cap=None, fwd_flags=None):
+    import paper_2311_11700_b200 as g
+    n = params.shape[1]
+    if key_cap is None:
+        key_cap, _ = key_cap_for(params, view, cam)
+    pipe = g.RenderPipeline(max(n, 1), key_cap, cam.width, cam.height)
+    P = to_dev(params)
+    V = to_dev(view)
+    fr = pipe.forward(P, n, V, cam, bin_flags=flags_bin,
+                      fwd_flags=g.GS_FLAG_EXAMINED if fwd_flags is None else fwd_flags)
+    torch.cuda.synchronize()
+    return pipe, P, V, fr
+
+
+def compare_images(gpu, orc, cam, params, view, label=""):
+    """Tolerance compare with the threshold-tie rule: a pixel outside tolerance is
+    accepted only if the oracle replayed with the GPU's n_last is within tolerance AND the oracle
+    flagged one of its own decisions as within 1e-5 relative of its threshold."""
+    H, W = cam.height, cam.width
+    gc = gpu["color"].cpu().numpy().astype(np.float64)
+    gd = gpu["depth"].cpu().numpy().astype(np.float64)
+    ga = gpu["alpha"].cpu().numpy().astype(np.float64)
+    err = np.maximum.reduce([np.abs(gc - orc["color"]).max(0), np.abs(gd - orc["depth"]), np.abs(ga - orc["alpha"])])
+    bad = np.flatnonzero(err.reshape(-1) > ATOL_IMG)
+    ties = 0
+    if bad.size:
+        nl = gpu["n_last"].cpu().numpy().reshape(-1)[bad]
+        rp = oracle.forward(params, view, cam, "f32", pixels=bad, replay_nlast=nl)
+        e2 = np.maximum.reduce([np.abs(gc.reshape(3, -1)[:, bad] - rp["color"]).max(0),
+                                np.abs(gd.reshape(-1)[bad] - rp["depth"]), np.abs(ga.reshape(-1)[bad] - rp["alpha"])])
+        amb = orc["ambiguous"].reshape(-1)[bad]
+        ok = (e2 <= ATOL_IMG) & (amb == 1)
+        assert ok.all(), f"{label}: {int((~ok).sum())} pixels outside tolerance, max err {float(err.max()):.3g}"
+        ties = int(bad.size)
+    assert ties <= max(3, int(1e-5 * H * W) + 3), f"{label}: {ties} tie pixels"
+    return ties
+
+
+def grad_close(gpu, ref, rtol=RTOL_GRAD, atol=ATOL_GRAD):
+    gpu = np.asarray(gpu, np.float64)
+    ref = np.asarray(ref, np.float64)
+    bad = np.abs(gpu - ref) > rtol * np.abs(ref) + atol
+    return bad

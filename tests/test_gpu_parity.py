@@ -1,0 +1,302 @@
+"""GPU parity tests (-m gpu): the CUDA path, called through the C ABI, against the oracle on the
+same seeded inputs (configs 0-2 of BASELINE.json). Integer work (depth keys,
+rects, tile lists, ranges) must be bit-exact; floats within the north_star tolerances."""
+import numpy as np
+import pytest
+import torch
+
+import gs_inputs as gi
+import oracle
+from gpu_helpers import (ATOL_IMG, compare_images, grad_close, key_cap_for, run_forward, to_dev)
+
+pytestmark = pytest.mark.gpu
+
+CFGS = [0, 1, 2]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2311_11700_b200  # noqa: F401  (fails loudly if libgs.so is missing)
+
+
+def scene(c):
+    cfg = gi.CONFIGS[c]
+    return cfg, cfg.scene(), cfg.view()
+
+
+# ------------------------------------------------------------------ O1 projection, bit-exact
+@pytest.mark.parametrize("c", CFGS)
+def test_project_bitexact(c):
+    cfg, p, v = scene(c)
+    pipe, P, V, _ = run_forward(p, v, cfg.cam)
+    a = pipe.arrays(p.shape[1])
+    o = oracle.project(p, v, cfg.cam, "f32")
+    assert np.array_equal(a["depth_key"].cpu().numpy().view(np.uint32), o["depth_bits"])
+    assert np.array_equal(a["radius"].cpu().numpy(), o["radius"])
+    assert np.array_equal(a["tiles"].cpu().numpy().view(np.uint32), o["tiles"])
+    rect = a["rect"].cpu().numpy().astype(np.int32).T
+    assert np.array_equal(rect, o["rect"])
+    rec = a["records"].cpu().numpy()
+    on = o["tiles"] > 0
+    assert np.array_equal(rec[on, 0], o["mean2d"][0, on]) and np.array_equal(rec[on, 1], o["mean2d"][1, on])
+    assert np.array_equal(rec[on, 2], o["conic"][0, on]) and np.array_equal(rec[on, 3], o["conic"][1, on])
+    assert np.array_equal(rec[on, 4], o["conic"][2, on])
+    assert np.array_equal(rec[on, 6], o["depth"][on])
+
+
+# ------------------------------------------------------------------ O2 binning + sort, bit-exact
+@pytest.mark.parametrize("c", CFGS)
+@pytest.mark.parametrize("path", ["bucket", "keys"])
+def test_bin_sort_bitexact(c, path):
+    import paper_2311_11700_b200 as g
+    cfg, p, v = scene(c)
+    flags = g.GS_FLAG_BINSORT_KEYS if path == "keys" else 0
+    pipe, P, V, fr = run_forward(p, v, cfg.cam, flags_bin=flags)
+    a = pipe.arrays(p.shape[1])
+    # binding check: the oracle bins the GPU's own projected depth keys and rects
+    dk = a["depth_key"].cpu().numpy().view(np.uint32)
+    rect = a["rect"].cpu().numpy().astype(np.int32).T.copy()
+    tiles = a["tiles"].cpu().numpy().view(np.uint32)
+    o = oracle.bin_sort(dk, rect, tiles, cfg.cam)
+    assert fr.n_keys == o["n_keys"] == int(a["n_keys_dev"].item())
+    assert np.array_equal(a["vals"].cpu().numpy().view(np.uint32), o["vals"])
+    if path == "keys":
+        assert np.array_equal(a["keys"].cpu().numpy().view(np.uint64), o["keys"])
+    assert np.array_equal(a["ranges"].cpu().numpy().view(np.uint32), o["ranges"])
+
+
+# ------------------------------------------------------------------ O3 forward
+@pytest.mark.parametrize("c", CFGS)
+def test_forward_parity(c):
+    cfg, p, v = scene(c)
+    pipe, P, V, fr = run_forward(p, v, cfg.cam)
+    a = pipe.arrays(p.shape[1])
+    o = oracle.forward(p, v, cfg.cam, "f32")
+    gpu = dict(color=fr.color, depth=fr.depth, alpha=fr.alpha, n_last=a["n_last"])
+    ties = compare_images(gpu, o, cfg.cam, p, v, f"cfg{c}")
+    nl = a["n_last"].cpu().numpy()
+    ex = a["examined"].cpu().numpy()
+    mism = (nl != o["n_last"]) | (ex != o["examined"])
+    assert int(mism.sum()) <= ties + max(3, int(1e-5 * nl.size)), int(mism.sum())
+    # weight identity on the GPU: 1 - alpha == T_final
+    assert torch.allclose(1 - fr.alpha, a["t_final"], atol=1e-6)
+
+
+def test_forward_sampled_pixels_match_full_oracle_cfg2():
+    """Full-size config 2 in the bench launch configuration: sampled pixels, oracle one by one."""
+    cfg, p, v = scene(2)
+    pipe, P, V, fr = run_forward(p, v, cfg.cam, fwd_flags=0)
+    rng = np.random.default_rng(0)
+    px = rng.choice(cfg.cam.width * cfg.cam.height, 4096, replace=False)
+    o = oracle.forward(p, v, cfg.cam, "f32", pixels=px)
+    gc = fr.color.reshape(3, -1)[:, px].cpu().numpy()
+    err = np.abs(gc - o["color"]).max()
+    ok = np.abs(gc - o["color"]).max(0) <= ATOL_IMG
+    assert ok.mean() >= 1 - 1e-3 and (ok | (o["ambiguous"] == 1)).all(), err
+
+
+# ------------------------------------------------------------------ O4 backward
+def _gpu_backward(pipe, P, V, cfg, dc, dd, cov=True):
+    import paper_2311_11700_b200 as g
+    n = P.shape[1]
+    grad = torch.zeros_like(P)
+    gpose = torch.zeros(6, dtype=torch.float64, device="cuda")
+    pipe.backward(P, n, V, cfg.cam, to_dev(dc), to_dev(dd), grad, gpose,
+                  flags=g.GS_FLAG_POSE_COV_PATH if cov else 0)
+    gpose2 = torch.zeros(6, dtype=torch.float64, device="cuda")
+    pipe.pose_grad(P, n, V, cfg.cam, to_dev(dc), to_dev(dd), gpose2, flags=g.GS_FLAG_POSE_COV_PATH if cov else 0)
+    torch.cuda.synchronize()
+    return grad.cpu().numpy(), gpose.cpu().numpy(), gpose2.cpu().numpy()
+
+
+@pytest.mark.parametrize("c", [0, 1])
+def test_backward_parity(c):
+    cfg, p, v = scene(c)
+    pipe, P, V, fr = run_forward(p, v, cfg.cam)
+    H, W = cfg.cam.height, cfg.cam.width
+    if c == 0:
+        dc, dd = gi.upstream(W, H, gi.UPSTREAM_SEED_CFG0)
+    else:   # L1 upstream against a seeded RGB-D target (same bytes on both sides)
+        tc, td = gi.random_images(W, H, 77)
+        o_f = oracle.forward(p, v, cfg.cam, "f32")
+        L = oracle.loss_l1(o_f["color"], o_f["depth"], tc, td, cfg.w_color, cfg.w_depth)
+        dc, dd = L["dL_dcolor"].astype(np.float32), L["dL_ddepth"].astype(np.float32)
+    nl = pipe.arrays(p.shape[1])["n_last"].cpu().numpy()
+    gg, gpose, gpose2 = _gpu_backward(pipe, P, V, cfg, dc, dd)
+    o = oracle.backward(p, v, cfg.cam, dc, dd, "f32", replay_nlast=nl)
+    bad = grad_close(gg, o["grad_params"])
+    frac = bad.mean()
+    assert frac <= 1e-3, (frac, np.argwhere(bad)[:10])
+    np.testing.assert_allclose(gpose, o["pose_twist"], rtol=2e-3, atol=1e-6)
+    np.testing.assert_array_equal(gpose, gpose2)   # gs_pose_grad == pose part of gs_render_bwd
+    # paper mode: without the covariance path
+    _, gp_paper, _ = _gpu_backward(pipe, P, V, cfg, dc, dd, cov=False)
+    np.testing.assert_allclose(gp_paper, o["pose_twist_paper"], rtol=2e-3, atol=1e-6)
+
+
+# ------------------------------------------------------------------ O5 loss / Adam / pose step
+def test_loss_parity():
+    import paper_2311_11700_b200 as g
+    W, H = 200, 120
+    c, d = gi.random_images(W, H, 5)
+    tc, td = gi.random_images(W, H, 6)
+    c[0, 3, 4] = tc[0, 3, 4]
+    pipe = g.RenderPipeline(16, 4096, W, H)
+    cam = gi.Camera(100.0, 100.0, 99.5, 59.5, W, H)
+    pipe.color.copy_(to_dev(c))
+    pipe.depth.copy_(to_dev(d))
+    dc, dd = pipe.loss_l1(cam, to_dev(tc), to_dev(td), 0.9, 0.1)
+    torch.cuda.synchronize()
+    o = oracle.loss_l1(c, d, tc, td, 0.9, 0.1)
+    np.testing.assert_allclose(dc.cpu().numpy(), o["dL_dcolor"], rtol=1e-6, atol=0)
+    np.testing.assert_allclose(dd.cpu().numpy(), o["dL_ddepth"], rtol=1e-6, atol=0)
+    assert abs(pipe.loss.item() - o["loss"]) <= 1e-6 * abs(o["loss"])
+
+
+def test_adam_parity():
+    import paper_2311_11700_b200 as g
+    rng = np.random.default_rng(3)
+    n, ld = 1000, 1024
+    raw = rng.normal(size=(14, ld)).astype(np.float32)
+    lr = [1.6e-5] * 3 + [2e-4] * 3 + [4e-5] * 4 + [1e-2] + [5e-4] * 3
+    R = to_dev(raw)
+    A = torch.zeros_like(R)
+    M = torch.zeros_like(R)
+    Vv = torch.zeros_like(R)
+    m = np.zeros((14, n))
+    vv = np.zeros((14, n))
+    r64 = raw[:, :n].astype(np.float64)
+    for step in (1, 2, 3):
+        gr = rng.normal(size=(14, ld)).astype(np.float32)
+        g.gs_adam_step(R, A, to_dev(gr), M, Vv, n, ld, lr, step)
+        out = oracle.adam_step(r64, gr[:, :n], m, vv, lr, step)
+        r64, m, vv = out["raw"], out["m"], out["v"]
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(R.cpu().numpy()[:, :n], r64, rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(A.cpu().numpy()[:, :n], oracle.activate(r64), rtol=1e-5, atol=1e-6)
+    assert np.array_equal(R.cpu().numpy()[:, n:], raw[:, n:])   # padding untouched
+
+
+def test_pose_step_parity():
+    import paper_2311_11700_b200 as g
+    view = gi.room_view(103).astype(np.float64)
+    V = to_dev(view)
+    m6 = torch.zeros(6, device="cuda")
+    v6 = torch.zeros(6, device="cuda")
+    mo = np.zeros(6)
+    vo = np.zeros(6)
+    vref = view.astype(np.float32).astype(np.float64)
+    rng = np.random.default_rng(1)
+    for step in (1, 2, 3):
+        gp = rng.normal(size=6)
+        g.gs_pose_step(V, torch.as_tensor(gp, device="cuda"), m6, v6, step, 1e-3, 1e-3)
+        o = oracle.pose_adam_step(vref, gp, mo, vo, step, 1e-3, 1e-3)
+        vref, mo, vo = o["view"], o["m"], o["v"]
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(V.cpu().numpy(), vref, atol=2e-6)
+
+
+# ------------------------------------------------------------------ densify / prune / select
+def test_densify_add_and_prune_parity():
+    import paper_2311_11700_b200 as g
+    cfg, p, v = scene(0)
+    pipe, P, V, fr = run_forward(p, v, cfg.cam)
+    tc, td = gi.random_images(cfg.cam.width, cfg.cam.height, 9)
+    cap = p.shape[1] + 4096
+    Pc = torch.zeros(14, cap, device="cuda")
+    Pc[:, :p.shape[1]] = P
+    n_dev = torch.tensor([p.shape[1]], dtype=torch.int64, device="cuda")
+    cfgd = g.densify_cfg(g.GS_DENSIFY_ADD, max_add=4096)
+    g.gs_densify_prune(Pc, None, n_dev, cap, cap, None, None, fr.alpha, fr.depth, to_dev(tc), to_dev(td), None, V,
+                       g.make_camera(cfg.cam), cfgd, None, None, pipe.ws)
+    torch.cuda.synchronize()
+    o = oracle.densify_add(fr.alpha.cpu().numpy(), fr.depth.cpu().numpy(), tc, td, v, cfg.cam)
+    n1 = int(n_dev.item())
+    assert n1 == p.shape[1] + o.shape[1]
+    np.testing.assert_allclose(Pc[:, p.shape[1]:n1].cpu().numpy(), o, rtol=1e-5, atol=1e-5)
+    # prune
+    Pc[10, :n1] = torch.rand(n1, device="cuda") * 0.01
+    keep = oracle.densify_prune_mask(Pc[10, :n1].cpu().numpy())
+    before = Pc[:, :n1].cpu().numpy()
+    g.gs_densify_prune(Pc, None, n_dev, cap, cap, None, None, None, None, None, None, None, None, None,
+                       g.densify_cfg(g.GS_DENSIFY_PRUNE), None, None, pipe.ws)
+    torch.cuda.synchronize()
+    n2 = int(n_dev.item())
+    assert n2 == int(keep.sum())
+    assert np.array_equal(Pc[:, :n2].cpu().numpy(), before[:, keep])
+
+
+def test_select_parity():
+    import paper_2311_11700_b200 as g
+    cfg, p, v = scene(1)
+    key_cap, _ = key_cap_for(p, v, cfg.cam)
+    pipe = g.RenderPipeline(p.shape[1], key_cap, cfg.cam.width, cfg.cam.height)
+    P, V = to_dev(p), to_dev(v)
+    aw = torch.zeros(p.shape[1], device="cuda")
+    fr = pipe.forward(P, p.shape[1], V, cfg.cam, fwd_flags=g.GS_FLAG_ACCUM_WEIGHT, accum_weight=aw)
+    _, td = gi.random_images(cfg.cam.width, cfg.cam.height, 10, 0.2, 0.4)
+    mask = torch.zeros(p.shape[1], dtype=torch.uint8, device="cuda")
+    n_dev = torch.tensor([p.shape[1]], dtype=torch.int64, device="cuda")
+    g.gs_densify_prune(P, None, n_dev, p.shape[1], p.shape[1], None, None, None, None, None, to_dev(td), aw, V,
+                       g.make_camera(cfg.cam), g.densify_cfg(g.GS_DENSIFY_SELECT), mask, None, pipe.ws)
+    torch.cuda.synchronize()
+    o = oracle.forward(p, v, cfg.cam, "f32", accum_weight=True, replay_nlast=pipe.arrays()["n_last"].cpu().numpy())
+    np.testing.assert_allclose(aw.cpu().numpy(), o["accum_weight"], rtol=2e-3, atol=1e-4)
+    pr = oracle.project(p, v, cfg.cam, "f32")
+    # decide with the GPU's weights (both sides take the decision on the same fp32 values)
+    want = oracle.select_mask(pr["mean2d"], pr["depth"], pr["tiles"], aw.cpu().numpy(), td)
+    assert np.array_equal(mask.cpu().numpy().astype(bool), want)
+
+
+# ------------------------------------------------------------------ edge cases
+def test_edge_empty_and_culled_and_ragged():
+    import paper_2311_11700_b200 as g
+    cam = gi.Camera(30.0, 30.0, 16.0, 10.0, 37, 21, bg=(0.2, 0.3, 0.4))   # ragged: 37x21 -> 3x2 tiles
+    for n in (0, 5):
+        p = np.zeros((14, max(n, 1)), np.float32)
+        p[2] = -1.0   # all behind the camera
+        p[6] = 1.0
+        p[3:6] = 0.1
+        pipe, P, V, fr = run_forward(p[:, :n] if n else p[:, :0], gi.identity_view(), cam, key_cap=4096)
+        assert fr.n_keys == 0
+        assert torch.allclose(fr.color[0], torch.full_like(fr.color[0], 0.2))
+        assert (fr.depth == 0).all() and (fr.alpha == 0).all()
+    # one Gaussian, ragged image: parity
+    p = np.zeros((14, 1), np.float32)
+    p[:, 0] = [0.05, 0.02, 1.5, 0.1, 0.05, 0.08, 0.9, 0.1, 0.2, 0.3, 0.7, 0.9, 0.5, 0.1]
+    pipe, P, V, fr = run_forward(p, gi.identity_view(), cam, key_cap=4096)
+    o = oracle.forward(p, gi.identity_view(), cam, "f32")
+    assert np.abs(fr.color.cpu().numpy() - o["color"]).max() <= ATOL_IMG
+
+
+def test_capacity_error_and_stale():
+    import paper_2311_11700_b200 as g
+    cfg, p, v = scene(0)
+    pipe = g.RenderPipeline(p.shape[1], 128, cfg.cam.width, cfg.cam.height)   # far too few keys
+    with pytest.raises(g.GSError) as e:
+        pipe.forward(to_dev(p), p.shape[1], to_dev(v), cfg.cam)
+    assert e.value.status == g.GS_ERR_CAPACITY
+    key_cap, _ = key_cap_for(p, v, cfg.cam)
+    pipe = g.RenderPipeline(p.shape[1], key_cap, cfg.cam.width, cfg.cam.height)
+    P, V = to_dev(p), to_dev(v)
+    pipe.forward(P, p.shape[1], V, cfg.cam)
+    g.gs_project(P, p.shape[1], p.shape[1], None, V, g.make_camera(cfg.cam), pipe.ws)   # project again
+    grad = torch.zeros_like(P)
+    with pytest.raises(g.GSError) as e:
+        pipe.backward(P, p.shape[1], V, cfg.cam, pipe.dL_dcolor, pipe.dL_ddepth, grad)
+    assert e.value.status == g.GS_ERR_STALE
+
+
+def test_no_host_sync_mode_matches():
+    import paper_2311_11700_b200 as g
+    cfg, p, v = scene(1)
+    pipe, P, V, fr = run_forward(p, v, cfg.cam)
+    ref = fr.color.clone()
+    vals = pipe.arrays()["vals"].clone()
+    pipe.forward(P, p.shape[1], V, cfg.cam, bin_flags=g.GS_FLAG_NO_HOST_SYNC)
+    torch.cuda.synchronize()
+    assert torch.equal(pipe.color, ref)
+    a = pipe.arrays(n_keys=vals.numel())
+    assert torch.equal(a["vals"], vals)
