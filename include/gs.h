@@ -61,9 +61,11 @@ enum {
                                      the device; overflow sets the device error flag (CUDA-graph mode) */
     GS_FLAG_ACCUM_WEIGHT = 4u,    /* gs_render_fwd: accumulate per-Gaussian sum_px alpha*T (Eq. 12 select) */
     GS_FLAG_EXAMINED = 8u,        /* gs_render_fwd: write the per-pixel examined count (for E_f) */
-    GS_FLAG_BINSORT_KEYS = 16u    /* gs_bin_sort: emit 64-bit (tile|depth) keys and onesweep-sort them
+    GS_FLAG_BINSORT_KEYS = 16u,   /* gs_bin_sort: emit 64-bit (tile|depth) keys and onesweep-sort them
                                      (north_star literal path); default = depth-presort + tile bucketing
                                      (bit-identical lists, fewer HBM bytes) */
+    GS_FLAG_BINSORT_EMIT_ONLY = 256u  /* testing: with GS_FLAG_BINSORT_KEYS, stop after key emission (the
+                                     view's keys/vals then hold the unsorted index-order emission) */
 };
 
 /* ---------------------------------------------------------------------------------------------
@@ -176,6 +178,7 @@ typedef struct {
     const int16_t* rect;         /* [n][4] xlo, xhi, ylo, yhi */
     const int32_t* radius;       /* [n] */
     const uint32_t* tiles;       /* [n] tiles touched */
+    const uint32_t* offsets;     /* [n] exclusive prefix of tiles (key-emission offsets, GS_FLAG_BINSORT_KEYS) */
     const uint64_t* keys;        /* [K] sorted (tile << 32 | depth key); valid after gs_bin_sort */
     const uint32_t* vals;        /* [K] sorted Gaussian indices */
     const uint32_t* ranges;      /* [GX*GY][2] */

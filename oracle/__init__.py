@@ -119,8 +119,10 @@ def bin_sort(depth_bits, rect, tiles, cam) -> dict:
 
 
 # ------------------------------------------------------------------------------------ O3
-def forward(params, view, cam, precision="f32", pixels=None, replay_nlast=None, accum_weight=False) -> dict:
-    """O3 (Eq. 4-5, cumulative opacity P:118). Full images unless `pixels` (linear ids) given."""
+def forward(params, view, cam, precision="f32", pixels=None, replay_nlast=None, accum_weight=False,
+            flip_skip_ties=False) -> dict:
+    """O3 (Eq. 4-5, cumulative opacity P:118). Full images unless `pixels` (linear ids) given.
+    replay_nlast / flip_skip_ties: the parity tie rule's replays (reading R1)."""
     dt = _dtype(precision)
     params = np.ascontiguousarray(params, dt)
     view = np.ascontiguousarray(view, dt)
@@ -145,7 +147,7 @@ def forward(params, view, cam, precision="f32", pixels=None, replay_nlast=None, 
     getattr(lib(), f"oracle_forward_{precision}")(
         _p(params), ctypes.c_int64(n), ctypes.c_int64(n), _p(view), ctypes.byref(c), _p(pixels),
         ctypes.c_int64(npx), _p(rp), _p(color), _p(depth), _p(alpha), _p(n_last), _p(examined), _p(amb),
-        _p(h), _p(aw))
+        _p(h), _p(aw), ctypes.c_int32(1 if flip_skip_ties else 0))
     out = dict(color=color.reshape((3,) + shape), depth=depth.reshape(shape), alpha=alpha.reshape(shape),
                n_last=n_last.reshape(shape), examined=examined.reshape(shape), ambiguous=amb.reshape(shape),
                hash=int(h[0]))

@@ -219,12 +219,18 @@ static inline void fnv(uint64_t& h, uint64_t v) {
 template <class R>
 static void blend_pixel(int u, int v, const std::vector<Proj<R>>& pj, const std::vector<int64_t>& order,
                         const R* params, int64_t ld, const Cam<R>& cam, int64_t replay_nlast, bool keep_list,
-                        PixelResult& out) {
+                        PixelResult& out, bool flip_skip_ties = false) {
     const int tx = u / TILE, ty = v / TILE;
     const R fu = R(u), fv = R(v);
     const R a_min = R(1) / R(255), a_max = R(0.99), t_min = R(1e-4);
     R T = R(1);
     uint32_t j = 0;
+    // Tie band (reading R1): a conforming fp32 evaluation may differ from this one by
+    // the exp's error (<= 2^-20 relative incl. argument rounding) in every unclamped alpha; the
+    // resulting relative divergence of T is bounded by sum_k (2^-20 alpha_k / (1 - alpha_k) + 2^-23).
+    // A decision value within that band (floor 1e-5 relative) of its threshold marks the pixel
+    // ambiguous.
+    double t_band = 0.0;
     for (int64_t i : order) {
         const Proj<R>& g = pj[size_t(i)];
         if (tx < g.xlo || tx >= g.xhi || ty < g.ylo || ty >= g.yhi) continue;
@@ -238,19 +244,26 @@ static void blend_pixel(int u, int v, const std::vector<Proj<R>>& pj, const std:
         const R o = params[10 * ld + i];
         const R og = o * G;
         const R alpha = std::min(a_max, og);
-        if (std::fabs(double(alpha) - double(a_min)) <= 1e-5 * double(a_min)) out.ambiguous = 1;
-        if (alpha < a_min) continue;
+        const bool amb_skip = std::fabs(double(alpha) - double(a_min)) <= 1e-5 * double(a_min);
+        if (amb_skip) out.ambiguous = 1;
+        bool skip = alpha < a_min;
+        if (flip_skip_ties && amb_skip) skip = !skip;   // tie-rule replay: take the other decision
+        if (skip) continue;
         const R Tn = T * (R(1) - alpha);
+        const bool clamped = og > a_max;
+        const double step_band = (clamped ? 0.0 : 9.5367431640625e-07 * double(alpha) / (1.0 - double(alpha))) +
+                                 1.1920928955078125e-07;
         if (replay_nlast < 0) {
-            if (std::fabs(double(Tn) - double(t_min)) <= 1e-5 * double(t_min)) out.ambiguous = 1;
+            const double band = std::max(1e-5, t_band + step_band);
+            if (std::fabs(double(Tn) - double(t_min)) <= band * double(t_min)) out.ambiguous = 1;
             if (Tn < t_min) break;   // terminating Gaussian is not blended
         }
+        t_band += step_band;
         const double w = double(alpha) * double(T);
         for (int c = 0; c < 3; ++c) out.color[c] += w * double(params[(11 + c) * ld + i]);
         out.depth += w * double(g.zc);
         T = Tn;
         out.n_last = j;
-        const bool clamped = og > a_max;
         fnv(out.hash, uint64_t(i) * 2 + (clamped ? 1 : 0));
         if (keep_list) out.list.push_back(Contrib{i, double(alpha), double(G), double(dx), double(dy), clamped});
     }
@@ -548,7 +561,7 @@ int64_t oracle_bin(const uint32_t* depth_bits, const int32_t* rect, const uint32
                              const int64_t* pixels, int64_t n_pix, const uint32_t* replay_nlast,          \
                              double* color, double* depth, double* alpha, uint32_t* n_last,               \
                              uint32_t* examined, uint8_t* ambiguous, uint64_t* hash,                      \
-                             double* accum_weight) {                                                      \
+                             double* accum_weight, int32_t flip_skip_ties) {                              \
         Cam<R> cam(*oc);                                                                                  \
         auto pj = project_all<R>(params, n, ld, view, cam);                                               \
         auto order = depth_order(pj);                                                                     \
@@ -560,7 +573,7 @@ int64_t oracle_bin(const uint32_t* depth_bits, const int32_t* rect, const uint32
             const int u = int(pid % cam.W), v = int(pid / cam.W);                                         \
             PixelResult r;                                                                                \
             blend_pixel<R>(u, v, pj, order, params, ld, cam, replay_nlast ? int64_t(replay_nlast[q]) : -1, \
-                           accum_weight != nullptr, r);                                                   \
+                           accum_weight != nullptr, r, flip_skip_ties != 0);                              \
             if (accum_weight) { /* Eq. 12 reading C24: per-Gaussian sum of alpha_i T_i */                 \
                 double Tk = 1.0;                                                                          \
                 for (const Contrib& ct : r.list) { atomic_add(accum_weight[ct.i], ct.alpha * Tk); Tk *= 1.0 - ct.alpha; } \

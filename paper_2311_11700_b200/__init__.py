@@ -26,6 +26,7 @@ GS_FLAG_NO_HOST_SYNC = 2
 GS_FLAG_ACCUM_WEIGHT = 4
 GS_FLAG_EXAMINED = 8
 GS_FLAG_BINSORT_KEYS = 16
+GS_FLAG_BINSORT_EMIT_ONLY = 256
 GS_DENSIFY_ADD, GS_DENSIFY_PRUNE, GS_DENSIFY_SELECT = 1, 2, 3
 
 
@@ -41,7 +42,8 @@ class gs_ws(ctypes.Structure):
 
 class gs_ws_view(ctypes.Structure):
     _fields_ = [("records", ctypes.c_void_p), ("depth_key", ctypes.c_void_p), ("rect", ctypes.c_void_p),
-                ("radius", ctypes.c_void_p), ("tiles", ctypes.c_void_p), ("keys", ctypes.c_void_p),
+                ("radius", ctypes.c_void_p), ("tiles", ctypes.c_void_p), ("offsets", ctypes.c_void_p),
+                ("keys", ctypes.c_void_p),
                 ("vals", ctypes.c_void_p), ("ranges", ctypes.c_void_p), ("t_final", ctypes.c_void_p),
                 ("n_last", ctypes.c_void_p), ("examined", ctypes.c_void_p), ("n_keys_dev", ctypes.c_void_p),
                 ("error_flag", ctypes.c_void_p), ("n", ctypes.c_int64), ("key_cap", ctypes.c_int64),

@@ -257,6 +257,7 @@ gs_status gs_ws_get_view(const gs_ws* ws, gs_ws_view* out) {
     out->rect = at<int16_t>(s, s->rect);
     out->radius = at<int32_t>(s, s->radius);
     out->tiles = at<uint32_t>(s, s->tiles);
+    out->offsets = at<uint32_t>(s, s->offsets);
     out->keys = s->sorted_in_1 ? at<uint64_t>(s, s->keys1) : at<uint64_t>(s, s->keys0);
     out->vals = s->sorted_in_1 ? at<uint32_t>(s, s->vals1) : at<uint32_t>(s, s->vals0);
     out->ranges = at<uint32_t>(s, s->ranges);

@@ -121,7 +121,8 @@ __global__ void __launch_bounds__(256) emit_keys_kernel(
     const uint32_t total = __reduce_add_sync(0xffffffffu, cnt);
     short4 rc = in ? rect[g] : make_short4(0, 0, 0, 0);
     const uint32_t dk = in ? dkey[g] : 0u;
-    for (uint32_t j = lane; j < total; j += 32) {
+    for (uint32_t j0 = 0; j0 < total; j0 += 32) {   // warp-uniform trip count (full-mask shuffles)
+        const uint32_t j = j0 + lane;
         int lo = 0;
 #pragma unroll
         for (int step = 16; step > 0; step >>= 1) {
@@ -133,13 +134,15 @@ __global__ void __launch_bounds__(256) emit_keys_kernel(
         const int xhi = __shfl_sync(0xffffffffu, int(rc.y), lo);
         const int ylo = __shfl_sync(0xffffffffu, int(rc.z), lo);
         const uint32_t d = __shfl_sync(0xffffffffu, dk, lo);
-        const uint32_t l = j - my_rel;
-        const uint32_t w = uint32_t(xhi - xlo);
-        const uint32_t row = l / w;
-        const uint32_t tx = uint32_t(xlo) + (l - row * w), ty = uint32_t(ylo) + row;
-        const uint64_t o = uint64_t(base) + j;
-        keys[o] = (uint64_t(ty * uint32_t(GX) + tx) << 32) | d;
-        vals[o] = uint32_t(g0 + lo);
+        if (j < total) {
+            const uint32_t l = j - my_rel;
+            const uint32_t w = uint32_t(xhi - xlo);
+            const uint32_t row = l / w;
+            const uint32_t tx = uint32_t(xlo) + (l - row * w), ty = uint32_t(ylo) + row;
+            const uint64_t o = uint64_t(base) + j;
+            keys[o] = (uint64_t(ty * uint32_t(GX) + tx) << 32) | d;
+            vals[o] = uint32_t(g0 + lo);
+        }
     }
 }
 
@@ -214,6 +217,10 @@ gs_status run_bin_sort_keys(WsState* s, int64_t* n_keys, uint32_t flags, cudaStr
                                                  at<short4>(s, s->rect), at<uint32_t>(s, s->depth_key), s->cam_gx,
                                                  &misc->n_keys, s->key_cap, &misc->error_flag,
                                                  at<uint64_t>(s, s->keys0), at<uint32_t>(s, s->vals0));
+    }
+    if (flags & GS_FLAG_BINSORT_EMIT_ONLY) {
+        s->sorted_in_1 = 0;
+        return check_launch(s, "bin_sort_keys(emit only)");
     }
     // onesweep LSD radix sort over bits [0, 32 + TB)
     const int bits = 32 + ceil_log2(uint32_t(ntiles));

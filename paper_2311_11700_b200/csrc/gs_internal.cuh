@@ -133,9 +133,13 @@ __device__ __forceinline__ AlphaEval eval_alpha(float4 r0, float4 r1, float px, 
     AlphaEval e;
     e.dx = __fsub_rn(r0.x, px);
     e.dy = __fsub_rn(r0.y, py);
-    // power = -0.5 (a dx^2 + c dy^2) - b dx dy
-    const float q = __fmaf_rn(__fmul_rn(r1.x, e.dy), e.dy, __fmul_rn(__fmul_rn(r0.z, e.dx), e.dx));
-    const float power = __fmaf_rn(-0.5f, q, -__fmul_rn(__fmul_rn(r0.w, e.dx), e.dy));
+    // power = -0.5 ((a dx) dx + (c dy) dy) - (b dx) dy, each operation rounded separately in the
+    // oracle's order (O3): for elongated conics the terms cancel, and any other
+    // evaluation order would move power by many ulps and flip alpha-vs-1/255 decisions.
+    const float t1 = __fmul_rn(__fmul_rn(r0.z, e.dx), e.dx);
+    const float t2 = __fmul_rn(__fmul_rn(r1.x, e.dy), e.dy);
+    const float t3 = __fmul_rn(__fmul_rn(r0.w, e.dx), e.dy);
+    const float power = __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(t1, t2)), t3);
     // G = exp(power) via ex2.approx (MUFU): power * log2(e)
     float G;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(G) : "f"(__fmul_rn(power, 1.4426950408889634f)));

@@ -34,8 +34,7 @@ template <bool kAccum>
 __global__ void __launch_bounds__(kTilePx) render_fwd_kernel(
     const float4* __restrict__ rec, const uint32_t* __restrict__ vals, const uint2* __restrict__ ranges, int W, int H,
     int GX, float bgr, float bgg, float bgb, float* __restrict__ color, float* __restrict__ depth,
-    float* __restrict__ alpha, float* __restrict__ ws_color, float* __restrict__ ws_depth,
-    float* __restrict__ t_final, uint32_t* __restrict__ n_last, uint32_t* __restrict__ examined,
+    float* __restrict__ alpha, float* __restrict__ t_final, uint32_t* __restrict__ n_last, uint32_t* __restrict__ examined,
     float* __restrict__ accum_weight) {
     __shared__ float4 s_rec[2][kFwdBatch][3];
     const int tile = blockIdx.x;
@@ -135,10 +134,6 @@ __global__ void __launch_bounds__(kTilePx) render_fwd_kernel(
         color[2 * plane + pix] = cb;
         depth[pix] = D;
         alpha[pix] = 1.f - T;
-        ws_color[pix] = cr;
-        ws_color[plane + pix] = cg;
-        ws_color[2 * plane + pix] = cb;
-        ws_depth[pix] = D;
         t_final[pix] = T;
         n_last[pix] = nl;
         if (examined) examined[pix] = exam;
@@ -148,9 +143,6 @@ __global__ void __launch_bounds__(kTilePx) render_fwd_kernel(
 void launch_render_fwd(WsState* s, const gs_camera& cam, float* color, float* depth, float* alpha,
                        float* accum_weight, uint32_t flags, cudaStream_t st) {
     const int ntiles = s->cam_gx * s->cam_gy;
-    const size_t plane = size_t(cam.width) * cam.height;
-    float* wsc = at<float>(s, s->scratch);             // [3][H][W] colour copy for the backward
-    float* wsd = wsc + 3 * plane;                      // [H][W] depth copy
     const uint32_t* sorted_vals = s->sorted_in_1 ? at<uint32_t>(s, s->vals1) : at<uint32_t>(s, s->vals0);
     uint32_t* exam = (flags & GS_FLAG_EXAMINED) ? at<uint32_t>(s, s->examined) : nullptr;
     if (ntiles == 0) return;
@@ -158,13 +150,13 @@ void launch_render_fwd(WsState* s, const gs_camera& cam, float* color, float* de
     if ((flags & GS_FLAG_ACCUM_WEIGHT) && accum_weight) {
         render_fwd_kernel<true><<<ntiles, kTilePx, 0, st>>>(
             at<float4>(s, s->rec), sorted_vals, at<uint2>(s, s->ranges), cam.width, cam.height, s->cam_gx, cam.bg[0],
-            cam.bg[1], cam.bg[2], color, depth, alpha, wsc, wsd, at<float>(s, s->t_final), at<uint32_t>(s, s->n_last),
-            exam, accum_weight);
+            cam.bg[1], cam.bg[2], color, depth, alpha, at<float>(s, s->t_final), at<uint32_t>(s, s->n_last), exam,
+            accum_weight);
     } else {
         render_fwd_kernel<false><<<ntiles, kTilePx, 0, st>>>(
             at<float4>(s, s->rec), sorted_vals, at<uint2>(s, s->ranges), cam.width, cam.height, s->cam_gx, cam.bg[0],
-            cam.bg[1], cam.bg[2], color, depth, alpha, wsc, wsd, at<float>(s, s->t_final), at<uint32_t>(s, s->n_last),
-            exam, nullptr);
+            cam.bg[1], cam.bg[2], color, depth, alpha, at<float>(s, s->t_final), at<uint32_t>(s, s->n_last), exam,
+            nullptr);
     }
 }
 
@@ -184,7 +176,7 @@ struct BwdSmem {
 
 __global__ void __launch_bounds__(kTilePx, 2) render_bwd_kernel(
     const float4* __restrict__ rec, const uint32_t* __restrict__ vals, const uint2* __restrict__ ranges, int W, int H,
-    int GX, const float* __restrict__ img_c, const float* __restrict__ img_d, const uint32_t* __restrict__ n_last,
+    int GX, const float* __restrict__ t_final, float bgr, float bgg, float bgb, const uint32_t* __restrict__ n_last,
     const float* __restrict__ dLdC, const float* __restrict__ dLdD, float* __restrict__ sgrad, int64_t sld) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BwdSmem& sm = *reinterpret_cast<BwdSmem*>(smem_raw);
@@ -201,12 +193,13 @@ __global__ void __launch_bounds__(kTilePx, 2) render_bwd_kernel(
 
     uint32_t nl = 0;
     float4 dl = make_float4(0.f, 0.f, 0.f, 0.f);
-    float Q = 0.f;
+    float T = 1.f;   // T_{i+1} while walking back; starts at T_final
     if (inside) {
         nl = n_last[pix];
         dl = make_float4(dLdC[pix], dLdC[plane + pix], dLdC[2 * plane + pix], dLdD[pix]);
-        Q = img_c[pix] * dl.x + img_c[plane + pix] * dl.y + img_c[2 * plane + pix] * dl.z + img_d[pix] * dl.w;
+        T = t_final[pix];
     }
+    const float tfb = T * (bgr * dl.x + bgg * dl.y + bgb * dl.z);   // T_f bg . dL/dC
     if (tid == 0) sm.max_nl = 0;
     sm.dl[tid] = dl;
     __syncthreads();
@@ -215,13 +208,14 @@ __global__ void __launch_bounds__(kTilePx, 2) render_bwd_kernel(
     const uint32_t len = sm.max_nl;
     const int nbatch = int((len + kBwdBatch - 1) / kBwdBatch);
 
-    auto stage = [&](int b) {
+    // batch bb holds list positions [bb*32, bb*32+32); batches are visited back to front
+    auto stage = [&](int bb, int slot) {
         if (tid < kBwdBatch) {
-            const uint32_t j = uint32_t(b) * kBwdBatch + tid;
+            const uint32_t j = uint32_t(bb) * kBwdBatch + tid;
             if (j < len) {
                 const uint32_t g = vals[start + j];
-                sm.idx[b & 1][tid] = g;
-                float4* dst = sm.rec[b & 1][tid];
+                sm.idx[slot][tid] = g;
+                float4* dst = sm.rec[slot][tid];
                 const float4* src = rec + 3 * size_t(g);
                 cp_async16(dst + 0, src + 0);
                 cp_async16(dst + 1, src + 1);
@@ -231,35 +225,37 @@ __global__ void __launch_bounds__(kTilePx, 2) render_bwd_kernel(
         cp_async_commit();
     };
 
-    float T = 1.f, P = 0.f;
-    if (nbatch > 0) stage(0);
-    for (int b = 0; b < nbatch; ++b) {
-        if (b + 1 < nbatch) {
-            stage(b + 1);
+    float S = 0.f;   // sum_{k>i} alpha_k T_k e_k  (suffix sum, accumulated from the back)
+    if (nbatch > 0) stage(nbatch - 1, 0);
+    for (int it = 0; it < nbatch; ++it) {
+        const int bb = nbatch - 1 - it;
+        if (it + 1 < nbatch) {
+            stage(bb - 1, (it + 1) & 1);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
         __syncthreads();
-        const int buf = b & 1;
-        const int cnt = min(kBwdBatch, int(len) - b * kBwdBatch);
-        // ---- phase 1: thread = pixel, front to back over the batch
+        const int buf = it & 1;
+        const int cnt = min(kBwdBatch, int(len) - bb * kBwdBatch);
+        // ---- phase 1: thread = pixel, back to front over the batch (3DGS-style recurrence):
+        //      T_i = T_{i+1} / (1 - alpha_i);  dL/dalpha_i = T_i e_i - (S_i + T_f bg.dL/dC) / (1 - alpha_i)
 #pragma unroll 4
-        for (int k = 0; k < kBwdBatch; ++k) {
+        for (int k = kBwdBatch - 1; k >= 0; --k) {
             float w = 0.f, go = 0.f;
-            const uint32_t jpos = uint32_t(b * kBwdBatch + k + 1);
+            const uint32_t jpos = uint32_t(bb * kBwdBatch + k + 1);
             if (k < cnt && jpos <= nl) {
                 const float4 r0 = sm.rec[buf][k][0], r1 = sm.rec[buf][k][1];
                 const AlphaEval e = eval_alpha(r0, r1, fpx, fpy);
                 if (e.alpha != 0.f) {
                     const float4 r2 = sm.rec[buf][k][2];
                     const float ev = fmaf(r2.x, dl.x, fmaf(r2.y, dl.y, fmaf(r2.z, dl.z, r1.z * dl.w)));
-                    const float oma = __fsub_rn(1.f, e.alpha);
-                    w = __fmul_rn(e.alpha, T);
-                    P = fmaf(w, ev, P);
-                    const float ga = fmaf(T, ev, -(Q - P) * __frcp_rn(oma));
+                    const float ro = __frcp_rn(__fsub_rn(1.f, e.alpha));
+                    T = T * ro;
+                    w = e.alpha * T;
+                    const float ga = fmaf(T, ev, -(S + tfb) * ro);
                     go = e.clamped ? 0.f : e.G * ga;
-                    T = __fmul_rn(T, oma);
+                    S = fmaf(w, ev, S);
                 }
             }
             sm.w[tid][k] = w;
@@ -294,23 +290,23 @@ __global__ void __launch_bounds__(kTilePx, 2) render_bwd_kernel(
         __syncthreads();
         // ---- combine the 8 warps; convert moments to screen-space gradients; one atomic each
         if (tid < cnt) {
-            float S[10];
+            float Mo[10];   // pixel moments of this Gaussian over the tile
 #pragma unroll
             for (int c = 0; c < 10; ++c) {
                 float a = 0.f;
 #pragma unroll
                 for (int w2 = 0; w2 < kWarps; ++w2) a += sm.part[w2][c][tid];
-                S[c] = a;
+                Mo[c] = a;
             }
             const float4 r0 = sm.rec[buf][tid][0], r1 = sm.rec[buf][tid][1];
             const float o = r1.y;
             const float X = r0.x - float(tx * kTile), Y = r0.y - float(ty * kTile);
             // sum g dx, sum g dy, sum g dx^2, sum g dx dy, sum g dy^2 with dx = X - lx, dy = Y - ly
-            const float gdx = X * S[0] - S[1];
-            const float gdy = Y * S[0] - S[2];
-            const float gdxx = X * X * S[0] - 2.f * X * S[1] + S[3];
-            const float gdxy = X * Y * S[0] - X * S[2] - Y * S[1] + S[4];
-            const float gdyy = Y * Y * S[0] - 2.f * Y * S[2] + S[5];
+            const float gdx = X * Mo[0] - Mo[1];
+            const float gdy = Y * Mo[0] - Mo[2];
+            const float gdxx = X * X * Mo[0] - 2.f * X * Mo[1] + Mo[3];
+            const float gdxy = X * Y * Mo[0] - X * Mo[2] - Y * Mo[1] + Mo[4];
+            const float gdyy = Y * Y * Mo[0] - 2.f * Y * Mo[2] + Mo[5];
             const float ca = r0.z, cb = r0.w, cc = r1.x;
             float out[10];
             out[0] = -o * (ca * gdx + cb * gdy);   // mean2d x
@@ -318,11 +314,11 @@ __global__ void __launch_bounds__(kTilePx, 2) render_bwd_kernel(
             out[2] = -0.5f * o * gdxx;             // conic a
             out[3] = -o * gdxy;                    // conic b
             out[4] = -0.5f * o * gdyy;             // conic c
-            out[5] = S[0];                         // opacity
-            out[6] = S[6];
-            out[7] = S[7];
-            out[8] = S[8];                         // rgb
-            out[9] = S[9];                         // depth
+            out[5] = Mo[0];                        // opacity
+            out[6] = Mo[6];
+            out[7] = Mo[7];
+            out[8] = Mo[8];                        // rgb
+            out[9] = Mo[9];                        // depth
             const uint32_t g = sm.idx[buf][tid];
 #pragma unroll
             for (int c = 0; c < 10; ++c)
@@ -336,9 +332,6 @@ void launch_render_bwd_tiles(WsState* s, const gs_camera& cam, const float*, con
                              const float* dL_ddepth, cudaStream_t st) {
     const int ntiles = s->cam_gx * s->cam_gy;
     if (ntiles == 0) return;
-    const size_t plane = size_t(cam.width) * cam.height;
-    const float* wsc = at<float>(s, s->scratch);
-    const float* wsd = wsc + 3 * plane;
     const uint32_t* sorted_vals = s->sorted_in_1 ? at<uint32_t>(s, s->vals1) : at<uint32_t>(s, s->vals0);
     static bool attr = false;
     if (!attr) {
@@ -347,8 +340,9 @@ void launch_render_bwd_tiles(WsState* s, const gs_camera& cam, const float*, con
     }
     KTimer kt(s, KID_BWD_TILE, st);
     render_bwd_kernel<<<ntiles, kTilePx, sizeof(BwdSmem), st>>>(
-        at<float4>(s, s->rec), sorted_vals, at<uint2>(s, s->ranges), cam.width, cam.height, s->cam_gx, wsc, wsd,
-        at<uint32_t>(s, s->n_last), dL_dcolor, dL_ddepth, at<float>(s, s->sgrad), s->n_cap);
+        at<float4>(s, s->rec), sorted_vals, at<uint2>(s, s->ranges), cam.width, cam.height, s->cam_gx,
+        at<float>(s, s->t_final), cam.bg[0], cam.bg[1], cam.bg[2], at<uint32_t>(s, s->n_last), dL_dcolor, dL_ddepth,
+        at<float>(s, s->sgrad), s->n_cap);
 }
 
 // ------------------------------------------------------------------ backward, per-Gaussian chain

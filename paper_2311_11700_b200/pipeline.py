@@ -90,6 +90,7 @@ class RenderPipeline:
         out = dict(records=t(v.records, n * 12, torch.float32).view(n, 12),
                    depth_key=t(v.depth_key, n, torch.int32), rect=t(v.rect, n * 4, torch.int16).view(n, 4),
                    radius=t(v.radius, n, torch.int32), tiles=t(v.tiles, n, torch.int32),
+                   offsets=t(v.offsets, n, torch.int32),
                    ranges=t(v.ranges, ntiles * 2, torch.int32).view(ntiles, 2),
                    t_final=t(v.t_final, npx, torch.float32).view(v.height, v.width),
                    n_last=t(v.n_last, npx, torch.int32).view(v.height, v.width),

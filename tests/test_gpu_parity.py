@@ -130,7 +130,8 @@ def test_backward_parity(c):
     frac = bad.mean()
     assert frac <= 1e-3, (frac, np.argwhere(bad)[:10])
     np.testing.assert_allclose(gpose, o["pose_twist"], rtol=2e-3, atol=1e-6)
-    np.testing.assert_array_equal(gpose, gpose2)   # gs_pose_grad == pose part of gs_render_bwd
+    # gs_pose_grad == pose part of gs_render_bwd (fp32 atomics: equal up to summation order)
+    np.testing.assert_allclose(gpose, gpose2, rtol=1e-3, atol=1e-6)
     # paper mode: without the covariance path
     _, gp_paper, _ = _gpu_backward(pipe, P, V, cfg, dc, dd, cov=False)
     np.testing.assert_allclose(gp_paper, o["pose_twist_paper"], rtol=2e-3, atol=1e-6)
@@ -202,9 +203,12 @@ def test_pose_step_parity():
 def test_densify_add_and_prune_parity():
     import paper_2311_11700_b200 as g
     cfg, p, v = scene(0)
-    pipe, P, V, fr = run_forward(p, v, cfg.cam)
-    tc, td = gi.random_images(cfg.cam.width, cfg.cam.height, 9)
     cap = p.shape[1] + 4096
+    key_cap, _ = key_cap_for(p, v, cfg.cam)
+    pipe = g.RenderPipeline(cap, key_cap, cfg.cam.width, cfg.cam.height)   # prune scratch sized for cap
+    P, V = to_dev(p), to_dev(v)
+    fr = pipe.forward(P, p.shape[1], V, cfg.cam)
+    tc, td = gi.random_images(cfg.cam.width, cfg.cam.height, 9)
     Pc = torch.zeros(14, cap, device="cuda")
     Pc[:, :p.shape[1]] = P
     n_dev = torch.tensor([p.shape[1]], dtype=torch.int64, device="cuda")
