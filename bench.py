@@ -284,7 +284,7 @@ def main_ours(args):
         out["kernels_launches_per_step"] = {k: v_[1] for k, v_ in per_step.items()}
         out["ms_per_step_with_event_log"] = ms_logged
         out["roofline"] = roofline(per_step, clocks, K=K, n=n, V_s=V_s, E_f=E_f, E_b=E_b,
-                                   npx=cam.width * cam.height)
+                                   npx=cam.width * cam.height, binsort=args.binsort)
         # ---- e2e through the public API with host buffers (pinned) and a loss readback
         if not args.no_e2e:
             hp = torch.empty_like(P, device="cpu").pin_memory()
@@ -331,26 +331,28 @@ def main_ours(args):
     return 0
 
 
-def roofline(per_step, clocks, K, n, V_s, E_f, E_b, npx):
+def roofline(per_step, clocks, K, n, V_s, E_f, E_b, npx, binsort="bucket"):
     peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json"), {}) or {}
     hbm_peak = peaks.get("hbm_gbs")
     hbm_src = "measured" if hbm_peak else "fallback"
     hbm_peak = hbm_peak or 6650.0
     sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz") or 1965.0
     alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e12   # FP32 lane-ops/s, T
-    work = {   # (bound, algorithmic amount per step, unit)
+    T = ((1200 + 15) // 16) * ((680 + 15) // 16)
+    work = {   # (bound, algorithmic amount PER LAUNCH, unit) -- DESIGN.md §6 table
         "render_bwd_tiles": ("alu", E_b * BWD_OPS_PER_EVAL / 1e12, "TFLOP/s"),
         "render_fwd": ("alu", E_f * FWD_OPS_PER_EVAL / 1e12, "TFLOP/s"),
-        "sort_pass": ("hbm", K * SORT_BYTES_PER_KEY / 1e9, "GB/s"),
+        # path A sorts K (u64, u32) pairs per pass; path B sorts n (u32, u32) depth pairs per pass
+        "sort_pass": ("hbm", (K * SORT_BYTES_PER_KEY if binsort == "keys" else n * 16) / 1e9, "GB/s"),
         "emit_keys": ("hbm", (K * 12 + n * 20) / 1e9, "GB/s"),
+        "bucket_emit": ("hbm", (K * 4 + V_s * 12) / 1e9, "GB/s"),
         "project": ("hbm", n * (56 + 72) / 1e9, "GB/s"),
         "gaussian_bwd": ("hbm", (n * 4 + V_s * 244) / 1e9, "GB/s"),
-        "loss_l1": ("hbm", npx * 48 / 1e9, "GB/s"),
+        "loss_l1": ("hbm", npx * 24 / 1e9, "GB/s"),
     }
     dom = max((k for k in per_step if k in work), key=lambda k: per_step[k][0])
-    bound, amount, unit = work[dom]
+    bound, per_launch_amount, unit = work[dom]
     t_ms, launches = per_step[dom]
-    per_launch_amount = amount / max(launches, 1)
     per_launch_s = t_ms / 1e3 / max(launches, 1)
     achieved = per_launch_amount / per_launch_s
     peak = alu_peak if bound == "alu" else hbm_peak

@@ -64,8 +64,10 @@ static void carve(WsState* s, Carver& c) {
     s->scratch14 = c.take(uint64_t(n) * 4 * 14);
     s->dkey_sorted = c.take(uint64_t(n) * 4 * 2);
     s->dval_sorted = c.take(uint64_t(n) * 4 * 2);
-    s->chunk_hist = c.take(uint64_t(std::max<int64_t>((n + 2047) / 2048, (px + 2047) / 2048) + 1) * 4 +
-                           uint64_t((n + 1023) / 1024 + 1) * tiles * 4);
+    s->chunk_hist = c.take(uint64_t(std::max<int64_t>((n + 2047) / 2048, (px + 2047) / 2048) + 1) * 4);
+    s->chunk_mat = c.take(uint64_t((n + 255) / 256 + 1) * tiles * 4);   // path B count/base matrix
+    s->srect = c.take(uint64_t(n) * 8);
+    s->tile_tot = c.take(uint64_t(tiles) * 4 * 2);
 }
 
 static bool ws_ok(const gs_ws* ws) { return ws && state(ws)->magic == kMagic; }
@@ -258,7 +260,7 @@ gs_status gs_ws_get_view(const gs_ws* ws, gs_ws_view* out) {
     out->radius = at<int32_t>(s, s->radius);
     out->tiles = at<uint32_t>(s, s->tiles);
     out->offsets = at<uint32_t>(s, s->offsets);
-    out->keys = s->sorted_in_1 ? at<uint64_t>(s, s->keys1) : at<uint64_t>(s, s->keys0);
+    out->keys = !s->keys_valid ? nullptr : s->sorted_in_1 ? at<uint64_t>(s, s->keys1) : at<uint64_t>(s, s->keys0);
     out->vals = s->sorted_in_1 ? at<uint32_t>(s, s->vals1) : at<uint32_t>(s, s->vals0);
     out->ranges = at<uint32_t>(s, s->ranges);
     out->t_final = at<float>(s, s->t_final);

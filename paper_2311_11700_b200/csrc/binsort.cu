@@ -218,6 +218,7 @@ gs_status run_bin_sort_keys(WsState* s, int64_t* n_keys, uint32_t flags, cudaStr
                                                  &misc->n_keys, s->key_cap, &misc->error_flag,
                                                  at<uint64_t>(s, s->keys0), at<uint32_t>(s, s->vals0));
     }
+    s->keys_valid = 1;
     if (flags & GS_FLAG_BINSORT_EMIT_ONLY) {
         s->sorted_in_1 = 0;
         return check_launch(s, "bin_sort_keys(emit only)");

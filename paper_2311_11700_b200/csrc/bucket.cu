@@ -1,8 +1,265 @@
-// gs_bin_sort path B placeholder: falls back to path A until the bucketed binning lands.
+// gs_bin_sort, path B (default): depth presort + ordered tile bucketing.
+//
+// Output-identical to path A (the stable sort of the index-order (tile|depth) keys, O2)
+// without materialising or sorting the K keys:
+//   B1  prep:       sort key = depth bits for on-screen Gaussians, 0xFFFFFFFF otherwise; value = i
+//   B2  depth sort: onesweep LSD radix sort of the n (u32, u32) pairs (stable: ties by index)
+//   B3  chunk count: the depth-ordered Gaussians are cut into chunks of 256; per chunk, a 2-D
+//                   difference array over the tile grid in shared memory gives count[c][t]
+//   B4  tile scan:  per-tile totals, one exclusive scan over tiles (ranges, K), then per-tile
+//                   exclusive scans over chunks -> base[c][t]
+//   B5  emission:   block = (chunk, 128-tile group); the chunk's Gaussians touching the group are
+//                   compacted in depth order; thread = tile walks them and writes the Gaussian
+//                   index at base[c][t] + running count (4 B per key, each tile's run sequential)
+// Per tile, entries come out in chunk order and in depth order within a chunk, i.e. ordered by
+// (depth bits, index): exactly the per-tile lists of path A (checked bit-exact in the tests).
+// HBM traffic is ~4 B per key (+ per-Gaussian and per-chunk terms) instead of ~150 B per key.
+#include <cub/block/block_scan.cuh>
+
+#include <algorithm>
+
 #include "gs_internal.cuh"
+#include "onesweep.cuh"
 
 namespace gs {
-gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t st) {
-    return run_bin_sort_keys(s, n_keys, flags | GS_FLAG_BINSORT_KEYS, st);
+
+constexpr int kChunk = 256;      // Gaussians per chunk (depth order)
+constexpr int kGroup = 128;      // tiles per emission block
+
+gs_status chained_scan(WsState* s, const uint32_t* in, uint32_t* out, int64_t n, unsigned long long* total,
+                       cudaStream_t st, int64_t cap, unsigned long long* total_eff);
+gs_status resolve_keys(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t st, int64_t* Kgrid);
+
+// B1 ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) prep_depth_kernel(int64_t n, const uint32_t* __restrict__ tiles,
+                                                         const uint32_t* __restrict__ dkey, uint32_t* __restrict__ k,
+                                                         uint32_t* __restrict__ v, unsigned int* n_on,
+                                                         unsigned long long* n_items) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    bool on = false;
+    if (i < n) {
+        on = tiles[i] > 0;
+        k[i] = on ? dkey[i] : 0xffffffffu;
+        v[i] = uint32_t(i);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, on);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(n_on, unsigned(__popc(m)));
+    if (i == 0) *n_items = (unsigned long long)n;
 }
+
+// B3 ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kChunk) chunk_count_kernel(const uint32_t* __restrict__ svals,
+                                                             const short4* __restrict__ rect,
+                                                             const unsigned int* __restrict__ n_on, int GX, int GY,
+                                                             uint32_t* __restrict__ cmat, short4* __restrict__ srect) {
+    extern __shared__ int diff[];   // (GY + 1) x (GX + 1)
+    const int c = blockIdx.x;
+    const uint32_t Von = *n_on;
+    const uint32_t base = uint32_t(c) * kChunk;
+    if (base >= Von) return;
+    const int W1 = GX + 1, cells = (GY + 1) * W1, T = GX * GY;
+    for (int i = threadIdx.x; i < cells; i += blockDim.x) diff[i] = 0;
+    __syncthreads();
+    const uint32_t s = base + threadIdx.x;
+    if (s < Von) {
+        const short4 r = rect[svals[s]];
+        srect[s] = r;
+        atomicAdd(&diff[r.z * W1 + r.x], 1);
+        atomicAdd(&diff[r.z * W1 + r.y], -1);
+        atomicAdd(&diff[r.w * W1 + r.x], -1);
+        atomicAdd(&diff[r.w * W1 + r.y], 1);
+    }
+    __syncthreads();
+    for (int y = threadIdx.x; y < GY; y += blockDim.x) {   // prefix along x
+        int run = 0;
+        for (int x = 0; x < GX; ++x) {
+            run += diff[y * W1 + x];
+            diff[y * W1 + x] = run;
+        }
+    }
+    __syncthreads();
+    uint32_t* row = cmat + size_t(c) * T;
+    for (int x = threadIdx.x; x < GX; x += blockDim.x) {   // prefix along y, write counts
+        int run = 0;
+        for (int y = 0; y < GY; ++y) {
+            run += diff[y * W1 + x];
+            row[y * GX + x] = uint32_t(run);
+        }
+    }
+}
+
+// B4 ---------------------------------------------------------------------------------------
+__global__ void tile_total_kernel(const uint32_t* __restrict__ cmat, const unsigned int* __restrict__ n_on, int T,
+                                  uint32_t* __restrict__ tot) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    const int nch = int((*n_on + kChunk - 1) / kChunk);
+    uint32_t sum = 0;
+    for (int c = 0; c < nch; ++c) sum += cmat[size_t(c) * T + t];
+    tot[t] = sum;
+}
+
+__global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restrict__ tot, int T,
+                                                         uint32_t* __restrict__ tstart, uint2* __restrict__ ranges,
+                                                         unsigned long long* n_keys, unsigned long long* n_keys_eff,
+                                                         int64_t key_cap, unsigned int* error_flag) {
+    using BS = cub::BlockScan<unsigned long long, 1024>;
+    __shared__ typename BS::TempStorage tmp;
+    __shared__ unsigned long long carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int b = 0; b < T; b += 1024) {
+        const int t = b + threadIdx.x;
+        const unsigned long long v = t < T ? tot[t] : 0ull;
+        unsigned long long ex, agg;
+        BS(tmp).ExclusiveSum(v, ex, agg);
+        const unsigned long long st = carry + ex;
+        if (t < T) {
+            tstart[t] = uint32_t(st);
+            ranges[t] = v ? make_uint2(uint32_t(st), uint32_t(st + v)) : make_uint2(0u, 0u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) carry += agg;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *n_keys = carry;
+        const bool over = carry > (unsigned long long)key_cap;
+        *n_keys_eff = over ? 0ull : carry;
+        if (over) atomicOr(error_flag, 1u);
+    }
+}
+
+__global__ void chunk_base_kernel(uint32_t* __restrict__ cmat, const uint32_t* __restrict__ tstart,
+                                  const unsigned int* __restrict__ n_on, int T) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    const int nch = int((*n_on + kChunk - 1) / kChunk);
+    uint32_t run = tstart[t];
+    for (int c = 0; c < nch; ++c) {
+        uint32_t* p = cmat + size_t(c) * T + t;
+        const uint32_t v = *p;
+        *p = run;
+        run += v;
+    }
+}
+
+// B5 ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kGroup) bucket_emit_kernel(
+    const uint32_t* __restrict__ svals, const short4* __restrict__ srect, const uint32_t* __restrict__ cmat,
+    const unsigned int* __restrict__ n_on, const unsigned long long* __restrict__ n_keys_eff,
+    const unsigned long long* __restrict__ n_keys, int GX, int T, uint32_t* __restrict__ vals_out) {
+    using BS = cub::BlockScan<int, kGroup>;
+    __shared__ typename BS::TempStorage tmp;
+    __shared__ short4 l_rect[kChunk];
+    __shared__ uint32_t l_g[kChunk];
+    __shared__ int l_n;
+    if (*n_keys_eff != *n_keys) return;   // capacity overflow: emit nothing (error flag is set)
+    const int c = blockIdx.x;
+    const uint32_t Von = *n_on;
+    const uint32_t base = uint32_t(c) * kChunk;
+    if (base >= Von) return;
+    const int t0 = blockIdx.y * kGroup, t1 = min(T, t0 + kGroup);
+    const int ya = t0 / GX, yb = (t1 - 1) / GX;
+    const int xa = (ya == yb) ? t0 % GX : 0, xb = (ya == yb) ? (t1 - 1) % GX : GX - 1;
+    // ordered compaction of the chunk's Gaussians whose rect meets the group's bounding box
+    constexpr int kPer = kChunk / kGroup;
+    short4 r[kPer];
+    bool keep[kPer];
+    int cnt = 0;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const uint32_t s = base + threadIdx.x * kPer + q;
+        keep[q] = false;
+        if (s < Von) {
+            r[q] = srect[s];
+            keep[q] = r[q].z <= yb && r[q].w > ya && r[q].x <= xb && r[q].y > xa;
+        }
+        cnt += keep[q];
+    }
+    int off, total;
+    BS(tmp).ExclusiveSum(cnt, off, total);
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        if (keep[q]) {
+            l_rect[off] = r[q];
+            l_g[off] = svals[base + threadIdx.x * kPer + q];
+            ++off;
+        }
+    }
+    if (threadIdx.x == 0) l_n = total;
+    __syncthreads();
+    const int t = t0 + threadIdx.x;
+    if (t >= t1) return;
+    const int tx = t % GX, ty = t / GX;
+    uint32_t pos = cmat[size_t(c) * T + t];
+    const int L = l_n;
+    for (int k = 0; k < L; ++k) {
+        const short4 q = l_rect[k];
+        if (tx >= q.x && tx < q.y && ty >= q.z && ty < q.w) vals_out[pos++] = l_g[k];
+    }
+}
+
+// ------------------------------------------------------------------ host driver
+gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t st) {
+    Misc* misc = at<Misc>(s, s->misc);
+    const int GX = s->cam_gx, GY = s->cam_gy, T = GX * GY;
+    const int64_t n = s->n;
+    cudaMemsetAsync(misc, 0, offsetof(Misc, loss_acc), st);   // K, flags, tickets, counters
+    uint32_t* k0 = at<uint32_t>(s, s->dkey_sorted);
+    uint32_t* k1 = k0 + s->n_cap;
+    uint32_t* v0 = at<uint32_t>(s, s->dval_sorted);
+    uint32_t* v1 = v0 + s->n_cap;
+    if (n > 0) {
+        KTimer kt(s, KID_DEPTH_SORT, st);
+        prep_depth_kernel<<<int((n + 255) / 256), 256, 0, st>>>(n, at<uint32_t>(s, s->tiles), at<uint32_t>(s, s->depth_key),
+                                                                 k0, v0, &misc->n_onscreen, &misc->n_items);
+    }
+    int which = 0;
+    gs_status rc = onesweep_sort_pairs<uint32_t>(s, k0, v0, k1, v1, &misc->n_items, n, 32, st, &which);
+    if (rc != GS_OK) return rc;
+    const uint32_t* svals = which ? v1 : v0;
+    uint32_t* cmat = at<uint32_t>(s, s->chunk_mat);
+    short4* srect = at<short4>(s, s->srect);
+    uint32_t* tot = at<uint32_t>(s, s->tile_tot);
+    uint32_t* tstart = tot + s->GX * s->GY;
+    const int nch = int((n + kChunk - 1) / kChunk);
+    if (nch > 0) {
+        const size_t smem = size_t(GX + 1) * (GY + 1) * sizeof(int);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(chunk_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            attr = true;
+        }
+        KTimer kt(s, KID_CHUNK_HIST, st);
+        chunk_count_kernel<<<nch, kChunk, smem, st>>>(svals, at<short4>(s, s->rect), &misc->n_onscreen, GX, GY, cmat,
+                                                      srect);
+    }
+    {
+        KTimer kt(s, KID_CHUNK_SCAN, st);
+        tile_total_kernel<<<(T + 255) / 256, 256, 0, st>>>(cmat, &misc->n_onscreen, T, tot);
+    }
+    {
+        KTimer kt(s, KID_CHUNK_SCAN, st);
+        tile_scan_kernel<<<1, 1024, 0, st>>>(tot, T, tstart, at<uint2>(s, s->ranges), &misc->n_keys, &misc->n_keys_eff,
+                                             s->key_cap, &misc->error_flag);
+    }
+    {
+        KTimer kt(s, KID_CHUNK_SCAN, st);
+        chunk_base_kernel<<<(T + 255) / 256, 256, 0, st>>>(cmat, tstart, &misc->n_onscreen, T);
+    }
+    if (nch > 0) {
+        KTimer kt(s, KID_BUCKET_EMIT, st);
+        dim3 grid(unsigned(nch), unsigned((T + kGroup - 1) / kGroup));
+        bucket_emit_kernel<<<grid, kGroup, 0, st>>>(svals, srect, cmat, &misc->n_onscreen, &misc->n_keys_eff,
+                                                    &misc->n_keys, GX, T, at<uint32_t>(s, s->vals0));
+    }
+    s->sorted_in_1 = 0;
+    s->keys_valid = 0;
+    int64_t Kgrid = 0;
+    rc = resolve_keys(s, n_keys, flags, st, &Kgrid);   // host-sync mode: K readback + capacity status
+    if (rc != GS_OK) return rc;
+    return check_launch(s, "bin_sort_bucket");
+}
+
 }  // namespace gs

@@ -24,13 +24,13 @@ struct WsState {
     // carve
     Region rec, depth_key, rect, radius, tiles, offsets, sgrad, scan_state,
         keys0, keys1, vals0, vals1, ranges, t_final, n_last, examined, sort_hist, sort_look,
-        misc, scratch, scratch14, dkey_sorted, dval_sorted, chunk_hist;
+        misc, scratch, scratch14, dkey_sorted, dval_sorted, chunk_hist, chunk_mat, srect, tile_tot;
     // run state
     int64_t n;                     // Gaussians of the last gs_project
     int32_t cam_w, cam_h, cam_gx, cam_gy;   // image of the last gs_project
     uint64_t gen_project, gen_fwd; // generation counters (GS_ERR_STALE)
     int32_t sorted_in_1;           // final sorted keys/vals live in buffer 1
-    int32_t pad0;
+    int32_t keys_valid;            // path A materialised the 64-bit keys (view.keys valid)
     int64_t n_keys_host;           // K of the last host-synced gs_bin_sort (-1 unknown)
     int64_t launches;              // kernels launched (gs_ws_launch_count)
     int64_t max_parts;             // sort lookback partitions per pass
@@ -54,6 +54,9 @@ struct Misc {
     unsigned int error_flag;
     unsigned int scan_counter;
     unsigned int sort_counter[8];  // per-pass partition counters
+    unsigned int n_onscreen;       // path B: Gaussians with tiles > 0
+    unsigned int pad_b;
+    unsigned long long n_items;    // path B: items of the depth sort (= n)
     double loss_acc[4];            // |C-C*| sum, |D-D*| valid sum, valid count, spare
     double pose_acc[16];
     unsigned long long add_count;  // densify

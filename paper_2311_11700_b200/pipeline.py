@@ -97,6 +97,7 @@ class RenderPipeline:
                    examined=t(v.examined, npx, torch.int32).view(v.height, v.width),
                    n_keys_dev=t(v.n_keys_dev, 1, torch.int64), error_flag=t(v.error_flag, 1, torch.int32))
         if K is not None and K >= 0:
-            out["keys"] = t(v.keys, K, torch.int64)
+            if v.keys:   # path A only (path B never materialises the 64-bit keys)
+                out["keys"] = t(v.keys, K, torch.int64)
             out["vals"] = t(v.vals, K, torch.int32)
         return out
