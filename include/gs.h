@@ -173,7 +173,8 @@ gs_status gs_densify_prune(float* params, float* params_raw /*nullable*/, int64_
 
 /* Introspection for tests and benchmarks (host struct of device pointers into the workspace). */
 typedef struct {
-    const float* records;        /* [n][12]: mx, my, conic a, b | conic c, opacity, depth, pad | r, g, b, pad */
+    const float* records;        /* [n][12]: mx, my, -a/2, -b | -c/2, opacity, depth, pad | r, g, b, pad
+                                    (conic [[a, b], [b, c]] = Sigma'^-1, exactly scaled) */
     const uint32_t* depth_key;   /* [n] float bits of z^c */
     const int16_t* rect;         /* [n][4] xlo, xhi, ylo, yhi */
     const int32_t* radius;       /* [n] */

@@ -238,7 +238,11 @@ static void blend_pixel(int u, int v, const std::vector<Proj<R>>& pj, const std:
         if (replay_nlast >= 0 && int64_t(j) > replay_nlast) break;
         out.examined = j;
         const R dx = g.mx - fu, dy = g.my - fv;
-        const R power = R(-0.5) * ((g.ca * dx) * dx + (g.cc * dy) * dy) - (g.cb * dx) * dy;
+        // power = -1/2 (a dx^2 + 2 b dx dy + c dy^2), evaluated in fp32 as two fused multiply-adds on
+        // the exactly scaled coefficients A = -a/2, B = -b, C = -c/2 (reading R1: the
+        // order every fp32 evaluation of this decision value uses, oracle and kernel alike)
+        const R A2 = R(-0.5) * g.ca, B2 = -g.cb, C2 = R(-0.5) * g.cc;
+        const R power = std::fma(A2 * dx, dx, std::fma(C2 * dy, dy, (B2 * dx) * dy));
         if (power > R(0)) continue;
         const R G = exp_r<R>(power);
         const R o = params[10 * ld + i];

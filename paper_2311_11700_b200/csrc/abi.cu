@@ -67,7 +67,8 @@ static void carve(WsState* s, Carver& c) {
     s->chunk_hist = c.take(uint64_t(std::max<int64_t>((n + 2047) / 2048, (px + 2047) / 2048) + 1) * 4);
     s->chunk_mat = c.take(uint64_t((n + 255) / 256 + 1) * tiles * 4);   // path B count/base matrix
     s->srect = c.take(uint64_t(n) * 8);
-    s->tile_tot = c.take(uint64_t(tiles) * 4 * 2);
+    s->tile_tot = c.take(uint64_t(tiles) * 4 * 10);   // totals, starts, 8 segment sums
+    s->pose_part = c.take(uint64_t((n + 255) / 256 + 1) * 16 * 8);   // per-block pose partials
 }
 
 static bool ws_ok(const gs_ws* ws) { return ws && state(ws)->magic == kMagic; }
@@ -173,7 +174,8 @@ static gs_status backward_common(const float* params, int64_t n, int64_t ld, con
         cam->height != s->cam_h)
         return GS_ERR_STALE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    cudaMemsetAsync(s->dev + s->sgrad.off, 0, size_t(s->n_cap) * 4 * 10, st);
+    if (n > 0)   // screen-space gradient accumulators [10][n_cap]: clear the live n columns only
+        cudaMemset2DAsync(s->dev + s->sgrad.off, size_t(s->n_cap) * 4, 0, size_t(n) * 4, 10, st);
     launch_render_bwd_tiles(s, *cam, nullptr, dLdC, dLdD, st);
     launch_gaussian_bwd(s, params, n, ld, viewmat, *cam, grad, grad_pose, flags, st);
     return check_launch(s, "gs_render_bwd");

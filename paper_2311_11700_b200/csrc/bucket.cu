@@ -6,11 +6,12 @@
 //   B2  depth sort: onesweep LSD radix sort of the n (u32, u32) pairs (stable: ties by index)
 //   B3  chunk count: the depth-ordered Gaussians are cut into chunks of 256; per chunk, a 2-D
 //                   difference array over the tile grid in shared memory gives count[c][t]
-//   B4  tile scan:  per-tile totals, one exclusive scan over tiles (ranges, K), then per-tile
-//                   exclusive scans over chunks -> base[c][t]
+//   B4  tile scan:  per-tile totals (8 chunk segments per tile in flight), one exclusive scan over
+//                   tiles (ranges, K), then per-tile exclusive scans over chunks -> base[c][t]
 //   B5  emission:   block = (chunk, 128-tile group); the chunk's Gaussians touching the group are
-//                   compacted in depth order; thread = tile walks them and writes the Gaussian
-//                   index at base[c][t] + running count (4 B per key, each tile's run sequential)
+//                   compacted in depth order; a warp takes one tile at a time, its lanes test 32
+//                   Gaussians, and a ballot/popc prefix places the hits at base[c][t] + rank
+//                   (coalesced 4-B stores, depth order preserved)
 // Per tile, entries come out in chunk order and in depth order within a chunk, i.e. ordered by
 // (depth bits, index): exactly the per-tile lists of path A (checked bit-exact in the tests).
 // HBM traffic is ~4 B per key (+ per-Gaussian and per-chunk terms) instead of ~150 B per key.
@@ -89,14 +90,39 @@ __global__ void __launch_bounds__(kChunk) chunk_count_kernel(const uint32_t* __r
 }
 
 // B4 ---------------------------------------------------------------------------------------
-__global__ void tile_total_kernel(const uint32_t* __restrict__ cmat, const unsigned int* __restrict__ n_on, int T,
-                                  uint32_t* __restrict__ tot) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= T) return;
+// Per-tile column sums over the chunks: block = 32 tiles (lanes) x 8 chunk segments (warps), so
+// 8 independent loads per thread are in flight and every warp load is one coalesced 128-B row.
+constexpr int kSegs = 8;
+
+__device__ __forceinline__ void seg_range(int nch, int seg, int& c0, int& c1) {
+    const int per = (nch + kSegs - 1) / kSegs;
+    c0 = min(nch, seg * per);
+    c1 = min(nch, c0 + per);
+}
+
+__global__ void __launch_bounds__(256) tile_total_kernel(const uint32_t* __restrict__ cmat,
+                                                         const unsigned int* __restrict__ n_on, int T,
+                                                         uint32_t* __restrict__ segsum, uint32_t* __restrict__ tot) {
+    __shared__ uint32_t sh[kSegs][32];
+    const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
+    const int t = blockIdx.x * 32 + lane;
     const int nch = int((*n_on + kChunk - 1) / kChunk);
+    int c0, c1;
+    seg_range(nch, seg, c0, c1);
     uint32_t sum = 0;
-    for (int c = 0; c < nch; ++c) sum += cmat[size_t(c) * T + t];
-    tot[t] = sum;
+    if (t < T) {
+#pragma unroll 8
+        for (int c = c0; c < c1; ++c) sum += __ldg(cmat + size_t(c) * T + t);
+        segsum[size_t(seg) * T + t] = sum;
+    }
+    sh[seg][lane] = sum;
+    __syncthreads();
+    if (seg == 0 && t < T) {
+        uint32_t s = 0;
+#pragma unroll
+        for (int q = 0; q < kSegs; ++q) s += sh[q][lane];
+        tot[t] = s;
+    }
 }
 
 __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restrict__ tot, int T,
@@ -130,26 +156,36 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
     }
 }
 
-__global__ void chunk_base_kernel(uint32_t* __restrict__ cmat, const uint32_t* __restrict__ tstart,
-                                  const unsigned int* __restrict__ n_on, int T) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) chunk_base_kernel(uint32_t* __restrict__ cmat,
+                                                         const uint32_t* __restrict__ tstart,
+                                                         const uint32_t* __restrict__ segsum,
+                                                         const unsigned int* __restrict__ n_on, int T) {
+    const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
+    const int t = blockIdx.x * 32 + lane;
     if (t >= T) return;
     const int nch = int((*n_on + kChunk - 1) / kChunk);
+    int c0, c1;
+    seg_range(nch, seg, c0, c1);
     uint32_t run = tstart[t];
-    for (int c = 0; c < nch; ++c) {
-        uint32_t* p = cmat + size_t(c) * T + t;
-        const uint32_t v = *p;
-        *p = run;
-        run += v;
+    for (int q = 0; q < seg; ++q) run += segsum[size_t(q) * T + t];
+    for (int cb = c0; cb < c1; cb += 8) {   // 8 independent loads in flight, then 8 stores
+        uint32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = (cb + u < c1) ? cmat[size_t(cb + u) * T + t] : 0u;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (cb + u < c1) cmat[size_t(cb + u) * T + t] = run;
+            run += v[u];
+        }
     }
 }
 
 // B5 ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kGroup) bucket_emit_kernel(
+__global__ void __launch_bounds__(256) bucket_emit_kernel(
     const uint32_t* __restrict__ svals, const short4* __restrict__ srect, const uint32_t* __restrict__ cmat,
     const unsigned int* __restrict__ n_on, const unsigned long long* __restrict__ n_keys_eff,
     const unsigned long long* __restrict__ n_keys, int GX, int T, uint32_t* __restrict__ vals_out) {
-    using BS = cub::BlockScan<int, kGroup>;
+    using BS = cub::BlockScan<int, 256>;
     __shared__ typename BS::TempStorage tmp;
     __shared__ short4 l_rect[kChunk];
     __shared__ uint32_t l_g[kChunk];
@@ -163,40 +199,38 @@ __global__ void __launch_bounds__(kGroup) bucket_emit_kernel(
     const int ya = t0 / GX, yb = (t1 - 1) / GX;
     const int xa = (ya == yb) ? t0 % GX : 0, xb = (ya == yb) ? (t1 - 1) % GX : GX - 1;
     // ordered compaction of the chunk's Gaussians whose rect meets the group's bounding box
-    constexpr int kPer = kChunk / kGroup;
-    short4 r[kPer];
-    bool keep[kPer];
-    int cnt = 0;
-#pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-        const uint32_t s = base + threadIdx.x * kPer + q;
-        keep[q] = false;
-        if (s < Von) {
-            r[q] = srect[s];
-            keep[q] = r[q].z <= yb && r[q].w > ya && r[q].x <= xb && r[q].y > xa;
-        }
-        cnt += keep[q];
+    const uint32_t s = base + threadIdx.x;   // kChunk == blockDim.x
+    short4 r = make_short4(0, 0, 0, 0);
+    int keep = 0;
+    if (s < Von) {
+        r = srect[s];
+        keep = r.z <= yb && r.w > ya && r.x <= xb && r.y > xa;
     }
     int off, total;
-    BS(tmp).ExclusiveSum(cnt, off, total);
-#pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-        if (keep[q]) {
-            l_rect[off] = r[q];
-            l_g[off] = svals[base + threadIdx.x * kPer + q];
-            ++off;
-        }
+    BS(tmp).ExclusiveSum(keep, off, total);
+    if (keep) {
+        l_rect[off] = r;
+        l_g[off] = svals[s];
     }
     if (threadIdx.x == 0) l_n = total;
     __syncthreads();
-    const int t = t0 + threadIdx.x;
-    if (t >= t1) return;
-    const int tx = t % GX, ty = t / GX;
-    uint32_t pos = cmat[size_t(c) * T + t];
     const int L = l_n;
-    for (int k = 0; k < L; ++k) {
-        const short4 q = l_rect[k];
-        if (tx >= q.x && tx < q.y && ty >= q.z && ty < q.w) vals_out[pos++] = l_g[k];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    for (int t = t0 + warp; t < t1; t += 8) {
+        const int tx = t % GX, ty = t / GX;
+        uint32_t pos = cmat[size_t(c) * T + t];
+        for (int k0 = 0; k0 < L; k0 += 32) {
+            const int k = k0 + lane;
+            bool hit = false;
+            if (k < L) {
+                const short4 q = l_rect[k];
+                hit = tx >= q.x && tx < q.y && ty >= q.z && ty < q.w;
+            }
+            const uint32_t m = __ballot_sync(0xffffffffu, hit);
+            if (hit) vals_out[pos + __popc(m & lt)] = l_g[k];
+            pos += __popc(m);
+        }
     }
 }
 
@@ -223,6 +257,7 @@ gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaS
     short4* srect = at<short4>(s, s->srect);
     uint32_t* tot = at<uint32_t>(s, s->tile_tot);
     uint32_t* tstart = tot + s->GX * s->GY;
+    uint32_t* segsum = tstart + s->GX * s->GY;   // [kSegs][T]
     const int nch = int((n + kChunk - 1) / kChunk);
     if (nch > 0) {
         const size_t smem = size_t(GX + 1) * (GY + 1) * sizeof(int);
@@ -237,7 +272,7 @@ gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaS
     }
     {
         KTimer kt(s, KID_CHUNK_SCAN, st);
-        tile_total_kernel<<<(T + 255) / 256, 256, 0, st>>>(cmat, &misc->n_onscreen, T, tot);
+        tile_total_kernel<<<(T + 31) / 32, 256, 0, st>>>(cmat, &misc->n_onscreen, T, segsum, tot);
     }
     {
         KTimer kt(s, KID_CHUNK_SCAN, st);
@@ -246,12 +281,12 @@ gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaS
     }
     {
         KTimer kt(s, KID_CHUNK_SCAN, st);
-        chunk_base_kernel<<<(T + 255) / 256, 256, 0, st>>>(cmat, tstart, &misc->n_onscreen, T);
+        chunk_base_kernel<<<(T + 31) / 32, 256, 0, st>>>(cmat, tstart, segsum, &misc->n_onscreen, T);
     }
     if (nch > 0) {
         KTimer kt(s, KID_BUCKET_EMIT, st);
         dim3 grid(unsigned(nch), unsigned((T + kGroup - 1) / kGroup));
-        bucket_emit_kernel<<<grid, kGroup, 0, st>>>(svals, srect, cmat, &misc->n_onscreen, &misc->n_keys_eff,
+        bucket_emit_kernel<<<grid, 256, 0, st>>>(svals, srect, cmat, &misc->n_onscreen, &misc->n_keys_eff,
                                                     &misc->n_keys, GX, T, at<uint32_t>(s, s->vals0));
     }
     s->sorted_in_1 = 0;

@@ -24,7 +24,7 @@ struct WsState {
     // carve
     Region rec, depth_key, rect, radius, tiles, offsets, sgrad, scan_state,
         keys0, keys1, vals0, vals1, ranges, t_final, n_last, examined, sort_hist, sort_look,
-        misc, scratch, scratch14, dkey_sorted, dval_sorted, chunk_hist, chunk_mat, srect, tile_tot;
+        misc, scratch, scratch14, dkey_sorted, dval_sorted, chunk_hist, chunk_mat, srect, tile_tot, pose_part;
     // run state
     int64_t n;                     // Gaussians of the last gs_project
     int32_t cam_w, cam_h, cam_gx, cam_gy;   // image of the last gs_project
@@ -125,24 +125,21 @@ gs_status run_densify(WsState* s, float* params, float* raw, int64_t* n_dev, int
 // ------------------------------------------------------------------ device helpers
 __device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
 
-// alpha of Gaussian record (r0 = {mx, my, a, b}, r1 = {c, o, d, -}) at pixel (px, py).
-// Shared by the forward and both backward kernels so every decision is bit-identical between
-// them. Written with explicit round-to-nearest intrinsics so no contraction choice of the
-// compiler can differ between call sites. Returns alpha (0 when skipped) and G, and whether the
-// 0.99 clamp is active.
+// Projected record (48 B): r0 = {mx, my, A, B}, r1 = {C, o, depth, -}, r2 = {r, g, b, -} with the
+// exactly scaled conic A = -a/2, B = -b, C = -c/2 (conic = Sigma'^-1 = [[a, b], [b, c]]).
+// alpha at pixel (px, py). Shared by the forward and both backward kernels so every decision is
+// bit-identical between them, and written with explicit round-to-nearest intrinsics in the
+// oracle's fp32 order (reading R1): power = fma(A dx, dx, fma(C dy, dy, (B dx) dy)).
+// For elongated conics the terms cancel, so any other order would move power by many ulps and
+// flip alpha-vs-1/255 decisions. Returns alpha (0 when skipped), G and the 0.99-clamp flag.
 struct AlphaEval { float alpha, G, dx, dy; bool clamped; };
 
 __device__ __forceinline__ AlphaEval eval_alpha(float4 r0, float4 r1, float px, float py) {
     AlphaEval e;
     e.dx = __fsub_rn(r0.x, px);
     e.dy = __fsub_rn(r0.y, py);
-    // power = -0.5 ((a dx) dx + (c dy) dy) - (b dx) dy, each operation rounded separately in the
-    // oracle's order (O3): for elongated conics the terms cancel, and any other
-    // evaluation order would move power by many ulps and flip alpha-vs-1/255 decisions.
-    const float t1 = __fmul_rn(__fmul_rn(r0.z, e.dx), e.dx);
-    const float t2 = __fmul_rn(__fmul_rn(r1.x, e.dy), e.dy);
-    const float t3 = __fmul_rn(__fmul_rn(r0.w, e.dx), e.dy);
-    const float power = __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(t1, t2)), t3);
+    const float inner = __fmaf_rn(__fmul_rn(r1.x, e.dy), e.dy, __fmul_rn(__fmul_rn(r0.w, e.dx), e.dy));
+    const float power = __fmaf_rn(__fmul_rn(r0.z, e.dx), e.dx, inner);
     // G = exp(power) via ex2.approx (MUFU): power * log2(e)
     float G;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(G) : "f"(__fmul_rn(power, 1.4426950408889634f)));

@@ -110,8 +110,9 @@ __global__ void __launch_bounds__(256) project_kernel(
             const int yhi = clamp_tile(floorf(((my + r) + 15.f) / 16.f), GY);
             rc = make_short4(short(xlo), short(xhi), short(ylo), short(yhi));
             tiles = uint32_t(max(0, xhi - xlo)) * uint32_t(max(0, yhi - ylo));
-            r0 = make_float4(mx, my, ca, cb);
-            r1 = make_float4(cc, p[10], zc, 0.f);
+            // exactly scaled conic for the blend: A = -a/2, B = -b, C = -c/2 (gs_internal.cuh)
+            r0 = make_float4(mx, my, -0.5f * ca, -cb);
+            r1 = make_float4(-0.5f * cc, p[10], zc, 0.f);
             r2 = make_float4(p[11], p[12], p[13], 0.f);
         } else {
             radius = 0;

@@ -140,6 +140,115 @@ __global__ void __launch_bounds__(kTilePx) render_fwd_kernel(
     }
 }
 
+// Fast forward: 128 threads per tile, two pixels per thread (rows ly and ly + 8) so the record
+// loads, the x-terms of power and the loop overhead are shared. Bit-identical decisions and
+// results to render_fwd_kernel (same per-pixel operation sequence as eval_alpha).
+struct PixState {
+    float T, Cr, Cg, Cb, D;
+    uint32_t nl, exam;
+    bool done;
+};
+
+__device__ __forceinline__ void blend_step(PixState& p, float power, float4 r1, const float4* r2p, uint32_t j) {
+    float G;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(G) : "f"(__fmul_rn(power, 1.4426950408889634f)));
+    float a = fminf(0.99f, __fmul_rn(r1.y, G));
+    if (power > 0.f || a < (1.0f / 255.0f)) return;
+    const float Tn = __fmul_rn(p.T, __fsub_rn(1.f, a));
+    if (Tn < 1e-4f) {
+        p.done = true;
+        p.exam = j;
+        return;
+    }
+    const float4 r2 = *r2p;
+    const float w = __fmul_rn(a, p.T);
+    p.Cr = fmaf(w, r2.x, p.Cr);
+    p.Cg = fmaf(w, r2.y, p.Cg);
+    p.Cb = fmaf(w, r2.z, p.Cb);
+    p.D = fmaf(w, r1.z, p.D);
+    p.T = Tn;
+    p.nl = j;
+}
+
+constexpr int kFwd2Batch = kTilePx / 2;   // one staged record per thread
+
+__global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
+    const float4* __restrict__ rec, const uint32_t* __restrict__ vals, const uint2* __restrict__ ranges, int W, int H,
+    int GX, float bgr, float bgg, float bgb, float* __restrict__ color, float* __restrict__ depth,
+    float* __restrict__ alpha, float* __restrict__ t_final, uint32_t* __restrict__ n_last,
+    uint32_t* __restrict__ examined) {
+    __shared__ float4 s_rec[2][kFwd2Batch][3];
+    const int tile = blockIdx.x;
+    const int tx = tile % GX, ty = tile / GX;
+    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;   // ly in [0, 8)
+    const int px = tx * kTile + lx, pyA = ty * kTile + ly, pyB = pyA + 8;
+    const bool inA = px < W && pyA < H, inB = px < W && pyB < H;
+    const float fpx = float(px), fyA = float(pyA), fyB = float(pyB);
+    const uint2 rg = ranges[tile];
+    const uint32_t start = rg.x, len = rg.y - rg.x;
+    const int nbatch = int((len + kFwd2Batch - 1) / kFwd2Batch);
+    PixState A{1.f, 0.f, 0.f, 0.f, 0.f, 0u, len, !inA}, B{1.f, 0.f, 0.f, 0.f, 0.f, 0u, len, !inB};
+
+    auto stage = [&](int b) {
+        const int slot = threadIdx.x;
+        const uint32_t j = uint32_t(b) * kFwd2Batch + slot;
+        if (j < len) {
+            const uint32_t g = vals[start + j];
+            float4* dst = s_rec[b & 1][slot];
+            const float4* src = rec + 3 * size_t(g);
+            cp_async16(dst + 0, src + 0);
+            cp_async16(dst + 1, src + 1);
+            cp_async16(dst + 2, src + 2);
+        }
+        cp_async_commit();
+    };
+    if (nbatch > 0) stage(0);
+    for (int b = 0; b < nbatch; ++b) {
+        if (b + 1 < nbatch) {
+            stage(b + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const int cnt = min(kFwd2Batch, int(len) - b * kFwd2Batch);
+        const float4(*buf)[3] = s_rec[b & 1];
+        for (int k = 0; k < cnt && !(A.done && B.done); ++k) {
+            const float4 r0 = buf[k][0], r1 = buf[k][1];
+            const uint32_t j = uint32_t(b * kFwd2Batch + k + 1);
+            // same operation sequence as eval_alpha, x-terms shared between the two pixels
+            const float dx = __fsub_rn(r0.x, fpx);
+            const float Adx = __fmul_rn(r0.z, dx), Bdx = __fmul_rn(r0.w, dx);
+            if (!A.done) {
+                const float dy = __fsub_rn(r0.y, fyA);
+                const float inner = __fmaf_rn(__fmul_rn(r1.x, dy), dy, __fmul_rn(Bdx, dy));
+                blend_step(A, __fmaf_rn(Adx, dx, inner), r1, &buf[k][2], j);
+            }
+            if (!B.done) {
+                const float dy = __fsub_rn(r0.y, fyB);
+                const float inner = __fmaf_rn(__fmul_rn(r1.x, dy), dy, __fmul_rn(Bdx, dy));
+                blend_step(B, __fmaf_rn(Adx, dx, inner), r1, &buf[k][2], j);
+            }
+        }
+        if (__syncthreads_and(A.done && B.done)) break;   // also orders buffer reuse
+    }
+    const size_t plane = size_t(W) * H;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const PixState& p = h ? B : A;
+        if (!(h ? inB : inA)) continue;
+        const size_t pix = size_t(h ? pyB : pyA) * W + px;
+        color[pix] = fmaf(p.T, bgr, p.Cr);
+        color[plane + pix] = fmaf(p.T, bgg, p.Cg);
+        color[2 * plane + pix] = fmaf(p.T, bgb, p.Cb);
+        depth[pix] = p.D;
+        alpha[pix] = 1.f - p.T;
+        t_final[pix] = p.T;
+        n_last[pix] = p.nl;
+        if (examined) examined[pix] = p.exam;
+    }
+}
+
 void launch_render_fwd(WsState* s, const gs_camera& cam, float* color, float* depth, float* alpha,
                        float* accum_weight, uint32_t flags, cudaStream_t st) {
     const int ntiles = s->cam_gx * s->cam_gy;
@@ -153,28 +262,29 @@ void launch_render_fwd(WsState* s, const gs_camera& cam, float* color, float* de
             cam.bg[1], cam.bg[2], color, depth, alpha, at<float>(s, s->t_final), at<uint32_t>(s, s->n_last), exam,
             accum_weight);
     } else {
-        render_fwd_kernel<false><<<ntiles, kTilePx, 0, st>>>(
+        render_fwd2_kernel<<<ntiles, kTilePx / 2, 0, st>>>(
             at<float4>(s, s->rec), sorted_vals, at<uint2>(s, s->ranges), cam.width, cam.height, s->cam_gx, cam.bg[0],
-            cam.bg[1], cam.bg[2], color, depth, alpha, at<float>(s, s->t_final), at<uint32_t>(s, s->n_last), exam,
-            nullptr);
+            cam.bg[1], cam.bg[2], color, depth, alpha, at<float>(s, s->t_final), at<uint32_t>(s, s->n_last), exam);
     }
 }
 
 // ------------------------------------------------------------------ backward, tile pass
-constexpr int kBwdBatch = 32;
+constexpr int kBB = 16;                 // Gaussians per backward batch
 constexpr int kWarps = kTilePx / 32;
+constexpr int kParts = kWarps * 2;      // phase-2 partial sets: (warp, row half)
 
 struct BwdSmem {
-    float4 rec[2][kBwdBatch][3];
-    float w[kTilePx][kBwdBatch + 1];    // alpha_i T_i     (padded: conflict-free row writes)
-    float go[kTilePx][kBwdBatch + 1];   // G dL/dalpha_i    (0 when clamped or skipped)
-    float4 dl[kTilePx];                 // dL/dC (r,g,b), dL/dD per pixel
-    float part[kWarps][10][kBwdBatch];  // per-warp partial sums
-    uint32_t idx[2][kBwdBatch];
+    float4 rec[2][kBB][3];
+    float w[kTilePx][kBB + 1];     // alpha_i T_i          (row stride 17: conflict-free both ways)
+    float go[kTilePx][kBB + 1];    // G dL/dalpha_i        (0 when clamped or skipped)
+    float4 dl[kTilePx];            // dL/dC (r,g,b), dL/dD per pixel
+    float part[kParts][10][kBB];   // per (warp, half) pixel moments
+    float red[10][kBB];            // combined moments
+    uint32_t idx[2][kBB];
     uint32_t max_nl;
 };
 
-__global__ void __launch_bounds__(kTilePx, 2) render_bwd_kernel(
+__global__ void __launch_bounds__(kTilePx, 4) render_bwd_kernel(
     const float4* __restrict__ rec, const uint32_t* __restrict__ vals, const uint2* __restrict__ ranges, int W, int H,
     int GX, const float* __restrict__ t_final, float bgr, float bgg, float bgb, const uint32_t* __restrict__ n_last,
     const float* __restrict__ dLdC, const float* __restrict__ dLdD, float* __restrict__ sgrad, int64_t sld) {
@@ -206,12 +316,12 @@ __global__ void __launch_bounds__(kTilePx, 2) render_bwd_kernel(
     if (nl) atomicMax(&sm.max_nl, nl);
     __syncthreads();
     const uint32_t len = sm.max_nl;
-    const int nbatch = int((len + kBwdBatch - 1) / kBwdBatch);
+    const int nbatch = int((len + kBB - 1) / kBB);
 
-    // batch bb holds list positions [bb*32, bb*32+32); batches are visited back to front
+    // batch bb holds list positions [bb*16, bb*16+16); batches are visited back to front
     auto stage = [&](int bb, int slot) {
-        if (tid < kBwdBatch) {
-            const uint32_t j = uint32_t(bb) * kBwdBatch + tid;
+        if (tid < kBB) {
+            const uint32_t j = uint32_t(bb) * kBB + tid;
             if (j < len) {
                 const uint32_t g = vals[start + j];
                 sm.idx[slot][tid] = g;
@@ -225,6 +335,8 @@ __global__ void __launch_bounds__(kTilePx, 2) render_bwd_kernel(
         cp_async_commit();
     };
 
+    // phase-2 lane roles: Gaussian k2 of the batch, pixel row ly2 = 2 warp + half
+    const int k2 = lane & (kBB - 1), half = lane >> 4, ly2 = 2 * warp + half;
     float S = 0.f;   // sum_{k>i} alpha_k T_k e_k  (suffix sum, accumulated from the back)
     if (nbatch > 0) stage(nbatch - 1, 0);
     for (int it = 0; it < nbatch; ++it) {
@@ -237,14 +349,14 @@ __global__ void __launch_bounds__(kTilePx, 2) render_bwd_kernel(
         }
         __syncthreads();
         const int buf = it & 1;
-        const int cnt = min(kBwdBatch, int(len) - bb * kBwdBatch);
+        const int cnt = min(kBB, int(len) - bb * kBB);
         // ---- phase 1: thread = pixel, back to front over the batch (3DGS-style recurrence):
         //      T_i = T_{i+1} / (1 - alpha_i);  dL/dalpha_i = T_i e_i - (S_i + T_f bg.dL/dC) / (1 - alpha_i)
+        const uint32_t base_pos = uint32_t(bb * kBB);
 #pragma unroll 4
-        for (int k = kBwdBatch - 1; k >= 0; --k) {
+        for (int k = kBB - 1; k >= 0; --k) {
             float w = 0.f, go = 0.f;
-            const uint32_t jpos = uint32_t(bb * kBwdBatch + k + 1);
-            if (k < cnt && jpos <= nl) {
+            if (k < cnt && base_pos + k + 1 <= nl) {
                 const float4 r0 = sm.rec[buf][k][0], r1 = sm.rec[buf][k][1];
                 const AlphaEval e = eval_alpha(r0, r1, fpx, fpy);
                 if (e.alpha != 0.f) {
@@ -262,69 +374,78 @@ __global__ void __launch_bounds__(kTilePx, 2) render_bwd_kernel(
             sm.go[tid][k] = go;
         }
         __syncthreads();
-        // ---- phase 2: warp = 32 pixels, lane = Gaussian; pixel moments
+        // ---- phase 2: lane = (Gaussian k2, row ly2); moments over the row's 16 pixels with
+        //      compile-time x coordinates; y moments follow from the lane's constant row
         {
-            float S0 = 0.f, Sx = 0.f, Sy = 0.f, Sxx = 0.f, Sxy = 0.f, Syy = 0.f, Sr = 0.f, Sg = 0.f, Sb = 0.f, Sd = 0.f;
-#pragma unroll 8
-            for (int p = 0; p < 32; ++p) {
-                const int q = warp * 32 + p;
-                const float fx = float(q & 15), fy = float(q >> 4);
-                const float g = sm.go[q][lane], w = sm.w[q][lane];
+            float S0 = 0.f, Sx = 0.f, Sxx = 0.f, Sr = 0.f, Sg = 0.f, Sb = 0.f, Sd = 0.f;
+#pragma unroll
+            for (int x = 0; x < 16; ++x) {
+                const int q = ly2 * 16 + x;
+                const float g = sm.go[q][k2], w = sm.w[q][k2];
                 const float4 d = sm.dl[q];
                 S0 += g;
-                Sx = fmaf(g, fx, Sx);
-                Sy = fmaf(g, fy, Sy);
-                Sxx = fmaf(g, fx * fx, Sxx);
-                Sxy = fmaf(g, fx * fy, Sxy);
-                Syy = fmaf(g, fy * fy, Syy);
+                Sx = fmaf(g, float(x), Sx);
+                Sxx = fmaf(g, float(x * x), Sxx);
                 Sr = fmaf(w, d.x, Sr);
                 Sg = fmaf(w, d.y, Sg);
                 Sb = fmaf(w, d.z, Sb);
                 Sd = fmaf(w, d.w, Sd);
             }
-            float* pp = &sm.part[warp][0][lane];
-            pp[0 * kBwdBatch] = S0; pp[1 * kBwdBatch] = Sx; pp[2 * kBwdBatch] = Sy; pp[3 * kBwdBatch] = Sxx;
-            pp[4 * kBwdBatch] = Sxy; pp[5 * kBwdBatch] = Syy; pp[6 * kBwdBatch] = Sr; pp[7 * kBwdBatch] = Sg;
-            pp[8 * kBwdBatch] = Sb; pp[9 * kBwdBatch] = Sd;
+            const float fy = float(ly2);
+            float* pp = &sm.part[warp * 2 + half][0][k2];
+            pp[0 * kBB] = S0;            // sum g
+            pp[1 * kBB] = Sx;            // sum g lx
+            pp[2 * kBB] = fy * S0;       // sum g ly
+            pp[3 * kBB] = Sxx;           // sum g lx^2
+            pp[4 * kBB] = fy * Sx;       // sum g lx ly
+            pp[5 * kBB] = fy * fy * S0;  // sum g ly^2
+            pp[6 * kBB] = Sr;
+            pp[7 * kBB] = Sg;
+            pp[8 * kBB] = Sb;
+            pp[9 * kBB] = Sd;
         }
         __syncthreads();
-        // ---- combine the 8 warps; convert moments to screen-space gradients; one atomic each
+        // ---- combine the 16 partial sets (160 threads: one (component, Gaussian) each)
+        if (tid < 10 * kBB) {
+            const int c = tid / kBB, k = tid % kBB;
+            float a = 0.f;
+#pragma unroll
+            for (int p = 0; p < kParts; ++p) a += sm.part[p][c][k];
+            sm.red[c][k] = a;
+        }
+        __syncthreads();
+        // ---- moments -> screen-space gradients; one atomic per (tile, Gaussian, component)
         if (tid < cnt) {
-            float Mo[10];   // pixel moments of this Gaussian over the tile
-#pragma unroll
-            for (int c = 0; c < 10; ++c) {
-                float a = 0.f;
-#pragma unroll
-                for (int w2 = 0; w2 < kWarps; ++w2) a += sm.part[w2][c][tid];
-                Mo[c] = a;
-            }
+            const float* Mo = &sm.red[0][tid];
+            const float M0 = Mo[0], Mx = Mo[kBB], My = Mo[2 * kBB], Mxx = Mo[3 * kBB], Mxy = Mo[4 * kBB],
+                        Myy = Mo[5 * kBB];
             const float4 r0 = sm.rec[buf][tid][0], r1 = sm.rec[buf][tid][1];
             const float o = r1.y;
             const float X = r0.x - float(tx * kTile), Y = r0.y - float(ty * kTile);
-            // sum g dx, sum g dy, sum g dx^2, sum g dx dy, sum g dy^2 with dx = X - lx, dy = Y - ly
-            const float gdx = X * Mo[0] - Mo[1];
-            const float gdy = Y * Mo[0] - Mo[2];
-            const float gdxx = X * X * Mo[0] - 2.f * X * Mo[1] + Mo[3];
-            const float gdxy = X * Y * Mo[0] - X * Mo[2] - Y * Mo[1] + Mo[4];
-            const float gdyy = Y * Y * Mo[0] - 2.f * Y * Mo[2] + Mo[5];
-            const float ca = r0.z, cb = r0.w, cc = r1.x;
+            // sums of g dx, g dy, g dx^2, g dx dy, g dy^2 with dx = X - lx, dy = Y - ly
+            const float gdx = X * M0 - Mx;
+            const float gdy = Y * M0 - My;
+            const float gdxx = X * X * M0 - 2.f * X * Mx + Mxx;
+            const float gdxy = X * Y * M0 - X * My - Y * Mx + Mxy;
+            const float gdyy = Y * Y * M0 - 2.f * Y * My + Myy;
+            const float A = r0.z, B = r0.w, C = r1.x;   // A = -a/2, B = -b, C = -c/2
             float out[10];
-            out[0] = -o * (ca * gdx + cb * gdy);   // mean2d x
-            out[1] = -o * (cb * gdx + cc * gdy);   // mean2d y
-            out[2] = -0.5f * o * gdxx;             // conic a
-            out[3] = -o * gdxy;                    // conic b
-            out[4] = -0.5f * o * gdyy;             // conic c
-            out[5] = Mo[0];                        // opacity
-            out[6] = Mo[6];
-            out[7] = Mo[7];
-            out[8] = Mo[8];                        // rgb
-            out[9] = Mo[9];                        // depth
+            out[0] = o * (2.f * A * gdx + B * gdy);   // mean2d x:  -o (a gdx + b gdy)
+            out[1] = o * (B * gdx + 2.f * C * gdy);   // mean2d y:  -o (b gdx + c gdy)
+            out[2] = -0.5f * o * gdxx;                // conic a
+            out[3] = -o * gdxy;                       // conic b
+            out[4] = -0.5f * o * gdyy;                // conic c
+            out[5] = M0;                              // opacity
+            out[6] = Mo[6 * kBB];
+            out[7] = Mo[7 * kBB];
+            out[8] = Mo[8 * kBB];                     // rgb
+            out[9] = Mo[9 * kBB];                     // depth
             const uint32_t g = sm.idx[buf][tid];
 #pragma unroll
             for (int c = 0; c < 10; ++c)
                 if (out[c] != 0.f) atomicAdd(sgrad + c * sld + g, out[c]);
         }
-        __syncthreads();   // protect sm.part / w / go / rec[buf] before the next batch
+        __syncthreads();   // protect sm.* before the next batch
     }
 }
 
@@ -353,7 +474,7 @@ constexpr int kPoseSums = 15;
 __global__ void __launch_bounds__(256) gaussian_bwd_kernel(
     const float* __restrict__ params, int64_t n, int64_t ld, const float* __restrict__ viewmat, gs_camera cam,
     const uint32_t* __restrict__ tiles, const float4* __restrict__ rec, const float* __restrict__ sgrad, int64_t sld,
-    float* __restrict__ grad, int cov_path, double* __restrict__ pose_acc) {
+    float* __restrict__ grad, int cov_path, double* __restrict__ pose_part) {
     __shared__ float V[12];
     if (threadIdx.x < 12) V[threadIdx.x] = viewmat[threadIdx.x];
     __syncthreads();
@@ -395,8 +516,8 @@ __global__ void __launch_bounds__(256) gaussian_bwd_kernel(
 #pragma unroll
             for (int k = 0; k < 3; ++k) E[a][k] = J[a][0] * W[0][k] + J[a][1] * W[1][k] + J[a][2] * W[2][k];
         // conic -> Sigma':  dSp = -Q Gbar Q
-        const float4 r0 = rec[3 * i], r1 = rec[3 * i + 1];
-        const float Q[2][2] = {{r0.z, r0.w}, {r0.w, r1.x}};
+        const float4 r0 = rec[3 * i], r1 = rec[3 * i + 1];   // scaled conic: A = -a/2, B = -b, C = -c/2
+        const float Q[2][2] = {{-2.f * r0.z, -r0.w}, {-r0.w, -2.f * r1.x}};
         const float Gb[2][2] = {{s[2], 0.5f * s[3]}, {0.5f * s[3], s[4]}};
         float QG[2][2], dSp[2][2];
 #pragma unroll
@@ -471,14 +592,15 @@ __global__ void __launch_bounds__(256) gaussian_bwd_kernel(
             grad[12 * ld + i] += s[7];
             grad[13 * ld + i] += s[8];
         }
-        if (pose_acc) {
-            const float* g = cov_path ? dX : dXm;
-            pose[0] = g[0];
-            pose[1] = g[1];
-            pose[2] = g[2];
-            pose[3] = y * g[2] - z * g[1];
-            pose[4] = z * g[0] - x * g[2];
-            pose[5] = x * g[1] - y * g[0];
+        if (pose_part) {
+            const float g0 = cov_path ? dX[0] : dXm[0], g1 = cov_path ? dX[1] : dXm[1],
+                        g2 = cov_path ? dX[2] : dXm[2];
+            pose[0] = g0;
+            pose[1] = g1;
+            pose[2] = g2;
+            pose[3] = y * g2 - z * g1;
+            pose[4] = z * g0 - x * g2;
+            pose[5] = x * g1 - y * g0;
             if (cov_path) {
 #pragma unroll
                 for (int a = 0; a < 3; ++a)
@@ -487,21 +609,41 @@ __global__ void __launch_bounds__(256) gaussian_bwd_kernel(
             }
         }
     }
-    if (pose_acc) {
-        using BR = cub::BlockReduce<double, 256>;
-        __shared__ typename BR::TempStorage tmp;
-#pragma unroll 1
+    if (pose_part) {   // per-block partial sums (fp64), reduced in a fixed order by pose_finalize_kernel
+        __shared__ double red[8][kPoseSums];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
         for (int k = 0; k < kPoseSums; ++k) {
-            const double v = BR(tmp).Sum(double(pose[k]));
-            if (threadIdx.x == 0 && v != 0.0) atomicAdd(pose_acc + k, v);
-            __syncthreads();
+            double v = double(pose[k]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) red[warp][k] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < kPoseSums) {   // component-major: pose_part[k][block]
+            double v = 0.0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
+            pose_part[size_t(threadIdx.x) * gridDim.x + blockIdx.x] = v;
         }
     }
 }
 
+// Fixed-order reduction of the per-block pose partials, then
 // twist = (rho, phi + (A12 - A21, A20 - A02, A01 - A10)),  A = W (sum dW_cov)^T
-__global__ void pose_finalize_kernel(const double* __restrict__ acc, const float* __restrict__ viewmat,
-                                     double* __restrict__ grad_pose) {
+__global__ void __launch_bounds__(512) pose_finalize_kernel(const double* __restrict__ part, int nblocks,
+                                                            const float* __restrict__ viewmat,
+                                                            double* __restrict__ grad_pose) {
+    __shared__ double acc[16];
+    const int lane = threadIdx.x & 31, k = threadIdx.x >> 5;   // warp k sums component k
+    if (k < kPoseSums) {
+        double v = 0.0;
+        for (int b = lane; b < nblocks; b += 32) v += part[size_t(k) * nblocks + b];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) acc[k] = v;
+    }
+    __syncthreads();
     if (threadIdx.x != 0) return;
     double W[3][3], A[3][3];
     for (int a = 0; a < 3; ++a)
@@ -520,19 +662,17 @@ __global__ void pose_finalize_kernel(const double* __restrict__ acc, const float
 void launch_gaussian_bwd(WsState* s, const float* params, int64_t n, int64_t ld, const float* viewmat,
                          const gs_camera& cam, float* grad_params, double* grad_pose, uint32_t flags, cudaStream_t st) {
     if (n == 0) return;
-    Misc* misc = at<Misc>(s, s->misc);
-    double* acc = grad_pose ? misc->pose_acc : nullptr;
-    if (acc) cudaMemsetAsync(misc->pose_acc, 0, sizeof(misc->pose_acc), st);
+    double* part = grad_pose ? at<double>(s, s->pose_part) : nullptr;
     const int blocks = int((n + 255) / 256);
     {
-    KTimer kt(s, KID_BWD_GAUSS, st);
-    gaussian_bwd_kernel<<<blocks, 256, 0, st>>>(params, n, ld, viewmat, cam, at<uint32_t>(s, s->tiles),
-                                                at<float4>(s, s->rec), at<float>(s, s->sgrad), s->n_cap, grad_params,
-                                                (flags & GS_FLAG_POSE_COV_PATH) ? 1 : 0, acc);
+        KTimer kt(s, KID_BWD_GAUSS, st);
+        gaussian_bwd_kernel<<<blocks, 256, 0, st>>>(params, n, ld, viewmat, cam, at<uint32_t>(s, s->tiles),
+                                                    at<float4>(s, s->rec), at<float>(s, s->sgrad), s->n_cap,
+                                                    grad_params, (flags & GS_FLAG_POSE_COV_PATH) ? 1 : 0, part);
     }
     if (grad_pose) {
         KTimer kt(s, KID_POSE_FIN, st);
-        pose_finalize_kernel<<<1, 32, 0, st>>>(acc, viewmat, grad_pose);
+        pose_finalize_kernel<<<1, 512, 0, st>>>(part, blocks, viewmat, grad_pose);
     }
 }
 

@@ -41,8 +41,9 @@ def test_project_bitexact(c):
     rec = a["records"].cpu().numpy()
     on = o["tiles"] > 0
     assert np.array_equal(rec[on, 0], o["mean2d"][0, on]) and np.array_equal(rec[on, 1], o["mean2d"][1, on])
-    assert np.array_equal(rec[on, 2], o["conic"][0, on]) and np.array_equal(rec[on, 3], o["conic"][1, on])
-    assert np.array_equal(rec[on, 4], o["conic"][2, on])
+    # record holds the exactly scaled conic (-a/2, -b, -c/2)
+    assert np.array_equal(-2 * rec[on, 2], o["conic"][0, on]) and np.array_equal(-rec[on, 3], o["conic"][1, on])
+    assert np.array_equal(-2 * rec[on, 4], o["conic"][2, on])
     assert np.array_equal(rec[on, 6], o["depth"][on])
 
 
