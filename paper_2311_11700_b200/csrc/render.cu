@@ -149,25 +149,25 @@ struct PixState {
     bool done;
 };
 
-__device__ __forceinline__ void blend_step(PixState& p, float power, float4 r1, const float4* r2p, uint32_t j) {
+// Branch-free blend step (predicated selects): a skipped, terminated or already-done pixel gets
+// w = 0, and fma(0, c, C) == C bitwise, so the result equals the branchy definition exactly.
+__device__ __forceinline__ void blend_step(PixState& p, float power, float4 r1, float4 r2, uint32_t j) {
     float G;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(G) : "f"(__fmul_rn(power, 1.4426950408889634f)));
-    float a = fminf(0.99f, __fmul_rn(r1.y, G));
-    if (power > 0.f || a < (1.0f / 255.0f)) return;
+    const float a = fminf(0.99f, __fmul_rn(r1.y, G));
+    const bool live = !p.done && !(power > 0.f) && a >= (1.0f / 255.0f);
     const float Tn = __fmul_rn(p.T, __fsub_rn(1.f, a));
-    if (Tn < 1e-4f) {
-        p.done = true;
-        p.exam = j;
-        return;
-    }
-    const float4 r2 = *r2p;
-    const float w = __fmul_rn(a, p.T);
+    const bool term = live && Tn < 1e-4f;
+    const bool blend = live && !(Tn < 1e-4f);
+    const float w = blend ? __fmul_rn(a, p.T) : 0.f;
     p.Cr = fmaf(w, r2.x, p.Cr);
     p.Cg = fmaf(w, r2.y, p.Cg);
     p.Cb = fmaf(w, r2.z, p.Cb);
     p.D = fmaf(w, r1.z, p.D);
-    p.T = Tn;
-    p.nl = j;
+    p.T = blend ? Tn : p.T;
+    p.nl = blend ? j : p.nl;
+    p.exam = term ? j : p.exam;
+    p.done = p.done || term;
 }
 
 constexpr int kFwd2Batch = kTilePx / 2;   // one staged record per thread
@@ -192,13 +192,18 @@ __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
     auto stage = [&](int b) {
         const int slot = threadIdx.x;
         const uint32_t j = uint32_t(b) * kFwd2Batch + slot;
+        float4* dst = s_rec[b & 1][slot];
         if (j < len) {
             const uint32_t g = vals[start + j];
-            float4* dst = s_rec[b & 1][slot];
             const float4* src = rec + 3 * size_t(g);
             cp_async16(dst + 0, src + 0);
             cp_async16(dst + 1, src + 1);
             cp_async16(dst + 2, src + 2);
+        } else {   // pad: opacity 0 -> alpha 0 -> skipped exactly (no blend, no termination)
+            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+            dst[0] = z;
+            dst[1] = z;
+            dst[2] = z;
         }
         cp_async_commit();
     };
@@ -213,21 +218,22 @@ __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
         __syncthreads();
         const int cnt = min(kFwd2Batch, int(len) - b * kFwd2Batch);
         const float4(*buf)[3] = s_rec[b & 1];
-        for (int k = 0; k < cnt && !(A.done && B.done); ++k) {
-            const float4 r0 = buf[k][0], r1 = buf[k][1];
-            const uint32_t j = uint32_t(b * kFwd2Batch + k + 1);
-            // same operation sequence as eval_alpha, x-terms shared between the two pixels
-            const float dx = __fsub_rn(r0.x, fpx);
-            const float Adx = __fmul_rn(r0.z, dx), Bdx = __fmul_rn(r0.w, dx);
-            if (!A.done) {
-                const float dy = __fsub_rn(r0.y, fyA);
-                const float inner = __fmaf_rn(__fmul_rn(r1.x, dy), dy, __fmul_rn(Bdx, dy));
-                blend_step(A, __fmaf_rn(Adx, dx, inner), r1, &buf[k][2], j);
-            }
-            if (!B.done) {
-                const float dy = __fsub_rn(r0.y, fyB);
-                const float inner = __fmaf_rn(__fmul_rn(r1.x, dy), dy, __fmul_rn(Bdx, dy));
-                blend_step(B, __fmaf_rn(Adx, dx, inner), r1, &buf[k][2], j);
+        constexpr int kU = 4;                   // Gaussians per early-exit check
+        for (int k0 = 0; k0 < cnt; k0 += kU) {  // slots past cnt are zero-opacity pads (< kFwd2Batch)
+            if (A.done && B.done) break;
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int k = k0 + u;
+                const float4 r0 = buf[k][0], r1 = buf[k][1], r2 = buf[k][2];
+                const uint32_t j = uint32_t(b * kFwd2Batch + k + 1);
+                // same operation sequence as eval_alpha, x-terms shared between the two pixels
+                const float dx = __fsub_rn(r0.x, fpx);
+                const float Adx = __fmul_rn(r0.z, dx), Bdx = __fmul_rn(r0.w, dx);
+                const float dyA = __fsub_rn(r0.y, fyA), dyB = __fsub_rn(r0.y, fyB);
+                const float inA = __fmaf_rn(__fmul_rn(r1.x, dyA), dyA, __fmul_rn(Bdx, dyA));
+                const float inB = __fmaf_rn(__fmul_rn(r1.x, dyB), dyB, __fmul_rn(Bdx, dyB));
+                blend_step(A, __fmaf_rn(Adx, dx, inA), r1, r2, j);
+                blend_step(B, __fmaf_rn(Adx, dx, inB), r1, r2, j);
             }
         }
         if (__syncthreads_and(A.done && B.done)) break;   // also orders buffer reuse
@@ -356,7 +362,7 @@ __global__ void __launch_bounds__(kTilePx, 4) render_bwd_kernel(
 #pragma unroll 4
         for (int k = kBB - 1; k >= 0; --k) {
             float w = 0.f, go = 0.f;
-            if (k < cnt && base_pos + k + 1 <= nl) {
+            if (k < cnt && base_pos + k + 1 <= nl) {   // pixels past their n_last skip the work
                 const float4 r0 = sm.rec[buf][k][0], r1 = sm.rec[buf][k][1];
                 const AlphaEval e = eval_alpha(r0, r1, fpx, fpy);
                 if (e.alpha != 0.f) {
