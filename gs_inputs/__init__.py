@@ -78,6 +78,37 @@ def gaussians(n: int, seed: int, lo=ROOM_LO, hi=ROOM_HI) -> np.ndarray:
     return out.astype(np.float32)
 
 
+def room_surface_gaussians(n: int, seed: int, lo=ROOM_LO, hi=ROOM_HI) -> np.ndarray:
+    """Seeded surface-like room (stands in for a Replica map, whose Gaussians sit on surfaces):
+    n flat Gaussians on the 6 faces of the room box (face chosen by area), in-plane log-scales
+    N(log 0.02, 0.3), normal scale 2 mm, axis-aligned (identity rotation), opacity sigmoid(N(2, 0.5)),
+    colour a smooth seeded texture of position. float32 SoA [14][n] (activated)."""
+    rng = np.random.default_rng(seed)
+    lo = np.asarray(lo, np.float64)
+    hi = np.asarray(hi, np.float64)
+    ext = hi - lo
+    faces = [(a, s) for a in range(3) for s in (0, 1)]   # normal axis, low/high side
+    area = np.array([np.prod(np.delete(ext, a)) for a, _ in faces])
+    f = rng.choice(len(faces), size=n, p=area / area.sum())
+    pos = lo + rng.uniform(size=(n, 3)) * ext
+    scale = np.exp(rng.normal(np.log(0.02), 0.3, size=(n, 3)))
+    for k, (a, s) in enumerate(faces):
+        sel = f == k
+        pos[sel, a] = hi[a] if s else lo[a]
+        scale[sel, a] = 0.002
+    logits = rng.normal(2.0, 0.5, size=n)
+    freq = rng.uniform(1.0, 4.0, size=(3, 3))
+    phase = rng.uniform(0, 2 * math.pi, size=3)
+    rgb = 0.5 + 0.45 * np.sin(pos @ freq.T + phase)
+    out = np.zeros((N_PARAM_ROWS, n), np.float64)
+    out[0:3] = pos.T
+    out[3:6] = scale.T
+    out[6] = 1.0
+    out[10] = 1.0 / (1.0 + np.exp(-logits))
+    out[11:14] = rgb.T
+    return out.astype(np.float32)
+
+
 def identity_view() -> np.ndarray:
     v = np.zeros((3, 4), np.float32)
     v[0, 0] = v[1, 1] = v[2, 2] = 1.0

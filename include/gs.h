@@ -150,8 +150,9 @@ gs_status gs_pose_step(float* viewmat, const double* grad_pose, float* m6, float
  *                    the inverse pose; init rgb = C*, opacity = init_opacity, quat (1,0,0,0),
  *                    scale = D* stride/(fx+fy) (reading C22). Appended at columns [n, n+added) of
  *                    params (and logit/log in params_raw, zero moments); n_dev updated; at most
- *                    max_add and capacity - n. If add_out != NULL the candidates are (also) written
- *                    to add_out[14][max_add] and *n_dev is NOT changed (multi-GPU gather mode).
+ *                    max_add and capacity - n. If add_out != NULL the candidates are instead written
+ *                    to add_out[14][max_add] (activated) and *n_dev RECEIVES their count (<= max_add)
+ *                    (multi-GPU gather mode; see gs_densify_append).
  *  GS_DENSIFY_PRUNE  drop Gaussians with opacity < min_opacity by stable compaction of params,
  *                    params_raw, adam_m, adam_v (any of the last three may be NULL); n_dev updated.
  *  GS_DENSIFY_SELECT Eq. 12 (reading C24): select_mask[i] = accum_weight[i] > sel_weight and
@@ -170,6 +171,15 @@ gs_status gs_densify_prune(float* params, float* params_raw /*nullable*/, int64_
                            const float* accum_weight, const float* viewmat, const gs_camera* cam /*(host)*/,
                            const gs_densify_cfg* cfg /*(host)*/, uint8_t* select_mask, float* add_out,
                            gs_ws* ws, void* stream);
+
+/* gs_densify_append — append gathered ADD candidates (multi-GPU mapping):
+ * cand[k][14][max_add] (activated, k < n_sets, in global keyframe order) with counts[k] (device
+ * int64) are appended in order k = 0, 1, ... at columns [n, n + sum counts) of params[14][ld]
+ * (raw copies: log-scale / logit-opacity; zero Adam moments), truncated at capacity; n_dev updated.
+ * Deterministic: every rank appending the same gathered sets produces identical parameters. */
+gs_status gs_densify_append(float* params, float* params_raw /*nullable*/, float* adam_m /*nullable*/,
+                            float* adam_v /*nullable*/, int64_t* n_dev, int64_t capacity, int64_t ld,
+                            const float* cand, const int64_t* counts, int32_t n_sets, int64_t max_add, void* stream);
 
 /* Introspection for tests and benchmarks (host struct of device pointers into the workspace). */
 typedef struct {

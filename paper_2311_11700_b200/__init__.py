@@ -79,6 +79,7 @@ _SIGS = {
     "gs_densify_prune": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P,
                                         ctypes.POINTER(gs_camera), ctypes.POINTER(gs_densify_cfg), _P, _P,
                                         ctypes.POINTER(gs_ws), _P]),
+    "gs_densify_append": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I64, _P, _P, _I32, _I64, _P]),
     "gs_ws_get_view": (ctypes.c_int, [ctypes.POINTER(gs_ws), ctypes.POINTER(gs_ws_view)]),
     "gs_ws_launch_count": (_I64, [ctypes.POINTER(gs_ws)]),
     "gs_ws_set_event_log": (ctypes.c_int, [ctypes.POINTER(gs_ws), _P, _P, _I32]),
@@ -269,6 +270,12 @@ def gs_densify_prune(params, params_raw, n_dev, capacity, ld, adam_m, adam_v, al
                                  _ptr(accum_weight), _ptr(viewmat), ctypes.byref(cam) if cam is not None else None,
                                  ctypes.byref(cfg), _ptr(select_mask), _ptr(add_out), ctypes.byref(ws.state),
                                  _stream(stream)), "gs_densify_prune")
+
+
+def gs_densify_append(params, params_raw, adam_m, adam_v, n_dev, capacity, ld, cand, counts, n_sets, max_add,
+                      stream=None):
+    _check(_lib.gs_densify_append(_ptr(params), _ptr(params_raw), _ptr(adam_m), _ptr(adam_v), _ptr(n_dev), capacity,
+                                  ld, _ptr(cand), _ptr(counts), n_sets, max_add, _stream(stream)), "gs_densify_append")
 
 
 from .pipeline import Frame, RenderPipeline  # noqa: E402  (convenience layer over the calls above)

@@ -252,6 +252,17 @@ gs_status gs_densify_prune(float* params, float* params_raw, int64_t* n_dev, int
                        static_cast<cudaStream_t>(stream));
 }
 
+gs_status gs_densify_append(float* params, float* params_raw, float* adam_m, float* adam_v, int64_t* n_dev,
+                            int64_t capacity, int64_t ld, const float* cand, const int64_t* counts, int32_t n_sets,
+                            int64_t max_add, void* stream) {
+    if (!params || !n_dev || capacity < 0 || ld < capacity || n_sets < 0 || max_add < 0 ||
+        (n_sets > 0 && (!cand || !counts)))
+        return GS_ERR_INVALID_ARG;
+    launch_append(params, params_raw, adam_m, adam_v, n_dev, capacity, ld, cand, counts, n_sets, max_add,
+                  static_cast<cudaStream_t>(stream));
+    return check_launch(nullptr, "gs_densify_append");
+}
+
 gs_status gs_ws_get_view(const gs_ws* ws, gs_ws_view* out) {
     if (!ws_ok(ws) || !out) return GS_ERR_INVALID_ARG;
     const WsState* s = state(ws);

@@ -117,6 +117,8 @@ void launch_adam(float* raw, float* act, const float* g, float* m, float* v, int
                  const float lr[14], int32_t step, float b1, float b2, float eps, cudaStream_t st);
 void launch_pose_step(float* viewmat, const double* gp, float* m6, float* v6, int32_t step, float lr_rho,
                       float lr_phi, cudaStream_t st);
+void launch_append(float* params, float* raw, float* m, float* v, int64_t* n_dev, int64_t capacity, int64_t ld,
+                   const float* cand, const int64_t* counts, int32_t n_sets, int64_t max_add, cudaStream_t st);
 gs_status run_densify(WsState* s, float* params, float* raw, int64_t* n_dev, int64_t capacity, int64_t ld,
                       float* m, float* v, const float* alpha, const float* depth, const float* trgb,
                       const float* tdepth, const float* accum, const float* viewmat, const gs_camera& cam,

@@ -277,6 +277,51 @@ struct AddEmit {
     }
 };
 
+__global__ void add_count_out_kernel(int64_t* n_dev, const unsigned long long* count, int64_t max_add) {
+    const int64_t a = int64_t(*count);
+    *n_dev = a < max_add ? a : max_add;
+}
+
+// Append gathered candidate sets in order (gs_densify_append). One thread per (set, candidate).
+__global__ void __launch_bounds__(256) append_kernel(float* __restrict__ params, float* __restrict__ raw,
+                                                     float* __restrict__ m, float* __restrict__ v, int64_t* n_dev,
+                                                     int64_t capacity, int64_t ld, const float* __restrict__ cand,
+                                                     const int64_t* __restrict__ counts, int n_sets, int64_t max_add) {
+    const int64_t n = *n_dev;
+    const int set = blockIdx.y;
+    int64_t off = 0;
+    for (int k = 0; k < set; ++k) off += counts[k];
+    const int64_t cnt = counts[set];
+    const float* src = cand + size_t(set) * 14 * max_add;
+    for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < cnt; j += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t col = n + off + j;
+        if (col >= capacity) break;
+        for (int k = 0; k < 14; ++k) params[k * ld + col] = src[k * max_add + j];
+        if (raw) {
+            for (int k = 0; k < 14; ++k) raw[k * ld + col] = src[k * max_add + j];
+            for (int k = 3; k < 6; ++k) raw[k * ld + col] = logf(src[k * max_add + j]);
+            const float o = src[10 * max_add + j];
+            raw[10 * ld + col] = logf(o / (1.f - o));
+        }
+        if (m) for (int k = 0; k < 14; ++k) m[k * ld + col] = 0.f;
+        if (v) for (int k = 0; k < 14; ++k) v[k * ld + col] = 0.f;
+    }
+}
+
+__global__ void append_commit_kernel(int64_t* n_dev, const int64_t* counts, int n_sets, int64_t capacity) {
+    int64_t n = *n_dev;
+    for (int k = 0; k < n_sets; ++k) n += counts[k];
+    *n_dev = n < capacity ? n : capacity;
+}
+
+void launch_append(float* params, float* raw, float* m, float* v, int64_t* n_dev, int64_t capacity, int64_t ld,
+                   const float* cand, const int64_t* counts, int32_t n_sets, int64_t max_add, cudaStream_t st) {
+    if (n_sets <= 0 || max_add <= 0) return;
+    dim3 grid(unsigned(std::min<int64_t>((max_add + 255) / 256, 64)), unsigned(n_sets));
+    append_kernel<<<grid, 256, 0, st>>>(params, raw, m, v, n_dev, capacity, ld, cand, counts, n_sets, max_add);
+    append_commit_kernel<<<1, 1, 0, st>>>(n_dev, counts, n_sets, capacity);
+}
+
 __global__ void add_commit_kernel(int64_t* n_dev, const unsigned long long* count, int64_t max_add, int64_t capacity) {
     const int64_t n = *n_dev;
     int64_t a = int64_t(*count);
@@ -358,6 +403,7 @@ gs_status run_densify(WsState* s, float* params, float* raw, int64_t* n_dev, int
         GS_K((scan_blocks_kernel<<<1, 1024, 0, st>>>(bcounts, nb, &misc->add_count)));
         GS_K((scatter_kernel<<<nb, kCmpThreads, 0, st>>>(npx, nullptr, pred, emit, bcounts)));
         if (!add_out) GS_K((add_commit_kernel<<<1, 1, 0, st>>>(n_dev, &misc->add_count, cfg.max_add, capacity)));
+        else GS_K((add_count_out_kernel<<<1, 1, 0, st>>>(n_dev, &misc->add_count, cfg.max_add)));
         return check_launch(s, "densify_add");
     }
     if (cfg.mode == GS_DENSIFY_PRUNE) {

@@ -1,0 +1,103 @@
+"""Coarse-to-fine camera tracking (Alg. 1; Eq. 10-12).
+
+Every step runs in libgs kernels; this module only sequences the calls:
+  coarse stage  T_c x [ gs_project (H/2 x W/2) -> gs_bin_sort -> gs_render_fwd -> gs_loss_l1
+                        -> gs_pose_grad -> gs_pose_step ]
+  selection     gs_render_fwd (full res, GS_FLAG_ACCUM_WEIGHT) -> gs_densify_prune(SELECT)  (Eq. 12)
+  fine stage    T_f x [ same at full resolution, gs_project with the selection mask ]
+The pose lives on the device (world->camera 3x4) and is updated in place; no host sync inside
+the loops (bin_sort runs in GS_FLAG_NO_HOST_SYNC mode). Readings: C12 (half-resolution camera),
+C23 (loss and twist learning rate), C24 (selection rule) of DESIGN.md §3.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+import torch
+
+from . import (GS_DENSIFY_SELECT, GS_FLAG_ACCUM_WEIGHT, GS_FLAG_NO_HOST_SYNC, GS_FLAG_POSE_COV_PATH, densify_cfg,
+               gs_densify_prune, gs_pose_step, make_camera)
+from .pipeline import RenderPipeline
+
+
+@dataclasses.dataclass
+class TrackConfig:
+    iters_coarse: int = 50
+    iters_fine: int = 50
+    lr_rho: float = 1e-3
+    lr_phi: float = 1e-3
+    w_color: float = 0.9
+    w_depth: float = 0.1
+    sel_weight: float = 0.5
+    sel_depth: float = 0.05
+    pose_flags: int = GS_FLAG_POSE_COV_PATH
+
+
+class Tracker:
+    def __init__(self, n_cap: int, key_cap_full: int, key_cap_half: int, cam_full, device="cuda"):
+        self.cam_full = cam_full
+        self.cam_half = cam_full.half()
+        self.full = RenderPipeline(n_cap, key_cap_full, cam_full.width, cam_full.height, device)
+        self.half = RenderPipeline(n_cap, key_cap_half, self.cam_half.width, self.cam_half.height, device)
+        dev = torch.device(device)
+        self.grad_pose = torch.zeros(6, dtype=torch.float64, device=dev)
+        self.m6 = torch.zeros(6, dtype=torch.float32, device=dev)
+        self.v6 = torch.zeros(6, dtype=torch.float32, device=dev)
+        self.mask = torch.zeros(n_cap, dtype=torch.uint8, device=dev)
+        self.accum = torch.zeros(n_cap, dtype=torch.float32, device=dev)
+        self.n_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.step = 0
+
+    def reset(self):
+        self.m6.zero_()
+        self.v6.zero_()
+        self.step = 0
+
+    def _iter(self, pipe, cam, P, n, V, tc, td, cfg: TrackConfig, mask=None):
+        pipe.forward(P, n, V, cam, mask=mask, bin_flags=GS_FLAG_NO_HOST_SYNC, fwd_flags=0)
+        dc, dd = pipe.loss_l1(cam, tc, td, cfg.w_color, cfg.w_depth)
+        self.grad_pose.zero_()
+        pipe.pose_grad(P, n, V, cam, dc, dd, self.grad_pose, flags=cfg.pose_flags)
+        self.step += 1
+        gs_pose_step(V, self.grad_pose, self.m6, self.v6, self.step, cfg.lr_rho, cfg.lr_phi)
+
+    def coarse_iter(self, P, n, V, tc_half, td_half, cfg: TrackConfig):
+        self._iter(self.half, self.cam_half, P, n, V, tc_half, td_half, cfg)
+
+    def select(self, P, n, V, td_full, cfg: TrackConfig):
+        """Eq. 12 with reading C24: accumulated alpha*T > sel_weight and |D* - d| < sel_depth."""
+        self.accum[:n].zero_()
+        self.full.forward(P, n, V, self.cam_full, bin_flags=GS_FLAG_NO_HOST_SYNC, fwd_flags=GS_FLAG_ACCUM_WEIGHT,
+                          accum_weight=self.accum)
+        self.n_dev.fill_(n)
+        gs_densify_prune(P, None, self.n_dev, n, P.shape[1], None, None, None, None, None, td_full, self.accum, V,
+                         make_camera(self.cam_full),
+                         densify_cfg(GS_DENSIFY_SELECT, sel_weight=cfg.sel_weight, sel_depth=cfg.sel_depth),
+                         self.mask, None, self.full.ws)
+        return self.mask[:n]
+
+    def fine_iter(self, P, n, V, tc_full, td_full, cfg: TrackConfig):
+        self._iter(self.full, self.cam_full, P, n, V, tc_full, td_full, cfg, mask=self.mask)
+
+    def track(self, P, n, V, tc_half, td_half, tc_full, td_full, cfg: TrackConfig = TrackConfig()):
+        """Alg. 1: T_c coarse iterations, selection, T_f fine iterations. Updates V in place."""
+        self.reset()
+        for _ in range(cfg.iters_coarse):
+            self.coarse_iter(P, n, V, tc_half, td_half, cfg)
+        self.select(P, n, V, td_full, cfg)
+        for _ in range(cfg.iters_fine):
+            self.fine_iter(P, n, V, tc_full, td_full, cfg)
+        return V
+
+
+def pose_error(view, view_gt) -> tuple[float, float]:
+    """(camera-centre distance in metres, rotation angle in degrees) between two world->camera poses."""
+    a = np.asarray(view, np.float64)
+    b = np.asarray(view_gt, np.float64)
+    ca = -a[:, :3].T @ a[:, 3]
+    cb = -b[:, :3].T @ b[:, 3]
+    dr = a[:, :3] @ b[:, :3].T
+    ang = math.degrees(math.acos(max(-1.0, min(1.0, (np.trace(dr) - 1.0) / 2.0))))
+    return float(np.linalg.norm(ca - cb)), ang
