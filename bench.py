@@ -367,10 +367,142 @@ def roofline(per_step, clocks, K, n, V_s, E_f, E_b, npx, binsort="bucket"):
             "share_of_step": t_ms / sum(v[0] for v in per_step.values())}
 
 
+def _timed_events(fn, steps):
+    import torch
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / max(steps, 1)
+
+
+def main_tracking(args):
+    """Config 3: coarse-to-fine tracking (Alg. 1). Throughput on the config-2 scene (the BASELINE
+    workload) and pose error both there and on a seeded surface-like room."""
+    import numpy as np
+    import torch
+
+    import gs_inputs as gi
+    import paper_2311_11700_b200 as g
+    from paper_2311_11700_b200.tracking import TrackConfig, Tracker, pose_error
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    out = {"metric": "coarse-to-fine tracking iters/s (config 3: 600x340 coarse, 1200x680 fine, 500k Gaussians)",
+           "unit": "iters/s", "n_gpus": world, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f32", "data": "synthetic", "steps": args.steps, "warmup": args.warmup}
+    results = {}
+    for name, scene, view in (("config2_fog", gi.CONFIGS[2].scene(), gi.CONFIGS[2].view()),
+                              ("surface_room", gi.room_surface_gaussians(500_000, 31), gi.room_view(131))):
+        cam = gi.CAM_REPLICA
+        n = scene.shape[1]
+        P = torch.as_tensor(scene, device="cuda")
+        Vgt = torch.as_tensor(view, device="cuda")
+        probe = g.RenderPipeline(n, 1 << 26, cam.width, cam.height)
+        K = probe.forward(P, n, Vgt, cam).n_keys
+        del probe
+        tr = Tracker(n, int(K * 1.5) + 65536, int(K * 0.6) + 65536, cam)
+        fh = tr.half.forward(P, n, Vgt, cam.half())
+        tch, tdh = fh.color.clone(), fh.depth.clone()
+        ff = tr.full.forward(P, n, Vgt, cam)
+        tcf, tdf = ff.color.clone(), ff.depth.clone()
+        # initial pose exp(delta^) T_gt with |rho| = 2 cm, |phi| = 1 deg (seed 105): input setup on the host
+        V = Vgt.clone()
+        Vh = view.astype(np.float64)
+        d = gi.twist_perturbation(gi.TRACK_PERTURB_SEED)
+        rho, phi = d[:3], d[3:]
+        th = float(np.linalg.norm(phi))
+        Kx = np.array([[0, -phi[2], phi[1]], [phi[2], 0, -phi[0]], [-phi[1], phi[0], 0]])
+        R = np.eye(3) + np.sin(th) / th * Kx + (1 - np.cos(th)) / th ** 2 * Kx @ Kx
+        Vm = np.eye(3) + (1 - np.cos(th)) / th ** 2 * Kx + (th - np.sin(th)) / th ** 3 * Kx @ Kx
+        Vp = np.concatenate([R @ Vh[:, :3], (R @ Vh[:, 3] + Vm @ rho)[:, None]], 1)
+        e0 = pose_error(Vp, view)
+        tcfg = TrackConfig()
+        V.copy_(torch.as_tensor(Vp, dtype=torch.float32))
+        tr.reset()
+        t_c = _timed_events(lambda: tr.coarse_iter(P, n, V, tch, tdh, tcfg), tcfg.iters_coarse)
+        tr.select(P, n, V, tdf, tcfg)
+        t_f = _timed_events(lambda: tr.fine_iter(P, n, V, tcf, tdf, tcfg), tcfg.iters_fine)
+        e1 = pose_error(V.cpu().numpy(), view)
+        results[name] = {"coarse_iters_per_s": 1000.0 / t_c, "fine_iters_per_s": 1000.0 / t_f,
+                         "selected": int(tr.mask[:n].sum().item()), "err_init_cm": e0[0] * 100,
+                         "err_init_deg": e0[1], "err_final_cm": e1[0] * 100, "err_final_deg": e1[1],
+                         "track_ms_per_frame": t_c * tcfg.iters_coarse + t_f * tcfg.iters_fine}
+        del tr
+        torch.cuda.empty_cache()
+    r = results["config2_fog"]
+    out["value"] = 1000.0 * (tcfg.iters_coarse + tcfg.iters_fine) / r["track_ms_per_frame"]
+    out["ms_per_step"] = r["track_ms_per_frame"] / (tcfg.iters_coarse + tcfg.iters_fine)
+    out["config"] = {"workload": "config 3: 50 coarse (600x340) + select + 50 fine (1200x680) pose iterations",
+                     "scenes": results}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    return 0
+
+
+def main_mapping(args):
+    """Config 4: keyframe-sharded mapping, 2M Gaussians, 8 keyframes at 1200x680 over N GPUs."""
+    import torch
+
+    import gs_inputs as gi
+    import paper_2311_11700_b200 as g
+    from paper_2311_11700_b200.mapping import Keyframe, ShardedMapper
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = init_dist(world, "nccl")
+    cfg = gi.CONFIGS[4]
+    cam = cfg.cam
+    n = cfg.n
+    cap = int(n * 1.05) + 65536
+    P = torch.zeros(14, cap, device="cuda")
+    P[:, :n] = torch.as_tensor(cfg.scene(), device="cuda")
+    tgt = torch.as_tensor(gi.gaussians(n, cfg.target_seed), device="cuda")
+    probe = g.RenderPipeline(n, 1 << 28, cam.width, cam.height)
+    kfs, kmax = [], 0
+    for s in gi.MAPPING_POSE_SEEDS:
+        V = torch.as_tensor(gi.room_view(s), device="cuda")
+        fr = probe.forward(tgt, n, V, cam)
+        kmax = max(kmax, fr.n_keys, probe.forward(P, n, V, cam).n_keys)
+        fr = probe.forward(tgt, n, V, cam)
+        kfs.append(Keyframe(V, fr.color.clone(), fr.depth.clone()))
+    del probe
+    torch.cuda.empty_cache()
+    mp = ShardedMapper(P, n, kfs, cam, int(kmax * 1.2) + (1 << 20), max_add_per_kf=8192, group=None)
+    for _ in range(max(args.warmup, 3)):
+        mp.step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = _timed_events(mp.step, args.steps)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    out = {"metric": "multi-keyframe mapping iters/s (config 4: 2M Gaussians, 8 keyframes 1200x680)",
+           "value": 1000.0 / ms, "unit": "iters/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic", "config": {"workload": "config 4 mapping", "keyframes": len(kfs),
+                                           "keyframes_per_rank": len(mp.local), "n_gaussians_end": mp.n,
+                                           "parallelism": f"keyframe shards x{world}, NCCL all_reduce"}}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == 3:
+        return main_tracking(args)
+    if args.config == 4:
+        return main_mapping(args)
     return main_ours(args)
 
 

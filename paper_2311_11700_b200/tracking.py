@@ -99,5 +99,7 @@ def pose_error(view, view_gt) -> tuple[float, float]:
     ca = -a[:, :3].T @ a[:, 3]
     cb = -b[:, :3].T @ b[:, 3]
     dr = a[:, :3] @ b[:, :3].T
-    ang = math.degrees(math.acos(max(-1.0, min(1.0, (np.trace(dr) - 1.0) / 2.0))))
+    s = 0.5 * np.linalg.norm([dr[2, 1] - dr[1, 2], dr[0, 2] - dr[2, 0], dr[1, 0] - dr[0, 1]])
+    c = 0.5 * (np.trace(dr) - 1.0)
+    ang = math.degrees(math.atan2(s, c))   # accurate for small angles, unlike acos
     return float(np.linalg.norm(ca - cb)), ang
