@@ -1,19 +1,19 @@
 // gs_render_fwd / gs_render_bwd / gs_pose_grad kernels (sm_100a).
 //
-// Forward (Eq. 4-5): one 256-thread CTA per 16x16 tile, one pixel per thread.
-// The tile's sorted Gaussian indices are gathered 256 records (48 B each) at a time into shared
-// memory with cp.async (LDGSTS; the records are an index gather, so a TMA tensor copy does not
-// apply), double-buffered against the blend of the previous batch.
+// Forward (Eq. 4-5): one CTA per 16x16 tile (render_fwd2_kernel: 128 threads, two
+// pixels each). The tile's sorted Gaussian indices are gathered into shared memory with cp.async
+// (LDGSTS; the records are an index gather, so a TMA tensor copy does not apply), double-buffered
+// against the blend of the previous batch. render_fwd_kernel<true> (one pixel per thread) is the
+// GS_FLAG_ACCUM_WEIGHT variant used by the Eq. 12 selection.
 //
-// Backward, front to back: with e_i = c_i.dL/dC + d_i dL/dD, Q = colour.dL/dC +
-// depth.dL/dD (forward outputs incl. T_f bg) and the running prefix P_i = sum_{k<=i} alpha_k T_k e_k,
-//     dL/dalpha_i = T_i e_i - (Q - P_i) / (1 - alpha_i)
-// which equals Eq. S6 plus its colour/background analogue. T_i is recomputed
-// front to back with the forward's exact fp32 operations, so no transmittance is recovered by
-// division. Per 32-Gaussian batch: phase 1 (thread = pixel) writes (alpha T, G dL/dalpha) to shared
-// memory; phase 2 (warp = 32 pixels, lane = Gaussian) accumulates the 10 per-Gaussian sums as
-// pixel moments; the 8 warps' partials are combined in shared memory and each (tile, Gaussian)
-// issues one atomic per component (warp/block reduction before global atomics, north_star).
+// Backward, back to front: T_i = T_{i+1} / (1 - alpha_i) from T_final, suffix
+// sum S_i = sum_{k>i} alpha_k T_k e_k with e_k = c_k.dL/dC + d_k dL/dD, and
+//     dL/dalpha_i = T_i e_i - (S_i + T_f bg.dL/dC) / (1 - alpha_i)
+// which is Eq. S6 plus its colour/background analogue. Per 16-Gaussian batch:
+// phase 1 (thread = pixel) writes (alpha T, G dL/dalpha) to shared memory; phase 2 (lane =
+// (Gaussian, pixel row)) accumulates the 10 per-Gaussian sums as pixel moments; the partial sets
+// are combined in shared memory and each (tile, Gaussian) issues one atomic per component
+// (block reduction before global atomics, north_star).
 #include <cub/block/block_reduce.cuh>
 
 #include "gs_internal.cuh"
@@ -368,7 +368,8 @@ __global__ void __launch_bounds__(kTilePx, 4) render_bwd_kernel(
                 if (e.alpha != 0.f) {
                     const float4 r2 = sm.rec[buf][k][2];
                     const float ev = fmaf(r2.x, dl.x, fmaf(r2.y, dl.y, fmaf(r2.z, dl.z, r1.z * dl.w)));
-                    const float ro = __frcp_rn(__fsub_rn(1.f, e.alpha));
+                    float ro;   // 1/(1 - alpha): MUFU rcp.approx (<= 1 ulp; gradients only, no decision)
+                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ro) : "f"(__fsub_rn(1.f, e.alpha)));
                     T = T * ro;
                     w = e.alpha * T;
                     const float ga = fmaf(T, ev, -(S + tfb) * ro);
