@@ -287,28 +287,49 @@ def main_ours(args):
                                    npx=cam.width * cam.height, binsort=args.binsort)
         # ---- e2e through the public API with host buffers (pinned) and a loss readback
         if not args.no_e2e:
+            # every step uploads its inputs (params, pose, RGB-D target) from pinned host memory and
+            # reads its loss back; uploads are double-buffered on a copy stream so step i+1's copy
+            # overlaps step i's kernels (both inside the timed region)
             hp = torch.empty_like(P, device="cpu").pin_memory()
             hp.copy_(P.cpu())
             hv = V.cpu().pin_memory()
             htc, htd = tc.cpu().pin_memory(), td.cpu().pin_memory()
             hloss = torch.empty(1, dtype=torch.float64).pin_memory()
-            Pd, Vd, tcd, tdd = torch.empty_like(P), torch.empty_like(V), torch.empty_like(tc), torch.empty_like(td)
+            bufs = [(torch.empty_like(P), torch.empty_like(V), torch.empty_like(tc), torch.empty_like(td))
+                    for _ in range(2)]
+            s_copy = torch.cuda.Stream()
+            ev_copied = [torch.cuda.Event() for _ in range(2)]
+            ev_used = [torch.cuda.Event() for _ in range(2)]
+            for e in ev_used:
+                e.record()
 
-            def e2e_step():
-                Pd.copy_(hp, non_blocking=True)
-                Vd.copy_(hv, non_blocking=True)
-                tcd.copy_(htc, non_blocking=True)
-                tdd.copy_(htd, non_blocking=True)
-                grad.zero_()
-                gpose.zero_()
-                pipe.iteration(Pd, n, Vd, cam, tcd, tdd, grad, gpose, bin_flags=flags, fwd_flags=0)
-                hloss.copy_(pipe.loss, non_blocking=True)
-            for _ in range(3):
-                e2e_step()
-            ms_e2e = timed(e2e_step, args.steps)
+            def upload(i):
+                b = bufs[i % 2]
+                with torch.cuda.stream(s_copy):
+                    s_copy.wait_event(ev_used[i % 2])
+                    for dst, src in zip(b, (hp, hv, htc, htd)):
+                        dst.copy_(src, non_blocking=True)
+                    ev_copied[i % 2].record(s_copy)
+
+            def e2e_run(steps):
+                cur = torch.cuda.current_stream()
+                s_copy.wait_stream(cur)   # the first upload starts inside the timed region
+                upload(0)
+                for i in range(steps):
+                    if i + 1 < steps:
+                        upload(i + 1)
+                    Pd, Vd, tcd, tdd = bufs[i % 2]
+                    cur.wait_event(ev_copied[i % 2])
+                    grad.zero_()
+                    gpose.zero_()
+                    pipe.iteration(Pd, n, Vd, cam, tcd, tdd, grad, gpose, bin_flags=flags, fwd_flags=0)
+                    ev_used[i % 2].record(cur)
+                    hloss.copy_(pipe.loss, non_blocking=True)
+            e2e_run(3)
+            ms_e2e = timed(lambda: e2e_run(args.steps), 1) / args.steps
             h2d = P.numel() * 4 + V.numel() * 4 + tc.numel() * 4 + td.numel() * 4
             out["e2e"] = {"value": world * 1000.0 / ms_e2e, "unit": "iters/s", "h2d_bytes_per_step": int(h2d),
-                          "d2h_bytes_per_step": 8}
+                          "d2h_bytes_per_step": 8, "overlap": "double-buffered H2D on a copy stream"}
         # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             try:

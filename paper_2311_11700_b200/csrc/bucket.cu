@@ -8,10 +8,10 @@
 //                   difference array over the tile grid in shared memory gives count[c][t]
 //   B4  tile scan:  per-tile totals (8 chunk segments per tile in flight), one exclusive scan over
 //                   tiles (ranges, K), then per-tile exclusive scans over chunks -> base[c][t]
-//   B5  emission:   block = (chunk, 128-tile group); the chunk's Gaussians touching the group are
-//                   compacted in depth order; a warp takes one tile at a time, its lanes test 32
-//                   Gaussians, and a ballot/popc prefix places the hits at base[c][t] + rank
-//                   (coalesced 4-B stores, depth order preserved)
+//   B5  emission:   block = (chunk, 128-tile group), warp = 16 consecutive tiles; each warp compacts
+//                   (in depth order) the chunk's Gaussians meeting its segment's bounding box, then
+//                   per tile its lanes test 32 of them at a time and a ballot/popc prefix places the
+//                   hits at base[c][t] + rank (coalesced 4-B stores, depth order preserved)
 // Per tile, entries come out in chunk order and in depth order within a chunk, i.e. ordered by
 // (depth bits, index): exactly the per-tile lists of path A (checked bit-exact in the tests).
 // HBM traffic is ~4 B per key (+ per-Gaussian and per-chunk terms) instead of ~150 B per key.
@@ -26,6 +26,7 @@ namespace gs {
 
 constexpr int kChunk = 256;      // Gaussians per chunk (depth order)
 constexpr int kGroup = 128;      // tiles per emission block
+constexpr int kSeg = 16;         // consecutive tiles per emission warp (kGroup / 8 warps)
 
 gs_status chained_scan(WsState* s, const uint32_t* in, uint32_t* out, int64_t n, unsigned long long* total,
                        cudaStream_t st, int64_t cap, unsigned long long* total_eff);
@@ -185,51 +186,61 @@ __global__ void __launch_bounds__(256) bucket_emit_kernel(
     const uint32_t* __restrict__ svals, const short4* __restrict__ srect, const uint32_t* __restrict__ cmat,
     const unsigned int* __restrict__ n_on, const unsigned long long* __restrict__ n_keys_eff,
     const unsigned long long* __restrict__ n_keys, int GX, int T, uint32_t* __restrict__ vals_out) {
-    using BS = cub::BlockScan<int, 256>;
-    __shared__ typename BS::TempStorage tmp;
-    __shared__ short4 l_rect[kChunk];
-    __shared__ uint32_t l_g[kChunk];
-    __shared__ int l_n;
+    __shared__ uint32_t l_mask[8][kChunk];
+    __shared__ uint32_t l_g[8][kChunk];
     if (*n_keys_eff != *n_keys) return;   // capacity overflow: emit nothing (error flag is set)
     const int c = blockIdx.x;
     const uint32_t Von = *n_on;
     const uint32_t base = uint32_t(c) * kChunk;
     if (base >= Von) return;
-    const int t0 = blockIdx.y * kGroup, t1 = min(T, t0 + kGroup);
-    const int ya = t0 / GX, yb = (t1 - 1) / GX;
-    const int xa = (ya == yb) ? t0 % GX : 0, xb = (ya == yb) ? (t1 - 1) % GX : GX - 1;
-    // ordered compaction of the chunk's Gaussians whose rect meets the group's bounding box
-    const uint32_t s = base + threadIdx.x;   // kChunk == blockDim.x
-    short4 r = make_short4(0, 0, 0, 0);
-    int keep = 0;
-    if (s < Von) {
-        r = srect[s];
-        keep = r.z <= yb && r.w > ya && r.x <= xb && r.y > xa;
-    }
-    int off, total;
-    BS(tmp).ExclusiveSum(keep, off, total);
-    if (keep) {
-        l_rect[off] = r;
-        l_g[off] = svals[s];
-    }
-    if (threadIdx.x == 0) l_n = total;
-    __syncthreads();
-    const int L = l_n;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
-    for (int t = t0 + warp; t < t1; t += 8) {
-        const int tx = t % GX, ty = t / GX;
-        uint32_t pos = cmat[size_t(c) * T + t];
-        for (int k0 = 0; k0 < L; k0 += 32) {
-            const int k = k0 + lane;
-            bool hit = false;
-            if (k < L) {
-                const short4 q = l_rect[k];
-                hit = tx >= q.x && tx < q.y && ty >= q.z && ty < q.w;
-            }
+    // this warp's segment: up to 16 consecutive tiles (row-major) starting at (tx0, ty0); it spans
+    // n0 tiles of row ty0 and possibly the first nseg - n0 tiles of row ty0 + 1
+    const int t0 = blockIdx.y * kGroup + warp * kSeg;
+    if (t0 >= T) return;   // warp-uniform; no block-level barrier below
+    const int nseg = min(kSeg, T - t0);
+    const int ty0 = t0 / GX, tx0 = t0 - ty0 * GX;
+    const int n0 = min(nseg, GX - tx0);
+    // bit j of a Gaussian's mask: its rect contains segment tile j
+    auto run_mask = [](short4 r, int row, int x0, int cnt, int bit0) -> uint32_t {
+        if (row < r.z || row >= r.w) return 0u;
+        const int lo = max(int(r.x), x0) - x0, hi = min(int(r.y), x0 + cnt) - x0;
+        return hi > lo ? (((1u << hi) - 1u) & ~((1u << lo) - 1u)) << bit0 : 0u;
+    };
+    // ordered (depth-order) compaction of the chunk's Gaussians meeting the segment, with masks
+    int L = 0;
+    for (int k0 = 0; k0 < kChunk; k0 += 32) {
+        const uint32_t s = base + k0 + lane;
+        uint32_t mask = 0;
+        if (s < Von) {
+            const short4 r = srect[s];
+            mask = run_mask(r, ty0, tx0, n0, 0);
+            if (n0 < nseg) mask |= run_mask(r, ty0 + 1, 0, nseg - n0, n0);
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, mask != 0u);
+        if (mask) {
+            const int o = L + __popc(m & lt);
+            l_mask[warp][o] = mask;
+            l_g[warp][o] = svals[s];
+        }
+        L += __popc(m);
+    }
+    __syncwarp();
+    // lane j < nseg keeps tile j's running output position
+    uint32_t mypos = lane < nseg ? cmat[size_t(c) * T + t0 + lane] : 0u;
+    for (int k0 = 0; k0 < L; k0 += 32) {
+        const int k = k0 + lane;
+        const uint32_t mask = k < L ? l_mask[warp][k] : 0u;
+        const uint32_t g = k < L ? l_g[warp][k] : 0u;
+#pragma unroll
+        for (int j = 0; j < kSeg; ++j) {
+            const bool hit = (mask >> j) & 1u;
             const uint32_t m = __ballot_sync(0xffffffffu, hit);
-            if (hit) vals_out[pos + __popc(m & lt)] = l_g[k];
-            pos += __popc(m);
+            if (m == 0u) continue;   // warp-uniform
+            const uint32_t pj = __shfl_sync(0xffffffffu, mypos, j);
+            if (hit) vals_out[pj + __popc(m & lt)] = g;
+            if (lane == j) mypos += __popc(m);
         }
     }
 }
