@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(256) bucket_emit_kernel(
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     // this warp's segment: up to 16 consecutive tiles (row-major) starting at (tx0, ty0); it spans
-    // n0 tiles of row ty0 and possibly the first nseg - n0 tiles of row ty0 + 1
+    // n0 tiles of row ty0 and then whole or partial following rows
     const int t0 = blockIdx.y * kGroup + warp * kSeg;
     if (t0 >= T) return;   // warp-uniform; no block-level barrier below
     const int nseg = min(kSeg, T - t0);
@@ -216,7 +216,8 @@ __global__ void __launch_bounds__(256) bucket_emit_kernel(
         if (s < Von) {
             const short4 r = srect[s];
             mask = run_mask(r, ty0, tx0, n0, 0);
-            if (n0 < nseg) mask |= run_mask(r, ty0 + 1, 0, nseg - n0, n0);
+            for (int bit = n0, row = ty0 + 1; bit < nseg; bit += GX, ++row)   // narrow grids: more rows
+                mask |= run_mask(r, row, 0, min(GX, nseg - bit), bit);
         }
         const uint32_t m = __ballot_sync(0xffffffffu, mask != 0u);
         if (mask) {
