@@ -57,7 +57,8 @@ static void carve(WsState* s, Carver& c) {
     s->n_last = c.take(uint64_t(px) * 4);
     s->examined = c.take(uint64_t(px) * 4);
     s->sort_hist = c.take(8 * 256 * 4);
-    s->max_parts = std::max(sort_parts(s->key_cap), sort_parts(s->n_cap));
+    // look-back rows: path A sorts key_cap keys in 4096-key partitions, path B n_cap keys in 1024-key ones
+    s->max_parts = std::max(sort_parts(s->key_cap), (std::max<int64_t>(s->n_cap, 1) + 1023) / 1024);
     s->sort_look = c.take(uint64_t(s->max_parts) * 256 * 8);
     s->misc = c.take(sizeof(Misc));
     s->scratch = c.take(uint64_t(px) * 4 * 4);
@@ -69,6 +70,7 @@ static void carve(WsState* s, Carver& c) {
     s->srect = c.take(uint64_t(n) * 8);
     s->tile_tot = c.take(uint64_t(tiles) * 4 * 10);   // totals, starts, 8 segment sums
     s->pose_part = c.take(uint64_t((n + 255) / 256 + 1) * 16 * 8);   // per-block pose partials
+    s->onlist = c.take(uint64_t(n) * 4);                              // on-screen Gaussians, index order
 }
 
 static bool ws_ok(const gs_ws* ws) { return ws && state(ws)->magic == kMagic; }

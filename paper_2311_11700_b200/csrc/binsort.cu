@@ -21,9 +21,93 @@ __device__ __forceinline__ unsigned long long scan_word(uint32_t epoch, uint32_t
     return (uint64_t(epoch & 0x3fffffffu) << 34) | (uint64_t(flag) << 32) | v;
 }
 
+// Decoupled look-back by one warp: publish this partition's aggregate, sum predecessors' words
+// (32 per round) until the nearest inclusive prefix, publish the inclusive prefix, and return the
+// exclusive prefix of the partition. Partition order comes from an atomic ticket, so every
+// predecessor of a running partition has started: the spin always makes progress.
+__device__ uint32_t lookback_prefix(unsigned long long* status, uint32_t part, uint32_t epoch, uint32_t agg) {
+    const unsigned lane = threadIdx.x & 31;
+    uint32_t prefix = 0;
+    if (part == 0) {
+        if (lane == 0) atomicExch(status + part, scan_word(epoch, 2, agg));
+        return 0;
+    }
+    if (lane == 0) atomicExch(status + part, scan_word(epoch, 1, agg));
+    int64_t j = int64_t(part) - 1 - lane;   // each lane inspects one predecessor
+    while (true) {
+        uint64_t w = 0;
+        uint32_t flag = 0;
+        if (j >= 0) {
+            do {
+                w = *reinterpret_cast<volatile unsigned long long*>(status + j);
+                flag = (uint32_t(w >> 34) == (epoch & 0x3fffffffu)) ? uint32_t((w >> 32) & 3u) : 0u;
+            } while (flag == 0);
+        } else {
+            flag = 2;   // virtual prefix 0 before partition 0
+            w = 0;
+        }
+        const uint32_t val = j >= 0 ? uint32_t(w) : 0u;
+        const unsigned pre_mask = __ballot_sync(0xffffffffu, flag == 2);
+        // lanes up to and including the nearest (lowest lane = highest index) prefix
+        const int stop = pre_mask ? __ffs(pre_mask) - 1 : 31;
+        uint32_t contrib = (int(lane) <= stop) ? val : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, o);
+        prefix += contrib;
+        if (pre_mask) break;
+        j -= 32;
+    }
+    if (lane == 0) atomicExch(status + part, scan_word(epoch, 2, prefix + agg));
+    return prefix;
+}
+
+// Ordered compaction of the on-screen Gaussians (tiles > 0), in index order: list[r] = i and the
+// depth-sort pairs (depth key, i); *count = V_s. Shared by both gs_bin_sort paths (the per-Gaussian
+// backward iterates the list) and the input of path B's depth sort.
+__global__ void __launch_bounds__(kScanThreads) compact_onscreen_kernel(
+    const uint32_t* __restrict__ tiles, const uint32_t* __restrict__ dkey, int64_t n,
+    unsigned long long* status, unsigned int* ticket, uint32_t epoch, uint32_t* __restrict__ list,
+    uint32_t* __restrict__ key_out, uint32_t* __restrict__ val_out, unsigned int* count,
+    unsigned long long* count64) {
+    using BlockScan = cub::BlockScan<uint32_t, kScanThreads>;
+    __shared__ typename BlockScan::TempStorage tmp;
+    __shared__ uint32_t s_part, s_excl;
+    if (threadIdx.x == 0) s_part = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t part = s_part;
+    const int64_t base = int64_t(part) * kScanTile + int64_t(threadIdx.x) * kScanItems;
+    bool f[kScanItems];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        f[k] = (base + k < n) && tiles[base + k] > 0;
+        sum += f[k];
+    }
+    uint32_t excl_thread, agg;
+    BlockScan(tmp).ExclusiveSum(sum, excl_thread, agg);
+    if (threadIdx.x < 32) {
+        const uint32_t prefix = lookback_prefix(status, part, epoch, agg);
+        if (threadIdx.x == 0) s_excl = prefix;
+    }
+    __syncthreads();
+    uint32_t r = s_excl + excl_thread;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        if (f[k]) {
+            const uint32_t i = uint32_t(base + k);
+            list[r] = i;
+            key_out[r] = dkey[i];
+            val_out[r] = i;
+            ++r;
+        }
+    }
+    if (base < n && base + kScanItems >= n) {   // the partition holding element n-1 publishes V_s
+        *count = r;
+        *count64 = r;
+    }
+}
+
 // Exclusive prefix of in[0..n) (u32) -> out (u32); total written to *total (u64).
-// Partition order is taken from an atomic ticket, so every predecessor of a running partition has
-// started: the look-back spin always makes progress.
 __global__ void __launch_bounds__(kScanThreads) chained_scan_kernel(
     const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int64_t n, unsigned long long* status,
     unsigned int* ticket, uint32_t epoch, unsigned long long* total, int64_t cap, unsigned long long* total_eff,
@@ -45,39 +129,8 @@ __global__ void __launch_bounds__(kScanThreads) chained_scan_kernel(
     uint32_t excl_thread, agg;
     BlockScan(tmp).ExclusiveSum(sum, excl_thread, agg);
     if (threadIdx.x < 32) {
-        const unsigned lane = threadIdx.x;
-        uint32_t prefix = 0;
-        if (part == 0) {
-            if (lane == 0) atomicExch(status + part, scan_word(epoch, 2, agg));
-        } else {
-            if (lane == 0) atomicExch(status + part, scan_word(epoch, 1, agg));
-            int64_t j = int64_t(part) - 1 - lane;   // each lane inspects one predecessor
-            while (true) {
-                uint64_t w = 0;
-                uint32_t flag = 0;
-                if (j >= 0) {
-                    do {
-                        w = *reinterpret_cast<volatile unsigned long long*>(status + j);
-                        flag = (uint32_t(w >> 34) == (epoch & 0x3fffffffu)) ? uint32_t((w >> 32) & 3u) : 0u;
-                    } while (flag == 0);
-                } else {
-                    flag = 2;   // virtual prefix 0 before partition 0
-                    w = 0;
-                }
-                const uint32_t val = j >= 0 ? uint32_t(w) : 0u;
-                const unsigned pre_mask = __ballot_sync(0xffffffffu, flag == 2);
-                // lanes up to and including the nearest (lowest lane = highest index) prefix
-                const int stop = pre_mask ? __ffs(pre_mask) - 1 : 31;
-                uint32_t contrib = (int(lane) <= stop) ? val : 0u;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, o);
-                prefix += contrib;
-                if (pre_mask) break;
-                j -= 32;
-            }
-            if (lane == 0) atomicExch(status + part, scan_word(epoch, 2, prefix + agg));
-        }
-        if (lane == 0) s_excl = prefix;
+        const uint32_t prefix = lookback_prefix(status, part, epoch, agg);
+        if (threadIdx.x == 0) s_excl = prefix;
     }
     __syncthreads();
     uint32_t run = s_excl + excl_thread;
@@ -176,6 +229,24 @@ gs_status chained_scan(WsState* s, const uint32_t* in, uint32_t* out, int64_t n,
     return GS_OK;
 }
 
+// On-screen compaction (both paths): list in index order + path B's depth-sort input in
+// dkey_sorted / dval_sorted (first half); V_s in misc->n_onscreen and misc->n_items.
+gs_status run_compact_onscreen(WsState* s, cudaStream_t st) {
+    Misc* misc = at<Misc>(s, s->misc);
+    cudaMemsetAsync(&misc->n_onscreen, 0, sizeof(misc->n_onscreen), st);
+    cudaMemsetAsync(&misc->n_items, 0, sizeof(misc->n_items), st);
+    if (s->n == 0) return GS_OK;
+    cudaMemsetAsync(&misc->scan_counter, 0, sizeof(misc->scan_counter), st);
+    const uint32_t epoch = uint32_t(++s->epoch) & 0x3fffffffu;
+    const int parts = int((s->n + kScanTile - 1) / kScanTile);
+    KTimer kt(s, KID_DEPTH_SORT, st);
+    compact_onscreen_kernel<<<parts, kScanThreads, 0, st>>>(
+        at<uint32_t>(s, s->tiles), at<uint32_t>(s, s->depth_key), s->n, at<unsigned long long>(s, s->scan_state),
+        &misc->scan_counter, epoch, at<uint32_t>(s, s->onlist), at<uint32_t>(s, s->dkey_sorted),
+        at<uint32_t>(s, s->dval_sorted), &misc->n_onscreen, &misc->n_items);
+    return GS_OK;
+}
+
 // K readback (host-sync mode) or device-only K (graph mode); returns the grid size to use.
 gs_status resolve_keys(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t st, int64_t* Kgrid) {
     Misc* misc = at<Misc>(s, s->misc);
@@ -205,6 +276,8 @@ gs_status run_bin_sort_keys(WsState* s, int64_t* n_keys, uint32_t flags, cudaStr
     cudaMemsetAsync(at<char>(s, s->ranges), 0, size_t(ntiles) * sizeof(uint2), st);
     gs_status rc = chained_scan(s, at<uint32_t>(s, s->tiles), at<uint32_t>(s, s->offsets), s->n, &misc->n_keys, st,
                                 s->key_cap, &misc->n_keys_eff);
+    if (rc != GS_OK) return rc;
+    rc = run_compact_onscreen(s, st);   // on-screen list for the per-Gaussian backward
     if (rc != GS_OK) return rc;
     int64_t Kgrid = 0;
     rc = resolve_keys(s, n_keys, flags, st, &Kgrid);

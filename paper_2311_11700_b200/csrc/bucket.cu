@@ -2,8 +2,8 @@
 //
 // Output-identical to path A (the stable sort of the index-order (tile|depth) keys, O2)
 // without materialising or sorting the K keys:
-//   B1  prep:       sort key = depth bits for on-screen Gaussians, 0xFFFFFFFF otherwise; value = i
-//   B2  depth sort: onesweep LSD radix sort of the n (u32, u32) pairs (stable: ties by index)
+//   B1  compaction: the V_s on-screen Gaussians in index order (decoupled look-back, binsort.cu)
+//   B2  depth sort: onesweep LSD radix sort of their (depth bits, index) pairs (stable: ties by index)
 //   B3  chunk count: the depth-ordered Gaussians are cut into chunks of 256; per chunk, a 2-D
 //                   difference array over the tile grid in shared memory gives count[c][t]
 //   B4  tile scan:  per-tile totals (8 chunk segments per tile in flight), one exclusive scan over
@@ -31,23 +31,6 @@ constexpr int kSeg = 16;         // consecutive tiles per emission warp (kGroup 
 gs_status chained_scan(WsState* s, const uint32_t* in, uint32_t* out, int64_t n, unsigned long long* total,
                        cudaStream_t st, int64_t cap, unsigned long long* total_eff);
 gs_status resolve_keys(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t st, int64_t* Kgrid);
-
-// B1 ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) prep_depth_kernel(int64_t n, const uint32_t* __restrict__ tiles,
-                                                         const uint32_t* __restrict__ dkey, uint32_t* __restrict__ k,
-                                                         uint32_t* __restrict__ v, unsigned int* n_on,
-                                                         unsigned long long* n_items) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    bool on = false;
-    if (i < n) {
-        on = tiles[i] > 0;
-        k[i] = on ? dkey[i] : 0xffffffffu;
-        v[i] = uint32_t(i);
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, on);
-    if ((threadIdx.x & 31) == 0 && m) atomicAdd(n_on, unsigned(__popc(m)));
-    if (i == 0) *n_items = (unsigned long long)n;
-}
 
 // B3 ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kChunk) chunk_count_kernel(const uint32_t* __restrict__ svals,
@@ -256,13 +239,12 @@ gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaS
     uint32_t* k1 = k0 + s->n_cap;
     uint32_t* v0 = at<uint32_t>(s, s->dval_sorted);
     uint32_t* v1 = v0 + s->n_cap;
-    if (n > 0) {
-        KTimer kt(s, KID_DEPTH_SORT, st);
-        prep_depth_kernel<<<int((n + 255) / 256), 256, 0, st>>>(n, at<uint32_t>(s, s->tiles), at<uint32_t>(s, s->depth_key),
-                                                                 k0, v0, &misc->n_onscreen, &misc->n_items);
-    }
+    // B1: ordered compaction of the on-screen Gaussians -> (depth key, index) pairs in k0/v0
+    gs_status rc = run_compact_onscreen(s, st);
+    if (rc != GS_OK) return rc;
+    // B2: stable depth sort of the V_s on-screen pairs (grid sized by n, V_s read on the device)
     int which = 0;
-    gs_status rc = onesweep_sort_pairs<uint32_t>(s, k0, v0, k1, v1, &misc->n_items, n, 32, st, &which);
+    rc = onesweep_sort_pairs<uint32_t, kSortItemsSmall>(s, k0, v0, k1, v1, &misc->n_items, n, 32, st, &which);
     if (rc != GS_OK) return rc;
     const uint32_t* svals = which ? v1 : v0;
     uint32_t* cmat = at<uint32_t>(s, s->chunk_mat);

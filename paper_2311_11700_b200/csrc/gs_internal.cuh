@@ -24,7 +24,8 @@ struct WsState {
     // carve
     Region rec, depth_key, rect, radius, tiles, offsets, sgrad, scan_state,
         keys0, keys1, vals0, vals1, ranges, t_final, n_last, examined, sort_hist, sort_look,
-        misc, scratch, scratch14, dkey_sorted, dval_sorted, chunk_hist, chunk_mat, srect, tile_tot, pose_part;
+        misc, scratch, scratch14, dkey_sorted, dval_sorted, chunk_hist, chunk_mat, srect, tile_tot, pose_part,
+        onlist;
     // run state
     int64_t n;                     // Gaussians of the last gs_project
     int32_t cam_w, cam_h, cam_gx, cam_gy;   // image of the last gs_project
@@ -103,6 +104,7 @@ void set_cuda_error(cudaError_t e, const char* what);
 void launch_project(WsState* s, const float* params, int64_t n, int64_t ld, const uint8_t* mask,
                     const float* viewmat, const gs_camera& cam, cudaStream_t st);
 gs_status run_bin_sort_keys(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t st);
+gs_status run_compact_onscreen(WsState* s, cudaStream_t st);
 gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t st);
 void launch_render_fwd(WsState* s, const gs_camera& cam, float* color, float* depth, float* alpha,
                        float* accum_weight, uint32_t flags, cudaStream_t st);

@@ -16,6 +16,7 @@
 namespace gs {
 
 constexpr int kSortThreads = 256, kSortItems = 16, kSortTile = kSortThreads * kSortItems;
+constexpr int kSortItemsSmall = 4;   // 1024-key partitions for small sorts (more CTAs, shorter latency)
 
 template <class KT>
 __global__ void __launch_bounds__(256) onesweep_hist_kernel(const KT* __restrict__ keys,
@@ -50,10 +51,10 @@ __device__ __forceinline__ unsigned long long look_word(uint32_t epoch, uint32_t
     return (uint64_t(epoch & 0x3fffffffu) << 34) | (uint64_t(flag) << 32) | v;
 }
 
-template <class KT>
+template <class KT, int IPT>
 struct OnesweepSmem {
-    KT keys[kSortTile];
-    uint32_t vals[kSortTile];
+    KT keys[kSortThreads * IPT];
+    uint32_t vals[kSortThreads * IPT];
     uint32_t wh[kSortThreads / 32][256];
     uint32_t local_start[256];
     uint32_t gbase[256];
@@ -61,27 +62,28 @@ struct OnesweepSmem {
     uint32_t part;
 };
 
-template <class KT>
+template <class KT, int IPT>
 __global__ void __launch_bounds__(kSortThreads) onesweep_pass_kernel(
     const KT* __restrict__ kin, const uint32_t* __restrict__ vin, KT* __restrict__ kout, uint32_t* __restrict__ vout,
     const unsigned long long* __restrict__ n_keys, int shift, const uint32_t* __restrict__ digit_base,
     unsigned long long* look, unsigned int* ticket, uint32_t epoch) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    OnesweepSmem<KT>& sm = *reinterpret_cast<OnesweepSmem<KT>*>(smem_raw);
+    OnesweepSmem<KT, IPT>& sm = *reinterpret_cast<OnesweepSmem<KT, IPT>*>(smem_raw);
+    constexpr int kTileKeys = kSortThreads * IPT;
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
     if (tid == 0) sm.part = atomicAdd(ticket, 1u);
     for (int i = tid; i < (kSortThreads / 32) * 256; i += kSortThreads) (&sm.wh[0][0])[i] = 0;
     __syncthreads();
     const uint32_t part = sm.part;
     const uint64_t K = *n_keys;
-    const uint64_t tile_base = uint64_t(part) * kSortTile;
+    const uint64_t tile_base = uint64_t(part) * kTileKeys;
     if (tile_base >= K) return;   // block-uniform
 
-    KT key[kSortItems];
-    uint32_t val[kSortItems], dig[kSortItems], rnk[kSortItems];
+    KT key[IPT];
+    uint32_t val[IPT], dig[IPT], rnk[IPT];
 #pragma unroll
-    for (int i = 0; i < kSortItems; ++i) {
-        const uint64_t idx = tile_base + uint64_t(w) * (32 * kSortItems) + uint64_t(i) * 32 + lane;
+    for (int i = 0; i < IPT; ++i) {
+        const uint64_t idx = tile_base + uint64_t(w) * (32 * IPT) + uint64_t(i) * 32 + lane;
         const bool ok = idx < K;
         key[i] = ok ? kin[idx] : KT(0);
         val[i] = ok ? vin[idx] : 0u;
@@ -89,7 +91,7 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass_kernel(
     }
     const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
-    for (int i = 0; i < kSortItems; ++i) {
+    for (int i = 0; i < IPT; ++i) {
         const uint32_t d = dig[i];
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
         const int leader = __ffs(peers) - 1;
@@ -117,17 +119,29 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass_kernel(
         atomicExch(my, look_word(epoch, 2, cnt));
     } else {
         atomicExch(my, look_word(epoch, 1, cnt));
+        // walk back 8 predecessors per round: 8 independent loads in flight, then consume in order
+        const uint32_t ep = epoch & 0x3fffffffu;
+        auto flag_of = [ep](uint64_t wd) { return (uint32_t(wd >> 34) == ep) ? uint32_t((wd >> 32) & 3u) : 0u; };
         int64_t j = int64_t(part) - 1;
-        while (j >= 0) {
-            uint64_t wd;
-            uint32_t flag;
-            do {
-                wd = *reinterpret_cast<volatile unsigned long long*>(look + uint64_t(j) * 256 + t);
-                flag = (uint32_t(wd >> 34) == (epoch & 0x3fffffffu)) ? uint32_t((wd >> 32) & 3u) : 0u;
-            } while (flag == 0);
-            excl += uint32_t(wd);
-            if (flag == 2) break;
-            --j;
+        bool done = false;
+        while (!done && j >= 0) {
+            uint64_t wd[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                wd[u] = (j - u >= 0) ? *reinterpret_cast<volatile unsigned long long*>(look + uint64_t(j - u) * 256 + t)
+                                     : 0ull;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (done || j - u < 0) break;
+                uint32_t flag = flag_of(wd[u]);
+                while (flag == 0) {   // not published yet: spin on this predecessor
+                    wd[u] = *reinterpret_cast<volatile unsigned long long*>(look + uint64_t(j - u) * 256 + t);
+                    flag = flag_of(wd[u]);
+                }
+                excl += uint32_t(wd[u]);
+                if (flag == 2) done = true;
+            }
+            j -= 8;
         }
         atomicExch(my, look_word(epoch, 2, excl + cnt));
     }
@@ -137,7 +151,7 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass_kernel(
     sm.gbase[t] = digit_base[t] + excl;
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < kSortItems; ++i) {
+    for (int i = 0; i < IPT; ++i) {
         const uint32_t d = dig[i];
         if (d < 256) {
             const uint32_t pos = sm.local_start[d] + sm.wh[w][d] + rnk[i];
@@ -147,7 +161,7 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass_kernel(
     }
     __syncthreads();
     const uint64_t rem = K - tile_base;
-    const uint32_t nvalid = rem < uint64_t(kSortTile) ? uint32_t(rem) : uint32_t(kSortTile);
+    const uint32_t nvalid = rem < uint64_t(kTileKeys) ? uint32_t(rem) : uint32_t(kTileKeys);
     for (uint32_t j = tid; j < nvalid; j += kSortThreads) {
         const KT k = sm.keys[j];
         const uint32_t d = uint32_t(k >> shift) & 255u;
@@ -159,7 +173,7 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass_kernel(
 
 // Sort (k0, v0) by bits [0, bits). Ping-pongs with (k1, v1); *which = buffer holding the result.
 // K lives on the device (n_keys); Kgrid >= K sizes the grids (exact in host-sync mode).
-template <class KT>
+template <class KT, int IPT = kSortItems>
 gs_status onesweep_sort_pairs(WsState* s, KT* k0, uint32_t* v0, KT* k1, uint32_t* v1, const unsigned long long* n_keys,
                               int64_t Kgrid, int bits, cudaStream_t st, int* which) {
     Misc* misc = at<Misc>(s, s->misc);
@@ -178,19 +192,19 @@ gs_status onesweep_sort_pairs(WsState* s, KT* k0, uint32_t* v0, KT* k1, uint32_t
         KTimer kt(s, KID_SORT_DSCAN, st);
         onesweep_digit_scan_kernel<<<npass, 256, 0, st>>>(hist);
     }
-    const size_t smem = sizeof(OnesweepSmem<KT>);
+    const size_t smem = sizeof(OnesweepSmem<KT, IPT>);
     static bool attr_set = false;   // idempotent attribute; benign race
     if (!attr_set) {
-        cudaFuncSetAttribute(onesweep_pass_kernel<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaFuncSetAttribute(onesweep_pass_kernel<KT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         attr_set = true;
     }
-    const int64_t parts = (Kgrid + kSortTile - 1) / kSortTile;
+    const int64_t parts = (Kgrid + kSortThreads * IPT - 1) / (kSortThreads * IPT);
     if (parts > s->max_parts) return GS_ERR_CAPACITY;
     KT* kin = k0; uint32_t* vin = v0; KT* ko = k1; uint32_t* vo = v1;
     for (int p = 0; p < npass; ++p) {
         const uint32_t epoch = uint32_t(++s->epoch) & 0x3fffffffu;
         KTimer kt(s, KID_SORT_PASS, st);
-        onesweep_pass_kernel<KT><<<int(parts), kSortThreads, smem, st>>>(
+        onesweep_pass_kernel<KT, IPT><<<int(parts), kSortThreads, smem, st>>>(
             kin, vin, ko, vo, n_keys, 8 * p, hist + 256 * p, at<unsigned long long>(s, s->sort_look),
             misc->sort_counter + p, epoch);
         std::swap(kin, ko);

@@ -480,16 +480,20 @@ constexpr int kPoseSums = 15;
 
 __global__ void __launch_bounds__(256) gaussian_bwd_kernel(
     const float* __restrict__ params, int64_t n, int64_t ld, const float* __restrict__ viewmat, gs_camera cam,
-    const uint32_t* __restrict__ tiles, const float4* __restrict__ rec, const float* __restrict__ sgrad, int64_t sld,
-    float* __restrict__ grad, int cov_path, double* __restrict__ pose_part) {
+    const uint32_t* __restrict__ onlist, const unsigned int* __restrict__ n_on, const float4* __restrict__ rec,
+    const float* __restrict__ sgrad, int64_t sld, float* __restrict__ grad, int cov_path,
+    double* __restrict__ pose_part) {
     __shared__ float V[12];
     if (threadIdx.x < 12) V[threadIdx.x] = viewmat[threadIdx.x];
     __syncthreads();
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    // thread t handles the t-th on-screen Gaussian (index order); off-screen ones have zero gradient
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool active = t < int64_t(*n_on);
+    const int64_t i = active ? int64_t(onlist[t]) : 0;
     float pose[kPoseSums];
 #pragma unroll
     for (int k = 0; k < kPoseSums; ++k) pose[k] = 0.f;
-    if (i < n && tiles[i] > 0) {
+    if (active && i < n) {
         float s[10];
 #pragma unroll
         for (int c = 0; c < 10; ++c) s[c] = sgrad[c * sld + i];
@@ -673,9 +677,11 @@ void launch_gaussian_bwd(WsState* s, const float* params, int64_t n, int64_t ld,
     const int blocks = int((n + 255) / 256);
     {
         KTimer kt(s, KID_BWD_GAUSS, st);
-        gaussian_bwd_kernel<<<blocks, 256, 0, st>>>(params, n, ld, viewmat, cam, at<uint32_t>(s, s->tiles),
-                                                    at<float4>(s, s->rec), at<float>(s, s->sgrad), s->n_cap,
-                                                    grad_params, (flags & GS_FLAG_POSE_COV_PATH) ? 1 : 0, part);
+        // grid sized by n (no host sync); blocks past V_s only write zero pose partials
+        gaussian_bwd_kernel<<<blocks, 256, 0, st>>>(params, n, ld, viewmat, cam, at<uint32_t>(s, s->onlist),
+                                                    &at<Misc>(s, s->misc)->n_onscreen, at<float4>(s, s->rec),
+                                                    at<float>(s, s->sgrad), s->n_cap, grad_params,
+                                                    (flags & GS_FLAG_POSE_COV_PATH) ? 1 : 0, part);
     }
     if (grad_pose) {
         KTimer kt(s, KID_POSE_FIN, st);
