@@ -210,6 +210,7 @@ def main_ours(args):
     K = fr.n_keys
     E_f = int(a["examined"].to(torch.int64).sum().item())
     E_b = int(a["n_last"].to(torch.int64).sum().item())
+    Lf, Lb = live_evals(a, cam)
     V_s = int((a["tiles"] > 0).sum().item())
     V_front = int((a["radius"] > 0).sum().item())
     del probe
@@ -263,6 +264,7 @@ def main_ours(args):
            "config": {"workload": f"config {args.config}: {cfg.name} {cam.width}x{cam.height}, {n} Gaussians, "
                                   f"fwd+bwd L1 (0.9/0.1) iteration", "n_gaussians": n, "width": cam.width,
                       "height": cam.height, "keys": K, "visible": V_front, "on_screen": V_s, "E_f": E_f, "E_b": E_b,
+                      "E_f_live": Lf, "E_b_live": Lb,
                       "binsort": args.binsort, "l2": "per-iteration working set > L2 (keys+values ~"
                       f"{K * 24 / 1e9:.2f} GB); no flush", "parallelism": f"replicas x{world}"},
            "evals_per_s": world * (E_f + E_b) * 1000.0 / ms, "clocks": clocks, "gpu_launches": int(launches)}
@@ -283,7 +285,7 @@ def main_ours(args):
         out["kernels_ms_per_step"] = {k: round(v_[0], 4) for k, v_ in sorted(per_step.items(), key=lambda x: -x[1][0])}
         out["kernels_launches_per_step"] = {k: v_[1] for k, v_ in per_step.items()}
         out["ms_per_step_with_event_log"] = ms_logged
-        out["roofline"] = roofline(per_step, clocks, K=K, n=n, V_s=V_s, E_f=E_f, E_b=E_b,
+        out["roofline"] = roofline(per_step, clocks, K=K, n=n, V_s=V_s, E_f=Lf, E_b=Lb,
                                    npx=cam.width * cam.height, binsort=args.binsort)
         # ---- e2e through the public API with host buffers (pinned) and a loss readback
         if not args.no_e2e:
@@ -350,6 +352,31 @@ def main_ours(args):
     if dist:
         dist.destroy_process_group()
     return 0
+
+
+def live_evals(a, cam):
+    """Pixel evaluations the render kernels perform: per pixel, the tile's live-list entries (those
+    that can reach alpha >= 1/255 in the tile) up to `examined` (forward) and up to
+    n_last (backward). These are the units of the render rows' algorithmic work."""
+    import torch
+    GX = (cam.width + 15) // 16
+    cnt = a["live_cnt"].to(torch.int64)
+    start = a["ranges"][:, 0].to(torch.int64)
+    T = cnt.numel()
+    dev = cnt.device
+    tid = torch.repeat_interleave(torch.arange(T, device=dev), cnt)
+    seg0 = torch.cumsum(cnt, 0) - cnt
+    off = torch.arange(tid.numel(), device=dev) - seg0[tid]
+    lj = a["live_j"][start[tid] + off].to(torch.int64) & 0xffffffff
+    key = (tid << 32) | lj                       # ascending: tiles in order, positions ascending
+    ys, xs = torch.meshgrid(torch.arange(cam.height, device=dev), torch.arange(cam.width, device=dev),
+                            indexing="ij")
+    ptile = ((ys // 16) * GX + xs // 16).to(torch.int64)
+
+    def count(upto):
+        q = (ptile << 32) | upto.to(torch.int64)
+        return int((torch.searchsorted(key, q.flatten(), right=True) - seg0[ptile.flatten()]).sum().item())
+    return count(a["examined"]), count(a["n_last"])
 
 
 def roofline(per_step, clocks, K, n, V_s, E_f, E_b, npx, binsort="bucket"):

@@ -198,6 +198,12 @@ typedef struct {
     const uint32_t* examined;    /* [H*W] (GS_FLAG_EXAMINED) */
     const uint64_t* n_keys_dev;  /* [1] K on the device */
     const uint32_t* error_flag;  /* [1] nonzero after a device-side capacity overflow */
+    /* live lists written by gs_render_fwd, walked by gs_render_bwd: for tile t, entries
+     * [ranges[t][0], ranges[t][0] + live_cnt[t]) hold (Gaussian, 1-based list position) of the
+     * list entries that can reach alpha >= 1/255 somewhere in the tile (ascending positions) */
+    const uint32_t* live_g;      /* [K] */
+    const uint32_t* live_j;      /* [K] */
+    const uint32_t* live_cnt;    /* [GX*GY] */
     int64_t n, key_cap, n_cap;
     int32_t grid_x, grid_y, width, height;
 } gs_ws_view;

@@ -46,7 +46,8 @@ class gs_ws_view(ctypes.Structure):
                 ("keys", ctypes.c_void_p),
                 ("vals", ctypes.c_void_p), ("ranges", ctypes.c_void_p), ("t_final", ctypes.c_void_p),
                 ("n_last", ctypes.c_void_p), ("examined", ctypes.c_void_p), ("n_keys_dev", ctypes.c_void_p),
-                ("error_flag", ctypes.c_void_p), ("n", ctypes.c_int64), ("key_cap", ctypes.c_int64),
+                ("error_flag", ctypes.c_void_p), ("live_g", ctypes.c_void_p), ("live_j", ctypes.c_void_p),
+                ("live_cnt", ctypes.c_void_p), ("n", ctypes.c_int64), ("key_cap", ctypes.c_int64),
                 ("n_cap", ctypes.c_int64), ("grid_x", ctypes.c_int32), ("grid_y", ctypes.c_int32),
                 ("width", ctypes.c_int32), ("height", ctypes.c_int32)]
 

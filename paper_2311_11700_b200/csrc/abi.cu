@@ -71,6 +71,7 @@ static void carve(WsState* s, Carver& c) {
     s->tile_tot = c.take(uint64_t(tiles) * 4 * 10);   // totals, starts, 8 segment sums
     s->pose_part = c.take(uint64_t((n + 255) / 256 + 1) * 16 * 8);   // per-block pose partials
     s->onlist = c.take(uint64_t(n) * 4);                              // on-screen Gaussians, index order
+    s->live_cnt = c.take(uint64_t(tiles) * 4);                        // per-tile live-list lengths
 }
 
 static bool ws_ok(const gs_ws* ws) { return ws && state(ws)->magic == kMagic; }
@@ -283,6 +284,11 @@ gs_status gs_ws_get_view(const gs_ws* ws, gs_ws_view* out) {
     out->examined = at<uint32_t>(s, s->examined);
     out->n_keys_dev = reinterpret_cast<const uint64_t*>(&misc->n_keys);
     out->error_flag = &misc->error_flag;
+    // live lists: the value / key buffers that do not hold the sorted list (render.cu live_bufs)
+    out->live_g = s->sorted_in_1 ? at<uint32_t>(s, s->vals0) : at<uint32_t>(s, s->vals1);
+    out->live_j = reinterpret_cast<const uint32_t*>(s->sorted_in_1 ? at<uint64_t>(s, s->keys0)
+                                                                   : at<uint64_t>(s, s->keys1));
+    out->live_cnt = at<uint32_t>(s, s->live_cnt);
     out->n = s->n;
     out->key_cap = s->key_cap;
     out->n_cap = s->n_cap;

@@ -15,6 +15,7 @@
 // are combined in shared memory and each (tile, Gaussian) issues one atomic per component
 // (block reduction before global atomics, north_star).
 #include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
 
 #include "gs_internal.cuh"
 
@@ -35,7 +36,8 @@ __global__ void __launch_bounds__(kTilePx) render_fwd_kernel(
     const float4* __restrict__ rec, const uint32_t* __restrict__ vals, const uint2* __restrict__ ranges, int W, int H,
     int GX, float bgr, float bgg, float bgb, float* __restrict__ color, float* __restrict__ depth,
     float* __restrict__ alpha, float* __restrict__ t_final, uint32_t* __restrict__ n_last, uint32_t* __restrict__ examined,
-    float* __restrict__ accum_weight) {
+    float* __restrict__ accum_weight, uint32_t* __restrict__ live_g, uint32_t* __restrict__ live_j,
+    uint32_t* __restrict__ live_cnt) {
     __shared__ float4 s_rec[2][kFwdBatch][3];
     const int tile = blockIdx.x;
     const int tx = tile % GX, ty = tile / GX;
@@ -51,10 +53,14 @@ __global__ void __launch_bounds__(kTilePx) render_fwd_kernel(
     uint32_t nl = 0, exam = len;
     bool done = !inside;
 
+    uint32_t staged = 0;   // this variant publishes every staged entry as live (no reach test)
     auto stage = [&](int b) {
         const uint32_t j = uint32_t(b) * kFwdBatch + threadIdx.x;
+        staged = min(len, uint32_t(b + 1) * kFwdBatch);
         if (j < len) {
             const uint32_t g = vals[start + j];
+            live_g[start + j] = g;
+            live_j[start + j] = j + 1;
             float4* dst = s_rec[b & 1][threadIdx.x];
             const float4* src = rec + 3 * size_t(g);
             cp_async16(dst + 0, src + 0);
@@ -126,6 +132,7 @@ __global__ void __launch_bounds__(kTilePx) render_fwd_kernel(
         }
         if (__syncthreads_and(done)) break;   // also orders buffer reuse
     }
+    if (threadIdx.x == 0) live_cnt[tile] = staged;
     if (inside) {
         const size_t pix = size_t(py) * W + px, plane = size_t(W) * H;
         const float cr = fmaf(T, bgr, Cr), cg = fmaf(T, bgg, Cg), cb = fmaf(T, bgb, Cb);
@@ -172,22 +179,57 @@ __device__ __forceinline__ void blend_step(PixState& p, float power, float4 r1, 
 
 constexpr int kFwd2Batch = kTilePx / 2;   // one staged record per thread
 
+// Can Gaussian (r0, r1) reach alpha >= 1/255 at any pixel of the box [x0, x1] x [y0, y1]? Conservative:
+// the quadratic form's minimum over the (continuous) box in fp64, with the fp32 evaluation error of
+// power bounded by 4e-6 of the terms' magnitude and a 1e-4 relative margin on alpha for the exp. A
+// "false" therefore guarantees that every per-pixel fp32 decision skips this Gaussian in this tile,
+// so dropping it changes no output.
+__device__ __forceinline__ bool can_reach(float4 r0, float4 r1, float x0, float y0, float x1, float y1) {
+    const double o = r1.y;
+    if (o * 255.0 * (1.0 - 1e-4) < 1.0) return false;   // alpha <= o everywhere
+    const double mx = r0.x, my = r0.y, a = -2.0 * double(r0.z), b = -double(r0.w), c = -2.0 * double(r1.x);
+    if (mx >= x0 && mx <= x1 && my >= y0 && my <= y1) return true;
+    auto q = [&](double dx, double dy) { return a * dx * dx + 2.0 * b * dx * dy + c * dy * dy; };
+    double qmin = 1e300;
+    for (int e = 0; e < 2; ++e) {   // vertical edges x = x0, x1: minimise over y in [y0, y1]
+        const double dx = mx - (e ? x1 : x0);
+        const double y = fmin(fmax(my + b * dx / c, double(y0)), double(y1));
+        qmin = fmin(qmin, q(dx, my - y));
+    }
+    for (int e = 0; e < 2; ++e) {   // horizontal edges y = y0, y1: minimise over x in [x0, x1]
+        const double dy = my - (e ? y1 : y0);
+        const double x = fmin(fmax(mx + b * dy / a, double(x0)), double(x1));
+        qmin = fmin(qmin, q(mx - x, dy));
+    }
+    const double dxm = fmax(fabs(mx - x0), fabs(mx - x1)), dym = fmax(fabs(my - y0), fabs(my - y1));
+    const double qmag = fabs(a) * dxm * dxm + 2.0 * fabs(b) * dxm * dym + fabs(c) * dym * dym;
+    return o * exp(-0.5 * qmin + 4e-6 * qmag + 1e-6) >= (1.0 / 255.0) * (1.0 - 1e-4);
+}
+
 __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
     const float4* __restrict__ rec, const uint32_t* __restrict__ vals, const uint2* __restrict__ ranges, int W, int H,
     int GX, float bgr, float bgg, float bgb, float* __restrict__ color, float* __restrict__ depth,
     float* __restrict__ alpha, float* __restrict__ t_final, uint32_t* __restrict__ n_last,
-    uint32_t* __restrict__ examined) {
+    uint32_t* __restrict__ examined, uint32_t* __restrict__ live_g, uint32_t* __restrict__ live_j,
+    uint32_t* __restrict__ live_cnt) {
+    using BS = cub::BlockScan<int, kFwd2Batch>;
+    __shared__ typename BS::TempStorage scan_tmp;
     __shared__ float4 s_rec[2][kFwd2Batch][3];
+    __shared__ uint32_t s_g[2][kFwd2Batch];
+    __shared__ int s_live[kFwd2Batch];
+    __shared__ int s_nlive;
     const int tile = blockIdx.x;
     const int tx = tile % GX, ty = tile / GX;
     const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;   // ly in [0, 8)
     const int px = tx * kTile + lx, pyA = ty * kTile + ly, pyB = pyA + 8;
     const bool inA = px < W && pyA < H, inB = px < W && pyB < H;
     const float fpx = float(px), fyA = float(pyA), fyB = float(pyB);
+    const float bx0 = float(tx * kTile), by0 = float(ty * kTile);
     const uint2 rg = ranges[tile];
     const uint32_t start = rg.x, len = rg.y - rg.x;
     const int nbatch = int((len + kFwd2Batch - 1) / kFwd2Batch);
     PixState A{1.f, 0.f, 0.f, 0.f, 0.f, 0u, len, !inA}, B{1.f, 0.f, 0.f, 0.f, 0.f, 0u, len, !inB};
+    uint32_t acc = 0;   // live entries written so far (this tile)
 
     auto stage = [&](int b) {
         const int slot = threadIdx.x;
@@ -195,6 +237,7 @@ __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
         float4* dst = s_rec[b & 1][slot];
         if (j < len) {
             const uint32_t g = vals[start + j];
+            s_g[b & 1][slot] = g;
             const float4* src = rec + 3 * size_t(g);
             cp_async16(dst + 0, src + 0);
             cp_async16(dst + 1, src + 1);
@@ -218,13 +261,33 @@ __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
         __syncthreads();
         const int cnt = min(kFwd2Batch, int(len) - b * kFwd2Batch);
         const float4(*buf)[3] = s_rec[b & 1];
-        constexpr int kU = 4;                   // Gaussians per early-exit check
-        for (int k0 = 0; k0 < cnt; k0 += kU) {  // slots past cnt are zero-opacity pads (< kFwd2Batch)
+        // ordered compaction of the batch's Gaussians that can reach alpha >= 1/255 in this tile;
+        // the live list (Gaussian, 1-based list position) is also what the backward walks
+        {
+            const int k = threadIdx.x;
+            const int lv = (k < cnt && can_reach(buf[k][0], buf[k][1], bx0, by0, bx0 + 15.f, by0 + 15.f)) ? 1 : 0;
+            int off, tot;
+            BS(scan_tmp).ExclusiveSum(lv, off, tot);
+            if (lv) {
+                s_live[off] = k;
+                live_g[start + acc + off] = s_g[b & 1][k];
+                live_j[start + acc + off] = uint32_t(b * kFwd2Batch + k + 1);
+            }
+            if (k == 0) s_nlive = tot;
+            __syncthreads();
+        }
+        const int nlive = s_nlive;
+        acc += uint32_t(nlive);
+        constexpr int kU = 4;                        // Gaussians per early-exit check
+        for (int k0 = 0; k0 < nlive; k0 += kU) {
             if (A.done && B.done) break;
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
-                const int k = k0 + u;
-                const float4 r0 = buf[k][0], r1 = buf[k][1], r2 = buf[k][2];
+                // past nlive: re-read slot 0 with zero opacity so the unrolled body stays branch-free
+                const bool real = k0 + u < nlive;
+                const int k = real ? s_live[k0 + u] : 0;
+                float4 r0 = buf[k][0], r1 = buf[k][1], r2 = buf[k][2];
+                if (!real) r1.y = 0.f;   // zero opacity -> alpha 0 -> skipped exactly
                 const uint32_t j = uint32_t(b * kFwd2Batch + k + 1);
                 // same operation sequence as eval_alpha, x-terms shared between the two pixels
                 const float dx = __fsub_rn(r0.x, fpx);
@@ -238,6 +301,7 @@ __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
         }
         if (__syncthreads_and(A.done && B.done)) break;   // also orders buffer reuse
     }
+    if (threadIdx.x == 0) live_cnt[tile] = acc;
     const size_t plane = size_t(W) * H;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -255,22 +319,36 @@ __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
     }
 }
 
+// Per-tile live lists written by the forward and walked by the backward: (Gaussian, 1-based list
+// position) of every entry that can reach alpha >= 1/255 in the tile, at [ranges[t].x, + live_cnt[t]).
+// They live in the value / key buffers that do not hold the sorted lists.
+struct LiveBufs {
+    uint32_t *g, *j, *cnt;
+};
+static LiveBufs live_bufs(WsState* s) {
+    uint32_t* g = s->sorted_in_1 ? at<uint32_t>(s, s->vals0) : at<uint32_t>(s, s->vals1);
+    uint32_t* j = reinterpret_cast<uint32_t*>(s->sorted_in_1 ? at<uint64_t>(s, s->keys0) : at<uint64_t>(s, s->keys1));
+    return {g, j, at<uint32_t>(s, s->live_cnt)};
+}
+
 void launch_render_fwd(WsState* s, const gs_camera& cam, float* color, float* depth, float* alpha,
                        float* accum_weight, uint32_t flags, cudaStream_t st) {
     const int ntiles = s->cam_gx * s->cam_gy;
     const uint32_t* sorted_vals = s->sorted_in_1 ? at<uint32_t>(s, s->vals1) : at<uint32_t>(s, s->vals0);
     uint32_t* exam = (flags & GS_FLAG_EXAMINED) ? at<uint32_t>(s, s->examined) : nullptr;
+    const LiveBufs lb = live_bufs(s);
     if (ntiles == 0) return;
     KTimer kt(s, KID_FWD, st);
     if ((flags & GS_FLAG_ACCUM_WEIGHT) && accum_weight) {
         render_fwd_kernel<true><<<ntiles, kTilePx, 0, st>>>(
             at<float4>(s, s->rec), sorted_vals, at<uint2>(s, s->ranges), cam.width, cam.height, s->cam_gx, cam.bg[0],
             cam.bg[1], cam.bg[2], color, depth, alpha, at<float>(s, s->t_final), at<uint32_t>(s, s->n_last), exam,
-            accum_weight);
+            accum_weight, lb.g, lb.j, lb.cnt);
     } else {
         render_fwd2_kernel<<<ntiles, kTilePx / 2, 0, st>>>(
             at<float4>(s, s->rec), sorted_vals, at<uint2>(s, s->ranges), cam.width, cam.height, s->cam_gx, cam.bg[0],
-            cam.bg[1], cam.bg[2], color, depth, alpha, at<float>(s, s->t_final), at<uint32_t>(s, s->n_last), exam);
+            cam.bg[1], cam.bg[2], color, depth, alpha, at<float>(s, s->t_final), at<uint32_t>(s, s->n_last), exam,
+            lb.g, lb.j, lb.cnt);
     }
 }
 
@@ -287,11 +365,14 @@ struct BwdSmem {
     float part[kParts][10][kBB];   // per (warp, half) pixel moments
     float red[10][kBB];            // combined moments
     uint32_t idx[2][kBB];
+    uint32_t pos[2][kBB];          // 1-based list positions of the staged live entries
     uint32_t max_nl;
+    uint32_t len;
 };
 
 __global__ void __launch_bounds__(kTilePx, 4) render_bwd_kernel(
-    const float4* __restrict__ rec, const uint32_t* __restrict__ vals, const uint2* __restrict__ ranges, int W, int H,
+    const float4* __restrict__ rec, const uint32_t* __restrict__ live_g, const uint32_t* __restrict__ live_j,
+    const uint32_t* __restrict__ live_cnt, const uint2* __restrict__ ranges, int W, int H,
     int GX, const float* __restrict__ t_final, float bgr, float bgg, float bgb, const uint32_t* __restrict__ n_last,
     const float* __restrict__ dLdC, const float* __restrict__ dLdD, float* __restrict__ sgrad, int64_t sld) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -321,16 +402,35 @@ __global__ void __launch_bounds__(kTilePx, 4) render_bwd_kernel(
     __syncthreads();
     if (nl) atomicMax(&sm.max_nl, nl);
     __syncthreads();
-    const uint32_t len = sm.max_nl;
+    // the live entries to walk: those with list position <= max n_last (positions ascend), found by
+    // one warp with a 32-ary search over the forward's live list
+    if (warp == 0) {
+        const uint32_t mx = sm.max_nl;
+        uint32_t lo = 0, hi = live_cnt[tile];   // answer in [lo, hi]
+        while (hi > lo) {
+            const uint32_t step = (hi - lo + 31) / 32;
+            const uint32_t probe = lo + uint32_t(lane) * step;   // is entry `probe` within max n_last?
+            const bool in = probe < hi && live_j[start + probe] <= mx;
+            const unsigned m = __ballot_sync(0xffffffffu, in);
+            if (m == 0u) { hi = lo; break; }
+            const uint32_t last = lo + uint32_t(31 - __clz(m)) * step;   // last probe within
+            lo = last + 1;
+            hi = min(hi, last + step);
+        }
+        if (lane == 0) sm.len = lo;
+    }
+    __syncthreads();
+    const uint32_t len = sm.len;
     const int nbatch = int((len + kBB - 1) / kBB);
 
-    // batch bb holds list positions [bb*16, bb*16+16); batches are visited back to front
+    // batch bb holds live entries [bb*16, bb*16+16); batches are visited back to front
     auto stage = [&](int bb, int slot) {
         if (tid < kBB) {
             const uint32_t j = uint32_t(bb) * kBB + tid;
             if (j < len) {
-                const uint32_t g = vals[start + j];
+                const uint32_t g = live_g[start + j];
                 sm.idx[slot][tid] = g;
+                sm.pos[slot][tid] = live_j[start + j];
                 float4* dst = sm.rec[slot][tid];
                 const float4* src = rec + 3 * size_t(g);
                 cp_async16(dst + 0, src + 0);
@@ -358,11 +458,10 @@ __global__ void __launch_bounds__(kTilePx, 4) render_bwd_kernel(
         const int cnt = min(kBB, int(len) - bb * kBB);
         // ---- phase 1: thread = pixel, back to front over the batch (3DGS-style recurrence):
         //      T_i = T_{i+1} / (1 - alpha_i);  dL/dalpha_i = T_i e_i - (S_i + T_f bg.dL/dC) / (1 - alpha_i)
-        const uint32_t base_pos = uint32_t(bb * kBB);
 #pragma unroll 4
         for (int k = kBB - 1; k >= 0; --k) {
             float w = 0.f, go = 0.f;
-            if (k < cnt && base_pos + k + 1 <= nl) {   // pixels past their n_last skip the work
+            if (k < cnt && sm.pos[buf][k] <= nl) {   // pixels past their n_last skip the work
                 const float4 r0 = sm.rec[buf][k][0], r1 = sm.rec[buf][k][1];
                 const AlphaEval e = eval_alpha(r0, r1, fpx, fpy);
                 if (e.alpha != 0.f) {
@@ -460,7 +559,7 @@ void launch_render_bwd_tiles(WsState* s, const gs_camera& cam, const float*, con
                              const float* dL_ddepth, cudaStream_t st) {
     const int ntiles = s->cam_gx * s->cam_gy;
     if (ntiles == 0) return;
-    const uint32_t* sorted_vals = s->sorted_in_1 ? at<uint32_t>(s, s->vals1) : at<uint32_t>(s, s->vals0);
+    const LiveBufs lb = live_bufs(s);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(render_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem)));
@@ -468,7 +567,7 @@ void launch_render_bwd_tiles(WsState* s, const gs_camera& cam, const float*, con
     }
     KTimer kt(s, KID_BWD_TILE, st);
     render_bwd_kernel<<<ntiles, kTilePx, sizeof(BwdSmem), st>>>(
-        at<float4>(s, s->rec), sorted_vals, at<uint2>(s, s->ranges), cam.width, cam.height, s->cam_gx,
+        at<float4>(s, s->rec), lb.g, lb.j, lb.cnt, at<uint2>(s, s->ranges), cam.width, cam.height, s->cam_gx,
         at<float>(s, s->t_final), cam.bg[0], cam.bg[1], cam.bg[2], at<uint32_t>(s, s->n_last), dL_dcolor, dL_ddepth,
         at<float>(s, s->sgrad), s->n_cap);
 }

@@ -95,9 +95,12 @@ class RenderPipeline:
                    t_final=t(v.t_final, npx, torch.float32).view(v.height, v.width),
                    n_last=t(v.n_last, npx, torch.int32).view(v.height, v.width),
                    examined=t(v.examined, npx, torch.int32).view(v.height, v.width),
-                   n_keys_dev=t(v.n_keys_dev, 1, torch.int64), error_flag=t(v.error_flag, 1, torch.int32))
+                   n_keys_dev=t(v.n_keys_dev, 1, torch.int64), error_flag=t(v.error_flag, 1, torch.int32),
+                   live_cnt=t(v.live_cnt, ntiles, torch.int32))
         if K is not None and K >= 0:
             if v.keys:   # path A only (path B never materialises the 64-bit keys)
                 out["keys"] = t(v.keys, K, torch.int64)
             out["vals"] = t(v.vals, K, torch.int32)
+            out["live_g"] = t(v.live_g, K, torch.int32)
+            out["live_j"] = t(v.live_j, K, torch.int32)
         return out

@@ -85,6 +85,53 @@ def test_forward_parity(c):
     assert torch.allclose(1 - fr.alpha, a["t_final"], atol=1e-6)
 
 
+@pytest.mark.parametrize("c", CFGS)
+def test_live_lists_valid_and_complete(c):
+    """The forward's per-tile live lists are an ordered sub-list of the tile list,
+    and conservative: every entry up to the tile's last examined position whose fp64 alpha reaches
+    1/255 at some pixel of the tile box is listed (the kernel's test keeps a 1e-4 margin below that)."""
+    cfg, p, v = scene(c)
+    pipe, P, V, fr = run_forward(p, v, cfg.cam)
+    a = pipe.arrays(p.shape[1])
+    vals = a["vals"].cpu().numpy().view(np.uint32)
+    lg = a["live_g"].cpu().numpy().view(np.uint32)
+    lj = a["live_j"].cpu().numpy().view(np.uint32).astype(np.int64)
+    cnt = a["live_cnt"].cpu().numpy().astype(np.int64)
+    rg = a["ranges"].cpu().numpy().view(np.uint32).astype(np.int64)
+    rec = a["records"].cpu().numpy().astype(np.float64)
+    ex = a["examined"].cpu().numpy()
+    GX, GY = (cfg.cam.width + 15) // 16, (cfg.cam.height + 15) // 16
+    rng = np.random.default_rng(c)
+    tiles = np.arange(GX * GY) if c < 2 else rng.choice(GX * GY, 48, replace=False)
+    ly, lx = np.meshgrid(np.arange(16.0), np.arange(16.0), indexing="ij")
+    listed = total = 0
+    for t in tiles:
+        s, e = rg[t]
+        n_t, k = e - s, cnt[t]
+        assert 0 <= k <= n_t
+        j = lj[s:s + k]
+        assert np.all(np.diff(j) > 0) and (k == 0 or (j[0] >= 1 and j[-1] <= n_t))
+        assert np.array_equal(lg[s:s + k], vals[s + j - 1])
+        ty, tx = divmod(int(t), GX)
+        exm = ex[ty * 16:(ty + 1) * 16, tx * 16:(tx + 1) * 16]
+        upto = int(exm.max()) if exm.size else 0
+        if upto == 0:
+            continue
+        r = rec[vals[s:s + upto]]
+        dx = r[:, 0, None, None] - (tx * 16 + lx)[None]
+        dy = r[:, 1, None, None] - (ty * 16 + ly)[None]
+        power = r[:, 2, None, None] * dx * dx + r[:, 3, None, None] * dx * dy + r[:, 4, None, None] * dy * dy
+        alpha = np.minimum(0.99, r[:, 5, None, None] * np.exp(np.minimum(power, 0.0)))
+        amax = alpha.reshape(upto, -1).max(1)
+        need = np.flatnonzero(amax >= 1 / 255) + 1
+        miss = np.setdiff1d(need, j)
+        assert miss.size == 0, (t, miss[:8], amax[miss[:8] - 1] * 255)
+        listed += int((j <= upto).sum())
+        total += upto
+    if c == 2:   # the skip is what makes the list worth having at the bench workload
+        assert listed < 0.8 * total, (listed, total)
+
+
 def test_forward_sampled_pixels_match_full_oracle_cfg2():
     """Full-size config 2 in the bench launch configuration: sampled pixels, oracle one by one."""
     cfg, p, v = scene(2)
