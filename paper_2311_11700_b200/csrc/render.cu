@@ -353,24 +353,63 @@ void launch_render_fwd(WsState* s, const gs_camera& cam, float* color, float* de
 }
 
 // ------------------------------------------------------------------ backward, tile pass
-constexpr int kBB = 16;                 // Gaussians per backward batch
-constexpr int kWarps = kTilePx / 32;
-constexpr int kParts = kWarps * 2;      // phase-2 partial sets: (warp, row half)
+// One CTA of 128 threads per tile; each thread owns two pixels (rows ly and ly + 8), so the record
+// loads and the x-terms of power are shared between them (same operation order as eval_alpha, so
+// every decision is bit-identical to the forward's). Live-list entries (§5.3) are processed in
+// batches of kBB, back to front:
+//   phase 1  thread = 2 pixels: T_i = T_{i+1} / (1 - alpha_i), suffix sum S, and
+//            (alpha_i T_i, G dL/dalpha_i) per (pixel, Gaussian) into shared memory (branch-free:
+//            after the live-list skip ~97 % of the walked evaluations blend at config 2)
+//   phase 2  lane = (Gaussian, row group): pixel moments with compile-time x
+//   combine  the row-group partial sets, then one thread per (component, Gaussian) turns moments
+//            into the screen-space gradient and issues its atomic.
+// The staged batches rotate through 3 slots, so a batch needs 4 block barriers and none at its end.
+constexpr int kBB = 16;                          // Gaussians per backward batch
+constexpr int kBwdThreads = kTilePx / 2;         // 128
+constexpr int kBwdWarps = kBwdThreads / 32;
+constexpr int kGroups = kBwdWarps * (32 / kBB);  // phase-2 row groups (= partial sets)
+constexpr int kRowsPerGroup = kTile / kGroups;
+constexpr int kSlots = 3;
+static_assert(kTile % kGroups == 0, "row groups must tile the 16 rows");
 
 struct BwdSmem {
-    float4 rec[2][kBB][3];
-    float w[kTilePx][kBB + 1];     // alpha_i T_i          (row stride 17: conflict-free both ways)
-    float go[kTilePx][kBB + 1];    // G dL/dalpha_i        (0 when clamped or skipped)
+    float4 rec[kSlots][kBB][3];
+    float2 wg[kTilePx][kBB + 1];   // (alpha_i T_i, G dL/dalpha_i); 0 when skipped or clamped
     float4 dl[kTilePx];            // dL/dC (r,g,b), dL/dD per pixel
-    float part[kParts][10][kBB];   // per (warp, half) pixel moments
+    float part[kGroups][10][kBB];  // per row-group pixel moments
     float red[10][kBB];            // combined moments
-    uint32_t idx[2][kBB];
-    uint32_t pos[2][kBB];          // 1-based list positions of the staged live entries
-    uint32_t max_nl;
-    uint32_t len;
+    uint32_t idx[kSlots][kBB];
+    uint32_t pos[kSlots][kBB];     // 1-based list positions of the staged live entries (~0u: padding)
+    uint32_t max_nl, len;
 };
 
-__global__ void __launch_bounds__(kTilePx, 4) render_bwd_kernel(
+struct BwdPix {
+    float T, S, tfb;   // T_{i+1} while walking back (starts at T_final), suffix sum, T_f bg.dL/dC
+    float4 dl;
+    uint32_t nl;
+};
+
+// One back-to-front step for one pixel; power in eval_alpha's order. A skipped entry (past n_last,
+// power > 0, alpha < 1/255, or padding) leaves T and S bitwise unchanged and yields (0, 0).
+__device__ __forceinline__ float2 bwd_step(BwdPix& p, float power, float4 r1, float4 r2, uint32_t pk) {
+    float G;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(G) : "f"(__fmul_rn(power, 1.4426950408889634f)));
+    const float og = __fmul_rn(r1.y, G);
+    const float a0 = fminf(0.99f, og);
+    const bool live = pk <= p.nl && !(power > 0.f) && a0 >= (1.0f / 255.0f);
+    const float a = live ? a0 : 0.f;
+    float ro;   // 1/(1 - alpha): MUFU rcp.approx (<= 1 ulp; gradients only, no decision)
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ro) : "f"(__fsub_rn(1.f, a)));
+    p.T = live ? p.T * ro : p.T;
+    const float w = a * p.T;
+    const float ev = fmaf(r2.x, p.dl.x, fmaf(r2.y, p.dl.y, fmaf(r2.z, p.dl.z, r1.z * p.dl.w)));
+    const float ga = fmaf(p.T, ev, -(p.S + p.tfb) * ro);   // dL/dalpha_i
+    const float go = (live && !(og > 0.99f)) ? G * ga : 0.f;
+    p.S = fmaf(w, ev, p.S);   // w == 0 when skipped: S unchanged (ev finite; padding is zero-filled)
+    return make_float2(w, go);
+}
+
+__global__ void __launch_bounds__(kBwdThreads, 4) render_bwd_kernel(
     const float4* __restrict__ rec, const uint32_t* __restrict__ live_g, const uint32_t* __restrict__ live_j,
     const uint32_t* __restrict__ live_cnt, const uint2* __restrict__ ranges, int W, int H,
     int GX, const float* __restrict__ t_final, float bgr, float bgg, float bgb, const uint32_t* __restrict__ n_last,
@@ -380,27 +419,35 @@ __global__ void __launch_bounds__(kTilePx, 4) render_bwd_kernel(
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tile = blockIdx.x;
     const int tx = tile % GX, ty = tile / GX;
-    const int lx = tid & 15, ly = tid >> 4;
-    const int px = tx * kTile + lx, py = ty * kTile + ly;
-    const bool inside = px < W && py < H;
-    const float fpx = float(px), fpy = float(py);
-    const uint2 rg = ranges[tile];
-    const uint32_t start = rg.x;
-    const size_t pix = size_t(py) * W + px, plane = size_t(W) * H;
+    const int lx = tid & 15, ly = tid >> 4;   // ly in [0, 8)
+    const int px = tx * kTile + lx, pyA = ty * kTile + ly, pyB = pyA + 8;
+    const float fpx = float(px), fyA = float(pyA), fyB = float(pyB);
+    const uint32_t start = ranges[tile].x;
+    const size_t plane = size_t(W) * H;
 
-    uint32_t nl = 0;
-    float4 dl = make_float4(0.f, 0.f, 0.f, 0.f);
-    float T = 1.f;   // T_{i+1} while walking back; starts at T_final
-    if (inside) {
-        nl = n_last[pix];
-        dl = make_float4(dLdC[pix], dLdC[plane + pix], dLdC[2 * plane + pix], dLdD[pix]);
-        T = t_final[pix];
-    }
-    const float tfb = T * (bgr * dl.x + bgg * dl.y + bgb * dl.z);   // T_f bg . dL/dC
+    auto load_pix = [&](BwdPix& p, int py, int q) {
+        p.nl = 0;
+        p.dl = make_float4(0.f, 0.f, 0.f, 0.f);
+        p.T = 1.f;
+        p.S = 0.f;
+        if (px < W && py < H) {
+            const size_t pix = size_t(py) * W + px;
+            p.nl = n_last[pix];
+            p.dl = make_float4(dLdC[pix], dLdC[plane + pix], dLdC[2 * plane + pix], dLdD[pix]);
+            p.T = t_final[pix];
+        }
+        p.tfb = p.T * (bgr * p.dl.x + bgg * p.dl.y + bgb * p.dl.z);
+        sm.dl[q] = p.dl;
+    };
+    BwdPix A, B;
     if (tid == 0) sm.max_nl = 0;
-    sm.dl[tid] = dl;
+    load_pix(A, pyA, tid);
+    load_pix(B, pyB, tid + kBwdThreads);
     __syncthreads();
-    if (nl) atomicMax(&sm.max_nl, nl);
+    uint32_t mnl = max(A.nl, B.nl);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mnl = max(mnl, __shfl_xor_sync(0xffffffffu, mnl, o));
+    if (lane == 0 && mnl) atomicMax(&sm.max_nl, mnl);
     __syncthreads();
     // the live entries to walk: those with list position <= max n_last (positions ascend), found by
     // one warp with a 32-ary search over the forward's live list
@@ -423,135 +470,137 @@ __global__ void __launch_bounds__(kTilePx, 4) render_bwd_kernel(
     const uint32_t len = sm.len;
     const int nbatch = int((len + kBB - 1) / kBB);
 
-    // batch bb holds live entries [bb*16, bb*16+16); batches are visited back to front
+    // batch bb holds live entries [bb*kBB, bb*kBB+kBB); batches are visited back to front
     auto stage = [&](int bb, int slot) {
         if (tid < kBB) {
             const uint32_t j = uint32_t(bb) * kBB + tid;
+            float4* dst = sm.rec[slot][tid];
             if (j < len) {
                 const uint32_t g = live_g[start + j];
                 sm.idx[slot][tid] = g;
                 sm.pos[slot][tid] = live_j[start + j];
-                float4* dst = sm.rec[slot][tid];
                 const float4* src = rec + 3 * size_t(g);
                 cp_async16(dst + 0, src + 0);
                 cp_async16(dst + 1, src + 1);
                 cp_async16(dst + 2, src + 2);
+            } else {   // padding: never live, zero record keeps every product finite
+                const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                sm.idx[slot][tid] = 0u;
+                sm.pos[slot][tid] = 0xffffffffu;
+                dst[0] = z;
+                dst[1] = z;
+                dst[2] = z;
             }
         }
         cp_async_commit();
     };
 
-    // phase-2 lane roles: Gaussian k2 of the batch, pixel row ly2 = 2 warp + half
-    const int k2 = lane & (kBB - 1), half = lane >> 4, ly2 = 2 * warp + half;
-    float S = 0.f;   // sum_{k>i} alpha_k T_k e_k  (suffix sum, accumulated from the back)
+    // phase-2 lane roles: Gaussian k2 of the batch, row group gi (rows gi + kGroups r)
+    const int k2 = lane & (kBB - 1), gi = warp * (32 / kBB) + lane / kBB;
     if (nbatch > 0) stage(nbatch - 1, 0);
     for (int it = 0; it < nbatch; ++it) {
         const int bb = nbatch - 1 - it;
+        const int buf = it % kSlots;
         if (it + 1 < nbatch) {
-            stage(bb - 1, (it + 1) & 1);
+            stage(bb - 1, (it + 1) % kSlots);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
-        __syncthreads();
-        const int buf = it & 1;
-        const int cnt = min(kBB, int(len) - bb * kBB);
-        // ---- phase 1: thread = pixel, back to front over the batch (3DGS-style recurrence):
-        //      T_i = T_{i+1} / (1 - alpha_i);  dL/dalpha_i = T_i e_i - (S_i + T_f bg.dL/dC) / (1 - alpha_i)
+        __syncthreads();   // [A] batch staged
+        // ---- phase 1
 #pragma unroll 4
         for (int k = kBB - 1; k >= 0; --k) {
-            float w = 0.f, go = 0.f;
-            if (k < cnt && sm.pos[buf][k] <= nl) {   // pixels past their n_last skip the work
-                const float4 r0 = sm.rec[buf][k][0], r1 = sm.rec[buf][k][1];
-                const AlphaEval e = eval_alpha(r0, r1, fpx, fpy);
-                if (e.alpha != 0.f) {
-                    const float4 r2 = sm.rec[buf][k][2];
-                    const float ev = fmaf(r2.x, dl.x, fmaf(r2.y, dl.y, fmaf(r2.z, dl.z, r1.z * dl.w)));
-                    float ro;   // 1/(1 - alpha): MUFU rcp.approx (<= 1 ulp; gradients only, no decision)
-                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ro) : "f"(__fsub_rn(1.f, e.alpha)));
-                    T = T * ro;
-                    w = e.alpha * T;
-                    const float ga = fmaf(T, ev, -(S + tfb) * ro);
-                    go = e.clamped ? 0.f : e.G * ga;
-                    S = fmaf(w, ev, S);
-                }
-            }
-            sm.w[tid][k] = w;
-            sm.go[tid][k] = go;
+            const uint32_t pk = sm.pos[buf][k];
+            const float4 r0 = sm.rec[buf][k][0], r1 = sm.rec[buf][k][1], r2 = sm.rec[buf][k][2];
+            const float dx = __fsub_rn(r0.x, fpx);
+            const float Adx = __fmul_rn(r0.z, dx), Bdx = __fmul_rn(r0.w, dx);
+            const float dyA = __fsub_rn(r0.y, fyA), dyB = __fsub_rn(r0.y, fyB);
+            const float pA = __fmaf_rn(Adx, dx, __fmaf_rn(__fmul_rn(r1.x, dyA), dyA, __fmul_rn(Bdx, dyA)));
+            const float pB = __fmaf_rn(Adx, dx, __fmaf_rn(__fmul_rn(r1.x, dyB), dyB, __fmul_rn(Bdx, dyB)));
+            sm.wg[tid][k] = bwd_step(A, pA, r1, r2, pk);
+            sm.wg[tid + kBwdThreads][k] = bwd_step(B, pB, r1, r2, pk);
         }
-        __syncthreads();
-        // ---- phase 2: lane = (Gaussian k2, row ly2); moments over the row's 16 pixels with
-        //      compile-time x coordinates; y moments follow from the lane's constant row
+        __syncthreads();   // [B] wg complete
+        // ---- phase 2: moments over the group's rows, 16 pixels each, compile-time x
         {
-            float S0 = 0.f, Sx = 0.f, Sxx = 0.f, Sr = 0.f, Sg = 0.f, Sb = 0.f, Sd = 0.f;
+            float S0 = 0.f, Sx = 0.f, Sxx = 0.f, Sy = 0.f, Sxy = 0.f, Syy = 0.f;
+            float Sr = 0.f, Sg = 0.f, Sb = 0.f, Sd = 0.f;
 #pragma unroll
-            for (int x = 0; x < 16; ++x) {
-                const int q = ly2 * 16 + x;
-                const float g = sm.go[q][k2], w = sm.w[q][k2];
-                const float4 d = sm.dl[q];
-                S0 += g;
-                Sx = fmaf(g, float(x), Sx);
-                Sxx = fmaf(g, float(x * x), Sxx);
-                Sr = fmaf(w, d.x, Sr);
-                Sg = fmaf(w, d.y, Sg);
-                Sb = fmaf(w, d.z, Sb);
-                Sd = fmaf(w, d.w, Sd);
+            for (int r = 0; r < kRowsPerGroup; ++r) {
+                const int row = gi + kGroups * r;
+                float R0 = 0.f, Rx = 0.f, Rxx = 0.f;
+#pragma unroll
+                for (int x = 0; x < 16; ++x) {
+                    const int q = row * 16 + x;
+                    const float2 v = sm.wg[q][k2];
+                    const float4 d = sm.dl[q];
+                    R0 += v.y;
+                    Rx = fmaf(v.y, float(x), Rx);
+                    Rxx = fmaf(v.y, float(x * x), Rxx);
+                    Sr = fmaf(v.x, d.x, Sr);
+                    Sg = fmaf(v.x, d.y, Sg);
+                    Sb = fmaf(v.x, d.z, Sb);
+                    Sd = fmaf(v.x, d.w, Sd);
+                }
+                const float fy = float(row);
+                S0 += R0;
+                Sx += Rx;
+                Sxx += Rxx;
+                Sy = fmaf(fy, R0, Sy);
+                Sxy = fmaf(fy, Rx, Sxy);
+                Syy = fmaf(fy * fy, R0, Syy);
             }
-            const float fy = float(ly2);
-            float* pp = &sm.part[warp * 2 + half][0][k2];
-            pp[0 * kBB] = S0;            // sum g
-            pp[1 * kBB] = Sx;            // sum g lx
-            pp[2 * kBB] = fy * S0;       // sum g ly
-            pp[3 * kBB] = Sxx;           // sum g lx^2
-            pp[4 * kBB] = fy * Sx;       // sum g lx ly
-            pp[5 * kBB] = fy * fy * S0;  // sum g ly^2
+            float* pp = &sm.part[gi][0][k2];
+            pp[0 * kBB] = S0;    // sum g
+            pp[1 * kBB] = Sx;    // sum g lx
+            pp[2 * kBB] = Sy;    // sum g ly
+            pp[3 * kBB] = Sxx;   // sum g lx^2
+            pp[4 * kBB] = Sxy;   // sum g lx ly
+            pp[5 * kBB] = Syy;   // sum g ly^2
             pp[6 * kBB] = Sr;
             pp[7 * kBB] = Sg;
             pp[8 * kBB] = Sb;
             pp[9 * kBB] = Sd;
         }
-        __syncthreads();
-        // ---- combine the 16 partial sets (160 threads: one (component, Gaussian) each)
-        if (tid < 10 * kBB) {
-            const int c = tid / kBB, k = tid % kBB;
+        __syncthreads();   // [C] partial sets complete
+        for (int t = tid; t < 10 * kBB; t += kBwdThreads) {
+            const int c = t / kBB, k = t % kBB;
             float a = 0.f;
 #pragma unroll
-            for (int p = 0; p < kParts; ++p) a += sm.part[p][c][k];
+            for (int p = 0; p < kGroups; ++p) a += sm.part[p][c][k];
             sm.red[c][k] = a;
         }
-        __syncthreads();
-        // ---- moments -> screen-space gradients; one atomic per (tile, Gaussian, component)
-        if (tid < cnt) {
-            const float* Mo = &sm.red[0][tid];
-            const float M0 = Mo[0], Mx = Mo[kBB], My = Mo[2 * kBB], Mxx = Mo[3 * kBB], Mxy = Mo[4 * kBB],
-                        Myy = Mo[5 * kBB];
-            const float4 r0 = sm.rec[buf][tid][0], r1 = sm.rec[buf][tid][1];
-            const float o = r1.y;
-            const float X = r0.x - float(tx * kTile), Y = r0.y - float(ty * kTile);
-            // sums of g dx, g dy, g dx^2, g dx dy, g dy^2 with dx = X - lx, dy = Y - ly
-            const float gdx = X * M0 - Mx;
-            const float gdy = Y * M0 - My;
-            const float gdxx = X * X * M0 - 2.f * X * Mx + Mxx;
-            const float gdxy = X * Y * M0 - X * My - Y * Mx + Mxy;
-            const float gdyy = Y * Y * M0 - 2.f * Y * My + Myy;
-            const float A = r0.z, B = r0.w, C = r1.x;   // A = -a/2, B = -b, C = -c/2
-            float out[10];
-            out[0] = o * (2.f * A * gdx + B * gdy);   // mean2d x:  -o (a gdx + b gdy)
-            out[1] = o * (B * gdx + 2.f * C * gdy);   // mean2d y:  -o (b gdx + c gdy)
-            out[2] = -0.5f * o * gdxx;                // conic a
-            out[3] = -o * gdxy;                       // conic b
-            out[4] = -0.5f * o * gdyy;                // conic c
-            out[5] = M0;                              // opacity
-            out[6] = Mo[6 * kBB];
-            out[7] = Mo[7 * kBB];
-            out[8] = Mo[8 * kBB];                     // rgb
-            out[9] = Mo[9 * kBB];                     // depth
-            const uint32_t g = sm.idx[buf][tid];
-#pragma unroll
-            for (int c = 0; c < 10; ++c)
-                if (out[c] != 0.f) atomicAdd(sgrad + c * sld + g, out[c]);
+        __syncthreads();   // [D] moments complete
+        // ---- moments -> screen-space gradients; one thread and one atomic per (component, Gaussian)
+        const int cnt = min(kBB, int(len) - bb * kBB);
+        for (int t = tid; t < 10 * kBB; t += kBwdThreads) {
+            const int c = t / kBB, k = t % kBB;
+            if (k >= cnt) continue;
+            float v;
+            if (c >= 5) {
+                v = sm.red[c == 5 ? 0 : c][k];   // opacity (sum g), rgb, depth
+            } else {
+                const float M0 = sm.red[0][k], Mx = sm.red[1][k], My = sm.red[2][k];
+                const float4 r0 = sm.rec[buf][k][0];
+                const float o = sm.rec[buf][k][1].y;
+                const float X = r0.x - float(tx * kTile), Y = r0.y - float(ty * kTile);
+                // sums of g dx, g dy, g dx^2, g dx dy, g dy^2 with dx = X - lx, dy = Y - ly
+                const float gdx = X * M0 - Mx, gdy = Y * M0 - My;
+                if (c == 0) {
+                    v = o * (2.f * r0.z * gdx + r0.w * gdy);            // mean2d x: -o (a gdx + b gdy)
+                } else if (c == 1) {
+                    v = o * (r0.w * gdx + 2.f * sm.rec[buf][k][1].x * gdy);   // mean2d y: -o (b gdx + c gdy)
+                } else if (c == 2) {
+                    v = -0.5f * o * (X * X * M0 - 2.f * X * Mx + sm.red[3][k]);            // conic a
+                } else if (c == 3) {
+                    v = -o * (X * Y * M0 - X * My - Y * Mx + sm.red[4][k]);                 // conic b
+                } else {
+                    v = -0.5f * o * (Y * Y * M0 - 2.f * Y * My + sm.red[5][k]);            // conic c
+                }
+            }
+            if (v != 0.f) atomicAdd(sgrad + c * sld + sm.idx[buf][k], v);
         }
-        __syncthreads();   // protect sm.* before the next batch
     }
 }
 
@@ -566,7 +615,7 @@ void launch_render_bwd_tiles(WsState* s, const gs_camera& cam, const float*, con
         attr = true;
     }
     KTimer kt(s, KID_BWD_TILE, st);
-    render_bwd_kernel<<<ntiles, kTilePx, sizeof(BwdSmem), st>>>(
+    render_bwd_kernel<<<ntiles, kBwdThreads, sizeof(BwdSmem), st>>>(
         at<float4>(s, s->rec), lb.g, lb.j, lb.cnt, at<uint2>(s, s->ranges), cam.width, cam.height, s->cam_gx,
         at<float>(s, s->t_final), cam.bg[0], cam.bg[1], cam.bg[2], at<uint32_t>(s, s->n_last), dL_dcolor, dL_ddepth,
         at<float>(s, s->sgrad), s->n_cap);
