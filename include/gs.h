@@ -183,8 +183,9 @@ gs_status gs_densify_append(float* params, float* params_raw /*nullable*/, float
 
 /* Introspection for tests and benchmarks (host struct of device pointers into the workspace). */
 typedef struct {
-    const float* records;        /* [n][12]: mx, my, -a/2, -b | -c/2, opacity, depth, pad | r, g, b, pad
-                                    (conic [[a, b], [b, c]] = Sigma'^-1, exactly scaled) */
+    const float* records;        /* [n][12]: mx, my, -a/2, -b | -c/2, opacity, depth, q_max | r, g, b, pad
+                                    (conic [[a, b], [b, c]] = Sigma'^-1, exactly scaled; q_max ~ 2 ln(255 o)
+                                    is the tile-reach bound of the forward's live lists) */
     const uint32_t* depth_key;   /* [n] float bits of z^c */
     const int16_t* rect;         /* [n][4] xlo, xhi, ylo, yhi */
     const int32_t* radius;       /* [n] */

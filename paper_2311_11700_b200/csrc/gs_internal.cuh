@@ -129,7 +129,7 @@ gs_status run_densify(WsState* s, float* params, float* raw, int64_t* n_dev, int
 // ------------------------------------------------------------------ device helpers
 __device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
 
-// Projected record (48 B): r0 = {mx, my, A, B}, r1 = {C, o, depth, -}, r2 = {r, g, b, -} with the
+// Projected record (48 B): r0 = {mx, my, A, B}, r1 = {C, o, depth, q_max}, r2 = {r, g, b, -} with the
 // exactly scaled conic A = -a/2, B = -b, C = -c/2 (conic = Sigma'^-1 = [[a, b], [b, c]]).
 // alpha at pixel (px, py). Shared by the forward and both backward kernels so every decision is
 // bit-identical between them, and written with explicit round-to-nearest intrinsics in the

@@ -112,7 +112,9 @@ __global__ void __launch_bounds__(256) project_kernel(
             tiles = uint32_t(max(0, xhi - xlo)) * uint32_t(max(0, yhi - ylo));
             // exactly scaled conic for the blend: A = -a/2, B = -b, C = -c/2 (gs_internal.cuh)
             r0 = make_float4(mx, my, -0.5f * ca, -cb);
-            r1 = make_float4(-0.5f * cc, p[10], zc, 0.f);
+            // r1.w: squared Mahalanobis reach q_max = 2 ln(255 o), where o exp(-q/2) = 1/255, plus a
+            // margin (render.cu can_reach; no decision uses it, so it is outside reading R1's order)
+            r1 = make_float4(-0.5f * cc, p[10], zc, 2.f * (logf(255.f * p[10]) + 1e-4f) + 2e-4f);
             r2 = make_float4(p[11], p[12], p[13], 0.f);
         } else {
             radius = 0;

@@ -177,33 +177,53 @@ __device__ __forceinline__ void blend_step(PixState& p, float power, float4 r1, 
     p.done = p.done || term;
 }
 
+// Blend step without the termination test (the fast path of render_fwd2_kernel): identical
+// arithmetic to blend_step for every entry that does not terminate the pixel. A skipped entry gets
+// alpha 0, so w = 0 and T (1 - 0) == T bitwise.
+__device__ __forceinline__ void blend_fast(PixState& p, float power, float4 r1, float4 r2, uint32_t j) {
+    float G;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(G) : "f"(__fmul_rn(power, 1.4426950408889634f)));
+    const float a0 = fminf(0.99f, __fmul_rn(r1.y, G));
+    const bool live = !p.done && !(power > 0.f) && a0 >= (1.0f / 255.0f);
+    const float a = live ? a0 : 0.f;
+    const float w = __fmul_rn(a, p.T);
+    p.Cr = fmaf(w, r2.x, p.Cr);
+    p.Cg = fmaf(w, r2.y, p.Cg);
+    p.Cb = fmaf(w, r2.z, p.Cb);
+    p.D = fmaf(w, r1.z, p.D);
+    p.T = __fmul_rn(p.T, __fsub_rn(1.f, a));
+    p.nl = live ? j : p.nl;
+}
+
 constexpr int kFwd2Batch = kTilePx / 2;   // one staged record per thread
 
 // Can Gaussian (r0, r1) reach alpha >= 1/255 at any pixel of the box [x0, x1] x [y0, y1]? Conservative:
-// the quadratic form's minimum over the (continuous) box in fp64, with the fp32 evaluation error of
-// power bounded by 4e-6 of the terms' magnitude and a 1e-4 relative margin on alpha for the exp. A
-// "false" therefore guarantees that every per-pixel fp32 decision skips this Gaussian in this tile,
-// so dropping it changes no output.
+// alpha >= 1/255 needs q = (conic quadratic form) <= q_max = 2 ln(255 o) (r1.w, from gs_project, with
+// a margin), so the test compares the minimum of q over the (continuous) box with q_max, loosened by
+// 3e-5 of the terms' magnitude (covers the fp32 evaluation error of both this minimum and the
+// kernel's per-pixel power) and 1e-5 absolute. A "false" therefore guarantees that every per-pixel
+// fp32 decision skips this Gaussian in this tile, so dropping it changes no output.
 __device__ __forceinline__ bool can_reach(float4 r0, float4 r1, float x0, float y0, float x1, float y1) {
-    const double o = r1.y;
-    if (o * 255.0 * (1.0 - 1e-4) < 1.0) return false;   // alpha <= o everywhere
-    const double mx = r0.x, my = r0.y, a = -2.0 * double(r0.z), b = -double(r0.w), c = -2.0 * double(r1.x);
-    if (mx >= x0 && mx <= x1 && my >= y0 && my <= y1) return true;
-    auto q = [&](double dx, double dy) { return a * dx * dx + 2.0 * b * dx * dy + c * dy * dy; };
-    double qmin = 1e300;
+    const float qmax = r1.w;
+    const float mx = r0.x, my = r0.y, a = -2.f * r0.z, b = -r0.w, c = -2.f * r1.x;
+    if (mx >= x0 && mx <= x1 && my >= y0 && my <= y1) return qmax >= -1e-5f;
+    auto q = [&](float dx, float dy) { return fmaf(a * dx, dx, fmaf(2.f * b * dx, dy, c * dy * dy)); };
+    float qmin = 3.0e38f;
+#pragma unroll
     for (int e = 0; e < 2; ++e) {   // vertical edges x = x0, x1: minimise over y in [y0, y1]
-        const double dx = mx - (e ? x1 : x0);
-        const double y = fmin(fmax(my + b * dx / c, double(y0)), double(y1));
-        qmin = fmin(qmin, q(dx, my - y));
+        const float dx = mx - (e ? x1 : x0);
+        const float y = fminf(fmaxf(my + b * dx / c, y0), y1);
+        qmin = fminf(qmin, q(dx, my - y));
     }
+#pragma unroll
     for (int e = 0; e < 2; ++e) {   // horizontal edges y = y0, y1: minimise over x in [x0, x1]
-        const double dy = my - (e ? y1 : y0);
-        const double x = fmin(fmax(mx + b * dy / a, double(x0)), double(x1));
-        qmin = fmin(qmin, q(mx - x, dy));
+        const float dy = my - (e ? y1 : y0);
+        const float x = fminf(fmaxf(mx + b * dy / a, x0), x1);
+        qmin = fminf(qmin, q(mx - x, dy));
     }
-    const double dxm = fmax(fabs(mx - x0), fabs(mx - x1)), dym = fmax(fabs(my - y0), fabs(my - y1));
-    const double qmag = fabs(a) * dxm * dxm + 2.0 * fabs(b) * dxm * dym + fabs(c) * dym * dym;
-    return o * exp(-0.5 * qmin + 4e-6 * qmag + 1e-6) >= (1.0 / 255.0) * (1.0 - 1e-4);
+    const float dxm = fmaxf(fabsf(mx - x0), fabsf(mx - x1)), dym = fmaxf(fabsf(my - y0), fabsf(my - y1));
+    const float qmag = fabsf(a) * dxm * dxm + 2.f * fabsf(b) * dxm * dym + fabsf(c) * dym * dym;
+    return qmin - 3e-5f * qmag - 1e-5f <= qmax;
 }
 
 __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
@@ -278,25 +298,52 @@ __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
         }
         const int nlive = s_nlive;
         acc += uint32_t(nlive);
-        constexpr int kU = 4;                        // Gaussians per early-exit check
+        // Groups of kU Gaussians run a fast path without the termination test, which is exact
+        // whenever no pixel of the warp terminates inside the group: T only decreases, so if T
+        // after the group is >= 1e-4, every T (1 - alpha) tested inside it was too. Otherwise the
+        // warp restores the group's entry state and replays it with the exact step (rare: once
+        // per pixel at most).
+        constexpr int kU = 4;
+        auto entry = [&](int k0, int u, float4& r1, float4& r2, uint32_t& j, float& pA, float& pB) {
+            // past nlive: re-read slot 0 with zero opacity so the unrolled body stays branch-free
+            const bool real = k0 + u < nlive;
+            const int k = real ? s_live[k0 + u] : 0;
+            const float4 r0 = buf[k][0];
+            r1 = buf[k][1];
+            r2 = buf[k][2];
+            if (!real) r1.y = 0.f;   // zero opacity -> alpha 0 -> skipped exactly
+            j = uint32_t(b * kFwd2Batch + k + 1);
+            // same operation sequence as eval_alpha, x-terms shared between the two pixels
+            const float dx = __fsub_rn(r0.x, fpx);
+            const float Adx = __fmul_rn(r0.z, dx), Bdx = __fmul_rn(r0.w, dx);
+            const float dyA = __fsub_rn(r0.y, fyA), dyB = __fsub_rn(r0.y, fyB);
+            pA = __fmaf_rn(Adx, dx, __fmaf_rn(__fmul_rn(r1.x, dyA), dyA, __fmul_rn(Bdx, dyA)));
+            pB = __fmaf_rn(Adx, dx, __fmaf_rn(__fmul_rn(r1.x, dyB), dyB, __fmul_rn(Bdx, dyB)));
+        };
         for (int k0 = 0; k0 < nlive; k0 += kU) {
-            if (A.done && B.done) break;
+            if (__all_sync(0xffffffffu, A.done && B.done)) break;
+            const PixState A0 = A, B0 = B;
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
-                // past nlive: re-read slot 0 with zero opacity so the unrolled body stays branch-free
-                const bool real = k0 + u < nlive;
-                const int k = real ? s_live[k0 + u] : 0;
-                float4 r0 = buf[k][0], r1 = buf[k][1], r2 = buf[k][2];
-                if (!real) r1.y = 0.f;   // zero opacity -> alpha 0 -> skipped exactly
-                const uint32_t j = uint32_t(b * kFwd2Batch + k + 1);
-                // same operation sequence as eval_alpha, x-terms shared between the two pixels
-                const float dx = __fsub_rn(r0.x, fpx);
-                const float Adx = __fmul_rn(r0.z, dx), Bdx = __fmul_rn(r0.w, dx);
-                const float dyA = __fsub_rn(r0.y, fyA), dyB = __fsub_rn(r0.y, fyB);
-                const float inA = __fmaf_rn(__fmul_rn(r1.x, dyA), dyA, __fmul_rn(Bdx, dyA));
-                const float inB = __fmaf_rn(__fmul_rn(r1.x, dyB), dyB, __fmul_rn(Bdx, dyB));
-                blend_step(A, __fmaf_rn(Adx, dx, inA), r1, r2, j);
-                blend_step(B, __fmaf_rn(Adx, dx, inB), r1, r2, j);
+                float4 r1, r2;
+                uint32_t j;
+                float pA, pB;
+                entry(k0, u, r1, r2, j, pA, pB);
+                blend_fast(A, pA, r1, r2, j);
+                blend_fast(B, pB, r1, r2, j);
+            }
+            if (__any_sync(0xffffffffu, A.T < 1e-4f || B.T < 1e-4f)) {
+                A = A0;
+                B = B0;
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    float4 r1, r2;
+                    uint32_t j;
+                    float pA, pB;
+                    entry(k0, u, r1, r2, j, pA, pB);
+                    blend_step(A, pA, r1, r2, j);
+                    blend_step(B, pB, r1, r2, j);
+                }
             }
         }
         if (__syncthreads_and(A.done && B.done)) break;   // also orders buffer reuse
