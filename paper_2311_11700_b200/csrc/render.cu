@@ -431,7 +431,8 @@ struct BwdSmem {
 };
 
 struct BwdPix {
-    float T, S, tfb;   // T_{i+1} while walking back (starts at T_final), suffix sum, T_f bg.dL/dC
+    float T, Q;        // T_{i+1} while walking back (starts at T_final); Q = S + T_f bg.dL/dC with the
+                       // suffix sum S_i = sum_{k>i} alpha_k T_k e_k
     float4 dl;
     uint32_t nl;
 };
@@ -447,12 +448,12 @@ __device__ __forceinline__ float2 bwd_step(BwdPix& p, float power, float4 r1, fl
     const float a = live ? a0 : 0.f;
     float ro;   // 1/(1 - alpha): MUFU rcp.approx (<= 1 ulp; gradients only, no decision)
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ro) : "f"(__fsub_rn(1.f, a)));
-    p.T = live ? p.T * ro : p.T;
+    p.T = p.T * ro;   // skipped: alpha 0, rcp.approx(1) == 1, T unchanged
     const float w = a * p.T;
     const float ev = fmaf(r2.x, p.dl.x, fmaf(r2.y, p.dl.y, fmaf(r2.z, p.dl.z, r1.z * p.dl.w)));
-    const float ga = fmaf(p.T, ev, -(p.S + p.tfb) * ro);   // dL/dalpha_i
+    const float ga = fmaf(p.T, ev, -p.Q * ro);   // dL/dalpha_i
     const float go = (live && !(og > 0.99f)) ? G * ga : 0.f;
-    p.S = fmaf(w, ev, p.S);   // w == 0 when skipped: S unchanged (ev finite; padding is zero-filled)
+    p.Q = fmaf(w, ev, p.Q);   // w == 0 when skipped: Q unchanged (ev finite; padding is zero-filled)
     return make_float2(w, go);
 }
 
@@ -476,14 +477,13 @@ __global__ void __launch_bounds__(kBwdThreads, 4) render_bwd_kernel(
         p.nl = 0;
         p.dl = make_float4(0.f, 0.f, 0.f, 0.f);
         p.T = 1.f;
-        p.S = 0.f;
         if (px < W && py < H) {
             const size_t pix = size_t(py) * W + px;
             p.nl = n_last[pix];
             p.dl = make_float4(dLdC[pix], dLdC[plane + pix], dLdC[2 * plane + pix], dLdD[pix]);
             p.T = t_final[pix];
         }
-        p.tfb = p.T * (bgr * p.dl.x + bgg * p.dl.y + bgb * p.dl.z);
+        p.Q = p.T * (bgr * p.dl.x + bgg * p.dl.y + bgb * p.dl.z);   // S = 0 at the back
         sm.dl[q] = p.dl;
     };
     BwdPix A, B;
