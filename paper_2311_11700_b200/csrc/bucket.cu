@@ -8,10 +8,10 @@
 //                   difference array over the tile grid in shared memory gives count[c][t]
 //   B4  tile scan:  per-tile totals (8 chunk segments per tile in flight), one exclusive scan over
 //                   tiles (ranges, K), then per-tile exclusive scans over chunks -> base[c][t]
-//   B5  emission:   block = (chunk, 128-tile group), warp = 16 consecutive tiles; each warp compacts
-//                   (in depth order) the chunk's Gaussians meeting its segment's bounding box, then
-//                   per tile its lanes test 32 of them at a time and a ballot/popc prefix places the
-//                   hits at base[c][t] + rank (coalesced 4-B stores, depth order preserved)
+//   B5  emission:   warp work item = (chunk, 32-tile segment): the warp compacts (in depth order)
+//                   the chunk's Gaussians meeting its segment, then per tile its lanes test 32 of
+//                   them at a time and a ballot/popc prefix places the hits at base[c][t] + rank
+//                   (coalesced 4-B stores, depth order preserved)
 // Per tile, entries come out in chunk order and in depth order within a chunk, i.e. ordered by
 // (depth bits, index): exactly the per-tile lists of path A (checked bit-exact in the tests).
 // HBM traffic is ~4 B per key (+ per-Gaussian and per-chunk terms) instead of ~150 B per key.
@@ -25,8 +25,7 @@
 namespace gs {
 
 constexpr int kChunk = 256;      // Gaussians per chunk (depth order)
-constexpr int kGroup = 128;      // tiles per emission block
-constexpr int kSeg = 16;         // consecutive tiles per emission warp (kGroup / 8 warps)
+constexpr int kSeg = 32;         // consecutive tiles per emission work item (one warp)
 
 gs_status chained_scan(WsState* s, const uint32_t* in, uint32_t* out, int64_t n, unsigned long long* total,
                        cudaStream_t st, int64_t cap, unsigned long long* total_eff);
@@ -165,39 +164,82 @@ __global__ void __launch_bounds__(256) chunk_base_kernel(uint32_t* __restrict__ 
 }
 
 // B5 ---------------------------------------------------------------------------------------
+// Block = (chunk, 8 segments of kSeg consecutive tiles); blocks of chunks beyond ceil(V_s / kChunk),
+// read on the device, exit at once. The block first pre-filters (ordered BlockScan compaction) the
+// chunk's Gaussians meeting its tile range; then each warp, independently, compacts those meeting its
+// segment with a per-Gaussian 32-bit tile mask, and per tile a ballot + popc ranks the hits of 32
+// Gaussians at a time and places them at base[chunk][tile] + rank (coalesced 4-B stores).
+__device__ __forceinline__ uint32_t bits_below(int n) { return n >= 32 ? 0xffffffffu : ((1u << n) - 1u); }
+
+// bits [lo, hi) of the segment mask for rect r on tile row `row`, whose segment tiles are columns
+// [x0, x0 + cnt) at mask bits [bit0, bit0 + cnt)
+__device__ __forceinline__ uint32_t run_mask(short4 r, int row, int x0, int cnt, int bit0) {
+    if (row < r.z || row >= r.w) return 0u;
+    const int lo = max(int(r.x), x0) - x0, hi = min(int(r.y), x0 + cnt) - x0;
+    return hi > lo ? (bits_below(hi) & ~bits_below(lo)) << bit0 : 0u;
+}
+
 __global__ void __launch_bounds__(256) bucket_emit_kernel(
     const uint32_t* __restrict__ svals, const short4* __restrict__ srect, const uint32_t* __restrict__ cmat,
     const unsigned int* __restrict__ n_on, const unsigned long long* __restrict__ n_keys_eff,
     const unsigned long long* __restrict__ n_keys, int GX, int T, uint32_t* __restrict__ vals_out) {
+    using BS = cub::BlockScan<int, 256>;
+    __shared__ typename BS::TempStorage scan;
+    __shared__ short4 b_rect[kChunk];
+    __shared__ uint32_t b_g[kChunk];
     __shared__ uint32_t l_mask[8][kChunk];
     __shared__ uint32_t l_g[8][kChunk];
     if (*n_keys_eff != *n_keys) return;   // capacity overflow: emit nothing (error flag is set)
-    const int c = blockIdx.x;
     const uint32_t Von = *n_on;
+    const int c = blockIdx.x;
     const uint32_t base = uint32_t(c) * kChunk;
-    if (base >= Von) return;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (base >= Von) return;   // chunk beyond the on-screen count (grid sized by n)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = (1u << lane) - 1u;
-    // this warp's segment: up to 16 consecutive tiles (row-major) starting at (tx0, ty0); it spans
-    // n0 tiles of row ty0 and then whole or partial following rows
-    const int t0 = blockIdx.y * kGroup + warp * kSeg;
-    if (t0 >= T) return;   // warp-uniform; no block-level barrier below
+    // 1. block pre-filter: the chunk's Gaussians (depth order kept) whose rect meets the block's
+    //    tile range [g0, g1] (8 segments)
+    const int g0 = blockIdx.y * (8 * kSeg), g1 = min(T, g0 + 8 * kSeg) - 1;
+    {
+        const int gy0 = g0 / GX, gy1 = g1 / GX;
+        const int cx0 = g0 - gy0 * GX, cx1 = g1 - gy1 * GX;   // first / last row columns
+        const uint32_t s = base + tid;
+        short4 r = make_short4(0, 0, 0, 0);
+        bool meet = false;
+        if (s < Von) {
+            r = srect[s];
+            const int ylo = max(int(r.z), gy0), yhi = min(int(r.w) - 1, gy1);
+            if (ylo <= yhi && r.x < r.y) {
+                auto row_meets = [&](int y) {
+                    const int c0 = y == gy0 ? cx0 : 0, c1 = y == gy1 ? cx1 + 1 : GX;
+                    return max(int(r.x), c0) < min(int(r.y), c1);
+                };
+                meet = (yhi - ylo >= 2) || row_meets(ylo) || row_meets(yhi);
+            }
+        }
+        int off, tot;
+        BS(scan).ExclusiveSum(meet ? 1 : 0, off, tot);
+        if (meet) {
+            b_rect[off] = r;
+            b_g[off] = svals[s];
+        }
+        if (tid == 0) l_g[0][0] = uint32_t(tot);   // broadcast (l_g is rewritten below, after the barrier)
+        __syncthreads();
+    }
+    const int tot = int(l_g[0][0]);
+    __syncthreads();
+    // 2. warp = one segment of kSeg consecutive tiles (row-major) starting at (tx0, ty0); it spans
+    //    n0 tiles of row ty0 and then whole or partial following rows. Warps are independent.
+    const int t0 = g0 + warp * kSeg;
+    if (t0 >= T || tot == 0) return;   // warp-uniform
     const int nseg = min(kSeg, T - t0);
     const int ty0 = t0 / GX, tx0 = t0 - ty0 * GX;
     const int n0 = min(nseg, GX - tx0);
-    // bit j of a Gaussian's mask: its rect contains segment tile j
-    auto run_mask = [](short4 r, int row, int x0, int cnt, int bit0) -> uint32_t {
-        if (row < r.z || row >= r.w) return 0u;
-        const int lo = max(int(r.x), x0) - x0, hi = min(int(r.y), x0 + cnt) - x0;
-        return hi > lo ? (((1u << hi) - 1u) & ~((1u << lo) - 1u)) << bit0 : 0u;
-    };
-    // ordered (depth-order) compaction of the chunk's Gaussians meeting the segment, with masks
     int L = 0;
-    for (int k0 = 0; k0 < kChunk; k0 += 32) {
-        const uint32_t s = base + k0 + lane;
+    for (int k0 = 0; k0 < tot; k0 += 32) {
+        const int k = k0 + lane;
         uint32_t mask = 0;
-        if (s < Von) {
-            const short4 r = srect[s];
+        if (k < tot) {
+            const short4 r = b_rect[k];
             mask = run_mask(r, ty0, tx0, n0, 0);
             for (int bit = n0, row = ty0 + 1; bit < nseg; bit += GX, ++row)   // narrow grids: more rows
                 mask |= run_mask(r, row, 0, min(GX, nseg - bit), bit);
@@ -206,7 +248,7 @@ __global__ void __launch_bounds__(256) bucket_emit_kernel(
         if (mask) {
             const int o = L + __popc(m & lt);
             l_mask[warp][o] = mask;
-            l_g[warp][o] = svals[s];
+            l_g[warp][o] = b_g[k];
         }
         L += __popc(m);
     }
@@ -279,7 +321,7 @@ gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaS
     }
     if (nch > 0) {
         KTimer kt(s, KID_BUCKET_EMIT, st);
-        dim3 grid(unsigned(nch), unsigned((T + kGroup - 1) / kGroup));
+        const dim3 grid(unsigned(nch), unsigned(((T + kSeg - 1) / kSeg + 7) / 8));
         bucket_emit_kernel<<<grid, 256, 0, st>>>(svals, srect, cmat, &misc->n_onscreen, &misc->n_keys_eff,
                                                     &misc->n_keys, GX, T, at<uint32_t>(s, s->vals0));
     }
