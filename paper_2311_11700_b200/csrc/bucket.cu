@@ -282,11 +282,11 @@ gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaS
     uint32_t* v0 = at<uint32_t>(s, s->dval_sorted);
     uint32_t* v1 = v0 + s->n_cap;
     // B1: ordered compaction of the on-screen Gaussians -> (depth key, index) pairs in k0/v0
-    gs_status rc = run_compact_onscreen(s, st);
+    gs_status rc = run_compact_onscreen(s, st, true);   // also the depth keys' digit histograms
     if (rc != GS_OK) return rc;
     // B2: stable depth sort of the V_s on-screen pairs (grid sized by n, V_s read on the device)
     int which = 0;
-    rc = onesweep_sort_pairs<uint32_t, kSortItemsSmall>(s, k0, v0, k1, v1, &misc->n_items, n, 32, st, &which);
+    rc = onesweep_sort_pairs<uint32_t, kSortItemsSmall>(s, k0, v0, k1, v1, &misc->n_items, n, 32, st, &which, true);
     if (rc != GS_OK) return rc;
     const uint32_t* svals = which ? v1 : v0;
     uint32_t* cmat = at<uint32_t>(s, s->chunk_mat);

@@ -1,5 +1,6 @@
 // Onesweep-style LSD radix sort of (key, u32 value) pairs, 8-bit digits (sm_100a).
-//  1. one upfront pass builds the digit histograms of every pass (reads the keys once);
+//  1. one upfront pass builds the digit histograms of every pass (reads the keys once), or the
+//     producer of the keys accumulates them; each pass kernel scans its histogram in-CTA;
 //  2. each digit pass is ONE kernel: a CTA takes the next partition from an atomic ticket
 //     (forward progress for the look-back), ranks its 4096 keys stably with warp match_any,
 //     publishes its per-digit counts, resolves its global digit offsets by decoupled look-back
@@ -37,16 +38,6 @@ __global__ void __launch_bounds__(256) onesweep_hist_kernel(const KT* __restrict
     }
 }
 
-// in-place exclusive scan of each pass' 256-bin histogram (one block per pass)
-static __global__ void onesweep_digit_scan_kernel(uint32_t* __restrict__ hist) {
-    using BlockScan = cub::BlockScan<uint32_t, 256>;
-    __shared__ typename BlockScan::TempStorage tmp;
-    uint32_t* h = hist + blockIdx.x * 256;
-    uint32_t v = h[threadIdx.x], ex;
-    BlockScan(tmp).ExclusiveSum(v, ex);
-    h[threadIdx.x] = ex;
-}
-
 __device__ __forceinline__ unsigned long long look_word(uint32_t epoch, uint32_t flag, uint32_t v) {
     return (uint64_t(epoch & 0x3fffffffu) << 34) | (uint64_t(flag) << 32) | v;
 }
@@ -65,7 +56,7 @@ struct OnesweepSmem {
 template <class KT, int IPT>
 __global__ void __launch_bounds__(kSortThreads) onesweep_pass_kernel(
     const KT* __restrict__ kin, const uint32_t* __restrict__ vin, KT* __restrict__ kout, uint32_t* __restrict__ vout,
-    const unsigned long long* __restrict__ n_keys, int shift, const uint32_t* __restrict__ digit_base,
+    const unsigned long long* __restrict__ n_keys, int shift, const uint32_t* __restrict__ digit_hist,
     unsigned long long* look, unsigned int* ticket, uint32_t epoch) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     OnesweepSmem<KT, IPT>& sm = *reinterpret_cast<OnesweepSmem<KT, IPT>*>(smem_raw);
@@ -73,6 +64,9 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass_kernel(
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
     if (tid == 0) sm.part = atomicAdd(ticket, 1u);
     for (int i = tid; i < (kSortThreads / 32) * 256; i += kSortThreads) (&sm.wh[0][0])[i] = 0;
+    // this pass' global digit offsets: exclusive scan of its histogram (thread t = digit t)
+    uint32_t dbase;
+    cub::BlockScan<uint32_t, 256>(sm.scan).ExclusiveSum(digit_hist[tid], dbase);
     __syncthreads();
     const uint32_t part = sm.part;
     const uint64_t K = *n_keys;
@@ -148,7 +142,7 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass_kernel(
     uint32_t lstart;
     cub::BlockScan<uint32_t, 256>(sm.scan).ExclusiveSum(cnt, lstart);
     sm.local_start[t] = lstart;
-    sm.gbase[t] = digit_base[t] + excl;
+    sm.gbase[t] = dbase + excl;
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
@@ -173,24 +167,22 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass_kernel(
 
 // Sort (k0, v0) by bits [0, bits). Ping-pongs with (k1, v1); *which = buffer holding the result.
 // K lives on the device (n_keys); Kgrid >= K sizes the grids (exact in host-sync mode).
+// hist_ready: the producer of (k0, v0) already accumulated the per-pass digit histograms into the
+// workspace's sort_hist (zeroed beforehand), so the histogram kernel is skipped.
 template <class KT, int IPT = kSortItems>
 gs_status onesweep_sort_pairs(WsState* s, KT* k0, uint32_t* v0, KT* k1, uint32_t* v1, const unsigned long long* n_keys,
-                              int64_t Kgrid, int bits, cudaStream_t st, int* which) {
+                              int64_t Kgrid, int bits, cudaStream_t st, int* which, bool hist_ready = false) {
     Misc* misc = at<Misc>(s, s->misc);
     const int npass = (bits + 7) / 8;
     uint32_t* hist = at<uint32_t>(s, s->sort_hist);
     *which = 0;
     if (Kgrid <= 0) return GS_OK;
-    cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 256 * npass, st);
     cudaMemsetAsync(misc->sort_counter, 0, sizeof(misc->sort_counter), st);
-    {
+    if (!hist_ready) {
+        cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 256 * npass, st);
         const int blocks = int(std::min<int64_t>((Kgrid + 255) / 256, 148 * 8));
-        {
-            KTimer kt(s, KID_SORT_HIST, st);
-            onesweep_hist_kernel<KT><<<blocks, 256, 0, st>>>(k0, n_keys, npass, hist);
-        }
-        KTimer kt(s, KID_SORT_DSCAN, st);
-        onesweep_digit_scan_kernel<<<npass, 256, 0, st>>>(hist);
+        KTimer kt(s, KID_SORT_HIST, st);
+        onesweep_hist_kernel<KT><<<blocks, 256, 0, st>>>(k0, n_keys, npass, hist);
     }
     const size_t smem = sizeof(OnesweepSmem<KT, IPT>);
     static bool attr_set = false;   // idempotent attribute; benign race
