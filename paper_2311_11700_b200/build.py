@@ -14,7 +14,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
 # projection decides integers (depth key, rect, radius) and must be bit-exact with the oracle:
 # no FMA contraction, IEEE division and sqrt
 PER_FILE = {"project.cu": ["-fmad=false", "-prec-div=true", "-prec-sqrt=true"]}
-SOURCES = ["abi.cu", "project.cu", "binsort.cu", "bucket.cu", "render.cu", "optim.cu"]
+SOURCES = ["abi.cu", "project.cu", "binsort.cu", "bucket.cu", "bincoop.cu", "render.cu", "optim.cu"]
 
 
 def nvcc() -> str:

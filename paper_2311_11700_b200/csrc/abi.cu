@@ -72,6 +72,11 @@ static void carve(WsState* s, Carver& c) {
     s->pose_part = c.take(uint64_t((n + 255) / 256 + 1) * 16 * 8);   // per-block pose partials
     s->onlist = c.take(uint64_t(n) * 4);                              // on-screen Gaussians, index order
     s->live_cnt = c.take(uint64_t(tiles) * 4);                        // per-tile live-list lengths
+    s->svals = c.take(uint64_t(n) * 4);                               // path B: depth-sorted on-screen Gaussians
+    // path B cooperative kernel: per-pass per-CTA digit histograms, pass totals, per-CTA counts,
+    // tile totals and per-(segment, tile) sums
+    s->coop = c.take((uint64_t(kCoopPasses) * kCoopGridMax * kCoopBins + kCoopPasses * kCoopBins + kCoopGridMax +
+                      uint64_t(tiles) * (1 + kCoopSegs)) * 4);
 }
 
 static bool ws_ok(const gs_ws* ws) { return ws && state(ws)->magic == kMagic; }
@@ -351,7 +356,7 @@ const char* gs_kernel_name(int32_t id) {
     static const char* names[KID_COUNT] = {"project", "chained_scan", "emit_keys", "sort_hist", "sort_digit_scan",
                                            "sort_pass", "tile_ranges", "render_fwd", "render_bwd_tiles",
                                            "gaussian_bwd", "pose_finalize", "loss_l1", "densify", "depth_sort",
-                                           "chunk_hist", "chunk_scan", "bucket_emit"};
+                                           "chunk_hist", "chunk_scan", "bucket_emit", "bin_coop"};
     return (id >= 0 && id < KID_COUNT) ? names[id] : "unknown";
 }
 

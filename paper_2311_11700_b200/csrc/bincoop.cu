@@ -1,0 +1,472 @@
+// gs_bin_sort, path B, front half: ONE cooperative (grid-synchronised) kernel, one CTA per SM.
+//
+// Everything before the bucket emission (bucket.cu B5) is latency-bound at the paper's sizes
+// (V_s ~ 1e5 on-screen Gaussians): as separate launches, compaction + a 4-pass onesweep depth sort +
+// chunk counts + three tile-scan kernels cost ~0.13 ms at config 2, mostly launch and look-back
+// latency. Here the same work runs as phases of one persistent kernel separated by grid barriers:
+//   C0  compaction: per CTA a contiguous slice of the n Gaussians; counts and
+//       the on-screen depth-key range -> barrier -> ordered writes of onlist[V_s] (index order) and
+//       the depth-sort pairs (key - kmin, i), with every pass' digit histogram
+//   C1  stable LSD radix sort (a4) of the V_s pairs over the bits that vary (kmax - kmin), in
+//       P = ceil(bits / 9) passes of <= 9-bit digits (3 passes at config 2). A pass: global digit
+//       base + the sum of the preceding CTAs' histograms of this digit -> stable in-CTA ranking
+//       (warp match_any, per-warp digit counts) -> scatter; the scatter also counts the next pass'
+//       digits per destination slice (global atomics), so each pass costs one barrier. Ties keep
+//       their order (slices are contiguous and ranked in order), so equal depths stay by index.
+//       The last pass writes svals[s] (the s-th on-screen Gaussian in (depth, index) order) and its
+//       rect srect[s] instead of keys.
+//   C2  chunk counts: per 256-Gaussian chunk of svals, a 2-D difference array over the tile grid in
+//       shared memory -> count[c][t] (4 chunks per CTA in flight)
+//   C3  per-(tile, chunk segment) sums and tile totals (atomics) -> barrier ->
+//   C4  exclusive scan of the tile totals (ranges = a5, K, capacity flag) and the exclusive scans over
+//       chunks: count[c][t] is replaced by base[c][t] = start of chunk c's entries in tile t's list.
+// The grid barrier is the cooperative-groups pattern (block barrier, one thread fences and arrives
+// on a monotone counter, spins on an acquire load); cudaLaunchCooperativeKernel guarantees that all
+// CTAs are co-resident. Data produced inside the kernel is read with ld.global.cg (L2), never
+// through the non-coherent L1.
+#include <cub/block/block_scan.cuh>
+
+#include <algorithm>
+
+#include "gs_internal.cuh"
+
+namespace gs {
+
+constexpr int kCT = 1024;                // threads per CTA
+constexpr int kCW = kCT / 32;            // warps per CTA
+constexpr int kDigitBits = 9;            // <= 9-bit digits (kCoopBins = 512)
+constexpr int kCGroups = 4;              // chunk-count groups of 256 threads
+
+struct CoopArgs {
+    const uint32_t* tiles;   // [n] tiles touched (gs_project)
+    const uint32_t* dkey;    // [n] depth key bits
+    const short4* rect;      // [n] tile rect {x_lo, x_hi, y_lo, y_hi}
+    int64_t n;
+    int GX, GY;
+    int64_t key_cap;
+    uint32_t* onlist;        // [n] on-screen Gaussians, index order
+    uint32_t* k0; uint32_t* v0; uint32_t* k1; uint32_t* v1;   // [n] ping-pong sort buffers
+    uint32_t* svals;         // [n] depth-sorted on-screen Gaussians
+    short4* srect;           // [n] their rects
+    uint32_t* cmat;          // [nch][T] counts -> bases
+    uint32_t* H;             // [kCoopPasses][kCoopGridMax][kCoopBins] per-pass per-CTA digit counts
+    uint32_t* hist_all;      // [kCoopPasses][kCoopBins] per-pass digit totals
+    uint32_t* cta_cnt;       // [kCoopGridMax] on-screen count per compaction slice
+    uint32_t* tot;           // [T] tile totals
+    uint32_t* segsum;        // [kCoopSegs][T]
+    uint2* ranges;           // [T]
+    Misc* misc;
+    int groups;              // chunk-count groups per CTA (shared-memory bound)
+};
+
+__device__ __forceinline__ uint32_t ldcg(const uint32_t* p) { return __ldcg(p); }
+
+__device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int& goal) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        goal += gridDim.x;
+        __threadfence();
+        atomicAdd(bar, 1u);
+        unsigned int v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        } while (v < goal);
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void group_sync(int g) {   // named barrier of one 256-thread group
+    asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(256) : "memory");
+}
+
+__device__ __forceinline__ void seg_range(int nch, int seg, int& c0, int& c1) {
+    const int per = (nch + kCoopSegs - 1) / kCoopSegs;
+    c0 = min(nch, seg * per);
+    c1 = min(nch, c0 + per);
+}
+
+__global__ void __launch_bounds__(kCT, 1) bin_coop_kernel(CoopArgs a) {
+    extern __shared__ __align__(16) uint32_t dyn[];
+    using BScan = cub::BlockScan<uint32_t, kCT>;
+    __shared__ typename BScan::TempStorage bscan;
+    __shared__ uint32_t s_hist[kCoopPasses][kCoopBins];
+    __shared__ uint32_t s_run[kCoopBins], s_gpos[kCoopBins];
+    __shared__ uint32_t s_u[8];
+    const int G = gridDim.x, k = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int T = a.GX * a.GY;
+    Misc* misc = a.misc;
+    unsigned int goal = 0;
+
+    // zero the accumulators of later phases (ordered before their use by the first barrier)
+    {
+        const int64_t nz1 = int64_t(kCoopPasses) * kCoopGridMax * kCoopBins;   // H (rows of passes >= 1 used)
+        for (int64_t i = int64_t(k) * kCT + tid; i < nz1; i += int64_t(G) * kCT)
+            if (i >= int64_t(kCoopGridMax) * kCoopBins) a.H[i] = 0u;
+        for (int i = k * kCT + tid; i < kCoopPasses * kCoopBins; i += G * kCT) a.hist_all[i] = 0u;
+        for (int i = k * kCT + tid; i < T; i += G * kCT) a.tot[i] = 0u;
+    }
+    // ---------------------------------------------------------------- C0 compaction: count
+    const int64_t S1 = (a.n + G - 1) / G;
+    const int64_t b0 = min(a.n, int64_t(k) * S1), b1 = min(a.n, b0 + S1);
+    uint32_t kmin = 0xffffffffu, kmax = 0u, cnt = 0;
+    if (tid == 0) { s_u[0] = 0xffffffffu; s_u[1] = 0u; }
+    __syncthreads();
+    for (int64_t r0 = b0; r0 < b1; r0 += kCT) {
+        const int64_t i = r0 + tid;
+        const bool f = i < b1 && a.tiles[i] > 0u;
+        if (f) {
+            const uint32_t key = a.dkey[i];
+            kmin = min(kmin, key);
+            kmax = max(kmax, key);
+        }
+        cnt += uint32_t(__syncthreads_count(f));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if (lane == 0 && kmax >= kmin) {
+        atomicMin(&s_u[0], kmin);
+        atomicMax(&s_u[1], kmax);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        a.cta_cnt[k] = cnt;
+        if (cnt) {
+            atomicMax(&misc->kmin_inv, ~s_u[0]);
+            atomicMax(&misc->kmax, s_u[1]);
+        }
+    }
+    grid_sync(&misc->coop_bar, goal);
+
+    // every CTA: its compaction base, V_s and the sort geometry
+    if (warp == 0) {
+        uint32_t pre = 0, all = 0;
+        for (int j = lane; j < G; j += 32) {
+            const uint32_t c = ldcg(a.cta_cnt + j);
+            all += c;
+            pre += j < k ? c : 0u;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            pre += __shfl_xor_sync(0xffffffffu, pre, o);
+            all += __shfl_xor_sync(0xffffffffu, all, o);
+        }
+        if (lane == 0) {
+            s_u[2] = pre;
+            s_u[3] = all;
+            s_u[4] = ~ldcg(&misc->kmin_inv);
+            s_u[5] = ldcg(&misc->kmax);
+        }
+    }
+    __syncthreads();
+    const uint32_t base_k = s_u[2], Vs = s_u[3], key_lo = s_u[4], key_hi = s_u[5];
+    const uint32_t range = Vs ? key_hi - key_lo : 0u;
+    const int bits = range ? 32 - __clz(range) : 0;
+    const int P = Vs == 0 ? 0 : (bits == 0 ? 1 : (bits + kDigitBits - 1) / kDigitBits);
+    const int dbits = P ? (bits + P - 1) / P : 0;
+    const uint32_t nbins = 1u << dbits, dmask = nbins - 1u;
+    const uint32_t S2 = (Vs + G - 1) / G;
+
+    // ---------------------------------------------------------------- C0 compaction: ordered writes
+    for (int i = tid; i < kCoopPasses * kCoopBins; i += kCT) (&s_hist[0][0])[i] = 0u;
+    __syncthreads();
+    {
+        uint32_t r = base_k;
+        for (int64_t r0 = b0; r0 < b1; r0 += kCT) {
+            const int64_t i = r0 + tid;
+            const bool f = i < b1 && a.tiles[i] > 0u;
+            uint32_t off, agg;
+            BScan(bscan).ExclusiveSum(f ? 1u : 0u, off, agg);
+            if (f) {
+                const uint32_t key = a.dkey[i] - key_lo;
+                a.onlist[r + off] = uint32_t(i);
+                a.k0[r + off] = key;
+                a.v0[r + off] = uint32_t(i);
+                for (int p = 0; p < P; ++p) atomicAdd(&s_hist[p][(key >> (p * dbits)) & dmask], 1u);
+            }
+            r += agg;
+            __syncthreads();   // bscan reuse
+        }
+    }
+    __syncthreads();
+    for (int d = tid; d < kCoopBins; d += kCT) a.H[size_t(k) * kCoopBins + d] = s_hist[0][d];   // pass-0 row
+    for (int i = tid; i < P * kCoopBins; i += kCT) {
+        const uint32_t c = (&s_hist[0][0])[i];
+        if (c) atomicAdd(a.hist_all + i, c);
+    }
+    if (k == 0 && tid == 0) {
+        misc->n_onscreen = Vs;
+        misc->n_items = Vs;
+    }
+    grid_sync(&misc->coop_bar, goal);
+
+    // ---------------------------------------------------------------- C1 depth sort passes
+    uint32_t* wh = dyn;   // [kCW][kCoopBins] per-warp digit counts -> offsets (also prefix partials)
+    for (int p = 0; p < P; ++p) {
+        const uint32_t* kin = (p & 1) ? a.k1 : a.k0;
+        const uint32_t* vin = (p & 1) ? a.v1 : a.v0;
+        uint32_t* kout = (p & 1) ? a.k0 : a.k1;
+        uint32_t* vout = (p & 1) ? a.v0 : a.v1;
+        const bool last = p == P - 1;
+        const int shift = p * dbits;
+        const uint32_t s0 = p == 0 ? base_k : min(Vs, uint32_t(k) * S2);
+        const uint32_t s1 = p == 0 ? base_k + ldcg(a.cta_cnt + k) : min(Vs, s0 + S2);
+        // global start of each digit for this CTA: digit base (scan of the pass totals) + the
+        // preceding CTAs' counts. Thread (4-bin column c4, row set rs) sums rows k' = rs, rs + 8, ...
+        // < k with 16-B loads (rows are zero beyond nbins).
+        const uint32_t* Hp = a.H + size_t(p) * kCoopGridMax * kCoopBins;
+        {
+            const int c4 = tid & (kCoopBins / 4 - 1), rs = tid / (kCoopBins / 4);   // 128 x 8
+            uint4 acc = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll 4
+            for (int kk = rs; kk < k; kk += kCT / (kCoopBins / 4)) {
+                const uint4 v = __ldcg(reinterpret_cast<const uint4*>(Hp + size_t(kk) * kCoopBins) + c4);
+                acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+            }
+            reinterpret_cast<uint4*>(wh + rs * kCoopBins)[c4] = acc;
+            __syncthreads();
+            uint32_t tot = 0, pre = 0;
+            if (uint32_t(tid) < nbins) {
+#pragma unroll
+                for (int q = 0; q < kCT / (kCoopBins / 4); ++q) pre += wh[q * kCoopBins + tid];
+                tot = ldcg(a.hist_all + p * kCoopBins + tid);
+            }
+            uint32_t dbase;
+            BScan(bscan).ExclusiveSum(tot, dbase);
+            if (uint32_t(tid) < nbins) {
+                s_gpos[tid] = dbase + pre;
+                s_run[tid] = 0u;
+            }
+            __syncthreads();
+        }
+        for (uint32_t r0 = s0; r0 < s1; r0 += kCT) {
+            for (int i = tid; i < (kCW << dbits); i += kCT) wh[(i >> dbits) * kCoopBins + (i & int(dmask))] = 0u;
+            __syncthreads();
+            const uint32_t idx = r0 + tid;
+            const bool ok = idx < s1;
+            const uint32_t key = ok ? ldcg(kin + idx) : 0u;
+            const uint32_t val = ok ? ldcg(vin + idx) : 0u;
+            const uint32_t dg = ok ? (key >> shift) & dmask : nbins;   // nbins: sentinel digit
+            const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+            const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+            if (ok && lane == __ffs(peers) - 1) wh[warp * kCoopBins + dg] = __popc(peers);
+            __syncthreads();
+            for (uint32_t d = tid; d < nbins; d += kCT) {   // per digit: exclusive over warps + running
+                uint32_t run = s_run[d];
+#pragma unroll 8
+                for (int w = 0; w < kCW; ++w) {
+                    const uint32_t c = wh[w * kCoopBins + d];
+                    wh[w * kCoopBins + d] = run;
+                    run += c;
+                }
+                s_run[d] = run;
+            }
+            __syncthreads();
+            if (ok) {
+                const uint32_t pos = s_gpos[dg] + wh[warp * kCoopBins + dg] + rank;
+                if (last) {
+                    a.svals[pos] = val;
+                    a.srect[pos] = a.rect[val];
+                } else {
+                    kout[pos] = key;
+                    vout[pos] = val;
+                    const uint32_t dn = (key >> (shift + dbits)) & dmask;
+                    atomicAdd(a.H + (size_t(p + 1) * kCoopGridMax + pos / S2) * kCoopBins + dn, 1u);
+                }
+            }
+            __syncthreads();
+        }
+        grid_sync(&misc->coop_bar, goal);
+    }
+
+    // ---------------------------------------------------------------- C2 chunk counts
+    const int nch = int((Vs + kChunk - 1) / kChunk);
+    {
+        const int GXp = a.GX + 1, cells = (a.GY + 1) * GXp;
+        const int g = tid >> 8, lt = tid & 255, gw = lt >> 5;
+        if (g < a.groups) {
+            int* diff = reinterpret_cast<int*>(dyn) + g * cells;
+            for (int c = k * a.groups + g; c < nch; c += G * a.groups) {
+                for (int i = lt; i < cells; i += 256) diff[i] = 0;
+                group_sync(g);
+                const uint32_t s = uint32_t(c) * kChunk + lt;
+                if (s < Vs) {
+                    const short4 r = __ldcg(a.srect + s);
+                    atomicAdd(&diff[r.z * GXp + r.x], 1);
+                    atomicAdd(&diff[r.z * GXp + r.y], -1);
+                    atomicAdd(&diff[r.w * GXp + r.x], -1);
+                    atomicAdd(&diff[r.w * GXp + r.y], 1);
+                }
+                group_sync(g);
+                for (int y = gw; y < a.GY; y += 8) {   // prefix along x: one warp per row
+                    int carry = 0;
+                    for (int x0 = 0; x0 < a.GX; x0 += 32) {
+                        const int x = x0 + lane;
+                        int v = x < a.GX ? diff[y * GXp + x] : 0;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int u = __shfl_up_sync(0xffffffffu, v, o);
+                            if (lane >= o) v += u;
+                        }
+                        v += carry;
+                        if (x < a.GX) diff[y * GXp + x] = v;
+                        carry = __shfl_sync(0xffffffffu, v, 31);
+                    }
+                }
+                group_sync(g);
+                uint32_t* row = a.cmat + size_t(c) * T;
+                for (int x = lt; x < a.GX; x += 256) {   // prefix along y, write counts
+                    int run = 0;
+                    for (int y = 0; y < a.GY; ++y) {
+                        run += diff[y * GXp + x];
+                        row[y * a.GX + x] = uint32_t(run);
+                    }
+                }
+                group_sync(g);
+            }
+        }
+    }
+    grid_sync(&misc->coop_bar, goal);
+
+    // ---------------------------------------------------------------- C3 segment sums, tile totals
+    const int ntg = (T + 31) / 32;
+    for (int item = k * kCW + warp; item < ntg * kCoopSegs; item += G * kCW) {
+        const int tg = item / kCoopSegs, seg = item % kCoopSegs;
+        const int t = tg * 32 + lane;
+        int c0, c1;
+        seg_range(nch, seg, c0, c1);
+        if (t < T) {
+            uint32_t sum = 0;
+#pragma unroll 8
+            for (int c = c0; c < c1; ++c) sum += ldcg(a.cmat + size_t(c) * T + t);
+            a.segsum[size_t(seg) * T + t] = sum;
+            if (sum) atomicAdd(a.tot + t, sum);
+        }
+    }
+    grid_sync(&misc->coop_bar, goal);
+
+    // ---------------------------------------------------------------- C4 tile scan and chunk bases
+    uint32_t* tstart = dyn;   // [T]
+    {
+        uint32_t carry = 0;
+        for (int b = 0; b < T; b += kCT) {
+            const int t = b + tid;
+            const uint32_t v = t < T ? ldcg(a.tot + t) : 0u;
+            uint32_t ex, agg;
+            BScan(bscan).ExclusiveSum(v, ex, agg);
+            if (t < T) {
+                tstart[t] = carry + ex;
+                if (k == 0) a.ranges[t] = v ? make_uint2(carry + ex, carry + ex + v) : make_uint2(0u, 0u);
+            }
+            carry += agg;
+            __syncthreads();
+        }
+        if (k == 0 && tid == 0) {
+            const unsigned long long K = carry;
+            misc->n_keys = K;
+            const bool over = K > (unsigned long long)a.key_cap;
+            misc->n_keys_eff = over ? 0ull : K;
+            if (over) atomicOr(&misc->error_flag, 1u);
+        }
+    }
+    for (int item = k * kCW + warp; item < ntg * kCoopSegs; item += G * kCW) {
+        const int tg = item / kCoopSegs, seg = item % kCoopSegs;
+        const int t = tg * 32 + lane;
+        int c0, c1;
+        seg_range(nch, seg, c0, c1);
+        if (t < T && c1 > c0) {
+            uint32_t run = tstart[t];
+            for (int q = 0; q < seg; ++q) run += ldcg(a.segsum + size_t(q) * T + t);
+            for (int cb = c0; cb < c1; cb += 8) {   // 8 loads in flight, then 8 stores
+                uint32_t v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = (cb + u < c1) ? ldcg(a.cmat + size_t(cb + u) * T + t) : 0u;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (cb + u < c1) a.cmat[size_t(cb + u) * T + t] = run;
+                    run += v[u];
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------ host driver
+struct CoopGeom {
+    int grid = 0;
+    size_t smem = 0;
+    int groups = 0;
+};
+
+static int coop_sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+    if (!cached[dev]) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+        cached[dev] = v;
+    }
+    return cached[dev];
+}
+
+gs_status run_bin_coop(WsState* s, cudaStream_t st) {
+    Misc* misc = at<Misc>(s, s->misc);
+    const int GX = s->cam_gx, GY = s->cam_gy, T = GX * GY;
+    const size_t cells = size_t(GX + 1) * (GY + 1) * sizeof(int);
+    constexpr size_t kSmemMax = 200 * 1024;
+    CoopGeom g;
+    g.groups = int(std::min<size_t>(kCGroups, kSmemMax / std::max<size_t>(cells, 1)));
+    if (g.groups < 1 || size_t(T) * 4 > kSmemMax) return GS_ERR_UNSUPPORTED;   // tile grid too large
+    g.smem = std::max({size_t(kCW) * kCoopBins * 4, size_t(g.groups) * cells, size_t(T) * 4});
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(bin_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemMax)) !=
+            cudaSuccess)
+            return check_launch(s, "bin_coop attribute");
+        attr = true;
+    }
+    const int sms = coop_sm_count();
+    if (sms <= 0) return check_launch(s, "bin_coop sm count");
+    g.grid = std::min(sms, kCoopGridMax);
+    CoopArgs a;
+    a.tiles = at<uint32_t>(s, s->tiles);
+    a.dkey = at<uint32_t>(s, s->depth_key);
+    a.rect = at<short4>(s, s->rect);
+    a.n = s->n;
+    a.GX = GX;
+    a.GY = GY;
+    a.key_cap = s->key_cap;
+    a.onlist = at<uint32_t>(s, s->onlist);
+    a.k0 = at<uint32_t>(s, s->dkey_sorted);
+    a.k1 = a.k0 + s->n_cap;
+    a.v0 = at<uint32_t>(s, s->dval_sorted);
+    a.v1 = a.v0 + s->n_cap;
+    a.svals = at<uint32_t>(s, s->svals);
+    a.srect = at<short4>(s, s->srect);
+    a.cmat = at<uint32_t>(s, s->chunk_mat);
+    uint32_t* c = at<uint32_t>(s, s->coop);
+    a.H = c;
+    a.hist_all = a.H + size_t(kCoopPasses) * kCoopGridMax * kCoopBins;
+    a.cta_cnt = a.hist_all + kCoopPasses * kCoopBins;
+    a.tot = a.cta_cnt + kCoopGridMax;
+    a.segsum = a.tot + size_t(s->GX) * s->GY;   // capacity tile grid (region layout)
+
+    a.ranges = at<uint2>(s, s->ranges);
+    a.misc = misc;
+    a.groups = g.groups;
+    void* args[] = {&a};
+    KTimer kt(s, KID_BIN_COOP, st);
+    const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bin_coop_kernel), dim3(g.grid),
+                                                      dim3(kCT), args, g.smem, st);
+    if (e != cudaSuccess) {
+        set_cuda_error(e, "bin_coop_kernel");
+        return GS_ERR_CUDA;
+    }
+    return GS_OK;
+}
+
+}  // namespace gs

@@ -11,6 +11,11 @@ namespace gs {
 constexpr int kTile = 16;                 // 16x16 pixel tiles (north_star)
 constexpr int kTilePx = kTile * kTile;    // 256 pixels = 256 threads per tile CTA
 constexpr int kRecFloats = 12;            // projected record: 3 x float4 (48 B)
+constexpr int kChunk = 256;               // path B: depth-ordered Gaussians per emission chunk
+constexpr int kCoopGridMax = 256;         // path B: CTAs of bin_coop_kernel (one per SM)
+constexpr int kCoopBins = 512;            // path B: depth-sort digit bins (<= 9-bit digits)
+constexpr int kCoopPasses = 4;            // path B: depth-sort passes at most (ceil(32 / 9))
+constexpr int kCoopSegs = 32;             // path B: chunk segments per tile in the tile scans
 
 // ------------------------------------------------------------------ workspace (host state)
 struct Region { uint64_t off, bytes; };
@@ -25,7 +30,7 @@ struct WsState {
     Region rec, depth_key, rect, radius, tiles, offsets, sgrad, scan_state,
         keys0, keys1, vals0, vals1, ranges, t_final, n_last, examined, sort_hist, sort_look,
         misc, scratch, scratch14, dkey_sorted, dval_sorted, chunk_hist, chunk_mat, srect, tile_tot, pose_part,
-        onlist, live_cnt;
+        onlist, live_cnt, svals, coop;
     // run state
     int64_t n;                     // Gaussians of the last gs_project
     int32_t cam_w, cam_h, cam_gx, cam_gy;   // image of the last gs_project
@@ -56,8 +61,11 @@ struct Misc {
     unsigned int scan_counter;
     unsigned int sort_counter[8];  // per-pass partition counters
     unsigned int n_onscreen;       // path B: Gaussians with tiles > 0
-    unsigned int pad_b;
-    unsigned long long n_items;    // path B: items of the depth sort (= n)
+    unsigned int coop_bar;         // path B: grid-barrier arrivals of bin_coop_kernel (zeroed per call)
+    unsigned long long n_items;    // path B: items of the depth sort (= V_s)
+    unsigned int kmin_inv;         // path B: ~min and max of the on-screen depth keys (atomicMax, zeroed)
+    unsigned int kmax;
+    unsigned int coop_pad[2];
     double loss_acc[4];            // |C-C*| sum, |D-D*| valid sum, valid count, spare
     double pose_acc[16];
     unsigned long long add_count;  // densify
@@ -71,7 +79,7 @@ struct Misc {
 enum KernelId {
     KID_PROJECT = 0, KID_SCAN, KID_EMIT, KID_SORT_HIST, KID_SORT_DSCAN, KID_SORT_PASS, KID_RANGES,
     KID_FWD, KID_BWD_TILE, KID_BWD_GAUSS, KID_POSE_FIN, KID_LOSS, KID_DENSIFY,
-    KID_DEPTH_SORT, KID_CHUNK_HIST, KID_CHUNK_SCAN, KID_BUCKET_EMIT, KID_COUNT
+    KID_DEPTH_SORT, KID_CHUNK_HIST, KID_CHUNK_SCAN, KID_BUCKET_EMIT, KID_BIN_COOP, KID_COUNT
 };
 
 // RAII bracket around one kernel launch: counts it and, when an event log is attached, records

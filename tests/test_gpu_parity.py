@@ -352,3 +352,56 @@ def test_no_host_sync_mode_matches():
     assert torch.equal(pipe.color, ref)
     a = pipe.arrays(n_keys=vals.numel())
     assert torch.equal(a["vals"], vals)
+
+
+# ------------------------------------------------------------------ depth-sort geometry edge cases
+def _bin_sort_check(p, v, cam):
+    pipe, P, V, fr = run_forward(p, v, cam)
+    a = pipe.arrays(p.shape[1])
+    dk = a["depth_key"].cpu().numpy().view(np.uint32)
+    rect = a["rect"].cpu().numpy().astype(np.int32).T.copy()
+    tiles = a["tiles"].cpu().numpy().view(np.uint32)
+    o = oracle.bin_sort(dk, rect, tiles, cam)
+    assert fr.n_keys == o["n_keys"]
+    assert np.array_equal(a["vals"].cpu().numpy().view(np.uint32), o["vals"])
+    assert np.array_equal(a["ranges"].cpu().numpy().view(np.uint32), o["ranges"])
+    return dk[tiles > 0]
+
+
+@pytest.mark.parametrize("kind", ["equal_depth", "wide_depth", "two_depths"])
+def test_bin_sort_depth_key_ranges(kind):
+    """Path B sorts only the depth-key bits that vary among on-screen Gaussians (bits of kmax - kmin
+    in passes of <= 9-bit digits): all-equal keys (0 varying bits, one copy pass, every pair a tie
+    kept by index), two distinct keys (1 bit), and keys spanning 0.25 m .. 2e4 m (> 27 bits, 4
+    passes). Lists must stay bit-exact with the oracle's stable sort."""
+    rng = np.random.default_rng(7)
+    cam = gi.CONFIGS[1].cam
+    n = 20000
+    p = np.zeros((14, n), np.float32)
+    if kind == "equal_depth":
+        z = np.full(n, 2.0)
+    elif kind == "two_depths":
+        z = np.where(rng.random(n) < 0.5, 2.0, 3.0)
+    else:
+        z = np.exp(rng.uniform(np.log(0.25), np.log(2e4), n))
+    p[2] = z
+    p[0] = rng.uniform(-0.6, 0.6, n) * z
+    p[1] = rng.uniform(-0.45, 0.45, n) * z
+    p[3:6] = (0.01 * z)[None, :] * rng.uniform(0.5, 2.0, (3, n))
+    p[6] = 1.0
+    p[10] = 0.5
+    p[11:14] = 0.5
+    dk = _bin_sort_check(p, gi.identity_view(), cam)
+    span = int(dk.max()) - int(dk.min())
+    if kind == "equal_depth":
+        assert span == 0
+    elif kind == "wide_depth":
+        assert span >= 1 << 27   # forces the 4-pass geometry
+
+
+def test_bin_sort_bitexact_2m_gaussians():
+    """Config-4 scale (2M Gaussians, the mapping workload): V_s far above config 2, several compaction
+    rounds per CTA and multi-round depth-sort slices. Lists bit-exact with the oracle."""
+    cfg = gi.CONFIGS[4]
+    p = cfg.scene()
+    _bin_sort_check(p, cfg.view(), cfg.cam)
