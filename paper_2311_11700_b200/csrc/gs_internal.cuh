@@ -137,6 +137,48 @@ gs_status run_densify(WsState* s, float* params, float* raw, int64_t* n_dev, int
 // ------------------------------------------------------------------ device helpers
 __device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
 
+// Packed fp32 pairs (sm_100 FADD2 / FMUL2 / FFMA2): one issue slot for two IEEE round-to-nearest
+// operations, each bit-identical to its scalar __fadd_rn / __fmul_rn / __fmaf_rn. The render kernels
+// keep two pixels per thread, so every per-pixel operation comes in pairs; a per-Gaussian scalar
+// operand is a broadcast pair, which ptxas encodes as a plain register (no extra move).
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float lo, float hi) {
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ f32x2 bc2(float v) { return pk2(v, v); }
+__device__ __forceinline__ float lo2(f32x2 v) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    return lo;
+}
+__device__ __forceinline__ float hi2(f32x2 v) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    return hi;
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+    f32x2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
 // Projected record (48 B): r0 = {mx, my, A, B}, r1 = {C, o, depth, q_max}, r2 = {r, g, b, -} with the
 // exactly scaled conic A = -a/2, B = -b, C = -c/2 (conic = Sigma'^-1 = [[a, b], [b, c]]).
 // alpha at pixel (px, py). Shared by the forward and both backward kernels so every decision is

@@ -195,6 +195,66 @@ __device__ __forceinline__ void blend_fast(PixState& p, float power, float4 r1, 
     p.nl = live ? j : p.nl;
 }
 
+// The same two steps for a PAIR of pixels (rows ly and ly + 8 of the thread), with the per-pixel
+// arithmetic in packed fp32 pairs (gs_internal.cuh): every operation is the scalar one above, per
+// pixel, in the same order and rounding, so results are bit-identical to blend_step / blend_fast.
+struct PixPair {
+    f32x2 T, Cr, Cg, Cb, D;   // lo = pixel A, hi = pixel B
+    uint32_t nlA, nlB, exA, exB;
+    bool dA, dB;
+};
+
+__device__ __forceinline__ f32x2 alpha_pair(f32x2 power, float o, f32x2& G) {
+    const f32x2 l = mul2(power, bc2(1.4426950408889634f));
+    float gA, gB;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(gA) : "f"(lo2(l)));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(gB) : "f"(hi2(l)));
+    G = pk2(gA, gB);
+    return mul2(bc2(o), G);   // o G
+}
+
+__device__ __forceinline__ void blend_fast_pair(PixPair& p, f32x2 power, float4 r1, float4 r2, uint32_t j) {
+    f32x2 G;
+    const f32x2 og = alpha_pair(power, r1.y, G);
+    const float a0A = fminf(0.99f, lo2(og)), a0B = fminf(0.99f, hi2(og));
+    const bool liveA = !p.dA && !(lo2(power) > 0.f) && a0A >= (1.0f / 255.0f);
+    const bool liveB = !p.dB && !(hi2(power) > 0.f) && a0B >= (1.0f / 255.0f);
+    const f32x2 a = pk2(liveA ? a0A : 0.f, liveB ? a0B : 0.f);
+    const f32x2 w = mul2(a, p.T);
+    p.Cr = fma2(w, bc2(r2.x), p.Cr);
+    p.Cg = fma2(w, bc2(r2.y), p.Cg);
+    p.Cb = fma2(w, bc2(r2.z), p.Cb);
+    p.D = fma2(w, bc2(r1.z), p.D);
+    p.T = mul2(p.T, sub2(bc2(1.f), a));
+    p.nlA = liveA ? j : p.nlA;
+    p.nlB = liveB ? j : p.nlB;
+}
+
+__device__ __forceinline__ void blend_step_pair(PixPair& p, f32x2 power, float4 r1, float4 r2, uint32_t j) {
+    f32x2 G;
+    const f32x2 og = alpha_pair(power, r1.y, G);
+    const float aA = fminf(0.99f, lo2(og)), aB = fminf(0.99f, hi2(og));
+    const bool liveA = !p.dA && !(lo2(power) > 0.f) && aA >= (1.0f / 255.0f);
+    const bool liveB = !p.dB && !(hi2(power) > 0.f) && aB >= (1.0f / 255.0f);
+    const f32x2 a = pk2(aA, aB);
+    const f32x2 Tn = mul2(p.T, sub2(bc2(1.f), a));
+    const bool termA = liveA && lo2(Tn) < 1e-4f, termB = liveB && hi2(Tn) < 1e-4f;
+    const bool blA = liveA && !(lo2(Tn) < 1e-4f), blB = liveB && !(hi2(Tn) < 1e-4f);
+    const f32x2 Ta = mul2(a, p.T);
+    const f32x2 w = pk2(blA ? lo2(Ta) : 0.f, blB ? hi2(Ta) : 0.f);
+    p.Cr = fma2(w, bc2(r2.x), p.Cr);
+    p.Cg = fma2(w, bc2(r2.y), p.Cg);
+    p.Cb = fma2(w, bc2(r2.z), p.Cb);
+    p.D = fma2(w, bc2(r1.z), p.D);
+    p.T = pk2(blA ? lo2(Tn) : lo2(p.T), blB ? hi2(Tn) : hi2(p.T));
+    p.nlA = blA ? j : p.nlA;
+    p.nlB = blB ? j : p.nlB;
+    p.exA = termA ? j : p.exA;
+    p.exB = termB ? j : p.exB;
+    p.dA = p.dA || termA;
+    p.dB = p.dB || termB;
+}
+
 constexpr int kFwd2Batch = kTilePx / 2;   // one staged record per thread
 
 // Can Gaussian (r0, r1) reach alpha >= 1/255 at any pixel of the box [x0, x1] x [y0, y1]? Conservative:
@@ -248,7 +308,8 @@ __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
     const uint2 rg = ranges[tile];
     const uint32_t start = rg.x, len = rg.y - rg.x;
     const int nbatch = int((len + kFwd2Batch - 1) / kFwd2Batch);
-    PixState A{1.f, 0.f, 0.f, 0.f, 0.f, 0u, len, !inA}, B{1.f, 0.f, 0.f, 0.f, 0.f, 0u, len, !inB};
+    PixPair P{bc2(1.f), bc2(0.f), bc2(0.f), bc2(0.f), bc2(0.f), 0u, 0u, len, len, !inA, !inB};
+    const f32x2 fy2 = pk2(fyA, fyB);
     uint32_t acc = 0;   // live entries written so far (this tile)
 
     auto stage = [&](int b) {
@@ -304,7 +365,7 @@ __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
         // warp restores the group's entry state and replays it with the exact step (rare: once
         // per pixel at most).
         constexpr int kU = 4;
-        auto entry = [&](int k0, int u, float4& r1, float4& r2, uint32_t& j, float& pA, float& pB) {
+        auto entry = [&](int k0, int u, float4& r1, float4& r2, uint32_t& j, f32x2& pw) {
             // past nlive: re-read slot 0 with zero opacity so the unrolled body stays branch-free
             const bool real = k0 + u < nlive;
             const int k = real ? s_live[k0 + u] : 0;
@@ -313,56 +374,52 @@ __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
             r2 = buf[k][2];
             if (!real) r1.y = 0.f;   // zero opacity -> alpha 0 -> skipped exactly
             j = uint32_t(b * kFwd2Batch + k + 1);
-            // same operation sequence as eval_alpha, x-terms shared between the two pixels
+            // eval_alpha's operation sequence per pixel; the x-terms are shared by the pair
             const float dx = __fsub_rn(r0.x, fpx);
             const float Adx = __fmul_rn(r0.z, dx), Bdx = __fmul_rn(r0.w, dx);
-            const float dyA = __fsub_rn(r0.y, fyA), dyB = __fsub_rn(r0.y, fyB);
-            pA = __fmaf_rn(Adx, dx, __fmaf_rn(__fmul_rn(r1.x, dyA), dyA, __fmul_rn(Bdx, dyA)));
-            pB = __fmaf_rn(Adx, dx, __fmaf_rn(__fmul_rn(r1.x, dyB), dyB, __fmul_rn(Bdx, dyB)));
+            const f32x2 dy = sub2(bc2(r0.y), fy2);
+            pw = fma2(bc2(Adx), bc2(dx), fma2(mul2(bc2(r1.x), dy), dy, mul2(bc2(Bdx), dy)));
         };
         for (int k0 = 0; k0 < nlive; k0 += kU) {
-            if (__all_sync(0xffffffffu, A.done && B.done)) break;
-            const PixState A0 = A, B0 = B;
+            if (__all_sync(0xffffffffu, P.dA && P.dB)) break;
+            const PixPair P0 = P;
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
                 float4 r1, r2;
                 uint32_t j;
-                float pA, pB;
-                entry(k0, u, r1, r2, j, pA, pB);
-                blend_fast(A, pA, r1, r2, j);
-                blend_fast(B, pB, r1, r2, j);
+                f32x2 pw;
+                entry(k0, u, r1, r2, j, pw);
+                blend_fast_pair(P, pw, r1, r2, j);
             }
-            if (__any_sync(0xffffffffu, A.T < 1e-4f || B.T < 1e-4f)) {
-                A = A0;
-                B = B0;
+            if (__any_sync(0xffffffffu, lo2(P.T) < 1e-4f || hi2(P.T) < 1e-4f)) {
+                P = P0;
 #pragma unroll
                 for (int u = 0; u < kU; ++u) {
                     float4 r1, r2;
                     uint32_t j;
-                    float pA, pB;
-                    entry(k0, u, r1, r2, j, pA, pB);
-                    blend_step(A, pA, r1, r2, j);
-                    blend_step(B, pB, r1, r2, j);
+                    f32x2 pw;
+                    entry(k0, u, r1, r2, j, pw);
+                    blend_step_pair(P, pw, r1, r2, j);
                 }
             }
         }
-        if (__syncthreads_and(A.done && B.done)) break;   // also orders buffer reuse
+        if (__syncthreads_and(P.dA && P.dB)) break;   // also orders buffer reuse
     }
     if (threadIdx.x == 0) live_cnt[tile] = acc;
     const size_t plane = size_t(W) * H;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-        const PixState& p = h ? B : A;
         if (!(h ? inB : inA)) continue;
+        const float T = h ? hi2(P.T) : lo2(P.T);
         const size_t pix = size_t(h ? pyB : pyA) * W + px;
-        color[pix] = fmaf(p.T, bgr, p.Cr);
-        color[plane + pix] = fmaf(p.T, bgg, p.Cg);
-        color[2 * plane + pix] = fmaf(p.T, bgb, p.Cb);
-        depth[pix] = p.D;
-        alpha[pix] = 1.f - p.T;
-        t_final[pix] = p.T;
-        n_last[pix] = p.nl;
-        if (examined) examined[pix] = p.exam;
+        color[pix] = fmaf(T, bgr, h ? hi2(P.Cr) : lo2(P.Cr));
+        color[plane + pix] = fmaf(T, bgg, h ? hi2(P.Cg) : lo2(P.Cg));
+        color[2 * plane + pix] = fmaf(T, bgb, h ? hi2(P.Cb) : lo2(P.Cb));
+        depth[pix] = h ? hi2(P.D) : lo2(P.D);
+        alpha[pix] = 1.f - T;
+        t_final[pix] = T;
+        n_last[pix] = h ? P.nlB : P.nlA;
+        if (examined) examined[pix] = h ? P.exB : P.exA;
     }
 }
 
@@ -419,42 +476,54 @@ constexpr int kRowsPerGroup = kTile / kGroups;
 constexpr int kSlots = 3;
 static_assert(kTile % kGroups == 0, "row groups must tile the 16 rows");
 
+static_assert(kRowsPerGroup == 2 && kGroups == 8, "phase 2 pairs rows ly and ly + 8 like phase 1");
+
+// Per-(pixel pair, Gaussian) values are stored as packed pairs: lo = pixel A (row ly), hi = pixel B
+// (row ly + 8) of thread ly * 16 + lx, so phase 2's lane (Gaussian, row group gi), whose two rows are
+// gi and gi + 8, reads exactly those pairs and accumulates them with packed fp32 operations.
 struct BwdSmem {
     float4 rec[kSlots][kBB][3];
-    float2 wg[kTilePx][kBB + 1];   // (alpha_i T_i, G dL/dalpha_i); 0 when skipped or clamped
-    float4 dl[kTilePx];            // dL/dC (r,g,b), dL/dD per pixel
-    float part[kGroups][10][kBB];  // per row-group pixel moments
-    float red[10][kBB];            // combined moments
+    f32x2 ww[kBwdThreads][kBB + 1];   // -(alpha_i T_i); 0 when skipped
+    f32x2 gg[kBwdThreads][kBB + 1];   // G dL/dalpha_i; 0 when skipped or clamped
+    f32x2 dl[kBwdThreads][4];         // dL/dC (r, g, b), dL/dD
+    float part[kGroups][10][kBB];     // per row-group pixel moments
+    float red[10][kBB];               // combined moments
     uint32_t idx[kSlots][kBB];
-    uint32_t pos[kSlots][kBB];     // 1-based list positions of the staged live entries (~0u: padding)
+    uint32_t pos[kSlots][kBB];        // 1-based list positions of the staged live entries (~0u: padding)
     uint32_t max_nl, len;
 };
 
-struct BwdPix {
-    float T, Q;        // T_{i+1} while walking back (starts at T_final); Q = S + T_f bg.dL/dC with the
-                       // suffix sum S_i = sum_{k>i} alpha_k T_k e_k
-    float4 dl;
-    uint32_t nl;
+struct BwdPair {
+    f32x2 T, Qn;              // T_{i+1} while walking back (starts at T_final); Qn = -(S + T_f bg.dL/dC)
+                              // with the suffix sum S_i = sum_{k>i} alpha_k T_k e_k
+    f32x2 dr, dg, db, dd;     // dL/dC, dL/dD
+    uint32_t nlA, nlB;
 };
 
-// One back-to-front step for one pixel; power in eval_alpha's order. A skipped entry (past n_last,
-// power > 0, alpha < 1/255, or padding) leaves T and S bitwise unchanged and yields (0, 0).
-__device__ __forceinline__ float2 bwd_step(BwdPix& p, float power, float4 r1, float4 r2, uint32_t pk) {
-    float G;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(G) : "f"(__fmul_rn(power, 1.4426950408889634f)));
-    const float og = __fmul_rn(r1.y, G);
-    const float a0 = fminf(0.99f, og);
-    const bool live = pk <= p.nl && !(power > 0.f) && a0 >= (1.0f / 255.0f);
-    const float a = live ? a0 : 0.f;
-    float ro;   // 1/(1 - alpha): MUFU rcp.approx (<= 1 ulp; gradients only, no decision)
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ro) : "f"(__fsub_rn(1.f, a)));
-    p.T = p.T * ro;   // skipped: alpha 0, rcp.approx(1) == 1, T unchanged
-    const float w = a * p.T;
-    const float ev = fmaf(r2.x, p.dl.x, fmaf(r2.y, p.dl.y, fmaf(r2.z, p.dl.z, r1.z * p.dl.w)));
-    const float ga = fmaf(p.T, ev, -p.Q * ro);   // dL/dalpha_i
-    const float go = (live && !(og > 0.99f)) ? G * ga : 0.f;
-    p.Q = fmaf(w, ev, p.Q);   // w == 0 when skipped: Q unchanged (ev finite; padding is zero-filled)
-    return make_float2(w, go);
+// One back-to-front step for the pixel pair; power in eval_alpha's order (the decisions match the
+// forward bit for bit). A skipped entry (past n_last, power > 0, alpha < 1/255, or padding) leaves T
+// and Q unchanged and yields (0, 0). Gradient arithmetic (no decisions) in packed pairs:
+//   T_i = T_{i+1} / (1 - alpha_i) (MUFU rcp.approx, <= 1 ulp), w = alpha_i T_i,
+//   e_i = c_i.dL/dC + d_i dL/dD, dL/dalpha_i = T_i e_i - Q / (1 - alpha_i), go = G dL/dalpha_i.
+__device__ __forceinline__ void bwd_step_pair(BwdPair& p, f32x2 power, float4 r1, float4 r2, uint32_t pk, f32x2& wn,
+                                              f32x2& go) {
+    f32x2 G;
+    const f32x2 og = alpha_pair(power, r1.y, G);
+    const float a0A = fminf(0.99f, lo2(og)), a0B = fminf(0.99f, hi2(og));
+    const bool liveA = pk <= p.nlA && !(lo2(power) > 0.f) && a0A >= (1.0f / 255.0f);
+    const bool liveB = pk <= p.nlB && !(hi2(power) > 0.f) && a0B >= (1.0f / 255.0f);
+    const f32x2 an = pk2(liveA ? -a0A : 0.f, liveB ? -a0B : 0.f);   // -alpha
+    const f32x2 om = add2(bc2(1.f), an);                              // 1 - alpha
+    float roA, roB;   // skipped: rcp.approx(1) == 1, T unchanged
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(roA) : "f"(lo2(om)));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(roB) : "f"(hi2(om)));
+    const f32x2 ro = pk2(roA, roB);
+    p.T = mul2(p.T, ro);
+    wn = mul2(an, p.T);
+    const f32x2 ev = fma2(bc2(r2.x), p.dr, fma2(bc2(r2.y), p.dg, fma2(bc2(r2.z), p.db, mul2(bc2(r1.z), p.dd))));
+    const f32x2 gG = mul2(G, fma2(p.T, ev, mul2(p.Qn, ro)));
+    go = pk2((liveA && !(lo2(og) > 0.99f)) ? lo2(gG) : 0.f, (liveB && !(hi2(og) > 0.99f)) ? hi2(gG) : 0.f);
+    p.Qn = fma2(wn, ev, p.Qn);   // wn == 0 when skipped: Q unchanged (ev finite; padding is zero-filled)
 }
 
 __global__ void __launch_bounds__(kBwdThreads, 4) render_bwd_kernel(
@@ -473,25 +542,42 @@ __global__ void __launch_bounds__(kBwdThreads, 4) render_bwd_kernel(
     const uint32_t start = ranges[tile].x;
     const size_t plane = size_t(W) * H;
 
-    auto load_pix = [&](BwdPix& p, int py, int q) {
-        p.nl = 0;
-        p.dl = make_float4(0.f, 0.f, 0.f, 0.f);
-        p.T = 1.f;
-        if (px < W && py < H) {
-            const size_t pix = size_t(py) * W + px;
-            p.nl = n_last[pix];
-            p.dl = make_float4(dLdC[pix], dLdC[plane + pix], dLdC[2 * plane + pix], dLdD[pix]);
-            p.T = t_final[pix];
+    BwdPair P;
+    {
+        float t[2] = {1.f, 1.f}, d[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+        uint32_t nl[2] = {0u, 0u};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int py = h ? pyB : pyA;
+            if (px < W && py < H) {
+                const size_t pix = size_t(py) * W + px;
+                nl[h] = n_last[pix];
+                d[h][0] = dLdC[pix];
+                d[h][1] = dLdC[plane + pix];
+                d[h][2] = dLdC[2 * plane + pix];
+                d[h][3] = dLdD[pix];
+                t[h] = t_final[pix];
+            }
         }
-        p.Q = p.T * (bgr * p.dl.x + bgg * p.dl.y + bgb * p.dl.z);   // S = 0 at the back
-        sm.dl[q] = p.dl;
-    };
-    BwdPix A, B;
+        P.T = pk2(t[0], t[1]);
+        P.dr = pk2(d[0][0], d[1][0]);
+        P.dg = pk2(d[0][1], d[1][1]);
+        P.db = pk2(d[0][2], d[1][2]);
+        P.dd = pk2(d[0][3], d[1][3]);
+        P.nlA = nl[0];
+        P.nlB = nl[1];
+        // S = 0 at the back: Q = T_f bg.dL/dC
+        P.Qn = pk2(-(t[0] * (bgr * d[0][0] + bgg * d[0][1] + bgb * d[0][2])),
+                   -(t[1] * (bgr * d[1][0] + bgg * d[1][1] + bgb * d[1][2])));
+        sm.dl[tid][0] = P.dr;
+        sm.dl[tid][1] = P.dg;
+        sm.dl[tid][2] = P.db;
+        sm.dl[tid][3] = P.dd;
+    }
+    const f32x2 fy2 = pk2(fyA, fyB);
     if (tid == 0) sm.max_nl = 0;
-    load_pix(A, pyA, tid);
-    load_pix(B, pyB, tid + kBwdThreads);
     __syncthreads();
-    uint32_t mnl = max(A.nl, B.nl);
+    uint32_t mnl = max(P.nlA, P.nlB);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mnl = max(mnl, __shfl_xor_sync(0xffffffffu, mnl, o));
     if (lane == 0 && mnl) atomicMax(&sm.max_nl, mnl);
@@ -556,59 +642,57 @@ __global__ void __launch_bounds__(kBwdThreads, 4) render_bwd_kernel(
         }
         __syncthreads();   // [A] batch staged
         // ---- phase 1
+        // records are read one step ahead (shared-memory latency off the dependent chain)
+        uint32_t pk_n = sm.pos[buf][kBB - 1];
+        float4 r0_n = sm.rec[buf][kBB - 1][0], r1_n = sm.rec[buf][kBB - 1][1], r2_n = sm.rec[buf][kBB - 1][2];
 #pragma unroll 4
         for (int k = kBB - 1; k >= 0; --k) {
-            const uint32_t pk = sm.pos[buf][k];
-            const float4 r0 = sm.rec[buf][k][0], r1 = sm.rec[buf][k][1], r2 = sm.rec[buf][k][2];
+            const uint32_t pk = pk_n;
+            const float4 r0 = r0_n, r1 = r1_n, r2 = r2_n;
+            const int kn = k > 0 ? k - 1 : 0;
+            pk_n = sm.pos[buf][kn];
+            r0_n = sm.rec[buf][kn][0];
+            r1_n = sm.rec[buf][kn][1];
+            r2_n = sm.rec[buf][kn][2];
             const float dx = __fsub_rn(r0.x, fpx);
             const float Adx = __fmul_rn(r0.z, dx), Bdx = __fmul_rn(r0.w, dx);
-            const float dyA = __fsub_rn(r0.y, fyA), dyB = __fsub_rn(r0.y, fyB);
-            const float pA = __fmaf_rn(Adx, dx, __fmaf_rn(__fmul_rn(r1.x, dyA), dyA, __fmul_rn(Bdx, dyA)));
-            const float pB = __fmaf_rn(Adx, dx, __fmaf_rn(__fmul_rn(r1.x, dyB), dyB, __fmul_rn(Bdx, dyB)));
-            sm.wg[tid][k] = bwd_step(A, pA, r1, r2, pk);
-            sm.wg[tid + kBwdThreads][k] = bwd_step(B, pB, r1, r2, pk);
+            const f32x2 dy = sub2(bc2(r0.y), fy2);
+            const f32x2 pw = fma2(bc2(Adx), bc2(dx), fma2(mul2(bc2(r1.x), dy), dy, mul2(bc2(Bdx), dy)));
+            f32x2 wn, go;
+            bwd_step_pair(P, pw, r1, r2, pk, wn, go);
+            sm.ww[tid][k] = wn;
+            sm.gg[tid][k] = go;
         }
-        __syncthreads();   // [B] wg complete
-        // ---- phase 2: moments over the group's rows, 16 pixels each, compile-time x
+        __syncthreads();   // [B] ww / gg complete
+        // ---- phase 2: moments over the group's two rows (gi, gi + 8) as packed pairs, compile-time x
         {
-            float S0 = 0.f, Sx = 0.f, Sxx = 0.f, Sy = 0.f, Sxy = 0.f, Syy = 0.f;
-            float Sr = 0.f, Sg = 0.f, Sb = 0.f, Sd = 0.f;
+            f32x2 R0 = bc2(0.f), Rx = bc2(0.f), Rxx = bc2(0.f);
+            f32x2 Sr = bc2(0.f), Sg = bc2(0.f), Sb = bc2(0.f), Sd = bc2(0.f);
 #pragma unroll
-            for (int r = 0; r < kRowsPerGroup; ++r) {
-                const int row = gi + kGroups * r;
-                float R0 = 0.f, Rx = 0.f, Rxx = 0.f;
-#pragma unroll
-                for (int x = 0; x < 16; ++x) {
-                    const int q = row * 16 + x;
-                    const float2 v = sm.wg[q][k2];
-                    const float4 d = sm.dl[q];
-                    R0 += v.y;
-                    Rx = fmaf(v.y, float(x), Rx);
-                    Rxx = fmaf(v.y, float(x * x), Rxx);
-                    Sr = fmaf(v.x, d.x, Sr);
-                    Sg = fmaf(v.x, d.y, Sg);
-                    Sb = fmaf(v.x, d.z, Sb);
-                    Sd = fmaf(v.x, d.w, Sd);
-                }
-                const float fy = float(row);
-                S0 += R0;
-                Sx += Rx;
-                Sxx += Rxx;
-                Sy = fmaf(fy, R0, Sy);
-                Sxy = fmaf(fy, Rx, Sxy);
-                Syy = fmaf(fy * fy, R0, Syy);
+            for (int x = 0; x < 16; ++x) {
+                const int q = gi * 16 + x;
+                const f32x2 g = sm.gg[q][k2];
+                const f32x2 w = sm.ww[q][k2];
+                R0 = add2(R0, g);
+                Rx = fma2(g, bc2(float(x)), Rx);
+                Rxx = fma2(g, bc2(float(x * x)), Rxx);
+                Sr = fma2(w, sm.dl[q][0], Sr);
+                Sg = fma2(w, sm.dl[q][1], Sg);
+                Sb = fma2(w, sm.dl[q][2], Sb);
+                Sd = fma2(w, sm.dl[q][3], Sd);
             }
+            const float fyA_ = float(gi), fyB_ = float(gi + kGroups);
             float* pp = &sm.part[gi][0][k2];
-            pp[0 * kBB] = S0;    // sum g
-            pp[1 * kBB] = Sx;    // sum g lx
-            pp[2 * kBB] = Sy;    // sum g ly
-            pp[3 * kBB] = Sxx;   // sum g lx^2
-            pp[4 * kBB] = Sxy;   // sum g lx ly
-            pp[5 * kBB] = Syy;   // sum g ly^2
-            pp[6 * kBB] = Sr;
-            pp[7 * kBB] = Sg;
-            pp[8 * kBB] = Sb;
-            pp[9 * kBB] = Sd;
+            pp[0 * kBB] = lo2(R0) + hi2(R0);                                   // sum g
+            pp[1 * kBB] = lo2(Rx) + hi2(Rx);                                   // sum g lx
+            pp[2 * kBB] = fyA_ * lo2(R0) + fyB_ * hi2(R0);                     // sum g ly
+            pp[3 * kBB] = lo2(Rxx) + hi2(Rxx);                                 // sum g lx^2
+            pp[4 * kBB] = fyA_ * lo2(Rx) + fyB_ * hi2(Rx);                     // sum g lx ly
+            pp[5 * kBB] = fyA_ * fyA_ * lo2(R0) + fyB_ * fyB_ * hi2(R0);       // sum g ly^2
+            pp[6 * kBB] = -(lo2(Sr) + hi2(Sr));                                // (ww holds -alpha T)
+            pp[7 * kBB] = -(lo2(Sg) + hi2(Sg));
+            pp[8 * kBB] = -(lo2(Sb) + hi2(Sb));
+            pp[9 * kBB] = -(lo2(Sd) + hi2(Sd));
         }
         __syncthreads();   // [C] partial sets complete
         for (int t = tid; t < 10 * kBB; t += kBwdThreads) {
