@@ -483,10 +483,10 @@ static_assert(kRowsPerGroup == 2 && kGroups == 8, "phase 2 pairs rows ly and ly 
 // gi and gi + 8, reads exactly those pairs and accumulates them with packed fp32 operations.
 struct BwdSmem {
     float4 rec[kSlots][kBB][3];
-    f32x2 ww[kBwdThreads][kBB + 1];   // -(alpha_i T_i); 0 when skipped
-    f32x2 gg[kBwdThreads][kBB + 1];   // G dL/dalpha_i; 0 when skipped or clamped
+    f32x2 ww[kBB][kBwdThreads + 1];   // -(alpha_i T_i); 0 when skipped (row padded: conflict-free)
+    f32x2 gg[kBB][kBwdThreads + 1];   // G dL/dalpha_i; 0 when skipped or clamped
     f32x2 dl[kBwdThreads][4];         // dL/dC (r, g, b), dL/dD
-    float part[kGroups][10][kBB];     // per row-group pixel moments
+    float part[kBwdWarps][10][kBB];   // per-warp pixel moments (its two row groups combined)
     float red[10][kBB];               // combined moments
     uint32_t idx[kSlots][kBB];
     uint32_t pos[kSlots][kBB];        // 1-based list positions of the staged live entries (~0u: padding)
@@ -526,7 +526,7 @@ __device__ __forceinline__ void bwd_step_pair(BwdPair& p, f32x2 power, float4 r1
     p.Qn = fma2(wn, ev, p.Qn);   // wn == 0 when skipped: Q unchanged (ev finite; padding is zero-filled)
 }
 
-__global__ void __launch_bounds__(kBwdThreads, 4) render_bwd_kernel(
+__global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
     const float4* __restrict__ rec, const uint32_t* __restrict__ live_g, const uint32_t* __restrict__ live_j,
     const uint32_t* __restrict__ live_cnt, const uint2* __restrict__ ranges, int W, int H,
     int GX, const float* __restrict__ t_final, float bgr, float bgg, float bgb, const uint32_t* __restrict__ n_last,
@@ -660,8 +660,8 @@ __global__ void __launch_bounds__(kBwdThreads, 4) render_bwd_kernel(
             const f32x2 pw = fma2(bc2(Adx), bc2(dx), fma2(mul2(bc2(r1.x), dy), dy, mul2(bc2(Bdx), dy)));
             f32x2 wn, go;
             bwd_step_pair(P, pw, r1, r2, pk, wn, go);
-            sm.ww[tid][k] = wn;
-            sm.gg[tid][k] = go;
+            sm.ww[k][tid] = wn;
+            sm.gg[k][tid] = go;
         }
         __syncthreads();   // [B] ww / gg complete
         // ---- phase 2: moments over the group's two rows (gi, gi + 8) as packed pairs, compile-time x
@@ -671,8 +671,8 @@ __global__ void __launch_bounds__(kBwdThreads, 4) render_bwd_kernel(
 #pragma unroll
             for (int x = 0; x < 16; ++x) {
                 const int q = gi * 16 + x;
-                const f32x2 g = sm.gg[q][k2];
-                const f32x2 w = sm.ww[q][k2];
+                const f32x2 g = sm.gg[k2][q];
+                const f32x2 w = sm.ww[k2][q];
                 R0 = add2(R0, g);
                 Rx = fma2(g, bc2(float(x)), Rx);
                 Rxx = fma2(g, bc2(float(x * x)), Rxx);
@@ -682,24 +682,31 @@ __global__ void __launch_bounds__(kBwdThreads, 4) render_bwd_kernel(
                 Sd = fma2(w, sm.dl[q][3], Sd);
             }
             const float fyA_ = float(gi), fyB_ = float(gi + kGroups);
-            float* pp = &sm.part[gi][0][k2];
-            pp[0 * kBB] = lo2(R0) + hi2(R0);                                   // sum g
-            pp[1 * kBB] = lo2(Rx) + hi2(Rx);                                   // sum g lx
-            pp[2 * kBB] = fyA_ * lo2(R0) + fyB_ * hi2(R0);                     // sum g ly
-            pp[3 * kBB] = lo2(Rxx) + hi2(Rxx);                                 // sum g lx^2
-            pp[4 * kBB] = fyA_ * lo2(Rx) + fyB_ * hi2(Rx);                     // sum g lx ly
-            pp[5 * kBB] = fyA_ * fyA_ * lo2(R0) + fyB_ * fyB_ * hi2(R0);       // sum g ly^2
-            pp[6 * kBB] = -(lo2(Sr) + hi2(Sr));                                // (ww holds -alpha T)
-            pp[7 * kBB] = -(lo2(Sg) + hi2(Sg));
-            pp[8 * kBB] = -(lo2(Sb) + hi2(Sb));
-            pp[9 * kBB] = -(lo2(Sd) + hi2(Sd));
+            float m[10];
+            m[0] = lo2(R0) + hi2(R0);                                 // sum g
+            m[1] = lo2(Rx) + hi2(Rx);                                 // sum g lx
+            m[2] = fyA_ * lo2(R0) + fyB_ * hi2(R0);                   // sum g ly
+            m[3] = lo2(Rxx) + hi2(Rxx);                               // sum g lx^2
+            m[4] = fyA_ * lo2(Rx) + fyB_ * hi2(Rx);                   // sum g lx ly
+            m[5] = fyA_ * fyA_ * lo2(R0) + fyB_ * fyB_ * hi2(R0);     // sum g ly^2
+            m[6] = -(lo2(Sr) + hi2(Sr));                              // (ww holds -alpha T)
+            m[7] = -(lo2(Sg) + hi2(Sg));
+            m[8] = -(lo2(Sb) + hi2(Sb));
+            m[9] = -(lo2(Sd) + hi2(Sd));
+            // lanes l and l + 16 hold the same Gaussian for the warp's two row groups
+#pragma unroll
+            for (int c = 0; c < 10; ++c) m[c] += __shfl_xor_sync(0xffffffffu, m[c], 16);
+            if (lane < kBB) {
+#pragma unroll
+                for (int c = 0; c < 10; ++c) sm.part[warp][c][k2] = m[c];
+            }
         }
         __syncthreads();   // [C] partial sets complete
         for (int t = tid; t < 10 * kBB; t += kBwdThreads) {
             const int c = t / kBB, k = t % kBB;
             float a = 0.f;
 #pragma unroll
-            for (int p = 0; p < kGroups; ++p) a += sm.part[p][c][k];
+            for (int p = 0; p < kBwdWarps; ++p) a += sm.part[p][c][k];
             sm.red[c][k] = a;
         }
         __syncthreads();   // [D] moments complete
@@ -743,6 +750,8 @@ void launch_render_bwd_tiles(WsState* s, const gs_camera& cam, const float*, con
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(render_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem)));
+        cudaFuncSetAttribute(render_bwd_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             int(cudaSharedmemCarveoutMaxShared));
         attr = true;
     }
     KTimer kt(s, KID_BWD_TILE, st);
