@@ -265,8 +265,8 @@ def main_ours(args):
                                   f"fwd+bwd L1 (0.9/0.1) iteration", "n_gaussians": n, "width": cam.width,
                       "height": cam.height, "keys": K, "visible": V_front, "on_screen": V_s, "E_f": E_f, "E_b": E_b,
                       "E_f_live": Lf, "E_b_live": Lb,
-                      "binsort": args.binsort, "l2": "per-iteration working set > L2 (keys+values ~"
-                      f"{K * 24 / 1e9:.2f} GB); no flush", "parallelism": f"replicas x{world}"},
+                      "binsort": args.binsort, "l2": "per-iteration working set > L2 (126 MB): tile lists "
+                      f"{K * 4 / 1e9:.2f} GB + live lists; no flush", "parallelism": f"replicas x{world}"},
            "evals_per_s": world * (E_f + E_b) * 1000.0 / ms, "clocks": clocks, "gpu_launches": int(launches)}
 
     if not args.quick:
@@ -285,8 +285,9 @@ def main_ours(args):
         out["kernels_ms_per_step"] = {k: round(v_[0], 4) for k, v_ in sorted(per_step.items(), key=lambda x: -x[1][0])}
         out["kernels_launches_per_step"] = {k: v_[1] for k, v_ in per_step.items()}
         out["ms_per_step_with_event_log"] = ms_logged
-        out["roofline"] = roofline(per_step, clocks, K=K, n=n, V_s=V_s, E_f=Lf, E_b=Lb,
-                                   npx=cam.width * cam.height, binsort=args.binsort)
+        out["roofline"], out["kernels_roofline"] = roofline(
+            per_step, clocks, K=K, n=n, V_s=V_s, E_f=Lf, E_b=Lb, npx=cam.width * cam.height, binsort=args.binsort,
+            GX=(cam.width + 15) // 16, GY=(cam.height + 15) // 16)
         # ---- e2e through the public API with host buffers (pinned) and a loss readback
         if not args.no_e2e:
             # every step uploads its inputs (params, pose, RGB-D target) from pinned host memory and
@@ -379,40 +380,50 @@ def live_evals(a, cam):
     return count(a["examined"]), count(a["n_last"])
 
 
-def roofline(per_step, clocks, K, n, V_s, E_f, E_b, npx, binsort="bucket"):
+def roofline(per_step, clocks, K, n, V_s, E_f, E_b, npx, binsort="bucket", GX=75, GY=43):
+    """Roofline of the dominant kernel (the JSON line's "roofline") plus the same figures for every
+    kernel with a defined algorithmic work (the line's "kernels_roofline"). Work per unit: DESIGN.md §6."""
     peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json"), {}) or {}
     hbm_peak = peaks.get("hbm_gbs")
     hbm_src = "measured" if hbm_peak else "fallback"
     hbm_peak = hbm_peak or 6650.0
     sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz") or 1965.0
     alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e12   # FP32 lane-ops/s, T
-    T = ((1200 + 15) // 16) * ((680 + 15) // 16)
+    T = GX * GY
+    nch = (V_s + 255) // 256
     work = {   # (bound, algorithmic amount PER LAUNCH, unit) -- DESIGN.md §6 table
         "render_bwd_tiles": ("alu", E_b * BWD_OPS_PER_EVAL / 1e12, "TFLOP/s"),
         "render_fwd": ("alu", E_f * FWD_OPS_PER_EVAL / 1e12, "TFLOP/s"),
-        # path A sorts K (u64, u32) pairs per pass; path B sorts n (u32, u32) depth pairs per pass
-        "sort_pass": ("hbm", (K * SORT_BYTES_PER_KEY if binsort == "keys" else n * 16) / 1e9, "GB/s"),
+        # path A sorts K (u64, u32) pairs per pass
+        "sort_pass": ("hbm", K * SORT_BYTES_PER_KEY / 1e9, "GB/s"),
         "emit_keys": ("hbm", (K * 12 + n * 20) / 1e9, "GB/s"),
+        # path B: the list itself (4 B per key) plus the per-Gaussian reads
         "bucket_emit": ("hbm", (K * 4 + V_s * 12) / 1e9, "GB/s"),
+        # compaction (8 B read per Gaussian, 12 B written per on-screen one), 3 depth-sort passes over
+        # (key, value) pairs (16 B per on-screen Gaussian each), sorted rects (16 B), chunk-count
+        # matrix written, read twice and rewritten (16 B per chunk and tile)
+        "bin_coop": ("hbm", (n * 8 + V_s * (12 + 3 * 16 + 16) + nch * T * 16) / 1e9, "GB/s"),
         "project": ("hbm", n * (56 + 72) / 1e9, "GB/s"),
         "gaussian_bwd": ("hbm", (n * 4 + V_s * 244) / 1e9, "GB/s"),
         "loss_l1": ("hbm", npx * 24 / 1e9, "GB/s"),
     }
-    dom = max((k for k in per_step if k in work), key=lambda k: per_step[k][0])
-    bound, per_launch_amount, unit = work[dom]
-    t_ms, launches = per_step[dom]
-    per_launch_s = t_ms / 1e3 / max(launches, 1)
-    achieved = per_launch_amount / per_launch_s
-    peak = alu_peak if bound == "alu" else hbm_peak
-    traffic = None
     prof = load_json(os.path.join(ROOT, "profiles", "ncu_traffic.json"), {}) or {}
-    if dom in prof:
-        traffic = prof[dom]
-    return {"kernel": dom, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-            "frac": achieved / peak, "traffic": traffic,
-            "peak_source": ("FP32 148 SMs x 128 lanes x measured median SM clock %.0f MHz" % sm_mhz)
-            if bound == "alu" else f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})",
-            "share_of_step": t_ms / sum(v[0] for v in per_step.values())}
+    table = {}
+    for k, (bound, amount, unit) in work.items():
+        if k not in per_step:
+            continue
+        t_ms, launches = per_step[k]
+        achieved = amount / (t_ms / 1e3 / max(launches, 1))
+        peak = alu_peak if bound == "alu" else hbm_peak
+        table[k] = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+                    "traffic": prof.get(k), "share_of_step": t_ms / sum(v[0] for v in per_step.values())}
+    dom = max(table, key=lambda k: per_step[k][0])
+    top = dict(table[dom])
+    top["kernel"] = dom
+    top["peak_source"] = (("FP32 148 SMs x 128 lanes x measured median SM clock %.0f MHz" % sm_mhz)
+                          if top["bound"] == "alu" else f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})")
+    return top, {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
+                 for k, v in table.items()}
 
 
 def _timed_events(fn, steps):

@@ -465,9 +465,9 @@ void launch_render_fwd(WsState* s, const gs_camera& cam, float* color, float* de
 //            (alpha_i T_i, G dL/dalpha_i) per (pixel, Gaussian) into shared memory (branch-free:
 //            after the live-list skip ~97 % of the walked evaluations blend at config 2)
 //   phase 2  lane = (Gaussian, row group): pixel moments with compile-time x
-//   combine  the row-group partial sets, then one thread per (component, Gaussian) turns moments
-//            into the screen-space gradient and issues its atomic.
-// The staged batches rotate through 3 slots, so a batch needs 4 block barriers and none at its end.
+//   combine  one thread per (component, Gaussian) sums the per-warp partial moments it needs, turns
+//            them into the screen-space gradient and issues its atomic.
+// The staged batches rotate through 3 slots, so a batch needs 3 block barriers and none at its end.
 constexpr int kBB = 16;                          // Gaussians per backward batch
 constexpr int kBwdThreads = kTilePx / 2;         // 128
 constexpr int kBwdWarps = kBwdThreads / 32;
@@ -487,7 +487,6 @@ struct BwdSmem {
     f32x2 gg[kBB][kBwdThreads + 1];   // G dL/dalpha_i; 0 when skipped or clamped
     f32x2 dl[kBwdThreads][4];         // dL/dC (r, g, b), dL/dD
     float part[kBwdWarps][10][kBB];   // per-warp pixel moments (its two row groups combined)
-    float red[10][kBB];               // combined moments
     uint32_t idx[kSlots][kBB];
     uint32_t pos[kSlots][kBB];        // 1-based list positions of the staged live entries (~0u: padding)
     uint32_t max_nl, len;
@@ -702,24 +701,24 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
             }
         }
         __syncthreads();   // [C] partial sets complete
-        for (int t = tid; t < 10 * kBB; t += kBwdThreads) {
-            const int c = t / kBB, k = t % kBB;
+        // ---- moments -> screen-space gradients; one thread and one atomic per (component, Gaussian).
+        // Each thread sums the per-warp partial sets it needs (no separate combine pass and barrier:
+        // part is rewritten only after the next batch's barriers [A] and [B]).
+        const int cnt = min(kBB, int(len) - bb * kBB);
+        auto moment = [&](int c, int k) {
             float a = 0.f;
 #pragma unroll
             for (int p = 0; p < kBwdWarps; ++p) a += sm.part[p][c][k];
-            sm.red[c][k] = a;
-        }
-        __syncthreads();   // [D] moments complete
-        // ---- moments -> screen-space gradients; one thread and one atomic per (component, Gaussian)
-        const int cnt = min(kBB, int(len) - bb * kBB);
+            return a;
+        };
         for (int t = tid; t < 10 * kBB; t += kBwdThreads) {
             const int c = t / kBB, k = t % kBB;
             if (k >= cnt) continue;
             float v;
             if (c >= 5) {
-                v = sm.red[c == 5 ? 0 : c][k];   // opacity (sum g), rgb, depth
+                v = moment(c == 5 ? 0 : c, k);   // opacity (sum g), rgb, depth
             } else {
-                const float M0 = sm.red[0][k], Mx = sm.red[1][k], My = sm.red[2][k];
+                const float M0 = moment(0, k), Mx = moment(1, k), My = moment(2, k);
                 const float4 r0 = sm.rec[buf][k][0];
                 const float o = sm.rec[buf][k][1].y;
                 const float X = r0.x - float(tx * kTile), Y = r0.y - float(ty * kTile);
@@ -730,11 +729,11 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
                 } else if (c == 1) {
                     v = o * (r0.w * gdx + 2.f * sm.rec[buf][k][1].x * gdy);   // mean2d y: -o (b gdx + c gdy)
                 } else if (c == 2) {
-                    v = -0.5f * o * (X * X * M0 - 2.f * X * Mx + sm.red[3][k]);            // conic a
+                    v = -0.5f * o * (X * X * M0 - 2.f * X * Mx + moment(3, k));            // conic a
                 } else if (c == 3) {
-                    v = -o * (X * Y * M0 - X * My - Y * Mx + sm.red[4][k]);                 // conic b
+                    v = -o * (X * Y * M0 - X * My - Y * Mx + moment(4, k));                 // conic b
                 } else {
-                    v = -0.5f * o * (Y * Y * M0 - 2.f * Y * My + sm.red[5][k]);            // conic c
+                    v = -0.5f * o * (Y * Y * M0 - 2.f * Y * My + moment(5, k));            // conic c
                 }
             }
             if (v != 0.f) atomicAdd(sgrad + c * sld + sm.idx[buf][k], v);
