@@ -71,7 +71,8 @@ struct Misc {
     unsigned long long add_count;  // densify
     unsigned long long keep_count;
     unsigned int chunk_counter;
-    unsigned int pad[3];
+    unsigned int pose_done;        // gaussian_bwd last-block ticket (self-resetting)
+    unsigned int pad[2];
 };
 
 // ------------------------------------------------------------------ launch helpers
