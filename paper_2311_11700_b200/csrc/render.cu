@@ -296,9 +296,10 @@ __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
     uint32_t* __restrict__ live_cnt) {
     using BS = cub::BlockScan<int, kFwd2Batch>;
     __shared__ typename BS::TempStorage scan_tmp;
-    __shared__ float4 s_rec[2][kFwd2Batch][3];
+    constexpr int kU = 4;   // Gaussians per fast-path group (below)
+    __shared__ float4 s_rec[2][kFwd2Batch + 1][3];   // slot kFwd2Batch: a zero record (padding entry)
     __shared__ uint32_t s_g[2][kFwd2Batch];
-    __shared__ int s_live[kFwd2Batch];
+    __shared__ int s_live[kFwd2Batch + kU];          // padded to a multiple of kU with the zero slot
     __shared__ int s_nlive;
     const int tile = blockIdx.x;
     const int tx = tile % GX, ty = tile / GX;
@@ -333,6 +334,7 @@ __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
         }
         cp_async_commit();
     };
+    if (threadIdx.x < 6) s_rec[threadIdx.x / 3][kFwd2Batch][threadIdx.x % 3] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (nbatch > 0) stage(0);
     for (int b = 0; b < nbatch; ++b) {
         if (b + 1 < nbatch) {
@@ -356,6 +358,7 @@ __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
                 live_g[start + acc + off] = s_g[b & 1][k];
                 live_j[start + acc + off] = uint32_t(b * kFwd2Batch + k + 1);
             }
+            if (k >= tot && k < ((tot + kU - 1) & ~(kU - 1))) s_live[k] = kFwd2Batch;   // zero record: alpha 0
             if (k == 0) s_nlive = tot;
             __syncthreads();
         }
@@ -366,16 +369,14 @@ __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
         // after the group is >= 1e-4, every T (1 - alpha) tested inside it was too. Otherwise the
         // warp restores the group's entry state and replays it with the exact step (rare: once
         // per pixel at most).
-        constexpr int kU = 4;
+        const uint32_t jb = uint32_t(b * kFwd2Batch + 1);
         auto entry = [&](int k0, int u, float4& r1, float4& r2, uint32_t& j, f32x2& pw) {
-            // past nlive: re-read slot 0 with zero opacity so the unrolled body stays branch-free
-            const bool real = k0 + u < nlive;
-            const int k = real ? s_live[k0 + u] : 0;
+            // past nlive the list is padded with the zero slot: opacity 0 -> alpha 0 -> skipped exactly
+            const int k = s_live[k0 + u];
             const float4 r0 = buf[k][0];
             r1 = buf[k][1];
             r2 = buf[k][2];
-            if (!real) r1.y = 0.f;   // zero opacity -> alpha 0 -> skipped exactly
-            j = uint32_t(b * kFwd2Batch + k + 1);
+            j = jb + uint32_t(k);
             // eval_alpha's operation sequence per pixel; the x-terms are shared by the pair
             const float dx = __fsub_rn(r0.x, fpx);
             const float Adx = __fmul_rn(r0.z, dx), Bdx = __fmul_rn(r0.w, dx);
