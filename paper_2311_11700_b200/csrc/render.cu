@@ -486,8 +486,8 @@ static_assert(kRowsPerGroup == 2 && kGroups == 8, "phase 2 pairs rows ly and ly 
 // gi and gi + 8, reads exactly those pairs and accumulates them with packed fp32 operations.
 struct BwdSmem {
     float4 rec[kSlots][kBB][3];
-    f32x2 ww[kBB][kBwdThreads + 1];   // -(alpha_i T_i); 0 when skipped (row padded: conflict-free)
-    f32x2 gg[kBB][kBwdThreads + 1];   // G dL/dalpha_i; 0 when skipped or clamped
+    float4 wg[kBB][kBwdThreads + 1];  // (-(alpha_i T_i) pair, G dL/dalpha_i pair); 0 when skipped, the
+                                      // second also when clamped (rows padded: conflict-free)
     f32x2 dl[kBwdThreads][4];         // dL/dC (r, g, b), dL/dD
     float part[kBwdWarps][10][kBB];   // per-warp pixel moments (its two row groups combined)
     uint32_t idx[kSlots][kBB];
@@ -523,8 +523,9 @@ __device__ __forceinline__ void bwd_step_pair(BwdPair& p, f32x2 power, float4 r1
     p.T = mul2(p.T, ro);
     wn = mul2(an, p.T);
     const f32x2 ev = fma2(bc2(r2.x), p.dr, fma2(bc2(r2.y), p.dg, fma2(bc2(r2.z), p.db, mul2(bc2(r1.z), p.dd))));
-    const f32x2 gG = mul2(G, fma2(p.T, ev, mul2(p.Qn, ro)));
-    go = pk2((liveA && !(lo2(og) > 0.99f)) ? lo2(gG) : 0.f, (liveB && !(hi2(og) > 0.99f)) ? hi2(gG) : 0.f);
+    // gradient to o and power only when live and not clamped: G masked in place (no select after)
+    const f32x2 Gm = pk2((liveA && !(lo2(og) > 0.99f)) ? lo2(G) : 0.f, (liveB && !(hi2(og) > 0.99f)) ? hi2(G) : 0.f);
+    go = mul2(Gm, fma2(p.T, ev, mul2(p.Qn, ro)));
     p.Qn = fma2(wn, ev, p.Qn);   // wn == 0 when skipped: Q unchanged (ev finite; padding is zero-filled)
 }
 
@@ -662,10 +663,9 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
             const f32x2 pw = fma2(bc2(Adx), bc2(dx), fma2(mul2(bc2(r1.x), dy), dy, mul2(bc2(Bdx), dy)));
             f32x2 wn, go;
             bwd_step_pair(P, pw, r1, r2, pk, wn, go);
-            sm.ww[k][tid] = wn;
-            sm.gg[k][tid] = go;
+            sm.wg[k][tid] = make_float4(lo2(wn), hi2(wn), lo2(go), hi2(go));
         }
-        __syncthreads();   // [B] ww / gg complete
+        __syncthreads();   // [B] wg complete
         // ---- phase 2: moments over the group's two rows (gi, gi + 8) as packed pairs, compile-time x
         {
             f32x2 R0 = bc2(0.f), Rx = bc2(0.f), Rxx = bc2(0.f);
@@ -673,8 +673,8 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
 #pragma unroll
             for (int x = 0; x < 16; ++x) {
                 const int q = gi * 16 + x;
-                const f32x2 g = sm.gg[k2][q];
-                const f32x2 w = sm.ww[k2][q];
+                const float4 v = sm.wg[k2][q];
+                const f32x2 w = pk2(v.x, v.y), g = pk2(v.z, v.w);
                 R0 = add2(R0, g);
                 Rx = fma2(g, bc2(float(x)), Rx);
                 Rxx = fma2(g, bc2(float(x * x)), Rxx);
@@ -691,7 +691,7 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
             m[3] = lo2(Rxx) + hi2(Rxx);                               // sum g lx^2
             m[4] = fyA_ * lo2(Rx) + fyB_ * hi2(Rx);                   // sum g lx ly
             m[5] = fyA_ * fyA_ * lo2(R0) + fyB_ * fyB_ * hi2(R0);     // sum g ly^2
-            m[6] = -(lo2(Sr) + hi2(Sr));                              // (ww holds -alpha T)
+            m[6] = -(lo2(Sr) + hi2(Sr));                              // (wg holds -alpha T)
             m[7] = -(lo2(Sg) + hi2(Sg));
             m[8] = -(lo2(Sb) + hi2(Sb));
             m[9] = -(lo2(Sd) + hi2(Sd));
