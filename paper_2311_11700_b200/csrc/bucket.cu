@@ -39,7 +39,7 @@ gs_status resolve_keys(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t
 // up to 4 chunks ahead of the slowest one instead of meeting it at a barrier every chunk.
 constexpr int kWX = 8, kWY = 4;        // consumer tile area (lane j = tile (j & 7, j >> 3))
 constexpr int kBX = 16, kBY = 16;      // block tile area: 2 x 4 consumer areas
-constexpr int kEmitChunkBlocks = 96;   // grid.x: chunk stride
+constexpr int kEmitChunkBlocks = 256;  // grid.x: chunk stride (measured: 96 -> 0.091 ms, 224-320 -> 0.081 ms)
 constexpr int kRing = 4;               // chunk slots in flight
 constexpr int kConsumers = 8;
 
