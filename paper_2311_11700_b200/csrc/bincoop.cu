@@ -17,9 +17,11 @@
 //       rect srect[s] instead of keys.
 //   C2  chunk counts: per 256-Gaussian chunk of svals, a 2-D difference array over the tile grid in
 //       shared memory -> count[c][t] (4 chunks per CTA in flight)
-//   C3  per-(tile, chunk segment) sums and tile totals (atomics) -> barrier ->
-//   C4  exclusive scan of the tile totals (ranges = a5, K, capacity flag) and the exclusive scans over
-//       chunks: count[c][t] is replaced by base[c][t] = start of chunk c's entries in tile t's list.
+//   C3  per tile group (CTA) and chunk segment (warp): segment sums, their exclusive prefix over the
+//       tile's segments and the tile totals, in shared memory -> barrier ->
+//   C4  per tile group: its start (sum of all earlier totals), the tiles' starts (ranges = a5, K,
+//       capacity flag) and the exclusive scans over chunks: count[c][t] is replaced by
+//       base[c][t] = start of chunk c's entries in tile t's list.
 // The grid barrier is the cooperative-groups pattern (block barrier, one thread fences and arrives
 // on a monotone counter, spins on an acquire load); cudaLaunchCooperativeKernel guarantees that all
 // CTAs are co-resident. Data produced inside the kernel is read with ld.global.cg (L2), never
@@ -36,6 +38,9 @@ constexpr int kCT = 1024;                // threads per CTA
 constexpr int kCW = kCT / 32;            // warps per CTA
 constexpr int kDigitBits = 9;            // <= 9-bit digits (kCoopBins = 512)
 constexpr int kCGroups = 4;              // chunk-count groups of 256 threads
+constexpr int kRounds = 4;               // compaction: 1024-element rounds loaded at once
+static_assert(kRounds * kCW <= kCT, "one scan over the (round, warp) counts");
+static_assert(kCoopSegs == kCW, "C3/C4: one warp per chunk segment");
 
 struct CoopArgs {
     const uint32_t* tiles;   // [n] tiles touched (gs_project)
@@ -53,7 +58,7 @@ struct CoopArgs {
     uint32_t* hist_all;      // [kCoopPasses][kCoopBins] per-pass digit totals
     uint32_t* cta_cnt;       // [kCoopGridMax] on-screen count per compaction slice
     uint32_t* tot;           // [T] tile totals
-    uint32_t* segsum;        // [kCoopSegs][T]
+    uint32_t* segsum;        // [kCoopSegs][T] exclusive prefix of a tile's chunk-segment sums
     uint2* ranges;           // [T]
     Misc* misc;
     int groups;              // chunk-count groups per CTA (shared-memory bound)
@@ -92,6 +97,8 @@ __global__ void __launch_bounds__(kCT, 1) bin_coop_kernel(CoopArgs a) {
     __shared__ uint32_t s_hist[kCoopPasses][kCoopBins];
     __shared__ uint32_t s_run[kCoopBins], s_gpos[kCoopBins];
     __shared__ uint32_t s_u[8];
+    __shared__ uint32_t s_wc[kCW];
+    __shared__ uint32_t s_rw[kRounds * kCW];   // per-(round, warp) on-screen counts -> offsets
     const int G = gridDim.x, k = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int T = a.GX * a.GY;
     Misc* misc = a.misc;
@@ -103,37 +110,50 @@ __global__ void __launch_bounds__(kCT, 1) bin_coop_kernel(CoopArgs a) {
         for (int64_t i = int64_t(k) * kCT + tid; i < nz1; i += int64_t(G) * kCT)
             if (i >= int64_t(kCoopGridMax) * kCoopBins) a.H[i] = 0u;
         for (int i = k * kCT + tid; i < kCoopPasses * kCoopBins; i += G * kCT) a.hist_all[i] = 0u;
-        for (int i = k * kCT + tid; i < T; i += G * kCT) a.tot[i] = 0u;
     }
     // ---------------------------------------------------------------- C0 compaction: count
+    // Slices are read kRounds x 1024 elements at a time, all loads in flight before any use.
     const int64_t S1 = (a.n + G - 1) / G;
     const int64_t b0 = min(a.n, int64_t(k) * S1), b1 = min(a.n, b0 + S1);
     uint32_t kmin = 0xffffffffu, kmax = 0u, cnt = 0;
     if (tid == 0) { s_u[0] = 0xffffffffu; s_u[1] = 0u; }
-    __syncthreads();
-    for (int64_t r0 = b0; r0 < b1; r0 += kCT) {
-        const int64_t i = r0 + tid;
-        const bool f = i < b1 && a.tiles[i] > 0u;
-        if (f) {
-            const uint32_t key = a.dkey[i];
-            kmin = min(kmin, key);
-            kmax = max(kmax, key);
+    for (int64_t r0 = b0; r0 < b1; r0 += int64_t(kRounds) * kCT) {
+        uint32_t tl[kRounds], dk[kRounds];
+#pragma unroll
+        for (int r = 0; r < kRounds; ++r) {
+            const int64_t i = r0 + int64_t(r) * kCT + tid;
+            tl[r] = i < b1 ? a.tiles[i] : 0u;
+            dk[r] = i < b1 ? a.dkey[i] : 0u;
         }
-        cnt += uint32_t(__syncthreads_count(f));
+#pragma unroll
+        for (int r = 0; r < kRounds; ++r) {
+            if (tl[r] > 0u) {
+                kmin = min(kmin, dk[r]);
+                kmax = max(kmax, dk[r]);
+                ++cnt;
+            }
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
         kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     }
-    if (lane == 0 && kmax >= kmin) {
-        atomicMin(&s_u[0], kmin);
-        atomicMax(&s_u[1], kmax);
+    __syncthreads();
+    if (lane == 0) {
+        if (kmax >= kmin) {
+            atomicMin(&s_u[0], kmin);
+            atomicMax(&s_u[1], kmax);
+        }
+        s_wc[warp] = cnt;
     }
     __syncthreads();
     if (tid == 0) {
-        a.cta_cnt[k] = cnt;
-        if (cnt) {
+        uint32_t c = 0;
+        for (int w = 0; w < kCW; ++w) c += s_wc[w];
+        a.cta_cnt[k] = c;
+        if (c) {
             atomicMax(&misc->kmin_inv, ~s_u[0]);
             atomicMax(&misc->kmax, s_u[1]);
         }
@@ -170,24 +190,44 @@ __global__ void __launch_bounds__(kCT, 1) bin_coop_kernel(CoopArgs a) {
     const uint32_t S2 = (Vs + G - 1) / G;
 
     // ---------------------------------------------------------------- C0 compaction: ordered writes
+    // Per batch of kRounds x 1024 elements: ballots give each (round, warp) its count; one scan over
+    // the kRounds x 32 counts, in element order, places every on-screen element.
     for (int i = tid; i < kCoopPasses * kCoopBins; i += kCT) (&s_hist[0][0])[i] = 0u;
-    __syncthreads();
     {
-        uint32_t r = base_k;
-        for (int64_t r0 = b0; r0 < b1; r0 += kCT) {
-            const int64_t i = r0 + tid;
-            const bool f = i < b1 && a.tiles[i] > 0u;
-            uint32_t off, agg;
-            BScan(bscan).ExclusiveSum(f ? 1u : 0u, off, agg);
-            if (f) {
-                const uint32_t key = a.dkey[i] - key_lo;
-                a.onlist[r + off] = uint32_t(i);
-                a.k0[r + off] = key;
-                a.v0[r + off] = uint32_t(i);
-                for (int p = 0; p < P; ++p) atomicAdd(&s_hist[p][(key >> (p * dbits)) & dmask], 1u);
+        uint32_t r_base = base_k;
+        for (int64_t r0 = b0; r0 < b1; r0 += int64_t(kRounds) * kCT) {
+            uint32_t tl[kRounds], dk[kRounds], bal[kRounds];
+#pragma unroll
+            for (int r = 0; r < kRounds; ++r) {
+                const int64_t i = r0 + int64_t(r) * kCT + tid;
+                tl[r] = i < b1 ? a.tiles[i] : 0u;
+                dk[r] = i < b1 ? a.dkey[i] : 0u;
             }
-            r += agg;
-            __syncthreads();   // bscan reuse
+#pragma unroll
+            for (int r = 0; r < kRounds; ++r) {
+                bal[r] = __ballot_sync(0xffffffffu, tl[r] > 0u);
+                if (lane == 0) s_rw[r * kCW + warp] = __popc(bal[r]);
+            }
+            __syncthreads();
+            const uint32_t v = tid < kRounds * kCW ? s_rw[tid] : 0u;
+            uint32_t ex, agg;
+            BScan(bscan).ExclusiveSum(v, ex, agg);
+            if (tid < kRounds * kCW) s_rw[tid] = ex;
+            __syncthreads();
+#pragma unroll
+            for (int r = 0; r < kRounds; ++r) {
+                if (tl[r] > 0u) {
+                    const uint32_t o = r_base + s_rw[r * kCW + warp] + __popc(bal[r] & ((1u << lane) - 1u));
+                    const uint32_t i = uint32_t(r0 + int64_t(r) * kCT + tid);
+                    const uint32_t key = dk[r] - key_lo;
+                    a.onlist[o] = i;
+                    a.k0[o] = key;
+                    a.v0[o] = i;
+                    for (int p = 0; p < P; ++p) atomicAdd(&s_hist[p][(key >> (p * dbits)) & dmask], 1u);
+                }
+            }
+            r_base += agg;
+            __syncthreads();   // s_rw / bscan reuse
         }
     }
     __syncthreads();
@@ -215,7 +255,8 @@ __global__ void __launch_bounds__(kCT, 1) bin_coop_kernel(CoopArgs a) {
         const uint32_t s1 = p == 0 ? base_k + ldcg(a.cta_cnt + k) : min(Vs, s0 + S2);
         // global start of each digit for this CTA: digit base (scan of the pass totals) + the
         // preceding CTAs' counts. Thread (4-bin column c4, row set rs) sums rows k' = rs, rs + 8, ...
-        // < k with 16-B loads (rows are zero beyond nbins).
+        // < k with 16-B loads (rows are zero beyond nbins). (Keeping per-group row sums to shorten
+        // this walk was measured slower: the extra scatter atomics contend.)
         const uint32_t* Hp = a.H + size_t(p) * kCoopGridMax * kCoopBins;
         {
             const int c4 = tid & (kCoopBins / 4 - 1), rs = tid / (kCoopBins / 4);   // 128 x 8
@@ -331,54 +372,68 @@ __global__ void __launch_bounds__(kCT, 1) bin_coop_kernel(CoopArgs a) {
     grid_sync(&misc->coop_bar, goal);
 
     // ---------------------------------------------------------------- C3 segment sums, tile totals
+    // CTA = group of 32 tiles (lanes), warp = chunk segment: the segment prefix over the 32 segments
+    // and the tile totals are formed in shared memory (no atomics, no deep load chains later)
     const int ntg = (T + 31) / 32;
-    for (int item = k * kCW + warp; item < ntg * kCoopSegs; item += G * kCW) {
-        const int tg = item / kCoopSegs, seg = item % kCoopSegs;
+    uint32_t* ssum = dyn;   // [kCW][32]
+    for (int tg = k; tg < ntg; tg += G) {
         const int t = tg * 32 + lane;
         int c0, c1;
-        seg_range(nch, seg, c0, c1);
+        seg_range(nch, warp, c0, c1);
+        uint32_t sum = 0;
         if (t < T) {
-            uint32_t sum = 0;
 #pragma unroll 8
             for (int c = c0; c < c1; ++c) sum += ldcg(a.cmat + size_t(c) * T + t);
-            a.segsum[size_t(seg) * T + t] = sum;
-            if (sum) atomicAdd(a.tot + t, sum);
         }
+        ssum[warp * 32 + lane] = sum;
+        __syncthreads();
+        uint32_t pre = 0;
+        for (int q = 0; q < warp; ++q) pre += ssum[q * 32 + lane];
+        if (t < T) {
+            a.segsum[size_t(warp) * T + t] = pre;   // exclusive prefix over the tile's segments
+            if (warp == kCW - 1) a.tot[t] = pre + sum;
+        }
+        __syncthreads();
     }
     grid_sync(&misc->coop_bar, goal);
 
-    // ---------------------------------------------------------------- C4 tile scan and chunk bases
-    uint32_t* tstart = dyn;   // [T]
-    {
-        uint32_t carry = 0;
-        for (int b = 0; b < T; b += kCT) {
-            const int t = b + tid;
+    // ---------------------------------------------------------------- C4 tile starts and chunk bases
+    for (int tg = k; tg < ntg; tg += G) {
+        // start of the group: sum of the totals of all earlier tiles
+        uint32_t part = 0;
+        for (int t = tid; t < tg * 32; t += kCT) part += ldcg(a.tot + t);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (lane == 0) dyn[warp] = part;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t base = 0;
+            for (int q = 0; q < kCW; ++q) base += dyn[q];
+            const int t = tg * 32 + lane;
             const uint32_t v = t < T ? ldcg(a.tot + t) : 0u;
-            uint32_t ex, agg;
-            BScan(bscan).ExclusiveSum(v, ex, agg);
-            if (t < T) {
-                tstart[t] = carry + ex;
-                if (k == 0) a.ranges[t] = v ? make_uint2(carry + ex, carry + ex + v) : make_uint2(0u, 0u);
+            uint32_t incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += u;
             }
-            carry += agg;
-            __syncthreads();
+            const uint32_t st = base + incl - v;
+            dyn[kCW + lane] = st;
+            if (t < T) a.ranges[t] = v ? make_uint2(st, st + v) : make_uint2(0u, 0u);
+            if (tg == ntg - 1 && lane == 31) {   // the last group knows K
+                const unsigned long long K = (unsigned long long)(base + incl);
+                misc->n_keys = K;
+                const bool over = K > (unsigned long long)a.key_cap;
+                misc->n_keys_eff = over ? 0ull : K;
+                if (over) atomicOr(&misc->error_flag, 1u);
+            }
         }
-        if (k == 0 && tid == 0) {
-            const unsigned long long K = carry;
-            misc->n_keys = K;
-            const bool over = K > (unsigned long long)a.key_cap;
-            misc->n_keys_eff = over ? 0ull : K;
-            if (over) atomicOr(&misc->error_flag, 1u);
-        }
-    }
-    for (int item = k * kCW + warp; item < ntg * kCoopSegs; item += G * kCW) {
-        const int tg = item / kCoopSegs, seg = item % kCoopSegs;
+        __syncthreads();
         const int t = tg * 32 + lane;
         int c0, c1;
-        seg_range(nch, seg, c0, c1);
+        seg_range(nch, warp, c0, c1);
         if (t < T && c1 > c0) {
-            uint32_t run = tstart[t];
-            for (int q = 0; q < seg; ++q) run += ldcg(a.segsum + size_t(q) * T + t);
+            uint32_t run = dyn[kCW + lane] + ldcg(a.segsum + size_t(warp) * T + t);
             for (int cb = c0; cb < c1; cb += 8) {   // 8 loads in flight, then 8 stores
                 uint32_t v[8];
 #pragma unroll
@@ -390,8 +445,8 @@ __global__ void __launch_bounds__(kCT, 1) bin_coop_kernel(CoopArgs a) {
                 }
             }
         }
+        __syncthreads();
     }
-    __syncthreads();
 }
 
 // ------------------------------------------------------------------ host driver
@@ -454,6 +509,7 @@ gs_status run_bin_coop(WsState* s, cudaStream_t st) {
     a.cta_cnt = a.hist_all + kCoopPasses * kCoopBins;
     a.tot = a.cta_cnt + kCoopGridMax;
     a.segsum = a.tot + size_t(s->GX) * s->GY;   // capacity tile grid (region layout)
+
 
     a.ranges = at<uint2>(s, s->ranges);
     a.misc = misc;
