@@ -8,26 +8,59 @@
 namespace gs {
 
 // ------------------------------------------------------------------ L1 loss, Eq. 6 (reading C20)
+// Two passes (the depth term's scale needs the valid-pixel count first). Both read four pixels per
+// thread per step with 16-B loads when the planes are 16-B aligned (npx % 4 == 0), else one.
+// Per-thread sums are fp32 over a few pixels; blocks reduce in fp64.
+template <int V>
+struct LossVec;
+template <>
+struct LossVec<4> {
+    using T = float4;
+    __device__ static float4 ld(const float* p, int64_t i) { return reinterpret_cast<const float4*>(p)[i]; }
+    __device__ static void st(float* p, int64_t i, float4 v) { reinterpret_cast<float4*>(p)[i] = v; }
+    __device__ static float get(const float4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
+    __device__ static void set(float4& v, int e, float x) {
+        if (e == 0) v.x = x; else if (e == 1) v.y = x; else if (e == 2) v.z = x; else v.w = x;
+    }
+};
+template <>
+struct LossVec<1> {
+    using T = float;
+    __device__ static float ld(const float* p, int64_t i) { return p[i]; }
+    __device__ static void st(float* p, int64_t i, float v) { p[i] = v; }
+    __device__ static float get(const float& v, int) { return v; }
+    __device__ static void set(float& v, int, float x) { v = x; }
+};
+
+template <int V>
 __global__ void __launch_bounds__(256) loss_reduce_kernel(const float* __restrict__ c, const float* __restrict__ d,
                                                           const float* __restrict__ tc, const float* __restrict__ td,
                                                           int64_t npx, double* __restrict__ acc) {
-    double sc = 0.0, sd = 0.0, nv = 0.0;
-    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < npx; p += int64_t(gridDim.x) * blockDim.x) {
-        sc += double(fabsf(c[p] - tc[p])) + double(fabsf(c[npx + p] - tc[npx + p])) +
-              double(fabsf(c[2 * npx + p] - tc[2 * npx + p]));
-        const float t = td[p];
-        if (t > 0.f) {
-            sd += double(fabsf(d[p] - t));
-            nv += 1.0;
+    using L = LossVec<V>;
+    const int64_t nv = npx / V;   // vectors per plane
+    float sc = 0.f, sd = 0.f, cn = 0.f;
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nv; q += int64_t(gridDim.x) * blockDim.x) {
+        const auto c0 = L::ld(c, q), c1 = L::ld(c + npx, q), c2 = L::ld(c + 2 * npx, q);
+        const auto t0 = L::ld(tc, q), t1 = L::ld(tc + npx, q), t2 = L::ld(tc + 2 * npx, q);
+        const auto dv = L::ld(d, q), tv = L::ld(td, q);
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+            sc += fabsf(L::get(c0, e) - L::get(t0, e)) + fabsf(L::get(c1, e) - L::get(t1, e)) +
+                  fabsf(L::get(c2, e) - L::get(t2, e));
+            const float t = L::get(tv, e);
+            if (t > 0.f) {
+                sd += fabsf(L::get(dv, e) - t);
+                cn += 1.f;
+            }
         }
     }
     using BR = cub::BlockReduce<double, 256>;
     __shared__ typename BR::TempStorage tmp;
-    const double a = BR(tmp).Sum(sc);
+    const double a = BR(tmp).Sum(double(sc));
     __syncthreads();
-    const double b = BR(tmp).Sum(sd);
+    const double b = BR(tmp).Sum(double(sd));
     __syncthreads();
-    const double e = BR(tmp).Sum(nv);
+    const double e = BR(tmp).Sum(double(cn));
     if (threadIdx.x == 0) {
         atomicAdd(acc + 0, a);
         atomicAdd(acc + 1, b);
@@ -37,21 +70,36 @@ __global__ void __launch_bounds__(256) loss_reduce_kernel(const float* __restric
 
 __device__ __forceinline__ float sgnf(float x) { return float((x > 0.f) - (x < 0.f)); }
 
+template <int V>
 __global__ void __launch_bounds__(256) loss_grad_kernel(const float* __restrict__ c, const float* __restrict__ d,
                                                         const float* __restrict__ tc, const float* __restrict__ td,
                                                         int64_t npx, float wc, float wd, const double* __restrict__ acc,
                                                         float* __restrict__ dc, float* __restrict__ dd,
                                                         double* __restrict__ loss) {
+    using L = LossVec<V>;
     const double nvalid = acc[2];
     const float sc = float(double(wc) / (3.0 * double(npx)));
     const float sd = nvalid > 0 ? float(double(wd) / nvalid) : 0.f;
     if (blockIdx.x == 0 && threadIdx.x == 0 && loss)
         *loss = double(sc) * acc[0] + (nvalid > 0 ? double(sd) * acc[1] : 0.0);
-    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < npx; p += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t nv = npx / V;
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nv; q += int64_t(gridDim.x) * blockDim.x) {
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) dc[ch * npx + p] = sc * sgnf(c[ch * npx + p] - tc[ch * npx + p]);
-        const float t = td[p];
-        dd[p] = t > 0.f ? sd * sgnf(d[p] - t) : 0.f;
+        for (int ch = 0; ch < 3; ++ch) {
+            const auto cv = L::ld(c + ch * npx, q), tv = L::ld(tc + ch * npx, q);
+            typename L::T o;
+#pragma unroll
+            for (int e = 0; e < V; ++e) L::set(o, e, sc * sgnf(L::get(cv, e) - L::get(tv, e)));
+            L::st(dc + ch * npx, q, o);
+        }
+        const auto dv = L::ld(d, q), tv = L::ld(td, q);
+        typename L::T o;
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+            const float t = L::get(tv, e);
+            L::set(o, e, t > 0.f ? sd * sgnf(L::get(dv, e) - t) : 0.f);
+        }
+        L::st(dd, q, o);
     }
 }
 
@@ -60,13 +108,19 @@ void launch_loss_l1(WsState* s, const float* color, const float* depth, const fl
     Misc* misc = at<Misc>(s, s->misc);
     const int64_t npx = int64_t(W) * H;
     cudaMemsetAsync(misc->loss_acc, 0, sizeof(misc->loss_acc), st);
-    const int blocks = int(std::min<int64_t>((npx + 255) / 256, 148 * 4));
+    auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    const bool v4 = npx % 4 == 0 && aligned(color) && aligned(depth) && aligned(tc) && aligned(td) && aligned(dc) &&
+                    aligned(dd);
+    const int64_t nv = v4 ? npx / 4 : npx;
+    const int blocks = int(std::min<int64_t>((nv + 255) / 256, 148 * 4));
     {
         KTimer kt(s, KID_LOSS, st);
-        loss_reduce_kernel<<<blocks, 256, 0, st>>>(color, depth, tc, td, npx, misc->loss_acc);
+        if (v4) loss_reduce_kernel<4><<<blocks, 256, 0, st>>>(color, depth, tc, td, npx, misc->loss_acc);
+        else loss_reduce_kernel<1><<<blocks, 256, 0, st>>>(color, depth, tc, td, npx, misc->loss_acc);
     }
     KTimer kt(s, KID_LOSS, st);
-    loss_grad_kernel<<<blocks, 256, 0, st>>>(color, depth, tc, td, npx, wc, wd, misc->loss_acc, dc, dd, loss);
+    if (v4) loss_grad_kernel<4><<<blocks, 256, 0, st>>>(color, depth, tc, td, npx, wc, wd, misc->loss_acc, dc, dd, loss);
+    else loss_grad_kernel<1><<<blocks, 256, 0, st>>>(color, depth, tc, td, npx, wc, wd, misc->loss_acc, dc, dd, loss);
 }
 
 // ------------------------------------------------------------------ Adam

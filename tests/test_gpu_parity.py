@@ -186,14 +186,14 @@ def test_backward_parity(c):
 
 
 # ------------------------------------------------------------------ O5 loss / Adam / pose step
-def test_loss_parity():
+@pytest.mark.parametrize("W,H", [(200, 120), (37, 21)])   # 16-B vector path and the ragged scalar path
+def test_loss_parity(W, H):
     import paper_2311_11700_b200 as g
-    W, H = 200, 120
     c, d = gi.random_images(W, H, 5)
     tc, td = gi.random_images(W, H, 6)
     c[0, 3, 4] = tc[0, 3, 4]
     pipe = g.RenderPipeline(16, 4096, W, H)
-    cam = gi.Camera(100.0, 100.0, 99.5, 59.5, W, H)
+    cam = gi.Camera(100.0, 100.0, (W - 1) / 2, (H - 1) / 2, W, H)
     pipe.color.copy_(to_dev(c))
     pipe.depth.copy_(to_dev(d))
     dc, dd = pipe.loss_l1(cam, to_dev(tc), to_dev(td), 0.9, 0.1)
