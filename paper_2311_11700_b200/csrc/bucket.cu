@@ -133,8 +133,13 @@ __global__ void __launch_bounds__((kConsumers + 1) * 32) bucket_emit_kernel(
     const bool warp_in = x0 < GX && y0 < GY;
     uint2* list = sm.l_mg[warp];
     int it = 0;
+    uint32_t pos_nx = (valid && blockIdx.x < nch) ? cmat[size_t(blockIdx.x) * T + ty * GX + tx] : 0u;
     for (int c = blockIdx.x; c < nch; c += gridDim.x, ++it) {
         const int slot = it % kRing;
+        // this chunk's base position of my tile, and the next chunk's (loaded a chunk ahead)
+        uint32_t mypos = pos_nx;
+        const int cn = c + gridDim.x;
+        pos_nx = (valid && cn < nch) ? cmat[size_t(cn) * T + ty * GX + tx] : 0u;
         mbar_wait(&sm.full[slot], (it / kRing) & 1);
         const int tot = sm.cnt[slot];
         int L = 0;
@@ -157,7 +162,6 @@ __global__ void __launch_bounds__((kConsumers + 1) * 32) bucket_emit_kernel(
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[slot]);   // the slot is no longer read by this warp
         if (L == 0) continue;                          // warp-uniform
-        uint32_t mypos = valid ? cmat[size_t(c) * T + ty * GX + tx] : 0u;
         for (int k0 = 0; k0 < L; k0 += 32) {
             const int k = k0 + lane;
             const uint2 mg = k < L ? list[k] : make_uint2(0u, 0u);
