@@ -165,11 +165,9 @@ __global__ void __launch_bounds__((kConsumers + 1) * 32) bucket_emit_kernel(
         for (int k0 = 0; k0 < L; k0 += 32) {
             const int k = k0 + lane;
             const uint2 mg = k < L ? list[k] : make_uint2(0u, 0u);
-            const uint32_t any = __reduce_or_sync(0xffffffffu, mg.x);
             uint32_t mine = 0;   // lane j: ballot of tile j
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-                if (!(any & (1u << j))) continue;   // warp-uniform
                 const bool hit = mg.x & (1u << j);
                 const uint32_t m = __ballot_sync(0xffffffffu, hit);
                 const uint32_t pj = __shfl_sync(0xffffffffu, mypos, j);
