@@ -776,7 +776,7 @@ constexpr int kPoseSums = 15;
 __device__ void pose_finalize_block(const double* __restrict__ part, int nblocks, const float* __restrict__ viewmat,
                                     double* __restrict__ grad_pose);
 
-__global__ void __launch_bounds__(256) gaussian_bwd_kernel(
+__global__ void __launch_bounds__(256, 4) gaussian_bwd_kernel(
     const float* __restrict__ params, int64_t n, int64_t ld, const float* __restrict__ viewmat, gs_camera cam,
     const uint32_t* __restrict__ onlist, const unsigned int* __restrict__ n_on, const float4* __restrict__ rec,
     const float* __restrict__ sgrad, int64_t sld, float* __restrict__ grad, int cov_path,
