@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--binsort", default="bucket", choices=["bucket", "keys"])
+    ap.add_argument("--sh", type=int, default=0, choices=[0, 1],
+                    help="colour model: 0 = RGB (BASELINE configs), 1 = degree-1 SH (NEXT-1, gs_project_sh)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="timed loop only (for ncu launch lists)")
@@ -194,6 +196,8 @@ def main_ours(args):
     cam = cfg.cam
     n = cfg.n
     p = cfg.scene()
+    if args.sh == 1:   # degree-1 SH coefficients instead of RGB rows (seeded, gs_inputs.with_sh)
+        p = gi.with_sh(p, cfg.scene_seed + 1000)
     v = cfg.view()
     P = torch.as_tensor(p, device=dev)
     V = torch.as_tensor(v, device=dev)
@@ -262,7 +266,8 @@ def main_ours(args):
            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Replica-shaped room scene, SURVEY.md §8(d))",
            "config": {"workload": f"config {args.config}: {cfg.name} {cam.width}x{cam.height}, {n} Gaussians, "
-                                  f"fwd+bwd L1 (0.9/0.1) iteration", "n_gaussians": n, "width": cam.width,
+                                  f"fwd+bwd L1 (0.9/0.1) iteration" + (", degree-1 SH colour" if args.sh else ""),
+                      "sh_degree": args.sh, "n_gaussians": n, "width": cam.width,
                       "height": cam.height, "keys": K, "visible": V_front, "on_screen": V_s, "E_f": E_f, "E_b": E_b,
                       "E_f_live": Lf, "E_b_live": Lb,
                       "binsort": args.binsort, "l2": "per-iteration working set > L2 (126 MB): tile lists "

@@ -109,6 +109,22 @@ def room_surface_gaussians(n: int, seed: int, lo=ROOM_LO, hi=ROOM_HI) -> np.ndar
     return out.astype(np.float32)
 
 
+def sh_coefficients(n: int, seed: int, lin: float = 0.3) -> np.ndarray:
+    """Degree-1 SH inputs: [12][n] fp32 draws, row 3k + c = coefficient k of
+    channel c; constant terms N(0, 1), linear terms N(0, lin). Appended to rows 0-10 of a scene they
+    give the [23][n] layout of gs_project_sh."""
+    rng = np.random.default_rng(seed)
+    out = np.empty((12, n), np.float64)
+    out[0:3] = rng.normal(0.0, 1.0, (3, n))
+    out[3:12] = rng.normal(0.0, lin, (9, n))
+    return out.astype(np.float32)
+
+
+def with_sh(params: np.ndarray, seed: int, lin: float = 0.3) -> np.ndarray:
+    """Rows 0-10 of `params` (geometry, opacity) + seeded degree-1 SH coefficients -> [23][n]."""
+    return np.concatenate([params[:11], sh_coefficients(params.shape[1], seed, lin)]).astype(np.float32)
+
+
 def identity_view() -> np.ndarray:
     v = np.zeros((3, 4), np.float32)
     v[0, 0] = v[1, 1] = v[2, 2] = 1.0

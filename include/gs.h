@@ -90,6 +90,19 @@ gs_status gs_ws_init(gs_ws* ws /*(host)*/, void* dev, size_t dev_bytes, int64_t 
 gs_status gs_project(const float* params, int64_t n, int64_t ld, const uint8_t* mask /*nullable*/,
                      const float* viewmat, const gs_camera* cam /*(host)*/, gs_ws* ws, void* stream);
 
+/* gs_project_sh — gs_project with the colour model selected by sh_degree:
+ *   0: params [14][ld], rows 11-13 = RGB (reading C17; identical to gs_project);
+ *   1: params [23][ld], rows 11 + 3k + c = degree-1 SH coefficient k of channel c ("1-degree
+ *      spherical harmonics per colour channel, a total of 12 coefficients"). The
+ *      colour is evaluated per Gaussian at the view direction u = (X - c)/|X - c|, c = -W^T t:
+ *      rgb_c = max(0, 1/2 + C0 Y_0c + C1 (-u_y Y_1c + u_z Y_2c - u_x Y_3c)) (reading C29).
+ * The degree is kept in the workspace: the following gs_render_bwd / gs_pose_grad use it, and
+ * grad_params then has the same row count (14 or 23). Errors: GS_ERR_INVALID_ARG if sh_degree is
+ * not 0 or 1, else as gs_project. */
+gs_status gs_project_sh(const float* params, int64_t n, int64_t ld, int32_t sh_degree,
+                        const uint8_t* mask /*nullable*/, const float* viewmat, const gs_camera* cam /*(host)*/,
+                        gs_ws* ws, void* stream);
+
 /* gs_bin_sort — tile binning + depth sort ("sorting the Gaussians in depth order", PAPER.md:83;
  * north_star: 64-bit (tile << 32 | depth-bits) keys, 16x16 tiles). Produces, per tile t, the list
  * of Gaussian indices whose rect contains t, ordered by (depth bits, index) — the stable ascending

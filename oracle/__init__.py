@@ -80,21 +80,30 @@ def grid(cam) -> tuple[int, int]:
     return (cam.width + 15) // 16, (cam.height + 15) // 16
 
 
+def sh_degree_of(params) -> int:
+    """Colour model from the parameter rows: 14 = RGB (reading C17), 23 = degree-1 SH (C29)."""
+    rows = np.asarray(params).shape[0]
+    if rows not in (14, 23):
+        raise ValueError(f"params must have 14 or 23 rows, got {rows}")
+    return 1 if rows == 23 else 0
+
+
 # ------------------------------------------------------------------------------------ O1
 def project(params, view, cam, precision="f32") -> dict:
-    """O1 (Eq. 2-3): per-Gaussian projection. params [14][n], view [3][4]."""
+    """O1 (Eq. 2-3): per-Gaussian projection. params [14][n] (RGB) or [23][n] (degree-1 SH, C29),
+    view [3][4]. rgb: the colour the blend uses (SH evaluated at the view direction)."""
     dt = _dtype(precision)
     params = np.ascontiguousarray(params, dt)
     view = np.ascontiguousarray(view, dt)
     n = params.shape[1]
     out = dict(mean2d=np.zeros((2, n), dt), conic=np.zeros((3, n), dt), depth=np.zeros(n, dt),
                radius=np.zeros(n, np.int32), rect=np.zeros((4, n), np.int32), tiles=np.zeros(n, np.uint32),
-               depth_bits=np.zeros(n, np.uint32), cov2d=np.zeros((3, n), dt))
+               depth_bits=np.zeros(n, np.uint32), cov2d=np.zeros((3, n), dt), rgb=np.zeros((3, n), dt))
     c = _cam(cam)
     fn = getattr(lib(), f"oracle_project_{precision}")
     fn(_p(params), ctypes.c_int64(n), ctypes.c_int64(n), _p(view), ctypes.byref(c), _p(out["mean2d"]),
        _p(out["conic"]), _p(out["depth"]), _p(out["radius"]), _p(out["rect"]), _p(out["tiles"]),
-       _p(out["depth_bits"]), _p(out["cov2d"]))
+       _p(out["depth_bits"]), _p(out["cov2d"]), ctypes.c_int32(sh_degree_of(params)), _p(out["rgb"]))
     return out
 
 
@@ -147,7 +156,7 @@ def forward(params, view, cam, precision="f32", pixels=None, replay_nlast=None, 
     getattr(lib(), f"oracle_forward_{precision}")(
         _p(params), ctypes.c_int64(n), ctypes.c_int64(n), _p(view), ctypes.byref(c), _p(pixels),
         ctypes.c_int64(npx), _p(rp), _p(color), _p(depth), _p(alpha), _p(n_last), _p(examined), _p(amb),
-        _p(h), _p(aw), ctypes.c_int32(1 if flip_skip_ties else 0))
+        _p(h), _p(aw), ctypes.c_int32(1 if flip_skip_ties else 0), ctypes.c_int32(sh_degree_of(params)))
     out = dict(color=color.reshape((3,) + shape), depth=depth.reshape(shape), alpha=alpha.reshape(shape),
                n_last=n_last.reshape(shape), examined=examined.reshape(shape), ambiguous=amb.reshape(shape),
                hash=int(h[0]))
@@ -159,7 +168,8 @@ def forward(params, view, cam, precision="f32", pixels=None, replay_nlast=None, 
 # ------------------------------------------------------------------------------------ O4
 def backward(params, view, cam, dL_dcolor, dL_ddepth, precision="f32", replay_nlast=None, qt_cov=True,
              pixels=None) -> dict:
-    """O4 (Eq. 11, S1-S6): fp64 gradients for the 14 params, screen grads, and the pose.
+    """O4 (Eq. 11, S1-S6): fp64 gradients for the 14 (RGB) or 23 (degree-1 SH) params, screen grads,
+    and the pose.
 
     pose_twist: (rho, phi) left-perturbation twist, covariance path included (reading C7);
     pose_twist_paper: same without the Sigma'-through-pose term (P:168, paper mode);
@@ -171,7 +181,7 @@ def backward(params, view, cam, dL_dcolor, dL_ddepth, precision="f32", replay_nl
     n = params.shape[1]
     dc = np.ascontiguousarray(dL_dcolor, np.float32).reshape(-1)
     dd = np.ascontiguousarray(dL_ddepth, np.float32).reshape(-1)
-    gp = np.zeros((14, n), np.float64)
+    gp = np.zeros((params.shape[0], n), np.float64)
     gs = np.zeros((10, n), np.float64)
     tw = np.zeros(6, np.float64)
     twp = np.zeros(6, np.float64)
@@ -182,7 +192,7 @@ def backward(params, view, cam, dL_dcolor, dL_ddepth, precision="f32", replay_nl
     getattr(lib(), f"oracle_backward_{precision}")(
         _p(params), ctypes.c_int64(n), ctypes.c_int64(n), _p(view), ctypes.byref(c), _p(dc), _p(dd), _p(rp),
         _p(gp), _p(gs), _p(tw), _p(twp), _p(qt), ctypes.c_int32(1 if qt_cov else 0), _p(px),
-        ctypes.c_int64(0 if px is None else px.shape[0]))
+        ctypes.c_int64(0 if px is None else px.shape[0]), ctypes.c_int32(sh_degree_of(params)))
     return dict(grad_params=gp, grad_screen=gs, pose_twist=tw, pose_twist_paper=twp,
                 pose_q=qt[0:4], pose_t=qt[4:7], pose_quat=qt[7:11])
 

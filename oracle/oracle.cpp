@@ -48,13 +48,25 @@ constexpr int TILE = 16;    // BASELINE.json north_star: 16x16 tiles
 template <class R> struct Cam {
     R fx, fy, cx, cy, znear, dil;
     int W, H, GX, GY;
+    int sh;                 // colour model: 0 = RGB rows 11-13 (reading C17), 1 = degree-1 SH (C29)
     double bg[3];
-    explicit Cam(const OracleCam& c)
+    explicit Cam(const OracleCam& c, int sh_degree = 0)
         : fx(R(c.fx)), fy(R(c.fy)), cx(R(c.cx)), cy(R(c.cy)), znear(R(c.znear)), dil(R(c.dil)),
-          W(c.width), H(c.height), GX((c.width + TILE - 1) / TILE), GY((c.height + TILE - 1) / TILE) {
+          W(c.width), H(c.height), GX((c.width + TILE - 1) / TILE), GY((c.height + TILE - 1) / TILE),
+          sh(sh_degree) {
         for (int k = 0; k < 3; ++k) bg[k] = c.bg[k];
     }
 };
+
+constexpr int MAXP = 23;    // parameter rows: 14 (RGB) or 23 (degree-1 SH, 12 coefficients)
+inline int n_rows(int sh) { return sh == 1 ? 23 : 14; }
+
+// Degree-1 real spherical harmonics (reading C29: the basis and the 0.5 offset / clamp at 0 of the
+// 3DGS rasterizer the paper extends; the paper fixes only "1-degree SH per colour channel,
+// 12 coefficients"). Coefficient Y[k][c] is parameter row 11 + 3k + c (k = 0 the constant
+// term, k = 1..3 the linear terms), so degree 0 keeps the RGB rows' positions.
+constexpr double SH_C0 = 0.28209479177387814;   // 1 / (2 sqrt(pi))
+constexpr double SH_C1 = 0.4886025119029199;    // sqrt(3) / (2 sqrt(pi))
 
 // ---------------------------------------------------------------- O1: projection (Eq. 2-3)
 template <class R> struct Proj {
@@ -66,7 +78,27 @@ template <class R> struct Proj {
     int32_t radius = 0;
     int32_t xlo = 0, xhi = 0, ylo = 0, yhi = 0;
     uint32_t tiles = 0;
+    R rgb[3] = {0, 0, 0};              // colour (RGB rows, or degree-1 SH at the view direction)
+    bool lit[3] = {true, true, true};  // SH: channel not clamped at 0 (the gradient flows)
 };
+
+// Colour of one Gaussian (SH degree 1): view direction from the camera centre c = -W^T t to the
+// mean, in world coordinates; fp32 in the fixed order below when R = float (the clamp at 0 decides
+// whether the channel's gradient flows, so both sides take it in fp32).
+template <class R> static void sh1_colour(const R* p, const R* V, R rgb[3], bool lit[3]) {
+    const R cwx = -((V[0] * V[3] + V[4] * V[7]) + V[8] * V[11]);
+    const R cwy = -((V[1] * V[3] + V[5] * V[7]) + V[9] * V[11]);
+    const R cwz = -((V[2] * V[3] + V[6] * V[7]) + V[10] * V[11]);
+    const R dx = p[0] - cwx, dy = p[1] - cwy, dz = p[2] - cwz;
+    const R len = std::sqrt((dx * dx + dy * dy) + dz * dz);
+    const R ux = dx / len, uy = dy / len, uz = dz / len;
+    for (int c = 0; c < 3; ++c) {
+        const R lin = ((-(uy * p[14 + c]) + uz * p[17 + c]) - ux * p[20 + c]);
+        const R v = (R(SH_C0) * p[11 + c] + R(SH_C1) * lin) + R(0.5);
+        lit[c] = v > R(0);
+        rgb[c] = lit[c] ? v : R(0);
+    }
+}
 
 template <class R> static inline int32_t clamp_tile(R v, int hi) {
     // clamp in floating point first (no UB on huge values), then convert exactly
@@ -83,6 +115,8 @@ template <> inline uint32_t bits_of<double>(double z) { float f = float(z); uint
 // V = world->camera 3x4 row-major. Steps numbered as DESIGN.md §3 O1.
 template <class R> static Proj<R> project_one(const R* p, const R* V, const Cam<R>& cam) {
     Proj<R> g;
+    if (cam.sh == 1) sh1_colour(p, V, g.rgb, g.lit);
+    else for (int c = 0; c < 3; ++c) g.rgb[c] = p[11 + c];
     const R x = p[0], y = p[1], z = p[2];
     // 1. camera coordinates
     g.xc = ((V[0] * x + V[1] * y) + V[2] * z) + V[3];
@@ -159,8 +193,8 @@ template <class R> static Proj<R> project_one(const R* p, const R* V, const Cam<
     return g;
 }
 
-template <class R> static void gather_params(const R* params, int64_t ld, int64_t i, R* p) {
-    for (int k = 0; k < 14; ++k) p[k] = params[k * ld + i];
+template <class R> static void gather_params(const R* params, int64_t ld, int64_t i, R* p, int rows) {
+    for (int k = 0; k < rows; ++k) p[k] = params[k * ld + i];
 }
 
 template <class R> static std::vector<Proj<R>> project_all(const R* params, int64_t n, int64_t ld, const R* V,
@@ -168,8 +202,8 @@ template <class R> static std::vector<Proj<R>> project_all(const R* params, int6
     std::vector<Proj<R>> out(static_cast<size_t>(n));
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) {
-        R p[14];
-        gather_params(params, ld, i, p);
+        R p[MAXP];
+        gather_params(params, ld, i, p, n_rows(cam.sh));
         out[size_t(i)] = project_one(p, V, cam);
     }
     return out;
@@ -264,7 +298,7 @@ static void blend_pixel(int u, int v, const std::vector<Proj<R>>& pj, const std:
         }
         t_band += step_band;
         const double w = double(alpha) * double(T);
-        for (int c = 0; c < 3; ++c) out.color[c] += w * double(params[(11 + c) * ld + i]);
+        for (int c = 0; c < 3; ++c) out.color[c] += w * double(g.rgb[c]);
         out.depth += w * double(g.zc);
         T = Tn;
         out.n_last = j;
@@ -303,7 +337,7 @@ static void backward_pixel(const PixelResult& px, const std::vector<Proj<R>>& pj
     for (size_t kk = n; kk-- > 0;) {
         const Contrib& ct = px.list[kk];
         const int64_t i = ct.i;
-        const double rgb[3] = {double(params[11 * ld + i]), double(params[12 * ld + i]), double(params[13 * ld + i])};
+        const double rgb[3] = {double(pj[size_t(i)].rgb[0]), double(pj[size_t(i)].rgb[1]), double(pj[size_t(i)].rgb[2])};
         const double d = double(pj[size_t(i)].zc);
         const double Ti = T[kk], a = ct.alpha, w = a * Ti;
         // dC/dalpha_i = c_i T_i - (sum_{m>i} c_m w_m + T_f bg)/(1 - alpha_i);  same for D without bg
@@ -351,7 +385,8 @@ static void rot_of(const double q[4], double Rm[3][3]) {   // Eq. S1
 }
 
 struct GaussianBack {     // result of the per-Gaussian chain (fp64)
-    double grad[14];      // dL/d(mean xyz, scale xyz, raw quat rijk, opacity, rgb)
+    double grad[MAXP];    // dL/d(mean xyz, scale xyz, raw quat rijk, opacity, rgb | SH coefficients)
+    double gdir[3];       // dL/dX (world) through the SH view direction (0 for RGB)
     double dXc_full[3];   // dL/dX^c through mean, depth and J paths
     double dXc_noJ[3];    // dL/dX^c through mean and depth only (paper mode)
     double dW[3][3];      // dL/dW through Sigma' (covariance path, Eq. S4-S5)
@@ -362,10 +397,10 @@ struct GaussianBack {     // result of the per-Gaussian chain (fp64)
 // (Eq. 11 P:155-168 and Supplement A). Recomputed in fp64 from the fp32 inputs.
 template <class R>
 static GaussianBack gaussian_backward(const R* params, int64_t ld, int64_t i, const R* Vr, const Cam<R>& camr,
-                                      const ScreenGrad& s) {
+                                      const ScreenGrad& s, const Proj<R>& pr) {
     GaussianBack out{};
-    double p[14], V[12];
-    for (int k = 0; k < 14; ++k) p[k] = double(params[k * ld + i]);
+    double p[MAXP], V[12];
+    for (int k = 0; k < n_rows(camr.sh); ++k) p[k] = double(params[k * ld + i]);
     for (int k = 0; k < 12; ++k) V[k] = double(Vr[k]);
     const double fx = double(camr.fx), fy = double(camr.fy);
     double W[3][3];
@@ -459,9 +494,34 @@ static GaussianBack gaussian_backward(const R* params, int64_t ld, int64_t i, co
     const double dot = dqh[0] * q[0] + dqh[1] * q[1] + dqh[2] * q[2] + dqh[3] * q[3];
     for (int m = 0; m < 4; ++m) out.grad[6 + m] = (dqh[m] - q[m] * dot) / nq;
     out.grad[10] = s.o;
-    out.grad[11] = s.r;
-    out.grad[12] = s.g;
-    out.grad[13] = s.bl;
+    if (camr.sh == 1) {
+        // colour = SH_C0 Y0 + SH_C1 (-u_y Y1 + u_z Y2 - u_x Y3) + 1/2 per channel, clamped at 0 (C29);
+        // u = (X - c) / |X - c|, c = -W^T t. The clamp decisions are the projection's (pr.lit).
+        double cw[3];
+        for (int k = 0; k < 3; ++k) cw[k] = -(W[0][k] * V[3] + W[1][k] * V[7] + W[2][k] * V[11]);
+        const double d[3] = {p[0] - cw[0], p[1] - cw[1], p[2] - cw[2]};
+        const double len = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+        const double u[3] = {d[0] / len, d[1] / len, d[2] / len};
+        const double gc[3] = {pr.lit[0] ? s.r : 0.0, pr.lit[1] ? s.g : 0.0, pr.lit[2] ? s.bl : 0.0};
+        const double basis[4] = {SH_C0, -SH_C1 * u[1], SH_C1 * u[2], -SH_C1 * u[0]};
+        double du[3] = {0, 0, 0};
+        for (int c = 0; c < 3; ++c) {
+            for (int k = 0; k < 4; ++k) out.grad[11 + 3 * k + c] = gc[c] * basis[k];
+            du[0] += gc[c] * (-SH_C1 * p[20 + c]);
+            du[1] += gc[c] * (-SH_C1 * p[14 + c]);
+            du[2] += gc[c] * (SH_C1 * p[17 + c]);
+        }
+        // u = d / |d|:  dL/dd = (dL/du - u (u . dL/du)) / |d|
+        const double ud = u[0] * du[0] + u[1] * du[1] + u[2] * du[2];
+        for (int k = 0; k < 3; ++k) {
+            out.gdir[k] = (du[k] - u[k] * ud) / len;
+            out.grad[k] += out.gdir[k];
+        }
+    } else {
+        out.grad[11] = s.r;
+        out.grad[12] = s.g;
+        out.grad[13] = s.bl;
+    }
     return out;
 }
 
@@ -491,8 +551,8 @@ void oracle_set_threads(int n) {
 #define ORACLE_PROJECT(SUF, R)                                                                             \
     int oracle_project_##SUF(const R* params, int64_t n, int64_t ld, const R* view, const OracleCam* oc,    \
                              R* mean2d, R* conic, R* depth, int32_t* radius, int32_t* rect,                \
-                             uint32_t* tiles, uint32_t* depth_bits, R* cov2d) {                            \
-        Cam<R> cam(*oc);                                                                                   \
+                             uint32_t* tiles, uint32_t* depth_bits, R* cov2d, int32_t sh_degree, R* rgb) { \
+        Cam<R> cam(*oc, sh_degree);                                                                        \
         auto pj = project_all<R>(params, n, ld, view, cam);                                                \
         for (int64_t i = 0; i < n; ++i) {                                                                  \
             const Proj<R>& g = pj[size_t(i)];                                                              \
@@ -505,6 +565,7 @@ void oracle_set_threads(int n) {
             rect[i] = g.xlo; rect[n + i] = g.xhi; rect[2 * n + i] = g.ylo; rect[3 * n + i] = g.yhi;        \
             tiles[i] = on ? g.tiles : 0u;                                                                  \
             depth_bits[i] = bits_of<R>(g.zc);                                                              \
+            if (rgb) for (int c = 0; c < 3; ++c) rgb[c * n + i] = g.rgb[c];                                \
         }                                                                                                  \
         return 0;                                                                                          \
     }
@@ -565,8 +626,8 @@ int64_t oracle_bin(const uint32_t* depth_bits, const int32_t* rect, const uint32
                              const int64_t* pixels, int64_t n_pix, const uint32_t* replay_nlast,          \
                              double* color, double* depth, double* alpha, uint32_t* n_last,               \
                              uint32_t* examined, uint8_t* ambiguous, uint64_t* hash,                      \
-                             double* accum_weight, int32_t flip_skip_ties) {                              \
-        Cam<R> cam(*oc);                                                                                  \
+                             double* accum_weight, int32_t flip_skip_ties, int32_t sh_degree) {           \
+        Cam<R> cam(*oc, sh_degree);                                                                       \
         auto pj = project_all<R>(params, n, ld, view, cam);                                               \
         auto order = depth_order(pj);                                                                     \
         const int64_t P = pixels ? n_pix : int64_t(cam.W) * cam.H;                                        \
@@ -612,8 +673,8 @@ ORACLE_FORWARD(f64, double)
                               const float* dLdC, const float* dLdD, const uint32_t* replay_nlast,              \
                               double* grad_params, double* grad_screen, double* pose_twist,                    \
                               double* pose_twist_paper, double* pose_qt, int32_t qt_cov,                       \
-                              const int64_t* pixels, int64_t n_pix) {                                          \
-        Cam<R> cam(*oc);                                                                                       \
+                              const int64_t* pixels, int64_t n_pix, int32_t sh_degree) {                       \
+        Cam<R> cam(*oc, sh_degree);                                                                            \
         auto pj = project_all<R>(params, n, ld, view, cam);                                                    \
         auto order = depth_order(pj);                                                                          \
         const int64_t P = int64_t(cam.W) * cam.H;                                                              \
@@ -634,6 +695,7 @@ ORACLE_FORWARD(f64, double)
         double dRpose[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};                                               \
         double dWsum[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};                                                \
         double dqS3[4] = {0, 0, 0, 0};                                                                         \
+        double Gdir[3] = {0, 0, 0};                                                                            \
         double qp[4];                                                                                          \
         {   /* pose quaternion of W (for the Eq. S3 path): robust matrix -> quaternion */                     \
             double W[3][3];                                                                                    \
@@ -653,8 +715,9 @@ ORACLE_FORWARD(f64, double)
         }                                                                                                      \
         for (int64_t i = 0; i < n; ++i) {                                                                      \
             if (!pj[size_t(i)].in_front || pj[size_t(i)].tiles == 0) continue;                                 \
-            GaussianBack gb = gaussian_backward<R>(params, ld, i, view, cam, sg[size_t(i)]);                   \
-            if (grad_params) for (int k = 0; k < 14; ++k) grad_params[k * n + i] += gb.grad[k];                \
+            GaussianBack gb = gaussian_backward<R>(params, ld, i, view, cam, sg[size_t(i)], pj[size_t(i)]);    \
+            if (grad_params) for (int k = 0; k < n_rows(cam.sh); ++k) grad_params[k * n + i] += gb.grad[k];    \
+            for (int a = 0; a < 3; ++a) Gdir[a] += gb.gdir[a];   /* SH view-direction path (C29) */          \
             const double* X = gb.Xc;                                                                           \
             for (int a = 0; a < 3; ++a) { rho[a] += gb.dXc_full[a]; rho_p[a] += gb.dXc_noJ[a]; }               \
             const double* g = gb.dXc_full; const double* gp = gb.dXc_noJ;                                      \
@@ -684,8 +747,12 @@ ORACLE_FORWARD(f64, double)
         for (int a = 0; a < 3; ++a) for (int b = 0; b < 3; ++b) W[a][b] = double(view[a * 4 + b]);            \
         for (int a = 0; a < 3; ++a) for (int b = 0; b < 3; ++b)                                                \
             A[a][b] = W[a][0] * dWsum[b][0] + W[a][1] * dWsum[b][1] + W[a][2] * dWsum[b][2];                   \
+        /* SH colour through the camera centre c = -W^T t (C29): dL/dc = -Gdir, so the twist gains        \
+           rho += W Gdir and phi gains nothing (first order); the paper's mode drops it (C8) */     \
+        double WG[3];                                                                                          \
+        for (int a = 0; a < 3; ++a) WG[a] = W[a][0] * Gdir[0] + W[a][1] * Gdir[1] + W[a][2] * Gdir[2];        \
         if (pose_twist) {                                                                                      \
-            for (int a = 0; a < 3; ++a) pose_twist[a] = rho[a];                                                \
+            for (int a = 0; a < 3; ++a) pose_twist[a] = rho[a] + WG[a];                                        \
             pose_twist[3] = phi[0] + (A[1][2] - A[2][1]);                                                      \
             pose_twist[4] = phi[1] + (A[2][0] - A[0][2]);                                                      \
             pose_twist[5] = phi[2] + (A[0][1] - A[1][0]);                                                      \
@@ -700,9 +767,12 @@ ORACLE_FORWARD(f64, double)
             for (int m = 0; m < 4; ++m) {                                                                      \
                 double acc = dqS3[m];                                                                          \
                 if (qt_cov) for (int a = 0; a < 3; ++a) for (int b = 0; b < 3; ++b) acc += dWsum[a][b] * dR[a][b][m]; \
+                /* colour path: c_k = -sum_a R_ak t_a, so dL/dR_ak = t_a Gdir_k */                          \
+                if (qt_cov) for (int a = 0; a < 3; ++a) for (int b = 0; b < 3; ++b)                           \
+                    acc += double(view[a * 4 + 3]) * Gdir[b] * dR[a][b][m];                                    \
                 pose_qt[m] = acc;                                                                              \
             }                                                                                                  \
-            for (int a = 0; a < 3; ++a) pose_qt[4 + a] = qt_cov ? rho[a] : rho_p[a];                           \
+            for (int a = 0; a < 3; ++a) pose_qt[4 + a] = qt_cov ? rho[a] + WG[a] : rho_p[a];                   \
             pose_qt[7] = qp[0]; pose_qt[8] = qp[1]; pose_qt[9] = qp[2]; pose_qt[10] = qp[3];                   \
         }                                                                                                      \
         return 0;                                                                                              \

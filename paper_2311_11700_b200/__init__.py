@@ -68,6 +68,8 @@ _SIGS = {
     "gs_workspace_bytes": (ctypes.c_size_t, [_I64, _I64, _I32, _I32]),
     "gs_ws_init": (ctypes.c_int, [ctypes.POINTER(gs_ws), _P, ctypes.c_size_t, _I64, _I64, _I32, _I32]),
     "gs_project": (ctypes.c_int, [_P, _I64, _I64, _P, _P, ctypes.POINTER(gs_camera), ctypes.POINTER(gs_ws), _P]),
+    "gs_project_sh": (ctypes.c_int, [_P, _I64, _I64, _I32, _P, _P, ctypes.POINTER(gs_camera), ctypes.POINTER(gs_ws),
+                                     _P]),
     "gs_bin_sort": (ctypes.c_int, [ctypes.POINTER(gs_ws), ctypes.POINTER(_I64), _U32, _P]),
     "gs_render_fwd": (ctypes.c_int, [ctypes.POINTER(gs_ws), ctypes.POINTER(gs_camera), _P, _P, _P, _P, _U32, _P]),
     "gs_render_bwd": (ctypes.c_int, [_P, _I64, _I64, _P, ctypes.POINTER(gs_ws), ctypes.POINTER(gs_camera), _P, _P,
@@ -207,6 +209,11 @@ class EventLog:
 def gs_project(params, n, ld, mask, viewmat, cam: gs_camera, ws: Workspace, stream=None):
     _check(_lib.gs_project(_ptr(params), n, ld, _ptr(mask), _ptr(viewmat), ctypes.byref(cam), ctypes.byref(ws.state),
                            _stream(stream)), "gs_project")
+
+
+def gs_project_sh(params, n, ld, sh_degree, mask, viewmat, cam: gs_camera, ws: Workspace, stream=None):
+    _check(_lib.gs_project_sh(_ptr(params), n, ld, sh_degree, _ptr(mask), _ptr(viewmat), ctypes.byref(cam),
+                              ctypes.byref(ws.state), _stream(stream)), "gs_project_sh")
 
 
 def gs_bin_sort(ws: Workspace, flags: int = 0, stream=None) -> int:

@@ -139,10 +139,18 @@ static bool cam_ok(const WsState* s, const gs_camera* cam) {
 
 gs_status gs_project(const float* params, int64_t n, int64_t ld, const uint8_t* mask, const float* viewmat,
                      const gs_camera* cam, gs_ws* ws, void* stream) {
+    return gs_project_sh(params, n, ld, 0, mask, viewmat, cam, ws, stream);
+}
+
+gs_status gs_project_sh(const float* params, int64_t n, int64_t ld, int32_t sh_degree, const uint8_t* mask,
+                        const float* viewmat, const gs_camera* cam, gs_ws* ws, void* stream) {
     if (!ws_ok(ws)) return GS_ERR_INVALID_ARG;
     WsState* s = state(ws);
-    if (n < 0 || n > s->n_cap || ld < n || (n > 0 && !params) || !viewmat || !cam_ok(s, cam)) return GS_ERR_INVALID_ARG;
+    if (n < 0 || n > s->n_cap || ld < n || (n > 0 && !params) || !viewmat || !cam_ok(s, cam) ||
+        (sh_degree != 0 && sh_degree != 1))
+        return GS_ERR_INVALID_ARG;
     s->n = n;
+    s->sh_degree = sh_degree;
     s->cam_w = cam->width;
     s->cam_h = cam->height;
     s->cam_gx = (cam->width + kTile - 1) / kTile;

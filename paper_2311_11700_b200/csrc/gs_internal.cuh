@@ -33,6 +33,8 @@ struct WsState {
         onlist, live_cnt, svals, coop;
     // run state
     int64_t n;                     // Gaussians of the last gs_project
+    int32_t sh_degree;             // colour model of the last gs_project_sh (0 = RGB, 1 = degree-1 SH)
+    int32_t pad_sh;
     int32_t cam_w, cam_h, cam_gx, cam_gy;   // image of the last gs_project
     uint64_t gen_project, gen_fwd; // generation counters (GS_ERR_STALE)
     int32_t sorted_in_1;           // final sorted keys/vals live in buffer 1
@@ -111,7 +113,7 @@ void set_cuda_error(cudaError_t e, const char* what);
 
 // kernels-side entry points (defined in the .cu files; host wrappers)
 void launch_project(WsState* s, const float* params, int64_t n, int64_t ld, const uint8_t* mask,
-                    const float* viewmat, const gs_camera& cam, cudaStream_t st);
+                    const float* viewmat, const gs_camera& cam, cudaStream_t st);   // colour: s->sh_degree
 gs_status run_bin_sort_keys(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t st);
 gs_status run_compact_onscreen(WsState* s, cudaStream_t st, bool depth_hist);
 gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t st);

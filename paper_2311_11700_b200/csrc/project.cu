@@ -14,7 +14,7 @@ __device__ __forceinline__ int clamp_tile(float v, int hi) {
 
 __global__ void __launch_bounds__(256) project_kernel(
     const float* __restrict__ params, int64_t n, int64_t ld, const uint8_t* __restrict__ mask,
-    const float* __restrict__ viewmat, gs_camera cam, int GX, int GY,
+    const float* __restrict__ viewmat, gs_camera cam, int GX, int GY, int sh,
     float4* __restrict__ rec, uint32_t* __restrict__ depth_key, short4* __restrict__ rect,
     int32_t* __restrict__ radius_out, uint32_t* __restrict__ tiles_out) {
     __shared__ float V[12];
@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(256) project_kernel(
 
     float p[14];
 #pragma unroll
-    for (int k = 0; k < 14; ++k) p[k] = __ldg(params + k * ld + i);
+    for (int k = 0; k < 14; ++k) p[k] = __ldg(params + k * ld + i);   // rows 11-13: RGB or SH constant terms
 
     float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0;
     int radius = 0;
@@ -115,7 +115,29 @@ __global__ void __launch_bounds__(256) project_kernel(
             // r1.w: squared Mahalanobis reach q_max = 2 ln(255 o), where o exp(-q/2) = 1/255, plus a
             // margin (render.cu can_reach; no decision uses it, so it is outside reading R1's order)
             r1 = make_float4(-0.5f * cc, p[10], zc, 2.f * (logf(255.f * p[10]) + 1e-4f) + 2e-4f);
-            r2 = make_float4(p[11], p[12], p[13], 0.f);
+            if (sh == 1) {
+                // degree-1 SH colour at the view direction (gs.h gs_project_sh, reading C29), in the
+                // oracle's fp32 order: camera centre c = -W^T t, u = (X - c)/|X - c|,
+                // rgb = max(0, 1/2 + C0 Y0 + C1 (-u_y Y1 + u_z Y2 - u_x Y3)); rows 11 + 3k + c
+                const float cwx = -((V[0] * V[3] + V[4] * V[7]) + V[8] * V[11]);
+                const float cwy = -((V[1] * V[3] + V[5] * V[7]) + V[9] * V[11]);
+                const float cwz = -((V[2] * V[3] + V[6] * V[7]) + V[10] * V[11]);
+                const float dx = p[0] - cwx, dy = p[1] - cwy, dz = p[2] - cwz;
+                const float len = sqrtf((dx * dx + dy * dy) + dz * dz);
+                const float ux = dx / len, uy = dy / len, uz = dz / len;
+                float rgb[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const float y1 = __ldg(params + (14 + c) * ld + i), y2 = __ldg(params + (17 + c) * ld + i),
+                                y3 = __ldg(params + (20 + c) * ld + i);
+                    const float lin = (-(uy * y1) + uz * y2) - ux * y3;
+                    const float v = (0.28209479177387814f * p[11 + c] + 0.4886025119029199f * lin) + 0.5f;
+                    rgb[c] = v > 0.f ? v : 0.f;
+                }
+                r2 = make_float4(rgb[0], rgb[1], rgb[2], 0.f);
+            } else {
+                r2 = make_float4(p[11], p[12], p[13], 0.f);
+            }
         } else {
             radius = 0;
         }
@@ -135,7 +157,8 @@ void launch_project(WsState* s, const float* params, int64_t n, int64_t ld, cons
     if (n == 0) return;
     const int blocks = int((n + 255) / 256);
     KTimer kt(s, KID_PROJECT, st);
-    project_kernel<<<blocks, 256, 0, st>>>(params, n, ld, mask, viewmat, cam, GX, GY, at<float4>(s, s->rec),
+    project_kernel<<<blocks, 256, 0, st>>>(params, n, ld, mask, viewmat, cam, GX, GY, s->sh_degree,
+                                           at<float4>(s, s->rec),
                                            at<uint32_t>(s, s->depth_key), at<short4>(s, s->rect),
                                            at<int32_t>(s, s->radius), at<uint32_t>(s, s->tiles));
 }

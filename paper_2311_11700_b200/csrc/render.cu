@@ -776,6 +776,7 @@ constexpr int kPoseSums = 15;
 __device__ void pose_finalize_block(const double* __restrict__ part, int nblocks, const float* __restrict__ viewmat,
                                     double* __restrict__ grad_pose);
 
+template <int SH>
 __global__ void __launch_bounds__(256, 4) gaussian_bwd_kernel(
     const float* __restrict__ params, int64_t n, int64_t ld, const float* __restrict__ viewmat, gs_camera cam,
     const uint32_t* __restrict__ onlist, const unsigned int* __restrict__ n_on, const float4* __restrict__ rec,
@@ -866,10 +867,46 @@ __global__ void __launch_bounds__(256, 4) gaussian_bwd_kernel(
                                   dJ[1][1] * (-cam.fy * iz2) + dJ[1][2] * (2.f * cam.fy * y * iz3)};
         const float dXm[3] = {J[0][0] * s[0], J[1][1] * s[1], J[0][2] * s[0] + J[1][2] * s[1] + s[9]};
         const float dX[3] = {dXm[0] + dXJ[0], dXm[1] + dXJ[1], dXm[2] + dXJ[2]};
-        if (grad) {
-            // mean: W^T dX
+        // degree-1 SH colour (gs_project_sh, reading C29): per channel c, rgb = max(0, 1/2 + C0 Y0 +
+        // C1 (-u_y Y1 + u_z Y2 - u_x Y3)), u = (X - c)/|X - c|, c = -W^T t. The clamp decision is
+        // recomputed in the projection's fp32 order (same bits). gdir = dL/dX through u.
+        float gdir[3] = {0.f, 0.f, 0.f};
+        if (SH == 1) {
+            const float cwx = -((V[0] * V[3] + V[4] * V[7]) + V[8] * V[11]);
+            const float cwy = -((V[1] * V[3] + V[5] * V[7]) + V[9] * V[11]);
+            const float cwz = -((V[2] * V[3] + V[6] * V[7]) + V[10] * V[11]);
+            const float ddx = __fsub_rn(p[0], cwx), ddy = __fsub_rn(p[1], cwy), ddz = __fsub_rn(p[2], cwz);
+            const float len = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(ddx, ddx), __fmul_rn(ddy, ddy)), __fmul_rn(ddz, ddz)));
+            const float ux = __fdiv_rn(ddx, len), uy = __fdiv_rn(ddy, len), uz = __fdiv_rn(ddz, len);
+            constexpr float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
+            float du[3] = {0.f, 0.f, 0.f};
 #pragma unroll
-            for (int k = 0; k < 3; ++k) grad[k * ld + i] += W[0][k] * dX[0] + W[1][k] * dX[1] + W[2][k] * dX[2];
+            for (int c = 0; c < 3; ++c) {
+                const float y1 = params[(14 + c) * ld + i], y2 = params[(17 + c) * ld + i], y3 = params[(20 + c) * ld + i];
+                const float lin = __fsub_rn(__fadd_rn(-__fmul_rn(uy, y1), __fmul_rn(uz, y2)), __fmul_rn(ux, y3));
+                const float v = __fadd_rn(__fadd_rn(__fmul_rn(C0, p[11 + c]), __fmul_rn(C1, lin)), 0.5f);
+                const float gc = v > 0.f ? s[6 + c] : 0.f;   // clamped channel: no gradient
+                if (grad) {
+                    grad[(11 + c) * ld + i] += gc * C0;
+                    grad[(14 + c) * ld + i] += gc * (-C1 * uy);
+                    grad[(17 + c) * ld + i] += gc * (C1 * uz);
+                    grad[(20 + c) * ld + i] += gc * (-C1 * ux);
+                }
+                du[0] -= gc * C1 * y3;
+                du[1] -= gc * C1 * y1;
+                du[2] += gc * C1 * y2;
+            }
+            const float ud = ux * du[0] + uy * du[1] + uz * du[2];
+            const float il = 1.f / len;
+            gdir[0] = (du[0] - ux * ud) * il;
+            gdir[1] = (du[1] - uy * ud) * il;
+            gdir[2] = (du[2] - uz * ud) * il;
+        }
+        if (grad) {
+            // mean: W^T dX (+ the SH view-direction path)
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                grad[k * ld + i] += W[0][k] * dX[0] + W[1][k] * dX[1] + W[2][k] * dX[2] + gdir[k];
             // Sigma = M M^T
             float dM[3][3];
 #pragma unroll
@@ -898,9 +935,11 @@ __global__ void __launch_bounds__(256, 4) gaussian_bwd_kernel(
             grad[8 * ld + i] += (dq[2] - qj * qd) / nq;
             grad[9 * ld + i] += (dq[3] - qk * qd) / nq;
             grad[10 * ld + i] += s[5];
-            grad[11 * ld + i] += s[6];
-            grad[12 * ld + i] += s[7];
-            grad[13 * ld + i] += s[8];
+            if (SH == 0) {
+                grad[11 * ld + i] += s[6];
+                grad[12 * ld + i] += s[7];
+                grad[13 * ld + i] += s[8];
+            }
         }
         if (pose_part) {
             const float g0 = cov_path ? dX[0] : dXm[0], g1 = cov_path ? dX[1] : dXm[1],
@@ -908,6 +947,10 @@ __global__ void __launch_bounds__(256, 4) gaussian_bwd_kernel(
             pose[0] += g0;
             pose[1] += g1;
             pose[2] += g2;
+            if (cov_path && SH == 1) {   // colour through the camera centre: rho += W gdir (phi: none)
+#pragma unroll
+                for (int a = 0; a < 3; ++a) pose[a] += W[a][0] * gdir[0] + W[a][1] * gdir[1] + W[a][2] * gdir[2];
+            }
             pose[3] += y * g2 - z * g1;
             pose[4] += z * g0 - x * g2;
             pose[5] += x * g1 - y * g0;
@@ -991,11 +1034,11 @@ void launch_gaussian_bwd(WsState* s, const float* params, int64_t n, int64_t ld,
     // grid sized without a host sync: at most 4 blocks per SM, at most ceil(n / 256)
     const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(sms) * 4));
     KTimer kt(s, KID_BWD_GAUSS, st);
-    gaussian_bwd_kernel<<<blocks, 256, 0, st>>>(params, n, ld, viewmat, cam, at<uint32_t>(s, s->onlist),
-                                                &at<Misc>(s, s->misc)->n_onscreen, at<float4>(s, s->rec),
-                                                at<float>(s, s->sgrad), s->n_cap, grad_params,
-                                                (flags & GS_FLAG_POSE_COV_PATH) ? 1 : 0, part,
-                                                &at<Misc>(s, s->misc)->pose_done, grad_pose);
+    auto kern = s->sh_degree == 1 ? gaussian_bwd_kernel<1> : gaussian_bwd_kernel<0>;
+    kern<<<blocks, 256, 0, st>>>(params, n, ld, viewmat, cam, at<uint32_t>(s, s->onlist),
+                                 &at<Misc>(s, s->misc)->n_onscreen, at<float4>(s, s->rec), at<float>(s, s->sgrad),
+                                 s->n_cap, grad_params, (flags & GS_FLAG_POSE_COV_PATH) ? 1 : 0, part,
+                                 &at<Misc>(s, s->misc)->pose_done, grad_pose);
 }
 
 }  // namespace gs

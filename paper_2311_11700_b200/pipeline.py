@@ -8,7 +8,7 @@ import dataclasses
 import torch
 
 from . import (GS_FLAG_EXAMINED, GS_FLAG_POSE_COV_PATH, Workspace, gs_bin_sort, gs_loss_l1, gs_pose_grad,
-               gs_project, gs_render_bwd, gs_render_fwd, make_camera)
+               gs_project_sh, gs_render_bwd, gs_render_fwd, make_camera)
 
 
 @dataclasses.dataclass
@@ -45,9 +45,11 @@ class RenderPipeline:
 
     def forward(self, params, n, viewmat, cam, mask=None, bin_flags=0, fwd_flags=GS_FLAG_EXAMINED,
                 accum_weight=None, stream=None) -> Frame:
+        """params [14][ld] (RGB) or [23][ld] (degree-1 SH, gs_project_sh)."""
         c = make_camera(cam)
         ld = params.shape[1]
-        gs_project(params, n, ld, mask, viewmat, c, self.ws, stream)
+        sh = {14: 0, 23: 1}[params.shape[0]]
+        gs_project_sh(params, n, ld, sh, mask, viewmat, c, self.ws, stream)
         self.n_keys = gs_bin_sort(self.ws, bin_flags, stream)
         color, depth, alpha = self._imgs(cam)
         gs_render_fwd(self.ws, c, color, depth, alpha, accum_weight, fwd_flags, stream)

@@ -405,3 +405,36 @@ def test_bin_sort_bitexact_2m_gaussians():
     cfg = gi.CONFIGS[4]
     p = cfg.scene()
     _bin_sort_check(p, cfg.view(), cfg.cam)
+
+
+# ------------------------------------------------------------------ degree-1 SH colour (NEXT-1, reading C29)
+@pytest.mark.parametrize("c", [0, 1])
+def test_sh1_parity(c):
+    """gs_project_sh(sh_degree = 1): the per-Gaussian colour at the view direction is bit-exact with
+    the oracle's fp32 evaluation (same operation order); images within 1e-4 (tie rule); the 23 row
+    gradients (12 SH coefficients, the mean through the view direction) and the pose twist (colour
+    through the camera centre) within the north_star gradient tolerance."""
+    cfg, p14, v = scene(c)
+    p = gi.with_sh(p14, 500 + c)
+    pipe, P, V, fr = run_forward(p, v, cfg.cam)
+    a = pipe.arrays(p.shape[1])
+    pr = oracle.project(p, v, cfg.cam, "f32")
+    on = pr["tiles"] > 0
+    rec = a["records"].cpu().numpy()
+    assert np.array_equal(rec[on, 8:11], pr["rgb"].T[on])
+    assert (pr["rgb"][:, on] == 0).any() and (pr["rgb"][:, on] > 0).any()   # both clamp branches occur
+    o = oracle.forward(p, v, cfg.cam, "f32")
+    gpu = dict(color=fr.color, depth=fr.depth, alpha=fr.alpha, n_last=a["n_last"])
+    compare_images(gpu, o, cfg.cam, p, v, f"sh1 cfg{c}")
+    H, W = cfg.cam.height, cfg.cam.width
+    dc, dd = gi.upstream(W, H, 600 + c)
+    nl = a["n_last"].cpu().numpy()
+    gg, gpose, gpose2 = _gpu_backward(pipe, P, V, cfg, dc, dd)
+    ob = oracle.backward(p, v, cfg.cam, dc, dd, "f32", replay_nlast=nl)
+    assert gg.shape == (23, p.shape[1])
+    bad = grad_close(gg, ob["grad_params"])
+    assert bad.mean() <= 1e-3, (bad.mean(), np.argwhere(bad)[:10])
+    np.testing.assert_allclose(gpose, ob["pose_twist"], rtol=2e-3, atol=1e-6)
+    np.testing.assert_allclose(gpose, gpose2, rtol=1e-3, atol=1e-6)
+    _, gp_paper, _ = _gpu_backward(pipe, P, V, cfg, dc, dd, cov=False)
+    np.testing.assert_allclose(gp_paper, ob["pose_twist_paper"], rtol=2e-3, atol=1e-6)

@@ -525,3 +525,145 @@ def test_select_mask_brute_force():
 def test_prune_mask():
     o = np.array([0.001, 0.005, 0.0049999, 0.5])
     assert oracle.densify_prune_mask(o).tolist() == [False, True, False, True]
+
+
+# ------------------------------------------------------------------ degree-1 SH colour (NEXT-1, reading C29)
+def sh1_of(p, seed, lin=0.6):
+    """Append degree-1 SH rows to a 14-row scene: constant terms Y0 ~ N(0, 1), linear terms ~ N(0, lin)
+    (rows 11 + 3k + c). The RGB rows are replaced by the constant terms."""
+    rng = np.random.default_rng(seed)
+    n = p.shape[1]
+    q = np.zeros((23, n))
+    q[:11] = p[:11]
+    q[11:14] = rng.normal(0.0, 1.0, (3, n))
+    q[14:23] = rng.normal(0.0, lin, (9, n))
+    return q
+
+
+def test_sh1_basis_normalised_on_the_sphere():
+    """The degree-1 real SH basis is orthonormal on the unit sphere: with one unit coefficient the
+    colour minus its 1/2 offset, squared and averaged over uniformly distributed view directions,
+    equals 1/(4 pi) (for l = 0 and each l = 1 term), and distinct terms are orthogonal."""
+    rng = np.random.default_rng(5)
+    n = 200_000
+    u = rng.normal(size=(3, n))
+    u /= np.linalg.norm(u, axis=0)
+    cam = gi.Camera(30.0, 30.0, 15.5, 15.5, 32, 32)
+    vals = []
+    for k in range(4):
+        p = np.zeros((23, n))
+        p[0:3] = 3.0 * u            # camera centre at the origin (identity pose): direction u
+        p[3:6] = 0.05
+        p[6] = 1.0
+        p[10] = 0.5
+        p[11 + 3 * k] = 1.0        # channel r: unit coefficient of basis term k
+        p[11 + 3 * k + 1] = 1.0    # channel g too (channel b stays 0: colour 1/2 exactly)
+        rgb = oracle.project(p, gi.identity_view(), cam, "f64")["rgb"]
+        # clamping at 0 would bias the integral: use a unit coefficient small enough to stay above 0
+        assert (rgb[0] > 0).all()
+        f = rgb[0] - 0.5
+        vals.append(f)
+        assert np.allclose(rgb[2], 0.5)
+        np.testing.assert_allclose(rgb[1], rgb[0], rtol=0, atol=1e-15)
+    for k in range(4):
+        assert abs(4 * math.pi * np.mean(vals[k] ** 2) - 1.0) < 0.01, k
+        for m in range(k):
+            assert abs(4 * math.pi * np.mean(vals[k] * vals[m])) < 0.01, (k, m)
+
+
+def test_sh1_odd_symmetry_and_rgb_reduction():
+    """The l = 1 terms are odd in the view direction: mirroring a Gaussian through the camera centre
+    flips them, so rgb(X) + rgb(2c - X) = 2 (1/2 + C0 Y0) (unclamped). With zero linear terms the SH
+    scene renders exactly like the RGB scene with rgb = 1/2 + C0 Y0 at any pose."""
+    p14, cam = tiny_scene(12, 41)
+    view = small_pose(42, rot_deg=20, trans=0.3)
+    p14[0:3] = view[:, :3].T @ (p14[0:3] - view[:, 3:4])
+    p = sh1_of(p14, 43, lin=0.1)
+    p[11:14] = np.abs(p[11:14]) + 0.5    # keep every channel above the clamp
+    c = -view[:, :3].T @ view[:, 3]
+    mirrored = p.copy()
+    mirrored[0:3] = 2 * c[:, None] - p[0:3]
+    a = oracle.project(p, view, cam, "f64")["rgb"]
+    b = oracle.project(mirrored, view, cam, "f64")["rgb"]
+    const = oracle.project(np.concatenate([p[:14], np.zeros((9, p.shape[1]))]), view, cam, "f64")["rgb"]
+    np.testing.assert_allclose(a + b, 2 * const, rtol=0, atol=1e-12)
+    # reduction: zero linear terms == RGB rows holding the constant-term colour
+    p0 = p.copy()
+    p0[14:23] = 0.0
+    rgb = p14.copy()
+    rgb[11:14] = oracle.project(p0, view, cam, "f64")["rgb"]
+    f_sh = oracle.forward(p0, view, cam, "f64")
+    f_rgb = oracle.forward(rgb, view, cam, "f64")
+    np.testing.assert_allclose(f_sh["color"], f_rgb["color"], rtol=0, atol=1e-12)
+    assert f_sh["hash"] == f_rgb["hash"]
+
+
+@pytest.mark.parametrize("seed", [61, 62])
+def test_sh1_backward_matches_central_fd(seed):
+    """Central FD on the fp64 oracle over all 23 parameter rows (12 SH coefficients, and the mean
+    through the view direction) and the 6 pose components (the colour reaches the pose through the
+    camera centre)."""
+    p14, cam = tiny_scene(10, seed)
+    view = small_pose(seed, rot_deg=10, trans=0.2)
+    p14[0:3] = view[:, :3].T @ (p14[0:3] - view[:, 3:4])
+    p = sh1_of(p14, seed + 1)
+    dc, dd = gi.upstream(cam.width, cam.height, seed + 100)
+    dc32, dd32 = dc.astype(np.float32).astype(np.float64), dd.astype(np.float32).astype(np.float64)
+    g = oracle.backward(p, view, cam, dc.astype(np.float32), dd.astype(np.float32), "f64")
+    checked = rejected = 0
+    for i in range(p.shape[1]):
+        for k in range(23):
+            h = 1e-6 * max(abs(p[k, i]), 0.05)
+            pp, pm = p.copy(), p.copy()
+            pp[k, i] += h
+            pm[k, i] -= h
+            lp, hp = linear_loss(pp, view, cam, dc32, dd32)
+            lm, hm = linear_loss(pm, view, cam, dc32, dd32)
+            rp = oracle.project(pp, view, cam, "f64")["rgb"][:, i]
+            rm = oracle.project(pm, view, cam, "f64")["rgb"][:, i]
+            if hp != hm or ((rp > 0) != (rm > 0)).any():   # a decision or a colour clamp flips
+                rejected += 1
+                continue
+            fd = (lp - lm) / (2 * h)
+            an = g["grad_params"][k, i]
+            assert abs(fd - an) <= 1e-3 * max(abs(fd), abs(an)) + 1e-8, (i, k, fd, an)
+            checked += 1
+    assert checked >= 0.9 * 23 * p.shape[1] and rejected < 0.1 * 23 * p.shape[1]
+    pose_checked = 0
+    for k in range(6):
+        for eps in (1e-6, 3e-7, 1e-7):
+            e = np.zeros(6)
+            e[k] = eps
+            lp, hp = linear_loss(p, oracle.apply_twist(e, view), cam, dc32, dd32)
+            lm, hm = linear_loss(p, oracle.apply_twist(-e, view), cam, dc32, dd32)
+            if hp == hm:
+                break
+        if hp != hm:
+            continue
+        fd = (lp - lm) / (2 * eps)
+        an = g["pose_twist"][k]
+        assert abs(fd - an) <= 1e-3 * max(abs(fd), abs(an)) + 1e-8, (k, fd, an)
+        pose_checked += 1
+    assert pose_checked >= 5
+
+
+def test_sh1_pose_qt_path_equals_twist_path():
+    """With degree-1 SH the colour depends on the camera centre c = -W^T t: the (q, t) path (which
+    sees c move with both q and t) mapped to the twist equals the twist path, whose colour term is
+    rho += W sum dL/dX_dir and nothing in phi."""
+    p14, cam = tiny_scene(15, 71)
+    view = small_pose(72, rot_deg=25, trans=0.2)
+    p14[0:3] = view[:, :3].T @ (p14[0:3] - view[:, 3:4])
+    p = sh1_of(p14, 73)
+    dc, dd = gi.upstream(cam.width, cam.height, 74)
+    g = oracle.backward(p, view, cam, dc, dd, "f64", qt_cov=True)
+    q = g["pose_quat"]
+    t = view[:, 3]
+    tw = np.zeros(6)
+    tw[:3] = g["pose_t"]
+    for k in range(3):
+        ek = np.zeros(3)
+        ek[k] = 1.0
+        dq = np.concatenate([[-0.5 * ek @ q[1:]], 0.5 * (q[0] * ek + np.cross(ek, q[1:]))])
+        tw[3 + k] = g["pose_q"] @ dq + g["pose_t"] @ np.cross(ek, t)
+    np.testing.assert_allclose(tw, g["pose_twist"], rtol=1e-9, atol=1e-12)
