@@ -170,13 +170,21 @@ gs_status gs_pose_step(float* viewmat, const double* grad_pose, float* m6, float
  *                    params_raw, adam_m, adam_v (any of the last three may be NULL); n_dev updated.
  *  GS_DENSIFY_SELECT Eq. 12 (reading C24): select_mask[i] = accum_weight[i] > sel_weight and
  *                    |D*(round m_i) - d_i| < sel_depth, using the last gs_project on this ws.
+ *  GS_DENSIFY_DEGENERATE  Eq. 9 (reading C27): every
+ *                    Gaussian visible in the last gs_project on this ws (tiles > 0) whose centre
+ *                    pixel round(m_i) is inside the image with valid D* > 0 and lies in front of
+ *                    the observed surface by more than gamma (D* - d_i > gamma, fp32) has its
+ *                    opacity scaled: o_i <- eta o_i (params row 10; params_raw row 10 <- logit of
+ *                    the new opacity if params_raw != NULL; Adam moments unchanged). select_mask
+ *                    (nullable) receives the per-Gaussian flag. The map size is unchanged.
  * n_dev: device int64 [1] (in/out). All compaction is deterministic. */
-enum { GS_DENSIFY_ADD = 1, GS_DENSIFY_PRUNE = 2, GS_DENSIFY_SELECT = 3 };
+enum { GS_DENSIFY_ADD = 1, GS_DENSIFY_PRUNE = 2, GS_DENSIFY_SELECT = 3, GS_DENSIFY_DEGENERATE = 4 };
 typedef struct {
     int32_t mode;
     float tau_alpha, tau_depth, min_opacity, sel_weight, sel_depth, init_opacity;
     int32_t stride;
     int64_t max_add;
+    float eta, gamma;        /* DEGENERATE: opacity factor (0.1) and floater margin in metres (0.10) */
 } gs_densify_cfg;
 gs_status gs_densify_prune(float* params, float* params_raw /*nullable*/, int64_t* n_dev, int64_t capacity,
                            int64_t ld, float* adam_m /*nullable*/, float* adam_v /*nullable*/, const float* alpha,

@@ -323,6 +323,31 @@ def densify_prune_mask(opacity, min_opacity=0.005) -> np.ndarray:
     return np.asarray(opacity, np.float64) >= min_opacity
 
 
+def degenerate_mask(mean2d, depth, tiles, tgt_depth, gamma=0.10) -> np.ndarray:
+    """Eq. 9, reading C27: a Gaussian visible in the frame (tiles > 0) is a floater iff its
+    centre pixel round(m) = floor(m + 0.5) is inside the image with valid D* > 0 and D* - d > gamma
+    ("in front of the scene surfaces"). The comparison is fp32 (both sides decide in fp32)."""
+    td = np.asarray(tgt_depth, np.float32)
+    h, w = td.shape
+    m = np.asarray(mean2d, np.float32)
+    u = np.floor(m[0] + np.float32(0.5))
+    v = np.floor(m[1] + np.float32(0.5))
+    inside = (u >= 0) & (u < w) & (v >= 0) & (v < h) & (np.asarray(tiles) > 0)
+    ui = np.where(inside, u, 0).astype(np.int64)
+    vi = np.where(inside, v, 0).astype(np.int64)
+    dstar = td[vi, ui]
+    return inside & (dstar > 0) & ((dstar - np.asarray(depth, np.float32)) > np.float32(gamma))
+
+
+def degenerate(opacity, mask, eta=0.1):
+    """Eq. 9: Lambda_i <- eta Lambda_i for the flagged Gaussians (fp32 product); the raw (logit) value
+    of the new opacity in fp64."""
+    o = np.asarray(opacity, np.float32).copy()
+    o[mask] = np.float32(eta) * o[mask]
+    od = o.astype(np.float64)
+    return o, np.log(od / (1.0 - od))
+
+
 def select_mask(mean2d, depth, tiles, accum_weight, tgt_depth, sel_weight=0.5, sel_depth=0.05) -> np.ndarray:
     """Eq. 12, reading C24: keep iff accumulated alpha*T > sel_weight and
     |D*(round m) - d| < sel_depth at pixel round(m) = floor(m + 0.5) inside the image, D* > 0."""

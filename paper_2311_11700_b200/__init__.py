@@ -27,7 +27,7 @@ GS_FLAG_ACCUM_WEIGHT = 4
 GS_FLAG_EXAMINED = 8
 GS_FLAG_BINSORT_KEYS = 16
 GS_FLAG_BINSORT_EMIT_ONLY = 256
-GS_DENSIFY_ADD, GS_DENSIFY_PRUNE, GS_DENSIFY_SELECT = 1, 2, 3
+GS_DENSIFY_ADD, GS_DENSIFY_PRUNE, GS_DENSIFY_SELECT, GS_DENSIFY_DEGENERATE = 1, 2, 3, 4
 
 
 class gs_camera(ctypes.Structure):
@@ -55,7 +55,8 @@ class gs_ws_view(ctypes.Structure):
 class gs_densify_cfg(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int32), ("tau_alpha", ctypes.c_float), ("tau_depth", ctypes.c_float),
                 ("min_opacity", ctypes.c_float), ("sel_weight", ctypes.c_float), ("sel_depth", ctypes.c_float),
-                ("init_opacity", ctypes.c_float), ("stride", ctypes.c_int32), ("max_add", ctypes.c_int64)]
+                ("init_opacity", ctypes.c_float), ("stride", ctypes.c_int32), ("max_add", ctypes.c_int64),
+                ("eta", ctypes.c_float), ("gamma", ctypes.c_float)]
 
 
 _P = ctypes.c_void_p
@@ -263,10 +264,11 @@ def gs_pose_step(viewmat, grad_pose, m6, v6, step, lr_rho, lr_phi, stream=None):
 
 
 def densify_cfg(mode, tau_alpha=0.5, tau_depth=0.10, min_opacity=0.005, sel_weight=0.5, sel_depth=0.05,
-                init_opacity=0.5, stride=2, max_add=0) -> gs_densify_cfg:
+                init_opacity=0.5, stride=2, max_add=0, eta=0.1, gamma=0.10) -> gs_densify_cfg:
     c = gs_densify_cfg()
     c.mode, c.tau_alpha, c.tau_depth, c.min_opacity = mode, tau_alpha, tau_depth, min_opacity
     c.sel_weight, c.sel_depth, c.init_opacity, c.stride, c.max_add = sel_weight, sel_depth, init_opacity, stride, max_add
+    c.eta, c.gamma = eta, gamma
     return c
 
 

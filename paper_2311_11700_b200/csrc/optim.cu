@@ -428,6 +428,31 @@ __global__ void select_kernel(int64_t n, const int64_t* n_dev, const float4* __r
     }
 }
 
+// Eq. 9 (reading C27): opacity degeneration of floaters in front of the observed surface
+__global__ void degenerate_kernel(int64_t n, const int64_t* n_dev, const float4* __restrict__ rec,
+                                  const uint32_t* __restrict__ tiles, const float* __restrict__ td, int W, int H,
+                                  float gamma, float eta, float* __restrict__ opacity, float* __restrict__ raw_opacity,
+                                  uint8_t* __restrict__ mask) {
+    const int64_t nn = n_dev ? *n_dev : n;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nn; i += int64_t(gridDim.x) * blockDim.x) {
+        bool hit = false;
+        if (tiles[i] > 0) {
+            const float4 r0 = rec[3 * i], r1 = rec[3 * i + 1];
+            const float u = floorf(r0.x + 0.5f), v = floorf(r0.y + 0.5f);
+            if (u >= 0.f && u < float(W) && v >= 0.f && v < float(H)) {
+                const float t = td[int64_t(v) * W + int64_t(u)];
+                hit = t > 0.f && __fsub_rn(t, r1.z) > gamma;
+            }
+        }
+        if (hit) {
+            const float o = __fmul_rn(eta, opacity[i]);
+            opacity[i] = o;
+            if (raw_opacity) raw_opacity[i] = logf(o / (1.f - o));
+        }
+        if (mask) mask[i] = hit ? 1 : 0;
+    }
+}
+
 #define GS_K(call)                              \
     do {                                        \
         KTimer kt_(s, KID_DENSIFY, st);         \
@@ -446,6 +471,13 @@ gs_status run_densify(WsState* s, float* params, float* raw, int64_t* n_dev, int
                                                     accum, tdepth, cam.width, cam.height, cfg.sel_weight,
                                                     cfg.sel_depth, select_mask)));
         return check_launch(s, "densify_select");
+    }
+    if (cfg.mode == GS_DENSIFY_DEGENERATE) {
+        const int blocks = int(std::min<int64_t>((capacity + 255) / 256, 148 * 8));
+        GS_K((degenerate_kernel<<<blocks, 256, 0, st>>>(capacity, n_dev, at<float4>(s, s->rec), at<uint32_t>(s, s->tiles),
+                                                        tdepth, cam.width, cam.height, cfg.gamma, cfg.eta,
+                                                        params + 10 * ld, raw ? raw + 10 * ld : nullptr, select_mask)));
+        return check_launch(s, "densify_degenerate");
     }
     if (cfg.mode == GS_DENSIFY_ADD) {
         const int64_t npx = int64_t(cam.width) * cam.height;

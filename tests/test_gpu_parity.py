@@ -302,6 +302,33 @@ def test_select_parity():
     assert np.array_equal(mask.cpu().numpy().astype(bool), want)
 
 
+def test_degenerate_parity():
+    """Eq. 9 opacity degeneration (NEXT-2): the flagged set bit-exact with the oracle (both decide in
+    fp32 on the bit-exact projection), the new opacities bit-exact, their logits within 1e-5."""
+    import paper_2311_11700_b200 as g
+    cfg, p, v = scene(1)
+    key_cap, _ = key_cap_for(p, v, cfg.cam)
+    pipe = g.RenderPipeline(p.shape[1], key_cap, cfg.cam.width, cfg.cam.height)
+    P, V = to_dev(p), to_dev(v)
+    pipe.forward(P, p.shape[1], V, cfg.cam)
+    _, td = gi.random_images(cfg.cam.width, cfg.cam.height, 11, 0.5, 3.0)
+    raw = torch.zeros_like(P)
+    mask = torch.zeros(p.shape[1], dtype=torch.uint8, device="cuda")
+    n_dev = torch.tensor([p.shape[1]], dtype=torch.int64, device="cuda")
+    g.gs_densify_prune(P, raw, n_dev, p.shape[1], p.shape[1], None, None, None, None, None, to_dev(td), None, V,
+                       g.make_camera(cfg.cam), g.densify_cfg(g.GS_DENSIFY_DEGENERATE, eta=0.1, gamma=0.10), mask,
+                       None, pipe.ws)
+    torch.cuda.synchronize()
+    pr = oracle.project(p, v, cfg.cam, "f32")
+    want = oracle.degenerate_mask(pr["mean2d"], pr["depth"], pr["tiles"], td, gamma=0.10)
+    got = mask.cpu().numpy().astype(bool)
+    assert np.array_equal(got, want) and 0 < want.sum() < want.size
+    o, lo = oracle.degenerate(p[10], want, eta=0.1)
+    assert np.array_equal(P[10].cpu().numpy(), o)
+    np.testing.assert_allclose(raw[10].cpu().numpy()[want], lo[want], rtol=1e-5, atol=1e-6)
+    assert int(n_dev.item()) == p.shape[1]
+
+
 # ------------------------------------------------------------------ edge cases
 def test_edge_empty_and_culled_and_ragged():
     import paper_2311_11700_b200 as g

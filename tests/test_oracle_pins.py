@@ -667,3 +667,36 @@ def test_sh1_pose_qt_path_equals_twist_path():
         dq = np.concatenate([[-0.5 * ek @ q[1:]], 0.5 * (q[0] * ek + np.cross(ek, q[1:]))])
         tw[3 + k] = g["pose_q"] @ dq + g["pose_t"] @ np.cross(ek, t)
     np.testing.assert_allclose(tw, g["pose_twist"], rtol=1e-9, atol=1e-12)
+
+
+# ------------------------------------------------------------------ Eq. 9 opacity degeneration (NEXT-2)
+def test_degenerate_hand_built_fixture():
+    """Eq. 9 with a flat wall at D* = 3 m seen head-on (reading C27: D* - d > gamma): a Gaussian
+    0.5 m in front of the wall is a floater; one 0.05 m in front (within gamma = 0.1), one behind the
+    wall, one whose centre pixel has no valid depth and one off-screen are not. Degeneration scales
+    the flagged opacity by eta and nothing else."""
+    W, H = 32, 24
+    cam = gi.Camera(30.0, 30.0, (W - 1) / 2, (H - 1) / 2, W, H)
+    zs = [2.5, 2.95, 3.4, 2.0, 2.0]
+    xs = [0.0, 0.3, -0.3, 0.0, 40.0]   # the last one projects far outside the image
+    ys = [0.0, 0.2, -0.2, 0.5, 0.0]
+    n = len(zs)
+    p = np.zeros((14, n))
+    p[0] = np.array(xs) * np.array(zs) / 10
+    p[1] = np.array(ys) * np.array(zs) / 10
+    p[2] = zs
+    p[3:6] = 0.02
+    p[6] = 1.0
+    p[10] = 0.8
+    p[11:14] = 0.5
+    td = np.full((H, W), 3.0, np.float32)
+    pr = oracle.project(p, gi.identity_view(), cam, "f32")
+    # invalidate the depth at Gaussian 3's centre pixel
+    u3 = int(np.floor(pr["mean2d"][0, 3] + 0.5))
+    v3 = int(np.floor(pr["mean2d"][1, 3] + 0.5))
+    td[v3, u3] = 0.0
+    mask = oracle.degenerate_mask(pr["mean2d"], pr["depth"], pr["tiles"], td, gamma=0.10)
+    assert mask.tolist() == [True, False, False, False, False]
+    o, raw = oracle.degenerate(p[10], mask, eta=0.1)
+    np.testing.assert_allclose(o, [0.08, 0.8, 0.8, 0.8, 0.8], rtol=1e-7)
+    np.testing.assert_allclose(raw[0], math.log(0.08 / 0.92), rtol=1e-6)
