@@ -8,6 +8,11 @@ One process per GPU; each rank holds a full replica of the map and renders ITS k
                        -> all_gather of candidate counts and padded candidates (rank order)
                        -> gs_densify_append in global keyframe order (identical on every rank)
                        -> gs_densify_prune(PRUNE, opacity < 0.005)
+  bundle adjustment:   Eq. 13 with `ba_iters`: map only for
+                       the first half of the iterations, then map and keyframe poses (gs_render_bwd
+                       with grad_pose per local keyframe -> gs_pose_step on that keyframe's view). A
+                       keyframe's pose gradient comes only from its own render, so it stays on the rank
+                       that owns the keyframe: no exchange.
 Learning rates follow PAPER.md:931-933 (position 1.6e-5 -> 1.7e-7 exponentially over 100 steps,
 colour 5e-4, opacity 1e-2, scale 2e-4, rotation 4e-5). The collective helpers are plain
 torch.distributed calls and work with gloo on CPU tensors as well (tests/test_dist_gloo.py).
@@ -20,7 +25,7 @@ import torch
 import torch.distributed as dist
 
 from . import (GS_DENSIFY_ADD, GS_DENSIFY_PRUNE, GS_FLAG_NO_HOST_SYNC, densify_cfg, gs_adam_step,
-               gs_densify_append, gs_densify_prune, make_camera)
+               gs_densify_append, gs_densify_prune, gs_pose_step, make_camera)
 from .pipeline import RenderPipeline
 
 
@@ -75,7 +80,7 @@ class Keyframe:
 class ShardedMapper:
     def __init__(self, params: torch.Tensor, n: int, keyframes: list[Keyframe], cam, key_cap: int,
                  max_add_per_kf: int = 8192, w_color: float = 0.9, w_depth: float = 0.1, group=None,
-                 densify: bool = True):
+                 densify: bool = True, ba_iters: int | None = None, lr_rho: float = 1e-3, lr_phi: float = 1e-3):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if self.world > 1 else 0
@@ -99,6 +104,17 @@ class ShardedMapper:
         self.cand = torch.zeros(L, 14, max_add_per_kf, device=params.device)
         self.counts = torch.zeros(L, dtype=torch.int64, device=params.device)
         self.it = 0
+        # bundle adjustment state (Eq. 13): per local keyframe pose gradient and Adam moments
+        self.ba_iters = ba_iters
+        self.lr_rho, self.lr_phi = lr_rho, lr_phi
+        self.gpose = torch.zeros(L, 6, dtype=torch.float64, device=params.device)
+        self.pm = torch.zeros(L, 6, device=params.device)
+        self.pv = torch.zeros(L, 6, device=params.device)
+        self.pose_step = 0
+
+    def poses_active(self) -> bool:
+        """Eq. 13: poses are optimised only in the second half of the BA iterations."""
+        return self.ba_iters is not None and self.it >= self.ba_iters // 2
 
     def render_backward(self):
         """fwd + L1 + bwd for every local keyframe, accumulating into grad."""
@@ -107,7 +123,11 @@ class ShardedMapper:
             kf = self.keyframes[k]
             self.pipe.forward(self.P, self.n, kf.view, self.cam, bin_flags=GS_FLAG_NO_HOST_SYNC, fwd_flags=0)
             dc, dd = self.pipe.loss_l1(self.cam, kf.color, kf.depth, self.w_color, self.w_depth)
-            self.pipe.backward(self.P, self.n, kf.view, self.cam, dc, dd, self.grad)
+            gp = None
+            if self.poses_active():
+                gp = self.gpose[j]
+                gp.zero_()
+            self.pipe.backward(self.P, self.n, kf.view, self.cam, dc, dd, self.grad, gp)
             if self.densify:   # Eq. 8 candidates from this keyframe's render (gather mode)
                 cnt = self.counts[j:j + 1]
                 gs_densify_prune(self.P, None, cnt, self.cap, self.cap, None, None, self.pipe.alpha, self.pipe.depth,
@@ -115,8 +135,14 @@ class ShardedMapper:
                                  densify_cfg(GS_DENSIFY_ADD, max_add=self.max_add), None, self.cand[j], self.pipe.ws)
 
     def step(self):
+        poses = self.poses_active()
         self.render_backward()
         allreduce_grads(self.grad, self.group)
+        if poses:   # each rank updates the poses of its own keyframes (device-only pose step)
+            self.pose_step += 1
+            for j, k in enumerate(self.local):
+                gs_pose_step(self.keyframes[k].view, self.gpose[j], self.pm[j], self.pv[j], self.pose_step,
+                             self.lr_rho, self.lr_phi)
         self.it += 1
         gs_adam_step(self.raw, self.P, self.grad, self.m, self.v, self.n, self.cap, learning_rates(self.it - 1),
                      self.it)
