@@ -297,9 +297,11 @@ __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
     using BS = cub::BlockScan<int, kFwd2Batch>;
     __shared__ typename BS::TempStorage scan_tmp;
     constexpr int kU = 4;   // Gaussians per fast-path group (below)
-    __shared__ float4 s_rec[2][kFwd2Batch + 1][3];   // slot kFwd2Batch: a zero record (padding entry)
+    __shared__ float4 s_rec[2][kFwd2Batch][3];       // staged records (double-buffered)
     __shared__ uint32_t s_g[2][kFwd2Batch];
-    __shared__ int s_live[kFwd2Batch + kU];          // padded to a multiple of kU with the zero slot
+    __shared__ float4 s_lrec[kFwd2Batch + kU][3];    // the batch's live records, in order, padded to a
+                                                     // multiple of kU with zero records; .w of the third
+                                                     // float4 holds the 1-based list position
     __shared__ int s_nlive;
     const int tile = blockIdx.x;
     const int tx = tile % GX, ty = tile / GX;
@@ -334,7 +336,6 @@ __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
         }
         cp_async_commit();
     };
-    if (threadIdx.x < 6) s_rec[threadIdx.x / 3][kFwd2Batch][threadIdx.x % 3] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (nbatch > 0) stage(0);
     for (int b = 0; b < nbatch; ++b) {
         if (b + 1 < nbatch) {
@@ -354,11 +355,21 @@ __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
             int off, tot;
             BS(scan_tmp).ExclusiveSum(lv, off, tot);
             if (lv) {
-                s_live[off] = k;
+                const uint32_t j = uint32_t(b * kFwd2Batch + k + 1);
                 live_g[start + acc + off] = s_g[b & 1][k];
-                live_j[start + acc + off] = uint32_t(b * kFwd2Batch + k + 1);
+                live_j[start + acc + off] = j;
+                float4 r2 = buf[k][2];
+                r2.w = __uint_as_float(j);
+                s_lrec[off][0] = buf[k][0];
+                s_lrec[off][1] = buf[k][1];
+                s_lrec[off][2] = r2;
             }
-            if (k >= tot && k < ((tot + kU - 1) & ~(kU - 1))) s_live[k] = kFwd2Batch;   // zero record: alpha 0
+            if (k >= tot && k < ((tot + kU - 1) & ~(kU - 1))) {   // zero record: opacity 0 -> alpha 0
+                const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                s_lrec[k][0] = z;
+                s_lrec[k][1] = z;
+                s_lrec[k][2] = z;
+            }
             if (k == 0) s_nlive = tot;
             __syncthreads();
         }
@@ -369,14 +380,12 @@ __global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
         // after the group is >= 1e-4, every T (1 - alpha) tested inside it was too. Otherwise the
         // warp restores the group's entry state and replays it with the exact step (rare: once
         // per pixel at most).
-        const uint32_t jb = uint32_t(b * kFwd2Batch + 1);
         auto entry = [&](int k0, int u, float4& r1, float4& r2, uint32_t& j, f32x2& pw) {
-            // past nlive the list is padded with the zero slot: opacity 0 -> alpha 0 -> skipped exactly
-            const int k = s_live[k0 + u];
-            const float4 r0 = buf[k][0];
-            r1 = buf[k][1];
-            r2 = buf[k][2];
-            j = jb + uint32_t(k);
+            // past nlive the list is padded with zero records: opacity 0 -> alpha 0 -> skipped exactly
+            const float4 r0 = s_lrec[k0 + u][0];
+            r1 = s_lrec[k0 + u][1];
+            r2 = s_lrec[k0 + u][2];
+            j = __float_as_uint(r2.w);
             // eval_alpha's operation sequence per pixel; the x-terms are shared by the pair
             const float dx = __fsub_rn(r0.x, fpx);
             const float Adx = __fmul_rn(r0.z, dx), Bdx = __fmul_rn(r0.w, dx);
