@@ -288,7 +288,7 @@ __device__ __forceinline__ bool can_reach(float4 r0, float4 r1, float x0, float 
     return qmin - 3e-5f * qmag - 1e-5f <= qmax;
 }
 
-__global__ void __launch_bounds__(kTilePx / 2) render_fwd2_kernel(
+__global__ void __launch_bounds__(kTilePx / 2, 6) render_fwd2_kernel(
     const float4* __restrict__ rec, const uint32_t* __restrict__ vals, const uint2* __restrict__ ranges, int W, int H,
     int GX, float bgr, float bgg, float bgb, float* __restrict__ color, float* __restrict__ depth,
     float* __restrict__ alpha, float* __restrict__ t_final, uint32_t* __restrict__ n_last,
