@@ -479,7 +479,7 @@ void launch_render_fwd(WsState* s, const gs_camera& cam, float* color, float* de
 //   phase 2  lane = (Gaussian, row group): pixel moments with compile-time x
 //   combine  one thread per (component, Gaussian) sums the per-warp partial moments it needs, turns
 //            them into the screen-space gradient and issues its atomic.
-// The staged batches rotate through 3 slots, so a batch needs 3 block barriers and none at its end.
+// The staged batches rotate through 3 slots, so a batch needs 2 block barriers and none at its end.
 constexpr int kBB = 16;                          // Gaussians per backward batch
 constexpr int kBwdThreads = kTilePx / 2;         // 128
 constexpr int kBwdWarps = kBwdThreads / 32;
@@ -643,6 +643,47 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
     // phase-2 lane roles: Gaussian k2 of the batch, row group gi (rows gi + kGroups r)
     const int k2 = lane & (kBB - 1), gi = warp * (32 / kBB) + lane / kBB;
     if (nbatch > 0) stage(nbatch - 1, 0);
+    // ---- moments -> screen-space gradients of batch bb (staged in slot gbuf); one thread and one
+    // atomic per (component, Gaussian). Each thread sums the per-warp partial sets it needs. Batch
+    // bb's gradients run right after the NEXT batch's barrier [A] (or after the loop): part and the
+    // slot are rewritten only after that batch's barrier [B] and two stagings later, so no barrier of
+    // their own is needed (two barriers per batch).
+    auto gradients = [&](int gbuf, int gbb) {
+        const int cnt = min(kBB, int(len) - gbb * kBB);
+        auto moment = [&](int c, int k) {
+            float a = 0.f;
+#pragma unroll
+            for (int p = 0; p < kBwdWarps; ++p) a += sm.part[p][c][k];
+            return a;
+        };
+        for (int t = tid; t < 10 * kBB; t += kBwdThreads) {
+            const int c = t / kBB, k = t % kBB;
+            if (k >= cnt) continue;
+            float v;
+            if (c >= 5) {
+                v = moment(c == 5 ? 0 : c, k);   // opacity (sum g), rgb, depth
+            } else {
+                const float M0 = moment(0, k), Mx = moment(1, k), My = moment(2, k);
+                const float4 r0 = sm.rec[gbuf][k][0];
+                const float o = sm.rec[gbuf][k][1].y;
+                const float X = r0.x - float(tx * kTile), Y = r0.y - float(ty * kTile);
+                // sums of g dx, g dy, g dx^2, g dx dy, g dy^2 with dx = X - lx, dy = Y - ly
+                const float gdx = X * M0 - Mx, gdy = Y * M0 - My;
+                if (c == 0) {
+                    v = o * (2.f * r0.z * gdx + r0.w * gdy);            // mean2d x: -o (a gdx + b gdy)
+                } else if (c == 1) {
+                    v = o * (r0.w * gdx + 2.f * sm.rec[gbuf][k][1].x * gdy);   // mean2d y: -o (b gdx + c gdy)
+                } else if (c == 2) {
+                    v = -0.5f * o * (X * X * M0 - 2.f * X * Mx + moment(3, k));            // conic a
+                } else if (c == 3) {
+                    v = -o * (X * Y * M0 - X * My - Y * Mx + moment(4, k));                 // conic b
+                } else {
+                    v = -0.5f * o * (Y * Y * M0 - 2.f * Y * My + moment(5, k));            // conic c
+                }
+            }
+            if (v != 0.f) atomicAdd(sgrad + c * sld + sm.idx[gbuf][k], v);
+        }
+    };
     for (int it = 0; it < nbatch; ++it) {
         const int bb = nbatch - 1 - it;
         const int buf = it % kSlots;
@@ -652,7 +693,8 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
         } else {
             cp_async_wait<0>();
         }
-        __syncthreads();   // [A] batch staged
+        __syncthreads();   // [A] batch staged (and the previous batch's partial sets complete)
+        if (it > 0) gradients((it - 1) % kSlots, bb + 1);
         // ---- phase 1
         // records are read one step ahead (shared-memory latency off the dependent chain)
         uint32_t pk_n = sm.pos[buf][kBB - 1];
@@ -712,44 +754,10 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
                 for (int c = 0; c < 10; ++c) sm.part[warp][c][k2] = m[c];
             }
         }
-        __syncthreads();   // [C] partial sets complete
-        // ---- moments -> screen-space gradients; one thread and one atomic per (component, Gaussian).
-        // Each thread sums the per-warp partial sets it needs (no separate combine pass and barrier:
-        // part is rewritten only after the next batch's barriers [A] and [B]).
-        const int cnt = min(kBB, int(len) - bb * kBB);
-        auto moment = [&](int c, int k) {
-            float a = 0.f;
-#pragma unroll
-            for (int p = 0; p < kBwdWarps; ++p) a += sm.part[p][c][k];
-            return a;
-        };
-        for (int t = tid; t < 10 * kBB; t += kBwdThreads) {
-            const int c = t / kBB, k = t % kBB;
-            if (k >= cnt) continue;
-            float v;
-            if (c >= 5) {
-                v = moment(c == 5 ? 0 : c, k);   // opacity (sum g), rgb, depth
-            } else {
-                const float M0 = moment(0, k), Mx = moment(1, k), My = moment(2, k);
-                const float4 r0 = sm.rec[buf][k][0];
-                const float o = sm.rec[buf][k][1].y;
-                const float X = r0.x - float(tx * kTile), Y = r0.y - float(ty * kTile);
-                // sums of g dx, g dy, g dx^2, g dx dy, g dy^2 with dx = X - lx, dy = Y - ly
-                const float gdx = X * M0 - Mx, gdy = Y * M0 - My;
-                if (c == 0) {
-                    v = o * (2.f * r0.z * gdx + r0.w * gdy);            // mean2d x: -o (a gdx + b gdy)
-                } else if (c == 1) {
-                    v = o * (r0.w * gdx + 2.f * sm.rec[buf][k][1].x * gdy);   // mean2d y: -o (b gdx + c gdy)
-                } else if (c == 2) {
-                    v = -0.5f * o * (X * X * M0 - 2.f * X * Mx + moment(3, k));            // conic a
-                } else if (c == 3) {
-                    v = -o * (X * Y * M0 - X * My - Y * Mx + moment(4, k));                 // conic b
-                } else {
-                    v = -0.5f * o * (Y * Y * M0 - 2.f * Y * My + moment(5, k));            // conic c
-                }
-            }
-            if (v != 0.f) atomicAdd(sgrad + c * sld + sm.idx[buf][k], v);
-        }
+    }
+    if (nbatch > 0) {
+        __syncthreads();   // the last batch's partial sets are complete
+        gradients((nbatch - 1) % kSlots, 0);
     }
 }
 
