@@ -26,7 +26,7 @@ gs_status resolve_keys(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t
 // B5 ---------------------------------------------------------------------------------------
 // Block = (16x16-tile area, chunks c = blockIdx.x + i * gridDim.x below ceil(V_s / 256), read on the
 // device). Warp-specialised, with no block barriers in the loop:
-//   producer warp (warp 8): per chunk, tests the chunk's 256 Gaussians (8 per lane, depth order)
+//   producer warps (8, 9; alternating chunks): per chunk, test its 256 Gaussians (8 per lane, depth order)
 //      against the block area and compacts the hits in order (ballot + popc) into a slot of a
 //      4-deep shared-memory ring, then arrives on the slot's "full" mbarrier;
 //   consumer warps 0-7, each an 8x4-tile sub-area (lane j = tile (j & 7, j >> 3)): wait on "full",
@@ -42,6 +42,7 @@ constexpr int kBX = 16, kBY = 16;      // block tile area: 2 x 4 consumer areas
 constexpr int kEmitChunkBlocks = 256;  // grid.x: chunk stride (measured: 96 -> 0.091 ms, 224-320 -> 0.081 ms)
 constexpr int kRing = 4;               // chunk slots in flight
 constexpr int kConsumers = 8;
+constexpr int kProducers = 2;          // producer warps, alternating chunks (ring order kept)
 
 struct EmitSmem {
     short4 rect[kRing][kChunk];
@@ -73,7 +74,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
     } while (!done);
 }
 
-__global__ void __launch_bounds__((kConsumers + 1) * 32) bucket_emit_kernel(
+__global__ void __launch_bounds__((kConsumers + kProducers) * 32) bucket_emit_kernel(
     const uint32_t* __restrict__ svals, const short4* __restrict__ srect, const uint32_t* __restrict__ cmat,
     const unsigned int* __restrict__ n_on, const unsigned long long* __restrict__ n_keys_eff,
     const unsigned long long* __restrict__ n_keys, int GX, int GY, uint32_t* __restrict__ vals_out) {
@@ -92,10 +93,11 @@ __global__ void __launch_bounds__((kConsumers + 1) * 32) bucket_emit_kernel(
         }
     }
     __syncthreads();
-    if (warp == kConsumers) {
-        // ---------------------------------------------------------------- producer
-        int it = 0;
-        for (int c = blockIdx.x; c < nch; c += gridDim.x, ++it) {
+    if (warp >= kConsumers) {
+        // ---------------------------------------------------------------- producers
+        const int pw = warp - kConsumers;
+        int it = pw;
+        for (int c = blockIdx.x + pw * gridDim.x; c < nch; c += kProducers * gridDim.x, it += kProducers) {
             const int slot = it % kRing;
             const uint32_t s0 = uint32_t(c) * kChunk;
             short4 r[kChunk / 32];
@@ -195,7 +197,7 @@ gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaS
         KTimer kt(s, KID_BUCKET_EMIT, st);
         const dim3 grid(unsigned(std::min(nch, kEmitChunkBlocks)), unsigned((s->cam_gx + kBX - 1) / kBX),
                         unsigned((s->cam_gy + kBY - 1) / kBY));
-        bucket_emit_kernel<<<grid, (kConsumers + 1) * 32, 0, st>>>(at<uint32_t>(s, s->svals), at<short4>(s, s->srect),
+        bucket_emit_kernel<<<grid, (kConsumers + kProducers) * 32, 0, st>>>(at<uint32_t>(s, s->svals), at<short4>(s, s->srect),
                                                  at<uint32_t>(s, s->chunk_mat), &misc->n_onscreen, &misc->n_keys_eff,
                                                  &misc->n_keys, s->cam_gx, s->cam_gy, at<uint32_t>(s, s->vals0));
     } else {
