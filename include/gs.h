@@ -193,6 +193,31 @@ gs_status gs_densify_prune(float* params, float* params_raw /*nullable*/, int64_
                            const gs_densify_cfg* cfg /*(host)*/, uint8_t* select_mask, float* add_out,
                            gs_ws* ws, void* stream);
 
+/* gs_densify_accum_grad — densification statistics (3DGS adaptive density control, which the paper
+ * uses for "splits large points into smaller ones and clones them"; reading C30):
+ * for every on-screen Gaussian i of the last gs_render_bwd on ws,
+ *   grad_accum[i] += |(dL/dm_x W/2, dL/dm_y H/2)|  (the screen-space mean gradient in NDC units),
+ *   count[i] += 1.
+ * grad_accum, count: device float[>= n]. Errors: GS_ERR_STALE without a backward since the last
+ * forward. */
+gs_status gs_densify_accum_grad(gs_ws* ws, float* grad_accum, float* count, void* stream);
+
+/* gs_densify_split_clone — one densification step (every 10 mapping iterations before the 70th,
+ * thresholds 0.002 and 0.02 m; reading C30) over params[14][ld] columns [0, n):
+ * avg_i = grad_accum_i / count_i (0 if count_i == 0); i is a candidate iff avg_i >= grad_thresh;
+ * a candidate with max scale <= scale_thresh is CLONED (a copy appended), otherwise SPLIT: two
+ * children X + R(q) diag(s) eps_k, k = 0, 1 (eps_k = noise rows 3k..3k+2 at column i, N(0,1) drawn by
+ * the caller), scale s / 1.6, the other parameters copied, are appended and the original removed.
+ * Result order: the kept originals (index order), then the clones (index order), then the children
+ * (index order, child 0 then child 1). Appends beyond capacity are dropped (clones first; a split
+ * is applied only if both children fit). Appended Gaussians get raw copies (log scale, logit
+ * opacity) and zero Adam moments; grad_accum and count are reset to 0 over [0, capacity); n_dev
+ * updated. Deterministic. noise: device float[6][ld]. */
+gs_status gs_densify_split_clone(float* params, float* params_raw /*nullable*/, float* adam_m /*nullable*/,
+                                 float* adam_v /*nullable*/, int64_t* n_dev, int64_t capacity, int64_t ld,
+                                 float* grad_accum, float* count, const float* noise, float grad_thresh,
+                                 float scale_thresh, gs_ws* ws, void* stream);
+
 /* gs_densify_append — append gathered ADD candidates (multi-GPU mapping):
  * cand[k][14][max_add] (activated, k < n_sets, in global keyframe order) with counts[k] (device
  * int64) are appended in order k = 0, 1, ... at columns [n, n + sum counts) of params[14][ld]

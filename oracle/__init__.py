@@ -323,6 +323,59 @@ def densify_prune_mask(opacity, min_opacity=0.005) -> np.ndarray:
     return np.asarray(opacity, np.float64) >= min_opacity
 
 
+def _rot(q):
+    q = np.asarray(q, np.float64)
+    r, x, y, z = q / np.linalg.norm(q)
+    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - r * z), 2 * (x * z + r * y)],
+                     [2 * (x * y + r * z), 1 - 2 * (x * x + z * z), 2 * (y * z - r * x)],
+                     [2 * (x * z - r * y), 2 * (y * z + r * x), 1 - 2 * (x * x + y * y)]])   # Eq. S1
+
+
+def accum_grad(grad_screen, tiles, W, H, accum, count):
+    """Reading C30 (3DGS adaptive density control): for the on-screen Gaussians,
+    accum += |(dL/dm_x W/2, dL/dm_y H/2)| (NDC units), count += 1."""
+    on = np.asarray(tiles) > 0
+    g = np.hypot(np.asarray(grad_screen[0], np.float64) * (W / 2), np.asarray(grad_screen[1], np.float64) * (H / 2))
+    a = np.asarray(accum, np.float64).copy()
+    c = np.asarray(count, np.float64).copy()
+    a[on] += g[on]
+    c[on] += 1
+    return a, c
+
+
+def split_clone(params, accum, count, noise, grad_thresh=0.002, scale_thresh=0.02, capacity=None):
+    """Reading C30: avg = accum / count (0 if count == 0); candidates avg >= grad_thresh; clone
+    (max scale <= scale_thresh) = a copy; split = two children X + R(q) diag(s) eps_k (noise rows 3k..3k+2)
+    with scale s / 1.6, the original removed. Order: kept originals, clones, children. Appends beyond
+    capacity are dropped (clones first; a split only if both children fit). Returns (params, appended
+    mask of the result [new columns], removed originals)."""
+    p = np.asarray(params, np.float64)
+    n = p.shape[1]
+    cap = n if capacity is None else capacity
+    cnt = np.asarray(count, np.float64)
+    avg = np.where(cnt > 0, np.asarray(accum, np.float64) / np.where(cnt > 0, cnt, 1), 0.0)
+    cand = avg >= grad_thresh
+    smax = p[3:6].max(0)
+    clone = np.flatnonzero(cand & (smax <= scale_thresh))
+    split = np.flatnonzero(cand & ~(smax <= scale_thresh))
+    avail = cap - n
+    clone = clone[:max(avail, 0)]
+    split = split[:max(avail - clone.size, 0) // 2]
+    new = [p[:, i] for i in clone]
+    for i in split:
+        R = _rot(p[6:10, i])
+        s = p[3:6, i]
+        for k in range(2):
+            c = p[:, i].copy()
+            c[0:3] = p[0:3, i] + R @ (s * np.asarray(noise, np.float64)[3 * k:3 * k + 3, i])
+            c[3:6] = s / 1.6
+            new.append(c)
+    keep = np.ones(n, bool)
+    keep[split] = False
+    out = np.concatenate([p[:, keep]] + ([np.stack(new, 1)] if new else []), axis=1)
+    return out, clone, split
+
+
 def degenerate_mask(mean2d, depth, tiles, tgt_depth, gamma=0.10) -> np.ndarray:
     """Eq. 9, reading C27: a Gaussian visible in the frame (tiles > 0) is a floater iff its
     centre pixel round(m) = floor(m + 0.5) is inside the image with valid D* > 0 and D* - d > gamma

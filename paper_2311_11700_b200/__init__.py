@@ -69,6 +69,9 @@ _SIGS = {
     "gs_workspace_bytes": (ctypes.c_size_t, [_I64, _I64, _I32, _I32]),
     "gs_ws_init": (ctypes.c_int, [ctypes.POINTER(gs_ws), _P, ctypes.c_size_t, _I64, _I64, _I32, _I32]),
     "gs_project": (ctypes.c_int, [_P, _I64, _I64, _P, _P, ctypes.POINTER(gs_camera), ctypes.POINTER(gs_ws), _P]),
+    "gs_densify_accum_grad": (ctypes.c_int, [ctypes.POINTER(gs_ws), _P, _P, _P]),
+    "gs_densify_split_clone": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _F, _F, ctypes.POINTER(gs_ws),
+                                              _P]),
     "gs_project_sh": (ctypes.c_int, [_P, _I64, _I64, _I32, _P, _P, ctypes.POINTER(gs_camera), ctypes.POINTER(gs_ws),
                                      _P]),
     "gs_bin_sort": (ctypes.c_int, [ctypes.POINTER(gs_ws), ctypes.POINTER(_I64), _U32, _P]),
@@ -280,6 +283,18 @@ def gs_densify_prune(params, params_raw, n_dev, capacity, ld, adam_m, adam_v, al
                                  _ptr(accum_weight), _ptr(viewmat), ctypes.byref(cam) if cam is not None else None,
                                  ctypes.byref(cfg), _ptr(select_mask), _ptr(add_out), ctypes.byref(ws.state),
                                  _stream(stream)), "gs_densify_prune")
+
+
+def gs_densify_accum_grad(ws: Workspace, grad_accum, count, stream=None):
+    _check(_lib.gs_densify_accum_grad(ctypes.byref(ws.state), _ptr(grad_accum), _ptr(count), _stream(stream)),
+           "gs_densify_accum_grad")
+
+
+def gs_densify_split_clone(params, params_raw, adam_m, adam_v, n_dev, capacity, ld, grad_accum, count, noise,
+                           grad_thresh, scale_thresh, ws: Workspace, stream=None):
+    _check(_lib.gs_densify_split_clone(_ptr(params), _ptr(params_raw), _ptr(adam_m), _ptr(adam_v), _ptr(n_dev), capacity,
+                                       ld, _ptr(grad_accum), _ptr(count), _ptr(noise), grad_thresh, scale_thresh,
+                                       ctypes.byref(ws.state), _stream(stream)), "gs_densify_split_clone")
 
 
 def gs_densify_append(params, params_raw, adam_m, adam_v, n_dev, capacity, ld, cand, counts, n_sets, max_add,

@@ -194,6 +194,7 @@ static gs_status backward_common(const float* params, int64_t n, int64_t ld, con
         cudaMemset2DAsync(s->dev + s->sgrad.off, size_t(s->n_cap) * 4, 0, size_t(n) * 4, 10, st);
     launch_render_bwd_tiles(s, *cam, nullptr, dLdC, dLdD, st);
     launch_gaussian_bwd(s, params, n, ld, viewmat, *cam, grad, grad_pose, flags, st);
+    s->gen_bwd = s->gen_fwd;
     return check_launch(s, "gs_render_bwd");
 }
 
@@ -283,6 +284,26 @@ gs_status gs_densify_append(float* params, float* params_raw, float* adam_m, flo
     launch_append(params, params_raw, adam_m, adam_v, n_dev, capacity, ld, cand, counts, n_sets, max_add,
                   static_cast<cudaStream_t>(stream));
     return check_launch(nullptr, "gs_densify_append");
+}
+
+gs_status gs_densify_accum_grad(gs_ws* ws, float* grad_accum, float* count, void* stream) {
+    if (!ws_ok(ws) || !grad_accum || !count) return GS_ERR_INVALID_ARG;
+    WsState* s = state(ws);
+    if (s->gen_fwd == 0 || s->gen_bwd != s->gen_fwd || s->gen_fwd != s->gen_project) return GS_ERR_STALE;
+    launch_accum_grad(s, grad_accum, count, static_cast<cudaStream_t>(stream));
+    return check_launch(s, "gs_densify_accum_grad");
+}
+
+gs_status gs_densify_split_clone(float* params, float* params_raw, float* adam_m, float* adam_v, int64_t* n_dev,
+                                 int64_t capacity, int64_t ld, float* grad_accum, float* count, const float* noise,
+                                 float grad_thresh, float scale_thresh, gs_ws* ws, void* stream) {
+    if (!ws_ok(ws) || !params || !n_dev || !grad_accum || !count || !noise || capacity < 0 || ld < capacity ||
+        !(grad_thresh >= 0.f) || !(scale_thresh >= 0.f))
+        return GS_ERR_INVALID_ARG;
+    WsState* s = state(ws);
+    if (capacity > s->n_cap) return GS_ERR_INVALID_ARG;
+    return run_split_clone(s, params, params_raw, adam_m, adam_v, n_dev, capacity, ld, grad_accum, count, noise,
+                           grad_thresh, scale_thresh, static_cast<cudaStream_t>(stream));
 }
 
 gs_status gs_ws_get_view(const gs_ws* ws, gs_ws_view* out) {

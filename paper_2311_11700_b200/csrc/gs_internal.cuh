@@ -37,6 +37,7 @@ struct WsState {
     int32_t pad_sh;
     int32_t cam_w, cam_h, cam_gx, cam_gy;   // image of the last gs_project
     uint64_t gen_project, gen_fwd; // generation counters (GS_ERR_STALE)
+    uint64_t gen_bwd;              // gen_fwd of the last gs_render_bwd / gs_pose_grad
     int32_t sorted_in_1;           // final sorted keys/vals live in buffer 1
     int32_t keys_valid;            // path A materialised the 64-bit keys (view.keys valid)
     int64_t n_keys_host;           // K of the last host-synced gs_bin_sort (-1 unknown)
@@ -132,6 +133,10 @@ void launch_pose_step(float* viewmat, const double* gp, float* m6, float* v6, in
                       float lr_phi, cudaStream_t st);
 void launch_append(float* params, float* raw, float* m, float* v, int64_t* n_dev, int64_t capacity, int64_t ld,
                    const float* cand, const int64_t* counts, int32_t n_sets, int64_t max_add, cudaStream_t st);
+void launch_accum_grad(WsState* s, float* grad_accum, float* count, cudaStream_t st);
+gs_status run_split_clone(WsState* s, float* params, float* raw, float* m, float* v, int64_t* n_dev, int64_t capacity,
+                          int64_t ld, float* grad_accum, float* count, const float* noise, float grad_thresh,
+                          float scale_thresh, cudaStream_t st);
 gs_status run_densify(WsState* s, float* params, float* raw, int64_t* n_dev, int64_t capacity, int64_t ld,
                       float* m, float* v, const float* alpha, const float* depth, const float* trgb,
                       const float* tdepth, const float* accum, const float* viewmat, const gs_camera& cam,

@@ -409,6 +409,159 @@ __global__ void copy_rows_kernel(const float* __restrict__ src, int64_t src_ld, 
 
 __global__ void set_n_kernel(int64_t* n_dev, const unsigned long long* count) { *n_dev = int64_t(*count); }
 
+// ------------------------------------------------------------------ split / clone (reading C30)
+__global__ void accum_grad_kernel(const uint32_t* __restrict__ onlist, const unsigned int* __restrict__ n_on,
+                                  const float* __restrict__ sgrad, int64_t sld, float hw, float hh,
+                                  float* __restrict__ accum, float* __restrict__ count) {
+    const int64_t V = int64_t(*n_on);
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < V; t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = onlist[t];
+        const float gx = sgrad[i] * hw, gy = sgrad[sld + i] * hh;   // dL/dm in NDC units
+        accum[i] += sqrtf(gx * gx + gy * gy);
+        count[i] += 1.f;
+    }
+}
+
+void launch_accum_grad(WsState* s, float* grad_accum, float* count, cudaStream_t st) {
+    KTimer kt(s, KID_DENSIFY, st);
+    accum_grad_kernel<<<148 * 4, 256, 0, st>>>(at<uint32_t>(s, s->onlist), &at<Misc>(s, s->misc)->n_onscreen,
+                                               at<float>(s, s->sgrad), s->n_cap, 0.5f * float(s->cam_w),
+                                               0.5f * float(s->cam_h), grad_accum, count);
+}
+
+// candidate type of Gaussian i: 1 clone, 2 split, 0 none
+__device__ __forceinline__ int dens_type(const float* params, int64_t ld, const float* accum, const float* count,
+                                         int64_t i, float gthr, float sthr) {
+    const float c = count[i];
+    const float avg = c > 0.f ? accum[i] / c : 0.f;
+    if (!(avg >= gthr)) return 0;
+    const float smax = fmaxf(fmaxf(params[3 * ld + i], params[4 * ld + i]), params[5 * ld + i]);
+    return smax <= sthr ? 1 : 2;
+}
+
+struct TypePred {
+    const float *params, *accum, *count;
+    int64_t ld;
+    float gthr, sthr;
+    int type;
+    __device__ bool operator()(int64_t i) const { return dens_type(params, ld, accum, count, i, gthr, sthr) == type; }
+};
+
+struct SplitCloneEmit {   // appends clones (type 1) or split children (type 2)
+    float *params, *raw, *m, *v, *accum;
+    const float* noise;
+    int64_t ld, capacity;
+    const int64_t* n_dev;
+    const unsigned long long* n_clone;   // clones found (type 2 pass: the clones applied come first)
+    int type;
+    __device__ void put(int64_t col, const float* rec) const {
+        for (int k = 0; k < 14; ++k) params[k * ld + col] = rec[k];
+        if (raw) {
+            for (int k = 0; k < 14; ++k) raw[k * ld + col] = rec[k];
+            for (int k = 3; k < 6; ++k) raw[k * ld + col] = logf(rec[k]);
+            raw[10 * ld + col] = logf(rec[10] / (1.f - rec[10]));
+        }
+        if (m) for (int k = 0; k < 14; ++k) m[k * ld + col] = 0.f;
+        if (v) for (int k = 0; k < 14; ++k) v[k * ld + col] = 0.f;
+    }
+    __device__ void operator()(int64_t i, uint32_t o) const {
+        const int64_t n = *n_dev, avail = capacity - n;
+        float rec[14];
+        for (int k = 0; k < 14; ++k) rec[k] = params[k * ld + i];
+        if (type == 1) {
+            if (int64_t(o) < avail) put(n + o, rec);
+            return;
+        }
+        const int64_t nc = min(int64_t(*n_clone), avail);
+        const int64_t col = n + nc + 2 * int64_t(o);
+        if (col + 2 > capacity) return;   // does not fit: the split is not applied
+        // children: X + R(q) diag(s) eps_k, scale s / 1.6 (3DGS, reading C30)
+        const float qn = sqrtf(rec[6] * rec[6] + rec[7] * rec[7] + rec[8] * rec[8] + rec[9] * rec[9]);
+        const float r = rec[6] / qn, x = rec[7] / qn, y = rec[8] / qn, z = rec[9] / qn;
+        const float R[3][3] = {{1.f - 2.f * (y * y + z * z), 2.f * (x * y - r * z), 2.f * (x * z + r * y)},
+                               {2.f * (x * y + r * z), 1.f - 2.f * (x * x + z * z), 2.f * (y * z - r * x)},
+                               {2.f * (x * z - r * y), 2.f * (y * z + r * x), 1.f - 2.f * (x * x + y * y)}};
+        float child[14];
+        for (int c = 0; c < 2; ++c) {
+            for (int k = 0; k < 14; ++k) child[k] = rec[k];
+            float e[3];
+            for (int a = 0; a < 3; ++a) e[a] = rec[3 + a] * noise[(3 * c + a) * ld + i];
+            for (int a = 0; a < 3; ++a) child[a] = rec[a] + (R[a][0] * e[0] + R[a][1] * e[1] + R[a][2] * e[2]);
+            for (int a = 0; a < 3; ++a) child[3 + a] = rec[3 + a] / 1.6f;
+            put(col + c, child);
+        }
+        accum[i] = -1.f;   // applied: the original is removed by the compaction below
+    }
+};
+
+struct KeepSplitPred {
+    const float* accum;
+    const int64_t* n_dev;
+    __device__ bool operator()(int64_t i) const { return i >= *n_dev || accum[i] >= 0.f; }
+};
+
+__global__ void split_clone_total_kernel(int64_t* total, const int64_t* n_dev, const unsigned long long* nc,
+                                         const unsigned long long* ns, int64_t capacity) {
+    const int64_t n = *n_dev, avail = capacity - n;
+    const int64_t c = min(int64_t(*nc), avail);
+    const int64_t sp = min(int64_t(*ns), (avail - c) / 2);
+    *total = n + c + 2 * sp;   // columns holding originals and appended Gaussians before the compaction
+}
+
+__global__ void zero2_kernel(float* a, float* b, int64_t n) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        a[i] = 0.f;
+        b[i] = 0.f;
+    }
+}
+
+gs_status run_split_clone(WsState* s, float* params, float* raw, float* m, float* v, int64_t* n_dev, int64_t capacity,
+                          int64_t ld, float* accum, float* count, const float* noise, float gthr, float sthr,
+                          cudaStream_t st) {
+    Misc* misc = at<Misc>(s, s->misc);
+    uint32_t* bcounts = at<uint32_t>(s, s->chunk_hist);
+    const int nb = int((capacity + kCmpTile - 1) / kCmpTile);
+    unsigned long long* nclone = &misc->add_count;
+    unsigned long long* nsplit = &misc->keep_count;
+    // clones (index order)
+    TypePred pc{params, accum, count, ld, gthr, sthr, 1};
+    KTimer kt(s, KID_DENSIFY, st);
+    count_kernel<<<nb, kCmpThreads, 0, st>>>(capacity, n_dev, pc, bcounts);
+    scan_blocks_kernel<<<1, 1024, 0, st>>>(bcounts, nb, nclone);
+    scatter_kernel<<<nb, kCmpThreads, 0, st>>>(capacity, n_dev, pc,
+                                               SplitCloneEmit{params, raw, m, v, accum, noise, ld, capacity, n_dev,
+                                                              nclone, 1},
+                                               bcounts);
+    // splits (index order), after the clones
+    TypePred ps{params, accum, count, ld, gthr, sthr, 2};
+    count_kernel<<<nb, kCmpThreads, 0, st>>>(capacity, n_dev, ps, bcounts);
+    scan_blocks_kernel<<<1, 1024, 0, st>>>(bcounts, nb, nsplit);
+    scatter_kernel<<<nb, kCmpThreads, 0, st>>>(capacity, n_dev, ps,
+                                               SplitCloneEmit{params, raw, m, v, accum, noise, ld, capacity, n_dev,
+                                                              nclone, 2},
+                                               bcounts);
+    // n_dev <- columns in use; then drop the applied split originals by stable compaction
+    int64_t* ncols = reinterpret_cast<int64_t*>(at<char>(s, s->scratch));
+    split_clone_total_kernel<<<1, 1, 0, st>>>(ncols, n_dev, nclone, nsplit, capacity);
+    const KeepSplitPred keep{accum, n_dev};
+    // compaction over [0, ncols): n_dev stays the original n inside the predicate (appended columns kept)
+    const int nb2 = int((capacity + kCmpTile - 1) / kCmpTile);
+    count_kernel<<<nb2, kCmpThreads, 0, st>>>(capacity, ncols, keep, bcounts);
+    scan_blocks_kernel<<<1, 1024, 0, st>>>(bcounts, nb2, &misc->keep_count);
+    float* scratch = at<float>(s, s->scratch14);
+    float* arrays[4] = {raw, m, v, params};
+    for (float* a : arrays) {
+        if (!a) continue;
+        scatter_kernel<<<nb2, kCmpThreads, 0, st>>>(capacity, ncols, keep, GatherEmit{a, scratch, ld, s->n_cap},
+                                                    bcounts);
+        dim3 g(unsigned(std::min<int64_t>((capacity + 255) / 256, 148 * 4)), 14);
+        copy_rows_kernel<<<g, 256, 0, st>>>(scratch, s->n_cap, a, ld, &misc->keep_count);
+    }
+    set_n_kernel<<<1, 1, 0, st>>>(n_dev, &misc->keep_count);
+    zero2_kernel<<<148 * 4, 256, 0, st>>>(accum, count, capacity);
+    return check_launch(s, "densify_split_clone");
+}
+
 __global__ void select_kernel(int64_t n, const int64_t* n_dev, const float4* __restrict__ rec,
                               const uint32_t* __restrict__ tiles, const float* __restrict__ accum,
                               const float* __restrict__ td, int W, int H, float sel_w, float sel_d,

@@ -465,3 +465,70 @@ def test_sh1_parity(c):
     np.testing.assert_allclose(gpose, gpose2, rtol=1e-3, atol=1e-6)
     _, gp_paper, _ = _gpu_backward(pipe, P, V, cfg, dc, dd, cov=False)
     np.testing.assert_allclose(gp_paper, ob["pose_twist_paper"], rtol=2e-3, atol=1e-6)
+
+
+def test_accum_grad_and_split_clone_parity():
+    """Densification (NEXT-2, reading C30): the NDC-unit screen-gradient statistics match the oracle's
+    screen gradients within the gradient tolerance; with the GPU's statistics as input (both sides
+    decide on the same values, thresholds placed between values) the split/clone layout is exact,
+    copies and raw values bit-exact / close, children within fp32 rounding, Adam moments zero for
+    the appended Gaussians, statistics reset."""
+    import paper_2311_11700_b200 as g
+    cfg, p, v = scene(0)
+    n = p.shape[1]
+    cap = n + 600
+    pc = np.zeros((14, cap), np.float32)
+    pc[:, :n] = p
+    key_cap, _ = key_cap_for(p, v, cfg.cam)
+    pipe = g.RenderPipeline(cap, key_cap, cfg.cam.width, cfg.cam.height)   # n_cap covers the appends
+    P, V = to_dev(p), to_dev(v)
+    pipe.forward(P, n, V, cfg.cam)
+    Pc = to_dev(pc)
+    H, W = cfg.cam.height, cfg.cam.width
+    dc, dd = gi.upstream(W, H, gi.UPSTREAM_SEED_CFG0)
+    nl = pipe.arrays(n)["n_last"].cpu().numpy()
+    grad = torch.zeros_like(P)
+    pipe.backward(P, n, V, cfg.cam, to_dev(dc), to_dev(dd), grad)
+    acc = torch.zeros(cap, device="cuda")
+    cnt = torch.zeros(cap, device="cuda")
+    for _ in range(2):   # two identical backward passes accumulate twice
+        g.gs_densify_accum_grad(pipe.ws, acc, cnt)
+    torch.cuda.synchronize()
+    ob = oracle.backward(p, v, cfg.cam, dc, dd, "f32", replay_nlast=nl)
+    pr = oracle.project(p, v, cfg.cam, "f32")
+    a0, c0 = oracle.accum_grad(ob["grad_screen"], pr["tiles"], W, H, np.zeros(n), np.zeros(n))
+    a0, c0 = 2 * a0, 2 * c0
+    ga, gc = acc.cpu().numpy()[:n], cnt.cpu().numpy()[:n]
+    assert np.array_equal(gc, c0)
+    bad = grad_close(ga, a0)
+    assert bad.mean() <= 1e-3
+    # split / clone with thresholds between observed values
+    avg = np.where(gc > 0, ga / np.where(gc > 0, gc, 1), 0).astype(np.float32)
+    pos = np.unique(avg[avg > 0])
+    gthr = float(0.5 * (pos[len(pos) // 2] + pos[len(pos) // 2 + 1]))
+    smax = p[3:6].max(0)
+    sv = np.unique(smax)
+    sthr = float(0.5 * (sv[len(sv) // 2] + sv[len(sv) // 2 + 1]))
+    noise = np.random.default_rng(9).normal(size=(6, cap)).astype(np.float32)
+    raw = torch.zeros_like(Pc)
+    raw[:, :n] = Pc[:, :n]
+    m = torch.ones_like(Pc)
+    vv = torch.ones_like(Pc)
+    n_dev = torch.tensor([n], dtype=torch.int64, device="cuda")
+    g.gs_densify_split_clone(Pc, raw, m, vv, n_dev, cap, cap, acc, cnt, to_dev(noise), gthr, sthr, pipe.ws)
+    torch.cuda.synchronize()
+    want, clone, split = oracle.split_clone(p, ga, gc, noise[:, :n], gthr, sthr, capacity=cap)
+    assert clone.size > 0 and split.size > 0
+    n2 = int(n_dev.item())
+    assert n2 == want.shape[1] == n - split.size + clone.size + 2 * split.size
+    got = Pc[:, :n2].cpu().numpy()
+    n_keep = n - split.size
+    assert np.array_equal(got[:, :n_keep + clone.size], want[:, :n_keep + clone.size].astype(np.float32))
+    np.testing.assert_allclose(got[:, n_keep + clone.size:], want[:, n_keep + clone.size:], rtol=1e-5, atol=1e-6)
+    new = slice(n_keep, n2)
+    assert float(m[:, new].abs().max()) == 0.0 and float(vv[:, new].abs().max()) == 0.0
+    rw = raw[:, new].cpu().numpy()
+    np.testing.assert_allclose(rw[3:6], np.log(want[3:6, n_keep:]), rtol=1e-5, atol=1e-6)
+    o = want[10, n_keep:]
+    np.testing.assert_allclose(rw[10], np.log(o / (1 - o)), rtol=1e-5, atol=1e-6)
+    assert float(acc.abs().max()) == 0.0 and float(cnt.abs().max()) == 0.0

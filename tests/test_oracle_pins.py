@@ -700,3 +700,39 @@ def test_degenerate_hand_built_fixture():
     o, raw = oracle.degenerate(p[10], mask, eta=0.1)
     np.testing.assert_allclose(o, [0.08, 0.8, 0.8, 0.8, 0.8], rtol=1e-7)
     np.testing.assert_allclose(raw[0], math.log(0.08 / 0.92), rtol=1e-6)
+
+
+# ------------------------------------------------------------------ split / clone (NEXT-2, reading C30)
+def test_split_clone_hand_built():
+    """Three Gaussians with hand-set statistics: below the gradient threshold (untouched), small and
+    above it (cloned: an exact copy appended), large and above it (split: removed, two children at
+    X + R diag(s) eps with scale s/1.6). With the identity rotation the children sit at X + s * eps
+    exactly; with a 90-degree rotation about z, (ex, ey) map to (-ey, ex)."""
+    p = np.zeros((14, 4))
+    p[0:3] = [[0, 1, 2, 3], [0, 0, 0, 0], [2, 2, 2, 2]]
+    p[3:6] = np.array([0.01, 0.01, 0.05, 0.04])[None, :] * np.array([[1.0], [0.5], [0.5]])
+    p[6] = 1.0
+    p[6:10, 3] = [math.cos(math.pi / 4), 0, 0, math.sin(math.pi / 4)]   # 90 deg about z
+    p[10] = [0.3, 0.4, 0.5, 0.6]
+    p[11:14] = 0.5
+    accum = np.array([0.001, 0.009, 0.012, 0.02])
+    count = np.array([1.0, 3.0, 4.0, 4.0])    # averages 0.001, 0.003, 0.003, 0.005
+    noise = np.zeros((6, 4))
+    noise[:, 2] = [1, 2, 3, -1, -2, -3]
+    noise[:, 3] = [1, 0, 0, 0, 1, 0]
+    out, clone, split = oracle.split_clone(p, accum, count, noise, 0.002, 0.02, capacity=10)
+    assert clone.tolist() == [1] and split.tolist() == [2, 3]
+    assert out.shape[1] == 4 - 2 + 1 + 4
+    np.testing.assert_array_equal(out[:, 0], p[:, 0])
+    np.testing.assert_array_equal(out[:, 1], p[:, 1])
+    np.testing.assert_array_equal(out[:, 2], p[:, 1])   # the clone
+    s2 = p[3:6, 2]
+    np.testing.assert_allclose(out[0:3, 3], p[0:3, 2] + s2 * [1, 2, 3])
+    np.testing.assert_allclose(out[0:3, 4], p[0:3, 2] - s2 * [1, 2, 3])
+    np.testing.assert_allclose(out[3:6, 3], s2 / 1.6)
+    s3 = p[3:6, 3]
+    np.testing.assert_allclose(out[0:3, 5], p[0:3, 3] + [0, s3[0], 0], atol=1e-12)    # e_x -> e_y
+    np.testing.assert_allclose(out[0:3, 6], p[0:3, 3] + [-s3[1], 0, 0], atol=1e-12)   # e_y -> -e_x
+    # capacity: one free column takes the clone only; no split fits
+    out2, c2, s2_ = oracle.split_clone(p, accum, count, noise, 0.002, 0.02, capacity=5)
+    assert c2.tolist() == [1] and s2_.size == 0 and out2.shape[1] == 5
