@@ -225,10 +225,8 @@ def main_ours(args):
     gpose = torch.zeros(6, dtype=torch.float64, device=dev)
     flags = bin_flags | g.GS_FLAG_NO_HOST_SYNC
 
-    def step():
-        grad.zero_()
-        gpose.zero_()
-        pipe.iteration(P, n, V, cam, tc, td, grad, gpose, bin_flags=flags, fwd_flags=0)
+    def step():   # the gradients are assigned (GS_FLAG_GRAD_ASSIGN): no zeroing pass
+        pipe.iteration(P, n, V, cam, tc, td, grad, gpose, bin_flags=flags, fwd_flags=0, assign_grads=True)
 
     def barrier():
         if dist:
@@ -331,9 +329,8 @@ def main_ours(args):
                         upload(i + 1)
                     Pd, Vd, tcd, tdd = bufs[i % 2]
                     cur.wait_event(ev_copied[i % 2])
-                    grad.zero_()
-                    gpose.zero_()
-                    pipe.iteration(Pd, n, Vd, cam, tcd, tdd, grad, gpose, bin_flags=flags, fwd_flags=0)
+                    pipe.iteration(Pd, n, Vd, cam, tcd, tdd, grad, gpose, bin_flags=flags, fwd_flags=0,
+                                   assign_grads=True)
                     ev_used[i % 2].record(cur)
                     hloss.copy_(pipe.loss, non_blocking=True)
             e2e_run(3)

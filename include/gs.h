@@ -64,6 +64,9 @@ enum {
     GS_FLAG_BINSORT_KEYS = 16u,   /* gs_bin_sort: emit 64-bit (tile|depth) keys and onesweep-sort them
                                      (north_star literal path); default = depth-presort + tile bucketing
                                      (bit-identical lists, fewer HBM bytes) */
+    GS_FLAG_GRAD_ASSIGN = 32u,    /* gs_render_bwd / gs_pose_grad: ASSIGN instead of accumulate: every column
+                                     [0, n) of grad_params is written (zero for off-screen Gaussians) and
+                                     grad_pose = the pose gradient; no zeroing pass needed by the caller */
     GS_FLAG_BINSORT_EMIT_ONLY = 256u  /* testing: with GS_FLAG_BINSORT_KEYS, stop after key emission (the
                                      view's keys/vals then hold the unsorted index-order emission) */
 };
@@ -123,7 +126,8 @@ gs_status gs_render_fwd(gs_ws* ws, const gs_camera* cam /*(host)*/, float* color
 /* gs_render_bwd — analytic backward of the last gs_render_fwd on this workspace (Eq. 11,
  * PAPER.md:155-168; Supplement A, PAPER.md:608-749 incl. Eq. S6): given dL/dcolor [3][H][W] and
  * dL/ddepth [H][W], ACCUMULATES (+=) dL/dparams into grad_params[14][ld] and, if grad_pose is
- * non-NULL, dL/d(rho, phi) into grad_pose[6] (fp64). params/viewmat must be those of the forward.
+ * non-NULL, dL/d(rho, phi) into grad_pose[6] (fp64); with GS_FLAG_GRAD_ASSIGN both are assigned
+ * instead (off-screen columns set to 0). params/viewmat must be those of the forward.
  * Returns GS_ERR_STALE if gs_project ran after the last gs_render_fwd or n changed. */
 gs_status gs_render_bwd(const float* params, int64_t n, int64_t ld, const float* viewmat, gs_ws* ws,
                         const gs_camera* cam /*(host)*/, const float* dL_dcolor, const float* dL_ddepth,

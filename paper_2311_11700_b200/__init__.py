@@ -26,6 +26,7 @@ GS_FLAG_NO_HOST_SYNC = 2
 GS_FLAG_ACCUM_WEIGHT = 4
 GS_FLAG_EXAMINED = 8
 GS_FLAG_BINSORT_KEYS = 16
+GS_FLAG_GRAD_ASSIGN = 32
 GS_FLAG_BINSORT_EMIT_ONLY = 256
 GS_DENSIFY_ADD, GS_DENSIFY_PRUNE, GS_DENSIFY_SELECT, GS_DENSIFY_DEGENERATE = 1, 2, 3, 4
 

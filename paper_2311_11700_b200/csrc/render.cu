@@ -791,14 +791,29 @@ constexpr int kPoseSums = 15;
 // and needs no second launch. (Clearing the screen-space accumulators here as they are consumed,
 // instead of the per-call memset, was measured 2x slower: scattered 4-B zero stores.)
 __device__ void pose_finalize_block(const double* __restrict__ part, int nblocks, const float* __restrict__ viewmat,
-                                    double* __restrict__ grad_pose);
+                                    double* __restrict__ grad_pose, int assign);
 
-template <int SH>
+__device__ __forceinline__ void gacc(float* p, float v, bool assign) {   // GS_FLAG_GRAD_ASSIGN: = instead of +=
+    if (assign) *p = v;
+    else *p += v;
+}
+
+// GS_FLAG_GRAD_ASSIGN: the off-screen columns of grad[rows][ld] get 0 (gaussian_bwd assigns the rest)
+__global__ void __launch_bounds__(256) zero_offscreen_kernel(const uint32_t* __restrict__ tiles, int64_t n, int64_t ld,
+                                                              int rows, float* __restrict__ grad) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        if (tiles[i] > 0u) continue;
+        for (int k = 0; k < rows; ++k) grad[k * ld + i] = 0.f;
+    }
+}
+
+template <int SH, bool ASSIGN>
 __global__ void __launch_bounds__(256, 4) gaussian_bwd_kernel(
     const float* __restrict__ params, int64_t n, int64_t ld, const float* __restrict__ viewmat, gs_camera cam,
     const uint32_t* __restrict__ onlist, const unsigned int* __restrict__ n_on, const float4* __restrict__ rec,
     const float* __restrict__ sgrad, int64_t sld, float* __restrict__ grad, int cov_path,
     double* __restrict__ pose_part, unsigned int* done_ctr, double* __restrict__ grad_pose) {
+    constexpr bool assign = ASSIGN;
     __shared__ float V[12];
     __shared__ bool s_last;
     if (threadIdx.x < 12) V[threadIdx.x] = viewmat[threadIdx.x];
@@ -904,10 +919,10 @@ __global__ void __launch_bounds__(256, 4) gaussian_bwd_kernel(
                 const float v = __fadd_rn(__fadd_rn(__fmul_rn(C0, p[11 + c]), __fmul_rn(C1, lin)), 0.5f);
                 const float gc = v > 0.f ? s[6 + c] : 0.f;   // clamped channel: no gradient
                 if (grad) {
-                    grad[(11 + c) * ld + i] += gc * C0;
-                    grad[(14 + c) * ld + i] += gc * (-C1 * uy);
-                    grad[(17 + c) * ld + i] += gc * (C1 * uz);
-                    grad[(20 + c) * ld + i] += gc * (-C1 * ux);
+                    gacc(grad + ((11 + c) * ld + i), gc * C0, assign);
+                    gacc(grad + ((14 + c) * ld + i), gc * (-C1 * uy), assign);
+                    gacc(grad + ((17 + c) * ld + i), gc * (C1 * uz), assign);
+                    gacc(grad + ((20 + c) * ld + i), gc * (-C1 * ux), assign);
                 }
                 du[0] -= gc * C1 * y3;
                 du[1] -= gc * C1 * y1;
@@ -923,7 +938,7 @@ __global__ void __launch_bounds__(256, 4) gaussian_bwd_kernel(
             // mean: W^T dX (+ the SH view-direction path)
 #pragma unroll
             for (int k = 0; k < 3; ++k)
-                grad[k * ld + i] += W[0][k] * dX[0] + W[1][k] * dX[1] + W[2][k] * dX[2] + gdir[k];
+                gacc(grad + (k * ld + i), W[0][k] * dX[0] + W[1][k] * dX[1] + W[2][k] * dX[2] + gdir[k], assign);
             // Sigma = M M^T
             float dM[3][3];
 #pragma unroll
@@ -931,7 +946,7 @@ __global__ void __launch_bounds__(256, 4) gaussian_bwd_kernel(
 #pragma unroll
                 for (int k = 0; k < 3; ++k) dM[a][k] = 2.f * (dS[a][0] * M[0][k] + dS[a][1] * M[1][k] + dS[a][2] * M[2][k]);
 #pragma unroll
-            for (int k = 0; k < 3; ++k) grad[(3 + k) * ld + i] += dM[0][k] * R[0][k] + dM[1][k] * R[1][k] + dM[2][k] * R[2][k];
+            for (int k = 0; k < 3; ++k) gacc(grad + ((3 + k) * ld + i), dM[0][k] * R[0][k] + dM[1][k] * R[1][k] + dM[2][k] * R[2][k], assign);
             float dR[3][3];
 #pragma unroll
             for (int a = 0; a < 3; ++a)
@@ -947,15 +962,15 @@ __global__ void __launch_bounds__(256, 4) gaussian_bwd_kernel(
             dq[3] = 2.f * (-2.f * qk * dR[0][0] - qr * dR[0][1] + qi * dR[0][2] + qr * dR[1][0] - 2.f * qk * dR[1][1] +
                            qj * dR[1][2] + qi * dR[2][0] + qj * dR[2][1]);
             const float qd = dq[0] * qr + dq[1] * qi + dq[2] * qj + dq[3] * qk;
-            grad[6 * ld + i] += (dq[0] - qr * qd) / nq;
-            grad[7 * ld + i] += (dq[1] - qi * qd) / nq;
-            grad[8 * ld + i] += (dq[2] - qj * qd) / nq;
-            grad[9 * ld + i] += (dq[3] - qk * qd) / nq;
-            grad[10 * ld + i] += s[5];
+            gacc(grad + (6 * ld + i), (dq[0] - qr * qd) / nq, assign);
+            gacc(grad + (7 * ld + i), (dq[1] - qi * qd) / nq, assign);
+            gacc(grad + (8 * ld + i), (dq[2] - qj * qd) / nq, assign);
+            gacc(grad + (9 * ld + i), (dq[3] - qk * qd) / nq, assign);
+            gacc(grad + (10 * ld + i), s[5], assign);
             if (SH == 0) {
-                grad[11 * ld + i] += s[6];
-                grad[12 * ld + i] += s[7];
-                grad[13 * ld + i] += s[8];
+                gacc(grad + (11 * ld + i), s[6], assign);
+                gacc(grad + (12 * ld + i), s[7], assign);
+                gacc(grad + (13 * ld + i), s[8], assign);
             }
         }
         if (pose_part) {
@@ -1002,7 +1017,7 @@ __global__ void __launch_bounds__(256, 4) gaussian_bwd_kernel(
         __syncthreads();
         if (s_last) {
             __threadfence();
-            pose_finalize_block(pose_part, gridDim.x, viewmat, grad_pose);
+            pose_finalize_block(pose_part, gridDim.x, viewmat, grad_pose, ASSIGN ? 1 : 0);
             if (threadIdx.x == 0) *done_ctr = 0u;   // ready for the next call
         }
     }
@@ -1011,7 +1026,7 @@ __global__ void __launch_bounds__(256, 4) gaussian_bwd_kernel(
 // Fixed-order reduction of the per-block pose partials (by the last block of gaussian_bwd_kernel), then
 // twist = (rho, phi + (A12 - A21, A20 - A02, A01 - A10)),  A = W (sum dW_cov)^T
 __device__ void pose_finalize_block(const double* __restrict__ part, int nblocks, const float* __restrict__ viewmat,
-                                    double* __restrict__ grad_pose) {
+                                    double* __restrict__ grad_pose, int assign) {
     __shared__ double acc[16];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;   // warp w sums components w, w + 8
     for (int k = w; k < kPoseSums; k += 8) {
@@ -1029,12 +1044,9 @@ __device__ void pose_finalize_block(const double* __restrict__ part, int nblocks
     const double* dW = acc + 6;
     for (int a = 0; a < 3; ++a)
         for (int b = 0; b < 3; ++b) A[a][b] = W[a][0] * dW[3 * b + 0] + W[a][1] * dW[3 * b + 1] + W[a][2] * dW[3 * b + 2];
-    grad_pose[0] += acc[0];
-    grad_pose[1] += acc[1];
-    grad_pose[2] += acc[2];
-    grad_pose[3] += acc[3] + (A[1][2] - A[2][1]);
-    grad_pose[4] += acc[4] + (A[2][0] - A[0][2]);
-    grad_pose[5] += acc[5] + (A[0][1] - A[1][0]);
+    const double tw[6] = {acc[0], acc[1], acc[2], acc[3] + (A[1][2] - A[2][1]), acc[4] + (A[2][0] - A[0][2]),
+                          acc[5] + (A[0][1] - A[1][0])};
+    for (int k = 0; k < 6; ++k) grad_pose[k] = (assign ? 0.0 : grad_pose[k]) + tw[k];
 }
 
 void launch_gaussian_bwd(WsState* s, const float* params, int64_t n, int64_t ld, const float* viewmat,
@@ -1051,7 +1063,12 @@ void launch_gaussian_bwd(WsState* s, const float* params, int64_t n, int64_t ld,
     // grid sized without a host sync: at most 4 blocks per SM, at most ceil(n / 256)
     const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(sms) * 4));
     KTimer kt(s, KID_BWD_GAUSS, st);
-    auto kern = s->sh_degree == 1 ? gaussian_bwd_kernel<1> : gaussian_bwd_kernel<0>;
+    const int assign = (flags & GS_FLAG_GRAD_ASSIGN) ? 1 : 0;
+    if (assign && grad_params)
+        zero_offscreen_kernel<<<int(std::min<int64_t>((n + 255) / 256, int64_t(sms) * 8)), 256, 0, st>>>(
+            at<uint32_t>(s, s->tiles), n, ld, s->sh_degree == 1 ? 23 : 14, grad_params);
+    auto kern = s->sh_degree == 1 ? (assign ? gaussian_bwd_kernel<1, true> : gaussian_bwd_kernel<1, false>)
+                                  : (assign ? gaussian_bwd_kernel<0, true> : gaussian_bwd_kernel<0, false>);
     kern<<<blocks, 256, 0, st>>>(params, n, ld, viewmat, cam, at<uint32_t>(s, s->onlist),
                                  &at<Misc>(s, s->misc)->n_onscreen, at<float4>(s, s->rec), at<float>(s, s->sgrad),
                                  s->n_cap, grad_params, (flags & GS_FLAG_POSE_COV_PATH) ? 1 : 0, part,

@@ -7,7 +7,7 @@ import dataclasses
 
 import torch
 
-from . import (GS_FLAG_EXAMINED, GS_FLAG_POSE_COV_PATH, Workspace, gs_bin_sort, gs_loss_l1, gs_pose_grad,
+from . import (GS_FLAG_EXAMINED, GS_FLAG_GRAD_ASSIGN, GS_FLAG_POSE_COV_PATH, Workspace, gs_bin_sort, gs_loss_l1, gs_pose_grad,
                gs_project_sh, gs_render_bwd, gs_render_fwd, make_camera)
 
 
@@ -75,11 +75,13 @@ class RenderPipeline:
                      flags, stream)
 
     def iteration(self, params, n, viewmat, cam, tgt_color, tgt_depth, grad_params, grad_pose=None, bin_flags=0,
-                  fwd_flags=0, w_color=0.9, w_depth=0.1, stream=None):
-        """The headline fwd+bwd iteration."""
+                  fwd_flags=0, w_color=0.9, w_depth=0.1, stream=None, assign_grads=False):
+        """The headline fwd+bwd iteration. assign_grads: the gradients overwrite
+        grad_params[:, :n] / grad_pose (GS_FLAG_GRAD_ASSIGN) instead of accumulating into them."""
         self.forward(params, n, viewmat, cam, bin_flags=bin_flags, fwd_flags=fwd_flags, stream=stream)
         dc, dd = self.loss_l1(cam, tgt_color, tgt_depth, w_color, w_depth, stream)
-        self.backward(params, n, viewmat, cam, dc, dd, grad_params, grad_pose, stream=stream)
+        flags = GS_FLAG_POSE_COV_PATH | (GS_FLAG_GRAD_ASSIGN if assign_grads else 0)
+        self.backward(params, n, viewmat, cam, dc, dd, grad_params, grad_pose, flags=flags, stream=stream)
 
     # ------------------------------------------------------------------ introspection (tests, bench)
     def arrays(self, n: int | None = None, n_keys: int | None = None) -> dict:

@@ -532,3 +532,25 @@ def test_accum_grad_and_split_clone_parity():
     o = want[10, n_keep:]
     np.testing.assert_allclose(rw[10], np.log(o / (1 - o)), rtol=1e-5, atol=1e-6)
     assert float(acc.abs().max()) == 0.0 and float(cnt.abs().max()) == 0.0
+
+
+def test_grad_assign_flag():
+    """GS_FLAG_GRAD_ASSIGN: grad_params[:, :n] and grad_pose are overwritten (off-screen columns 0) and
+    equal the accumulate-into-zeros result bit for bit up to fp32 atomics order."""
+    import paper_2311_11700_b200 as g
+    cfg, p, v = scene(0)
+    n = p.shape[1]
+    pipe, P, V, fr = run_forward(p, v, cfg.cam)
+    dc, dd = gi.upstream(cfg.cam.width, cfg.cam.height, gi.UPSTREAM_SEED_CFG0)
+    ref = torch.zeros_like(P)
+    gp_ref = torch.zeros(6, dtype=torch.float64, device="cuda")
+    pipe.backward(P, n, V, cfg.cam, to_dev(dc), to_dev(dd), ref, gp_ref)
+    got = torch.full_like(P, 123.0)
+    gp = torch.full((6,), 7.0, dtype=torch.float64, device="cuda")
+    pipe.backward(P, n, V, cfg.cam, to_dev(dc), to_dev(dd), got, gp,
+                  flags=g.GS_FLAG_POSE_COV_PATH | g.GS_FLAG_GRAD_ASSIGN)
+    torch.cuda.synchronize()
+    off = pipe.arrays(n)["tiles"].cpu().numpy() == 0
+    assert off.any() and float(got[:, torch.as_tensor(off, device="cuda")].abs().max()) == 0.0
+    np.testing.assert_allclose(got.cpu().numpy(), ref.cpu().numpy(), rtol=1e-5, atol=1e-7)
+    np.testing.assert_allclose(gp.cpu().numpy(), gp_ref.cpu().numpy(), rtol=1e-4, atol=1e-9)   # atomics order
