@@ -62,20 +62,17 @@ __device__ uint32_t lookback_prefix(unsigned long long* status, uint32_t part, u
 }
 
 // Ordered compaction of the on-screen Gaussians (tiles > 0), in index order: list[r] = i and the
-// depth-sort pairs (depth key, i); *count = V_s. Shared by both gs_bin_sort paths (the per-Gaussian
-// backward iterates the list) and the input of path B's depth sort.
+// (depth key, i) pairs; *count = V_s. Path A's on-screen list for the per-Gaussian backward (path B
+// compacts inside bincoop.cu).
 __global__ void __launch_bounds__(kScanThreads) compact_onscreen_kernel(
     const uint32_t* __restrict__ tiles, const uint32_t* __restrict__ dkey, int64_t n,
     unsigned long long* status, unsigned int* ticket, uint32_t epoch, uint32_t* __restrict__ list,
     uint32_t* __restrict__ key_out, uint32_t* __restrict__ val_out, unsigned int* count,
-    unsigned long long* count64, uint32_t* __restrict__ hist) {
+    unsigned long long* count64) {
     using BlockScan = cub::BlockScan<uint32_t, kScanThreads>;
     __shared__ typename BlockScan::TempStorage tmp;
     __shared__ uint32_t s_part, s_excl;
-    __shared__ uint32_t s_hist[4][256];   // digit histograms of the emitted depth keys (hist != null)
     if (threadIdx.x == 0) s_part = atomicAdd(ticket, 1u);
-    if (hist)
-        for (int k = threadIdx.x; k < 4 * 256; k += kScanThreads) (&s_hist[0][0])[k] = 0u;
     __syncthreads();
     const uint32_t part = s_part;
     const int64_t base = int64_t(part) * kScanTile + int64_t(threadIdx.x) * kScanItems;
@@ -98,22 +95,10 @@ __global__ void __launch_bounds__(kScanThreads) compact_onscreen_kernel(
     for (int k = 0; k < kScanItems; ++k) {
         if (f[k]) {
             const uint32_t i = uint32_t(base + k);
-            const uint32_t key = dkey[i];
             list[r] = i;
-            key_out[r] = key;
+            key_out[r] = dkey[i];
             val_out[r] = i;
             ++r;
-            if (hist) {
-#pragma unroll
-                for (int p = 0; p < 4; ++p) atomicAdd(&s_hist[p][(key >> (8 * p)) & 255u], 1u);
-            }
-        }
-    }
-    if (hist) {   // block-uniform
-        __syncthreads();
-        for (int k = threadIdx.x; k < 4 * 256; k += kScanThreads) {
-            const uint32_t c = (&s_hist[0][0])[k];
-            if (c) atomicAdd(hist + k, c);
         }
     }
     if (base < n && base + kScanItems >= n) {   // the partition holding element n-1 publishes V_s
@@ -246,12 +231,10 @@ gs_status chained_scan(WsState* s, const uint32_t* in, uint32_t* out, int64_t n,
 
 // On-screen compaction (both paths): list in index order + path B's depth-sort input in
 // dkey_sorted / dval_sorted (first half); V_s in misc->n_onscreen and misc->n_items.
-gs_status run_compact_onscreen(WsState* s, cudaStream_t st, bool depth_hist) {
+gs_status run_compact_onscreen(WsState* s, cudaStream_t st) {
     Misc* misc = at<Misc>(s, s->misc);
     cudaMemsetAsync(&misc->n_onscreen, 0, sizeof(misc->n_onscreen), st);
     cudaMemsetAsync(&misc->n_items, 0, sizeof(misc->n_items), st);
-    uint32_t* hist = depth_hist ? at<uint32_t>(s, s->sort_hist) : nullptr;
-    if (hist) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 4 * 256, st);
     if (s->n == 0) return GS_OK;
     cudaMemsetAsync(&misc->scan_counter, 0, sizeof(misc->scan_counter), st);
     const uint32_t epoch = uint32_t(++s->epoch) & 0x3fffffffu;
@@ -260,7 +243,7 @@ gs_status run_compact_onscreen(WsState* s, cudaStream_t st, bool depth_hist) {
     compact_onscreen_kernel<<<parts, kScanThreads, 0, st>>>(
         at<uint32_t>(s, s->tiles), at<uint32_t>(s, s->depth_key), s->n, at<unsigned long long>(s, s->scan_state),
         &misc->scan_counter, epoch, at<uint32_t>(s, s->onlist), at<uint32_t>(s, s->dkey_sorted),
-        at<uint32_t>(s, s->dval_sorted), &misc->n_onscreen, &misc->n_items, hist);
+        at<uint32_t>(s, s->dval_sorted), &misc->n_onscreen, &misc->n_items);
     return GS_OK;
 }
 
@@ -294,7 +277,7 @@ gs_status run_bin_sort_keys(WsState* s, int64_t* n_keys, uint32_t flags, cudaStr
     gs_status rc = chained_scan(s, at<uint32_t>(s, s->tiles), at<uint32_t>(s, s->offsets), s->n, &misc->n_keys, st,
                                 s->key_cap, &misc->n_keys_eff);
     if (rc != GS_OK) return rc;
-    rc = run_compact_onscreen(s, st, false);   // on-screen list for the per-Gaussian backward
+    rc = run_compact_onscreen(s, st);   // on-screen list for the per-Gaussian backward
     if (rc != GS_OK) return rc;
     int64_t Kgrid = 0;
     rc = resolve_keys(s, n_keys, flags, st, &Kgrid);

@@ -116,7 +116,7 @@ void set_cuda_error(cudaError_t e, const char* what);
 void launch_project(WsState* s, const float* params, int64_t n, int64_t ld, const uint8_t* mask,
                     const float* viewmat, const gs_camera& cam, cudaStream_t st);   // colour: s->sh_degree
 gs_status run_bin_sort_keys(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t st);
-gs_status run_compact_onscreen(WsState* s, cudaStream_t st, bool depth_hist);
+gs_status run_compact_onscreen(WsState* s, cudaStream_t st);   // path A
 gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t st);
 void launch_render_fwd(WsState* s, const gs_camera& cam, float* color, float* depth, float* alpha,
                        float* accum_weight, uint32_t flags, cudaStream_t st);
