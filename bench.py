@@ -225,8 +225,9 @@ def main_ours(args):
     gpose = torch.zeros(6, dtype=torch.float64, device=dev)
     flags = bin_flags | g.GS_FLAG_NO_HOST_SYNC
 
-    def step():   # the gradients are assigned (GS_FLAG_GRAD_ASSIGN): no zeroing pass
-        pipe.iteration(P, n, V, cam, tc, td, grad, gpose, bin_flags=flags, fwd_flags=0, assign_grads=True)
+    def step():   # gradients assigned (GS_FLAG_GRAD_ASSIGN, no zeroing pass); L1 loss fused into the backward
+        pipe.iteration(P, n, V, cam, tc, td, grad, gpose, bin_flags=flags, fwd_flags=0, assign_grads=True,
+                       fused_loss=True)
 
     def barrier():
         if dist:
@@ -330,7 +331,7 @@ def main_ours(args):
                     Pd, Vd, tcd, tdd = bufs[i % 2]
                     cur.wait_event(ev_copied[i % 2])
                     pipe.iteration(Pd, n, Vd, cam, tcd, tdd, grad, gpose, bin_flags=flags, fwd_flags=0,
-                                   assign_grads=True)
+                                   assign_grads=True, fused_loss=True)
                     ev_used[i % 2].record(cur)
                     hloss.copy_(pipe.loss, non_blocking=True)
             e2e_run(3)

@@ -134,6 +134,18 @@ gs_status gs_render_bwd(const float* params, int64_t n, int64_t ld, const float*
                         float* grad_params /*[14][ld], +=*/, double* grad_pose /*nullable [6], +=*/,
                         uint32_t flags, void* stream);
 
+/* gs_render_bwd_l1 — gs_loss_l1 followed by gs_render_bwd in one pass over the pixels: the L1 loss
+ * of Eq. 6 (reading C20: L = w_c/(3HW) sum|C - C*| + w_d/#valid sum_valid|D - D*|)
+ * is formed inside the backward's pixel loads (dL/dC = w_c/(3HW) sign(C - C*), dL/dD = w_d/#valid
+ * sign(D - D*) on valid pixels: the same fp32 values gs_loss_l1 writes), so dL/dC, dL/dD are never
+ * written to memory. color [3][H][W], depth [H][W] are the last gs_render_fwd's outputs; loss
+ * (nullable, device fp64 [1]) receives L. Other arguments, flags and errors as gs_render_bwd. */
+gs_status gs_render_bwd_l1(const float* params, int64_t n, int64_t ld, const float* viewmat, gs_ws* ws,
+                           const gs_camera* cam /*(host)*/, const float* color, const float* depth,
+                           const float* tgt_color, const float* tgt_depth, float w_color, float w_depth,
+                           float* grad_params, double* grad_pose /*nullable*/, double* loss /*nullable*/,
+                           uint32_t flags, void* stream);
+
 /* gs_pose_grad — pose-only backward (Eq. 11; tracking, Alg. 1): same inputs as
  * gs_render_bwd, ACCUMULATES dL/d(rho, phi) into grad_pose[6]; no per-Gaussian outputs. */
 gs_status gs_pose_grad(const float* params, int64_t n, int64_t ld, const float* viewmat, gs_ws* ws,

@@ -73,6 +73,8 @@ _SIGS = {
     "gs_densify_accum_grad": (ctypes.c_int, [ctypes.POINTER(gs_ws), _P, _P, _P]),
     "gs_densify_split_clone": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _F, _F, ctypes.POINTER(gs_ws),
                                               _P]),
+    "gs_render_bwd_l1": (ctypes.c_int, [_P, _I64, _I64, _P, ctypes.POINTER(gs_ws), ctypes.POINTER(gs_camera), _P, _P,
+                                        _P, _P, _F, _F, _P, _P, _P, _U32, _P]),
     "gs_project_sh": (ctypes.c_int, [_P, _I64, _I64, _I32, _P, _P, ctypes.POINTER(gs_camera), ctypes.POINTER(gs_ws),
                                      _P]),
     "gs_bin_sort": (ctypes.c_int, [ctypes.POINTER(gs_ws), ctypes.POINTER(_I64), _U32, _P]),
@@ -240,6 +242,15 @@ def gs_render_bwd(params, n, ld, viewmat, ws: Workspace, cam: gs_camera, dL_dcol
     _check(_lib.gs_render_bwd(_ptr(params), n, ld, _ptr(viewmat), ctypes.byref(ws.state), ctypes.byref(cam),
                               _ptr(dL_dcolor), _ptr(dL_ddepth), _ptr(grad_params), _ptr(grad_pose), flags,
                               _stream(stream)), "gs_render_bwd")
+
+
+def gs_render_bwd_l1(params, n, ld, viewmat, ws: Workspace, cam: gs_camera, color, depth, tgt_color, tgt_depth,
+                     w_color, w_depth, grad_params, grad_pose=None, loss=None, flags: int = GS_FLAG_POSE_COV_PATH,
+                     stream=None):
+    _check(_lib.gs_render_bwd_l1(_ptr(params), n, ld, _ptr(viewmat), ctypes.byref(ws.state), ctypes.byref(cam),
+                                 _ptr(color), _ptr(depth), _ptr(tgt_color), _ptr(tgt_depth), w_color, w_depth,
+                                 _ptr(grad_params), _ptr(grad_pose), _ptr(loss), flags, _stream(stream)),
+           "gs_render_bwd_l1")
 
 
 def gs_pose_grad(params, n, ld, viewmat, ws: Workspace, cam: gs_camera, dL_dcolor, dL_ddepth, grad_pose,

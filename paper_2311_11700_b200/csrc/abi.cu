@@ -182,17 +182,18 @@ gs_status gs_render_fwd(gs_ws* ws, const gs_camera* cam, float* color, float* de
 
 static gs_status backward_common(const float* params, int64_t n, int64_t ld, const float* viewmat, gs_ws* ws,
                                  const gs_camera* cam, const float* dLdC, const float* dLdD, float* grad,
-                                 double* grad_pose, uint32_t flags, void* stream) {
+                                 double* grad_pose, uint32_t flags, void* stream, const L1Fuse* fuse = nullptr) {
     if (!ws_ok(ws)) return GS_ERR_INVALID_ARG;
     WsState* s = state(ws);
-    if (!cam_ok(s, cam) || !dLdC || !dLdD || !viewmat || (n > 0 && !params) || ld < n) return GS_ERR_INVALID_ARG;
+    if (!cam_ok(s, cam) || (!fuse && (!dLdC || !dLdD)) || !viewmat || (n > 0 && !params) || ld < n)
+        return GS_ERR_INVALID_ARG;
     if (s->gen_fwd == 0 || s->gen_fwd != s->gen_project || n != s->n || cam->width != s->cam_w ||
         cam->height != s->cam_h)
         return GS_ERR_STALE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (n > 0)   // screen-space gradient accumulators [10][n_cap]: clear the live n columns only
         cudaMemset2DAsync(s->dev + s->sgrad.off, size_t(s->n_cap) * 4, 0, size_t(n) * 4, 10, st);
-    launch_render_bwd_tiles(s, *cam, nullptr, dLdC, dLdD, st);
+    launch_render_bwd_tiles(s, *cam, nullptr, dLdC, dLdD, st, fuse);
     launch_gaussian_bwd(s, params, n, ld, viewmat, *cam, grad, grad_pose, flags, st);
     s->gen_bwd = s->gen_fwd;
     return check_launch(s, "gs_render_bwd");
@@ -204,6 +205,16 @@ gs_status gs_render_bwd(const float* params, int64_t n, int64_t ld, const float*
     if (!grad_params) return GS_ERR_INVALID_ARG;
     return backward_common(params, n, ld, viewmat, ws, cam, dL_dcolor, dL_ddepth, grad_params, grad_pose, flags,
                            stream);
+}
+
+gs_status gs_render_bwd_l1(const float* params, int64_t n, int64_t ld, const float* viewmat, gs_ws* ws,
+                           const gs_camera* cam, const float* color, const float* depth, const float* tgt_color,
+                           const float* tgt_depth, float w_color, float w_depth, float* grad_params,
+                           double* grad_pose, double* loss, uint32_t flags, void* stream) {
+    if (!grad_params || !color || !depth || !tgt_color || !tgt_depth) return GS_ERR_INVALID_ARG;
+    const L1Fuse fuse{color, depth, tgt_color, tgt_depth, w_color, w_depth, loss};
+    return backward_common(params, n, ld, viewmat, ws, cam, nullptr, nullptr, grad_params, grad_pose, flags, stream,
+                           &fuse);
 }
 
 gs_status gs_pose_grad(const float* params, int64_t n, int64_t ld, const float* viewmat, gs_ws* ws,

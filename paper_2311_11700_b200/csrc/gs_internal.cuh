@@ -120,8 +120,14 @@ gs_status run_compact_onscreen(WsState* s, cudaStream_t st);   // path A
 gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t st);
 void launch_render_fwd(WsState* s, const gs_camera& cam, float* color, float* depth, float* alpha,
                        float* accum_weight, uint32_t flags, cudaStream_t st);
+struct L1Fuse {   // gs_render_bwd_l1: the L1 loss formed inside the backward's pixel loads
+    const float *color, *depth, *tc, *td;
+    float wc, wd;
+    double* loss;    // nullable
+};
 void launch_render_bwd_tiles(WsState* s, const gs_camera& cam, const float* color_unused,
-                             const float* dL_dcolor, const float* dL_ddepth, cudaStream_t st);
+                             const float* dL_dcolor, const float* dL_ddepth, cudaStream_t st,
+                             const L1Fuse* fuse = nullptr);
 void launch_gaussian_bwd(WsState* s, const float* params, int64_t n, int64_t ld, const float* viewmat,
                          const gs_camera& cam, float* grad_params, double* grad_pose, uint32_t flags,
                          cudaStream_t st);

@@ -538,11 +538,24 @@ __device__ __forceinline__ void bwd_step_pair(BwdPair& p, f32x2 power, float4 r1
     p.Qn = fma2(wn, ev, p.Qn);   // wn == 0 when skipped: Q unchanged (ev finite; padding is zero-filled)
 }
 
+// Fused L1 loss (gs_render_bwd_l1): the pixel loads form dL/dC, dL/dD of Eq. 6 (reading C20) from
+// the rendered and target images with exactly gs_loss_l1's arithmetic, and each block adds its
+// |C - C*| and valid |D - D*| sums to acc[0], acc[1] (acc[2] = valid-pixel count, counted before).
+struct FusedL1 {
+    const float *color, *depth, *tc, *td;
+    float wc, wd;
+    double* acc;
+};
+
+__device__ __forceinline__ float sgn1(float x) { return float((x > 0.f) - (x < 0.f)); }
+
+template <bool L1>
 __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
     const float4* __restrict__ rec, const uint32_t* __restrict__ live_g, const uint32_t* __restrict__ live_j,
     const uint32_t* __restrict__ live_cnt, const uint2* __restrict__ ranges, int W, int H,
     int GX, const float* __restrict__ t_final, float bgr, float bgg, float bgb, const uint32_t* __restrict__ n_last,
-    const float* __restrict__ dLdC, const float* __restrict__ dLdD, float* __restrict__ sgrad, int64_t sld) {
+    const float* __restrict__ dLdC, const float* __restrict__ dLdD, float* __restrict__ sgrad, int64_t sld,
+    FusedL1 l1) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BwdSmem& sm = *reinterpret_cast<BwdSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -558,17 +571,47 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
     {
         float t[2] = {1.f, 1.f}, d[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
         uint32_t nl[2] = {0u, 0u};
+        float sum_c = 0.f, sum_d = 0.f;   // L1: this thread's |C - C*| and valid |D - D*|
+        float sc = 0.f, sd = 0.f;
+        if (L1) {
+            const double nvalid = __ldcg(l1.acc + 2);
+            sc = float(double(l1.wc) / (3.0 * double(plane)));
+            sd = nvalid > 0 ? float(double(l1.wd) / nvalid) : 0.f;
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int py = h ? pyB : pyA;
             if (px < W && py < H) {
                 const size_t pix = size_t(py) * W + px;
                 nl[h] = n_last[pix];
-                d[h][0] = dLdC[pix];
-                d[h][1] = dLdC[plane + pix];
-                d[h][2] = dLdC[2 * plane + pix];
-                d[h][3] = dLdD[pix];
+                if (L1) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float e = l1.color[c * plane + pix] - l1.tc[c * plane + pix];
+                        sum_c += fabsf(e);
+                        d[h][c] = sc * sgn1(e);
+                    }
+                    const float tdv = l1.td[pix], e = l1.depth[pix] - tdv;
+                    if (tdv > 0.f) sum_d += fabsf(e);
+                    d[h][3] = tdv > 0.f ? sd * sgn1(e) : 0.f;
+                } else {
+                    d[h][0] = dLdC[pix];
+                    d[h][1] = dLdC[plane + pix];
+                    d[h][2] = dLdC[2 * plane + pix];
+                    d[h][3] = dLdD[pix];
+                }
                 t[h] = t_final[pix];
+            }
+        }
+        if (L1) {   // block sums -> one fp64 atomic per quantity
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                sum_c += __shfl_xor_sync(0xffffffffu, sum_c, o);
+                sum_d += __shfl_xor_sync(0xffffffffu, sum_d, o);
+            }
+            if (lane == 0) {
+                atomicAdd(l1.acc + 0, double(sum_c));
+                atomicAdd(l1.acc + 1, double(sum_d));
             }
         }
         P.T = pk2(t[0], t[1]);
@@ -761,23 +804,73 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
     }
 }
 
+// valid-pixel count of the target depth (the L1 depth term's mean, reading C20) into acc[2]
+__global__ void __launch_bounds__(256) valid_count_kernel(const float4* __restrict__ td4, const float* __restrict__ td,
+                                                          int64_t npx, double* acc) {
+    __shared__ uint32_t s_c[8];
+    uint32_t c = 0;
+    const int64_t n4 = td4 ? npx / 4 : 0;
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n4; q += int64_t(gridDim.x) * blockDim.x) {
+        const float4 v = td4[q];
+        c += (v.x > 0.f) + (v.y > 0.f) + (v.z > 0.f) + (v.w > 0.f);
+    }
+    for (int64_t p = 4 * n4 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < npx;
+         p += int64_t(gridDim.x) * blockDim.x)
+        c += td[p] > 0.f ? 1u : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) s_c[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < 8; ++w) t += s_c[w];
+        if (t) atomicAdd(acc + 2, double(t));
+    }
+}
+
+__global__ void loss_finalize_kernel(const double* acc, int64_t npx, float wc, float wd, double* loss) {
+    const double nvalid = acc[2];
+    const float sc = float(double(wc) / (3.0 * double(npx)));
+    const float sd = nvalid > 0 ? float(double(wd) / nvalid) : 0.f;
+    *loss = double(sc) * acc[0] + (nvalid > 0 ? double(sd) * acc[1] : 0.0);
+}
+
 void launch_render_bwd_tiles(WsState* s, const gs_camera& cam, const float*, const float* dL_dcolor,
-                             const float* dL_ddepth, cudaStream_t st) {
+                             const float* dL_ddepth, cudaStream_t st, const L1Fuse* fuse) {
     const int ntiles = s->cam_gx * s->cam_gy;
     if (ntiles == 0) return;
     const LiveBufs lb = live_bufs(s);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(render_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem)));
-        cudaFuncSetAttribute(render_bwd_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             int(cudaSharedmemCarveoutMaxShared));
+        for (auto k : {render_bwd_kernel<false>, render_bwd_kernel<true>}) {
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem)));
+            cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, int(cudaSharedmemCarveoutMaxShared));
+        }
         attr = true;
     }
-    KTimer kt(s, KID_BWD_TILE, st);
-    render_bwd_kernel<<<ntiles, kBwdThreads, sizeof(BwdSmem), st>>>(
-        at<float4>(s, s->rec), lb.g, lb.j, lb.cnt, at<uint2>(s, s->ranges), cam.width, cam.height, s->cam_gx,
-        at<float>(s, s->t_final), cam.bg[0], cam.bg[1], cam.bg[2], at<uint32_t>(s, s->n_last), dL_dcolor, dL_ddepth,
-        at<float>(s, s->sgrad), s->n_cap);
+    FusedL1 l1{};
+    double* acc = at<Misc>(s, s->misc)->loss_acc;
+    const int64_t npx = int64_t(cam.width) * cam.height;
+    if (fuse) {
+        l1 = FusedL1{fuse->color, fuse->depth, fuse->tc, fuse->td, fuse->wc, fuse->wd, acc};
+        cudaMemsetAsync(acc, 0, 3 * sizeof(double), st);
+        KTimer kt(s, KID_LOSS, st);
+        const bool v4 = (reinterpret_cast<uintptr_t>(fuse->td) & 15) == 0;
+        valid_count_kernel<<<148, 256, 0, st>>>(v4 ? reinterpret_cast<const float4*>(fuse->td) : nullptr, fuse->td, npx,
+                                                acc);
+    }
+    {
+        KTimer kt(s, KID_BWD_TILE, st);
+        auto k = fuse ? render_bwd_kernel<true> : render_bwd_kernel<false>;
+        k<<<ntiles, kBwdThreads, sizeof(BwdSmem), st>>>(
+            at<float4>(s, s->rec), lb.g, lb.j, lb.cnt, at<uint2>(s, s->ranges), cam.width, cam.height, s->cam_gx,
+            at<float>(s, s->t_final), cam.bg[0], cam.bg[1], cam.bg[2], at<uint32_t>(s, s->n_last), dL_dcolor,
+            dL_ddepth, at<float>(s, s->sgrad), s->n_cap, l1);
+    }
+    if (fuse && fuse->loss) {
+        KTimer kt(s, KID_LOSS, st);
+        loss_finalize_kernel<<<1, 1, 0, st>>>(acc, npx, fuse->wc, fuse->wd, fuse->loss);
+    }
 }
 
 // ------------------------------------------------------------------ backward, per-Gaussian chain

@@ -8,7 +8,7 @@ import dataclasses
 import torch
 
 from . import (GS_FLAG_EXAMINED, GS_FLAG_GRAD_ASSIGN, GS_FLAG_POSE_COV_PATH, Workspace, gs_bin_sort, gs_loss_l1, gs_pose_grad,
-               gs_project_sh, gs_render_bwd, gs_render_fwd, make_camera)
+               gs_project_sh, gs_render_bwd, gs_render_bwd_l1, gs_render_fwd, make_camera)
 
 
 @dataclasses.dataclass
@@ -75,12 +75,19 @@ class RenderPipeline:
                      flags, stream)
 
     def iteration(self, params, n, viewmat, cam, tgt_color, tgt_depth, grad_params, grad_pose=None, bin_flags=0,
-                  fwd_flags=0, w_color=0.9, w_depth=0.1, stream=None, assign_grads=False):
+                  fwd_flags=0, w_color=0.9, w_depth=0.1, stream=None, assign_grads=False, fused_loss=False):
         """The headline fwd+bwd iteration. assign_grads: the gradients overwrite
-        grad_params[:, :n] / grad_pose (GS_FLAG_GRAD_ASSIGN) instead of accumulating into them."""
+        grad_params[:, :n] / grad_pose (GS_FLAG_GRAD_ASSIGN) instead of accumulating into them.
+        fused_loss: gs_render_bwd_l1 (the L1 loss formed in the backward's pixel loads; dL/dC and
+        dL/dD are not materialised) instead of gs_loss_l1 + gs_render_bwd. self.loss receives L."""
         self.forward(params, n, viewmat, cam, bin_flags=bin_flags, fwd_flags=fwd_flags, stream=stream)
-        dc, dd = self.loss_l1(cam, tgt_color, tgt_depth, w_color, w_depth, stream)
         flags = GS_FLAG_POSE_COV_PATH | (GS_FLAG_GRAD_ASSIGN if assign_grads else 0)
+        if fused_loss:
+            color, depth, _ = self._imgs(cam)
+            gs_render_bwd_l1(params, n, params.shape[1], viewmat, self.ws, make_camera(cam), color, depth, tgt_color,
+                             tgt_depth, w_color, w_depth, grad_params, grad_pose, self.loss, flags, stream)
+            return
+        dc, dd = self.loss_l1(cam, tgt_color, tgt_depth, w_color, w_depth, stream)
         self.backward(params, n, viewmat, cam, dc, dd, grad_params, grad_pose, flags=flags, stream=stream)
 
     # ------------------------------------------------------------------ introspection (tests, bench)

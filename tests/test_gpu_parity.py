@@ -554,3 +554,28 @@ def test_grad_assign_flag():
     assert off.any() and float(got[:, torch.as_tensor(off, device="cuda")].abs().max()) == 0.0
     np.testing.assert_allclose(got.cpu().numpy(), ref.cpu().numpy(), rtol=1e-5, atol=1e-7)
     np.testing.assert_allclose(gp.cpu().numpy(), gp_ref.cpu().numpy(), rtol=1e-4, atol=1e-9)   # atomics order
+
+
+@pytest.mark.parametrize("c", [0, 1])
+def test_fused_l1_backward_equals_loss_then_backward(c):
+    """gs_render_bwd_l1 == gs_loss_l1 + gs_render_bwd: same loss (fp64 sums in another order) and the
+    same gradients up to fp32 atomics order (the upstream values are bit-identical)."""
+    import paper_2311_11700_b200 as g
+    cfg, p, v = scene(c)
+    n = p.shape[1]
+    pipe, P, V, fr = run_forward(p, v, cfg.cam)
+    tc, td = gi.random_images(cfg.cam.width, cfg.cam.height, 88)
+    tc, td = to_dev(tc), to_dev(td)
+    ref, gp_ref = torch.zeros_like(P), torch.zeros(6, dtype=torch.float64, device="cuda")
+    dc, dd = pipe.loss_l1(cfg.cam, tc, td, 0.9, 0.1)
+    loss_ref = pipe.loss.clone()
+    pipe.backward(P, n, V, cfg.cam, dc, dd, ref, gp_ref)
+    got, gp = torch.zeros_like(P), torch.zeros(6, dtype=torch.float64, device="cuda")
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    g.gs_render_bwd_l1(P, n, n, V, pipe.ws, g.make_camera(cfg.cam), pipe.color, pipe.depth, tc, td, 0.9, 0.1,
+                       got, gp, loss)
+    torch.cuda.synchronize()
+    assert abs(loss.item() - loss_ref.item()) <= 1e-6 * abs(loss_ref.item())
+    bad = grad_close(got.cpu().numpy(), ref.cpu().numpy())   # fp32 atomics order only
+    assert bad.mean() <= 1e-4, bad.mean()
+    np.testing.assert_allclose(gp.cpu().numpy(), gp_ref.cpu().numpy(), rtol=1e-3, atol=1e-9)
