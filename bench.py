@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--sh", type=int, default=0, choices=[0, 1],
                     help="colour model: 0 = RGB (BASELINE configs), 1 = degree-1 SH (NEXT-1, gs_project_sh)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the iteration's calls on the stream instead of "
+                                                             "replaying their CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="timed loop only (for ncu launch lists)")
     return ap.parse_args()
@@ -251,12 +253,34 @@ def main_ours(args):
             ms = float(t.item())
         return ms
 
+    def capture(fn):
+        """The iteration's library calls recorded once as a CUDA graph (NO_HOST_SYNC mode: no host
+        read-back, no allocation), replayed per step: same kernels, less launch overhead."""
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            fn()   # (first call on the capture stream)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph):
+            fn()
+        torch.cuda.synchronize()
+        return graph
+
     for _ in range(max(args.warmup, 3)):
         step()
     l0 = pipe.ws.launches()
+    step()   # launches of one step (the graph replays exactly these)
+    launches = pipe.ws.launches() - l0
+    run = step
+    if not args.no_graph:
+        graph = capture(step)
+        run = graph.replay
+        for _ in range(2):
+            run()
     with ClockSampler(local) as clk:
-        ms = timed(step, args.steps)
-    launches = (pipe.ws.launches() - l0) // args.steps
+        ms = timed(run, args.steps)
     err = int(pipe.arrays()["error_flag"].item())
     assert err == 0, "device-side key capacity overflow during the timed region"
     clocks = clk.summary()
@@ -269,7 +293,7 @@ def main_ours(args):
                       "sh_degree": args.sh, "n_gaussians": n, "width": cam.width,
                       "height": cam.height, "keys": K, "visible": V_front, "on_screen": V_s, "E_f": E_f, "E_b": E_b,
                       "E_f_live": Lf, "E_b_live": Lb,
-                      "binsort": args.binsort, "l2": "per-iteration working set > L2 (126 MB): tile lists "
+                      "binsort": args.binsort, "cuda_graph": not args.no_graph, "l2": "per-iteration working set > L2 (126 MB): tile lists "
                       f"{K * 4 / 1e9:.2f} GB + live lists; no flush", "parallelism": f"replicas x{world}"},
            "evals_per_s": world * (E_f + E_b) * 1000.0 / ms, "clocks": clocks, "gpu_launches": int(launches),
            # the paper's own numbers: another GPU, real scenes of unstated size; context only
@@ -321,6 +345,16 @@ def main_ours(args):
                         dst.copy_(src, non_blocking=True)
                     ev_copied[i % 2].record(s_copy)
 
+            def iteration_on(b):
+                Pd, Vd, tcd, tdd = b
+                return lambda: pipe.iteration(Pd, n, Vd, cam, tcd, tdd, grad, gpose, bin_flags=flags, fwd_flags=0,
+                                              assign_grads=True, fused_loss=True)
+
+            # one captured graph per upload buffer set (as in the device-timed run)
+            its = [iteration_on(b) for b in bufs]
+            if not args.no_graph:
+                its = [capture(f).replay for f in its]
+
             def e2e_run(steps):
                 cur = torch.cuda.current_stream()
                 s_copy.wait_stream(cur)   # the first upload starts inside the timed region
@@ -328,10 +362,8 @@ def main_ours(args):
                 for i in range(steps):
                     if i + 1 < steps:
                         upload(i + 1)
-                    Pd, Vd, tcd, tdd = bufs[i % 2]
                     cur.wait_event(ev_copied[i % 2])
-                    pipe.iteration(Pd, n, Vd, cam, tcd, tdd, grad, gpose, bin_flags=flags, fwd_flags=0,
-                                   assign_grads=True, fused_loss=True)
+                    its[i % 2]()
                     ev_used[i % 2].record(cur)
                     hloss.copy_(pipe.loss, non_blocking=True)
             e2e_run(3)
