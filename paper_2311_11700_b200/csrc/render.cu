@@ -1157,10 +1157,11 @@ void launch_gaussian_bwd(WsState* s, const float* params, int64_t n, int64_t ld,
     const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(sms) * 4));
     KTimer kt(s, KID_BWD_GAUSS, st);
     const int assign = (flags & GS_FLAG_GRAD_ASSIGN) ? 1 : 0;
-    if (assign && grad_params)
-        s->launches += 1,   // (timed with gaussian_bwd)
+    if (assign && grad_params) {   // (timed with gaussian_bwd)
+        s->launches += 1;
         zero_offscreen_kernel<<<int(std::min<int64_t>((n + 255) / 256, int64_t(sms) * 8)), 256, 0, st>>>(
             at<uint32_t>(s, s->tiles), n, ld, s->sh_degree == 1 ? 23 : 14, grad_params);
+    }
     auto kern = s->sh_degree == 1 ? (assign ? gaussian_bwd_kernel<1, true> : gaussian_bwd_kernel<1, false>)
                                   : (assign ? gaussian_bwd_kernel<0, true> : gaussian_bwd_kernel<0, false>);
     kern<<<blocks, 256, 0, st>>>(params, n, ld, viewmat, cam, at<uint32_t>(s, s->onlist),
