@@ -191,8 +191,7 @@ static gs_status backward_common(const float* params, int64_t n, int64_t ld, con
         cam->height != s->cam_h)
         return GS_ERR_STALE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (n > 0)   // screen-space gradient accumulators [10][n_cap]: clear the live n columns only
-        cudaMemset2DAsync(s->dev + s->sgrad.off, size_t(s->n_cap) * 4, 0, size_t(n) * 4, 10, st);
+    if (n > 0) launch_zero_sgrad(s, st);   // screen accumulators [10][V_s], indexed by on-screen rank
     launch_render_bwd_tiles(s, *cam, nullptr, dLdC, dLdD, st, fuse);
     launch_gaussian_bwd(s, params, n, ld, viewmat, *cam, grad, grad_pose, flags, st);
     s->gen_bwd = s->gen_fwd;

@@ -50,6 +50,7 @@ struct CoopArgs {
     int GX, GY;
     int64_t key_cap;
     uint32_t* onlist;        // [n] on-screen Gaussians, index order
+    float* rec_f;            // projected records, 12 floats each (r2.w <- on-screen rank)
     uint32_t* k0; uint32_t* v0; uint32_t* k1; uint32_t* v1;   // [n] ping-pong sort buffers
     uint32_t* svals;         // [n] depth-sorted on-screen Gaussians
     short4* srect;           // [n] their rects
@@ -221,6 +222,7 @@ __global__ void __launch_bounds__(kCT, 1) bin_coop_kernel(CoopArgs a) {
                     const uint32_t i = uint32_t(r0 + int64_t(r) * kCT + tid);
                     const uint32_t key = dk[r] - key_lo;
                     a.onlist[o] = i;
+                    a.rec_f[kRecFloats * size_t(i) + 11] = __uint_as_float(o);   // on-screen rank -> record r2.w
                     a.k0[o] = key;
                     a.v0[o] = i;
                     for (int p = 0; p < P; ++p) atomicAdd(&s_hist[p][(key >> (p * dbits)) & dmask], 1u);
@@ -496,6 +498,7 @@ gs_status run_bin_coop(WsState* s, cudaStream_t st) {
     a.GY = GY;
     a.key_cap = s->key_cap;
     a.onlist = at<uint32_t>(s, s->onlist);
+    a.rec_f = at<float>(s, s->rec);
     a.k0 = at<uint32_t>(s, s->dkey_sorted);
     a.k1 = a.k0 + s->n_cap;
     a.v0 = at<uint32_t>(s, s->dval_sorted);

@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(kScanThreads) compact_onscreen_kernel(
     const uint32_t* __restrict__ tiles, const uint32_t* __restrict__ dkey, int64_t n,
     unsigned long long* status, unsigned int* ticket, uint32_t epoch, uint32_t* __restrict__ list,
     uint32_t* __restrict__ key_out, uint32_t* __restrict__ val_out, unsigned int* count,
-    unsigned long long* count64) {
+    unsigned long long* count64, float* __restrict__ rec_f) {
     using BlockScan = cub::BlockScan<uint32_t, kScanThreads>;
     __shared__ typename BlockScan::TempStorage tmp;
     __shared__ uint32_t s_part, s_excl;
@@ -96,6 +96,7 @@ __global__ void __launch_bounds__(kScanThreads) compact_onscreen_kernel(
         if (f[k]) {
             const uint32_t i = uint32_t(base + k);
             list[r] = i;
+            rec_f[kRecFloats * size_t(i) + 11] = __uint_as_float(r);   // on-screen rank -> record r2.w
             key_out[r] = dkey[i];
             val_out[r] = i;
             ++r;
@@ -243,7 +244,7 @@ gs_status run_compact_onscreen(WsState* s, cudaStream_t st) {
     compact_onscreen_kernel<<<parts, kScanThreads, 0, st>>>(
         at<uint32_t>(s, s->tiles), at<uint32_t>(s, s->depth_key), s->n, at<unsigned long long>(s, s->scan_state),
         &misc->scan_counter, epoch, at<uint32_t>(s, s->onlist), at<uint32_t>(s, s->dkey_sorted),
-        at<uint32_t>(s, s->dval_sorted), &misc->n_onscreen, &misc->n_items);
+        at<uint32_t>(s, s->dval_sorted), &misc->n_onscreen, &misc->n_items, at<float>(s, s->rec));
     return GS_OK;
 }
 

@@ -120,6 +120,7 @@ gs_status run_compact_onscreen(WsState* s, cudaStream_t st);   // path A
 gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t st);
 void launch_render_fwd(WsState* s, const gs_camera& cam, float* color, float* depth, float* alpha,
                        float* accum_weight, uint32_t flags, cudaStream_t st);
+void launch_zero_sgrad(WsState* s, cudaStream_t st);
 struct L1Fuse {   // gs_render_bwd_l1: the L1 loss formed inside the backward's pixel loads
     const float *color, *depth, *tc, *td;
     float wc, wd;
@@ -193,7 +194,9 @@ __device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
     return r;
 }
 
-// Projected record (48 B): r0 = {mx, my, A, B}, r1 = {C, o, depth, q_max}, r2 = {r, g, b, -} with the
+// Projected record (48 B): r0 = {mx, my, A, B}, r1 = {C, o, depth, q_max}, r2 = {r, g, b, rank} (rank:
+// the on-screen rank as uint bits, written by gs_bin_sort's compaction; indexes the backward's screen
+// accumulators) with the
 // exactly scaled conic A = -a/2, B = -b, C = -c/2 (conic = Sigma'^-1 = [[a, b], [b, c]]).
 // alpha at pixel (px, py). Shared by the forward and both backward kernels so every decision is
 // bit-identical between them, and written with explicit round-to-nearest intrinsics in the

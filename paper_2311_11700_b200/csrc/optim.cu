@@ -416,7 +416,7 @@ __global__ void accum_grad_kernel(const uint32_t* __restrict__ onlist, const uns
     const int64_t V = int64_t(*n_on);
     for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < V; t += int64_t(gridDim.x) * blockDim.x) {
         const int64_t i = onlist[t];
-        const float gx = sgrad[i] * hw, gy = sgrad[sld + i] * hh;   // dL/dm in NDC units
+        const float gx = sgrad[t] * hw, gy = sgrad[sld + t] * hh;   // dL/dm in NDC units (rank-indexed)
         accum[i] += sqrtf(gx * gx + gy * gy);
         count[i] += 1.f;
     }

@@ -499,7 +499,6 @@ struct BwdSmem {
                                       // second also when clamped (rows padded: conflict-free)
     f32x2 dl[kBwdThreads][4];         // dL/dC (r, g, b), dL/dD
     float part[kBwdWarps][10][kBB];   // per-warp pixel moments (its two row groups combined)
-    uint32_t idx[kSlots][kBB];
     uint32_t pos[kSlots][kBB];        // 1-based list positions of the staged live entries (~0u: padding)
     uint32_t max_nl, len;
 };
@@ -665,7 +664,6 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
             float4* dst = sm.rec[slot][tid];
             if (j < len) {
                 const uint32_t g = live_g[start + j];
-                sm.idx[slot][tid] = g;
                 sm.pos[slot][tid] = live_j[start + j];
                 const float4* src = rec + 3 * size_t(g);
                 cp_async16(dst + 0, src + 0);
@@ -673,7 +671,6 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
                 cp_async16(dst + 2, src + 2);
             } else {   // padding: never live, zero record keeps every product finite
                 const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-                sm.idx[slot][tid] = 0u;
                 sm.pos[slot][tid] = 0xffffffffu;
                 dst[0] = z;
                 dst[1] = z;
@@ -724,7 +721,8 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
                     v = -0.5f * o * (Y * Y * M0 - 2.f * Y * My + moment(5, k));            // conic c
                 }
             }
-            if (v != 0.f) atomicAdd(sgrad + c * sld + sm.idx[gbuf][k], v);
+            // screen accumulators are indexed by on-screen rank (record r2.w, written by gs_bin_sort)
+            if (v != 0.f) atomicAdd(sgrad + c * sld + __float_as_uint(sm.rec[gbuf][k][2].w), v);
         }
     };
     for (int it = 0; it < nbatch; ++it) {
@@ -802,6 +800,20 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
         __syncthreads();   // the last batch's partial sets are complete
         gradients((nbatch - 1) % kSlots, 0);
     }
+}
+
+// the screen accumulators [10][V_s] (rank-indexed) cleared at the start of every backward
+__global__ void __launch_bounds__(256) zero_sgrad_kernel(float* __restrict__ sgrad, int64_t sld,
+                                                         const unsigned int* __restrict__ n_on) {
+    const int64_t V = int64_t(*n_on);
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < V; t += int64_t(gridDim.x) * blockDim.x)
+#pragma unroll
+        for (int c = 0; c < 10; ++c) sgrad[c * sld + t] = 0.f;
+}
+
+void launch_zero_sgrad(WsState* s, cudaStream_t st) {
+    KTimer kt(s, KID_BWD_TILE, st);
+    zero_sgrad_kernel<<<148 * 4, 256, 0, st>>>(at<float>(s, s->sgrad), s->n_cap, &at<Misc>(s, s->misc)->n_onscreen);
 }
 
 // valid-pixel count of the target depth (the L1 depth term's mean, reading C20) into acc[2]
@@ -921,7 +933,7 @@ __global__ void __launch_bounds__(256, 4) gaussian_bwd_kernel(
         if (i >= n) continue;
         float s[10];
 #pragma unroll
-        for (int c = 0; c < 10; ++c) s[c] = sgrad[c * sld + i];
+        for (int c = 0; c < 10; ++c) s[c] = sgrad[c * sld + t];   // rank-indexed (coalesced)
         float p[14];
 #pragma unroll
         for (int k = 0; k < 14; ++k) p[k] = params[k * ld + i];
