@@ -192,8 +192,13 @@ static gs_status backward_common(const float* params, int64_t n, int64_t ld, con
         return GS_ERR_STALE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (n > 0) launch_zero_sgrad(s, st);   // screen accumulators [10][V_s], indexed by on-screen rank
-    launch_render_bwd_tiles(s, *cam, nullptr, dLdC, dLdD, st, fuse);
-    launch_gaussian_bwd(s, params, n, ld, viewmat, *cam, grad, grad_pose, flags, st);
+    // fused L1 with a pose gradient: gaussian_bwd's last block (which exists then) writes the loss
+    const bool fin_in_gbwd = fuse && fuse->loss && grad_pose && n > 0;
+    launch_render_bwd_tiles(s, *cam, nullptr, dLdC, dLdD, st, fuse, !fin_in_gbwd);
+    LossFin lf{nullptr, nullptr, 0.f, 0.f, 0};
+    if (fin_in_gbwd)
+        lf = LossFin{at<Misc>(s, s->misc)->loss_acc, fuse->loss, fuse->wc, fuse->wd, int64_t(cam->width) * cam->height};
+    launch_gaussian_bwd(s, params, n, ld, viewmat, *cam, grad, grad_pose, flags, st, lf);
     s->gen_bwd = s->gen_fwd;
     return check_launch(s, "gs_render_bwd");
 }
@@ -401,7 +406,8 @@ const char* gs_kernel_name(int32_t id) {
     static const char* names[KID_COUNT] = {"project", "chained_scan", "emit_keys", "sort_hist", "sort_digit_scan",
                                            "sort_pass", "tile_ranges", "render_fwd", "render_bwd_tiles",
                                            "gaussian_bwd", "pose_finalize", "loss_l1", "densify", "depth_sort",
-                                           "chunk_hist", "chunk_scan", "bucket_emit", "bin_coop"};
+                                           "chunk_hist", "chunk_scan", "bucket_emit", "bin_coop", "sgrad_clear",
+                                           "loss_count", "loss_finalize"};
     return (id >= 0 && id < KID_COUNT) ? names[id] : "unknown";
 }
 

@@ -83,7 +83,8 @@ struct Misc {
 enum KernelId {
     KID_PROJECT = 0, KID_SCAN, KID_EMIT, KID_SORT_HIST, KID_SORT_DSCAN, KID_SORT_PASS, KID_RANGES,
     KID_FWD, KID_BWD_TILE, KID_BWD_GAUSS, KID_POSE_FIN, KID_LOSS, KID_DENSIFY,
-    KID_DEPTH_SORT, KID_CHUNK_HIST, KID_CHUNK_SCAN, KID_BUCKET_EMIT, KID_BIN_COOP, KID_COUNT
+    KID_DEPTH_SORT, KID_CHUNK_HIST, KID_CHUNK_SCAN, KID_BUCKET_EMIT, KID_BIN_COOP, KID_SGRAD_CLEAR,
+    KID_LOSS_COUNT, KID_LOSS_FINALIZE, KID_COUNT
 };
 
 // RAII bracket around one kernel launch: counts it and, when an event log is attached, records
@@ -128,10 +129,16 @@ struct L1Fuse {   // gs_render_bwd_l1: the L1 loss formed inside the backward's 
 };
 void launch_render_bwd_tiles(WsState* s, const gs_camera& cam, const float* color_unused,
                              const float* dL_dcolor, const float* dL_ddepth, cudaStream_t st,
-                             const L1Fuse* fuse = nullptr);
+                             const L1Fuse* fuse = nullptr, bool finalize_loss = true);
+struct LossFin {   // the fused L1 loss scalar, written by gaussian_bwd's last block (loss == nullptr: none)
+    const double* acc;
+    double* loss;
+    float wc, wd;
+    int64_t npx;
+};
 void launch_gaussian_bwd(WsState* s, const float* params, int64_t n, int64_t ld, const float* viewmat,
                          const gs_camera& cam, float* grad_params, double* grad_pose, uint32_t flags,
-                         cudaStream_t st);
+                         cudaStream_t st, LossFin lf = LossFin{nullptr, nullptr, 0.f, 0.f, 0});
 void launch_loss_l1(WsState* s, const float* color, const float* depth, const float* tc, const float* td,
                     int32_t W, int32_t H, float wc, float wd, float* dc, float* dd, double* loss, cudaStream_t st);
 void launch_adam(float* raw, float* act, const float* g, float* m, float* v, int64_t n, int64_t ld,

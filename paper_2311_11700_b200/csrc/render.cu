@@ -812,7 +812,7 @@ __global__ void __launch_bounds__(256) zero_sgrad_kernel(float* __restrict__ sgr
 }
 
 void launch_zero_sgrad(WsState* s, cudaStream_t st) {
-    KTimer kt(s, KID_BWD_TILE, st);
+    KTimer kt(s, KID_SGRAD_CLEAR, st);
     zero_sgrad_kernel<<<148 * 4, 256, 0, st>>>(at<float>(s, s->sgrad), s->n_cap, &at<Misc>(s, s->misc)->n_onscreen);
 }
 
@@ -848,7 +848,7 @@ __global__ void loss_finalize_kernel(const double* acc, int64_t npx, float wc, f
 }
 
 void launch_render_bwd_tiles(WsState* s, const gs_camera& cam, const float*, const float* dL_dcolor,
-                             const float* dL_ddepth, cudaStream_t st, const L1Fuse* fuse) {
+                             const float* dL_ddepth, cudaStream_t st, const L1Fuse* fuse, bool finalize_loss) {
     const int ntiles = s->cam_gx * s->cam_gy;
     if (ntiles == 0) return;
     const LiveBufs lb = live_bufs(s);
@@ -866,7 +866,7 @@ void launch_render_bwd_tiles(WsState* s, const gs_camera& cam, const float*, con
     if (fuse) {
         l1 = FusedL1{fuse->color, fuse->depth, fuse->tc, fuse->td, fuse->wc, fuse->wd, acc};
         cudaMemsetAsync(acc, 0, 3 * sizeof(double), st);
-        KTimer kt(s, KID_LOSS, st);
+        KTimer kt(s, KID_LOSS_COUNT, st);
         const bool v4 = (reinterpret_cast<uintptr_t>(fuse->td) & 15) == 0;
         valid_count_kernel<<<148, 256, 0, st>>>(v4 ? reinterpret_cast<const float4*>(fuse->td) : nullptr, fuse->td, npx,
                                                 acc);
@@ -879,8 +879,8 @@ void launch_render_bwd_tiles(WsState* s, const gs_camera& cam, const float*, con
             at<float>(s, s->t_final), cam.bg[0], cam.bg[1], cam.bg[2], at<uint32_t>(s, s->n_last), dL_dcolor,
             dL_ddepth, at<float>(s, s->sgrad), s->n_cap, l1);
     }
-    if (fuse && fuse->loss) {
-        KTimer kt(s, KID_LOSS, st);
+    if (fuse && fuse->loss && finalize_loss) {
+        KTimer kt(s, KID_LOSS_FINALIZE, st);
         loss_finalize_kernel<<<1, 1, 0, st>>>(acc, npx, fuse->wc, fuse->wd, fuse->loss);
     }
 }
@@ -917,7 +917,7 @@ __global__ void __launch_bounds__(256, 4) gaussian_bwd_kernel(
     const float* __restrict__ params, int64_t n, int64_t ld, const float* __restrict__ viewmat, gs_camera cam,
     const uint32_t* __restrict__ onlist, const unsigned int* __restrict__ n_on, const float4* __restrict__ rec,
     const float* __restrict__ sgrad, int64_t sld, float* __restrict__ grad, int cov_path,
-    double* __restrict__ pose_part, unsigned int* done_ctr, double* __restrict__ grad_pose) {
+    double* __restrict__ pose_part, unsigned int* done_ctr, double* __restrict__ grad_pose, LossFin lf) {
     constexpr bool assign = ASSIGN;
     __shared__ float V[12];
     __shared__ bool s_last;
@@ -1123,6 +1123,12 @@ __global__ void __launch_bounds__(256, 4) gaussian_bwd_kernel(
         if (s_last) {
             __threadfence();
             pose_finalize_block(pose_part, gridDim.x, viewmat, grad_pose, ASSIGN ? 1 : 0);
+            if (lf.loss && threadIdx.x == 0) {   // fused L1: the loss scalar (as loss_finalize_kernel)
+                const double nvalid = __ldcg(lf.acc + 2);
+                const float sc = float(double(lf.wc) / (3.0 * double(lf.npx)));
+                const float sd = nvalid > 0 ? float(double(lf.wd) / nvalid) : 0.f;
+                *lf.loss = double(sc) * __ldcg(lf.acc) + (nvalid > 0 ? double(sd) * __ldcg(lf.acc + 1) : 0.0);
+            }
             if (threadIdx.x == 0) *done_ctr = 0u;   // ready for the next call
         }
     }
@@ -1155,7 +1161,8 @@ __device__ void pose_finalize_block(const double* __restrict__ part, int nblocks
 }
 
 void launch_gaussian_bwd(WsState* s, const float* params, int64_t n, int64_t ld, const float* viewmat,
-                         const gs_camera& cam, float* grad_params, double* grad_pose, uint32_t flags, cudaStream_t st) {
+                         const gs_camera& cam, float* grad_params, double* grad_pose, uint32_t flags, cudaStream_t st,
+                         LossFin lf) {
     if (n == 0) return;
     double* part = grad_pose ? at<double>(s, s->pose_part) : nullptr;
     static int sms = 0;
@@ -1179,7 +1186,7 @@ void launch_gaussian_bwd(WsState* s, const float* params, int64_t n, int64_t ld,
     kern<<<blocks, 256, 0, st>>>(params, n, ld, viewmat, cam, at<uint32_t>(s, s->onlist),
                                  &at<Misc>(s, s->misc)->n_onscreen, at<float4>(s, s->rec), at<float>(s, s->sgrad),
                                  s->n_cap, grad_params, (flags & GS_FLAG_POSE_COV_PATH) ? 1 : 0, part,
-                                 &at<Misc>(s, s->misc)->pose_done, grad_pose);
+                                 &at<Misc>(s, s->misc)->pose_done, grad_pose, part ? lf : LossFin{});
 }
 
 }  // namespace gs

@@ -574,8 +574,12 @@ def test_fused_l1_backward_equals_loss_then_backward(c):
     loss = torch.zeros(1, dtype=torch.float64, device="cuda")
     g.gs_render_bwd_l1(P, n, n, V, pipe.ws, g.make_camera(cfg.cam), pipe.color, pipe.depth, tc, td, 0.9, 0.1,
                        got, gp, loss)
+    loss2 = torch.zeros(1, dtype=torch.float64, device="cuda")   # no pose gradient: separate finalize kernel
+    g.gs_render_bwd_l1(P, n, n, V, pipe.ws, g.make_camera(cfg.cam), pipe.color, pipe.depth, tc, td, 0.9, 0.1,
+                       torch.zeros_like(P), None, loss2)
     torch.cuda.synchronize()
     assert abs(loss.item() - loss_ref.item()) <= 1e-6 * abs(loss_ref.item())
+    assert abs(loss2.item() - loss_ref.item()) <= 1e-6 * abs(loss_ref.item())
     bad = grad_close(got.cpu().numpy(), ref.cpu().numpy())   # fp32 atomics order only
     assert bad.mean() <= 1e-4, bad.mean()
     np.testing.assert_allclose(gp.cpu().numpy(), gp_ref.cpu().numpy(), rtol=1e-3, atol=1e-9)
