@@ -69,7 +69,7 @@ static void carve(WsState* s, Carver& c) {
     s->chunk_mat = c.take(uint64_t((n + 255) / 256 + 1) * tiles * 4);   // path B count/base matrix
     s->srect = c.take(uint64_t(n) * 8);
     s->tile_tot = c.take(uint64_t(tiles) * 4 * 10);   // totals, starts, 8 segment sums
-    s->pose_part = c.take(uint64_t((n + 255) / 256 + 1) * 16 * 8);   // per-block pose partials (<= ceil(n/256) blocks)
+    s->pose_part = c.take(uint64_t(2 * ((n + 255) / 256) + 1) * 16 * 8);   // per-block pose partials (gaussian_bwd grid)
     s->onlist = c.take(uint64_t(n) * 4);                              // on-screen Gaussians, index order
     s->live_cnt = c.take(uint64_t(tiles) * 4);                        // per-tile live-list lengths
     s->svals = c.take(uint64_t(n) * 4);                               // path B: depth-sorted on-screen Gaussians

@@ -903,21 +903,13 @@ __device__ __forceinline__ void gacc(float* p, float v, bool assign) {   // GS_F
     else *p += v;
 }
 
-// GS_FLAG_GRAD_ASSIGN: the off-screen columns of grad[rows][ld] get 0 (gaussian_bwd assigns the rest)
-__global__ void __launch_bounds__(256) zero_offscreen_kernel(const uint32_t* __restrict__ tiles, int64_t n, int64_t ld,
-                                                              int rows, float* __restrict__ grad) {
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        if (tiles[i] > 0u) continue;
-        for (int k = 0; k < rows; ++k) grad[k * ld + i] = 0.f;
-    }
-}
-
 template <int SH, bool ASSIGN>
 __global__ void __launch_bounds__(256, 4) gaussian_bwd_kernel(
     const float* __restrict__ params, int64_t n, int64_t ld, const float* __restrict__ viewmat, gs_camera cam,
     const uint32_t* __restrict__ onlist, const unsigned int* __restrict__ n_on, const float4* __restrict__ rec,
     const float* __restrict__ sgrad, int64_t sld, float* __restrict__ grad, int cov_path,
-    double* __restrict__ pose_part, unsigned int* done_ctr, double* __restrict__ grad_pose, LossFin lf) {
+    double* __restrict__ pose_part, unsigned int* done_ctr, double* __restrict__ grad_pose, LossFin lf,
+    const uint32_t* __restrict__ tiles, int zero_blocks) {
     constexpr bool assign = ASSIGN;
     __shared__ float V[12];
     __shared__ bool s_last;
@@ -928,7 +920,18 @@ __global__ void __launch_bounds__(256, 4) gaussian_bwd_kernel(
     for (int k = 0; k < kPoseSums; ++k) pose[k] = 0.f;
     const int64_t Von = int64_t(*n_on);
     // thread t handles the t-th on-screen Gaussians (index order); off-screen ones have zero gradient
-    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < Von; t += int64_t(gridDim.x) * blockDim.x) {
+    // GS_FLAG_GRAD_ASSIGN: the last zero_blocks blocks write the off-screen columns' zero gradients,
+    // concurrently with the compute blocks (they then join the pose epilogue with zero partials)
+    const int compute_blocks = int(gridDim.x) - zero_blocks;
+    if (ASSIGN && int(blockIdx.x) >= compute_blocks) {
+        const int rows = SH == 1 ? 23 : 14;
+        for (int64_t i = int64_t(blockIdx.x - compute_blocks) * blockDim.x + threadIdx.x; i < n;
+             i += int64_t(zero_blocks) * blockDim.x)
+            if (tiles[i] == 0u)
+                for (int k = 0; k < rows; ++k) grad[k * ld + i] = 0.f;
+    }
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < Von && int(blockIdx.x) < compute_blocks;
+         t += int64_t(compute_blocks) * blockDim.x) {
         const int64_t i = int64_t(onlist[t]);
         if (i >= n) continue;
         float s[10];
@@ -1176,17 +1179,14 @@ void launch_gaussian_bwd(WsState* s, const float* params, int64_t n, int64_t ld,
     const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(sms) * 4));
     KTimer kt(s, KID_BWD_GAUSS, st);
     const int assign = (flags & GS_FLAG_GRAD_ASSIGN) ? 1 : 0;
-    if (assign && grad_params) {   // (timed with gaussian_bwd)
-        s->launches += 1;
-        zero_offscreen_kernel<<<int(std::min<int64_t>((n + 255) / 256, int64_t(sms) * 8)), 256, 0, st>>>(
-            at<uint32_t>(s, s->tiles), n, ld, s->sh_degree == 1 ? 23 : 14, grad_params);
-    }
+    const int zero_blocks = (assign && grad_params) ? std::min(sms, int((n + 255) / 256)) : 0;
     auto kern = s->sh_degree == 1 ? (assign ? gaussian_bwd_kernel<1, true> : gaussian_bwd_kernel<1, false>)
                                   : (assign ? gaussian_bwd_kernel<0, true> : gaussian_bwd_kernel<0, false>);
-    kern<<<blocks, 256, 0, st>>>(params, n, ld, viewmat, cam, at<uint32_t>(s, s->onlist),
-                                 &at<Misc>(s, s->misc)->n_onscreen, at<float4>(s, s->rec), at<float>(s, s->sgrad),
-                                 s->n_cap, grad_params, (flags & GS_FLAG_POSE_COV_PATH) ? 1 : 0, part,
-                                 &at<Misc>(s, s->misc)->pose_done, grad_pose, part ? lf : LossFin{});
+    kern<<<blocks + zero_blocks, 256, 0, st>>>(
+        params, n, ld, viewmat, cam, at<uint32_t>(s, s->onlist), &at<Misc>(s, s->misc)->n_onscreen,
+        at<float4>(s, s->rec), at<float>(s, s->sgrad), s->n_cap, grad_params, (flags & GS_FLAG_POSE_COV_PATH) ? 1 : 0,
+        part, &at<Misc>(s, s->misc)->pose_done, grad_pose, part ? lf : LossFin{}, at<uint32_t>(s, s->tiles),
+        zero_blocks);
 }
 
 }  // namespace gs
