@@ -173,6 +173,29 @@ gs_status gs_adam_step(float* params_raw, float* params_act, const float* grad_a
 gs_status gs_pose_step(float* viewmat, const double* grad_pose, float* m6, float* v6, int32_t step,
                        float lr_rho, float lr_phi, void* stream);
 
+/* gs_pose_extrapolate — constant-velocity initialisation of a new frame's pose ("transforms the last
+ * known pose based on the relative transformation between the second-to-last pose and the last pose",
+ * PAPER.md:147): with world->camera poses T1 (second-to-last) and T2 (last),
+ * out = (T2 T1^-1) T2, computed in fp64 on the device. All three are device float[12] (3x4 row-major);
+ * out may alias neither input. */
+gs_status gs_pose_extrapolate(const float* view_prev2, const float* view_prev, float* view_out, void* stream);
+
+/* gs_frame_stats — the keyframe rule's measurement ("the proportion of the currently
+ * observed image's reliable region"): counts[0] = pixels with valid target
+ * depth that are reliable by Eq. 8 (alpha >= tau_alpha and |D* - D| <= tau_depth), counts[1] = pixels
+ * with valid target depth, counts[2] = pixels with alpha >= tau_alpha (observed). counts: device u32[3],
+ * overwritten. */
+gs_status gs_frame_stats(const float* alpha, const float* depth, const float* target_depth, int32_t W, int32_t H,
+                         float tau_alpha, float tau_depth, uint32_t* counts, void* stream);
+
+/* gs_loss_l1_masked — the tracking loss restricted to previously observed areas ("only rendered at
+ * previously observed areas"; reading C31): as gs_loss_l1 over the pixels with
+ * alpha >= alpha_min only, the colour mean over those pixels (3 N_obs) and the depth mean over those
+ * with valid D*; other pixels get zero gradient. alpha: the render's [H][W] alpha. */
+gs_status gs_loss_l1_masked(const float* color, const float* depth, const float* tgt_color, const float* tgt_depth,
+                            const float* alpha, float alpha_min, int32_t W, int32_t H, float w_color, float w_depth,
+                            float* dL_dcolor, float* dL_ddepth, double* loss /*[1]*/, gs_ws* ws, void* stream);
+
 /* gs_densify_prune — adaptive expansion (Sec. 3.2) and selection (Eq. 12):
  *  GS_DENSIFY_ADD    Eq. 8: pixel unreliable iff alpha < tau_alpha or |D* - D| > tau_depth, with
  *                    D* > 0 and (u+v) % stride == 0, in pixel order; back-projected at D* through

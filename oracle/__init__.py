@@ -376,6 +376,45 @@ def split_clone(params, accum, count, noise, grad_thresh=0.002, scale_thresh=0.0
     return out, clone, split
 
 
+def pose_extrapolate(view_prev2, view_prev) -> np.ndarray:
+    """Constant velocity: out = (T2 T1^-1) T2 for world->camera 3x4 poses (fp64)."""
+    def h(v):
+        m = np.eye(4)
+        m[:3] = np.asarray(v, np.float64)
+        return m
+    T1, T2 = h(view_prev2), h(view_prev)
+    return (T2 @ np.linalg.inv(T1) @ T2)[:3]
+
+
+def frame_stats(alpha, depth, tgt_depth, tau_alpha=0.5, tau_depth=0.10) -> tuple[int, int, int]:
+    """Keyframe rule measurement: (reliable valid pixels by Eq. 8's complement, valid pixels,
+    observed pixels alpha >= tau_alpha). Comparisons in fp32."""
+    a = np.asarray(alpha, np.float32)
+    d = np.asarray(depth, np.float32)
+    t = np.asarray(tgt_depth, np.float32)
+    valid = t > 0
+    obs = a >= np.float32(tau_alpha)
+    rel = valid & obs & (np.abs(t - d) <= np.float32(tau_depth))
+    return int(rel.sum()), int(valid.sum()), int(obs.sum())
+
+
+def loss_l1_masked(color, depth, tgt_color, tgt_depth, alpha, alpha_min=0.5, w_color=0.9, w_depth=0.1) -> dict:
+    """Reading C31 (tracking only on previously observed areas): Eq. 6 as means over the
+    observed pixels (alpha >= alpha_min): colour over 3 N_obs values, depth over the observed pixels
+    with valid D*; zero gradient elsewhere."""
+    obs = np.asarray(alpha, np.float32) >= np.float32(alpha_min)
+    c = np.asarray(color, np.float64)
+    d = np.asarray(depth, np.float64)
+    tc = np.asarray(tgt_color, np.float64)
+    td = np.asarray(tgt_depth, np.float64)
+    valid = obs & (td > 0)
+    nobs, nv = int(obs.sum()), int(valid.sum())
+    sc = w_color / (3.0 * nobs) if nobs else 0.0
+    sd = w_depth / nv if nv else 0.0
+    loss = sc * np.abs(c - tc)[:, obs].sum() + sd * np.abs(d - td)[valid].sum()
+    return dict(loss=loss, dL_dcolor=sc * np.sign(c - tc) * obs, dL_ddepth=sd * np.sign(d - td) * valid)
+
+
 def degenerate_mask(mean2d, depth, tiles, tgt_depth, gamma=0.10) -> np.ndarray:
     """Eq. 9, reading C27: a Gaussian visible in the frame (tiles > 0) is a floater iff its
     centre pixel round(m) = floor(m + 0.5) is inside the image with valid D* > 0 and D* - d > gamma

@@ -75,6 +75,10 @@ _SIGS = {
                                               _P]),
     "gs_render_bwd_l1": (ctypes.c_int, [_P, _I64, _I64, _P, ctypes.POINTER(gs_ws), ctypes.POINTER(gs_camera), _P, _P,
                                         _P, _P, _F, _F, _P, _P, _P, _U32, _P]),
+    "gs_pose_extrapolate": (ctypes.c_int, [_P, _P, _P, _P]),
+    "gs_frame_stats": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _F, _F, _P, _P]),
+    "gs_loss_l1_masked": (ctypes.c_int, [_P, _P, _P, _P, _P, _F, _I32, _I32, _F, _F, _P, _P, _P, ctypes.POINTER(gs_ws),
+                                         _P]),
     "gs_project_sh": (ctypes.c_int, [_P, _I64, _I64, _I32, _P, _P, ctypes.POINTER(gs_camera), ctypes.POINTER(gs_ws),
                                      _P]),
     "gs_bin_sort": (ctypes.c_int, [ctypes.POINTER(gs_ws), ctypes.POINTER(_I64), _U32, _P]),
@@ -265,6 +269,23 @@ def gs_loss_l1(color, depth, tgt_color, tgt_depth, width, height, w_color, w_dep
     _check(_lib.gs_loss_l1(_ptr(color), _ptr(depth), _ptr(tgt_color), _ptr(tgt_depth), width, height, w_color,
                            w_depth, _ptr(dL_dcolor), _ptr(dL_ddepth), _ptr(loss), ctypes.byref(ws.state),
                            _stream(stream)), "gs_loss_l1")
+
+
+def gs_pose_extrapolate(view_prev2, view_prev, view_out, stream=None):
+    _check(_lib.gs_pose_extrapolate(_ptr(view_prev2), _ptr(view_prev), _ptr(view_out), _stream(stream)),
+           "gs_pose_extrapolate")
+
+
+def gs_frame_stats(alpha, depth, target_depth, width, height, tau_alpha, tau_depth, counts, stream=None):
+    _check(_lib.gs_frame_stats(_ptr(alpha), _ptr(depth), _ptr(target_depth), width, height, tau_alpha, tau_depth,
+                               _ptr(counts), _stream(stream)), "gs_frame_stats")
+
+
+def gs_loss_l1_masked(color, depth, tgt_color, tgt_depth, alpha, alpha_min, width, height, w_color, w_depth,
+                      dL_dcolor, dL_ddepth, loss, ws: Workspace, stream=None):
+    _check(_lib.gs_loss_l1_masked(_ptr(color), _ptr(depth), _ptr(tgt_color), _ptr(tgt_depth), _ptr(alpha), alpha_min,
+                                  width, height, w_color, w_depth, _ptr(dL_dcolor), _ptr(dL_ddepth), _ptr(loss),
+                                  ctypes.byref(ws.state), _stream(stream)), "gs_loss_l1_masked")
 
 
 def gs_adam_step(params_raw, params_act, grad_act, m, v, n, ld, lr, step, b1=0.9, b2=0.999, eps=1e-8, stream=None):

@@ -239,6 +239,32 @@ gs_status gs_loss_l1(const float* color, const float* depth, const float* tgt_co
     return check_launch(s, "gs_loss_l1");
 }
 
+gs_status gs_loss_l1_masked(const float* color, const float* depth, const float* tgt_color, const float* tgt_depth,
+                            const float* alpha, float alpha_min, int32_t W, int32_t H, float w_color, float w_depth,
+                            float* dL_dcolor, float* dL_ddepth, double* loss, gs_ws* ws, void* stream) {
+    if (!ws_ok(ws) || !color || !depth || !tgt_color || !tgt_depth || !alpha || !dL_dcolor || !dL_ddepth || W <= 0 ||
+        H <= 0)
+        return GS_ERR_INVALID_ARG;
+    WsState* s = state(ws);
+    launch_loss_l1_masked(s, color, depth, tgt_color, tgt_depth, alpha, alpha_min, W, H, w_color, w_depth, dL_dcolor,
+                          dL_ddepth, loss, static_cast<cudaStream_t>(stream));
+    return check_launch(s, "gs_loss_l1_masked");
+}
+
+gs_status gs_frame_stats(const float* alpha, const float* depth, const float* target_depth, int32_t W, int32_t H,
+                         float tau_alpha, float tau_depth, uint32_t* counts, void* stream) {
+    if (!alpha || !depth || !target_depth || !counts || W <= 0 || H <= 0) return GS_ERR_INVALID_ARG;
+    launch_frame_stats(alpha, depth, target_depth, W, H, tau_alpha, tau_depth, counts, static_cast<cudaStream_t>(stream));
+    return check_launch(nullptr, "gs_frame_stats");
+}
+
+gs_status gs_pose_extrapolate(const float* view_prev2, const float* view_prev, float* view_out, void* stream) {
+    if (!view_prev2 || !view_prev || !view_out || view_out == view_prev || view_out == view_prev2)
+        return GS_ERR_INVALID_ARG;
+    launch_pose_extrapolate(view_prev2, view_prev, view_out, static_cast<cudaStream_t>(stream));
+    return check_launch(nullptr, "gs_pose_extrapolate");
+}
+
 gs_status gs_adam_step(float* params_raw, float* params_act, const float* grad_act, float* m, float* v, int64_t n,
                        int64_t ld, const float lr[14], int32_t step, float b1, float b2, float eps, void* stream) {
     if ((n > 0 && (!params_raw || !params_act || !grad_act || !m || !v)) || !lr || n < 0 || ld < n || step < 1)

@@ -123,6 +123,135 @@ void launch_loss_l1(WsState* s, const float* color, const float* depth, const fl
     else loss_grad_kernel<1><<<blocks, 256, 0, st>>>(color, depth, tc, td, npx, wc, wd, misc->loss_acc, dc, dd, loss);
 }
 
+// ------------------------------------------------------------------ tracking front end (NEXT-4)
+// masked L1 (reading C31): pass 1 counts / sums over the observed pixels, pass 2 writes the gradients
+__global__ void __launch_bounds__(256) loss_masked_reduce_kernel(const float* __restrict__ c,
+                                                                 const float* __restrict__ d,
+                                                                 const float* __restrict__ tc,
+                                                                 const float* __restrict__ td,
+                                                                 const float* __restrict__ alpha, float amin,
+                                                                 int64_t npx, double* __restrict__ acc) {
+    float sc = 0.f, sd = 0.f, nobs = 0.f, nv = 0.f;
+    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < npx; p += int64_t(gridDim.x) * blockDim.x) {
+        if (!(alpha[p] >= amin)) continue;
+        nobs += 1.f;
+        sc += fabsf(c[p] - tc[p]) + fabsf(c[npx + p] - tc[npx + p]) + fabsf(c[2 * npx + p] - tc[2 * npx + p]);
+        const float t = td[p];
+        if (t > 0.f) {
+            sd += fabsf(d[p] - t);
+            nv += 1.f;
+        }
+    }
+    using BR = cub::BlockReduce<double, 256>;
+    __shared__ typename BR::TempStorage tmp;
+    const double v[4] = {double(sc), double(sd), double(nv), double(nobs)};
+    for (int k = 0; k < 4; ++k) {
+        const double r = BR(tmp).Sum(v[k]);
+        if (threadIdx.x == 0) atomicAdd(acc + k, r);
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(256) loss_masked_grad_kernel(const float* __restrict__ c, const float* __restrict__ d,
+                                                               const float* __restrict__ tc,
+                                                               const float* __restrict__ td,
+                                                               const float* __restrict__ alpha, float amin,
+                                                               int64_t npx, float wc, float wd,
+                                                               const double* __restrict__ acc, float* __restrict__ dc,
+                                                               float* __restrict__ dd, double* __restrict__ loss) {
+    const double nvalid = acc[2], nobs = acc[3];
+    const float sc = nobs > 0 ? float(double(wc) / (3.0 * nobs)) : 0.f;
+    const float sd = nvalid > 0 ? float(double(wd) / nvalid) : 0.f;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && loss)
+        *loss = (nobs > 0 ? double(sc) * acc[0] : 0.0) + (nvalid > 0 ? double(sd) * acc[1] : 0.0);
+    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < npx; p += int64_t(gridDim.x) * blockDim.x) {
+        const bool obs = alpha[p] >= amin;
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) dc[ch * npx + p] = obs ? sc * sgnf(c[ch * npx + p] - tc[ch * npx + p]) : 0.f;
+        const float t = td[p];
+        dd[p] = (obs && t > 0.f) ? sd * sgnf(d[p] - t) : 0.f;
+    }
+}
+
+void launch_loss_l1_masked(WsState* s, const float* color, const float* depth, const float* tc, const float* td,
+                           const float* alpha, float amin, int32_t W, int32_t H, float wc, float wd, float* dc,
+                           float* dd, double* loss, cudaStream_t st) {
+    Misc* misc = at<Misc>(s, s->misc);
+    const int64_t npx = int64_t(W) * H;
+    cudaMemsetAsync(misc->loss_acc, 0, sizeof(misc->loss_acc), st);
+    const int blocks = int(std::min<int64_t>((npx + 255) / 256, 148 * 4));
+    {
+        KTimer kt(s, KID_LOSS, st);
+        loss_masked_reduce_kernel<<<blocks, 256, 0, st>>>(color, depth, tc, td, alpha, amin, npx, misc->loss_acc);
+    }
+    KTimer kt(s, KID_LOSS, st);
+    loss_masked_grad_kernel<<<blocks, 256, 0, st>>>(color, depth, tc, td, alpha, amin, npx, wc, wd, misc->loss_acc,
+                                                    dc, dd, loss);
+}
+
+__global__ void frame_stats_kernel(const float* __restrict__ alpha, const float* __restrict__ depth,
+                                   const float* __restrict__ td, int64_t npx, float ta, float tdep,
+                                   uint32_t* __restrict__ counts) {
+    uint32_t rel = 0, val = 0, obs = 0;
+    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < npx; p += int64_t(gridDim.x) * blockDim.x) {
+        const float t = td[p];
+        const bool o = alpha[p] >= ta;
+        obs += o;
+        if (t > 0.f) {
+            ++val;
+            rel += (o && fabsf(t - depth[p]) <= tdep) ? 1u : 0u;
+        }
+    }
+#pragma unroll
+    for (int k = 16; k > 0; k >>= 1) {
+        rel += __shfl_xor_sync(0xffffffffu, rel, k);
+        val += __shfl_xor_sync(0xffffffffu, val, k);
+        obs += __shfl_xor_sync(0xffffffffu, obs, k);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(counts + 0, rel);
+        atomicAdd(counts + 1, val);
+        atomicAdd(counts + 2, obs);
+    }
+}
+
+void launch_frame_stats(const float* alpha, const float* depth, const float* td, int32_t W, int32_t H, float ta,
+                        float tdep, uint32_t* counts, cudaStream_t st) {
+    cudaMemsetAsync(counts, 0, 3 * sizeof(uint32_t), st);
+    const int64_t npx = int64_t(W) * H;
+    frame_stats_kernel<<<int(std::min<int64_t>((npx + 255) / 256, 148 * 2)), 256, 0, st>>>(alpha, depth, td, npx, ta,
+                                                                                           tdep, counts);
+}
+
+// constant velocity: out = (T2 T1^-1) T2 for world->camera [R | t] poses, fp64
+__global__ void pose_extrapolate_kernel(const float* __restrict__ t1, const float* __restrict__ t2,
+                                        float* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double R1[3][3], R2[3][3], a[3], b[3];
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j) {
+            R1[i][j] = t1[4 * i + j];
+            R2[i][j] = t2[4 * i + j];
+        }
+        a[i] = t1[4 * i + 3];
+        b[i] = t2[4 * i + 3];
+    }
+    // D = T2 T1^-1: R_D = R2 R1^T, t_D = b - R_D a;  out = D T2: R = R_D R2, t = R_D b + t_D
+    double RD[3][3], tD[3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) RD[i][j] = R2[i][0] * R1[j][0] + R2[i][1] * R1[j][1] + R2[i][2] * R1[j][2];
+    for (int i = 0; i < 3; ++i) tD[i] = b[i] - (RD[i][0] * a[0] + RD[i][1] * a[1] + RD[i][2] * a[2]);
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j)
+            out[4 * i + j] = float(RD[i][0] * R2[0][j] + RD[i][1] * R2[1][j] + RD[i][2] * R2[2][j]);
+        out[4 * i + 3] = float(RD[i][0] * b[0] + RD[i][1] * b[1] + RD[i][2] * b[2] + tD[i]);
+    }
+}
+
+void launch_pose_extrapolate(const float* t1, const float* t2, float* out, cudaStream_t st) {
+    pose_extrapolate_kernel<<<1, 32, 0, st>>>(t1, t2, out);
+}
+
 // ------------------------------------------------------------------ Adam
 struct Lr14 { float v[14]; };
 

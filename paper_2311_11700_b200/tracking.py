@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import (GS_DENSIFY_SELECT, GS_FLAG_ACCUM_WEIGHT, GS_FLAG_NO_HOST_SYNC, GS_FLAG_POSE_COV_PATH, densify_cfg,
-               gs_densify_prune, gs_pose_step, make_camera)
+               gs_densify_prune, gs_frame_stats, gs_loss_l1_masked, gs_pose_extrapolate, gs_pose_step, make_camera)
 from .pipeline import RenderPipeline
 
 
@@ -33,6 +33,7 @@ class TrackConfig:
     sel_weight: float = 0.5
     sel_depth: float = 0.05
     pose_flags: int = GS_FLAG_POSE_COV_PATH
+    observed_alpha: float | None = None   # NEXT-4 / reading C31: loss only where the render's alpha >= this
 
 
 class Tracker:
@@ -57,7 +58,15 @@ class Tracker:
 
     def _iter(self, pipe, cam, P, n, V, tc, td, cfg: TrackConfig, mask=None):
         pipe.forward(P, n, V, cam, mask=mask, bin_flags=GS_FLAG_NO_HOST_SYNC, fwd_flags=0)
-        dc, dd = pipe.loss_l1(cam, tc, td, cfg.w_color, cfg.w_depth)
+        if cfg.observed_alpha is None:
+            dc, dd = pipe.loss_l1(cam, tc, td, cfg.w_color, cfg.w_depth)
+        else:   # "only rendered at previously observed areas"
+            color, depth, alpha = pipe._imgs(cam)
+            npx = cam.width * cam.height
+            dc = pipe.dL_dcolor.view(-1)[:3 * npx].view(3, cam.height, cam.width)
+            dd = pipe.dL_ddepth.view(-1)[:npx].view(cam.height, cam.width)
+            gs_loss_l1_masked(color, depth, tc, td, alpha, cfg.observed_alpha, cam.width, cam.height, cfg.w_color,
+                              cfg.w_depth, dc, dd, pipe.loss, pipe.ws)
         self.grad_pose.zero_()
         pipe.pose_grad(P, n, V, cam, dc, dd, self.grad_pose, flags=cfg.pose_flags)
         self.step += 1
@@ -90,6 +99,56 @@ class Tracker:
         for _ in range(cfg.iters_fine):
             self.fine_iter(P, n, V, tc_full, td_full, cfg)
         return V
+
+
+@dataclasses.dataclass
+class FrontendConfig:
+    track: TrackConfig = dataclasses.field(default_factory=lambda: TrackConfig(observed_alpha=0.5))
+    kf_reliable: float = 0.7     # keyframe when the reliable share of valid pixels drops below this
+    kf_max_gap: int = 30         # ... or this many frames after the last keyframe (mu_k)
+    tau_alpha: float = 0.5       # Eq. 8 thresholds for "reliable"
+    tau_depth: float = 0.10
+
+
+class Frontend:
+    """Tracking front end: constant-velocity pose
+    initialisation (gs_pose_extrapolate), coarse-to-fine tracking on previously observed areas
+    (gs_loss_l1_masked), and the keyframe rule (gs_frame_stats: reliable share of the observed
+    image, or a maximum frame gap). One host read per frame (the keyframe decision)."""
+
+    def __init__(self, tracker: Tracker, cfg: FrontendConfig = FrontendConfig()):
+        self.tr = tracker
+        self.cfg = cfg
+        self.poses: list[torch.Tensor] = []
+        self.since_kf = 0
+        self.counts = torch.zeros(3, dtype=torch.int32, device=tracker.grad_pose.device)
+
+    def initial_pose(self) -> torch.Tensor:
+        """Constant velocity from the last two poses (or the last one)."""
+        V = torch.empty(3, 4, dtype=torch.float32, device=self.counts.device)
+        if len(self.poses) >= 2:
+            gs_pose_extrapolate(self.poses[-2], self.poses[-1], V)
+        else:
+            V.copy_(self.poses[-1])
+        return V
+
+    def add_pose(self, V: torch.Tensor, keyframe: bool = True):
+        self.poses.append(V.clone())
+        self.since_kf = 0 if keyframe else self.since_kf + 1
+
+    def track_frame(self, P, n, tc_half, td_half, tc_full, td_full) -> tuple[torch.Tensor, bool, float]:
+        """Track one frame from the constant-velocity guess; returns (pose, keyframe?, reliable share)."""
+        V = self.initial_pose()
+        self.tr.track(P, n, V, tc_half, td_half, tc_full, td_full, self.cfg.track)
+        cam = self.tr.cam_full
+        fr = self.tr.full.forward(P, n, V, cam, bin_flags=GS_FLAG_NO_HOST_SYNC, fwd_flags=0)
+        gs_frame_stats(fr.alpha, fr.depth, td_full, cam.width, cam.height, self.cfg.tau_alpha, self.cfg.tau_depth,
+                       self.counts)
+        rel, valid, _ = (int(x) for x in self.counts.cpu().tolist())
+        share = rel / max(valid, 1)
+        keyframe = share < self.cfg.kf_reliable or self.since_kf + 1 >= self.cfg.kf_max_gap
+        self.add_pose(V, keyframe)
+        return V, keyframe, share
 
 
 def pose_error(view, view_gt) -> tuple[float, float]:

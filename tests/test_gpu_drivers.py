@@ -143,3 +143,49 @@ def test_bundle_adjustment_refines_keyframe_poses():
         e1 = pose_error(kf.view.cpu().numpy(), vv)
         print("BA pose error before", e, "after", e1)
         assert e1[0] < 0.7 * e[0] and e1[1] < 0.7 * e[1]
+
+
+def test_frontend_tracks_a_constant_velocity_trajectory():
+    """NEXT-4 front end on a surface room: frames rendered along a constant-twist trajectory; with
+    the first two poses known, frame 2 starts from the constant-velocity guess (exact for this
+    trajectory up to fp32) perturbed by ~1 cm / 0.5 deg, frame 3 from the guess built on frame 2's
+    tracked pose; tracking on the observed areas must halve both starting errors. The keyframe
+    rule reads a high reliable share on the well-explained frames and fires on the frame gap."""
+    import paper_2311_11700_b200 as g
+    from paper_2311_11700_b200.tracking import Frontend, FrontendConfig, TrackConfig, Tracker, pose_error
+    cam = gi.CAM_TUM
+    p = gi.room_surface_gaussians(200_000, 51)
+    n = p.shape[1]
+    v0 = gi.room_view(151).astype(np.float64)
+    delta = np.array([0.01, 0.0, 0.005, 0.0, 0.01, 0.0])
+    traj = [v0]
+    for _ in range(3):
+        traj.append(oracle.apply_twist(delta, traj[-1]))
+    kc = max(key_cap_for(p, v.astype(np.float32), cam, slack=1.6)[0] for v in traj)
+    kh = max(key_cap_for(p, v.astype(np.float32), cam.half(), slack=1.6)[0] for v in traj)
+    tr = Tracker(n, kc, kh, cam)
+    P = to_dev(p)
+    fe = Frontend(tr, FrontendConfig(track=TrackConfig(iters_coarse=30, iters_fine=30, observed_alpha=0.5),
+                                     kf_max_gap=2))
+    fe.add_pose(to_dev(traj[0]))
+    fe.add_pose(to_dev(traj[1]), keyframe=False)
+    kfs = []
+    for k in (2, 3):
+        tc_h, td_h = _render(tr.half, P, n, to_dev(traj[k]), cam.half())
+        tc_f, td_f = _render(tr.full, P, n, to_dev(traj[k]), cam)
+        if k == 2:   # poses 0, 1 are exact: the constant-velocity guess is the true pose; perturb pose 1
+            guess = oracle.pose_extrapolate(fe.poses[-2].cpu().numpy(), fe.poses[-1].cpu().numpy())
+            assert pose_error(guess, traj[k])[0] < 1e-4
+            # the extrapolation applies the perturbation twice: the guess is off by ~1 cm / 0.5 deg
+            fe.poses[-1] = to_dev(oracle.apply_twist(gi.twist_perturbation(400 + k, 0.005, 0.25),
+                                                     fe.poses[-1].cpu().numpy().astype(np.float64)))
+        # frame 3 starts from frame 2's tracked pose: its residual error, doubled, is the guess error
+        e0 = pose_error(oracle.pose_extrapolate(fe.poses[-2].cpu().numpy(), fe.poses[-1].cpu().numpy()), traj[k])
+        V, kf, share = fe.track_frame(P, n, tc_h, td_h, tc_f, td_f)
+        torch.cuda.synchronize()
+        e1 = pose_error(V.cpu().numpy(), traj[k])
+        print("frame", k, "guess error", e0, "tracked", e1, "keyframe", kf, "reliable share", share)
+        assert e1[0] < 0.5 * e0[0] and e1[1] < 0.5 * e0[1]
+        assert share > 0.8
+        kfs.append(kf)
+    assert kfs == [True, False]   # gap rule: frame 2 is the second after the last keyframe (max gap 2)

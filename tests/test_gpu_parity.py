@@ -583,3 +583,36 @@ def test_fused_l1_backward_equals_loss_then_backward(c):
     bad = grad_close(got.cpu().numpy(), ref.cpu().numpy())   # fp32 atomics order only
     assert bad.mean() <= 1e-4, bad.mean()
     np.testing.assert_allclose(gp.cpu().numpy(), gp_ref.cpu().numpy(), rtol=1e-3, atol=1e-9)
+
+
+# ------------------------------------------------------------------ tracking front end (NEXT-4)
+def test_frontend_kernels_parity():
+    """gs_pose_extrapolate against the fp64 oracle (fp32 output); gs_frame_stats bit-exact counts;
+    gs_loss_l1_masked against the oracle (reading C31)."""
+    import paper_2311_11700_b200 as g
+    v1 = oracle.apply_twist(np.array([0.1, -0.05, 0.2, 0.05, -0.1, 0.2]), gi.identity_view().astype(np.float64))
+    v2 = oracle.apply_twist(np.array([0.02, 0.01, -0.03, 0.01, 0.02, -0.015]), v1)
+    out = torch.zeros(3, 4, device="cuda")
+    g.gs_pose_extrapolate(to_dev(v1), to_dev(v2), out)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(out.cpu().numpy(), oracle.pose_extrapolate(v1.astype(np.float32), v2.astype(np.float32)),
+                               atol=2e-6)
+    W, H = 64, 40
+    c, d = gi.random_images(W, H, 21)
+    tc, td = gi.random_images(W, H, 22)
+    a = np.random.default_rng(23).uniform(0, 1, (H, W)).astype(np.float32)
+    counts = torch.zeros(3, dtype=torch.int32, device="cuda")
+    g.gs_frame_stats(to_dev(a), to_dev(d), to_dev(td), W, H, 0.5, 1.0, counts)
+    torch.cuda.synchronize()
+    assert tuple(counts.cpu().tolist()) == oracle.frame_stats(a, d, td, 0.5, 1.0)
+    pipe = g.RenderPipeline(16, 4096, W, H)
+    dc = torch.zeros(3, H, W, device="cuda")
+    dd = torch.zeros(H, W, device="cuda")
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    g.gs_loss_l1_masked(to_dev(c), to_dev(d), to_dev(tc), to_dev(td), to_dev(a), 0.5, W, H, 0.9, 0.1, dc, dd, loss,
+                        pipe.ws)
+    torch.cuda.synchronize()
+    o = oracle.loss_l1_masked(c, d, tc, td, a, 0.5)
+    np.testing.assert_allclose(dc.cpu().numpy(), o["dL_dcolor"], rtol=1e-6, atol=0)
+    np.testing.assert_allclose(dd.cpu().numpy(), o["dL_ddepth"], rtol=1e-6, atol=0)
+    assert abs(loss.item() - o["loss"]) <= 1e-6 * abs(o["loss"])

@@ -736,3 +736,42 @@ def test_split_clone_hand_built():
     # capacity: one free column takes the clone only; no split fits
     out2, c2, s2_ = oracle.split_clone(p, accum, count, noise, 0.002, 0.02, capacity=5)
     assert c2.tolist() == [1] and s2_.size == 0 and out2.shape[1] == 5
+
+
+# ------------------------------------------------------------------ tracking front end (NEXT-4)
+def test_pose_extrapolate_constant_twist():
+    """Constant velocity: on a trajectory T_k = exp(k delta) T_0 the extrapolation of T_1, T_2
+    is exactly T_3 (SE(3) exponential from scipy's expm)."""
+    from scipy.linalg import expm
+    delta = np.array([0.03, -0.01, 0.02, 0.01, 0.04, -0.02])
+    X = np.zeros((4, 4))
+    X[:3, :3] = oracle.skew(delta[3:])
+    X[:3, 3] = delta[:3]
+    E = expm(X)
+    T0 = np.eye(4)
+    T0[:3] = oracle.apply_twist(np.array([0.1, 0.2, -0.3, 0.2, -0.1, 0.3]), gi.identity_view().astype(np.float64))
+    T = [np.linalg.matrix_power(E, k) @ T0 for k in range(4)]
+    np.testing.assert_allclose(oracle.pose_extrapolate(T[1][:3], T[2][:3]), T[3][:3], atol=1e-12)
+
+
+def test_masked_loss_and_frame_stats_brute_force():
+    """Masked L1 (reading C31): all pixels observed reduces to Eq. 6's colour mean over 3HW and depth
+    mean over valid pixels (the unmasked oracle loss); a brute-force loop checks a partial mask.
+    Frame statistics: brute-force counts."""
+    W, H = 12, 9
+    c, d = gi.random_images(W, H, 3)
+    tc, td = gi.random_images(W, H, 4)
+    full = oracle.loss_l1_masked(c, d, tc, td, np.ones((H, W)), 0.5)
+    ref = oracle.loss_l1(c, d, tc, td)
+    assert abs(full["loss"] - ref["loss"]) <= 1e-12 * abs(ref["loss"])
+    a = np.random.default_rng(5).uniform(0, 1, (H, W)).astype(np.float32)
+    m = oracle.loss_l1_masked(c, d, tc, td, a, 0.5)
+    obs = [(v, u) for v in range(H) for u in range(W) if a[v, u] >= 0.5]
+    val = [(v, u) for v, u in obs if td[v, u] > 0]
+    lc = sum(abs(float(c[ch, v, u]) - float(tc[ch, v, u])) for v, u in obs for ch in range(3)) * 0.9 / (3 * len(obs))
+    ld = sum(abs(float(d[v, u]) - float(td[v, u])) for v, u in val) * 0.1 / len(val)
+    assert abs(m["loss"] - (lc + ld)) <= 1e-12
+    assert (m["dL_dcolor"][:, a < 0.5] == 0).all()
+    rel = sum(1 for v in range(H) for u in range(W)
+              if td[v, u] > 0 and a[v, u] >= 0.5 and abs(float(td[v, u]) - float(d[v, u])) <= np.float32(0.1))
+    assert oracle.frame_stats(a, d, td, 0.5, 0.10) == (rel, int((td > 0).sum()), int((a >= 0.5).sum()))
