@@ -189,12 +189,19 @@ gs_status gs_frame_stats(const float* alpha, const float* depth, const float* ta
                          float tau_alpha, float tau_depth, uint32_t* counts, void* stream);
 
 /* gs_loss_l1_masked — the tracking loss restricted to previously observed areas ("only rendered at
- * previously observed areas"; reading C31): as gs_loss_l1 over the pixels with
- * alpha >= alpha_min only, the colour mean over those pixels (3 N_obs) and the depth mean over those
- * with valid D*; other pixels get zero gradient. alpha: the render's [H][W] alpha. */
+ * previously observed areas"; reading C31): as gs_loss_l1 over the kept pixels only,
+ * the colour mean over those pixels (3 N_kept) and the depth mean over those with valid D*; other
+ * pixels get zero gradient. Kept = alpha >= alpha_min (alpha: the render's [H][W] alpha) and, when
+ * outlier_k > 0, the outlier rule of PAPER.md:954 ("if the loss on the pixel is more than ten times
+ * the median loss, the pixel will be ignored"; reading C32): l_p = (|dC_0| + |dC_1|) + |dC_2| in fp32,
+ * m = the lower median of l_p over the alpha-kept pixels, kept iff l_p <= outlier_k * m (fp32).
+ * outlier_k = 0 turns the rule off; negative or NaN -> GS_ERR_INVALID_ARG. The outlier path is one
+ * cooperative launch (one CTA per SM) that uses the workspace's binning scratch: do not run it
+ * concurrently with gs_bin_sort on the same workspace. */
 gs_status gs_loss_l1_masked(const float* color, const float* depth, const float* tgt_color, const float* tgt_depth,
-                            const float* alpha, float alpha_min, int32_t W, int32_t H, float w_color, float w_depth,
-                            float* dL_dcolor, float* dL_ddepth, double* loss /*[1]*/, gs_ws* ws, void* stream);
+                            const float* alpha, float alpha_min, float outlier_k, int32_t W, int32_t H, float w_color,
+                            float w_depth, float* dL_dcolor, float* dL_ddepth, double* loss /*[1]*/, gs_ws* ws,
+                            void* stream);
 
 /* gs_densify_prune — adaptive expansion (Sec. 3.2) and selection (Eq. 12):
  *  GS_DENSIFY_ADD    Eq. 8: pixel unreliable iff alpha < tau_alpha or |D* - D| > tau_depth, with

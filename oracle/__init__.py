@@ -398,11 +398,30 @@ def frame_stats(alpha, depth, tgt_depth, tau_alpha=0.5, tau_depth=0.10) -> tuple
     return int(rel.sum()), int(valid.sum()), int(obs.sum())
 
 
-def loss_l1_masked(color, depth, tgt_color, tgt_depth, alpha, alpha_min=0.5, w_color=0.9, w_depth=0.1) -> dict:
-    """Reading C31 (tracking only on previously observed areas): Eq. 6 as means over the
-    observed pixels (alpha >= alpha_min): colour over 3 N_obs values, depth over the observed pixels
-    with valid D*; zero gradient elsewhere."""
+def pixel_colour_loss(color, tgt_color) -> np.ndarray:
+    """Reading C32 ("the loss on the pixel"): the per-pixel colour L1, (|dC_0| + |dC_1|) + |dC_2|,
+    evaluated in fp32 in that order."""
+    c = np.asarray(color, np.float32)
+    t = np.asarray(tgt_color, np.float32)
+    e = np.abs(c - t)
+    return (e[0] + e[1]) + e[2]
+
+
+def loss_l1_masked(color, depth, tgt_color, tgt_depth, alpha, alpha_min=0.5, w_color=0.9, w_depth=0.1,
+                   outlier_k=0.0) -> dict:
+    """Reading C31 (tracking only on previously observed areas): Eq. 6 as means over the kept
+    pixels: colour over 3 N_kept values, depth over the kept pixels with valid D*; zero gradient
+    elsewhere. Kept = observed (alpha >= alpha_min) and, with outlier_k > 0, reading C32 (P:954,
+    "more than ten times the median loss ... ignored"): l_p <= outlier_k * m in fp32, m the lower
+    median of l_p over the observed pixels."""
     obs = np.asarray(alpha, np.float32) >= np.float32(alpha_min)
+    if outlier_k > 0 and obs.any():
+        lp = pixel_colour_loss(color, tgt_color)
+        vals = np.sort(lp[obs])
+        med = vals[(vals.size - 1) // 2]
+        obs = obs & (lp <= np.float32(outlier_k) * med)
+    elif outlier_k > 0:
+        obs = np.zeros_like(obs)
     c = np.asarray(color, np.float64)
     d = np.asarray(depth, np.float64)
     tc = np.asarray(tgt_color, np.float64)
@@ -412,7 +431,7 @@ def loss_l1_masked(color, depth, tgt_color, tgt_depth, alpha, alpha_min=0.5, w_c
     sc = w_color / (3.0 * nobs) if nobs else 0.0
     sd = w_depth / nv if nv else 0.0
     loss = sc * np.abs(c - tc)[:, obs].sum() + sd * np.abs(d - td)[valid].sum()
-    return dict(loss=loss, dL_dcolor=sc * np.sign(c - tc) * obs, dL_ddepth=sd * np.sign(d - td) * valid)
+    return dict(loss=loss, dL_dcolor=sc * np.sign(c - tc) * obs, dL_ddepth=sd * np.sign(d - td) * valid, kept=obs)
 
 
 def degenerate_mask(mean2d, depth, tiles, tgt_depth, gamma=0.10) -> np.ndarray:

@@ -77,7 +77,7 @@ _SIGS = {
                                         _P, _P, _F, _F, _P, _P, _P, _U32, _P]),
     "gs_pose_extrapolate": (ctypes.c_int, [_P, _P, _P, _P]),
     "gs_frame_stats": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _F, _F, _P, _P]),
-    "gs_loss_l1_masked": (ctypes.c_int, [_P, _P, _P, _P, _P, _F, _I32, _I32, _F, _F, _P, _P, _P, ctypes.POINTER(gs_ws),
+    "gs_loss_l1_masked": (ctypes.c_int, [_P, _P, _P, _P, _P, _F, _F, _I32, _I32, _F, _F, _P, _P, _P, ctypes.POINTER(gs_ws),
                                          _P]),
     "gs_project_sh": (ctypes.c_int, [_P, _I64, _I64, _I32, _P, _P, ctypes.POINTER(gs_camera), ctypes.POINTER(gs_ws),
                                      _P]),
@@ -281,10 +281,10 @@ def gs_frame_stats(alpha, depth, target_depth, width, height, tau_alpha, tau_dep
                                _ptr(counts), _stream(stream)), "gs_frame_stats")
 
 
-def gs_loss_l1_masked(color, depth, tgt_color, tgt_depth, alpha, alpha_min, width, height, w_color, w_depth,
-                      dL_dcolor, dL_ddepth, loss, ws: Workspace, stream=None):
+def gs_loss_l1_masked(color, depth, tgt_color, tgt_depth, alpha, alpha_min, outlier_k, width, height, w_color,
+                      w_depth, dL_dcolor, dL_ddepth, loss, ws: Workspace, stream=None):
     _check(_lib.gs_loss_l1_masked(_ptr(color), _ptr(depth), _ptr(tgt_color), _ptr(tgt_depth), _ptr(alpha), alpha_min,
-                                  width, height, w_color, w_depth, _ptr(dL_dcolor), _ptr(dL_ddepth), _ptr(loss),
+                                  outlier_k, width, height, w_color, w_depth, _ptr(dL_dcolor), _ptr(dL_ddepth), _ptr(loss),
                                   ctypes.byref(ws.state), _stream(stream)), "gs_loss_l1_masked")
 
 

@@ -240,13 +240,13 @@ gs_status gs_loss_l1(const float* color, const float* depth, const float* tgt_co
 }
 
 gs_status gs_loss_l1_masked(const float* color, const float* depth, const float* tgt_color, const float* tgt_depth,
-                            const float* alpha, float alpha_min, int32_t W, int32_t H, float w_color, float w_depth,
-                            float* dL_dcolor, float* dL_ddepth, double* loss, gs_ws* ws, void* stream) {
+                            const float* alpha, float alpha_min, float outlier_k, int32_t W, int32_t H, float w_color,
+                            float w_depth, float* dL_dcolor, float* dL_ddepth, double* loss, gs_ws* ws, void* stream) {
     if (!ws_ok(ws) || !color || !depth || !tgt_color || !tgt_depth || !alpha || !dL_dcolor || !dL_ddepth || W <= 0 ||
-        H <= 0)
+        H <= 0 || !(outlier_k >= 0.f))
         return GS_ERR_INVALID_ARG;
     WsState* s = state(ws);
-    launch_loss_l1_masked(s, color, depth, tgt_color, tgt_depth, alpha, alpha_min, W, H, w_color, w_depth, dL_dcolor,
+    launch_loss_l1_masked(s, color, depth, tgt_color, tgt_depth, alpha, alpha_min, outlier_k, W, H, w_color, w_depth, dL_dcolor,
                           dL_ddepth, loss, static_cast<cudaStream_t>(stream));
     return check_launch(s, "gs_loss_l1_masked");
 }

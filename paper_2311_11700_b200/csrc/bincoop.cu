@@ -67,20 +67,6 @@ struct CoopArgs {
 
 __device__ __forceinline__ uint32_t ldcg(const uint32_t* p) { return __ldcg(p); }
 
-__device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int& goal) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        goal += gridDim.x;
-        __threadfence();
-        atomicAdd(bar, 1u);
-        unsigned int v;
-        do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-        } while (v < goal);
-    }
-    __syncthreads();
-}
-
 __device__ __forceinline__ void group_sync(int g) {   // named barrier of one 256-thread group
     asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(256) : "memory");
 }
@@ -457,18 +443,6 @@ struct CoopGeom {
     size_t smem = 0;
     int groups = 0;
 };
-
-static int coop_sm_count() {
-    static int cached[64] = {0};
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
-    if (!cached[dev]) {
-        int v = 0;
-        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
-        cached[dev] = v;
-    }
-    return cached[dev];
-}
 
 gs_status run_bin_coop(WsState* s, cudaStream_t st) {
     Misc* misc = at<Misc>(s, s->misc);

@@ -78,6 +78,23 @@ struct Misc {
     unsigned int pad[2];
 };
 
+// Grid barrier for cooperative launches (all CTAs co-resident): block barrier, one thread fences and
+// arrives on a monotone counter (zeroed before the launch), spins on an acquire load.
+__device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int& goal) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        goal += gridDim.x;
+        __threadfence();
+        atomicAdd(bar, 1u);
+        unsigned int v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        } while (v < goal);
+    }
+    __syncthreads();
+}
+int coop_sm_count();   // SMs of the current device (cached)
+
 // ------------------------------------------------------------------ launch helpers
 // Kernel ids for the event log; names in gs_kernel_name (abi.cu). Keep in sync.
 enum KernelId {
@@ -142,8 +159,8 @@ void launch_gaussian_bwd(WsState* s, const float* params, int64_t n, int64_t ld,
 void launch_loss_l1(WsState* s, const float* color, const float* depth, const float* tc, const float* td,
                     int32_t W, int32_t H, float wc, float wd, float* dc, float* dd, double* loss, cudaStream_t st);
 void launch_loss_l1_masked(WsState* s, const float* color, const float* depth, const float* tc, const float* td,
-                           const float* alpha, float amin, int32_t W, int32_t H, float wc, float wd, float* dc,
-                           float* dd, double* loss, cudaStream_t st);
+                           const float* alpha, float amin, float outlier_k, int32_t W, int32_t H, float wc, float wd,
+                           float* dc, float* dd, double* loss, cudaStream_t st);
 void launch_frame_stats(const float* alpha, const float* depth, const float* td, int32_t W, int32_t H, float ta,
                         float tdep, uint32_t* counts, cudaStream_t st);
 void launch_pose_extrapolate(const float* t1, const float* t2, float* out, cudaStream_t st);

@@ -123,6 +123,18 @@ void launch_loss_l1(WsState* s, const float* color, const float* depth, const fl
     else loss_grad_kernel<1><<<blocks, 256, 0, st>>>(color, depth, tc, td, npx, wc, wd, misc->loss_acc, dc, dd, loss);
 }
 
+int coop_sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+    if (!cached[dev]) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+        cached[dev] = v;
+    }
+    return cached[dev];
+}
+
 // ------------------------------------------------------------------ tracking front end (NEXT-4)
 // masked L1 (reading C31): pass 1 counts / sums over the observed pixels, pass 2 writes the gradients
 __global__ void __launch_bounds__(256) loss_masked_reduce_kernel(const float* __restrict__ c,
@@ -173,12 +185,176 @@ __global__ void __launch_bounds__(256) loss_masked_grad_kernel(const float* __re
     }
 }
 
+// 10x-median pixel rejection (reading C32), one cooperative kernel: the per-pixel
+// colour loss l_p = (|dC_0| + |dC_1|) + |dC_2| (fp32) of the observed pixels is non-negative, so its
+// bit pattern orders like the value; a three-pass radix select (11 + 11 + 9 bits, block histograms
+// -> global histogram -> every CTA scans it) finds the lower median m (rank floor((N_obs - 1) / 2)).
+// Pixels with l_p > k m (fp32) are dropped from both loss terms; then the masked reduction and the
+// gradient pass run as above. l_p is recomputed each pass from the images (28 B/px, L2-resident
+// after the first pass) rather than stored.
+struct RobustScratch {   // in the workspace's coop region, zeroed before the launch
+    uint32_t h0[2048], h1[2048], h2[512];
+    uint32_t bar, nobs, pad[2];
+};
+
+__device__ __forceinline__ uint32_t pixel_loss_bits(const float* __restrict__ c, const float* __restrict__ tc,
+                                                    int64_t npx, int64_t p) {
+    const float l = __fadd_rn(__fadd_rn(fabsf(c[p] - tc[p]), fabsf(c[npx + p] - tc[npx + p])),
+                              fabsf(c[2 * npx + p] - tc[2 * npx + p]));
+    return __float_as_uint(l);
+}
+
+// every CTA: find the bin of rank k in hist[nb] (ld.cg: written by other CTAs before the barrier);
+// returns the bin and leaves the rank within it in k
+template <int NB>
+__device__ __forceinline__ uint32_t select_bin(const uint32_t* hist, uint32_t& k, uint32_t* sh) {
+    using BS = cub::BlockScan<uint32_t, 1024>;
+    __shared__ typename BS::TempStorage tmp;
+    constexpr int PER = (NB + 1023) / 1024;
+    uint32_t v[PER], tot = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const int b = threadIdx.x * PER + j;
+        v[j] = b < NB ? __ldcg(hist + b) : 0u;
+        tot += v[j];
+    }
+    uint32_t ex;
+    BS(tmp).ExclusiveSum(tot, ex);
+    if (ex <= k && k < ex + tot) {   // exactly one thread holds rank k
+        uint32_t run = ex;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            if (run <= k && k < run + v[j]) {
+                sh[0] = threadIdx.x * PER + j;
+                sh[1] = k - run;
+            }
+            run += v[j];
+        }
+    }
+    __syncthreads();
+    const uint32_t b = sh[0];
+    k = sh[1];
+    __syncthreads();
+    return b;
+}
+
+__global__ void __launch_bounds__(1024, 1) loss_robust_kernel(const float* __restrict__ c, const float* __restrict__ d,
+                                                              const float* __restrict__ tc,
+                                                              const float* __restrict__ td,
+                                                              const float* __restrict__ alpha, float amin, float kout,
+                                                              int64_t npx, float wc, float wd, RobustScratch* rs,
+                                                              double* __restrict__ acc, float* __restrict__ dc,
+                                                              float* __restrict__ dd, double* __restrict__ loss) {
+    __shared__ uint32_t sh_h[2048];
+    __shared__ uint32_t sh[4];
+    unsigned int goal = 0;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    const int64_t p0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    // pass 1: top 11 bits (bit 31 is the sign: 0)
+    for (int b = threadIdx.x; b < 2048; b += blockDim.x) sh_h[b] = 0;
+    __syncthreads();
+    uint32_t nobs = 0;
+    for (int64_t p = p0; p < npx; p += stride) {
+        if (!(alpha[p] >= amin)) continue;
+        ++nobs;
+        atomicAdd(sh_h + (pixel_loss_bits(c, tc, npx, p) >> 20), 1u);
+    }
+    nobs = __reduce_add_sync(0xffffffffu, nobs);
+    if ((threadIdx.x & 31) == 0 && nobs) atomicAdd(&rs->nobs, nobs);
+    __syncthreads();
+    for (int b = threadIdx.x; b < 2048; b += blockDim.x)
+        if (sh_h[b]) atomicAdd(rs->h0 + b, sh_h[b]);
+    grid_sync(&rs->bar, goal);
+    const uint32_t n_obs = __ldcg(&rs->nobs);
+    float thr = -1.f;   // no observed pixel: nothing kept
+    if (n_obs > 0) {
+        uint32_t k = (n_obs - 1) / 2;
+        const uint32_t b0 = select_bin<2048>(rs->h0, k, sh);
+        // pass 2: bits 20..9 of the pixels in bin b0
+        for (int b = threadIdx.x; b < 2048; b += blockDim.x) sh_h[b] = 0;
+        __syncthreads();
+        for (int64_t p = p0; p < npx; p += stride) {
+            if (!(alpha[p] >= amin)) continue;
+            const uint32_t key = pixel_loss_bits(c, tc, npx, p);
+            if ((key >> 20) == b0) atomicAdd(sh_h + ((key >> 9) & 2047u), 1u);
+        }
+        __syncthreads();
+        for (int b = threadIdx.x; b < 2048; b += blockDim.x)
+            if (sh_h[b]) atomicAdd(rs->h1 + b, sh_h[b]);
+        grid_sync(&rs->bar, goal);
+        const uint32_t b1 = select_bin<2048>(rs->h1, k, sh);
+        const uint32_t hi = (b0 << 11) | b1;
+        // pass 3: bits 8..0
+        for (int b = threadIdx.x; b < 512; b += blockDim.x) sh_h[b] = 0;
+        __syncthreads();
+        for (int64_t p = p0; p < npx; p += stride) {
+            if (!(alpha[p] >= amin)) continue;
+            const uint32_t key = pixel_loss_bits(c, tc, npx, p);
+            if ((key >> 9) == hi) atomicAdd(sh_h + (key & 511u), 1u);
+        }
+        __syncthreads();
+        for (int b = threadIdx.x; b < 512; b += blockDim.x)
+            if (sh_h[b]) atomicAdd(rs->h2 + b, sh_h[b]);
+        grid_sync(&rs->bar, goal);
+        const uint32_t b2 = select_bin<512>(rs->h2, k, sh);
+        thr = __fmul_rn(kout, __uint_as_float((hi << 9) | b2));
+    }
+    // pass 4: sums over the kept pixels
+    float sc = 0.f, sd = 0.f, nk = 0.f, nv = 0.f;
+    for (int64_t p = p0; p < npx; p += stride) {
+        if (!(alpha[p] >= amin) || !(__uint_as_float(pixel_loss_bits(c, tc, npx, p)) <= thr)) continue;
+        nk += 1.f;
+        sc += fabsf(c[p] - tc[p]) + fabsf(c[npx + p] - tc[npx + p]) + fabsf(c[2 * npx + p] - tc[2 * npx + p]);
+        const float t = td[p];
+        if (t > 0.f) {
+            sd += fabsf(d[p] - t);
+            nv += 1.f;
+        }
+    }
+    {
+        using BR = cub::BlockReduce<double, 1024>;
+        __shared__ typename BR::TempStorage tmp;
+        const double v[4] = {double(sc), double(sd), double(nv), double(nk)};
+        for (int q = 0; q < 4; ++q) {
+            const double r = BR(tmp).Sum(v[q]);
+            if (threadIdx.x == 0) atomicAdd(acc + q, r);
+            __syncthreads();
+        }
+    }
+    grid_sync(&rs->bar, goal);
+    // pass 5: gradients
+    const double nvalid = __ldcg(acc + 2), nkept = __ldcg(acc + 3);
+    const float scl = nkept > 0 ? float(double(wc) / (3.0 * nkept)) : 0.f;
+    const float sdl = nvalid > 0 ? float(double(wd) / nvalid) : 0.f;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && loss)
+        *loss = (nkept > 0 ? double(scl) * __ldcg(acc) : 0.0) + (nvalid > 0 ? double(sdl) * __ldcg(acc + 1) : 0.0);
+    for (int64_t p = p0; p < npx; p += stride) {
+        const bool kept = alpha[p] >= amin && __uint_as_float(pixel_loss_bits(c, tc, npx, p)) <= thr;
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) dc[ch * npx + p] = kept ? scl * sgnf(c[ch * npx + p] - tc[ch * npx + p]) : 0.f;
+        const float t = td[p];
+        dd[p] = (kept && t > 0.f) ? sdl * sgnf(d[p] - t) : 0.f;
+    }
+}
+
 void launch_loss_l1_masked(WsState* s, const float* color, const float* depth, const float* tc, const float* td,
-                           const float* alpha, float amin, int32_t W, int32_t H, float wc, float wd, float* dc,
-                           float* dd, double* loss, cudaStream_t st) {
+                           const float* alpha, float amin, float outlier_k, int32_t W, int32_t H, float wc, float wd,
+                           float* dc, float* dd, double* loss, cudaStream_t st) {
     Misc* misc = at<Misc>(s, s->misc);
     const int64_t npx = int64_t(W) * H;
     cudaMemsetAsync(misc->loss_acc, 0, sizeof(misc->loss_acc), st);
+    if (outlier_k > 0.f) {
+        RobustScratch* rs = at<RobustScratch>(s, s->coop);
+        cudaMemsetAsync(rs, 0, sizeof(RobustScratch), st);
+        const int grid = coop_sm_count();
+        if (grid <= 0) return;   // check_launch reports the device error
+        int64_t n = npx;
+        double* acc = misc->loss_acc;
+        void* args[] = {&color, &depth, &tc, &td, &alpha, &amin, &outlier_k, &n, &wc, &wd, &rs, &acc, &dc, &dd, &loss};
+        KTimer kt(s, KID_LOSS, st);
+        cudaLaunchCooperativeKernel(reinterpret_cast<void*>(loss_robust_kernel), dim3(grid), dim3(1024), args, 0, st);
+        return;
+    }
     const int blocks = int(std::min<int64_t>((npx + 255) / 256, 148 * 4));
     {
         KTimer kt(s, KID_LOSS, st);

@@ -34,6 +34,7 @@ class TrackConfig:
     sel_depth: float = 0.05
     pose_flags: int = GS_FLAG_POSE_COV_PATH
     observed_alpha: float | None = None   # NEXT-4 / reading C31: loss only where the render's alpha >= this
+    outlier_k: float = 0.0                # reading C32: drop pixels whose loss > k x median; 0 = off
 
 
 class Tracker:
@@ -58,14 +59,15 @@ class Tracker:
 
     def _iter(self, pipe, cam, P, n, V, tc, td, cfg: TrackConfig, mask=None):
         pipe.forward(P, n, V, cam, mask=mask, bin_flags=GS_FLAG_NO_HOST_SYNC, fwd_flags=0)
-        if cfg.observed_alpha is None:
+        if cfg.observed_alpha is None and cfg.outlier_k == 0:
             dc, dd = pipe.loss_l1(cam, tc, td, cfg.w_color, cfg.w_depth)
         else:   # "only rendered at previously observed areas"
             color, depth, alpha = pipe._imgs(cam)
             npx = cam.width * cam.height
             dc = pipe.dL_dcolor.view(-1)[:3 * npx].view(3, cam.height, cam.width)
             dd = pipe.dL_ddepth.view(-1)[:npx].view(cam.height, cam.width)
-            gs_loss_l1_masked(color, depth, tc, td, alpha, cfg.observed_alpha, cam.width, cam.height, cfg.w_color,
+            amin = cfg.observed_alpha if cfg.observed_alpha is not None else float("-inf")
+            gs_loss_l1_masked(color, depth, tc, td, alpha, amin, cfg.outlier_k, cam.width, cam.height, cfg.w_color,
                               cfg.w_depth, dc, dd, pipe.loss, pipe.ws)
         self.grad_pose.zero_()
         pipe.pose_grad(P, n, V, cam, dc, dd, self.grad_pose, flags=cfg.pose_flags)
@@ -103,7 +105,7 @@ class Tracker:
 
 @dataclasses.dataclass
 class FrontendConfig:
-    track: TrackConfig = dataclasses.field(default_factory=lambda: TrackConfig(observed_alpha=0.5))
+    track: TrackConfig = dataclasses.field(default_factory=lambda: TrackConfig(observed_alpha=0.5, outlier_k=10.0))
     kf_reliable: float = 0.7     # keyframe when the reliable share of valid pixels drops below this
     kf_max_gap: int = 30         # ... or this many frames after the last keyframe (mu_k)
     tau_alpha: float = 0.5       # Eq. 8 thresholds for "reliable"
@@ -113,7 +115,7 @@ class FrontendConfig:
 class Frontend:
     """Tracking front end: constant-velocity pose
     initialisation (gs_pose_extrapolate), coarse-to-fine tracking on previously observed areas
-    (gs_loss_l1_masked), and the keyframe rule (gs_frame_stats: reliable share of the observed
+    with the 10x-median pixel rejection (gs_loss_l1_masked, readings C31-C32), and the keyframe rule (gs_frame_stats: reliable share of the observed
     image, or a maximum frame gap). One host read per frame (the keyframe decision)."""
 
     def __init__(self, tracker: Tracker, cfg: FrontendConfig = FrontendConfig()):

@@ -165,7 +165,7 @@ def test_frontend_tracks_a_constant_velocity_trajectory():
     kh = max(key_cap_for(p, v.astype(np.float32), cam.half(), slack=1.6)[0] for v in traj)
     tr = Tracker(n, kc, kh, cam)
     P = to_dev(p)
-    fe = Frontend(tr, FrontendConfig(track=TrackConfig(iters_coarse=30, iters_fine=30, observed_alpha=0.5),
+    fe = Frontend(tr, FrontendConfig(track=TrackConfig(iters_coarse=30, iters_fine=30, observed_alpha=0.5, outlier_k=10.0),
                                      kf_max_gap=2))
     fe.add_pose(to_dev(traj[0]))
     fe.add_pose(to_dev(traj[1]), keyframe=False)

@@ -609,10 +609,41 @@ def test_frontend_kernels_parity():
     dc = torch.zeros(3, H, W, device="cuda")
     dd = torch.zeros(H, W, device="cuda")
     loss = torch.zeros(1, dtype=torch.float64, device="cuda")
-    g.gs_loss_l1_masked(to_dev(c), to_dev(d), to_dev(tc), to_dev(td), to_dev(a), 0.5, W, H, 0.9, 0.1, dc, dd, loss,
-                        pipe.ws)
+    g.gs_loss_l1_masked(to_dev(c), to_dev(d), to_dev(tc), to_dev(td), to_dev(a), 0.5, 0.0, W, H, 0.9, 0.1, dc, dd,
+                        loss, pipe.ws)
     torch.cuda.synchronize()
     o = oracle.loss_l1_masked(c, d, tc, td, a, 0.5)
+    np.testing.assert_allclose(dc.cpu().numpy(), o["dL_dcolor"], rtol=1e-6, atol=0)
+    np.testing.assert_allclose(dd.cpu().numpy(), o["dL_ddepth"], rtol=1e-6, atol=0)
+    assert abs(loss.item() - o["loss"]) <= 1e-6 * abs(o["loss"])
+
+
+@pytest.mark.parametrize("W,H,quant,frac_obs", [(64, 40, 0, 0.7), (1200, 680, 0, 0.9), (333, 217, 16, 0.6),
+                                                (64, 48, 0, 0.0), (1, 1, 0, 1.0)])
+def test_outlier_rejection_parity(W, H, quant, frac_obs):
+    """Reading C32: the cooperative radix-select median and the 10x rule against the oracle's
+    sort; quant > 0 quantises the images to multiples of 1/quant so that many pixel losses tie at the
+    median; frac_obs = 0 leaves nothing observed (zero gradient and loss); 1x1 is a single pixel."""
+    import paper_2311_11700_b200 as g
+    c, d = gi.random_images(W, H, 61)
+    tc, td = gi.random_images(W, H, 62)
+    rng = np.random.default_rng(63)
+    tc = np.where(rng.uniform(0, 1, tc.shape) < 0.95, np.clip(c + rng.normal(0, 0.02, c.shape), 0, 1), tc)
+    if quant:
+        c = np.round(c * quant) / quant
+        tc = np.round(tc * quant) / quant
+    c, tc = c.astype(np.float32), tc.astype(np.float32)
+    a = (rng.uniform(0, 1, (H, W)) < frac_obs).astype(np.float32)
+    pipe = g.RenderPipeline(16, 4096, W, H)
+    dc = torch.full((3, H, W), 7.0, device="cuda")
+    dd = torch.full((H, W), 7.0, device="cuda")
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    g.gs_loss_l1_masked(to_dev(c), to_dev(d), to_dev(tc), to_dev(td), to_dev(a), 0.5, 10.0, W, H, 0.9, 0.1, dc, dd,
+                        loss, pipe.ws)
+    torch.cuda.synchronize()
+    o = oracle.loss_l1_masked(c, d, tc, td, a, 0.5, 0.9, 0.1, outlier_k=10.0)
+    if frac_obs > 0 and W * H > 1:
+        assert 0 < (~o["kept"] & (a >= 0.5)).sum()   # the rule drops something
     np.testing.assert_allclose(dc.cpu().numpy(), o["dL_dcolor"], rtol=1e-6, atol=0)
     np.testing.assert_allclose(dd.cpu().numpy(), o["dL_ddepth"], rtol=1e-6, atol=0)
     assert abs(loss.item() - o["loss"]) <= 1e-6 * abs(o["loss"])

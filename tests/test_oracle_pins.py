@@ -775,3 +775,34 @@ def test_masked_loss_and_frame_stats_brute_force():
     rel = sum(1 for v in range(H) for u in range(W)
               if td[v, u] > 0 and a[v, u] >= 0.5 and abs(float(td[v, u]) - float(d[v, u])) <= np.float32(0.1))
     assert oracle.frame_stats(a, d, td, 0.5, 0.10) == (rel, int((td > 0).sum()), int((a >= 0.5).sum()))
+
+
+def test_outlier_rejection_brute_force():
+    """Reading C32: the lower median by Python's statistics.median_low over the observed
+    pixels' colour losses; a planted set of 5 gross outliers (colour off by 1.0 in every channel) is
+    dropped at k = 10 and nothing else is; the kept-pixel loss equals the masked loss with the
+    outliers made unobserved; k large enough keeps everything (reduces to reading C31)."""
+    import statistics
+    W, H = 16, 11
+    c, d = gi.random_images(W, H, 31)
+    tc = np.clip(c + np.random.default_rng(32).normal(0, 0.01, c.shape), 0, 1).astype(np.float32)
+    td = d.copy()
+    a = np.ones((H, W), np.float32)
+    a[0, :3] = 0.2
+    bad = [(2, 3), (5, 7), (9, 1), (10, 15), (4, 4)]
+    for v, u in bad:
+        tc[:, v, u] = np.where(c[:, v, u] > 0.5, c[:, v, u] - 1.0, c[:, v, u] + 1.0)
+    o = oracle.loss_l1_masked(c, d, tc, td, a, 0.5, outlier_k=10.0)
+    lp = [[sum(abs(float(c[ch, v, u]) - float(tc[ch, v, u])) for ch in range(3)) for u in range(W)] for v in range(H)]
+    med = statistics.median_low([lp[v][u] for v in range(H) for u in range(W) if a[v, u] >= 0.5])
+    drop = {(v, u) for v in range(H) for u in range(W) if a[v, u] >= 0.5 and lp[v][u] > 10 * med}
+    assert drop == set(bad)
+    assert set(zip(*np.nonzero(~o["kept"] & (a >= 0.5)))) == set(bad)
+    a2 = a.copy()
+    for v, u in bad:
+        a2[v, u] = 0.0
+    ref = oracle.loss_l1_masked(c, d, tc, td, a2, 0.5)
+    assert abs(o["loss"] - ref["loss"]) <= 1e-12 * ref["loss"]
+    np.testing.assert_array_equal(o["dL_dcolor"], ref["dL_dcolor"])
+    everything = oracle.loss_l1_masked(c, d, tc, td, a, 0.5, outlier_k=1e9)
+    assert everything["loss"] == oracle.loss_l1_masked(c, d, tc, td, a, 0.5)["loss"]
