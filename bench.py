@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--binsort", default="bucket", choices=["bucket", "keys"])
     ap.add_argument("--sh", type=int, default=0, choices=[0, 1],
                     help="colour model: 0 = RGB (BASELINE configs), 1 = degree-1 SH (NEXT-1, gs_project_sh)")
+    ap.add_argument("--opacity-radius", action="store_true",
+                    help="GS_FLAG_OPACITY_RADIUS (NEXT-4, reading C33): exact 1/255-reach tiling instead of the "
+                         "paper's 3-sigma box (a different render: not the BASELINE workload)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the iteration's calls on the stream instead of "
                                                              "replaying their CUDA graph")
@@ -204,14 +207,15 @@ def main_ours(args):
     P = torch.as_tensor(p, device=dev)
     V = torch.as_tensor(v, device=dev)
     bin_flags = g.GS_FLAG_BINSORT_KEYS if args.binsort == "keys" else 0
+    proj_flags = g.GS_FLAG_OPACITY_RADIUS if args.opacity_radius else 0
 
     # ---- setup (untimed): target = render of a second seeded scene at the same pose (config 2)
     probe = g.RenderPipeline(n, 1 << 26, cam.width, cam.height, dev)
     tgt_seed = cfg.target_seed if cfg.target_seed is not None else cfg.scene_seed + 1
     Pt = torch.as_tensor(gi.gaussians(n, tgt_seed, cfg.lo, cfg.hi), device=dev)
-    fr_t = probe.forward(Pt, n, V, cam, bin_flags=bin_flags)
+    fr_t = probe.forward(Pt, n, V, cam, bin_flags=bin_flags, proj_flags=proj_flags)
     tc, td = fr_t.color.clone(), fr_t.depth.clone()
-    fr = probe.forward(P, n, V, cam, bin_flags=bin_flags, fwd_flags=g.GS_FLAG_EXAMINED)
+    fr = probe.forward(P, n, V, cam, bin_flags=bin_flags, fwd_flags=g.GS_FLAG_EXAMINED, proj_flags=proj_flags)
     a = probe.arrays(n)
     K = fr.n_keys
     E_f = int(a["examined"].to(torch.int64).sum().item())
@@ -229,7 +233,7 @@ def main_ours(args):
 
     def step():   # gradients assigned (GS_FLAG_GRAD_ASSIGN, no zeroing pass); L1 loss fused into the backward
         pipe.iteration(P, n, V, cam, tc, td, grad, gpose, bin_flags=flags, fwd_flags=0, assign_grads=True,
-                       fused_loss=True)
+                       fused_loss=True, proj_flags=proj_flags)
 
     def barrier():
         if dist:
@@ -289,7 +293,8 @@ def main_ours(args):
            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Replica-shaped room scene, SURVEY.md §8(d))",
            "config": {"workload": f"config {args.config}: {cfg.name} {cam.width}x{cam.height}, {n} Gaussians, "
-                                  f"fwd+bwd L1 (0.9/0.1) iteration" + (", degree-1 SH colour" if args.sh else ""),
+                                  f"fwd+bwd L1 (0.9/0.1) iteration" + (", degree-1 SH colour" if args.sh else "")
+                                  + (", opacity-aware radius (C33)" if args.opacity_radius else ""),
                       "sh_degree": args.sh, "n_gaussians": n, "width": cam.width,
                       "height": cam.height, "keys": K, "visible": V_front, "on_screen": V_s, "E_f": E_f, "E_b": E_b,
                       "E_f_live": Lf, "E_b_live": Lb,
@@ -348,7 +353,7 @@ def main_ours(args):
             def iteration_on(b):
                 Pd, Vd, tcd, tdd = b
                 return lambda: pipe.iteration(Pd, n, Vd, cam, tcd, tdd, grad, gpose, bin_flags=flags, fwd_flags=0,
-                                              assign_grads=True, fused_loss=True)
+                                              assign_grads=True, fused_loss=True, proj_flags=proj_flags)
 
             # one captured graph per upload buffer set (as in the device-timed run)
             its = [iteration_on(b) for b in bufs]

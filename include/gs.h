@@ -67,6 +67,7 @@ enum {
     GS_FLAG_GRAD_ASSIGN = 32u,    /* gs_render_bwd / gs_pose_grad: ASSIGN instead of accumulate: every column
                                      [0, n) of grad_params is written (zero for off-screen Gaussians) and
                                      grad_pose = the pose gradient; no zeroing pass needed by the caller */
+    GS_FLAG_OPACITY_RADIUS = 64u, /* gs_project_ex: opacity-aware radius (reading C33) */
     GS_FLAG_BINSORT_EMIT_ONLY = 256u  /* testing: with GS_FLAG_BINSORT_KEYS, stop after key emission (the
                                      view's keys/vals then hold the unsorted index-order emission) */
 };
@@ -103,6 +104,18 @@ gs_status gs_project(const float* params, int64_t n, int64_t ld, const uint8_t* 
  * grad_params then has the same row count (14 or 23). Errors: GS_ERR_INVALID_ARG if sh_degree is
  * not 0 or 1, else as gs_project. */
 gs_status gs_project_sh(const float* params, int64_t n, int64_t ld, int32_t sh_degree,
+                        const uint8_t* mask /*nullable*/, const float* viewmat, const gs_camera* cam /*(host)*/,
+                        gs_ws* ws, void* stream);
+
+/* gs_project_ex — gs_project_sh with flags. GS_FLAG_OPACITY_RADIUS replaces the 3-sigma radius by
+ * the reach of the alpha >= 1/255 test (PAPER.md:27 skip rule applied to Eq. 4's
+ * alpha = o exp(-q/2); reading C33): q_o = fp32(2 ln(255 o)) evaluated in fp64 and rounded once;
+ * o <= 1/255 (q_o <= 0) culls the Gaussian (radius 0, no tiles), else r = ceil(sqrt(q_o lambda_max))
+ * (fp32, that order), and the rect, tile count and lists follow from r as before. Every pixel where
+ * alpha >= 1/255 lies inside the rect, so the tile lists hold exactly the contributing Gaussians
+ * and no more; the image differs from the 3-sigma one where the 3-sigma box cuts a Gaussian with
+ * o > e^4.5/255 ~ 0.35 short. Other flags: GS_ERR_INVALID_ARG. */
+gs_status gs_project_ex(const float* params, int64_t n, int64_t ld, int32_t sh_degree, uint32_t flags,
                         const uint8_t* mask /*nullable*/, const float* viewmat, const gs_camera* cam /*(host)*/,
                         gs_ws* ws, void* stream);
 

@@ -88,10 +88,16 @@ def sh_degree_of(params) -> int:
     return 1 if rows == 23 else 0
 
 
+def _mode(params, opacity_radius) -> int:
+    """Oracle C ABI mode word: colour model | (opacity-aware radius, reading C33) << 8."""
+    return sh_degree_of(params) | (256 if opacity_radius else 0)
+
+
 # ------------------------------------------------------------------------------------ O1
-def project(params, view, cam, precision="f32") -> dict:
+def project(params, view, cam, precision="f32", opacity_radius=False) -> dict:
     """O1 (Eq. 2-3): per-Gaussian projection. params [14][n] (RGB) or [23][n] (degree-1 SH, C29),
-    view [3][4]. rgb: the colour the blend uses (SH evaluated at the view direction)."""
+    view [3][4]. rgb: the colour the blend uses (SH evaluated at the view direction).
+    opacity_radius: reading C33's radius (the alpha >= 1/255 reach) instead of 3 sigma."""
     dt = _dtype(precision)
     params = np.ascontiguousarray(params, dt)
     view = np.ascontiguousarray(view, dt)
@@ -103,7 +109,7 @@ def project(params, view, cam, precision="f32") -> dict:
     fn = getattr(lib(), f"oracle_project_{precision}")
     fn(_p(params), ctypes.c_int64(n), ctypes.c_int64(n), _p(view), ctypes.byref(c), _p(out["mean2d"]),
        _p(out["conic"]), _p(out["depth"]), _p(out["radius"]), _p(out["rect"]), _p(out["tiles"]),
-       _p(out["depth_bits"]), _p(out["cov2d"]), ctypes.c_int32(sh_degree_of(params)), _p(out["rgb"]))
+       _p(out["depth_bits"]), _p(out["cov2d"]), ctypes.c_int32(_mode(params, opacity_radius)), _p(out["rgb"]))
     return out
 
 
@@ -129,7 +135,7 @@ def bin_sort(depth_bits, rect, tiles, cam) -> dict:
 
 # ------------------------------------------------------------------------------------ O3
 def forward(params, view, cam, precision="f32", pixels=None, replay_nlast=None, accum_weight=False,
-            flip_skip_ties=False) -> dict:
+            flip_skip_ties=False, opacity_radius=False) -> dict:
     """O3 (Eq. 4-5, cumulative opacity P:118). Full images unless `pixels` (linear ids) given.
     replay_nlast / flip_skip_ties: the parity tie rule's replays (reading R1)."""
     dt = _dtype(precision)
@@ -156,7 +162,7 @@ def forward(params, view, cam, precision="f32", pixels=None, replay_nlast=None, 
     getattr(lib(), f"oracle_forward_{precision}")(
         _p(params), ctypes.c_int64(n), ctypes.c_int64(n), _p(view), ctypes.byref(c), _p(pixels),
         ctypes.c_int64(npx), _p(rp), _p(color), _p(depth), _p(alpha), _p(n_last), _p(examined), _p(amb),
-        _p(h), _p(aw), ctypes.c_int32(1 if flip_skip_ties else 0), ctypes.c_int32(sh_degree_of(params)))
+        _p(h), _p(aw), ctypes.c_int32(1 if flip_skip_ties else 0), ctypes.c_int32(_mode(params, opacity_radius)))
     out = dict(color=color.reshape((3,) + shape), depth=depth.reshape(shape), alpha=alpha.reshape(shape),
                n_last=n_last.reshape(shape), examined=examined.reshape(shape), ambiguous=amb.reshape(shape),
                hash=int(h[0]))
@@ -167,7 +173,7 @@ def forward(params, view, cam, precision="f32", pixels=None, replay_nlast=None, 
 
 # ------------------------------------------------------------------------------------ O4
 def backward(params, view, cam, dL_dcolor, dL_ddepth, precision="f32", replay_nlast=None, qt_cov=True,
-             pixels=None) -> dict:
+             pixels=None, opacity_radius=False) -> dict:
     """O4 (Eq. 11, S1-S6): fp64 gradients for the 14 (RGB) or 23 (degree-1 SH) params, screen grads,
     and the pose.
 
@@ -192,7 +198,7 @@ def backward(params, view, cam, dL_dcolor, dL_ddepth, precision="f32", replay_nl
     getattr(lib(), f"oracle_backward_{precision}")(
         _p(params), ctypes.c_int64(n), ctypes.c_int64(n), _p(view), ctypes.byref(c), _p(dc), _p(dd), _p(rp),
         _p(gp), _p(gs), _p(tw), _p(twp), _p(qt), ctypes.c_int32(1 if qt_cov else 0), _p(px),
-        ctypes.c_int64(0 if px is None else px.shape[0]), ctypes.c_int32(sh_degree_of(params)))
+        ctypes.c_int64(0 if px is None else px.shape[0]), ctypes.c_int32(_mode(params, opacity_radius)))
     return dict(grad_params=gp, grad_screen=gs, pose_twist=tw, pose_twist_paper=twp,
                 pose_q=qt[0:4], pose_t=qt[4:7], pose_quat=qt[7:11])
 

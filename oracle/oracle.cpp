@@ -49,11 +49,13 @@ template <class R> struct Cam {
     R fx, fy, cx, cy, znear, dil;
     int W, H, GX, GY;
     int sh;                 // colour model: 0 = RGB rows 11-13 (reading C17), 1 = degree-1 SH (C29)
+    bool orad;              // radius: false = 3 sigma (C11), true = alpha >= 1/255 reach (C33)
     double bg[3];
-    explicit Cam(const OracleCam& c, int sh_degree = 0)
+    // mode = sh_degree | (opacity_radius << 8)
+    explicit Cam(const OracleCam& c, int mode = 0)
         : fx(R(c.fx)), fy(R(c.fy)), cx(R(c.cx)), cy(R(c.cy)), znear(R(c.znear)), dil(R(c.dil)),
           W(c.width), H(c.height), GX((c.width + TILE - 1) / TILE), GY((c.height + TILE - 1) / TILE),
-          sh(sh_degree) {
+          sh(mode & 0xff), orad(((mode >> 8) & 1) != 0) {
         for (int k = 0; k < 3; ++k) bg[k] = c.bg[k];
     }
 };
@@ -173,21 +175,42 @@ template <class R> static Proj<R> project_one(const R* p, const R* V, const Cam<
     g.ca = g.C * inv;
     g.cb = -(g.B * inv);
     g.cc = g.A * inv;
-    // 8. 3-sigma radius of the larger eigenvalue (reading C11), clamped to 2^24 px
+    // 8. 3-sigma radius of the larger eigenvalue (reading C11), clamped to 2^24 px; or (reading
+    //    C33) the reach of alpha = o exp(-q/2) >= 1/255: q <= q_o = 2 ln(255 o) (o <= 1/255 never
+    //    reaches the skip threshold: culled), with a margin q_m = q_o + 2e-3; r = ceil(sqrt(q_m
+    //    lambda_max)) and the ellipse's bounding box |x| <= sqrt(q_m A), |y| <= sqrt(q_m C)
     const R mid = R(0.5) * (g.A + g.C);
     const R lam1 = mid + std::sqrt(std::max(R(0.1), mid * mid - g.det));
-    R rf = std::ceil(R(3) * std::sqrt(lam1));
+    R rf, rx = 0, ry = 0;
+    if (cam.orad) {
+        const R qo = R(2.0 * std::log(255.0 * double(p[10])));
+        if (!(qo > R(0))) return g;   // radius 0, no tiles
+        const R qm = qo + R(2e-3f);
+        rf = std::ceil(std::sqrt(qm * lam1));
+        rx = std::sqrt(qm * g.A);
+        ry = std::sqrt(qm * g.C);
+    } else {
+        rf = std::ceil(R(3) * std::sqrt(lam1));
+    }
     if (!(rf < R(16777216))) rf = R(16777216);
     g.radius = int32_t(rf);
     // 9. projected mean m_i (pinhole)
     g.mx = cam.fx * tx + cam.cx;
     g.my = cam.fy * ty + cam.cy;
-    // 10. tile rect [xlo, xhi) x [ylo, yhi) of the 3-sigma box
-    const R r = R(g.radius);
-    g.xlo = clamp_tile(std::floor((g.mx - r) / R(TILE)), cam.GX);
-    g.xhi = clamp_tile(std::floor(((g.mx + r) + R(TILE - 1)) / R(TILE)), cam.GX);
-    g.ylo = clamp_tile(std::floor((g.my - r) / R(TILE)), cam.GY);
-    g.yhi = clamp_tile(std::floor(((g.my + r) + R(TILE - 1)) / R(TILE)), cam.GY);
+    // 10. tile rect [xlo, xhi) x [ylo, yhi): the 3DGS box of the 3-sigma radius, or (C33) the tiles
+    //     holding the integer pixels of [ceil(m - r), floor(m + r)] per axis
+    if (cam.orad) {
+        g.xlo = clamp_tile(std::floor(std::ceil(g.mx - rx) / R(TILE)), cam.GX);
+        g.xhi = clamp_tile(std::floor(std::floor(g.mx + rx) / R(TILE)) + R(1), cam.GX);
+        g.ylo = clamp_tile(std::floor(std::ceil(g.my - ry) / R(TILE)), cam.GY);
+        g.yhi = clamp_tile(std::floor(std::floor(g.my + ry) / R(TILE)) + R(1), cam.GY);
+    } else {
+        const R r = R(g.radius);
+        g.xlo = clamp_tile(std::floor((g.mx - r) / R(TILE)), cam.GX);
+        g.xhi = clamp_tile(std::floor(((g.mx + r) + R(TILE - 1)) / R(TILE)), cam.GX);
+        g.ylo = clamp_tile(std::floor((g.my - r) / R(TILE)), cam.GY);
+        g.yhi = clamp_tile(std::floor(((g.my + r) + R(TILE - 1)) / R(TILE)), cam.GY);
+    }
     g.tiles = uint32_t(std::max(0, g.xhi - g.xlo)) * uint32_t(std::max(0, g.yhi - g.ylo));
     g.in_front = true;
     return g;
@@ -551,8 +574,8 @@ void oracle_set_threads(int n) {
 #define ORACLE_PROJECT(SUF, R)                                                                             \
     int oracle_project_##SUF(const R* params, int64_t n, int64_t ld, const R* view, const OracleCam* oc,    \
                              R* mean2d, R* conic, R* depth, int32_t* radius, int32_t* rect,                \
-                             uint32_t* tiles, uint32_t* depth_bits, R* cov2d, int32_t sh_degree, R* rgb) { \
-        Cam<R> cam(*oc, sh_degree);                                                                        \
+                             uint32_t* tiles, uint32_t* depth_bits, R* cov2d, int32_t mode, R* rgb) { \
+        Cam<R> cam(*oc, mode);                                                                        \
         auto pj = project_all<R>(params, n, ld, view, cam);                                                \
         for (int64_t i = 0; i < n; ++i) {                                                                  \
             const Proj<R>& g = pj[size_t(i)];                                                              \
@@ -626,8 +649,8 @@ int64_t oracle_bin(const uint32_t* depth_bits, const int32_t* rect, const uint32
                              const int64_t* pixels, int64_t n_pix, const uint32_t* replay_nlast,          \
                              double* color, double* depth, double* alpha, uint32_t* n_last,               \
                              uint32_t* examined, uint8_t* ambiguous, uint64_t* hash,                      \
-                             double* accum_weight, int32_t flip_skip_ties, int32_t sh_degree) {           \
-        Cam<R> cam(*oc, sh_degree);                                                                       \
+                             double* accum_weight, int32_t flip_skip_ties, int32_t mode) {                \
+        Cam<R> cam(*oc, mode);                                                                       \
         auto pj = project_all<R>(params, n, ld, view, cam);                                               \
         auto order = depth_order(pj);                                                                     \
         const int64_t P = pixels ? n_pix : int64_t(cam.W) * cam.H;                                        \
@@ -673,8 +696,8 @@ ORACLE_FORWARD(f64, double)
                               const float* dLdC, const float* dLdD, const uint32_t* replay_nlast,              \
                               double* grad_params, double* grad_screen, double* pose_twist,                    \
                               double* pose_twist_paper, double* pose_qt, int32_t qt_cov,                       \
-                              const int64_t* pixels, int64_t n_pix, int32_t sh_degree) {                       \
-        Cam<R> cam(*oc, sh_degree);                                                                            \
+                              const int64_t* pixels, int64_t n_pix, int32_t mode) {                              \
+        Cam<R> cam(*oc, mode);                                                                            \
         auto pj = project_all<R>(params, n, ld, view, cam);                                                    \
         auto order = depth_order(pj);                                                                          \
         const int64_t P = int64_t(cam.W) * cam.H;                                                              \

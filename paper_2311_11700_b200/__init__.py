@@ -27,6 +27,7 @@ GS_FLAG_ACCUM_WEIGHT = 4
 GS_FLAG_EXAMINED = 8
 GS_FLAG_BINSORT_KEYS = 16
 GS_FLAG_GRAD_ASSIGN = 32
+GS_FLAG_OPACITY_RADIUS = 64
 GS_FLAG_BINSORT_EMIT_ONLY = 256
 GS_DENSIFY_ADD, GS_DENSIFY_PRUNE, GS_DENSIFY_SELECT, GS_DENSIFY_DEGENERATE = 1, 2, 3, 4
 
@@ -79,6 +80,8 @@ _SIGS = {
     "gs_frame_stats": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _F, _F, _P, _P]),
     "gs_loss_l1_masked": (ctypes.c_int, [_P, _P, _P, _P, _P, _F, _F, _I32, _I32, _F, _F, _P, _P, _P, ctypes.POINTER(gs_ws),
                                          _P]),
+    "gs_project_ex": (ctypes.c_int, [_P, _I64, _I64, _I32, _U32, _P, _P, ctypes.POINTER(gs_camera),
+                                     ctypes.POINTER(gs_ws), _P]),
     "gs_project_sh": (ctypes.c_int, [_P, _I64, _I64, _I32, _P, _P, ctypes.POINTER(gs_camera), ctypes.POINTER(gs_ws),
                                      _P]),
     "gs_bin_sort": (ctypes.c_int, [ctypes.POINTER(gs_ws), ctypes.POINTER(_I64), _U32, _P]),
@@ -225,6 +228,11 @@ def gs_project(params, n, ld, mask, viewmat, cam: gs_camera, ws: Workspace, stre
 def gs_project_sh(params, n, ld, sh_degree, mask, viewmat, cam: gs_camera, ws: Workspace, stream=None):
     _check(_lib.gs_project_sh(_ptr(params), n, ld, sh_degree, _ptr(mask), _ptr(viewmat), ctypes.byref(cam),
                               ctypes.byref(ws.state), _stream(stream)), "gs_project_sh")
+
+
+def gs_project_ex(params, n, ld, sh_degree, flags, mask, viewmat, cam: gs_camera, ws: Workspace, stream=None):
+    _check(_lib.gs_project_ex(_ptr(params), n, ld, sh_degree, flags, _ptr(mask), _ptr(viewmat), ctypes.byref(cam),
+                              ctypes.byref(ws.state), _stream(stream)), "gs_project_ex")
 
 
 def gs_bin_sort(ws: Workspace, flags: int = 0, stream=None) -> int:

@@ -144,13 +144,19 @@ gs_status gs_project(const float* params, int64_t n, int64_t ld, const uint8_t* 
 
 gs_status gs_project_sh(const float* params, int64_t n, int64_t ld, int32_t sh_degree, const uint8_t* mask,
                         const float* viewmat, const gs_camera* cam, gs_ws* ws, void* stream) {
+    return gs_project_ex(params, n, ld, sh_degree, 0u, mask, viewmat, cam, ws, stream);
+}
+
+gs_status gs_project_ex(const float* params, int64_t n, int64_t ld, int32_t sh_degree, uint32_t flags,
+                        const uint8_t* mask, const float* viewmat, const gs_camera* cam, gs_ws* ws, void* stream) {
     if (!ws_ok(ws)) return GS_ERR_INVALID_ARG;
     WsState* s = state(ws);
     if (n < 0 || n > s->n_cap || ld < n || (n > 0 && !params) || !viewmat || !cam_ok(s, cam) ||
-        (sh_degree != 0 && sh_degree != 1))
+        (sh_degree != 0 && sh_degree != 1) || (flags & ~uint32_t(GS_FLAG_OPACITY_RADIUS)))
         return GS_ERR_INVALID_ARG;
     s->n = n;
     s->sh_degree = sh_degree;
+    s->opacity_radius = (flags & GS_FLAG_OPACITY_RADIUS) ? 1 : 0;
     s->cam_w = cam->width;
     s->cam_h = cam->height;
     s->cam_gx = (cam->width + kTile - 1) / kTile;

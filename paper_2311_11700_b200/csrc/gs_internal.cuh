@@ -34,6 +34,7 @@ struct WsState {
     // run state
     int64_t n;                     // Gaussians of the last gs_project
     int32_t sh_degree;             // colour model of the last gs_project_sh (0 = RGB, 1 = degree-1 SH)
+    int32_t opacity_radius;        // last gs_project_ex used GS_FLAG_OPACITY_RADIUS (reading C33)
     int32_t pad_sh;
     int32_t cam_w, cam_h, cam_gx, cam_gy;   // image of the last gs_project
     uint64_t gen_project, gen_fwd; // generation counters (GS_ERR_STALE)

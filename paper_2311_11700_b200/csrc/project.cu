@@ -14,7 +14,7 @@ __device__ __forceinline__ int clamp_tile(float v, int hi) {
 
 __global__ void __launch_bounds__(256) project_kernel(
     const float* __restrict__ params, int64_t n, int64_t ld, const uint8_t* __restrict__ mask,
-    const float* __restrict__ viewmat, gs_camera cam, int GX, int GY, int sh,
+    const float* __restrict__ viewmat, gs_camera cam, int GX, int GY, int sh, int orad,
     float4* __restrict__ rec, uint32_t* __restrict__ depth_key, short4* __restrict__ rect,
     int32_t* __restrict__ radius_out, uint32_t* __restrict__ tiles_out) {
     __shared__ float V[12];
@@ -93,23 +93,47 @@ __global__ void __launch_bounds__(256) project_kernel(
         if (det > 0.f) {
             const float inv = 1.f / det;
             const float ca = C * inv, cb = -(B * inv), cc = A * inv;
-            // 8. radius
+            // 8. radius: 3 sigma, or the alpha >= 1/255 reach (GS_FLAG_OPACITY_RADIUS, reading C33):
+            //    q <= q_m = 2 ln(255 o) + 2e-3 (margin over the renderer's fp32 skip test); the
+            //    ellipse's bounding box is |x| <= sqrt(q_m A), |y| <= sqrt(q_m C)
             const float mid = 0.5f * (A + C);
             const float lam1 = mid + sqrtf(fmaxf(0.1f, mid * mid - det));
-            float rf = ceilf(3.f * sqrtf(lam1));
+            float rf, rx = 0.f, ry = 0.f;
+            bool reach = true;
+            if (orad) {
+                const float qo = float(2.0 * log(255.0 * double(p[10])));
+                reach = qo > 0.f;
+                const float qm = qo + 2e-3f;
+                rf = ceilf(sqrtf(qm * lam1));
+                rx = sqrtf(qm * A);
+                ry = sqrtf(qm * C);
+            } else {
+                rf = ceilf(3.f * sqrtf(lam1));
+            }
             if (!(rf < 16777216.f)) rf = 16777216.f;
-            radius = int(rf);
+            radius = reach ? int(rf) : 0;
             // 9. mean
             const float mx = cam.fx * tx + cam.cx;
             const float my = cam.fy * ty + cam.cy;
-            // 10. rect
-            const float r = float(radius);
-            const int xlo = clamp_tile(floorf((mx - r) / 16.f), GX);
-            const int xhi = clamp_tile(floorf(((mx + r) + 15.f) / 16.f), GX);
-            const int ylo = clamp_tile(floorf((my - r) / 16.f), GY);
-            const int yhi = clamp_tile(floorf(((my + r) + 15.f) / 16.f), GY);
-            rc = make_short4(short(xlo), short(xhi), short(ylo), short(yhi));
-            tiles = uint32_t(max(0, xhi - xlo)) * uint32_t(max(0, yhi - ylo));
+            // 10. rect: the 3DGS tile box of the radius, or (C33) the tiles holding the integer pixels
+            //     of the bounding box [ceil(m - r), floor(m + r)]
+            int xlo, xhi, ylo, yhi;
+            if (orad) {
+                xlo = clamp_tile(floorf(ceilf(mx - rx) / 16.f), GX);
+                xhi = clamp_tile(floorf(floorf(mx + rx) / 16.f) + 1.f, GX);
+                ylo = clamp_tile(floorf(ceilf(my - ry) / 16.f), GY);
+                yhi = clamp_tile(floorf(floorf(my + ry) / 16.f) + 1.f, GY);
+            } else {
+                const float r = float(radius);
+                xlo = clamp_tile(floorf((mx - r) / 16.f), GX);
+                xhi = clamp_tile(floorf(((mx + r) + 15.f) / 16.f), GX);
+                ylo = clamp_tile(floorf((my - r) / 16.f), GY);
+                yhi = clamp_tile(floorf(((my + r) + 15.f) / 16.f), GY);
+            }
+            if (reach) {
+                rc = make_short4(short(xlo), short(xhi), short(ylo), short(yhi));
+                tiles = uint32_t(max(0, xhi - xlo)) * uint32_t(max(0, yhi - ylo));
+            }
             // exactly scaled conic for the blend: A = -a/2, B = -b, C = -c/2 (gs_internal.cuh)
             r0 = make_float4(mx, my, -0.5f * ca, -cb);
             // r1.w: squared Mahalanobis reach q_max = 2 ln(255 o), where o exp(-q/2) = 1/255, plus a
@@ -158,7 +182,7 @@ void launch_project(WsState* s, const float* params, int64_t n, int64_t ld, cons
     const int blocks = int((n + 255) / 256);
     KTimer kt(s, KID_PROJECT, st);
     project_kernel<<<blocks, 256, 0, st>>>(params, n, ld, mask, viewmat, cam, GX, GY, s->sh_degree,
-                                           at<float4>(s, s->rec),
+                                           s->opacity_radius, at<float4>(s, s->rec),
                                            at<uint32_t>(s, s->depth_key), at<short4>(s, s->rect),
                                            at<int32_t>(s, s->radius), at<uint32_t>(s, s->tiles));
 }

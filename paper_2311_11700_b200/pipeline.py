@@ -8,7 +8,7 @@ import dataclasses
 import torch
 
 from . import (GS_FLAG_EXAMINED, GS_FLAG_GRAD_ASSIGN, GS_FLAG_POSE_COV_PATH, Workspace, gs_bin_sort, gs_loss_l1, gs_pose_grad,
-               gs_project_sh, gs_render_bwd, gs_render_bwd_l1, gs_render_fwd, make_camera)
+               gs_project_ex, gs_render_bwd, gs_render_bwd_l1, gs_render_fwd, make_camera)
 
 
 @dataclasses.dataclass
@@ -44,12 +44,13 @@ class RenderPipeline:
                 self.alpha.view(-1)[:npx].view(h, w))
 
     def forward(self, params, n, viewmat, cam, mask=None, bin_flags=0, fwd_flags=GS_FLAG_EXAMINED,
-                accum_weight=None, stream=None) -> Frame:
-        """params [14][ld] (RGB) or [23][ld] (degree-1 SH, gs_project_sh)."""
+                accum_weight=None, stream=None, proj_flags=0) -> Frame:
+        """params [14][ld] (RGB) or [23][ld] (degree-1 SH, gs_project_sh); proj_flags: gs_project_ex
+        flags (GS_FLAG_OPACITY_RADIUS)."""
         c = make_camera(cam)
         ld = params.shape[1]
         sh = {14: 0, 23: 1}[params.shape[0]]
-        gs_project_sh(params, n, ld, sh, mask, viewmat, c, self.ws, stream)
+        gs_project_ex(params, n, ld, sh, proj_flags, mask, viewmat, c, self.ws, stream)
         self.n_keys = gs_bin_sort(self.ws, bin_flags, stream)
         color, depth, alpha = self._imgs(cam)
         gs_render_fwd(self.ws, c, color, depth, alpha, accum_weight, fwd_flags, stream)
@@ -75,12 +76,14 @@ class RenderPipeline:
                      flags, stream)
 
     def iteration(self, params, n, viewmat, cam, tgt_color, tgt_depth, grad_params, grad_pose=None, bin_flags=0,
-                  fwd_flags=0, w_color=0.9, w_depth=0.1, stream=None, assign_grads=False, fused_loss=False):
+                  fwd_flags=0, w_color=0.9, w_depth=0.1, stream=None, assign_grads=False, fused_loss=False,
+                  proj_flags=0):
         """The headline fwd+bwd iteration. assign_grads: the gradients overwrite
         grad_params[:, :n] / grad_pose (GS_FLAG_GRAD_ASSIGN) instead of accumulating into them.
         fused_loss: gs_render_bwd_l1 (the L1 loss formed in the backward's pixel loads; dL/dC and
         dL/dD are not materialised) instead of gs_loss_l1 + gs_render_bwd. self.loss receives L."""
-        self.forward(params, n, viewmat, cam, bin_flags=bin_flags, fwd_flags=fwd_flags, stream=stream)
+        self.forward(params, n, viewmat, cam, bin_flags=bin_flags, fwd_flags=fwd_flags, stream=stream,
+                     proj_flags=proj_flags)
         flags = GS_FLAG_POSE_COV_PATH | (GS_FLAG_GRAD_ASSIGN if assign_grads else 0)
         if fused_loss:
             color, depth, _ = self._imgs(cam)

@@ -16,27 +16,27 @@ def to_dev(a, dtype=torch.float32):
     return torch.as_tensor(np.ascontiguousarray(a)).to(device="cuda", dtype=dtype)
 
 
-def key_cap_for(params, view, cam, slack=1.05):
-    pr = oracle.project(params, view, cam, "f32")
+def key_cap_for(params, view, cam, slack=1.05, opacity_radius=False):
+    pr = oracle.project(params, view, cam, "f32", opacity_radius=opacity_radius)
     k = int(pr["tiles"].astype(np.int64).sum())
     return max(int(k * slack) + 1024, 4096), pr
 
 
-def run_forward(params, view, cam, flags_bin=0, key_cap=None, fwd_flags=None):
+def run_forward(params, view, cam, flags_bin=0, key_cap=None, fwd_flags=None, proj_flags=0):
     import paper_2311_11700_b200 as g
     n = params.shape[1]
     if key_cap is None:
-        key_cap, _ = key_cap_for(params, view, cam)
+        key_cap, _ = key_cap_for(params, view, cam, opacity_radius=bool(proj_flags & g.GS_FLAG_OPACITY_RADIUS))
     pipe = g.RenderPipeline(max(n, 1), key_cap, cam.width, cam.height)
     P = to_dev(params)
     V = to_dev(view)
     fr = pipe.forward(P, n, V, cam, bin_flags=flags_bin,
-                      fwd_flags=g.GS_FLAG_EXAMINED if fwd_flags is None else fwd_flags)
+                      fwd_flags=g.GS_FLAG_EXAMINED if fwd_flags is None else fwd_flags, proj_flags=proj_flags)
     torch.cuda.synchronize()
     return pipe, P, V, fr
 
 
-def compare_images(gpu, orc, cam, params, view, label=""):
+def compare_images(gpu, orc, cam, params, view, label="", opacity_radius=False):
     """Tolerance compare with the threshold-tie rule: a pixel outside tolerance is
     accepted only if the oracle replayed with the GPU's n_last is within tolerance AND the oracle
     flagged one of its own decisions as within 1e-5 relative of its threshold."""
@@ -49,12 +49,13 @@ def compare_images(gpu, orc, cam, params, view, label=""):
     ties = 0
     if bad.size:
         nl = gpu["n_last"].cpu().numpy().reshape(-1)[bad]
-        rp = oracle.forward(params, view, cam, "f32", pixels=bad, replay_nlast=nl)
+        rp = oracle.forward(params, view, cam, "f32", pixels=bad, replay_nlast=nl, opacity_radius=opacity_radius)
         e2 = np.maximum.reduce([np.abs(gc.reshape(3, -1)[:, bad] - rp["color"]).max(0),
                                 np.abs(gd.reshape(-1)[bad] - rp["depth"]), np.abs(ga.reshape(-1)[bad] - rp["alpha"])])
         amb = orc["ambiguous"].reshape(-1)[bad]
         # a flipped alpha-vs-1/255 decision cannot be replayed by n_last: replay it the other way
-        rf = oracle.forward(params, view, cam, "f32", pixels=bad, replay_nlast=nl, flip_skip_ties=True)
+        rf = oracle.forward(params, view, cam, "f32", pixels=bad, replay_nlast=nl, flip_skip_ties=True,
+                            opacity_radius=opacity_radius)
         e3 = np.maximum.reduce([np.abs(gc.reshape(3, -1)[:, bad] - rf["color"]).max(0),
                                 np.abs(gd.reshape(-1)[bad] - rf["depth"]), np.abs(ga.reshape(-1)[bad] - rf["alpha"])])
         e2 = np.minimum(e2, e3)

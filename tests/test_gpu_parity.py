@@ -647,3 +647,34 @@ def test_outlier_rejection_parity(W, H, quant, frac_obs):
     np.testing.assert_allclose(dc.cpu().numpy(), o["dL_dcolor"], rtol=1e-6, atol=0)
     np.testing.assert_allclose(dd.cpu().numpy(), o["dL_ddepth"], rtol=1e-6, atol=0)
     assert abs(loss.item() - o["loss"]) <= 1e-6 * abs(o["loss"])
+
+
+# ------------------------------------------------------------------ opacity-aware radius (NEXT-4, C33)
+@pytest.mark.parametrize("c", CFGS)
+def test_opacity_radius_parity(c):
+    """GS_FLAG_OPACITY_RADIUS: radius, rect, tile counts and the tile lists bit-exact with the oracle;
+    images within tolerance (threshold-tie rule); at configs 0-1 the gradients too."""
+    import paper_2311_11700_b200 as g
+    cfg, p, v = scene(c)
+    pipe, P, V, fr = run_forward(p, v, cfg.cam, proj_flags=g.GS_FLAG_OPACITY_RADIUS)
+    a = pipe.arrays(p.shape[1])
+    o = oracle.project(p, v, cfg.cam, "f32", opacity_radius=True)
+    assert np.array_equal(a["radius"].cpu().numpy(), o["radius"])
+    assert np.array_equal(a["tiles"].cpu().numpy().view(np.uint32), o["tiles"])
+    assert np.array_equal(a["rect"].cpu().numpy().astype(np.int32).T, o["rect"])
+    ob = oracle.bin_sort(o["depth_bits"], o["rect"], o["tiles"], cfg.cam)
+    assert fr.n_keys == ob["n_keys"]
+    assert np.array_equal(a["vals"].cpu().numpy().view(np.uint32), ob["vals"])
+    assert np.array_equal(a["ranges"].cpu().numpy().view(np.uint32), ob["ranges"])
+    if c == 2:
+        return
+    of = oracle.forward(p, v, cfg.cam, "f32", opacity_radius=True)
+    compare_images(dict(color=fr.color, depth=fr.depth, alpha=fr.alpha, n_last=a["n_last"]), of, cfg.cam, p, v,
+                   f"orad cfg{c}", opacity_radius=True)
+    dc, dd = gi.upstream(cfg.cam.width, cfg.cam.height, 70 + c)
+    gp, gpose, _ = _gpu_backward(pipe, P, V, cfg, dc, dd)
+    ob = oracle.backward(p, v, cfg.cam, dc, dd, "f32", replay_nlast=a["n_last"].cpu().numpy(),
+                         opacity_radius=True)
+    bad = grad_close(gp, ob["grad_params"])
+    assert bad.mean() <= 1e-3, bad.mean()
+    np.testing.assert_allclose(gpose, ob["pose_twist"], rtol=2e-3, atol=1e-6)

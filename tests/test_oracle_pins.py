@@ -806,3 +806,112 @@ def test_outlier_rejection_brute_force():
     np.testing.assert_array_equal(o["dL_dcolor"], ref["dL_dcolor"])
     everything = oracle.loss_l1_masked(c, d, tc, td, a, 0.5, outlier_k=1e9)
     assert everything["loss"] == oracle.loss_l1_masked(c, d, tc, td, a, 0.5)["loss"]
+
+
+def test_opacity_radius_box_holds_every_contributing_pixel():
+    """Reading C33: with the opacity-aware radius every pixel where the closed-form footprint
+    (library rotation, numeric Jacobian) reaches alpha >= 1/255 lies in a tile of the rect; the
+    rect holds no tile without such a pixel beyond the box's own rounding (each edge tile meets the
+    ellipse's bounding box); o <= 1/255 is culled; on an isotropic footprint the radius is
+    ceil(sqrt((2 ln(255 o) + 2e-3) lambda))."""
+    rng = np.random.default_rng(11)
+    cam = gi.CAM_TUM
+    view = small_pose(5, rot_deg=10, trans=0.2)
+    uu, vv = np.meshgrid(np.arange(cam.width), np.arange(cam.height))
+    for k in range(40):
+        z = rng.uniform(1.0, 5)
+        mean = np.array([rng.uniform(-0.4, 0.4) * z, rng.uniform(-0.3, 0.3) * z, z])
+        mean_w = view[:, :3].T @ (mean - view[:, 3])
+        scale = np.exp(rng.normal(-3.5, 0.6, 3))
+        q = rng.normal(size=4)
+        o = [0.003, 0.0039, 0.004, 0.05, 0.3, 0.7, 0.99][k % 7]
+        p = single(mean_w, scale, q, o, [0, 0, 0])
+        pr = oracle.project(p, view, cam, "f32", opacity_radius=True)
+        if o <= 1 / 255:
+            assert pr["tiles"][0] == 0 and pr["radius"][0] == 0
+            continue
+        m, Sp, _ = ewa_reference(mean_w, scale, q / np.linalg.norm(q), view, cam)
+        d = np.stack([m[0] - uu, m[1] - vv], -1)
+        Q = np.linalg.inv(Sp)
+        qq = np.einsum("...i,ij,...j->...", d, Q, d)
+        hit = o * np.exp(-0.5 * qq) >= 1 / 255
+        xlo, xhi, ylo, yhi = pr["rect"][:, 0]
+        tx, ty = uu // 16, vv // 16
+        inside = (tx >= xlo) & (tx < xhi) & (ty >= ylo) & (ty < yhi)
+        assert not (hit & ~inside).any(), k
+        if hit.any():   # edge tiles meet the bounding box of the 1/255 ellipse (plus the margin)
+            qm = 2 * math.log(255 * o) + 2e-3
+            rx, ry = math.sqrt(qm * Sp[0, 0]), math.sqrt(qm * Sp[1, 1])
+            assert xlo * 16 <= m[0] + rx + 1e-3 and (xhi - 1) * 16 + 15 >= m[0] - rx - 1e-3
+            assert xlo * 16 + 16 > m[0] - rx - 1 and (xhi - 1) * 16 <= m[0] + rx + 1e-3
+            assert ylo * 16 + 16 > m[1] - ry - 1 and (yhi - 1) * 16 <= m[1] + ry + 1e-3
+    # isotropic: Sigma' = (f s / z)^2 I + 0.3 I at the image centre; lambda_max carries the
+    # rasterizer's floor sqrt(max(0.1, mid^2 - det)) = sqrt(0.1) (reading C11)
+    cam0 = gi.CAM_TINY
+    p = single([0.0, 0.0, 2.0], [0.05, 0.05, 0.05], [1, 0, 0, 0], 0.5, [0, 0, 0])
+    lam = (60.0 * 0.05 / 2.0) ** 2 + 0.3 + math.sqrt(0.1)
+    pr = oracle.project(p, gi.identity_view().astype(np.float64), cam0, "f64", opacity_radius=True)
+    assert pr["radius"][0] == math.ceil(math.sqrt((2 * math.log(255 * 0.5) + 2e-3) * lam))
+
+
+def test_opacity_radius_render_equals_untiled_brute_force():
+    """Reading C33: with exact tiling the tiled render equals a brute-force blend that visits every
+    Gaussian at every pixel in depth order (no tiles, no rect): the image no longer depends on the
+    tile grid. A scene of large, opaque Gaussians placed so that the 3-sigma tile boxes cut some
+    of them short shows that the 3-sigma render does depend on it."""
+    cam = dataclasses.replace(gi.CAM_TINY, bg=(0.2, 0.3, 0.4))
+    rng = np.random.default_rng(3)
+    ps = []
+    for k in range(10):
+        z = 1.5 + 0.3 * k
+        ps.append(single([rng.uniform(-0.4, 0.4) * z, rng.uniform(-0.3, 0.3) * z, z],
+                         np.exp(rng.normal(-2.8, 0.3, 3)) * z / 2, rng.normal(size=4), rng.uniform(0.6, 0.99),
+                         rng.uniform(0, 1, 3)))
+    p = np.concatenate(ps, 1)
+    view = gi.identity_view().astype(np.float64)
+    f = oracle.forward(p, view, cam, "f64", opacity_radius=True)
+    f3 = oracle.forward(p, view, cam, "f64")
+    pr = oracle.project(p, view, cam, "f64")
+    order = np.argsort(pr["depth"], kind="stable")
+    H, W = cam.height, cam.width
+    col = np.zeros((3, H, W))
+    dep = np.zeros((H, W))
+    alp = np.zeros((H, W))
+    for v in range(H):
+        for u in range(W):
+            T, c, dd = 1.0, np.zeros(3), 0.0
+            for i in order:
+                if pr["depth"][i] <= cam.znear:
+                    continue
+                a = footprint(p, i, u, v, cam, view)
+                if a < 1 / 255:
+                    continue
+                if T * (1 - a) < 1e-4:
+                    break
+                c += p[11:14, i] * a * T
+                dd += pr["depth"][i] * a * T
+                T *= 1 - a
+            col[:, v, u] = c + np.array(cam.bg) * T
+            dep[v, u] = dd
+            alp[v, u] = 1 - T
+    np.testing.assert_allclose(f["color"], col, atol=2e-6)
+    np.testing.assert_allclose(f["depth"], dep, atol=2e-5)
+    np.testing.assert_allclose(f["alpha"], alp, atol=2e-6)
+    assert np.abs(f3["alpha"] - alp).max() > 1e-3   # the 3-sigma box cuts contributions
+
+
+def test_opacity_radius_leaves_low_opacity_renders_unchanged():
+    """Reading C33: for o <= 0.3 < e^4.5/255 the 1/255 reach lies inside 3 sigma, so the opacity
+    radius drops only Gaussians and tiles that never pass the skip test: the image is identical to
+    the 3-sigma render (n_last, a position in the shorter list, differs), with fewer keys."""
+    cfg = gi.CONFIGS[1]
+    p = cfg.scene().copy()
+    p[10] = np.minimum(p[10], 0.3)
+    v = cfg.view()
+    a = oracle.forward(p, v, cfg.cam, "f32")
+    b = oracle.forward(p, v, cfg.cam, "f32", opacity_radius=True)
+    for k in ("color", "depth", "alpha"):
+        assert np.array_equal(a[k], b[k]), k
+    ka = oracle.project(p, v, cfg.cam, "f32")["tiles"].astype(np.int64).sum()
+    kb = oracle.project(p, v, cfg.cam, "f32", opacity_radius=True)["tiles"].astype(np.int64).sum()
+    assert kb < 0.8 * ka, (kb, ka)
