@@ -193,6 +193,15 @@ gs_status gs_pose_step(float* viewmat, const double* grad_pose, float* m6, float
  * out may alias neither input. */
 gs_status gs_pose_extrapolate(const float* view_prev2, const float* view_prev, float* view_out, void* stream);
 
+/* gs_image_half — the coarse stage's H/2 x W/2 target ("a coarse image with resolution
+ * H/2 x W/2"; reading C12's camera: half pixel (u, v) covers full pixels 2u..2u+1 x 2v..2v+1):
+ * colour_half = ((c00 + c01) + (c10 + c11)) * 0.25 per channel (fp32, that order), depth_half = the
+ * mean of the valid (> 0) depths among the four in the order 00, 01, 10, 11, or 0 if none. color
+ * [3][H][W], depth [H][W] in; color_half [3][H/2][W/2], depth_half [H/2][W/2] out (floor sizes;
+ * an odd last row / column is dropped). W, H >= 2, else GS_ERR_INVALID_ARG. */
+gs_status gs_image_half(const float* color, const float* depth, int32_t W, int32_t H, float* color_half,
+                        float* depth_half, void* stream);
+
 /* gs_frame_stats — the keyframe rule's measurement ("the proportion of the currently
  * observed image's reliable region"): counts[0] = pixels with valid target
  * depth that are reliable by Eq. 8 (alpha >= tau_alpha and |D* - D| <= tau_depth), counts[1] = pixels

@@ -392,6 +392,26 @@ def pose_extrapolate(view_prev2, view_prev) -> np.ndarray:
     return (T2 @ np.linalg.inv(T1) @ T2)[:3]
 
 
+def image_half(color, depth):
+    """PAPER.md:173 coarse image (reading C12's half camera): 2x2 mean of colour in the order
+    ((c00 + c01) + (c10 + c11)) * 0.25 in fp32; depth = mean of the valid samples (00, 01, 10, 11)."""
+    c = np.asarray(color, np.float32)
+    d = np.asarray(depth, np.float32)
+    H, W = d.shape
+    Hh, Wh = H // 2, W // 2
+    c = c[:, :2 * Hh, :2 * Wh]
+    d = d[:2 * Hh, :2 * Wh]
+    ch = ((c[:, 0::2, 0::2] + c[:, 0::2, 1::2]) + (c[:, 1::2, 0::2] + c[:, 1::2, 1::2])) * np.float32(0.25)
+    s = np.zeros((Hh, Wh), np.float32)
+    cnt = np.zeros((Hh, Wh), np.int32)
+    for dv, du in ((0, 0), (0, 1), (1, 0), (1, 1)):
+        x = d[dv::2, du::2]
+        s = np.where(x > 0, s + x, s).astype(np.float32)
+        cnt += x > 0
+    dh = np.where(cnt > 0, s / np.maximum(cnt, 1).astype(np.float32), np.float32(0)).astype(np.float32)
+    return ch.astype(np.float32), dh
+
+
 def frame_stats(alpha, depth, tgt_depth, tau_alpha=0.5, tau_depth=0.10) -> tuple[int, int, int]:
     """Keyframe rule measurement: (reliable valid pixels by Eq. 8's complement, valid pixels,
     observed pixels alpha >= tau_alpha). Comparisons in fp32."""

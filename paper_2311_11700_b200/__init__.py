@@ -77,6 +77,7 @@ _SIGS = {
     "gs_render_bwd_l1": (ctypes.c_int, [_P, _I64, _I64, _P, ctypes.POINTER(gs_ws), ctypes.POINTER(gs_camera), _P, _P,
                                         _P, _P, _F, _F, _P, _P, _P, _U32, _P]),
     "gs_pose_extrapolate": (ctypes.c_int, [_P, _P, _P, _P]),
+    "gs_image_half": (ctypes.c_int, [_P, _P, _I32, _I32, _P, _P, _P]),
     "gs_frame_stats": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _F, _F, _P, _P]),
     "gs_loss_l1_masked": (ctypes.c_int, [_P, _P, _P, _P, _P, _F, _F, _I32, _I32, _F, _F, _P, _P, _P, ctypes.POINTER(gs_ws),
                                          _P]),
@@ -282,6 +283,11 @@ def gs_loss_l1(color, depth, tgt_color, tgt_depth, width, height, w_color, w_dep
 def gs_pose_extrapolate(view_prev2, view_prev, view_out, stream=None):
     _check(_lib.gs_pose_extrapolate(_ptr(view_prev2), _ptr(view_prev), _ptr(view_out), _stream(stream)),
            "gs_pose_extrapolate")
+
+
+def gs_image_half(color, depth, width, height, color_half, depth_half, stream=None):
+    _check(_lib.gs_image_half(_ptr(color), _ptr(depth), width, height, _ptr(color_half), _ptr(depth_half),
+                              _stream(stream)), "gs_image_half")
 
 
 def gs_frame_stats(alpha, depth, target_depth, width, height, tau_alpha, tau_depth, counts, stream=None):

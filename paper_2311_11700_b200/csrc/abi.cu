@@ -271,6 +271,13 @@ gs_status gs_pose_extrapolate(const float* view_prev2, const float* view_prev, f
     return check_launch(nullptr, "gs_pose_extrapolate");
 }
 
+gs_status gs_image_half(const float* color, const float* depth, int32_t W, int32_t H, float* color_half,
+                        float* depth_half, void* stream) {
+    if (!color || !depth || !color_half || !depth_half || W < 2 || H < 2) return GS_ERR_INVALID_ARG;
+    launch_image_half(color, depth, W, H, color_half, depth_half, static_cast<cudaStream_t>(stream));
+    return check_launch(nullptr, "gs_image_half");
+}
+
 gs_status gs_adam_step(float* params_raw, float* params_act, const float* grad_act, float* m, float* v, int64_t n,
                        int64_t ld, const float lr[14], int32_t step, float b1, float b2, float eps, void* stream) {
     if ((n > 0 && (!params_raw || !params_act || !grad_act || !m || !v)) || !lr || n < 0 || ld < n || step < 1)

@@ -424,6 +424,41 @@ __global__ void pose_extrapolate_kernel(const float* __restrict__ t1, const floa
     }
 }
 
+// 2x2 mean of the RGB-D frame for the coarse stage (reading C12's half-resolution camera: half
+// pixel (u, v) covers full pixels 2u..2u+1 x 2v..2v+1): colour ((c00 + c01) + (c10 + c11)) * 0.25,
+// depth the mean of the valid (> 0) samples in the order 00, 01, 10, 11, else 0.
+__global__ void image_half_kernel(const float* __restrict__ c, const float* __restrict__ d, int W, int H,
+                                  float* __restrict__ ch, float* __restrict__ dh) {
+    const int Wh = W / 2, Hh = H / 2;
+    const int64_t nh = int64_t(Wh) * Hh, n = int64_t(W) * H;
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nh; q += int64_t(gridDim.x) * blockDim.x) {
+        const int v = int(q / Wh), u = int(q - int64_t(v) * Wh);
+        const int64_t p00 = int64_t(2 * v) * W + 2 * u, p10 = p00 + W;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float* ck = c + k * n;
+            ch[k * nh + q] = __fmul_rn(__fadd_rn(__fadd_rn(ck[p00], ck[p00 + 1]), __fadd_rn(ck[p10], ck[p10 + 1])), 0.25f);
+        }
+        const float ds[4] = {d[p00], d[p00 + 1], d[p10], d[p10 + 1]};
+        float s = 0.f;
+        int cnt = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (ds[k] > 0.f) {
+                s = __fadd_rn(s, ds[k]);
+                ++cnt;
+            }
+        dh[q] = cnt ? __fdiv_rn(s, float(cnt)) : 0.f;
+    }
+}
+
+void launch_image_half(const float* c, const float* d, int32_t W, int32_t H, float* ch, float* dh, cudaStream_t st) {
+    const int64_t nh = int64_t(W / 2) * (H / 2);
+    if (nh == 0) return;
+    const int blocks = int(std::min<int64_t>((nh + 255) / 256, 148 * 8));
+    image_half_kernel<<<blocks, 256, 0, st>>>(c, d, W, H, ch, dh);
+}
+
 void launch_pose_extrapolate(const float* t1, const float* t2, float* out, cudaStream_t st) {
     pose_extrapolate_kernel<<<1, 32, 0, st>>>(t1, t2, out);
 }

@@ -92,25 +92,32 @@ class ShardedMapper:
         self.grad = torch.zeros_like(params)
         self.n = n
         self.n_dev = torch.tensor([n], dtype=torch.int64, device=params.device)
-        self.keyframes = keyframes
-        self.local = shard(len(keyframes), self.world, self.rank)
         self.cam = cam
         self.cm = make_camera(cam)
         self.pipe = RenderPipeline(self.cap, key_cap, cam.width, cam.height, params.device)
         self.w_color, self.w_depth = w_color, w_depth
         self.max_add = max_add_per_kf
         self.densify = densify
-        L = len(self.local)
-        self.cand = torch.zeros(L, 14, max_add_per_kf, device=params.device)
-        self.counts = torch.zeros(L, dtype=torch.int64, device=params.device)
         self.it = 0
-        # bundle adjustment state (Eq. 13): per local keyframe pose gradient and Adam moments
         self.ba_iters = ba_iters
         self.lr_rho, self.lr_phi = lr_rho, lr_phi
-        self.gpose = torch.zeros(L, 6, dtype=torch.float64, device=params.device)
-        self.pm = torch.zeros(L, 6, device=params.device)
-        self.pv = torch.zeros(L, 6, device=params.device)
         self.pose_step = 0
+        self.set_keyframes(keyframes)
+
+    def set_keyframes(self, keyframes: list[Keyframe]):
+        """(Re)assign the keyframe set (the SLAM driver's window, slam.py); per-keyframe buffers
+        follow the local count."""
+        dev = self.P.device
+        self.keyframes = keyframes
+        self.local = shard(len(keyframes), self.world, self.rank)
+        L = len(self.local)
+        if getattr(self, "cand", None) is None or self.cand.shape[0] != L:
+            self.cand = torch.zeros(L, 14, self.max_add, device=dev)
+            self.counts = torch.zeros(L, dtype=torch.int64, device=dev)
+            # bundle adjustment state (Eq. 13): per local keyframe pose gradient and Adam moments
+            self.gpose = torch.zeros(L, 6, dtype=torch.float64, device=dev)
+            self.pm = torch.zeros(L, 6, device=dev)
+            self.pv = torch.zeros(L, 6, device=dev)
 
     def poses_active(self) -> bool:
         """Eq. 13: poses are optimised only in the second half of the BA iterations."""

@@ -678,3 +678,16 @@ def test_opacity_radius_parity(c):
     bad = grad_close(gp, ob["grad_params"])
     assert bad.mean() <= 1e-3, bad.mean()
     np.testing.assert_allclose(gpose, ob["pose_twist"], rtol=2e-3, atol=1e-6)
+
+
+@pytest.mark.parametrize("W,H", [(640, 480), (1200, 680), (37, 21)])
+def test_image_half_bitexact(W, H):
+    import paper_2311_11700_b200 as g
+    c, d = gi.random_images(W, H, 91)
+    d[np.random.default_rng(92).uniform(0, 1, d.shape) < 0.3] = 0
+    ch = torch.zeros(3, H // 2, W // 2, device="cuda")
+    dh = torch.zeros(H // 2, W // 2, device="cuda")
+    g.gs_image_half(to_dev(c), to_dev(d), W, H, ch, dh)
+    torch.cuda.synchronize()
+    oc, od = oracle.image_half(c, d)
+    assert np.array_equal(ch.cpu().numpy(), oc) and np.array_equal(dh.cpu().numpy(), od)

@@ -915,3 +915,32 @@ def test_opacity_radius_leaves_low_opacity_renders_unchanged():
     ka = oracle.project(p, v, cfg.cam, "f32")["tiles"].astype(np.int64).sum()
     kb = oracle.project(p, v, cfg.cam, "f32", opacity_radius=True)["tiles"].astype(np.int64).sum()
     assert kb < 0.8 * ka, (kb, ka)
+
+
+def test_image_half_brute_force():
+    """PAPER.md:173 coarse image, reading C12: pure-Python 2x2 loops in fp32, odd sizes drop the last
+    row / column, invalid (zero) depths excluded from the mean; a constant image stays constant."""
+    W, H = 9, 7
+    c, d = gi.random_images(W, H, 41)
+    d[1, 2] = 0.0
+    d[0, 0] = d[0, 1] = d[1, 0] = d[1, 1] = 0.0
+    ch, dh = oracle.image_half(c, d)
+    assert ch.shape == (3, 3, 4) and dh.shape == (3, 4)
+    f = np.float32
+    for v in range(3):
+        for u in range(4):
+            for k in range(3):
+                want = f(f(f(c[k, 2 * v, 2 * u]) + f(c[k, 2 * v, 2 * u + 1])) +
+                         f(f(c[k, 2 * v + 1, 2 * u]) + f(c[k, 2 * v + 1, 2 * u + 1]))) * f(0.25)
+                assert ch[k, v, u] == want
+            vals = [d[2 * v + a, 2 * u + b] for a in (0, 1) for b in (0, 1) if d[2 * v + a, 2 * u + b] > 0]
+            want = f(0)
+            if vals:
+                s = f(0)
+                for x in vals:
+                    s = f(s + f(x))
+                want = f(s / f(len(vals)))
+            assert dh[v, u] == want
+    assert dh[0, 0] == 0
+    ch, dh = oracle.image_half(np.full((3, 4, 6), 0.3, np.float32), np.full((4, 6), 2.5, np.float32))
+    assert (ch == np.float32(0.3)).all() and (dh == np.float32(2.5)).all()
