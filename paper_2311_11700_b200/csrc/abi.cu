@@ -77,6 +77,7 @@ static void carve(WsState* s, Carver& c) {
     // tile totals and per-(segment, tile) sums
     s->coop = c.take((uint64_t(kCoopPasses) * kCoopGridMax * kCoopBins + kCoopPasses * kCoopBins + kCoopGridMax +
                       uint64_t(tiles) * (1 + kCoopSegs)) * 4);
+    s->tile_order = c.take(uint64_t(tiles) * 4);                     // backward LPT tile order
 }
 
 static bool ws_ok(const gs_ws* ws) { return ws && state(ws)->magic == kMagic; }

@@ -30,7 +30,7 @@ struct WsState {
     Region rec, depth_key, rect, radius, tiles, offsets, sgrad, scan_state,
         keys0, keys1, vals0, vals1, ranges, t_final, n_last, examined, sort_hist, sort_look,
         misc, scratch, scratch14, dkey_sorted, dval_sorted, chunk_hist, chunk_mat, srect, tile_tot, pose_part,
-        onlist, live_cnt, svals, coop;
+        onlist, live_cnt, svals, coop, tile_order;
     // run state
     int64_t n;                     // Gaussians of the last gs_project
     int32_t sh_degree;             // colour model of the last gs_project_sh (0 = RGB, 1 = degree-1 SH)

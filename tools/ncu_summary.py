@@ -14,7 +14,8 @@ import sys
 NAMES = {"render_bwd_kernel": "render_bwd_tiles", "render_fwd2_kernel": "render_fwd", "render_fwd_kernel": "render_fwd",
          "bucket_emit_kernel": "bucket_emit", "gaussian_bwd_kernel": "gaussian_bwd", "onesweep_pass_kernel": "sort_pass",
          "project_kernel": "project", "chunk_count_kernel": "chunk_hist", "emit_keys_kernel": "emit_keys",
-         "bin_coop_kernel": "bin_coop", "zero_sgrad_kernel": "sgrad_clear", "valid_count_kernel": "loss_count"}
+         "bin_coop_kernel": "bin_coop", "zero_sgrad_kernel": "sgrad_clear", "valid_count_kernel": "loss_count",
+         "tile_order_fwd_kernel": "tile_order"}
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
            "sm__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__issue_active.avg.pct_of_peak_sustained_active",
