@@ -428,8 +428,7 @@ __global__ void __launch_bounds__(kTilePx / 2, 6) render_fwd2_kernel(
             const f32x2 dy = sub2(bc2(r0.y), fy2);
             pw = fma2(bc2(Adx), bc2(dx), fma2(mul2(bc2(r1.x), dy), dy, mul2(bc2(Bdx), dy)));
         };
-        for (int k0 = 0; k0 < nlive; k0 += kU) {
-            if (__all_sync(0xffffffffu, P.dA && P.dB)) break;
+        auto group = [&](int k0) {
             const PixPair P0 = P;
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
@@ -450,6 +449,14 @@ __global__ void __launch_bounds__(kTilePx / 2, 6) render_fwd2_kernel(
                     blend_step_pair(P, pw, r1, r2, j);
                 }
             }
+        };
+        // two groups per trip: the second group's state can take the registers the first group's
+        // entry state (kept for its replay) held, so the loop carries no register copies
+        for (int k0 = 0; k0 < nlive; k0 += 2 * kU) {
+            if (__all_sync(0xffffffffu, P.dA && P.dB)) break;
+            group(k0);
+            if (k0 + kU >= nlive || __all_sync(0xffffffffu, P.dA && P.dB)) break;
+            group(k0 + kU);
         }
         if (__syncthreads_and(P.dA && P.dB)) break;   // also orders buffer reuse
     }

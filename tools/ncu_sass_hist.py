@@ -8,7 +8,7 @@ import sys
 def main():
     rep, kname = sys.argv[1], sys.argv[2]
     top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", kname],
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "--kernel-name", kname],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     h = None
