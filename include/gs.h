@@ -245,8 +245,15 @@ gs_status gs_loss_l1_masked(const float* color, const float* depth, const float*
  *                    opacity scaled: o_i <- eta o_i (params row 10; params_raw row 10 <- logit of
  *                    the new opacity if params_raw != NULL; Adam moments unchanged). select_mask
  *                    (nullable) receives the per-Gaussian flag. The map size is unchanged.
+ *  GS_DENSIFY_DEGENERATE_FLAG  the same test, but only ORed into select_mask (select_mask[i] = 1 for
+ *                    every flagged Gaussian, others untouched; params may be NULL and are not
+ *                    changed): the per-keyframe half of a multi-keyframe / multi-GPU degeneration
+ *                    (mapping.py: flags of all keyframes, max-all-reduced over ranks, then APPLY).
+ *  GS_DENSIFY_DEGENERATE_APPLY  o_i <- eta o_i for every i < n with select_mask[i] != 0 (params
+ *                    row 10; params_raw row 10 <- logit if non-NULL). No projection needed.
  * n_dev: device int64 [1] (in/out). All compaction is deterministic. */
-enum { GS_DENSIFY_ADD = 1, GS_DENSIFY_PRUNE = 2, GS_DENSIFY_SELECT = 3, GS_DENSIFY_DEGENERATE = 4 };
+enum { GS_DENSIFY_ADD = 1, GS_DENSIFY_PRUNE = 2, GS_DENSIFY_SELECT = 3, GS_DENSIFY_DEGENERATE = 4,
+       GS_DENSIFY_DEGENERATE_FLAG = 5, GS_DENSIFY_DEGENERATE_APPLY = 6 };
 typedef struct {
     int32_t mode;
     float tau_alpha, tau_depth, min_opacity, sel_weight, sel_depth, init_opacity;

@@ -321,6 +321,13 @@ gs_status gs_densify_prune(float* params, float* params_raw, int64_t* n_dev, int
                 return GS_ERR_INVALID_ARG;
             if (s->gen_project == 0) return GS_ERR_STALE;
             break;
+        case GS_DENSIFY_DEGENERATE_FLAG:
+            if (!select_mask || !target_depth || !cam_ok(s, cam) || capacity > s->n_cap) return GS_ERR_INVALID_ARG;
+            if (s->gen_project == 0) return GS_ERR_STALE;
+            break;
+        case GS_DENSIFY_DEGENERATE_APPLY:
+            if (!params || !select_mask || !(cfg->eta >= 0.f) || !(cfg->eta <= 1.f)) return GS_ERR_INVALID_ARG;
+            break;
         default:
             return GS_ERR_INVALID_ARG;
     }

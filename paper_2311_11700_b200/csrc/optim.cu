@@ -925,7 +925,7 @@ __global__ void select_kernel(int64_t n, const int64_t* n_dev, const float4* __r
 __global__ void degenerate_kernel(int64_t n, const int64_t* n_dev, const float4* __restrict__ rec,
                                   const uint32_t* __restrict__ tiles, const float* __restrict__ td, int W, int H,
                                   float gamma, float eta, float* __restrict__ opacity, float* __restrict__ raw_opacity,
-                                  uint8_t* __restrict__ mask) {
+                                  uint8_t* __restrict__ mask, bool flag_only) {
     const int64_t nn = n_dev ? *n_dev : n;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nn; i += int64_t(gridDim.x) * blockDim.x) {
         bool hit = false;
@@ -937,12 +937,28 @@ __global__ void degenerate_kernel(int64_t n, const int64_t* n_dev, const float4*
                 hit = t > 0.f && __fsub_rn(t, r1.z) > gamma;
             }
         }
+        if (flag_only) {   // GS_DENSIFY_DEGENERATE_FLAG: OR into the mask, opacities untouched
+            if (hit) mask[i] = 1;
+            continue;
+        }
         if (hit) {
             const float o = __fmul_rn(eta, opacity[i]);
             opacity[i] = o;
             if (raw_opacity) raw_opacity[i] = logf(o / (1.f - o));
         }
         if (mask) mask[i] = hit ? 1 : 0;
+    }
+}
+
+// GS_DENSIFY_DEGENERATE_APPLY: the Eq. 9 scaling for the Gaussians a (reduced) flag mask names
+__global__ void degenerate_apply_kernel(int64_t n, const int64_t* n_dev, const uint8_t* __restrict__ mask, float eta,
+                                        float* __restrict__ opacity, float* __restrict__ raw_opacity) {
+    const int64_t nn = n_dev ? *n_dev : n;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nn; i += int64_t(gridDim.x) * blockDim.x) {
+        if (!mask[i]) continue;
+        const float o = __fmul_rn(eta, opacity[i]);
+        opacity[i] = o;
+        if (raw_opacity) raw_opacity[i] = logf(o / (1.f - o));
     }
 }
 
@@ -965,12 +981,20 @@ gs_status run_densify(WsState* s, float* params, float* raw, int64_t* n_dev, int
                                                     cfg.sel_depth, select_mask)));
         return check_launch(s, "densify_select");
     }
-    if (cfg.mode == GS_DENSIFY_DEGENERATE) {
+    if (cfg.mode == GS_DENSIFY_DEGENERATE || cfg.mode == GS_DENSIFY_DEGENERATE_FLAG) {
         const int blocks = int(std::min<int64_t>((capacity + 255) / 256, 148 * 8));
         GS_K((degenerate_kernel<<<blocks, 256, 0, st>>>(capacity, n_dev, at<float4>(s, s->rec), at<uint32_t>(s, s->tiles),
                                                         tdepth, cam.width, cam.height, cfg.gamma, cfg.eta,
-                                                        params + 10 * ld, raw ? raw + 10 * ld : nullptr, select_mask)));
+                                                        params ? params + 10 * ld : nullptr,
+                                                        raw ? raw + 10 * ld : nullptr, select_mask,
+                                                        cfg.mode == GS_DENSIFY_DEGENERATE_FLAG)));
         return check_launch(s, "densify_degenerate");
+    }
+    if (cfg.mode == GS_DENSIFY_DEGENERATE_APPLY) {
+        const int blocks = int(std::min<int64_t>((capacity + 255) / 256, 148 * 8));
+        GS_K((degenerate_apply_kernel<<<blocks, 256, 0, st>>>(capacity, n_dev, select_mask, cfg.eta, params + 10 * ld,
+                                                              raw ? raw + 10 * ld : nullptr)));
+        return check_launch(s, "densify_degenerate_apply");
     }
     if (cfg.mode == GS_DENSIFY_ADD) {
         const int64_t npx = int64_t(cam.width) * cam.height;

@@ -24,7 +24,8 @@ import dataclasses
 import torch
 import torch.distributed as dist
 
-from . import (GS_DENSIFY_ADD, GS_DENSIFY_PRUNE, GS_FLAG_NO_HOST_SYNC, densify_cfg, gs_adam_step,
+from . import (GS_DENSIFY_ADD, GS_DENSIFY_DEGENERATE_APPLY, GS_DENSIFY_DEGENERATE_FLAG, GS_DENSIFY_PRUNE,
+               GS_FLAG_NO_HOST_SYNC, densify_cfg, gs_adam_step,
                gs_densify_append, gs_densify_prune, gs_pose_step, make_camera)
 from .pipeline import RenderPipeline
 
@@ -46,6 +47,12 @@ def allreduce_grads(grad: torch.Tensor, group=None) -> None:
     """Sum the gradient buffer over ranks in place (NCCL on GPU, gloo on CPU)."""
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=group)
+
+
+def allreduce_mask(mask: torch.Tensor, group=None) -> None:
+    """OR of per-rank u8 flag masks (max all-reduce), so every rank applies the same Eq. 9 set."""
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(mask, op=dist.ReduceOp.MAX, group=group)
 
 
 def gather_candidates(cand: torch.Tensor, counts: torch.Tensor, group=None):
@@ -80,7 +87,8 @@ class Keyframe:
 class ShardedMapper:
     def __init__(self, params: torch.Tensor, n: int, keyframes: list[Keyframe], cam, key_cap: int,
                  max_add_per_kf: int = 8192, w_color: float = 0.9, w_depth: float = 0.1, group=None,
-                 densify: bool = True, ba_iters: int | None = None, lr_rho: float = 1e-3, lr_phi: float = 1e-3):
+                 densify: bool = True, ba_iters: int | None = None, lr_rho: float = 1e-3, lr_phi: float = 1e-3,
+                 degenerate: tuple[float, float] | None = None):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if self.world > 1 else 0
@@ -102,6 +110,9 @@ class ShardedMapper:
         self.ba_iters = ba_iters
         self.lr_rho, self.lr_phi = lr_rho, lr_phi
         self.pose_step = 0
+        # Eq. 9 opacity degeneration (NEXT-2, reading C27) in expansion steps: (eta, gamma)
+        self.degenerate = degenerate
+        self.dmask = torch.zeros(self.cap, dtype=torch.uint8, device=params.device) if degenerate else None
         self.set_keyframes(keyframes)
 
     def set_keyframes(self, keyframes: list[Keyframe]):
@@ -126,9 +137,17 @@ class ShardedMapper:
     def render_backward(self):
         """fwd + L1 + bwd for every local keyframe, accumulating into grad."""
         self.grad[:, :self.n].zero_()
+        degen = self.degenerate is not None and self.densify
+        if degen:
+            self.dmask.zero_()
         for j, k in enumerate(self.local):
             kf = self.keyframes[k]
             self.pipe.forward(self.P, self.n, kf.view, self.cam, bin_flags=GS_FLAG_NO_HOST_SYNC, fwd_flags=0)
+            if degen:   # Eq. 9 flags from this keyframe's projection, ORed over the local keyframes
+                gs_densify_prune(None, None, self.n_dev, self.n, self.cap, None, None, None, None, None, kf.depth,
+                                 None, kf.view, self.cm, densify_cfg(GS_DENSIFY_DEGENERATE_FLAG,
+                                                                     gamma=self.degenerate[1]),
+                                 self.dmask, None, self.pipe.ws)
             dc, dd = self.pipe.loss_l1(self.cam, kf.color, kf.depth, self.w_color, self.w_depth)
             gp = None
             if self.poses_active():
@@ -145,6 +164,11 @@ class ShardedMapper:
         poses = self.poses_active()
         self.render_backward()
         allreduce_grads(self.grad, self.group)
+        if self.degenerate is not None and self.densify:   # one Eq. 9 application per expansion step
+            allreduce_mask(self.dmask, self.group)
+            gs_densify_prune(self.P, self.raw, self.n_dev, self.n, self.cap, None, None, None, None, None, None,
+                             None, None, None, densify_cfg(GS_DENSIFY_DEGENERATE_APPLY, eta=self.degenerate[0]),
+                             self.dmask, None, self.pipe.ws)
         if poses:   # each rank updates the poses of its own keyframes (device-only pose step)
             self.pose_step += 1
             for j, k in enumerate(self.local):

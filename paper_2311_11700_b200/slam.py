@@ -40,6 +40,7 @@ class SlamConfig:
     max_add: int | None = None  # Eq. 8 candidates per keyframe (default H W / 2: the first frame fills)
     parallel: bool = True
     seed: int = 0              # window sampling
+    degenerate: tuple[float, float] | None = None   # Eq. 9 (eta, gamma) in the expansion step (NEXT-2)
 
 
 class SlamSystem:
@@ -53,7 +54,7 @@ class SlamSystem:
         max_add = cfg.max_add or (cam.width * cam.height) // 2
         with torch.cuda.stream(self.ms):
             self.mapper = ShardedMapper(torch.zeros(14, n_cap, device=dev), 0, [], cam, key_cap_full,
-                                        max_add_per_kf=max_add, densify=True)
+                                        max_add_per_kf=max_add, densify=True, degenerate=cfg.degenerate)
         with torch.cuda.stream(self.ts):
             self.tracker = Tracker(n_cap, key_cap_full, key_cap_half, cam, device)
             self.frontend = Frontend(self.tracker, cfg.frontend)

@@ -29,7 +29,8 @@ def _mapping_module():
         except ImportError:
             stub = types.ModuleType("paper_2311_11700_b200")
             stub.__path__ = [os.path.join(ROOT, "paper_2311_11700_b200")]
-            for name in ("GS_DENSIFY_ADD", "GS_DENSIFY_PRUNE", "GS_FLAG_NO_HOST_SYNC"):
+            for name in ("GS_DENSIFY_ADD", "GS_DENSIFY_PRUNE", "GS_FLAG_NO_HOST_SYNC", "GS_DENSIFY_DEGENERATE_APPLY",
+                         "GS_DENSIFY_DEGENERATE_FLAG"):
                 setattr(stub, name, 0)
             for name in ("densify_cfg", "gs_adam_step", "gs_densify_append", "gs_densify_prune", "make_camera"):
                 setattr(stub, name, None)
@@ -90,6 +91,14 @@ def _tiny_world(seed=0):
     return p, cam, views
 
 
+def _degen_flags(p, cam, views, k):
+    import gs_inputs as gi
+    import oracle
+    pr = oracle.project(p, views[k], cam, "f32")
+    _, td = gi.random_images(cam.width, cam.height, 200 + k, 0.5, 3.0)
+    return oracle.degenerate_mask(pr["mean2d"], pr["depth"], pr["tiles"], td, gamma=0.10)
+
+
 def _worker(rank, world, port, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -113,7 +122,12 @@ def _worker(rank, world, port, out):
             counts[j] = k + 1
             cand[j, :, : k + 1] = float(k)
         allc, allk = m.gather_candidates(cand, counts)
-        out[rank] = (grad.numpy().copy(), allc.numpy().copy(), allk.numpy().copy())
+        # Eq. 9 flags: OR over the local keyframes, then the max all-reduce (ShardedMapper.step)
+        mask = torch.zeros(p.shape[1], dtype=torch.uint8)
+        for k in local:
+            mask |= torch.from_numpy(_degen_flags(p, cam, views, k).astype(np.uint8))
+        m.allreduce_mask(mask)
+        out[rank] = (grad.numpy().copy(), allc.numpy().copy(), allk.numpy().copy(), mask.numpy().copy())
     finally:
         dist.destroy_process_group()
 
@@ -137,8 +151,15 @@ def test_gloo_world2_allreduce_and_candidate_gather():
     for k in range(len(views)):
         dc, dd = gi.upstream(cam.width, cam.height, 100 + k)
         want += oracle.backward(p, views[k], cam, dc, dd, "f64")["grad_params"]
-    g0, c0, k0 = out[0]
-    g1, c1, k1 = out[1]
+    g0, c0, k0, m0 = out[0]
+    g1, c1, k1, m1 = out[1]
+    want_m = np.zeros(p.shape[1], bool)
+    per = [_degen_flags(p, cam, views, k) for k in range(len(views))]
+    for f in per:
+        want_m |= f
+    np.testing.assert_array_equal(m0, m1)
+    np.testing.assert_array_equal(m0.astype(bool), want_m)
+    assert want_m.sum() > max(f.sum() for f in per)   # the union is larger than any one keyframe's set
     np.testing.assert_array_equal(g0, g1)                 # identical reduced bytes on every rank
     np.testing.assert_allclose(g0, want, rtol=1e-12, atol=1e-12)
     np.testing.assert_array_equal(c0, c1)

@@ -233,3 +233,36 @@ def test_slam_sequence_tracks_and_maps(parallel):
     assert max(t for t, _ in errs) < 0.03 and max(r for _, r in errs) < 2.0
     assert slam.map_rounds == sum(slam.kf_flags) >= 2
     assert slam.mapper.n > 20_000
+
+
+def test_mapper_degeneration_in_expansion_steps():
+    """NEXT-2 wired into ShardedMapper(degenerate=(eta, gamma)): in a densifying step the union of
+    the keyframes' Eq. 9 sets (computed by the oracle from the map before the step) is the mask the
+    mapper applied, and only expansion steps apply it."""
+    import paper_2311_11700_b200 as g
+    from paper_2311_11700_b200.mapping import Keyframe, ShardedMapper
+    cfg = gi.CONFIGS[1]
+    p = cfg.scene()
+    cam = cfg.cam
+    views = [cfg.view(), oracle.apply_twist(np.array([0.1, 0.0, 0.05, 0.0, 0.08, 0.0]),
+                                            cfg.view().astype(np.float64)).astype(np.float32)]
+    kfs = []
+    want = np.zeros(p.shape[1], bool)
+    for k, v in enumerate(views):
+        tc, td = gi.random_images(cam.width, cam.height, 310 + k, 0.5, 3.0)
+        kfs.append(Keyframe(to_dev(v), to_dev(tc), to_dev(td)))
+        pr = oracle.project(p, v, cam, "f32")
+        want |= oracle.degenerate_mask(pr["mean2d"], pr["depth"], pr["tiles"], td, gamma=0.10)
+    key_cap = max(key_cap_for(p, v, cam)[0] for v in views)
+    cap = p.shape[1] + 2 * 8192
+    P = torch.zeros(14, cap, device="cuda")
+    P[:, :p.shape[1]] = to_dev(p)
+    m = ShardedMapper(P, p.shape[1], kfs, cam, key_cap, max_add_per_kf=8192, densify=True, degenerate=(0.1, 0.10))
+    m.step()
+    torch.cuda.synchronize()
+    assert np.array_equal(m.dmask[:p.shape[1]].cpu().numpy().astype(bool), want) and want.any()
+    m.densify = False
+    before = m.dmask.clone()
+    m.step()
+    torch.cuda.synchronize()
+    assert torch.equal(m.dmask, before)   # no flagging outside expansion steps

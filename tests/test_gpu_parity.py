@@ -691,3 +691,41 @@ def test_image_half_bitexact(W, H):
     torch.cuda.synchronize()
     oc, od = oracle.image_half(c, d)
     assert np.array_equal(ch.cpu().numpy(), oc) and np.array_equal(dh.cpu().numpy(), od)
+
+
+def test_degenerate_flag_or_and_apply_parity():
+    """Multi-keyframe Eq. 9 (NEXT-2): GS_DENSIFY_DEGENERATE_FLAG ORs each view's flags into the mask
+    (opacities untouched), GS_DENSIFY_DEGENERATE_APPLY scales the union once: the union bit-exact
+    with the OR of the oracle's per-view sets, the opacities bit-exact with oracle.degenerate."""
+    import paper_2311_11700_b200 as g
+    cfg, p, v0 = scene(1)
+    views = [v0, oracle.apply_twist(np.array([0.1, 0.0, 0.05, 0.0, 0.08, 0.0]), v0.astype(np.float64))]
+    key_cap = max(key_cap_for(p, v.astype(np.float32), cfg.cam)[0] for v in views)
+    pipe = g.RenderPipeline(p.shape[1], key_cap, cfg.cam.width, cfg.cam.height)
+    P = to_dev(p)
+    raw = torch.zeros_like(P)
+    n = p.shape[1]
+    n_dev = torch.tensor([n], dtype=torch.int64, device="cuda")
+    mask = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    want = np.zeros(n, bool)
+    per = []
+    for k, v in enumerate(views):
+        _, td = gi.random_images(cfg.cam.width, cfg.cam.height, 300 + k, 0.5, 3.0)
+        V = to_dev(v)
+        pipe.forward(P, n, V, cfg.cam)
+        g.gs_densify_prune(None, None, n_dev, n, n, None, None, None, None, None, to_dev(td), None, V,
+                           g.make_camera(cfg.cam), g.densify_cfg(g.GS_DENSIFY_DEGENERATE_FLAG, gamma=0.10), mask,
+                           None, pipe.ws)
+        pr = oracle.project(p, v.astype(np.float32), cfg.cam, "f32")
+        per.append(oracle.degenerate_mask(pr["mean2d"], pr["depth"], pr["tiles"], td, gamma=0.10))
+        want |= per[-1]
+    torch.cuda.synchronize()
+    assert np.array_equal(P[10].cpu().numpy(), p[10].astype(np.float32))   # FLAG leaves opacities alone
+    assert np.array_equal(mask.cpu().numpy().astype(bool), want)
+    assert want.sum() > max(f.sum() for f in per)
+    g.gs_densify_prune(P, raw, n_dev, n, n, None, None, None, None, None, None, None, None, None,
+                       g.densify_cfg(g.GS_DENSIFY_DEGENERATE_APPLY, eta=0.1), mask, None, pipe.ws)
+    torch.cuda.synchronize()
+    o, lo = oracle.degenerate(p[10], want, eta=0.1)
+    assert np.array_equal(P[10].cpu().numpy(), o)
+    np.testing.assert_allclose(raw[10].cpu().numpy()[want], lo[want], rtol=1e-5, atol=1e-6)
