@@ -11,6 +11,7 @@ Prints ONE JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import subprocess
@@ -49,6 +50,8 @@ def parse():
     ap.add_argument("--binsort", default="bucket", choices=["bucket", "keys"])
     ap.add_argument("--sh", type=int, default=0, choices=[0, 1],
                     help="colour model: 0 = RGB (BASELINE configs), 1 = degree-1 SH (NEXT-1, gs_project_sh)")
+    ap.add_argument("--pose-seed", type=int, default=None,
+                    help="override the config's pose seed (tools/pose_sweep.py: SURVEY.md §8(d) sweeps 8 poses)")
     ap.add_argument("--opacity-radius", action="store_true",
                     help="GS_FLAG_OPACITY_RADIUS (NEXT-4, reading C33): exact 1/255-reach tiling instead of the "
                          "paper's 3-sigma box (a different render: not the BASELINE workload)")
@@ -198,6 +201,8 @@ def main_ours(args):
     dist = init_dist(world, "nccl")
     dev = torch.device("cuda", local)
     cfg = gi.CONFIGS[args.config]
+    if args.pose_seed is not None:
+        cfg = dataclasses.replace(cfg, pose_seed=args.pose_seed)
     cam = cfg.cam
     n = cfg.n
     p = cfg.scene()
@@ -239,18 +244,21 @@ def main_ours(args):
         if dist:
             dist.barrier()
 
+    per_step = []
+
     def timed(fn, steps):
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(steps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        ev[0].record()
+        for i in range(steps):
             fn()
-        e1.record()
+            ev[i + 1].record()
         torch.cuda.synchronize()
         barrier()
-        ms = e0.elapsed_time(e1) / steps
+        ms = ev[0].elapsed_time(ev[-1]) / steps
+        per_step[:] = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
         if dist:
             t = torch.tensor([ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -301,6 +309,9 @@ def main_ours(args):
                       "binsort": args.binsort, "cuda_graph": not args.no_graph, "l2": "per-iteration working set > L2 (126 MB): tile lists "
                       f"{K * 4 / 1e9:.2f} GB + live lists; no flush", "parallelism": f"replicas x{world}"},
            "evals_per_s": world * (E_f + E_b) * 1000.0 / ms, "clocks": clocks, "gpu_launches": int(launches),
+           # per-step distribution of the timed region (events between graph replays)
+           "step_ms": {"median": float(np.median(per_step)), "p10": float(np.percentile(per_step, 10)),
+                       "p90": float(np.percentile(per_step, 90))},
            # the paper's own numbers: another GPU, real scenes of unstated size; context only
            "paper_context": {"gpu": "RTX 4090", "render_fps_forward_only": 386.91, "tracking_iters_per_s": 84.0,
                              "mapping_iters_per_s": 78.0, "cite": "PAPER.md:474 (Table 6), :400 (Table 4)"}}
