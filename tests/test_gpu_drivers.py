@@ -266,3 +266,31 @@ def test_mapper_degeneration_in_expansion_steps():
     m.step()
     torch.cuda.synchronize()
     assert torch.equal(m.dmask, before)   # no flagging outside expansion steps
+
+
+def test_tracking_graph_replay_matches_eager():
+    """Tracker.track(graph=True): the captured coarse and fine stages replayed from the same start
+    end at the eager run's pose (fp32 atomics reorder sums, so within 1 mm / 0.05 deg), twice."""
+    from paper_2311_11700_b200.tracking import TrackConfig, Tracker, pose_error
+    cam = gi.CAM_TUM
+    p = gi.room_surface_gaussians(200_000, 53)
+    n = p.shape[1]
+    v_gt = gi.room_view(153)
+    kc, _ = key_cap_for(p, v_gt, cam, slack=1.5)
+    kh, _ = key_cap_for(p, v_gt, cam.half(), slack=1.5)
+    tr = Tracker(n, kc, kh, cam)
+    P = to_dev(p)
+    tc_h, td_h = _render(tr.half, P, n, to_dev(v_gt), cam.half())
+    tc_f, td_f = _render(tr.full, P, n, to_dev(v_gt), cam)
+    v0 = oracle.apply_twist(gi.twist_perturbation(7, 0.015, 0.75), v_gt.astype(np.float64))
+    cfg = TrackConfig(iters_coarse=20, iters_fine=20)
+    V = to_dev(v0)
+    tr.track(P, n, V, tc_h, td_h, tc_f, td_f, cfg)
+    eager = V.cpu().numpy()
+    for _ in range(2):
+        V.copy_(to_dev(v0))
+        tr.track(P, n, V, tc_h, td_h, tc_f, td_f, cfg, graph=True)
+        torch.cuda.synchronize()
+        d = pose_error(V.cpu().numpy(), eager)
+        assert d[0] < 1e-3 and d[1] < 0.05, d
+    assert pose_error(eager, v_gt)[0] < 0.5 * pose_error(v0, v_gt)[0]
