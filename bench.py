@@ -180,7 +180,9 @@ def run_reference(args):
     line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3 / frac, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"config {args.config}: {cfg.name} {cfg.cam.width}x{cfg.cam.height}, {cfg.n} Gaussians"},
+            "config": {"workload": f"config {args.config}: {cfg.name} {cfg.cam.width}x{cfg.cam.height}, {cfg.n} Gaussians, "
+                                   f"fwd+bwd L1 (0.9/0.1) iteration", "n_gaussians": cfg.n, "width": cfg.cam.width,
+                                   "height": cfg.cam.height},
             "cpu_baseline": {"value": value, "unit": "iters/s", "cores": oracle.num_threads(), "kind": "oracle",
                              "sample": desc},
             "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
