@@ -939,6 +939,7 @@ void launch_render_bwd_tiles(WsState* s, const gs_camera& cam, const float*, con
 // Screen-space gradients -> the 14 parameters (Eq. 11 / Supplement A) and the pose twist.
 // pose partial sums: rho(3), phi(3), dW_cov(9)  (reading C7: A = W (sum dW_cov)^T).
 constexpr int kPoseSums = 15;
+constexpr int kGbwdBlocksPerSM = 2;   // resident blocks per SM (register budget 128: no spills)
 
 // Persistent grid (a few blocks per SM) striding over the on-screen list; each thread keeps its pose
 // partial sums across its Gaussians. The last block to finish (atomic ticket) reduces the per-block
@@ -954,7 +955,7 @@ __device__ __forceinline__ void gacc(float* p, float v, bool assign) {   // GS_F
 }
 
 template <int SH, bool ASSIGN>
-__global__ void __launch_bounds__(256, 4) gaussian_bwd_kernel(
+__global__ void __launch_bounds__(256, kGbwdBlocksPerSM) gaussian_bwd_kernel(
     const float* __restrict__ params, int64_t n, int64_t ld, const float* __restrict__ viewmat, gs_camera cam,
     const uint32_t* __restrict__ onlist, const unsigned int* __restrict__ n_on, const float4* __restrict__ rec,
     const float* __restrict__ sgrad, int64_t sld, float* __restrict__ grad, int cov_path,
@@ -1226,7 +1227,7 @@ void launch_gaussian_bwd(WsState* s, const float* params, int64_t n, int64_t ld,
         sms = std::max(sms, 1);
     }
     // grid sized without a host sync: at most 4 blocks per SM, at most ceil(n / 256)
-    const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(sms) * 4));
+    const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(sms) * kGbwdBlocksPerSM));
     KTimer kt(s, KID_BWD_GAUSS, st);
     const int assign = (flags & GS_FLAG_GRAD_ASSIGN) ? 1 : 0;
     const int zero_blocks = (assign && grad_params) ? std::min(sms, int((n + 255) / 256)) : 0;
