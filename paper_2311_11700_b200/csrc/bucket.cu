@@ -167,16 +167,23 @@ __global__ void __launch_bounds__((kConsumers + kProducers) * 32) bucket_emit_ke
         for (int k0 = 0; k0 < L; k0 += 32) {
             const int k = k0 + lane;
             const uint2 mg = k < L ? list[k] : make_uint2(0u, 0u);
-            uint32_t mine = 0;   // lane j: ballot of tile j
+            // the 32x32 bit matrix (row = lane's tile mask) transposed with five butterfly exchanges:
+            // lane j then holds column j, i.e. which of the 32 Gaussians hit tile j (its ballot)
+            uint32_t x = mg.x;
+#pragma unroll
+            for (int sh = 16; sh >= 1; sh >>= 1) {
+                const uint32_t lo = sh == 16 ? 0x0000FFFFu : sh == 8 ? 0x00FF00FFu : sh == 4 ? 0x0F0F0F0Fu
+                                  : sh == 2 ? 0x33333333u : 0x55555555u;
+                const uint32_t y = __shfl_xor_sync(0xffffffffu, x, sh);
+                x = (lane & sh) ? ((x & ~lo) | ((y & ~lo) >> sh)) : ((x & lo) | ((y & lo) << sh));
+            }
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-                const bool hit = mg.x & (1u << j);
-                const uint32_t m = __ballot_sync(0xffffffffu, hit);
+                const uint32_t m = __shfl_sync(0xffffffffu, x, j);
                 const uint32_t pj = __shfl_sync(0xffffffffu, mypos, j);
-                if (hit) vals_out[pj + __popc(m & lt)] = mg.y;
-                mine = lane == j ? m : mine;
+                if (mg.x & (1u << j)) vals_out[pj + __popc(m & lt)] = mg.y;
             }
-            mypos += __popc(mine);
+            mypos += __popc(x);
         }
         __syncwarp();   // list reuse
     }
