@@ -729,3 +729,49 @@ def test_degenerate_flag_or_and_apply_parity():
     o, lo = oracle.degenerate(p[10], want, eta=0.1)
     assert np.array_equal(P[10].cpu().numpy(), o)
     np.testing.assert_allclose(raw[10].cpu().numpy()[want], lo[want], rtol=1e-5, atol=1e-6)
+
+
+# ------------------------------------------------------------------ maximum sizes
+def test_4k_image_lists_and_sampled_pixels():
+    """A 3840x2160 frame (240x135 = 32400 tiles, near bin_coop's shared-memory tile-grid bound) with
+    300k Gaussians: projection bit-exact, tile lists bit-exact (binding check on the GPU's projection),
+    and 2048 sampled pixels against the oracle one by one (tie rule)."""
+    cam = gi.Camera(1800.0, 1800.0, 1919.5, 1079.5, 3840, 2160)
+    p = gi.gaussians(300_000, 77, gi.ROOM_LO, gi.ROOM_HI)
+    v = gi.room_view(177)
+    o = oracle.project(p, v, cam, "f32")
+    pipe, P, V, fr = run_forward(p, v, cam, fwd_flags=0)
+    a = pipe.arrays(p.shape[1])
+    assert np.array_equal(a["tiles"].cpu().numpy().view(np.uint32), o["tiles"])
+    assert np.array_equal(a["rect"].cpu().numpy().astype(np.int32).T, o["rect"])
+    ob = oracle.bin_sort(o["depth_bits"], o["rect"], o["tiles"], cam)
+    assert fr.n_keys == ob["n_keys"] and fr.n_keys > 10_000_000
+    assert np.array_equal(a["vals"].cpu().numpy().view(np.uint32), ob["vals"])
+    assert np.array_equal(a["ranges"].cpu().numpy().view(np.uint32), ob["ranges"])
+    px = np.random.default_rng(1).choice(cam.width * cam.height, 2048, replace=False)
+    of = oracle.forward(p, v, cam, "f32", pixels=px)
+    gc = fr.color.reshape(3, -1)[:, px].cpu().numpy()
+    ok = np.abs(gc - of["color"]).max(0) <= ATOL_IMG
+    assert ok.mean() >= 1 - 1e-3 and (ok | (of["ambiguous"] == 1)).all()
+
+
+def test_tile_grid_beyond_the_cooperative_bound():
+    """An 8192x8192 frame has 262144 tiles, beyond the cooperative binning kernel's shared-memory
+    tile grid: the default path returns GS_ERR_UNSUPPORTED (loudly, no fallback), and the key-sort
+    path (GS_FLAG_BINSORT_KEYS) bins it with lists bit-exact with the oracle."""
+    import paper_2311_11700_b200 as g
+    cam = gi.Camera(4000.0, 4000.0, 4095.5, 4095.5, 8192, 8192)
+    p = gi.gaussians(20_000, 78, gi.ROOM_LO, gi.ROOM_HI)
+    v = gi.room_view(178)
+    key_cap, o = key_cap_for(p, v, cam)
+    pipe = g.RenderPipeline(p.shape[1], key_cap, cam.width, cam.height)
+    P, V = to_dev(p), to_dev(v)
+    with pytest.raises(g.GSError, match="UNSUPPORTED"):
+        pipe.forward(P, p.shape[1], V, cam, fwd_flags=0)
+    fr = pipe.forward(P, p.shape[1], V, cam, bin_flags=g.GS_FLAG_BINSORT_KEYS, fwd_flags=0)
+    torch.cuda.synchronize()
+    a = pipe.arrays(p.shape[1])
+    ob = oracle.bin_sort(o["depth_bits"], o["rect"], o["tiles"], cam)
+    assert fr.n_keys == ob["n_keys"]
+    assert np.array_equal(a["vals"].cpu().numpy().view(np.uint32), ob["vals"])
+    assert np.array_equal(a["ranges"].cpu().numpy().view(np.uint32), ob["ranges"])
