@@ -462,9 +462,8 @@ def roofline(per_step, clocks, K, n, V_s, E_f, E_b, npx, binsort="bucket", GX=75
         "project": ("hbm", n * (56 + 72) / 1e9, "GB/s"),
         "gaussian_bwd": ("hbm", (n * 4 + V_s * 244) / 1e9, "GB/s"),
         "loss_l1": ("hbm", npx * 24 / 1e9, "GB/s"),
-        # fused L1 (gs_render_bwd_l1): the valid-pixel count reads the target depth
-        "loss_count": ("hbm", npx * 4 / 1e9, "GB/s"),
-        "sgrad_clear": ("hbm", V_s * 40 / 1e9, "GB/s"),
+        # backward prologue: accumulator clear + (fused L1) the valid-pixel count of the target depth
+        "sgrad_clear": ("hbm", (V_s * 40 + npx * 4) / 1e9, "GB/s"),
     }
     prof = load_json(os.path.join(ROOT, "profiles", "ncu_traffic.json"), {}) or {}
     table = {}

@@ -65,7 +65,8 @@ static void carve(WsState* s, Carver& c) {
     s->scratch14 = c.take(uint64_t(n) * 4 * 14);
     s->dkey_sorted = c.take(uint64_t(n) * 4 * 2);
     s->dval_sorted = c.take(uint64_t(n) * 4 * 2);
-    s->chunk_hist = c.take(uint64_t(std::max<int64_t>((n + 2047) / 2048, (px + 2047) / 2048) + 1) * 4);
+    // densify block counts; also the backward prologue's per-block valid counts (148 * 4 blocks)
+    s->chunk_hist = c.take(uint64_t(std::max<int64_t>({(n + 2047) / 2048, (px + 2047) / 2048, 1024}) + 1) * 4);
     s->chunk_mat = c.take(uint64_t((n + 255) / 256 + 1) * tiles * 4);   // path B count/base matrix
     s->srect = c.take(uint64_t(n) * 8);
     s->tile_tot = c.take(uint64_t(tiles) * 4 * 10);   // totals, starts, 8 segment sums
@@ -198,7 +199,9 @@ static gs_status backward_common(const float* params, int64_t n, int64_t ld, con
         cam->height != s->cam_h)
         return GS_ERR_STALE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (n > 0) launch_zero_sgrad(s, st);   // screen accumulators [10][V_s], indexed by on-screen rank
+    // prologue: screen accumulators [10][V_s] (rank-indexed), LPT tile order, fused-L1 valid count
+    if (n > 0 || fuse)
+        launch_zero_sgrad(s, st, fuse ? fuse->td : nullptr, fuse ? int64_t(cam->width) * cam->height : 0);
     // fused L1 with a pose gradient: gaussian_bwd's last block (which exists then) writes the loss
     const bool fin_in_gbwd = fuse && fuse->loss && grad_pose && n > 0;
     launch_render_bwd_tiles(s, *cam, nullptr, dLdC, dLdD, st, fuse, !fin_in_gbwd);

@@ -76,7 +76,8 @@ struct Misc {
     unsigned long long keep_count;
     unsigned int chunk_counter;
     unsigned int pose_done;        // gaussian_bwd last-block ticket (self-resetting)
-    unsigned int pad[2];
+    unsigned int prep_done;        // bwd_prep_kernel last-block ticket (self-resetting)
+    unsigned int pad;
 };
 
 // Grid barrier for cooperative launches (all CTAs co-resident): block barrier, one thread fences and
@@ -139,7 +140,7 @@ gs_status run_compact_onscreen(WsState* s, cudaStream_t st);   // path A
 gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t st);
 void launch_render_fwd(WsState* s, const gs_camera& cam, float* color, float* depth, float* alpha,
                        float* accum_weight, uint32_t flags, cudaStream_t st);
-void launch_zero_sgrad(WsState* s, cudaStream_t st);
+void launch_zero_sgrad(WsState* s, cudaStream_t st, const float* td_l1 = nullptr, int64_t npx = 0);
 struct L1Fuse {   // gs_render_bwd_l1: the L1 loss formed inside the backward's pixel loads
     const float *color, *depth, *tc, *td;
     float wc, wd;

@@ -845,32 +845,31 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
     }
 }
 
-// the screen accumulators [10][V_s] (rank-indexed) cleared at the start of every backward
+// Backward prologue (one launch): the screen accumulators [10][V_s] (rank-indexed) cleared; block 0
+// builds the LPT tile order; with the fused L1 loss, the valid-pixel count of the target depth
+// (reading C20's depth mean): per-block counts, and the last block to finish (atomic ticket,
+// self-resetting) sums them in a fixed order into acc[2] and zeroes the loss sums acc[0..1] that
+// the tile pass accumulates. No memset and no second kernel.
+constexpr int kPrepBlocks = 148 * 4;
 __global__ void __launch_bounds__(256) zero_sgrad_kernel(float* __restrict__ sgrad, int64_t sld,
                                                          const unsigned int* __restrict__ n_on,
                                                          const uint32_t* __restrict__ live_cnt, int T,
-                                                         uint32_t* __restrict__ order) {
+                                                         uint32_t* __restrict__ order, const float* __restrict__ td,
+                                                         int64_t npx, uint32_t* __restrict__ part, double* acc,
+                                                         unsigned int* ticket) {
     // block 0 also builds the backward's LPT tile order from the forward's live-list lengths
     if (blockIdx.x == 0) lpt_tile_order<256>([&](int t) { return live_cnt[t]; }, T, order);
     const int64_t V = int64_t(*n_on);
     for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < V; t += int64_t(gridDim.x) * blockDim.x)
 #pragma unroll
         for (int c = 0; c < 10; ++c) sgrad[c * sld + t] = 0.f;
-}
-
-void launch_zero_sgrad(WsState* s, cudaStream_t st) {
-    KTimer kt(s, KID_SGRAD_CLEAR, st);
-    zero_sgrad_kernel<<<148 * 4, 256, 0, st>>>(at<float>(s, s->sgrad), s->n_cap, &at<Misc>(s, s->misc)->n_onscreen,
-                                               at<uint32_t>(s, s->live_cnt), s->cam_gx * s->cam_gy,
-                                               at<uint32_t>(s, s->tile_order));
-}
-
-// valid-pixel count of the target depth (the L1 depth term's mean, reading C20) into acc[2]
-__global__ void __launch_bounds__(256) valid_count_kernel(const float4* __restrict__ td4, const float* __restrict__ td,
-                                                          int64_t npx, double* acc) {
+    if (!td) return;
     __shared__ uint32_t s_c[8];
+    __shared__ bool s_last;
     uint32_t c = 0;
-    const int64_t n4 = td4 ? npx / 4 : 0;
+    const bool v4 = (reinterpret_cast<uintptr_t>(td) & 15) == 0;
+    const int64_t n4 = v4 ? npx / 4 : 0;
+    const float4* td4 = reinterpret_cast<const float4*>(td);
     for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n4; q += int64_t(gridDim.x) * blockDim.x) {
         const float4 v = td4[q];
         c += (v.x > 0.f) + (v.y > 0.f) + (v.z > 0.f) + (v.w > 0.f);
@@ -885,8 +884,37 @@ __global__ void __launch_bounds__(256) valid_count_kernel(const float4* __restri
     if (threadIdx.x == 0) {
         uint32_t t = 0;
         for (int w = 0; w < 8; ++w) t += s_c[w];
-        if (t) atomicAdd(acc + 2, double(t));
+        part[blockIdx.x] = t;
+        __threadfence();
+        s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    uint32_t t = 0;   // fixed-order sum of the block counts (integers: exact in any order anyway)
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) t += __ldcg(part + b);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) s_c[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t tot = 0;
+        for (int w = 0; w < 8; ++w) tot += s_c[w];
+        acc[0] = 0.0;
+        acc[1] = 0.0;
+        acc[2] = double(tot);
+        *ticket = 0u;
+    }
+}
+
+void launch_zero_sgrad(WsState* s, cudaStream_t st, const float* td_l1, int64_t npx) {
+    KTimer kt(s, KID_SGRAD_CLEAR, st);
+    Misc* misc = at<Misc>(s, s->misc);
+    zero_sgrad_kernel<<<kPrepBlocks, 256, 0, st>>>(at<float>(s, s->sgrad), s->n_cap, &misc->n_onscreen,
+                                                   at<uint32_t>(s, s->live_cnt), s->cam_gx * s->cam_gy,
+                                                   at<uint32_t>(s, s->tile_order), td_l1, npx,
+                                                   at<uint32_t>(s, s->chunk_hist), misc->loss_acc, &misc->prep_done);
 }
 
 __global__ void loss_finalize_kernel(const double* acc, int64_t npx, float wc, float wd, double* loss) {
@@ -912,14 +940,7 @@ void launch_render_bwd_tiles(WsState* s, const gs_camera& cam, const float*, con
     FusedL1 l1{};
     double* acc = at<Misc>(s, s->misc)->loss_acc;
     const int64_t npx = int64_t(cam.width) * cam.height;
-    if (fuse) {
-        l1 = FusedL1{fuse->color, fuse->depth, fuse->tc, fuse->td, fuse->wc, fuse->wd, acc};
-        cudaMemsetAsync(acc, 0, 3 * sizeof(double), st);
-        KTimer kt(s, KID_LOSS_COUNT, st);
-        const bool v4 = (reinterpret_cast<uintptr_t>(fuse->td) & 15) == 0;
-        valid_count_kernel<<<148, 256, 0, st>>>(v4 ? reinterpret_cast<const float4*>(fuse->td) : nullptr, fuse->td, npx,
-                                                acc);
-    }
+    if (fuse) l1 = FusedL1{fuse->color, fuse->depth, fuse->tc, fuse->td, fuse->wc, fuse->wd, acc};   // acc: zero_sgrad_kernel
     {
         KTimer kt(s, KID_BWD_TILE, st);
         auto k = fuse ? render_bwd_kernel<true> : render_bwd_kernel<false>;

@@ -552,7 +552,9 @@ def test_grad_assign_flag():
     torch.cuda.synchronize()
     off = pipe.arrays(n)["tiles"].cpu().numpy() == 0
     assert off.any() and float(got[:, torch.as_tensor(off, device="cuda")].abs().max()) == 0.0
-    np.testing.assert_allclose(got.cpu().numpy(), ref.cpu().numpy(), rtol=1e-5, atol=1e-7)
+    # fp32 atomics order differs between the two runs: a near-cancelling element can move by a few
+    # 1e-7 absolute, so the floor is north_star's 1e-6 absolute gradient floor
+    np.testing.assert_allclose(got.cpu().numpy(), ref.cpu().numpy(), rtol=1e-5, atol=1e-6)
     np.testing.assert_allclose(gp.cpu().numpy(), gp_ref.cpu().numpy(), rtol=1e-4, atol=1e-9)   # atomics order
 
 
