@@ -79,6 +79,7 @@ __global__ void __launch_bounds__((kConsumers + kProducers) * 32) bucket_emit_ke
     const unsigned int* __restrict__ n_on, const unsigned long long* __restrict__ n_keys_eff,
     const unsigned long long* __restrict__ n_keys, int GX, int GY, uint32_t* __restrict__ vals_out) {
     __shared__ EmitSmem sm;
+    griddep_wait();   // PDL (gs_internal.cuh)
     if (*n_keys_eff != *n_keys) return;   // capacity overflow: emit nothing (error flag is set)
     const uint32_t Von = *n_on;
     const int nch = int((Von + kChunk - 1) / kChunk);
@@ -204,7 +205,7 @@ gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaS
         KTimer kt(s, KID_BUCKET_EMIT, st);
         const dim3 grid(unsigned(std::min(nch, kEmitChunkBlocks)), unsigned((s->cam_gx + kBX - 1) / kBX),
                         unsigned((s->cam_gy + kBY - 1) / kBY));
-        bucket_emit_kernel<<<grid, (kConsumers + kProducers) * 32, 0, st>>>(at<uint32_t>(s, s->svals), at<short4>(s, s->srect),
+        launch_pdl(bucket_emit_kernel, grid, dim3((kConsumers + kProducers) * 32), 0, st, at<uint32_t>(s, s->svals), at<short4>(s, s->srect),
                                                  at<uint32_t>(s, s->chunk_mat), &misc->n_onscreen, &misc->n_keys_eff,
                                                  &misc->n_keys, s->cam_gx, s->cam_gy, at<uint32_t>(s, s->vals0));
     } else {

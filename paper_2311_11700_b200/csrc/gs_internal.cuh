@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <utility>
 #include <stdint.h>
 
 #include "../../include/gs.h"
@@ -79,6 +80,28 @@ struct Misc {
     unsigned int prep_done;        // bwd_prep_kernel last-block ticket (self-resetting)
     unsigned int pad;
 };
+
+// Programmatic dependent launch (PDL): kernels of the iteration are launched with programmatic
+// stream serialisation, so a kernel's CTAs can be scheduled while its predecessor's last wave drains;
+// each such kernel waits (griddepcontrol.wait) before touching anything, so data dependencies are
+// exactly those of plain stream order. Without the attribute the wait is a no-op.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // Grid barrier for cooperative launches (all CTAs co-resident): block barrier, one thread fences and
 // arrives on a monotone counter (zeroed before the launch), spins on an acquire load.

@@ -17,6 +17,7 @@ __global__ void __launch_bounds__(256) project_kernel(
     const float* __restrict__ viewmat, gs_camera cam, int GX, int GY, int sh, int orad,
     float4* __restrict__ rec, uint32_t* __restrict__ depth_key, short4* __restrict__ rect,
     int32_t* __restrict__ radius_out, uint32_t* __restrict__ tiles_out) {
+    griddep_wait();   // PDL: the previous kernel's writes (and its reads of what this one writes) are done
     __shared__ float V[12];
     if (threadIdx.x < 12) V[threadIdx.x] = viewmat[threadIdx.x];
     __syncthreads();
@@ -181,7 +182,7 @@ void launch_project(WsState* s, const float* params, int64_t n, int64_t ld, cons
     if (n == 0) return;
     const int blocks = int((n + 255) / 256);
     KTimer kt(s, KID_PROJECT, st);
-    project_kernel<<<blocks, 256, 0, st>>>(params, n, ld, mask, viewmat, cam, GX, GY, s->sh_degree,
+    launch_pdl(project_kernel, dim3(blocks), dim3(256), 0, st, params, n, ld, mask, viewmat, cam, GX, GY, s->sh_degree,
                                            s->opacity_radius, at<float4>(s, s->rec),
                                            at<uint32_t>(s, s->depth_key), at<short4>(s, s->rect),
                                            at<int32_t>(s, s->radius), at<uint32_t>(s, s->tiles));

@@ -330,6 +330,7 @@ __global__ void __launch_bounds__(kTilePx / 2, 6) render_fwd2_kernel(
     float* __restrict__ alpha, float* __restrict__ t_final, uint32_t* __restrict__ n_last,
     uint32_t* __restrict__ examined, uint32_t* __restrict__ live_g, uint32_t* __restrict__ live_j,
     uint32_t* __restrict__ live_cnt) {
+    griddep_wait();   // PDL (gs_internal.cuh)
     using BS = cub::BlockScan<int, kFwd2Batch>;
     __shared__ typename BS::TempStorage scan_tmp;
     constexpr int kU = 4;   // Gaussians per fast-path group (below)
@@ -504,7 +505,7 @@ void launch_render_fwd(WsState* s, const gs_camera& cam, float* color, float* de
             cam.bg[1], cam.bg[2], color, depth, alpha, at<float>(s, s->t_final), at<uint32_t>(s, s->n_last), exam,
             accum_weight, lb.g, lb.j, lb.cnt);
     } else {
-        render_fwd2_kernel<<<ntiles, kTilePx / 2, 0, st>>>(
+        launch_pdl(render_fwd2_kernel, dim3(ntiles), dim3(kTilePx / 2), 0, st,
             at<float4>(s, s->rec), sorted_vals, at<uint2>(s, s->ranges), cam.width, cam.height, s->cam_gx, cam.bg[0],
             cam.bg[1], cam.bg[2], color, depth, alpha, at<float>(s, s->t_final), at<uint32_t>(s, s->n_last), exam,
             lb.g, lb.j, lb.cnt);
@@ -598,6 +599,7 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
     int GX, const float* __restrict__ t_final, float bgr, float bgg, float bgb, const uint32_t* __restrict__ n_last,
     const float* __restrict__ dLdC, const float* __restrict__ dLdD, float* __restrict__ sgrad, int64_t sld,
     FusedL1 l1, const uint32_t* __restrict__ order) {
+    griddep_wait();   // PDL (gs_internal.cuh)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BwdSmem& sm = *reinterpret_cast<BwdSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -857,6 +859,7 @@ __global__ void __launch_bounds__(256) zero_sgrad_kernel(float* __restrict__ sgr
                                                          uint32_t* __restrict__ order, const float* __restrict__ td,
                                                          int64_t npx, uint32_t* __restrict__ part, double* acc,
                                                          unsigned int* ticket) {
+    griddep_wait();   // PDL (gs_internal.cuh)
     // block 0 also builds the backward's LPT tile order from the forward's live-list lengths
     if (blockIdx.x == 0) lpt_tile_order<256>([&](int t) { return live_cnt[t]; }, T, order);
     const int64_t V = int64_t(*n_on);
@@ -911,7 +914,7 @@ __global__ void __launch_bounds__(256) zero_sgrad_kernel(float* __restrict__ sgr
 void launch_zero_sgrad(WsState* s, cudaStream_t st, const float* td_l1, int64_t npx) {
     KTimer kt(s, KID_SGRAD_CLEAR, st);
     Misc* misc = at<Misc>(s, s->misc);
-    zero_sgrad_kernel<<<kPrepBlocks, 256, 0, st>>>(at<float>(s, s->sgrad), s->n_cap, &misc->n_onscreen,
+    launch_pdl(zero_sgrad_kernel, dim3(kPrepBlocks), dim3(256), 0, st, at<float>(s, s->sgrad), s->n_cap, &misc->n_onscreen,
                                                    at<uint32_t>(s, s->live_cnt), s->cam_gx * s->cam_gy,
                                                    at<uint32_t>(s, s->tile_order), td_l1, npx,
                                                    at<uint32_t>(s, s->chunk_hist), misc->loss_acc, &misc->prep_done);
@@ -944,7 +947,7 @@ void launch_render_bwd_tiles(WsState* s, const gs_camera& cam, const float*, con
     {
         KTimer kt(s, KID_BWD_TILE, st);
         auto k = fuse ? render_bwd_kernel<true> : render_bwd_kernel<false>;
-        k<<<ntiles, kBwdThreads, sizeof(BwdSmem), st>>>(
+        launch_pdl(k, dim3(ntiles), dim3(kBwdThreads), sizeof(BwdSmem), st,
             at<float4>(s, s->rec), lb.g, lb.j, lb.cnt, at<uint2>(s, s->ranges), cam.width, cam.height, s->cam_gx,
             at<float>(s, s->t_final), cam.bg[0], cam.bg[1], cam.bg[2], at<uint32_t>(s, s->n_last), dL_dcolor,
             dL_ddepth, at<float>(s, s->sgrad), s->n_cap, l1,
@@ -982,6 +985,7 @@ __global__ void __launch_bounds__(256, kGbwdBlocksPerSM) gaussian_bwd_kernel(
     const float* __restrict__ sgrad, int64_t sld, float* __restrict__ grad, int cov_path,
     double* __restrict__ pose_part, unsigned int* done_ctr, double* __restrict__ grad_pose, LossFin lf,
     const uint32_t* __restrict__ tiles, int zero_blocks) {
+    griddep_wait();   // PDL (gs_internal.cuh)
     constexpr bool assign = ASSIGN;
     __shared__ float V[12];
     __shared__ bool s_last;
@@ -1254,7 +1258,7 @@ void launch_gaussian_bwd(WsState* s, const float* params, int64_t n, int64_t ld,
     const int zero_blocks = (assign && grad_params) ? std::min(sms, int((n + 255) / 256)) : 0;
     auto kern = s->sh_degree == 1 ? (assign ? gaussian_bwd_kernel<1, true> : gaussian_bwd_kernel<1, false>)
                                   : (assign ? gaussian_bwd_kernel<0, true> : gaussian_bwd_kernel<0, false>);
-    kern<<<blocks + zero_blocks, 256, 0, st>>>(
+    launch_pdl(kern, dim3(blocks + zero_blocks), dim3(256), 0, st,
         params, n, ld, viewmat, cam, at<uint32_t>(s, s->onlist), &at<Misc>(s, s->misc)->n_onscreen,
         at<float4>(s, s->rec), at<float>(s, s->sgrad), s->n_cap, grad_params, (flags & GS_FLAG_POSE_COV_PATH) ? 1 : 0,
         part, &at<Misc>(s, s->misc)->pose_done, grad_pose, part ? lf : LossFin{}, at<uint32_t>(s, s->tiles),
