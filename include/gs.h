@@ -181,6 +181,14 @@ gs_status gs_adam_step(float* params_raw, float* params_act, const float* grad_a
                        int64_t n, int64_t ld, const float lr[14] /*(host)*/, int32_t step, float b1, float b2,
                        float eps, void* stream);
 
+/* gs_adam_step_rows — gs_adam_step over `rows` parameter rows: 14 (RGB, identical to gs_adam_step)
+ * or 23 (degree-1 SH, gs_project_sh's layout): rows 3-5 log-scale, row 10
+ * logit-opacity, every other row (mean, quaternion, colour / SH coefficients) identity. lr: host
+ * float[rows]. Other row counts: GS_ERR_INVALID_ARG. */
+gs_status gs_adam_step_rows(float* params_raw, float* params_act, const float* grad_act, float* m, float* v,
+                            int64_t n, int64_t ld, int32_t rows, const float* lr /*(host) [rows]*/, int32_t step,
+                            float b1, float b2, float eps, void* stream);
+
 /* gs_pose_step — Adam on the pose twist (reading C23; "FusedAdam" PAPER.md:954) then
  * T <- exp(delta^) T applied to viewmat in place (device-only, no host sync). m6, v6: float[6]. */
 gs_status gs_pose_step(float* viewmat, const double* grad_pose, float* m6, float* v6, int32_t step,

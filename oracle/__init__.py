@@ -234,7 +234,8 @@ def activate(raw) -> np.ndarray:
 
 def adam_step(raw, grad_act, m, v, lr, step, b1=0.9, b2=0.999, eps=1e-8) -> dict:
     """Textbook Adam (betas/eps unstated -> 0.9/0.999/1e-8) in raw space with the
-    activation chain rule: d/dlog s = s d/ds, d/dlogit o = o(1-o) d/do. lr: 14 per-row rates."""
+    activation chain rule: d/dlog s = s d/ds, d/dlogit o = o(1-o) d/do. lr: one rate per row (14
+    rows, or 23 for the degree-1 SH layout, whose extra rows are identity-activated)."""
     raw = np.asarray(raw, np.float64)
     g = np.asarray(grad_act, np.float64).copy()
     act = activate(raw)
@@ -244,7 +245,7 @@ def adam_step(raw, grad_act, m, v, lr, step, b1=0.9, b2=0.999, eps=1e-8) -> dict
     v = b2 * np.asarray(v, np.float64) + (1 - b2) * g * g
     mh = m / (1 - b1 ** step)
     vh = v / (1 - b2 ** step)
-    lr = np.asarray(lr, np.float64).reshape(14, 1)
+    lr = np.asarray(lr, np.float64).reshape(raw.shape[0], 1)
     new_raw = raw - lr * mh / (np.sqrt(vh) + eps)
     return dict(raw=new_raw, act=activate(new_raw), m=m, v=v)
 

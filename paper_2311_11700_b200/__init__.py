@@ -78,6 +78,7 @@ _SIGS = {
     "gs_render_bwd_l1": (ctypes.c_int, [_P, _I64, _I64, _P, ctypes.POINTER(gs_ws), ctypes.POINTER(gs_camera), _P, _P,
                                         _P, _P, _F, _F, _P, _P, _P, _U32, _P]),
     "gs_pose_extrapolate": (ctypes.c_int, [_P, _P, _P, _P]),
+    "gs_adam_step_rows": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I64, _I32, _P, _I32, _F, _F, _F, _P]),
     "gs_image_half": (ctypes.c_int, [_P, _P, _I32, _I32, _P, _P, _P]),
     "gs_frame_stats": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _F, _F, _P, _P]),
     "gs_loss_l1_masked": (ctypes.c_int, [_P, _P, _P, _P, _P, _F, _F, _I32, _I32, _F, _F, _P, _P, _P, ctypes.POINTER(gs_ws),
@@ -301,6 +302,14 @@ def gs_loss_l1_masked(color, depth, tgt_color, tgt_depth, alpha, alpha_min, outl
     _check(_lib.gs_loss_l1_masked(_ptr(color), _ptr(depth), _ptr(tgt_color), _ptr(tgt_depth), _ptr(alpha), alpha_min,
                                   outlier_k, width, height, w_color, w_depth, _ptr(dL_dcolor), _ptr(dL_ddepth), _ptr(loss),
                                   ctypes.byref(ws.state), _stream(stream)), "gs_loss_l1_masked")
+
+
+def gs_adam_step_rows(params_raw, params_act, grad_act, m, v, n, ld, rows, lr, step, b1=0.9, b2=0.999, eps=1e-8,
+                      stream=None):
+    lr_arr = (ctypes.c_float * rows)(*[float(x) for x in lr])
+    _check(_lib.gs_adam_step_rows(_ptr(params_raw), _ptr(params_act), _ptr(grad_act), _ptr(m), _ptr(v), n, ld, rows,
+                                  ctypes.cast(lr_arr, ctypes.c_void_p), step, b1, b2, eps, _stream(stream)),
+           "gs_adam_step_rows")
 
 
 def gs_adam_step(params_raw, params_act, grad_act, m, v, n, ld, lr, step, b1=0.9, b2=0.999, eps=1e-8, stream=None):

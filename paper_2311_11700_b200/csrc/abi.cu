@@ -286,8 +286,20 @@ gs_status gs_adam_step(float* params_raw, float* params_act, const float* grad_a
                        int64_t ld, const float lr[14], int32_t step, float b1, float b2, float eps, void* stream) {
     if ((n > 0 && (!params_raw || !params_act || !grad_act || !m || !v)) || !lr || n < 0 || ld < n || step < 1)
         return GS_ERR_INVALID_ARG;
-    launch_adam(params_raw, params_act, grad_act, m, v, n, ld, lr, step, b1, b2, eps, static_cast<cudaStream_t>(stream));
+    launch_adam(params_raw, params_act, grad_act, m, v, n, ld, lr, 14, step, b1, b2, eps,
+                static_cast<cudaStream_t>(stream));
     return check_launch(nullptr, "gs_adam_step");
+}
+
+gs_status gs_adam_step_rows(float* params_raw, float* params_act, const float* grad_act, float* m, float* v,
+                            int64_t n, int64_t ld, int32_t rows, const float* lr, int32_t step, float b1, float b2,
+                            float eps, void* stream) {
+    if ((n > 0 && (!params_raw || !params_act || !grad_act || !m || !v)) || !lr || n < 0 || ld < n || step < 1 ||
+        (rows != 14 && rows != 23))
+        return GS_ERR_INVALID_ARG;
+    launch_adam(params_raw, params_act, grad_act, m, v, n, ld, lr, rows, step, b1, b2, eps,
+                static_cast<cudaStream_t>(stream));
+    return check_launch(nullptr, "gs_adam_step_rows");
 }
 
 gs_status gs_pose_step(float* viewmat, const double* grad_pose, float* m6, float* v6, int32_t step, float lr_rho,

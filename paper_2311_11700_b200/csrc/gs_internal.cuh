@@ -190,8 +190,8 @@ void launch_frame_stats(const float* alpha, const float* depth, const float* td,
                         float tdep, uint32_t* counts, cudaStream_t st);
 void launch_pose_extrapolate(const float* t1, const float* t2, float* out, cudaStream_t st);
 void launch_image_half(const float* c, const float* d, int32_t W, int32_t H, float* ch, float* dh, cudaStream_t st);
-void launch_adam(float* raw, float* act, const float* g, float* m, float* v, int64_t n, int64_t ld,
-                 const float lr[14], int32_t step, float b1, float b2, float eps, cudaStream_t st);
+void launch_adam(float* raw, float* act, const float* g, float* m, float* v, int64_t n, int64_t ld, const float* lr,
+                 int32_t rows, int32_t step, float b1, float b2, float eps, cudaStream_t st);
 void launch_pose_step(float* viewmat, const double* gp, float* m6, float* v6, int32_t step, float lr_rho,
                       float lr_phi, cudaStream_t st);
 void launch_append(float* params, float* raw, float* m, float* v, int64_t* n_dev, int64_t capacity, int64_t ld,

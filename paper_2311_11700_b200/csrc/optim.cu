@@ -464,7 +464,7 @@ void launch_pose_extrapolate(const float* t1, const float* t2, float* out, cudaS
 }
 
 // ------------------------------------------------------------------ Adam
-struct Lr14 { float v[14]; };
+struct Lr14 { float v[23]; };   // per-row rates: 14 (RGB) or 23 (degree-1 SH) rows
 
 __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ raw, float* __restrict__ act,
                                                    const float* __restrict__ g, float* __restrict__ m,
@@ -488,13 +488,13 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ raw, floa
     }
 }
 
-void launch_adam(float* raw, float* act, const float* g, float* m, float* v, int64_t n, int64_t ld, const float lr[14],
-                 int32_t step, float b1, float b2, float eps, cudaStream_t st) {
+void launch_adam(float* raw, float* act, const float* g, float* m, float* v, int64_t n, int64_t ld, const float* lr,
+                 int32_t rows, int32_t step, float b1, float b2, float eps, cudaStream_t st) {
     if (n == 0) return;
-    Lr14 l;
-    for (int k = 0; k < 14; ++k) l.v[k] = lr[k];
+    Lr14 l{};
+    for (int k = 0; k < rows; ++k) l.v[k] = lr[k];
     const float bc1 = float(1.0 - std::pow(double(b1), step)), bc2 = float(1.0 - std::pow(double(b2), step));
-    dim3 grid(unsigned(std::min<int64_t>((n + 255) / 256, 148 * 2)), 14);
+    dim3 grid(unsigned(std::min<int64_t>((n + 255) / 256, 148 * 2)), unsigned(rows));
     adam_kernel<<<grid, 256, 0, st>>>(raw, act, g, m, v, n, ld, l, b1, b2, eps, bc1, bc2);
 }
 

@@ -204,22 +204,27 @@ def test_loss_parity(W, H):
     assert abs(pipe.loss.item() - o["loss"]) <= 1e-6 * abs(o["loss"])
 
 
-def test_adam_parity():
+@pytest.mark.parametrize("rows", [14, 23])
+def test_adam_parity(rows):
+    """gs_adam_step (14 rows) and gs_adam_step_rows (23: degree-1 SH layout) against the fp64 oracle."""
     import paper_2311_11700_b200 as g
     rng = np.random.default_rng(3)
     n, ld = 1000, 1024
-    raw = rng.normal(size=(14, ld)).astype(np.float32)
-    lr = [1.6e-5] * 3 + [2e-4] * 3 + [4e-5] * 4 + [1e-2] + [5e-4] * 3
+    raw = rng.normal(size=(rows, ld)).astype(np.float32)
+    lr = [1.6e-5] * 3 + [2e-4] * 3 + [4e-5] * 4 + [1e-2] + [5e-4] * (rows - 11)
     R = to_dev(raw)
     A = torch.zeros_like(R)
     M = torch.zeros_like(R)
     Vv = torch.zeros_like(R)
-    m = np.zeros((14, n))
-    vv = np.zeros((14, n))
+    m = np.zeros((rows, n))
+    vv = np.zeros((rows, n))
     r64 = raw[:, :n].astype(np.float64)
     for step in (1, 2, 3):
-        gr = rng.normal(size=(14, ld)).astype(np.float32)
-        g.gs_adam_step(R, A, to_dev(gr), M, Vv, n, ld, lr, step)
+        gr = rng.normal(size=(rows, ld)).astype(np.float32)
+        if rows == 14:
+            g.gs_adam_step(R, A, to_dev(gr), M, Vv, n, ld, lr, step)
+        else:
+            g.gs_adam_step_rows(R, A, to_dev(gr), M, Vv, n, ld, rows, lr, step)
         out = oracle.adam_step(r64, gr[:, :n], m, vv, lr, step)
         r64, m, vv = out["raw"], out["m"], out["v"]
     torch.cuda.synchronize()

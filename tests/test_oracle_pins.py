@@ -439,31 +439,34 @@ def test_loss_l1_brute_force():
     assert L["dL_dcolor"][1, 1, 2] == math.copysign(0.9 / (3 * H * W), c[1, 1, 2] - tc[1, 1, 2])
 
 
-def test_adam_matches_torch():
+@pytest.mark.parametrize("rows", [14, 23])
+def test_adam_matches_torch(rows):
+    """O5 Adam against torch.optim.Adam with autograd through the activations; 23 rows is the
+    degree-1 SH layout (rows 11-22 identity-activated)."""
     torch = pytest.importorskip("torch")
     rng = np.random.default_rng(4)
     n = 7
-    raw = rng.normal(size=(14, n))
-    lr = [1.6e-5] * 3 + [2e-4] * 3 + [4e-5] * 4 + [1e-2] + [5e-4] * 3
-    m = np.zeros((14, n))
-    v = np.zeros((14, n))
+    raw = rng.normal(size=(rows, n))
+    lr = [1.6e-5] * 3 + [2e-4] * 3 + [4e-5] * 4 + [1e-2] + [5e-4] * (rows - 11)
+    m = np.zeros((rows, n))
+    v = np.zeros((rows, n))
     traw = torch.tensor(raw, dtype=torch.float64, requires_grad=True)
     groups = [{"params": [], "lr": r} for r in lr]
-    rows = [torch.nn.Parameter(traw[k].detach().clone()) for k in range(14)]
-    for k in range(14):
-        groups[k]["params"] = [rows[k]]
+    prm = [torch.nn.Parameter(traw[k].detach().clone()) for k in range(rows)]
+    for k in range(rows):
+        groups[k]["params"] = [prm[k]]
     opt = torch.optim.Adam(groups, betas=(0.9, 0.999), eps=1e-8)
     for step in range(1, 4):
-        gact = rng.normal(size=(14, n))
+        gact = rng.normal(size=(rows, n))
         out = oracle.adam_step(raw, gact, m, v, lr, step)
         opt.zero_grad()
-        act = [rows[k] for k in range(14)]
-        act[3:6] = [torch.exp(rows[k]) for k in range(3, 6)]
-        act[10] = torch.sigmoid(rows[10])
+        act = [prm[k] for k in range(rows)]
+        act[3:6] = [torch.exp(prm[k]) for k in range(3, 6)]
+        act[10] = torch.sigmoid(prm[10])
         sum((a * torch.tensor(gact[k])).sum() for k, a in enumerate(act)).backward()
         opt.step()
         raw, m, v = out["raw"], out["m"], out["v"]
-        np.testing.assert_allclose(raw, np.stack([r.detach().numpy() for r in rows]), rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(raw, np.stack([r.detach().numpy() for r in prm]), rtol=1e-12, atol=1e-15)
 
 
 def test_se3_exp_matches_expm():
