@@ -268,6 +268,9 @@ typedef struct {
     int32_t stride;
     int64_t max_add;
     float eta, gamma;        /* DEGENERATE: opacity factor (0.1) and floater margin in metres (0.10) */
+    int32_t rows;            /* parameter rows: 0 or 14 = RGB, 23 = degree-1 SH (ADD writes the colour as
+                                the DC coefficient (c - 1/2)/C0 and zero linear terms, reading C34; PRUNE
+                                compacts all rows; other values: GS_ERR_INVALID_ARG) */
 } gs_densify_cfg;
 gs_status gs_densify_prune(float* params, float* params_raw /*nullable*/, int64_t* n_dev, int64_t capacity,
                            int64_t ld, float* adam_m /*nullable*/, float* adam_v /*nullable*/, const float* alpha,
@@ -286,7 +289,8 @@ gs_status gs_densify_prune(float* params, float* params_raw /*nullable*/, int64_
 gs_status gs_densify_accum_grad(gs_ws* ws, float* grad_accum, float* count, void* stream);
 
 /* gs_densify_split_clone — one densification step (every 10 mapping iterations before the 70th,
- * thresholds 0.002 and 0.02 m; reading C30) over params[14][ld] columns [0, n):
+ * thresholds 0.002 and 0.02 m; reading C30) over params[rows][ld] columns [0, n)
+ * (rows 14, or 23 for degree-1 SH: children copy the SH rows):
  * avg_i = grad_accum_i / count_i (0 if count_i == 0); i is a candidate iff avg_i >= grad_thresh;
  * a candidate with max scale <= scale_thresh is CLONED (a copy appended), otherwise SPLIT: two
  * children X + R(q) diag(s) eps_k, k = 0, 1 (eps_k = noise rows 3k..3k+2 at column i, N(0,1) drawn by
@@ -299,16 +303,17 @@ gs_status gs_densify_accum_grad(gs_ws* ws, float* grad_accum, float* count, void
 gs_status gs_densify_split_clone(float* params, float* params_raw /*nullable*/, float* adam_m /*nullable*/,
                                  float* adam_v /*nullable*/, int64_t* n_dev, int64_t capacity, int64_t ld,
                                  float* grad_accum, float* count, const float* noise, float grad_thresh,
-                                 float scale_thresh, gs_ws* ws, void* stream);
+                                 float scale_thresh, int32_t rows /*14 or 23*/, gs_ws* ws, void* stream);
 
 /* gs_densify_append — append gathered ADD candidates (multi-GPU mapping):
- * cand[k][14][max_add] (activated, k < n_sets, in global keyframe order) with counts[k] (device
- * int64) are appended in order k = 0, 1, ... at columns [n, n + sum counts) of params[14][ld]
+ * cand[k][rows][max_add] (activated, k < n_sets, in global keyframe order; rows 14 or 23) with
+ * counts[k] (device int64) are appended in order k = 0, 1, ... at columns [n, n + sum counts) of params[rows][ld]
  * (raw copies: log-scale / logit-opacity; zero Adam moments), truncated at capacity; n_dev updated.
  * Deterministic: every rank appending the same gathered sets produces identical parameters. */
 gs_status gs_densify_append(float* params, float* params_raw /*nullable*/, float* adam_m /*nullable*/,
                             float* adam_v /*nullable*/, int64_t* n_dev, int64_t capacity, int64_t ld,
-                            const float* cand, const int64_t* counts, int32_t n_sets, int64_t max_add, void* stream);
+                            const float* cand, const int64_t* counts, int32_t n_sets, int64_t max_add,
+                            int32_t rows /*14 or 23*/, void* stream);
 
 /* Introspection for tests and benchmarks (host struct of device pointers into the workspace). */
 typedef struct {

@@ -295,11 +295,12 @@ def pose_adam_step(view, grad_twist, m6, v6, step, lr_rho, lr_phi, b1=0.9, b2=0.
 
 
 def densify_add(alpha, depth, tgt_color, tgt_depth, view, cam, tau_alpha=0.5, tau_depth=0.10, stride=2,
-                init_opacity=0.5, max_add=None) -> np.ndarray:
+                init_opacity=0.5, max_add=None, sh_degree=0) -> np.ndarray:
     """Eq. 8 (P:118-125): unreliable iff T < tau_T or |D - D_hat| > tau_D (T = alpha image);
     restricted to valid target depth and the stride-2 checkerboard ((u+v) % 2 == 0, the HW/2 of
     Eq. 7), ordered by pixel index; back-projected from the target depth through the inverse
-    pose; init per reading C22. Returns activated params [14][n_add]."""
+    pose; init per reading C22. Returns activated params [14][n_add], or [23][n_add] with sh_degree=1
+    (reading C34: the colour becomes the DC coefficient (c - 1/2)/C0 in fp32, linear terms 0)."""
     a = np.asarray(alpha, np.float64)
     d = np.asarray(depth, np.float64)
     td = np.asarray(tgt_depth, np.float64)
@@ -316,12 +317,15 @@ def densify_add(alpha, depth, tgt_color, tgt_depth, view, cam, tau_alpha=0.5, ta
     xc = np.stack([(u - cam.cx) / cam.fx * z, (v - cam.cy) / cam.fy * z, z])
     V = np.asarray(view, np.float64)
     X = V[:, :3].T @ (xc - V[:, 3:4])
-    out = np.zeros((14, idx.size))
+    out = np.zeros((23 if sh_degree == 1 else 14, idx.size))
     out[0:3] = X
     out[3:6] = z * stride / (cam.fx + cam.fy)
     out[6] = 1.0
     out[10] = init_opacity
     out[11:14] = tc.reshape(3, -1)[:, idx]
+    if sh_degree == 1:
+        c = tc.reshape(3, -1)[:, idx].astype(np.float32)
+        out[11:14] = (c - np.float32(0.5)) / np.float32(0.28209479177387814)
     return out
 
 

@@ -59,7 +59,7 @@ class gs_densify_cfg(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int32), ("tau_alpha", ctypes.c_float), ("tau_depth", ctypes.c_float),
                 ("min_opacity", ctypes.c_float), ("sel_weight", ctypes.c_float), ("sel_depth", ctypes.c_float),
                 ("init_opacity", ctypes.c_float), ("stride", ctypes.c_int32), ("max_add", ctypes.c_int64),
-                ("eta", ctypes.c_float), ("gamma", ctypes.c_float)]
+                ("eta", ctypes.c_float), ("gamma", ctypes.c_float), ("rows", ctypes.c_int32)]
 
 
 _P = ctypes.c_void_p
@@ -73,7 +73,7 @@ _SIGS = {
     "gs_ws_init": (ctypes.c_int, [ctypes.POINTER(gs_ws), _P, ctypes.c_size_t, _I64, _I64, _I32, _I32]),
     "gs_project": (ctypes.c_int, [_P, _I64, _I64, _P, _P, ctypes.POINTER(gs_camera), ctypes.POINTER(gs_ws), _P]),
     "gs_densify_accum_grad": (ctypes.c_int, [ctypes.POINTER(gs_ws), _P, _P, _P]),
-    "gs_densify_split_clone": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _F, _F, ctypes.POINTER(gs_ws),
+    "gs_densify_split_clone": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _F, _F, _I32, ctypes.POINTER(gs_ws),
                                               _P]),
     "gs_render_bwd_l1": (ctypes.c_int, [_P, _I64, _I64, _P, ctypes.POINTER(gs_ws), ctypes.POINTER(gs_camera), _P, _P,
                                         _P, _P, _F, _F, _P, _P, _P, _U32, _P]),
@@ -99,7 +99,7 @@ _SIGS = {
     "gs_densify_prune": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P,
                                         ctypes.POINTER(gs_camera), ctypes.POINTER(gs_densify_cfg), _P, _P,
                                         ctypes.POINTER(gs_ws), _P]),
-    "gs_densify_append": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I64, _P, _P, _I32, _I64, _P]),
+    "gs_densify_append": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I64, _P, _P, _I32, _I64, _I32, _P]),
     "gs_ws_get_view": (ctypes.c_int, [ctypes.POINTER(gs_ws), ctypes.POINTER(gs_ws_view)]),
     "gs_ws_launch_count": (_I64, [ctypes.POINTER(gs_ws)]),
     "gs_ws_set_event_log": (ctypes.c_int, [ctypes.POINTER(gs_ws), _P, _P, _I32]),
@@ -324,11 +324,11 @@ def gs_pose_step(viewmat, grad_pose, m6, v6, step, lr_rho, lr_phi, stream=None):
 
 
 def densify_cfg(mode, tau_alpha=0.5, tau_depth=0.10, min_opacity=0.005, sel_weight=0.5, sel_depth=0.05,
-                init_opacity=0.5, stride=2, max_add=0, eta=0.1, gamma=0.10) -> gs_densify_cfg:
+                init_opacity=0.5, stride=2, max_add=0, eta=0.1, gamma=0.10, rows=14) -> gs_densify_cfg:
     c = gs_densify_cfg()
     c.mode, c.tau_alpha, c.tau_depth, c.min_opacity = mode, tau_alpha, tau_depth, min_opacity
     c.sel_weight, c.sel_depth, c.init_opacity, c.stride, c.max_add = sel_weight, sel_depth, init_opacity, stride, max_add
-    c.eta, c.gamma = eta, gamma
+    c.eta, c.gamma, c.rows = eta, gamma, rows
     return c
 
 
@@ -348,16 +348,17 @@ def gs_densify_accum_grad(ws: Workspace, grad_accum, count, stream=None):
 
 
 def gs_densify_split_clone(params, params_raw, adam_m, adam_v, n_dev, capacity, ld, grad_accum, count, noise,
-                           grad_thresh, scale_thresh, ws: Workspace, stream=None):
+                           grad_thresh, scale_thresh, ws: Workspace, stream=None, rows=14):
     _check(_lib.gs_densify_split_clone(_ptr(params), _ptr(params_raw), _ptr(adam_m), _ptr(adam_v), _ptr(n_dev), capacity,
                                        ld, _ptr(grad_accum), _ptr(count), _ptr(noise), grad_thresh, scale_thresh,
-                                       ctypes.byref(ws.state), _stream(stream)), "gs_densify_split_clone")
+                                       rows, ctypes.byref(ws.state), _stream(stream)), "gs_densify_split_clone")
 
 
 def gs_densify_append(params, params_raw, adam_m, adam_v, n_dev, capacity, ld, cand, counts, n_sets, max_add,
-                      stream=None):
+                      stream=None, rows=14):
     _check(_lib.gs_densify_append(_ptr(params), _ptr(params_raw), _ptr(adam_m), _ptr(adam_v), _ptr(n_dev), capacity,
-                                  ld, _ptr(cand), _ptr(counts), n_sets, max_add, _stream(stream)), "gs_densify_append")
+                                  ld, _ptr(cand), _ptr(counts), n_sets, max_add, rows, _stream(stream)),
+           "gs_densify_append")
 
 
 from .pipeline import Frame, RenderPipeline  # noqa: E402  (convenience layer over the calls above)

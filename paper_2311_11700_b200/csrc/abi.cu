@@ -62,7 +62,7 @@ static void carve(WsState* s, Carver& c) {
     s->sort_look = c.take(uint64_t(s->max_parts) * 256 * 8);
     s->misc = c.take(sizeof(Misc));
     s->scratch = c.take(uint64_t(px) * 4 * 4);
-    s->scratch14 = c.take(uint64_t(n) * 4 * 14);
+    s->scratch14 = c.take(uint64_t(n) * 4 * 23);   // compaction scratch: up to 23 parameter rows
     s->dkey_sorted = c.take(uint64_t(n) * 4 * 2);
     s->dval_sorted = c.take(uint64_t(n) * 4 * 2);
     // densify block counts; also the backward prologue's per-block valid counts (148 * 4 blocks)
@@ -316,6 +316,7 @@ gs_status gs_densify_prune(float* params, float* params_raw, int64_t* n_dev, int
                            uint8_t* select_mask, float* add_out, gs_ws* ws, void* stream) {
     if (!ws_ok(ws) || !cfg || !n_dev || capacity < 0 || ld < capacity) return GS_ERR_INVALID_ARG;
     WsState* s = state(ws);
+    if (cfg->rows != 0 && cfg->rows != 14 && cfg->rows != 23) return GS_ERR_INVALID_ARG;
     switch (cfg->mode) {
         case GS_DENSIFY_ADD:
             if (!params || !alpha || !depth || !target_rgb || !target_depth || !viewmat || !cam_ok(s, cam) ||
@@ -354,11 +355,11 @@ gs_status gs_densify_prune(float* params, float* params_raw, int64_t* n_dev, int
 
 gs_status gs_densify_append(float* params, float* params_raw, float* adam_m, float* adam_v, int64_t* n_dev,
                             int64_t capacity, int64_t ld, const float* cand, const int64_t* counts, int32_t n_sets,
-                            int64_t max_add, void* stream) {
+                            int64_t max_add, int32_t rows, void* stream) {
     if (!params || !n_dev || capacity < 0 || ld < capacity || n_sets < 0 || max_add < 0 ||
-        (n_sets > 0 && (!cand || !counts)))
+        (n_sets > 0 && (!cand || !counts)) || (rows != 14 && rows != 23))
         return GS_ERR_INVALID_ARG;
-    launch_append(params, params_raw, adam_m, adam_v, n_dev, capacity, ld, cand, counts, n_sets, max_add,
+    launch_append(params, params_raw, adam_m, adam_v, n_dev, capacity, ld, cand, counts, n_sets, max_add, rows,
                   static_cast<cudaStream_t>(stream));
     return check_launch(nullptr, "gs_densify_append");
 }
@@ -373,14 +374,14 @@ gs_status gs_densify_accum_grad(gs_ws* ws, float* grad_accum, float* count, void
 
 gs_status gs_densify_split_clone(float* params, float* params_raw, float* adam_m, float* adam_v, int64_t* n_dev,
                                  int64_t capacity, int64_t ld, float* grad_accum, float* count, const float* noise,
-                                 float grad_thresh, float scale_thresh, gs_ws* ws, void* stream) {
+                                 float grad_thresh, float scale_thresh, int32_t rows, gs_ws* ws, void* stream) {
     if (!ws_ok(ws) || !params || !n_dev || !grad_accum || !count || !noise || capacity < 0 || ld < capacity ||
-        !(grad_thresh >= 0.f) || !(scale_thresh >= 0.f))
+        !(grad_thresh >= 0.f) || !(scale_thresh >= 0.f) || (rows != 14 && rows != 23))
         return GS_ERR_INVALID_ARG;
     WsState* s = state(ws);
     if (capacity > s->n_cap) return GS_ERR_INVALID_ARG;
     return run_split_clone(s, params, params_raw, adam_m, adam_v, n_dev, capacity, ld, grad_accum, count, noise,
-                           grad_thresh, scale_thresh, static_cast<cudaStream_t>(stream));
+                           grad_thresh, scale_thresh, rows, static_cast<cudaStream_t>(stream));
 }
 
 gs_status gs_ws_get_view(const gs_ws* ws, gs_ws_view* out) {

@@ -195,11 +195,12 @@ void launch_adam(float* raw, float* act, const float* g, float* m, float* v, int
 void launch_pose_step(float* viewmat, const double* gp, float* m6, float* v6, int32_t step, float lr_rho,
                       float lr_phi, cudaStream_t st);
 void launch_append(float* params, float* raw, float* m, float* v, int64_t* n_dev, int64_t capacity, int64_t ld,
-                   const float* cand, const int64_t* counts, int32_t n_sets, int64_t max_add, cudaStream_t st);
+                   const float* cand, const int64_t* counts, int32_t n_sets, int64_t max_add, int32_t rows,
+                   cudaStream_t st);
 void launch_accum_grad(WsState* s, float* grad_accum, float* count, cudaStream_t st);
 gs_status run_split_clone(WsState* s, float* params, float* raw, float* m, float* v, int64_t* n_dev, int64_t capacity,
                           int64_t ld, float* grad_accum, float* count, const float* noise, float grad_thresh,
-                          float scale_thresh, cudaStream_t st);
+                          float scale_thresh, int32_t rows, cudaStream_t st);
 gs_status run_densify(WsState* s, float* params, float* raw, int64_t* n_dev, int64_t capacity, int64_t ld,
                       float* m, float* v, const float* alpha, const float* depth, const float* trgb,
                       const float* tdepth, const float* accum, const float* viewmat, const gs_camera& cam,

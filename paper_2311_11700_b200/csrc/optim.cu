@@ -608,6 +608,8 @@ __global__ void __launch_bounds__(kCmpThreads) scatter_kernel(int64_t n, const i
         if (f[k]) emit(base + k, o++);
 }
 
+constexpr int kMaxRows = 23;   // parameter rows: 14 (RGB) or 23 (degree-1 SH)
+
 struct AddPred {
     const float *alpha, *depth, *td;
     int W;
@@ -633,6 +635,7 @@ struct AddEmit {
     float* out;      // nullable: [14][max_add] candidate records
     int64_t ld, capacity, max_add;
     const int64_t* n_dev;
+    int rows;        // 14 (RGB) or 23 (degree-1 SH: colour as the DC coefficient, reading C34)
     __device__ void operator()(int64_t p, uint32_t o) const {
         if (int64_t(o) >= max_add) return;
         const int64_t n = *n_dev;
@@ -642,7 +645,7 @@ struct AddEmit {
         const float* V = viewmat;
         // X = W^T (X^c - t)
         const float a0 = xc - V[3], a1 = yc - V[7], a2 = zc - V[11];
-        float rec[14];
+        float rec[kMaxRows];
         rec[0] = V[0] * a0 + V[4] * a1 + V[8] * a2;
         rec[1] = V[1] * a0 + V[5] * a1 + V[9] * a2;
         rec[2] = V[2] * a0 + V[6] * a1 + V[10] * a2;
@@ -651,23 +654,26 @@ struct AddEmit {
         rec[6] = 1.f;
         rec[7] = rec[8] = rec[9] = 0.f;
         rec[10] = init_o;
-        rec[11] = trgb[p];
-        rec[12] = trgb[npx + p];
-        rec[13] = trgb[2 * npx + p];
+        for (int c = 0; c < 3; ++c) {
+            const float col = trgb[c * npx + p];
+            // SH: the DC coefficient whose view-independent colour 1/2 + C0 Y0 is the target colour
+            rec[11 + c] = rows == 23 ? (col - 0.5f) / 0.28209479177387814f : col;
+        }
+        for (int k = 14; k < rows; ++k) rec[k] = 0.f;
         if (out) {
-            for (int k = 0; k < 14; ++k) out[k * max_add + o] = rec[k];
+            for (int k = 0; k < rows; ++k) out[k * max_add + o] = rec[k];
             return;
         }
         const int64_t col = n + o;
         if (col >= capacity) return;
-        for (int k = 0; k < 14; ++k) params[k * ld + col] = rec[k];
+        for (int k = 0; k < rows; ++k) params[k * ld + col] = rec[k];
         if (raw) {
-            for (int k = 0; k < 14; ++k) raw[k * ld + col] = rec[k];
+            for (int k = 0; k < rows; ++k) raw[k * ld + col] = rec[k];
             for (int k = 3; k < 6; ++k) raw[k * ld + col] = logf(s);
             raw[10 * ld + col] = logf(init_o / (1.f - init_o));
         }
-        if (m) for (int k = 0; k < 14; ++k) m[k * ld + col] = 0.f;
-        if (v) for (int k = 0; k < 14; ++k) v[k * ld + col] = 0.f;
+        if (m) for (int k = 0; k < rows; ++k) m[k * ld + col] = 0.f;
+        if (v) for (int k = 0; k < rows; ++k) v[k * ld + col] = 0.f;
     }
 };
 
@@ -680,25 +686,26 @@ __global__ void add_count_out_kernel(int64_t* n_dev, const unsigned long long* c
 __global__ void __launch_bounds__(256) append_kernel(float* __restrict__ params, float* __restrict__ raw,
                                                      float* __restrict__ m, float* __restrict__ v, int64_t* n_dev,
                                                      int64_t capacity, int64_t ld, const float* __restrict__ cand,
-                                                     const int64_t* __restrict__ counts, int n_sets, int64_t max_add) {
+                                                     const int64_t* __restrict__ counts, int n_sets, int64_t max_add,
+                                                     int rows) {
     const int64_t n = *n_dev;
     const int set = blockIdx.y;
     int64_t off = 0;
     for (int k = 0; k < set; ++k) off += counts[k];
     const int64_t cnt = counts[set];
-    const float* src = cand + size_t(set) * 14 * max_add;
+    const float* src = cand + size_t(set) * rows * max_add;
     for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < cnt; j += int64_t(gridDim.x) * blockDim.x) {
         const int64_t col = n + off + j;
         if (col >= capacity) break;
-        for (int k = 0; k < 14; ++k) params[k * ld + col] = src[k * max_add + j];
+        for (int k = 0; k < rows; ++k) params[k * ld + col] = src[k * max_add + j];
         if (raw) {
-            for (int k = 0; k < 14; ++k) raw[k * ld + col] = src[k * max_add + j];
+            for (int k = 0; k < rows; ++k) raw[k * ld + col] = src[k * max_add + j];
             for (int k = 3; k < 6; ++k) raw[k * ld + col] = logf(src[k * max_add + j]);
             const float o = src[10 * max_add + j];
             raw[10 * ld + col] = logf(o / (1.f - o));
         }
-        if (m) for (int k = 0; k < 14; ++k) m[k * ld + col] = 0.f;
-        if (v) for (int k = 0; k < 14; ++k) v[k * ld + col] = 0.f;
+        if (m) for (int k = 0; k < rows; ++k) m[k * ld + col] = 0.f;
+        if (v) for (int k = 0; k < rows; ++k) v[k * ld + col] = 0.f;
     }
 }
 
@@ -709,10 +716,11 @@ __global__ void append_commit_kernel(int64_t* n_dev, const int64_t* counts, int 
 }
 
 void launch_append(float* params, float* raw, float* m, float* v, int64_t* n_dev, int64_t capacity, int64_t ld,
-                   const float* cand, const int64_t* counts, int32_t n_sets, int64_t max_add, cudaStream_t st) {
+                   const float* cand, const int64_t* counts, int32_t n_sets, int64_t max_add, int32_t rows,
+                   cudaStream_t st) {
     if (n_sets <= 0 || max_add <= 0) return;
     dim3 grid(unsigned(std::min<int64_t>((max_add + 255) / 256, 64)), unsigned(n_sets));
-    append_kernel<<<grid, 256, 0, st>>>(params, raw, m, v, n_dev, capacity, ld, cand, counts, n_sets, max_add);
+    append_kernel<<<grid, 256, 0, st>>>(params, raw, m, v, n_dev, capacity, ld, cand, counts, n_sets, max_add, rows);
     append_commit_kernel<<<1, 1, 0, st>>>(n_dev, counts, n_sets, capacity);
 }
 
@@ -734,8 +742,9 @@ struct GatherEmit {
     const float* src;
     float* dst;
     int64_t src_ld, dst_ld;
+    int rows;
     __device__ void operator()(int64_t i, uint32_t o) const {
-        for (int k = 0; k < 14; ++k) dst[k * dst_ld + o] = src[k * src_ld + i];
+        for (int k = 0; k < rows; ++k) dst[k * dst_ld + o] = src[k * src_ld + i];
     }
 };
 
@@ -794,20 +803,21 @@ struct SplitCloneEmit {   // appends clones (type 1) or split children (type 2)
     const int64_t* n_dev;
     const unsigned long long* n_clone;   // clones found (type 2 pass: the clones applied come first)
     int type;
+    int rows;                            // 14 or 23: children copy every row but mean and scale
     __device__ void put(int64_t col, const float* rec) const {
-        for (int k = 0; k < 14; ++k) params[k * ld + col] = rec[k];
+        for (int k = 0; k < rows; ++k) params[k * ld + col] = rec[k];
         if (raw) {
-            for (int k = 0; k < 14; ++k) raw[k * ld + col] = rec[k];
+            for (int k = 0; k < rows; ++k) raw[k * ld + col] = rec[k];
             for (int k = 3; k < 6; ++k) raw[k * ld + col] = logf(rec[k]);
             raw[10 * ld + col] = logf(rec[10] / (1.f - rec[10]));
         }
-        if (m) for (int k = 0; k < 14; ++k) m[k * ld + col] = 0.f;
-        if (v) for (int k = 0; k < 14; ++k) v[k * ld + col] = 0.f;
+        if (m) for (int k = 0; k < rows; ++k) m[k * ld + col] = 0.f;
+        if (v) for (int k = 0; k < rows; ++k) v[k * ld + col] = 0.f;
     }
     __device__ void operator()(int64_t i, uint32_t o) const {
         const int64_t n = *n_dev, avail = capacity - n;
-        float rec[14];
-        for (int k = 0; k < 14; ++k) rec[k] = params[k * ld + i];
+        float rec[kMaxRows];
+        for (int k = 0; k < rows; ++k) rec[k] = params[k * ld + i];
         if (type == 1) {
             if (int64_t(o) < avail) put(n + o, rec);
             return;
@@ -821,9 +831,9 @@ struct SplitCloneEmit {   // appends clones (type 1) or split children (type 2)
         const float R[3][3] = {{1.f - 2.f * (y * y + z * z), 2.f * (x * y - r * z), 2.f * (x * z + r * y)},
                                {2.f * (x * y + r * z), 1.f - 2.f * (x * x + z * z), 2.f * (y * z - r * x)},
                                {2.f * (x * z - r * y), 2.f * (y * z + r * x), 1.f - 2.f * (x * x + y * y)}};
-        float child[14];
+        float child[kMaxRows];
         for (int c = 0; c < 2; ++c) {
-            for (int k = 0; k < 14; ++k) child[k] = rec[k];
+            for (int k = 0; k < rows; ++k) child[k] = rec[k];
             float e[3];
             for (int a = 0; a < 3; ++a) e[a] = rec[3 + a] * noise[(3 * c + a) * ld + i];
             for (int a = 0; a < 3; ++a) child[a] = rec[a] + (R[a][0] * e[0] + R[a][1] * e[1] + R[a][2] * e[2]);
@@ -857,7 +867,7 @@ __global__ void zero2_kernel(float* a, float* b, int64_t n) {
 
 gs_status run_split_clone(WsState* s, float* params, float* raw, float* m, float* v, int64_t* n_dev, int64_t capacity,
                           int64_t ld, float* accum, float* count, const float* noise, float gthr, float sthr,
-                          cudaStream_t st) {
+                          int32_t rows, cudaStream_t st) {
     Misc* misc = at<Misc>(s, s->misc);
     uint32_t* bcounts = at<uint32_t>(s, s->chunk_hist);
     const int nb = int((capacity + kCmpTile - 1) / kCmpTile);
@@ -870,7 +880,7 @@ gs_status run_split_clone(WsState* s, float* params, float* raw, float* m, float
     scan_blocks_kernel<<<1, 1024, 0, st>>>(bcounts, nb, nclone);
     scatter_kernel<<<nb, kCmpThreads, 0, st>>>(capacity, n_dev, pc,
                                                SplitCloneEmit{params, raw, m, v, accum, noise, ld, capacity, n_dev,
-                                                              nclone, 1},
+                                                              nclone, 1, rows},
                                                bcounts);
     // splits (index order), after the clones
     TypePred ps{params, accum, count, ld, gthr, sthr, 2};
@@ -878,7 +888,7 @@ gs_status run_split_clone(WsState* s, float* params, float* raw, float* m, float
     scan_blocks_kernel<<<1, 1024, 0, st>>>(bcounts, nb, nsplit);
     scatter_kernel<<<nb, kCmpThreads, 0, st>>>(capacity, n_dev, ps,
                                                SplitCloneEmit{params, raw, m, v, accum, noise, ld, capacity, n_dev,
-                                                              nclone, 2},
+                                                              nclone, 2, rows},
                                                bcounts);
     // n_dev <- columns in use; then drop the applied split originals by stable compaction
     int64_t* ncols = reinterpret_cast<int64_t*>(at<char>(s, s->scratch));
@@ -892,9 +902,9 @@ gs_status run_split_clone(WsState* s, float* params, float* raw, float* m, float
     float* arrays[4] = {raw, m, v, params};
     for (float* a : arrays) {
         if (!a) continue;
-        scatter_kernel<<<nb2, kCmpThreads, 0, st>>>(capacity, ncols, keep, GatherEmit{a, scratch, ld, s->n_cap},
-                                                    bcounts);
-        dim3 g(unsigned(std::min<int64_t>((capacity + 255) / 256, 148 * 4)), 14);
+        scatter_kernel<<<nb2, kCmpThreads, 0, st>>>(capacity, ncols, keep,
+                                                    GatherEmit{a, scratch, ld, s->n_cap, rows}, bcounts);
+        dim3 g(unsigned(std::min<int64_t>((capacity + 255) / 256, 148 * 4)), unsigned(rows));
         copy_rows_kernel<<<g, 256, 0, st>>>(scratch, s->n_cap, a, ld, &misc->keep_count);
     }
     set_n_kernel<<<1, 1, 0, st>>>(n_dev, &misc->keep_count);
@@ -974,6 +984,7 @@ gs_status run_densify(WsState* s, float* params, float* raw, int64_t* n_dev, int
                       uint8_t* select_mask, float* add_out, cudaStream_t st) {
     Misc* misc = at<Misc>(s, s->misc);
     uint32_t* bcounts = at<uint32_t>(s, s->chunk_hist);
+    const int rows = cfg.rows == 23 ? 23 : 14;   // 0 -> 14 (RGB)
     if (cfg.mode == GS_DENSIFY_SELECT) {
         const int blocks = int(std::min<int64_t>((capacity + 255) / 256, 148 * 8));
         GS_K((select_kernel<<<blocks, 256, 0, st>>>(capacity, n_dev, at<float4>(s, s->rec), at<uint32_t>(s, s->tiles),
@@ -1001,7 +1012,7 @@ gs_status run_densify(WsState* s, float* params, float* raw, int64_t* n_dev, int
         const int nb = int((npx + kCmpTile - 1) / kCmpTile);
         AddPred pred{alpha, depth, tdepth, cam.width, cfg.tau_alpha, cfg.tau_depth, cfg.stride};
         AddEmit emit{tdepth, trgb, viewmat, cam.width, npx, cam.fx, cam.fy, cam.cx, cam.cy, cfg.init_opacity,
-                     cfg.stride, params, raw, m, v, add_out, ld, capacity, cfg.max_add, n_dev};
+                     cfg.stride, params, raw, m, v, add_out, ld, capacity, cfg.max_add, n_dev, rows};
         GS_K((count_kernel<<<nb, kCmpThreads, 0, st>>>(npx, nullptr, pred, bcounts)));
         GS_K((scan_blocks_kernel<<<1, 1024, 0, st>>>(bcounts, nb, &misc->add_count)));
         GS_K((scatter_kernel<<<nb, kCmpThreads, 0, st>>>(npx, nullptr, pred, emit, bcounts)));
@@ -1019,8 +1030,8 @@ gs_status run_densify(WsState* s, float* params, float* raw, int64_t* n_dev, int
         for (float* a : arrays) {
             if (!a) continue;
             GS_K((scatter_kernel<<<nb, kCmpThreads, 0, st>>>(capacity, n_dev, pred,
-                                                             GatherEmit{a, scratch, ld, s->n_cap}, bcounts)));
-            dim3 g(unsigned(std::min<int64_t>((capacity + 255) / 256, 148 * 4)), 14);
+                                                             GatherEmit{a, scratch, ld, s->n_cap, rows}, bcounts)));
+            dim3 g(unsigned(std::min<int64_t>((capacity + 255) / 256, 148 * 4)), unsigned(rows));
             GS_K((copy_rows_kernel<<<g, 256, 0, st>>>(scratch, s->n_cap, a, ld, &misc->keep_count)));
         }
         GS_K((set_n_kernel<<<1, 1, 0, st>>>(n_dev, &misc->keep_count)));

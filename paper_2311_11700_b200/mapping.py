@@ -25,7 +25,7 @@ import torch
 import torch.distributed as dist
 
 from . import (GS_DENSIFY_ADD, GS_DENSIFY_DEGENERATE_APPLY, GS_DENSIFY_DEGENERATE_FLAG, GS_DENSIFY_PRUNE,
-               GS_FLAG_NO_HOST_SYNC, densify_cfg, gs_adam_step,
+               GS_FLAG_NO_HOST_SYNC, densify_cfg, gs_adam_step, gs_adam_step_rows,
                gs_densify_append, gs_densify_prune, gs_pose_step, make_camera)
 from .pipeline import RenderPipeline
 
@@ -36,11 +36,12 @@ def shard(n_items: int, world: int, rank: int) -> list[int]:
     return list(range(min(n_items, rank * per), min(n_items, (rank + 1) * per)))
 
 
-def learning_rates(it: int, iters: int = 100) -> list[float]:
-    """Per-row Adam learning rates at iteration `it`."""
+def learning_rates(it: int, iters: int = 100, rows: int = 14) -> list[float]:
+    """Per-row Adam learning rates at iteration `it`; with 23 rows (degree-1 SH)
+    every SH coefficient takes the colour rate (the paper prints one colour rate)."""
     t = min(max(it, 0) / max(iters, 1), 1.0)
     lr_x = 1.6e-5 * (1.7e-7 / 1.6e-5) ** t
-    return [lr_x] * 3 + [2e-4] * 3 + [4e-5] * 4 + [1e-2] + [5e-4] * 3
+    return [lr_x] * 3 + [2e-4] * 3 + [4e-5] * 4 + [1e-2] + [5e-4] * (rows - 11)
 
 
 def allreduce_grads(grad: torch.Tensor, group=None) -> None:
@@ -92,7 +93,8 @@ class ShardedMapper:
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if self.world > 1 else 0
-        self.P = params                                   # activated [14][cap]
+        self.P = params                                   # activated [14][cap] or [23][cap] (degree-1 SH)
+        self.rows = params.shape[0]
         self.cap = params.shape[1]
         self.raw = raw_from_activated(params)
         self.m = torch.zeros_like(params)
@@ -123,7 +125,7 @@ class ShardedMapper:
         self.local = shard(len(keyframes), self.world, self.rank)
         L = len(self.local)
         if getattr(self, "cand", None) is None or self.cand.shape[0] != L:
-            self.cand = torch.zeros(L, 14, self.max_add, device=dev)
+            self.cand = torch.zeros(L, self.rows, self.max_add, device=dev)
             self.counts = torch.zeros(L, dtype=torch.int64, device=dev)
             # bundle adjustment state (Eq. 13): per local keyframe pose gradient and Adam moments
             self.gpose = torch.zeros(L, 6, dtype=torch.float64, device=dev)
@@ -158,7 +160,8 @@ class ShardedMapper:
                 cnt = self.counts[j:j + 1]
                 gs_densify_prune(self.P, None, cnt, self.cap, self.cap, None, None, self.pipe.alpha, self.pipe.depth,
                                  kf.color, kf.depth, None, kf.view, self.cm,
-                                 densify_cfg(GS_DENSIFY_ADD, max_add=self.max_add), None, self.cand[j], self.pipe.ws)
+                                 densify_cfg(GS_DENSIFY_ADD, max_add=self.max_add, rows=self.rows), None, self.cand[j],
+                                 self.pipe.ws)
 
     def step(self):
         poses = self.poses_active()
@@ -175,13 +178,16 @@ class ShardedMapper:
                 gs_pose_step(self.keyframes[k].view, self.gpose[j], self.pm[j], self.pv[j], self.pose_step,
                              self.lr_rho, self.lr_phi)
         self.it += 1
-        gs_adam_step(self.raw, self.P, self.grad, self.m, self.v, self.n, self.cap, learning_rates(self.it - 1),
-                     self.it)
+        lr = learning_rates(self.it - 1, rows=self.rows)
+        if self.rows == 14:
+            gs_adam_step(self.raw, self.P, self.grad, self.m, self.v, self.n, self.cap, lr, self.it)
+        else:
+            gs_adam_step_rows(self.raw, self.P, self.grad, self.m, self.v, self.n, self.cap, self.rows, lr, self.it)
         if self.densify:
             cand, counts = gather_candidates(self.cand, self.counts, self.group)
             gs_densify_append(self.P, self.raw, self.m, self.v, self.n_dev, self.cap, self.cap, cand, counts,
-                              cand.shape[0], self.max_add)
+                              cand.shape[0], self.max_add, rows=self.rows)
             gs_densify_prune(self.P, self.raw, self.n_dev, self.cap, self.cap, self.m, self.v, None, None, None, None,
-                             None, None, None, densify_cfg(GS_DENSIFY_PRUNE), None, None, self.pipe.ws)
+                             None, None, None, densify_cfg(GS_DENSIFY_PRUNE, rows=self.rows), None, None, self.pipe.ws)
             self.n = int(self.n_dev.item())   # one host read per mapping iteration (map size)
         return self.n

@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol(gslib):
 def test_struct_layouts(gslib):
     assert ctypes.sizeof(gslib.gs_ws) == 1024
     assert ctypes.sizeof(gslib.gs_camera) == 4 * 4 + 2 * 4 + 4 + 12 + 4
-    assert ctypes.sizeof(gslib.gs_densify_cfg) == 4 * 8 + 8 + 2 * 4
+    assert ctypes.sizeof(gslib.gs_densify_cfg) == 4 * 8 + 8 + 2 * 4 + 4 + 4   # + rows, padded to 8
 
 
 def test_workspace_sizing_and_argument_errors(gslib):

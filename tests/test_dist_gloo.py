@@ -32,7 +32,8 @@ def _mapping_module():
             for name in ("GS_DENSIFY_ADD", "GS_DENSIFY_PRUNE", "GS_FLAG_NO_HOST_SYNC", "GS_DENSIFY_DEGENERATE_APPLY",
                          "GS_DENSIFY_DEGENERATE_FLAG"):
                 setattr(stub, name, 0)
-            for name in ("densify_cfg", "gs_adam_step", "gs_densify_append", "gs_densify_prune", "make_camera"):
+            for name in ("densify_cfg", "gs_adam_step", "gs_adam_step_rows", "gs_densify_append", "gs_densify_prune",
+                         "make_camera"):
                 setattr(stub, name, None)
             sys.modules["paper_2311_11700_b200"] = stub
             pl = types.ModuleType("paper_2311_11700_b200.pipeline")

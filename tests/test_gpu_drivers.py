@@ -294,3 +294,28 @@ def test_tracking_graph_replay_matches_eager():
         d = pose_error(V.cpu().numpy(), eager)
         assert d[0] < 1e-3 and d[1] < 0.05, d
     assert pose_error(eager, v_gt)[0] < 0.5 * pose_error(v0, v_gt)[0]
+
+
+def test_mapper_runs_on_the_sh_layout():
+    """ShardedMapper over degree-1 SH parameters (23 rows): render + backward through gs_project_sh,
+    Adam over 23 rows, Eq. 8 additions with the SH init and the prune, two steps; the map stays
+    finite and the SH rows move."""
+    from paper_2311_11700_b200.mapping import Keyframe, ShardedMapper
+    cfg = gi.CONFIGS[1]
+    cam = cfg.cam
+    p = gi.with_sh(cfg.scene(), 31)
+    v = cfg.view()
+    tc, td = gi.random_images(cam.width, cam.height, 32, 0.5, 3.0)
+    key_cap = key_cap_for(cfg.scene(), v, cam, slack=1.5)[0]
+    cap = p.shape[1] + 2 * 8192
+    P = torch.zeros(23, cap, device="cuda")
+    P[:, :p.shape[1]] = to_dev(p)
+    m = ShardedMapper(P, p.shape[1], [Keyframe(to_dev(v), to_dev(tc), to_dev(td))], cam, key_cap,
+                      max_add_per_kf=8192, densify=True)
+    before = P[11:, :p.shape[1]].clone()
+    for _ in range(2):
+        m.step()
+    torch.cuda.synchronize()
+    assert torch.isfinite(m.P[:, :m.n]).all()
+    assert m.n != p.shape[1]   # additions and / or prunes happened
+    assert not torch.equal(m.P[11:, :1000], before[:, :1000])

@@ -253,7 +253,10 @@ def test_pose_step_parity():
 
 
 # ------------------------------------------------------------------ densify / prune / select
-def test_densify_add_and_prune_parity():
+@pytest.mark.parametrize("rows", [14, 23])
+def test_densify_add_and_prune_parity(rows):
+    """Eq. 8 ADD and the opacity PRUNE; 23 rows = the degree-1 SH layout (reading C34: colour as the DC
+    coefficient, linear terms zero; PRUNE compacts all rows)."""
     import paper_2311_11700_b200 as g
     cfg, p, v = scene(0)
     cap = p.shape[1] + 4096
@@ -262,14 +265,17 @@ def test_densify_add_and_prune_parity():
     P, V = to_dev(p), to_dev(v)
     fr = pipe.forward(P, p.shape[1], V, cfg.cam)
     tc, td = gi.random_images(cfg.cam.width, cfg.cam.height, 9)
-    Pc = torch.zeros(14, cap, device="cuda")
-    Pc[:, :p.shape[1]] = P
+    Pc = torch.zeros(rows, cap, device="cuda")
+    Pc[:14, :p.shape[1]] = P
+    if rows == 23:
+        Pc[14:, :p.shape[1]] = torch.randn(9, p.shape[1], device="cuda")
     n_dev = torch.tensor([p.shape[1]], dtype=torch.int64, device="cuda")
-    cfgd = g.densify_cfg(g.GS_DENSIFY_ADD, max_add=4096)
+    cfgd = g.densify_cfg(g.GS_DENSIFY_ADD, max_add=4096, rows=rows)
     g.gs_densify_prune(Pc, None, n_dev, cap, cap, None, None, fr.alpha, fr.depth, to_dev(tc), to_dev(td), None, V,
                        g.make_camera(cfg.cam), cfgd, None, None, pipe.ws)
     torch.cuda.synchronize()
-    o = oracle.densify_add(fr.alpha.cpu().numpy(), fr.depth.cpu().numpy(), tc, td, v, cfg.cam)
+    o = oracle.densify_add(fr.alpha.cpu().numpy(), fr.depth.cpu().numpy(), tc, td, v, cfg.cam,
+                           sh_degree=1 if rows == 23 else 0)
     n1 = int(n_dev.item())
     assert n1 == p.shape[1] + o.shape[1]
     np.testing.assert_allclose(Pc[:, p.shape[1]:n1].cpu().numpy(), o, rtol=1e-5, atol=1e-5)
@@ -278,7 +284,7 @@ def test_densify_add_and_prune_parity():
     keep = oracle.densify_prune_mask(Pc[10, :n1].cpu().numpy())
     before = Pc[:, :n1].cpu().numpy()
     g.gs_densify_prune(Pc, None, n_dev, cap, cap, None, None, None, None, None, None, None, None, None,
-                       g.densify_cfg(g.GS_DENSIFY_PRUNE), None, None, pipe.ws)
+                       g.densify_cfg(g.GS_DENSIFY_PRUNE, rows=rows), None, None, pipe.ws)
     torch.cuda.synchronize()
     n2 = int(n_dev.item())
     assert n2 == int(keep.sum())
@@ -782,3 +788,49 @@ def test_tile_grid_beyond_the_cooperative_bound():
     assert fr.n_keys == ob["n_keys"]
     assert np.array_equal(a["vals"].cpu().numpy().view(np.uint32), ob["vals"])
     assert np.array_equal(a["ranges"].cpu().numpy().view(np.uint32), ob["ranges"])
+
+
+def test_sh_rows_split_clone_and_append():
+    """Degree-1 SH layout (23 rows) in split/clone (children copy the SH rows; reading C30) and in the
+    gathered append: layout and values against the oracle / the candidate sets."""
+    import paper_2311_11700_b200 as g
+    rng = np.random.default_rng(21)
+    n, cap = 500, 900
+    p = gi.with_sh(gi.gaussians(n, 22, gi.ROOM_LO, gi.ROOM_HI), 23)
+    pc = np.zeros((23, cap), np.float32)
+    pc[:, :n] = p
+    acc = rng.uniform(0, 0.004, cap).astype(np.float32)
+    cnt = np.where(rng.uniform(0, 1, cap) < 0.8, 2.0, 0.0).astype(np.float32)
+    acc[n:] = 0
+    cnt[n:] = 0
+    sv = np.unique(p[3:6].max(0))
+    sthr = float(0.5 * (sv[len(sv) // 2] + sv[len(sv) // 2 + 1]))
+    avg = np.where(cnt > 0, acc / np.where(cnt > 0, cnt, 1), 0).astype(np.float32)
+    pos = np.unique(avg[avg > 0])
+    gthr = float(0.5 * (pos[len(pos) // 2] + pos[len(pos) // 2 + 1]))
+    noise = rng.normal(size=(6, cap)).astype(np.float32)
+    pipe = g.RenderPipeline(cap, 4096, 64, 48)
+    Pc = to_dev(pc)
+    n_dev = torch.tensor([n], dtype=torch.int64, device="cuda")
+    A, C = to_dev(acc), to_dev(cnt)
+    g.gs_densify_split_clone(Pc, None, None, None, n_dev, cap, cap, A, C, to_dev(noise), gthr, sthr, pipe.ws, rows=23)
+    torch.cuda.synchronize()
+    want, clone, split = oracle.split_clone(p, acc[:n], cnt[:n], noise[:, :n], gthr, sthr, capacity=cap)
+    assert clone.size > 0 and split.size > 0
+    n2 = int(n_dev.item())
+    assert n2 == want.shape[1]
+    got = Pc[:, :n2].cpu().numpy()
+    np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-6)
+    assert np.array_equal(got[11:], want[11:].astype(np.float32))   # SH rows are copied exactly
+    # append two gathered 23-row candidate sets
+    max_add = 40
+    cand = rng.uniform(0.1, 0.9, (2, 23, max_add)).astype(np.float32)
+    counts = torch.tensor([7, 13], dtype=torch.int64, device="cuda")
+    raw = torch.zeros_like(Pc)
+    g.gs_densify_append(Pc, raw, None, None, n_dev, cap, cap, to_dev(cand), counts, 2, max_add, rows=23)
+    torch.cuda.synchronize()
+    n3 = int(n_dev.item())
+    assert n3 == n2 + 20
+    got = Pc[:, n2:n3].cpu().numpy()
+    assert np.array_equal(got, np.concatenate([cand[0, :, :7], cand[1, :, :13]], 1))
+    np.testing.assert_allclose(raw[14:, n2:n3].cpu().numpy(), got[14:], rtol=0, atol=0)   # SH rows: identity

@@ -947,3 +947,23 @@ def test_image_half_brute_force():
     assert dh[0, 0] == 0
     ch, dh = oracle.image_half(np.full((3, 4, 6), 0.3, np.float32), np.full((4, 6), 2.5, np.float32))
     assert (ch == np.float32(0.3)).all() and (dh == np.float32(2.5)).all()
+
+
+def test_sh_densify_init_reproduces_the_target_colour():
+    """Reading C34: a Gaussian added with the degree-1 SH layout renders, through the SH evaluation
+    of reading C29 (oracle.project's colour at the view direction), the target colour at ANY view:
+    DC = (c - 1/2)/C0 and zero linear terms."""
+    cam = gi.CAM_TINY
+    W, H = cam.width, cam.height
+    tc, td = gi.random_images(W, H, 61)
+    alpha = np.zeros((H, W))
+    depth = np.zeros((H, W))
+    view = small_pose(9)
+    add = oracle.densify_add(alpha, depth, tc, td, view, cam, sh_degree=1)
+    rgb = oracle.densify_add(alpha, depth, tc, td, view, cam)
+    assert add.shape[0] == 23 and add.shape[1] == rgb.shape[1] > 0
+    assert (add[14:] == 0).all()
+    for seed in (1, 2):
+        v2 = small_pose(seed, rot_deg=30, trans=0.5)
+        pr = oracle.project(add, v2, cam, "f64")
+        np.testing.assert_allclose(pr["rgb"], rgb[11:14], rtol=0, atol=2e-6)
