@@ -41,6 +41,7 @@ class SlamConfig:
     parallel: bool = True
     seed: int = 0              # window sampling
     degenerate: tuple[float, float] | None = None   # Eq. 9 (eta, gamma) in the expansion step (NEXT-2)
+    sh_degree: int = 0         # 1: the paper's degree-1 SH colour (23 parameter rows, NEXT-1)
 
 
 class SlamSystem:
@@ -52,8 +53,9 @@ class SlamSystem:
         self.ts = torch.cuda.Stream(dev)
         self.ms = torch.cuda.Stream(dev)
         max_add = cfg.max_add or (cam.width * cam.height) // 2
+        rows = 23 if cfg.sh_degree == 1 else 14
         with torch.cuda.stream(self.ms):
-            self.mapper = ShardedMapper(torch.zeros(14, n_cap, device=dev), 0, [], cam, key_cap_full,
+            self.mapper = ShardedMapper(torch.zeros(rows, n_cap, device=dev), 0, [], cam, key_cap_full,
                                         max_add_per_kf=max_add, densify=True, degenerate=cfg.degenerate)
         with torch.cuda.stream(self.ts):
             self.tracker = Tracker(n_cap, key_cap_full, key_cap_half, cam, device)
@@ -61,7 +63,7 @@ class SlamSystem:
             half = cam.half()
             self.ch = torch.zeros(3, half.height, half.width, device=dev)
             self.dh = torch.zeros(half.height, half.width, device=dev)
-        self.snap = [torch.zeros(14, n_cap, device=dev) for _ in range(2)]
+        self.snap = [torch.zeros(rows, n_cap, device=dev) for _ in range(2)]
         self.snap_n = [0, 0]
         self.ready = [torch.cuda.Event(), torch.cuda.Event()]
         self.released = [torch.cuda.Event(), torch.cuda.Event()]

@@ -191,8 +191,8 @@ def test_frontend_tracks_a_constant_velocity_trajectory():
     assert kfs == [True, False]   # gap rule: frame 2 is the second after the last keyframe (max gap 2)
 
 
-@pytest.mark.parametrize("parallel", [False, True])
-def test_slam_sequence_tracks_and_maps(parallel):
+@pytest.mark.parametrize("parallel,sh", [(False, 0), (True, 0), (False, 1)])
+def test_slam_sequence_tracks_and_maps(parallel, sh):
     """NEXT-4 end to end (slam.py): an RGB-D sequence rendered from a surface room along a smooth
     trajectory; the map starts EMPTY and is built from the first frame (Eq. 7-8 expansion with the
     known first pose), every later frame is tracked from the constant-velocity guess against the
@@ -219,7 +219,7 @@ def test_slam_sequence_tracks_and_maps(parallel):
     frames = [_render(src, G, gt.shape[1], to_dev(v), cam) for v in traj]
     cfg = SlamConfig(frontend=FrontendConfig(track=TrackConfig(iters_coarse=30, iters_fine=30, observed_alpha=0.5,
                                                                outlier_k=10.0), kf_max_gap=2),
-                     map_iters=60, window=4, parallel=parallel)
+                     map_iters=60, window=4, parallel=parallel, sh_degree=sh)
     slam = SlamSystem(cam, 400_000, 8 << 20, 4 << 20, cfg)
     errs = []
     for k, (c, d) in enumerate(frames):
@@ -228,7 +228,7 @@ def test_slam_sequence_tracks_and_maps(parallel):
             torch.cuda.synchronize()
             errs.append(pose_error(V.cpu().numpy(), traj[k]))
     slam.finish()
-    print("parallel" if parallel else "sequential", "errors", [(round(t * 100, 2), round(r, 2)) for t, r in errs],
+    print("parallel" if parallel else "sequential", f"sh{sh}", "errors", [(round(t * 100, 2), round(r, 2)) for t, r in errs],
           "keyframes", slam.kf_flags, "map", slam.mapper.n, "rounds", slam.map_rounds)
     assert max(t for t, _ in errs) < 0.03 and max(r for _, r in errs) < 2.0
     assert slam.map_rounds == sum(slam.kf_flags) >= 2
