@@ -88,9 +88,10 @@ def sh_degree_of(params) -> int:
     return 1 if rows == 23 else 0
 
 
-def _mode(params, opacity_radius) -> int:
-    """Oracle C ABI mode word: colour model | (opacity-aware radius, reading C33) << 8."""
-    return sh_degree_of(params) | (256 if opacity_radius else 0)
+def _mode(params, opacity_radius, o3_power=False) -> int:
+    """Oracle C ABI mode word: colour model | (opacity-aware radius, reading C33) << 8 | (power in
+    SURVEY.md §8(c) O3's printed order instead of reading R1's fma order) << 9."""
+    return sh_degree_of(params) | (256 if opacity_radius else 0) | (512 if o3_power else 0)
 
 
 # ------------------------------------------------------------------------------------ O1
@@ -135,9 +136,12 @@ def bin_sort(depth_bits, rect, tiles, cam) -> dict:
 
 # ------------------------------------------------------------------------------------ O3
 def forward(params, view, cam, precision="f32", pixels=None, replay_nlast=None, accum_weight=False,
-            flip_skip_ties=False, opacity_radius=False) -> dict:
+            flip_skip_ties=False, opacity_radius=False, o3_power=False) -> dict:
     """O3 (Eq. 4-5, cumulative opacity P:118). Full images unless `pixels` (linear ids) given.
-    replay_nlast / flip_skip_ties: the parity tie rule's replays (reading R1)."""
+    replay_nlast / flip_skip_ties: the parity tie rule's replays (reading R1).
+    o3_power: evaluate the exponent in the order SURVEY.md §8(c) O3 prints,
+    -0.5*((a*dx)*dx + (c*dy)*dy) - (b*dx)*dy, instead of R1's fma order (for the pin that both
+    orders take the same decisions outside the tie band)."""
     dt = _dtype(precision)
     params = np.ascontiguousarray(params, dt)
     view = np.ascontiguousarray(view, dt)
@@ -162,7 +166,8 @@ def forward(params, view, cam, precision="f32", pixels=None, replay_nlast=None, 
     getattr(lib(), f"oracle_forward_{precision}")(
         _p(params), ctypes.c_int64(n), ctypes.c_int64(n), _p(view), ctypes.byref(c), _p(pixels),
         ctypes.c_int64(npx), _p(rp), _p(color), _p(depth), _p(alpha), _p(n_last), _p(examined), _p(amb),
-        _p(h), _p(aw), ctypes.c_int32(1 if flip_skip_ties else 0), ctypes.c_int32(_mode(params, opacity_radius)))
+        _p(h), _p(aw), ctypes.c_int32(1 if flip_skip_ties else 0),
+        ctypes.c_int32(_mode(params, opacity_radius, o3_power)))
     out = dict(color=color.reshape((3,) + shape), depth=depth.reshape(shape), alpha=alpha.reshape(shape),
                n_last=n_last.reshape(shape), examined=examined.reshape(shape), ambiguous=amb.reshape(shape),
                hash=int(h[0]))
@@ -173,13 +178,17 @@ def forward(params, view, cam, precision="f32", pixels=None, replay_nlast=None, 
 
 # ------------------------------------------------------------------------------------ O4
 def backward(params, view, cam, dL_dcolor, dL_ddepth, precision="f32", replay_nlast=None, qt_cov=True,
-             pixels=None, opacity_radius=False) -> dict:
+             pixels=None, opacity_radius=False, bound=False) -> dict:
     """O4 (Eq. 11, S1-S6): fp64 gradients for the 14 (RGB) or 23 (degree-1 SH) params, screen grads,
     and the pose.
 
     pose_twist: (rho, phi) left-perturbation twist, covariance path included (reading C7);
     pose_twist_paper: same without the Sigma'-through-pose term (P:168, paper mode);
     pose_qt: dL/d(q_r,q_i,q_j,q_k,t) via Eq. S1/S3 (independent path), plus the pose quaternion.
+    bound=True adds grad_bound [rows][n], pose_bound[6], pose_bound_paper[6], screen_bound [10][n]
+    (the screen quantities' sums of term magnitudes): the error-bound scale
+    of each result, sum_j |d grad / d s_j| sum_p |c_pj| (the per-pixel terms' magnitudes carried
+    through the linear per-Gaussian chain; oracle.cpp error_bound). |result| <= bound always.
     """
     dt = _dtype(precision)
     params = np.ascontiguousarray(params, dt)
@@ -194,13 +203,21 @@ def backward(params, view, cam, dL_dcolor, dL_ddepth, precision="f32", replay_nl
     qt = np.zeros(11, np.float64)
     rp = np.ascontiguousarray(replay_nlast, np.uint32).reshape(-1) if replay_nlast is not None else None
     px = np.ascontiguousarray(pixels, np.int64) if pixels is not None else None
+    gb = np.zeros((params.shape[0], n), np.float64) if bound else None
+    pb = np.zeros(6, np.float64) if bound else None
+    pbp = np.zeros(6, np.float64) if bound else None
+    sb = np.zeros((10, n), np.float64) if bound else None
     c = _cam(cam)
     getattr(lib(), f"oracle_backward_{precision}")(
         _p(params), ctypes.c_int64(n), ctypes.c_int64(n), _p(view), ctypes.byref(c), _p(dc), _p(dd), _p(rp),
         _p(gp), _p(gs), _p(tw), _p(twp), _p(qt), ctypes.c_int32(1 if qt_cov else 0), _p(px),
-        ctypes.c_int64(0 if px is None else px.shape[0]), ctypes.c_int32(_mode(params, opacity_radius)))
-    return dict(grad_params=gp, grad_screen=gs, pose_twist=tw, pose_twist_paper=twp,
-                pose_q=qt[0:4], pose_t=qt[4:7], pose_quat=qt[7:11])
+        ctypes.c_int64(0 if px is None else px.shape[0]), ctypes.c_int32(_mode(params, opacity_radius)),
+        _p(gb), _p(pb), _p(pbp), _p(sb))
+    out = dict(grad_params=gp, grad_screen=gs, pose_twist=tw, pose_twist_paper=twp,
+               pose_q=qt[0:4], pose_t=qt[4:7], pose_quat=qt[7:11])
+    if bound:
+        out.update(grad_bound=gb, pose_bound=pb, pose_bound_paper=pbp, screen_bound=sb)
+    return out
 
 
 # ------------------------------------------------------------------------------------ O5 (numpy fp64)

@@ -50,12 +50,13 @@ template <class R> struct Cam {
     int W, H, GX, GY;
     int sh;                 // colour model: 0 = RGB rows 11-13 (reading C17), 1 = degree-1 SH (C29)
     bool orad;              // radius: false = 3 sigma (C11), true = alpha >= 1/255 reach (C33)
+    bool o3pow;             // power in SURVEY.md §8(c) O3's printed order instead of R1's fma order
     double bg[3];
-    // mode = sh_degree | (opacity_radius << 8)
+    // mode = sh_degree | (opacity_radius << 8) | (o3_power_order << 9)
     explicit Cam(const OracleCam& c, int mode = 0)
         : fx(R(c.fx)), fy(R(c.fy)), cx(R(c.cx)), cy(R(c.cy)), znear(R(c.znear)), dil(R(c.dil)),
           W(c.width), H(c.height), GX((c.width + TILE - 1) / TILE), GY((c.height + TILE - 1) / TILE),
-          sh(mode & 0xff), orad(((mode >> 8) & 1) != 0) {
+          sh(mode & 0xff), orad(((mode >> 8) & 1) != 0), o3pow(((mode >> 9) & 1) != 0) {
         for (int k = 0; k < 3; ++k) bg[k] = c.bg[k];
     }
 };
@@ -283,10 +284,10 @@ static void blend_pixel(int u, int v, const std::vector<Proj<R>>& pj, const std:
     R T = R(1);
     uint32_t j = 0;
     // Tie band (reading R1): a conforming fp32 evaluation may differ from this one by
-    // the exp's error (<= 2^-20 relative incl. argument rounding) in every unclamped alpha; the
-    // resulting relative divergence of T is bounded by sum_k (2^-20 alpha_k / (1 - alpha_k) + 2^-23).
-    // A decision value within that band (floor 1e-5 relative) of its threshold marks the pixel
-    // ambiguous.
+    // the exp's error (<= 2^-20 relative incl. argument rounding) and the power's evaluation order
+    // (perr below) in every unclamped alpha; the resulting relative divergence of T is bounded by
+    // sum_k ((2^-20 + perr_k) alpha_k / (1 - alpha_k) + 2^-23). A decision value within that band
+    // (floor 1e-5 relative) of its threshold marks the pixel ambiguous.
     double t_band = 0.0;
     for (int64_t i : order) {
         const Proj<R>& g = pj[size_t(i)];
@@ -299,21 +300,31 @@ static void blend_pixel(int u, int v, const std::vector<Proj<R>>& pj, const std:
         // the exactly scaled coefficients A = -a/2, B = -b, C = -c/2 (reading R1: the
         // order every fp32 evaluation of this decision value uses, oracle and kernel alike)
         const R A2 = R(-0.5) * g.ca, B2 = -g.cb, C2 = R(-0.5) * g.cc;
-        const R power = std::fma(A2 * dx, dx, std::fma(C2 * dy, dy, (B2 * dx) * dy));
+        // cam.o3pow: the order SURVEY.md §8(c) O3 prints, each operation rounded separately; used
+        // only by the pin that both orders take the same decisions outside the tie band
+        const R power = cam.o3pow ? R(R(-0.5) * ((g.ca * dx) * dx + (g.cc * dy) * dy)) - (g.cb * dx) * dy
+                                  : std::fma(A2 * dx, dx, std::fma(C2 * dy, dy, (B2 * dx) * dy));
         if (power > R(0)) continue;
         const R G = exp_r<R>(power);
         const R o = params[10 * ld + i];
         const R og = o * G;
         const R alpha = std::min(a_max, og);
-        const bool amb_skip = std::fabs(double(alpha) - double(a_min)) <= 1e-5 * double(a_min);
+        // any fp32 evaluation order of the power's three terms (R1's fma order, O3's printed order)
+        // is within 4 u (sum of the terms' magnitudes) of the exact value, u = 2^-24; the relative
+        // change of alpha is that absolute change of the power
+        const double perr = 2.384185791015625e-07 * (std::fabs(double(A2) * double(dx) * double(dx)) +
+                                                     std::fabs(double(C2) * double(dy) * double(dy)) +
+                                                     std::fabs(double(B2) * double(dx) * double(dy)));
+        const bool amb_skip = std::fabs(double(alpha) - double(a_min)) <= std::max(1e-5, 9.5367431640625e-07 + perr) * double(a_min);
         if (amb_skip) out.ambiguous = 1;
         bool skip = alpha < a_min;
         if (flip_skip_ties && amb_skip) skip = !skip;   // tie-rule replay: take the other decision
         if (skip) continue;
         const R Tn = T * (R(1) - alpha);
         const bool clamped = og > a_max;
-        const double step_band = (clamped ? 0.0 : 9.5367431640625e-07 * double(alpha) / (1.0 - double(alpha))) +
-                                 1.1920928955078125e-07;
+        const double step_band =
+            (clamped ? 0.0 : (9.5367431640625e-07 + perr) * double(alpha) / (1.0 - double(alpha))) +
+            1.1920928955078125e-07;
         if (replay_nlast < 0) {
             const double band = std::max(1e-5, t_band + step_band);
             if (std::fabs(double(Tn) - double(t_min)) <= band * double(t_min)) out.ambiguous = 1;
@@ -346,7 +357,8 @@ static inline void atomic_add(double& dst, double v) {
 // for depth and its colour analogue, plus the background term; suffix sums in fp64.
 template <class R>
 static void backward_pixel(const PixelResult& px, const std::vector<Proj<R>>& pj, const R* params, int64_t ld,
-                           const Cam<R>& cam, const double dLdC[3], double dLdD, std::vector<ScreenGrad>& sg) {
+                           const Cam<R>& cam, const double dLdC[3], double dLdD, std::vector<ScreenGrad>& sg,
+                           std::vector<ScreenGrad>* sa = nullptr) {
     const size_t n = px.list.size();
     if (n == 0) return;
     std::vector<double> T(static_cast<size_t>(n + 1));
@@ -384,6 +396,32 @@ static void backward_pixel(const PixelResult& px, const std::vector<Proj<R>>& pj
             atomic_add(s.a, -0.5 * gp * ct.dx * ct.dx);
             atomic_add(s.b, -gp * ct.dx * ct.dy);
             atomic_add(s.c, -0.5 * gp * ct.dy * ct.dy);
+        }
+        if (sa) {   // magnitude of every term of this pixel's contribution (the error-bound scale)
+            double ga = 0;
+            for (int c = 0; c < 3; ++c)
+                ga += (std::fabs(rgb[c]) * Ti + std::fabs(Rs[c]) / (1.0 - a)) * std::fabs(dLdC[c]);
+            ga += (std::fabs(d) * Ti + std::fabs(Ds) / (1.0 - a)) * std::fabs(dLdD);
+            double bga = 0;
+            for (int c = 0; c < 3; ++c) bga += std::fabs(cam.bg[c] * dLdC[c]);
+            ga += Tf / (1.0 - a) * bga;
+            ScreenGrad& m = (*sa)[size_t(i)];
+            atomic_add(m.r, std::fabs(w * dLdC[0]));
+            atomic_add(m.g, std::fabs(w * dLdC[1]));
+            atomic_add(m.bl, std::fabs(w * dLdC[2]));
+            atomic_add(m.d, std::fabs(w * dLdD));
+            if (!ct.clamped) {
+                const Proj<R>& g = pj[size_t(i)];
+                const double o = std::fabs(double(params[10 * ld + i]));
+                const double ca = std::fabs(double(g.ca)), cb = std::fabs(double(g.cb)), cc = std::fabs(double(g.cc));
+                const double adx = std::fabs(ct.dx), ady = std::fabs(ct.dy), gp = o * ct.G * ga;
+                atomic_add(m.o, ct.G * ga);
+                atomic_add(m.mx, gp * (ca * adx + cb * ady));
+                atomic_add(m.my, gp * (cb * adx + cc * ady));
+                atomic_add(m.a, 0.5 * gp * adx * adx);
+                atomic_add(m.b, gp * adx * ady);
+                atomic_add(m.c, 0.5 * gp * ady * ady);
+            }
         }
         for (int c = 0; c < 3; ++c) Rs[c] += rgb[c] * w;
         Ds += d * w;
@@ -548,6 +586,73 @@ static GaussianBack gaussian_backward(const R* params, int64_t ld, int64_t i, co
     return out;
 }
 
+// Error-bound scale of every gradient (parity tolerance): the sums over pixels of
+// the magnitudes of the per-pixel terms, S_j = sum_p |c_pj| for the 10 screen quantities j
+// (backward_pixel with `sa`), carried through the per-Gaussian chain, which is linear in the screen
+// gradient: bound_k = sum_j |d grad_k / d s_j| S_j, i.e. the chain of S_j e_j for each j separately,
+// in absolute value. Same for the pose twist, with and without the covariance path. A result summed
+// in another order and precision p from the same terms differs from the exact sum by at most about
+// (number of terms) p bound_k; a dropped term, a wrong sign or a transposed operand moves a gradient
+// by the size of its terms, O(bound_k), so a tolerance of 2e-3 bound_k keeps the comparison's power.
+template <class R>
+static void error_bound(const R* params, int64_t n, int64_t ld, const R* view, const Cam<R>& cam,
+                        const std::vector<Proj<R>>& pj, const std::vector<ScreenGrad>& sabs, double* grad_bound,
+                        double* pose_bound, double* pose_bound_paper) {
+    const int rows = n_rows(cam.sh);
+    double W[3][3];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) W[a][b] = double(view[a * 4 + b]);
+    double pb[6] = {0, 0, 0, 0, 0, 0}, pbp[6] = {0, 0, 0, 0, 0, 0};
+#pragma omp parallel
+    {
+        double lpb[6] = {0, 0, 0, 0, 0, 0}, lpbp[6] = {0, 0, 0, 0, 0, 0};
+#pragma omp for schedule(dynamic, 256)
+        for (int64_t i = 0; i < n; ++i) {
+            if (!pj[size_t(i)].in_front || pj[size_t(i)].tiles == 0) continue;
+            const ScreenGrad& m = sabs[size_t(i)];
+            const double v10[10] = {m.mx, m.my, m.a, m.b, m.c, m.o, m.r, m.g, m.bl, m.d};
+            for (int j = 0; j < 10; ++j) {
+                if (v10[j] == 0) continue;
+                double e[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+                e[j] = v10[j];
+                const ScreenGrad ej{e[0], e[1], e[2], e[3], e[4], e[5], e[6], e[7], e[8], e[9]};
+                const GaussianBack gb = gaussian_backward<R>(params, ld, i, view, cam, ej, pj[size_t(i)]);
+                if (grad_bound)
+                    for (int k = 0; k < rows; ++k) grad_bound[k * n + i] += std::fabs(gb.grad[k]);
+                const double* X = gb.Xc;
+                const double* g = gb.dXc_full;
+                const double* gp = gb.dXc_noJ;
+                double A[3][3];   // this Gaussian's share of A = W (sum_i dW_i)^T
+                for (int a = 0; a < 3; ++a)
+                    for (int b = 0; b < 3; ++b)
+                        A[a][b] = W[a][0] * gb.dW[b][0] + W[a][1] * gb.dW[b][1] + W[a][2] * gb.dW[b][2];
+                double WG[3];
+                for (int a = 0; a < 3; ++a)
+                    WG[a] = W[a][0] * gb.gdir[0] + W[a][1] * gb.gdir[1] + W[a][2] * gb.gdir[2];
+                const double tw[6] = {g[0] + WG[0], g[1] + WG[1], g[2] + WG[2],
+                                      X[1] * g[2] - X[2] * g[1] + (A[1][2] - A[2][1]),
+                                      X[2] * g[0] - X[0] * g[2] + (A[2][0] - A[0][2]),
+                                      X[0] * g[1] - X[1] * g[0] + (A[0][1] - A[1][0])};
+                const double twp[6] = {gp[0], gp[1], gp[2], X[1] * gp[2] - X[2] * gp[1],
+                                       X[2] * gp[0] - X[0] * gp[2], X[0] * gp[1] - X[1] * gp[0]};
+                for (int k = 0; k < 6; ++k) {
+                    lpb[k] += std::fabs(tw[k]);
+                    lpbp[k] += std::fabs(twp[k]);
+                }
+            }
+        }
+#pragma omp critical
+        for (int k = 0; k < 6; ++k) {
+            pb[k] += lpb[k];
+            pbp[k] += lpbp[k];
+        }
+    }
+    for (int k = 0; k < 6; ++k) {
+        if (pose_bound) pose_bound[k] = pb[k];
+        if (pose_bound_paper) pose_bound_paper[k] = pbp[k];
+    }
+}
+
 }  // namespace
 
 // ============================================================================================
@@ -687,6 +792,8 @@ ORACLE_FORWARD(f64, double)
 
 // O4 backward for the whole image with upstream dL/dC [3][H][W], dL/dD [H][W].
 // Outputs (all fp64, may be NULL): grad_params [14][n] (+=), grad_screen [10][n]
+// (error-bound scales, see error_bound: grad_bound [rows][n], pose_bound[6], pose_bound_paper[6],
+// screen_bound [10][n] = S_j, the sums of the per-pixel terms' magnitudes; all =)
 // (mx,my,a,b,c,o,r,g,b,d) (=), pose_twist[6] (rho, phi) with the covariance path,
 // pose_twist_paper[6] without it, pose_qt[7] = dL/d(q_r,q_i,q_j,q_k, t_x,t_y,t_z) of the
 // world->camera pose through Eq. S1/S3 (the second, independent pose path), computed with the
@@ -696,13 +803,16 @@ ORACLE_FORWARD(f64, double)
                               const float* dLdC, const float* dLdD, const uint32_t* replay_nlast,              \
                               double* grad_params, double* grad_screen, double* pose_twist,                    \
                               double* pose_twist_paper, double* pose_qt, int32_t qt_cov,                       \
-                              const int64_t* pixels, int64_t n_pix, int32_t mode) {                              \
+                              const int64_t* pixels, int64_t n_pix, int32_t mode, double* grad_bound,          \
+                              double* pose_bound, double* pose_bound_paper, double* screen_bound) {            \
         Cam<R> cam(*oc, mode);                                                                            \
         auto pj = project_all<R>(params, n, ld, view, cam);                                                    \
         auto order = depth_order(pj);                                                                          \
         const int64_t P = int64_t(cam.W) * cam.H;                                                              \
         const int64_t NQ = pixels ? n_pix : P; /* optional pixel subset (bounded CPU-baseline sample) */       \
         std::vector<ScreenGrad> sg(size_t(n), ScreenGrad{0, 0, 0, 0, 0, 0, 0, 0, 0, 0});                       \
+        const bool want_bound = grad_bound || pose_bound || pose_bound_paper || screen_bound;                  \
+        std::vector<ScreenGrad> sabs(want_bound ? size_t(n) : 0, ScreenGrad{0, 0, 0, 0, 0, 0, 0, 0, 0, 0});   \
         _Pragma("omp parallel for schedule(dynamic, 64)")                                                     \
         for (int64_t qi = 0; qi < NQ; ++qi) {                                                                  \
             const int64_t q = pixels ? pixels[qi] : qi;                                                        \
@@ -711,7 +821,13 @@ ORACLE_FORWARD(f64, double)
             blend_pixel<R>(u, v, pj, order, params, ld, cam, replay_nlast ? int64_t(replay_nlast[q]) : -1,     \
                            true, r);                                                                           \
             const double dc[3] = {double(dLdC[q]), double(dLdC[P + q]), double(dLdC[2 * P + q])};             \
-            backward_pixel<R>(r, pj, params, ld, cam, dc, double(dLdD[q]), sg);                                \
+            backward_pixel<R>(r, pj, params, ld, cam, dc, double(dLdD[q]), sg, want_bound ? &sabs : nullptr);  \
+        }                                                                                                      \
+        if (want_bound) error_bound<R>(params, n, ld, view, cam, pj, sabs, grad_bound, pose_bound, pose_bound_paper); \
+        if (screen_bound) for (int64_t i = 0; i < n; ++i) {                                                    \
+            const ScreenGrad& m = sabs[size_t(i)];                                                             \
+            const double v10[10] = {m.mx, m.my, m.a, m.b, m.c, m.o, m.r, m.g, m.bl, m.d};                      \
+            for (int k = 0; k < 10; ++k) screen_bound[k * n + i] = v10[k];                                     \
         }                                                                                                      \
         double rho[3] = {0, 0, 0}, phi[3] = {0, 0, 0}, rho_p[3] = {0, 0, 0}, phi_p[3] = {0, 0, 0};            \
         double A[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};                                                    \

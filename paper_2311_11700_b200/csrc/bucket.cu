@@ -77,10 +77,18 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 __global__ void __launch_bounds__((kConsumers + kProducers) * 32) bucket_emit_kernel(
     const uint32_t* __restrict__ svals, const short4* __restrict__ srect, const uint32_t* __restrict__ cmat,
     const unsigned int* __restrict__ n_on, const unsigned long long* __restrict__ n_keys_eff,
-    const unsigned long long* __restrict__ n_keys, int GX, int GY, uint32_t* __restrict__ vals_out) {
+    const unsigned long long* __restrict__ n_keys, int GX, int GY, uint32_t* __restrict__ vals_out,
+    uint2* __restrict__ ranges) {
     __shared__ EmitSmem sm;
     griddep_wait();   // PDL (gs_internal.cuh)
-    if (*n_keys_eff != *n_keys) return;   // capacity overflow: emit nothing (error flag is set)
+    if (*n_keys_eff != *n_keys) {
+        // capacity overflow (the error flag is set): emit nothing and empty every tile's range, so the
+        // render kernels that follow in NO_HOST_SYNC mode read no list entry beyond key_cap
+        const int nb = gridDim.x * gridDim.y * gridDim.z;
+        const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+        for (int t = b * blockDim.x + threadIdx.x; t < GX * GY; t += nb * blockDim.x) ranges[t] = make_uint2(0u, 0u);
+        return;
+    }
     const uint32_t Von = *n_on;
     const int nch = int((Von + kChunk - 1) / kChunk);
     const int T = GX * GY;
@@ -207,7 +215,8 @@ gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaS
                         unsigned((s->cam_gy + kBY - 1) / kBY));
         launch_pdl(bucket_emit_kernel, grid, dim3((kConsumers + kProducers) * 32), 0, st, at<uint32_t>(s, s->svals), at<short4>(s, s->srect),
                                                  at<uint32_t>(s, s->chunk_mat), &misc->n_onscreen, &misc->n_keys_eff,
-                                                 &misc->n_keys, s->cam_gx, s->cam_gy, at<uint32_t>(s, s->vals0));
+                                                 &misc->n_keys, s->cam_gx, s->cam_gy, at<uint32_t>(s, s->vals0),
+                                                 at<uint2>(s, s->ranges));
     } else {
         cudaMemsetAsync(at<char>(s, s->ranges), 0, size_t(T) * sizeof(uint2), st);
     }

@@ -751,7 +751,9 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
                 const float M0 = moment(0, k), Mx = moment(1, k), My = moment(2, k);
                 const float4 r0 = sm.rec[gbuf][k][0];
                 const float o = sm.rec[gbuf][k][1].y;
-                const float X = r0.x - float(tx * kTile), Y = r0.y - float(ty * kTile);
+                // moments are about the tile centre (lx, ly in -7.5 .. 7.5: no cancellation between
+                // X^2 M0, 2 X Mx and Mxx beyond the sum's own when the mean is near the tile)
+                const float X = r0.x - (float(tx * kTile) + 7.5f), Y = r0.y - (float(ty * kTile) + 7.5f);
                 // sums of g dx, g dy, g dx^2, g dx dy, g dy^2 with dx = X - lx, dy = Y - ly
                 const float gdx = X * M0 - Mx, gdy = Y * M0 - My;
                 if (c == 0) {
@@ -813,14 +815,14 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
                 const float4 v = sm.wg[k2][q];
                 const f32x2 w = pk2(v.x, v.y), g = pk2(v.z, v.w);
                 R0 = add2(R0, g);
-                Rx = fma2(g, bc2(float(x)), Rx);
-                Rxx = fma2(g, bc2(float(x * x)), Rxx);
+                Rx = fma2(g, bc2(float(x) - 7.5f), Rx);                               // exact constants
+                Rxx = fma2(g, bc2((float(x) - 7.5f) * (float(x) - 7.5f)), Rxx);
                 Sr = fma2(w, sm.dl[q][0], Sr);
                 Sg = fma2(w, sm.dl[q][1], Sg);
                 Sb = fma2(w, sm.dl[q][2], Sb);
                 Sd = fma2(w, sm.dl[q][3], Sd);
             }
-            const float fyA_ = float(gi), fyB_ = float(gi + kGroups);
+            const float fyA_ = float(gi) - 7.5f, fyB_ = float(gi + kGroups) - 7.5f;   // about the centre
             float m[10];
             m[0] = lo2(R0) + hi2(R0);                                 // sum g
             m[1] = lo2(Rx) + hi2(Rx);                                 // sum g lx

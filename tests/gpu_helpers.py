@@ -66,8 +66,8 @@ def compare_images(gpu, orc, cam, params, view, label="", opacity_radius=False):
                           f"{list(zip(nl[:8].tolist(), orc['n_last'].reshape(-1)[bad][:8].tolist()))}")
         ties = int(bad.size)
     # every tie is replay-consistent and inside the oracle's arithmetic band (checked above); their
-    # number is reported, and bounded well below the 1e-3 of pixels the band model predicts
-    assert ties <= max(3, int(1e-3 * H * W)), f"{label}: {ties} tie pixels"
+    # number is reported and capped at SURVEY.md §8(c)'s target: <= 1e-5 of the pixels (0 at config 0)
+    assert ties <= int(1e-5 * H * W), f"{label}: {ties} tie pixels (cap {int(1e-5 * H * W)})"
     print(f"{label}: {ties} threshold-tie pixels of {H * W}")
     return ties
 
@@ -77,3 +77,43 @@ def grad_close(gpu, ref, rtol=RTOL_GRAD, atol=ATOL_GRAD):
     ref = np.asarray(ref, np.float64)
     bad = np.abs(gpu - ref) > rtol * np.abs(ref) + atol
     return bad
+
+
+# Gradient criterion. An element passes the north_star rule |gpu - ref| <= 2e-3 |ref|
+# + 1e-6, or, where the exact sum cancels, the summation bound |gpu - ref| <= k * bound + 1e-6, with
+# bound = the oracle's sum of the magnitudes of the element's per-pixel terms carried through the
+# chain (oracle.backward(bound=True)). An fp32 evaluation of the same terms differs from the exact
+# sum by (its relative error per term) * bound: summation rounding (~2^-24 per addition level), and
+# the kernel's back-to-front transmittance recovery T_i = T_{i+1} / (1 - alpha_i), which adds <= 2 ulp
+# (rcp.approx + multiply, 2.4e-7) per walked contributor. So k = max(1e-4, 2.4e-7 * max n_last);
+# a dropped term, a sign or an index error moves the element by O(bound). No element may fail.
+K_BOUND = 1e-4
+ULP2 = 2.384185791015625e-07   # 2 ulp of fp32 (2^-22)
+
+
+def bound_factor(n_last) -> float:
+    """k of the summation-bound criterion for a render whose deepest pixel walked max(n_last) contributors."""
+    nl = np.asarray(n_last)
+    return max(K_BOUND, ULP2 * float(nl.max() if nl.size else 0))
+
+
+def check_grads(gpu, ref, bound, label="", rtol=RTOL_GRAD, atol=ATOL_GRAD, k=K_BOUND):
+    gpu = np.asarray(gpu, np.float64)
+    ref = np.asarray(ref, np.float64)
+    bound = np.asarray(bound, np.float64)
+    err = np.abs(gpu - ref)
+    plain = err <= rtol * np.abs(ref) + atol
+    ok = plain | (err <= k * bound + atol)
+    nb = int((~plain).sum())
+    worst = float((err[~plain] / np.maximum(bound[~plain], 1e-300)).max()) if nb else 0.0
+    print(f"{label}: {err.size} elements, {nb} outside 2e-3 rel / 1e-6 abs (cancelling sums), "
+          f"max err/bound there {worst:.3g} (limit {k:g}); max err {float(err.max()) if err.size else 0:.3g}")
+    assert ok.all(), (f"{label}: {int((~ok).sum())} elements fail; first {np.argwhere(~ok)[:8].tolist()}, "
+                      f"err {err[~ok][:8].tolist()}, ref {ref[~ok][:8].tolist()}, bound {bound[~ok][:8].tolist()}")
+    return nb, worst
+
+
+def check_pose(gpu, ref, bound, label="", k=K_BOUND):
+    """The 6-vector twist: 2e-3 relative / 1e-6 absolute per component, or the summation bound."""
+    return check_grads(np.asarray(gpu).reshape(-1), np.asarray(ref).reshape(-1), np.asarray(bound).reshape(-1),
+                       label, k=k)

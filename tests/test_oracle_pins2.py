@@ -1,0 +1,146 @@
+"""Oracle pins added in round 2 (CPU, -m "not gpu"): every function is checked against something
+other than itself.
+
+- accum_grad (reading C30): hand-computed NDC norms and a finite-difference NDC chain rule;
+- pose_adam_step (reading C23): torch.optim.Adam on a 6-vector twist, scipy.linalg.expm for SE(3);
+- the backward's error-bound scale: dominance and exactness on sign-definite sums;
+- the power's evaluation order (reading R1 against SURVEY.md §8(c) O3): both orders take the same
+  decisions outside the oracle's tie band at configs 0-2.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import gs_inputs as gi
+import oracle
+
+
+# ------------------------------------------------------------------ accum_grad (reading C30)
+def test_accum_grad_hand_computed():
+    """Pixel-space mean gradients (3, 4) and (-6, 0.5) on a 200x100 image: NDC units multiply by
+    (W/2, H/2) = (100, 50), so the norms are |(300, 200)| = 360.5551 and |(-600, 25)| = 600.5206.
+    The off-screen Gaussian (tiles 0) is untouched; count increments only on screen."""
+    gs = np.zeros((10, 3))
+    gs[0] = [3.0, -6.0, 7.0]
+    gs[1] = [4.0, 0.5, 7.0]
+    tiles = np.array([2, 1, 0], np.uint32)
+    a, c = oracle.accum_grad(gs, tiles, 200, 100, np.array([1.0, 0.0, 5.0]), np.array([1.0, 0.0, 2.0]))
+    np.testing.assert_allclose(a, [1.0 + math.sqrt(300.0 ** 2 + 200.0 ** 2), math.sqrt(600.0 ** 2 + 25.0 ** 2), 5.0],
+                               rtol=1e-15)
+    np.testing.assert_array_equal(c, [2.0, 1.0, 2.0])
+
+
+def test_accum_grad_is_the_ndc_gradient_norm():
+    """Independent of the W/2, H/2 factors as typed: L(m) = g . m with m the pixel mean; in NDC
+    m = ((x + 1) W - 1) / 2 (3DGS's ndc2Pix), so dL/dx_ndc by central differences of L over x_ndc
+    must give the accumulated norm."""
+    rng = np.random.default_rng(5)
+    W, H = 640, 480
+    g = rng.normal(size=2)
+
+    def L(ndc):
+        m = np.array([((ndc[0] + 1.0) * W - 1.0) * 0.5, ((ndc[1] + 1.0) * H - 1.0) * 0.5])
+        return float(g @ m)
+    x0 = np.array([0.1, -0.2])
+    h = 1e-6
+    fd = np.array([(L(x0 + h * e) - L(x0 - h * e)) / (2 * h) for e in np.eye(2)])
+    gs = np.zeros((10, 1))
+    gs[0, 0], gs[1, 0] = g
+    a, c = oracle.accum_grad(gs, np.array([1], np.uint32), W, H, np.zeros(1), np.zeros(1))
+    np.testing.assert_allclose(a[0], np.linalg.norm(fd), rtol=1e-8)
+    assert c[0] == 1.0
+
+
+# ------------------------------------------------------------------ pose Adam + SE(3) (reading C23)
+def test_pose_adam_step_matches_torch_adam_and_expm():
+    """The twist delta of each step is torch.optim.Adam's update of a 6-vector parameter (per-group
+    lr for rho and phi); the pose is expm of the 4x4 twist matrix times the previous pose."""
+    torch = pytest.importorskip("torch")
+    from scipy.linalg import expm
+    rng = np.random.default_rng(8)
+    view = gi.room_view(103).astype(np.float64)
+    lr_rho, lr_phi = 2e-3, 5e-3
+    rho = torch.nn.Parameter(torch.zeros(3, dtype=torch.float64))
+    phi = torch.nn.Parameter(torch.zeros(3, dtype=torch.float64))
+    opt = torch.optim.Adam([{"params": [rho], "lr": lr_rho}, {"params": [phi], "lr": lr_phi}],
+                           betas=(0.9, 0.999), eps=1e-8)
+    m6, v6 = np.zeros(6), np.zeros(6)
+    ref = np.vstack([view, [0, 0, 0, 1]])
+    for step in range(1, 6):
+        gtw = rng.normal(size=6) * 10.0 ** rng.uniform(-3, 1)
+        before = torch.cat([rho, phi]).detach().numpy().copy()
+        opt.zero_grad()
+        rho.grad = torch.tensor(gtw[:3])
+        phi.grad = torch.tensor(gtw[3:])
+        opt.step()
+        delta_t = torch.cat([rho, phi]).detach().numpy() - before
+        out = oracle.pose_adam_step(view, gtw, m6, v6, step, lr_rho, lr_phi)
+        np.testing.assert_allclose(out["delta"], delta_t, rtol=1e-9, atol=1e-15)
+        X = np.zeros((4, 4))
+        X[:3, :3] = [[0, -delta_t[5], delta_t[4]], [delta_t[5], 0, -delta_t[3]], [-delta_t[4], delta_t[3], 0]]
+        X[:3, 3] = delta_t[:3]
+        ref = expm(X) @ ref
+        np.testing.assert_allclose(out["view"], ref[:3], atol=1e-12)
+        view, m6, v6 = out["view"], out["m"], out["v"]
+
+
+# ------------------------------------------------------------------ backward error-bound scale
+def _one(mean, scale, o, rgb, quat=(1.0, 0.0, 0.0, 0.0)):
+    p = np.zeros((14, 1))
+    p[0:3, 0], p[3:6, 0], p[6:10, 0], p[10, 0], p[11:14, 0] = mean, scale, quat, o, rgb
+    return p
+
+
+def test_error_bound_dominates_and_is_exact_on_sign_definite_sums():
+    """|grad| <= bound everywhere (config 0, N(0,1) upstream). For one Gaussian, black background
+    and positive upstream every per-pixel term of the opacity, colour and depth-path sums is
+    positive, so the bound equals the gradient there (rows 10-13); the mean rows mix signs left and
+    right of the centre, so their bound is strictly larger."""
+    cfg = gi.CONFIGS[0]
+    p, v, cam = cfg.scene(), cfg.view(), cfg.cam
+    dc, dd = gi.upstream(cam.width, cam.height, gi.UPSTREAM_SEED_CFG0)
+    o = oracle.backward(p, v, cam, dc, dd, "f32", bound=True)
+    assert np.all(np.abs(o["grad_params"]) <= o["grad_bound"] * (1 + 1e-12))
+    assert np.all(np.abs(o["pose_twist"]) <= o["pose_bound"] * (1 + 1e-12))
+    assert np.all(np.abs(o["pose_twist_paper"]) <= o["pose_bound_paper"] * (1 + 1e-12))
+    # cancellation is real at config 0: the median gradient is a few % of its scale
+    on = o["grad_bound"] > 0
+    assert np.median(np.abs(o["grad_params"][on]) / o["grad_bound"][on]) < 0.2
+
+    cam1 = gi.Camera(40.0, 40.0, 15.5, 15.5, 32, 32)
+    p1 = _one([0.05, -0.03, 2.0], [0.12, 0.08, 0.1], 0.7, [0.2, 0.5, 0.9],
+              quat=(0.9, 0.1, -0.2, 0.3))
+    rng = np.random.default_rng(2)
+    dc1 = rng.uniform(0.1, 1.0, (3, 32, 32)).astype(np.float32)
+    dd1 = rng.uniform(0.1, 1.0, (32, 32)).astype(np.float32)
+    o1 = oracle.backward(p1, gi.identity_view(), cam1, dc1, dd1, "f64", bound=True)
+    g, b = o1["grad_params"][:, 0], o1["grad_bound"][:, 0]
+    np.testing.assert_allclose(g[10:14], b[10:14], rtol=1e-12)
+    assert np.all(b[0:2] > np.abs(g[0:2]) * 1.01)
+
+
+# ------------------------------------------------------------------ power order (R1 vs O3)
+@pytest.mark.parametrize("c", [0, 1, 2])
+def test_power_order_decisions_equal_outside_tie_band(c):
+    """Reading R1 evaluates the exponent as fma(A dx, dx, fma(C dy, dy, (B dx) dy)); SURVEY.md §8(c)
+    O3 prints -0.5*((a*dx)*dx + (c*dy)*dy) - (b*dx)*dy. Both are fp32 evaluations of the plain
+    -1/2 d^T Sigma'^-1 d. Every pixel whose decisions (examined count, n_last) differ between the two
+    orders, or whose images differ by more than the parity tolerance (a flipped skip inside the list),
+    must be flagged ambiguous by the oracle (its tie band covers 4 u of the terms' magnitudes).
+    Config 2: 40k sampled pixels."""
+    cfg = gi.CONFIGS[c]
+    p, v, cam = cfg.scene(), cfg.view(), cfg.cam
+    px = None
+    if c == 2:
+        px = np.random.default_rng(0).choice(cam.width * cam.height, 40000, replace=False)
+    a = oracle.forward(p, v, cam, "f32", pixels=px)
+    b = oracle.forward(p, v, cam, "f32", pixels=px, o3_power=True)
+    img = np.maximum.reduce([np.abs(a["color"] - b["color"]).max(0), np.abs(a["depth"] - b["depth"]),
+                             np.abs(a["alpha"] - b["alpha"])])
+    # a flipped skip inside the list changes the image but not n_last / examined
+    dec = (a["n_last"] != b["n_last"]) | (a["examined"] != b["examined"]) | (img > 1e-4)
+    amb = (a["ambiguous"] == 1) | (b["ambiguous"] == 1)
+    assert not np.any(dec & ~amb), int((dec & ~amb).sum())
+    print(f"cfg{c}: {int(dec.sum())} pixels take other decisions, all in the tie band "
+          f"({int(amb.sum())} flagged of {dec.size})")
