@@ -2,10 +2,12 @@
 """Benchmark of the GS-SLAM hot path on B200 (BASELINE.json metric):
    fwd+bwd RGB-D render iters/s at 1200x680 with 500k Gaussians (config 2), and Gaussian-px evals/s.
 
-One step = gs_project + gs_bin_sort + gs_render_fwd + gs_loss_l1 + gs_render_bwd over one synthetic
-Replica-shaped frame, inputs resident in HBM. N > 1 (torchrun): independent
-replicas, one frame per rank ("replicas only" for single-frame rendering), time =
-max over ranks. `--impl reference` times the CPU oracle (the reference arm of this tier).
+One step at N = 1 = gs_project + gs_bin_sort + gs_render_fwd + gs_loss_l1 + gs_render_bwd over one
+synthetic Replica-shaped frame (config 2), inputs resident in HBM. At N > 1 the
+default is the path that shards: config 4's keyframe-sharded mapping (8 keyframes over N ranks,
+NCCL all-reduce of the gradient); `--gpus N` outside torchrun re-launches itself
+under torch.distributed.run. Time = max over ranks. `--impl reference` times the CPU oracle (the
+reference arm of this tier).
 Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
@@ -46,7 +48,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=None,
+                    help="default: 2 (the headline frame) at N = 1, 4 (keyframe-sharded mapping) at N > 1")
     ap.add_argument("--binsort", default="bucket", choices=["bucket", "keys"])
     ap.add_argument("--sh", type=int, default=0, choices=[0, 1],
                     help="colour model: 0 = RGB (BASELINE configs), 1 = degree-1 SH (NEXT-1, gs_project_sh)")
@@ -131,33 +134,56 @@ def dist_env():
 def init_dist(world, backend):
     import torch.distributed as dist
     if world > 1 and not dist.is_initialized():
+        if backend == "nccl":   # communicator set-up lines on stderr (stdout keeps the JSON line)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group(backend)
     return dist if world > 1 else None
 
 
 # ----------------------------------------------------------------------------------- reference arm
-def cpu_sample(cfg, frac_rows=16):
-    """Bounded oracle sample of one config-`cfg` iteration: every `frac_rows`-th pixel row."""
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_iteration(cfg):
+    """One WHOLE oracle iteration of config `cfg` (no sampling, no scaling): oracle.forward (its own
+    projection, global depth sort and per-pixel blend of every pixel), the Eq. 6 L1 loss against the
+    config's target, and oracle.backward (which re-blends every pixel and chains every Gaussian). The
+    target is the oracle's own render of the config's target scene at the same pose (the workload our
+    arm times), made once, untimed. Returns run() -> per-stage seconds."""
     import numpy as np
     import gs_inputs as gi
     import oracle
     cam = cfg.cam
-    rows = np.arange(0, cam.height, frac_rows)
-    px = (rows[:, None] * cam.width + np.arange(cam.width)[None, :]).reshape(-1)
     p, v = cfg.scene(), cfg.view()
-    tc, td = gi.random_images(cam.width, cam.height, 77)
+    if cfg.target_seed is not None:
+        t = oracle.forward(gi.gaussians(cfg.n, cfg.target_seed, cfg.lo, cfg.hi), v, cam, "f32")
+        tc, td = t["color"].astype(np.float32), t["depth"].astype(np.float32)
+    else:
+        tc, td = gi.random_images(cam.width, cam.height, 77)
 
     def run():
-        f = oracle.forward(p, v, cam, "f32", pixels=px)
-        L = oracle.loss_l1(f["color"].reshape(3, 1, -1), f["depth"].reshape(1, -1), tc.reshape(3, -1)[:, px][:, None],
-                           td.reshape(-1)[px][None], cfg.w_color, cfg.w_depth)
-        dc = np.zeros((3, cam.height * cam.width), np.float32)
-        dd = np.zeros(cam.height * cam.width, np.float32)
-        dc[:, px] = L["dL_dcolor"].reshape(3, -1)
-        dd[px] = L["dL_ddepth"].reshape(-1)
-        oracle.backward(p, v, cam, dc, dd, "f32", pixels=px)
-    return run, px.size / (cam.width * cam.height), f"every {frac_rows}th pixel row ({px.size} px) of one " \
-        f"config-{2} fwd+bwd iteration; value scaled to whole iterations"
+        t0 = time.perf_counter()
+        f = oracle.forward(p, v, cam, "f32")
+        t1 = time.perf_counter()
+        L = oracle.loss_l1(f["color"], f["depth"], tc, td, cfg.w_color, cfg.w_depth)
+        t2 = time.perf_counter()
+        oracle.backward(p, v, cam, L["dL_dcolor"], L["dL_ddepth"], "f32")
+        t3 = time.perf_counter()
+        return {"forward": t1 - t0, "loss_l1": t2 - t1, "backward": t3 - t2}
+    desc = (f"one whole config-{cfg_index(cfg)} ({cfg.name}) iteration per step ({cam.width}x{cam.height}, {cfg.n} Gaussians): "
+            "oracle forward (projection, global depth sort, every pixel), L1 loss, backward (re-blend, chain); "
+            "no sampling or scaling")
+    return run, desc
 
 
 def run_reference(args):
@@ -168,26 +194,43 @@ def run_reference(args):
     import oracle
     cores = len(os.sched_getaffinity(0))
     oracle.set_threads(cores)
-    cfg = gi.CONFIGS[args.config]
-    run, frac, desc = cpu_sample(cfg)
+    cfg = gi.CONFIGS[args.config if args.config is not None else 2]
+    mapping = cfg_index(cfg) == 4
+    run, desc = oracle_iteration(cfg)
     for _ in range(max(args.warmup, 0)):
         run()
+    stages = {}
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        run()
+        for k, dt_ in run().items():
+            stages[k] = stages.get(k, 0.0) + dt_
     dt = (time.perf_counter() - t0) / max(args.steps, 1)
-    value = frac / dt
-    line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": dt * 1e3 / frac, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"config {args.config}: {cfg.name} {cfg.cam.width}x{cfg.cam.height}, {cfg.n} Gaussians, "
-                                   f"fwd+bwd L1 (0.9/0.1) iteration", "n_gaussians": cfg.n, "width": cfg.cam.width,
-                                   "height": cfg.cam.height},
-            "cpu_baseline": {"value": value, "unit": "iters/s", "cores": oracle.num_threads(), "kind": "oracle",
-                             "sample": desc},
-            "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    value = 1.0 / dt
+    unit = "iters/s"
+    if mapping:   # a step is one keyframe's render of the 8-keyframe mapping iteration (our arm's unit)
+        value, unit = value / len(gi.MAPPING_POSE_SEEDS), "mapping iters/s"
+        desc += (f"; config 4 sample: keyframe 0 of the {len(gi.MAPPING_POSE_SEEDS)}-keyframe mapping iteration per "
+                 "step, value = 1 / (8 x step time); the oracle's Adam and densify (numpy, per-Gaussian) not timed")
+    cpu = {"value": value, "unit": unit, "cores": oracle.num_threads(), "kind": "oracle", "sample": desc,
+           "cpu_model": cpu_model(), "stage_s": {k: v_ / max(args.steps, 1) for k, v_ in stages.items()}}
+    line = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Replica-shaped room scene, SURVEY.md §8(d))",
+            "impl": "reference",
+            "config": {"workload": f"config {cfg_index(cfg)}: {cfg.name} {cfg.cam.width}x{cfg.cam.height}, {cfg.n} "
+                                   f"Gaussians, fwd+bwd L1 (0.9/0.1) iteration", "sh_degree": 0,
+                       "n_gaussians": cfg.n, "width": cfg.cam.width, "height": cfg.cam.height,
+                       "target": f"render of scene seed {cfg.target_seed} at the same pose",
+                       "parallelism": "oracle on the host cores (OpenMP)"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def cfg_index(cfg):
+    import gs_inputs as gi
+    return next(k for k, c in gi.CONFIGS.items() if c is cfg)
 
 
 # ----------------------------------------------------------------------------------- our arm
@@ -227,7 +270,7 @@ def main_ours(args):
     K = fr.n_keys
     E_f = int(a["examined"].to(torch.int64).sum().item())
     E_b = int(a["n_last"].to(torch.int64).sum().item())
-    Lf, Lb = live_evals(a, cam)
+    Lf, Lb, Sf, Sb = live_evals(a, cam)
     V_s = int((a["tiles"] > 0).sum().item())
     V_front = int((a["radius"] > 0).sum().item())
     del probe
@@ -307,7 +350,7 @@ def main_ours(args):
                                   + (", opacity-aware radius (C33)" if args.opacity_radius else ""),
                       "sh_degree": args.sh, "n_gaussians": n, "width": cam.width,
                       "height": cam.height, "keys": K, "visible": V_front, "on_screen": V_s, "E_f": E_f, "E_b": E_b,
-                      "E_f_live": Lf, "E_b_live": Lb,
+                      "E_f_live": Lf, "E_b_live": Lb, "block_slots_fwd": Sf, "block_slots_bwd": Sb,
                       "binsort": args.binsort, "cuda_graph": not args.no_graph, "l2": "per-iteration working set > L2 (126 MB): tile lists "
                       f"{K * 4 / 1e9:.2f} GB + live lists; no flush", "parallelism": f"replicas x{world}"},
            "evals_per_s": world * (E_f + E_b) * 1000.0 / ms, "clocks": clocks, "gpu_launches": int(launches),
@@ -336,71 +379,92 @@ def main_ours(args):
         out["ms_per_step_with_event_log"] = ms_logged
         out["roofline"], out["kernels_roofline"] = roofline(
             per_step, clocks, K=K, n=n, V_s=V_s, E_f=Lf, E_b=Lb, npx=cam.width * cam.height, binsort=args.binsort,
-            GX=(cam.width + 15) // 16, GY=(cam.height + 15) // 16)
-        # ---- e2e through the public API with host buffers (pinned) and a loss readback
+            GX=(cam.width + 15) // 16, GY=(cam.height + 15) // 16,
+            sms=torch.cuda.get_device_properties(dev).multi_processor_count)
+        # ---- e2e through the public API with host buffers (pinned): every step uploads its inputs
+        # (params, pose, RGB-D target) from pinned host memory and reads its result back (the 14 x n
+        # gradient, the pose twist and the loss). Buffer sets are double-buffered: step i+1's upload
+        # (copy stream) and step i-1's read-back (a second copy stream) overlap step i's kernels; all
+        # of it inside the timed region.
         if not args.no_e2e:
-            # every step uploads its inputs (params, pose, RGB-D target) from pinned host memory and
-            # reads its loss back; uploads are double-buffered on a copy stream so step i+1's copy
-            # overlaps step i's kernels (both inside the timed region)
             hp = torch.empty_like(P, device="cpu").pin_memory()
             hp.copy_(P.cpu())
             hv = V.cpu().pin_memory()
             htc, htd = tc.cpu().pin_memory(), td.cpu().pin_memory()
-            hloss = torch.empty(1, dtype=torch.float64).pin_memory()
-            bufs = [(torch.empty_like(P), torch.empty_like(V), torch.empty_like(tc), torch.empty_like(td))
-                    for _ in range(2)]
-            s_copy = torch.cuda.Stream()
+            hgrad = [torch.empty_like(grad, device="cpu").pin_memory() for _ in range(2)]
+            hpose = [torch.empty(6, dtype=torch.float64).pin_memory() for _ in range(2)]
+            hloss = [torch.empty(1, dtype=torch.float64).pin_memory() for _ in range(2)]
+            bufs = [(torch.empty_like(P), torch.empty_like(V), torch.empty_like(tc), torch.empty_like(td),
+                     torch.empty_like(grad), torch.empty_like(gpose), torch.empty_like(pipe.loss)) for _ in range(2)]
+            s_up, s_down = torch.cuda.Stream(), torch.cuda.Stream()
             ev_copied = [torch.cuda.Event() for _ in range(2)]
-            ev_used = [torch.cuda.Event() for _ in range(2)]
-            for e in ev_used:
+            ev_done = [torch.cuda.Event() for _ in range(2)]
+            ev_read = [torch.cuda.Event() for _ in range(2)]
+            for e in ev_read:
                 e.record()
 
             def upload(i):
                 b = bufs[i % 2]
-                with torch.cuda.stream(s_copy):
-                    s_copy.wait_event(ev_used[i % 2])
-                    for dst, src in zip(b, (hp, hv, htc, htd)):
+                with torch.cuda.stream(s_up):
+                    s_up.wait_event(ev_done[i % 2])    # the step that last read these inputs is done
+                    for dst, src in zip(b[:4], (hp, hv, htc, htd)):
                         dst.copy_(src, non_blocking=True)
-                    ev_copied[i % 2].record(s_copy)
+                    ev_copied[i % 2].record(s_up)
+
+            def download(i):
+                b = bufs[i % 2]
+                with torch.cuda.stream(s_down):
+                    s_down.wait_event(ev_done[i % 2])
+                    hgrad[i % 2].copy_(b[4], non_blocking=True)
+                    hpose[i % 2].copy_(b[5], non_blocking=True)
+                    hloss[i % 2].copy_(b[6], non_blocking=True)
+                    ev_read[i % 2].record(s_down)
 
             def iteration_on(b):
-                Pd, Vd, tcd, tdd = b
-                return lambda: pipe.iteration(Pd, n, Vd, cam, tcd, tdd, grad, gpose, bin_flags=flags, fwd_flags=0,
-                                              assign_grads=True, fused_loss=True, proj_flags=proj_flags)
+                Pd, Vd, tcd, tdd, gd, gpd, ld = b
 
-            # one captured graph per upload buffer set (as in the device-timed run)
+                def it():
+                    pipe.iteration(Pd, n, Vd, cam, tcd, tdd, gd, gpd, bin_flags=flags, fwd_flags=0,
+                                   assign_grads=True, fused_loss=True, proj_flags=proj_flags)
+                    ld.copy_(pipe.loss)
+                return it
+
             its = [iteration_on(b) for b in bufs]
             if not args.no_graph:
                 its = [capture(f).replay for f in its]
 
             def e2e_run(steps):
                 cur = torch.cuda.current_stream()
-                s_copy.wait_stream(cur)   # the first upload starts inside the timed region
+                s_up.wait_stream(cur)   # the first upload starts inside the timed region
                 upload(0)
                 for i in range(steps):
                     if i + 1 < steps:
                         upload(i + 1)
                     cur.wait_event(ev_copied[i % 2])
+                    cur.wait_event(ev_read[i % 2])   # step i-2's result has left this buffer set
                     its[i % 2]()
-                    ev_used[i % 2].record(cur)
-                    hloss.copy_(pipe.loss, non_blocking=True)
+                    ev_done[i % 2].record(cur)
+                    download(i)
+                cur.wait_stream(s_down)   # the last read-back is inside the timed region
             e2e_run(3)
             ms_e2e = timed(lambda: e2e_run(args.steps), 1) / args.steps
             h2d = P.numel() * 4 + V.numel() * 4 + tc.numel() * 4 + td.numel() * 4
+            d2h = n * 14 * 4 + 6 * 8 + 8
             out["e2e"] = {"value": world * 1000.0 / ms_e2e, "unit": "iters/s", "h2d_bytes_per_step": int(h2d),
-                          "d2h_bytes_per_step": 8, "overlap": "double-buffered H2D on a copy stream"}
-        # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
+                          "d2h_bytes_per_step": int(d2h),
+                          "overlap": "double-buffered H2D and D2H on two copy streams (PCIe)",
+                          "d2h": "grad[14][n] (assigned), pose twist f64[6], loss f64"}
+        # ---- CPU baseline: one whole oracle iteration of the same workload (rank 0, N = 1 only)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             try:
                 import oracle
                 cores = len(os.sched_getaffinity(0))
                 oracle.set_threads(cores)
-                run, frac, desc = cpu_sample(cfg)
-                t0 = time.perf_counter()
-                run()
-                dt = time.perf_counter() - t0
-                out["cpu_baseline"] = {"value": frac / dt, "unit": "iters/s", "cores": oracle.num_threads(),
-                                       "kind": "oracle", "sample": desc}
+                run, desc = oracle_iteration(cfg)
+                st = run()
+                dt = sum(st.values())
+                out["cpu_baseline"] = {"value": 1.0 / dt, "unit": "iters/s", "cores": oracle.num_threads(),
+                                       "kind": "oracle", "sample": desc, "cpu_model": cpu_model(), "stage_s": st}
             except Exception as exc:   # the baseline is reported, never required for our number
                 out["cpu_baseline"] = {"value": None, "unit": "iters/s", "cores": None, "kind": "oracle",
                                        "sample": f"failed: {exc!r}"}
@@ -433,23 +497,34 @@ def live_evals(a, cam):
     def count(upto):
         q = (ptile << 32) | upto.to(torch.int64)
         return int((torch.searchsorted(key, q.flatten(), right=True) - seg0[ptile.flatten()]).sum().item())
-    return count(a["examined"]), count(a["n_last"])
+
+    def slots(upto):
+        """Block-slot evaluations: 256 x the live entries a tile's block walks, i.e.
+        those up to the tile's deepest pixel."""
+        tmax = torch.zeros(T, dtype=torch.int64, device=dev).scatter_reduce(
+            0, ptile.flatten(), upto.flatten().to(torch.int64), reduce="amax")
+        q = (torch.arange(T, device=dev) << 32) | tmax
+        return int(256 * (torch.searchsorted(key, q, right=True) - seg0).sum().item())
+    return count(a["examined"]), count(a["n_last"]), slots(a["examined"]), slots(a["n_last"])
 
 
-def roofline(per_step, clocks, K, n, V_s, E_f, E_b, npx, binsort="bucket", GX=75, GY=43):
+def roofline(per_step, clocks, K, n, V_s, E_f, E_b, npx, binsort="bucket", GX=75, GY=43, sms=148):
     """Roofline of the dominant kernel (the JSON line's "roofline") plus the same figures for every
-    kernel with a defined algorithmic work (the line's "kernels_roofline"). Work per unit: DESIGN.md §6."""
+    kernel with a defined algorithmic work (the line's "kernels_roofline"). Work per unit: DESIGN.md §6.
+    ALU kernels count FP32 lane operations (an FFMA is one), against sms x 128 lanes x the SM clock
+    sampled during the run; `ncu` adds the measured FMA-pipe and issue activity of the same kernel
+    (profiles/ncu_metrics.json, from the round's --set full capture)."""
     peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json"), {}) or {}
     hbm_peak = peaks.get("hbm_gbs")
     hbm_src = "measured" if hbm_peak else "fallback"
     hbm_peak = hbm_peak or 6650.0
     sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz") or 1965.0
-    alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e12   # FP32 lane-ops/s, T
+    alu_peak = sms * 128 * sm_mhz * 1e6 / 1e12   # FP32 lane-ops/s, T
     T = GX * GY
     nch = (V_s + 255) // 256
     work = {   # (bound, algorithmic amount PER LAUNCH, unit) -- DESIGN.md §6 table
-        "render_bwd_tiles": ("alu", E_b * BWD_OPS_PER_EVAL / 1e12, "TFLOP/s"),
-        "render_fwd": ("alu", E_f * FWD_OPS_PER_EVAL / 1e12, "TFLOP/s"),
+        "render_bwd_tiles": ("alu", E_b * BWD_OPS_PER_EVAL / 1e12, "T FP32 lane-op/s"),
+        "render_fwd": ("alu", E_f * FWD_OPS_PER_EVAL / 1e12, "T FP32 lane-op/s"),
         # path A sorts K (u64, u32) pairs per pass
         "sort_pass": ("hbm", K * SORT_BYTES_PER_KEY / 1e9, "GB/s"),
         "emit_keys": ("hbm", (K * 12 + n * 20) / 1e9, "GB/s"),
@@ -466,6 +541,7 @@ def roofline(per_step, clocks, K, n, V_s, E_f, E_b, npx, binsort="bucket", GX=75
         "sgrad_clear": ("hbm", (V_s * 40 + npx * 4) / 1e9, "GB/s"),
     }
     prof = load_json(os.path.join(ROOT, "profiles", "ncu_traffic.json"), {}) or {}
+    ncu = load_json(os.path.join(ROOT, "profiles", "ncu_metrics.json"), {}) or {}
     table = {}
     for k, (bound, amount, unit) in work.items():
         if k not in per_step:
@@ -475,10 +551,13 @@ def roofline(per_step, clocks, K, n, V_s, E_f, E_b, npx, binsort="bucket", GX=75
         peak = alu_peak if bound == "alu" else hbm_peak
         table[k] = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
                     "traffic": prof.get(k), "share_of_step": t_ms / sum(v[0] for v in per_step.values())}
+        if k in ncu:
+            table[k]["ncu"] = ncu[k]
     dom = max(table, key=lambda k: per_step[k][0])
     top = dict(table[dom])
     top["kernel"] = dom
-    top["peak_source"] = (("FP32 148 SMs x 128 lanes x measured median SM clock %.0f MHz" % sm_mhz)
+    top["peak_source"] = (("FP32 %d SMs (multiProcessorCount) x 128 lanes x measured median SM clock %.0f MHz"
+                           % (sms, sm_mhz))
                           if top["bound"] == "alu" else f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})")
     return top, {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                  for k, v in table.items()}
@@ -576,8 +655,24 @@ def main_tracking(args):
     return 0
 
 
+def count_own_kernels(fn) -> int:
+    """Kernels of libgs.so (namespace gs::) launched by one call of fn, from a CUPTI trace (outside
+    any timed region)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    return sum(1 for e in prof.events() if e.device_type.name == "CUDA" and "gs::" in e.name)
+
+
 def main_mapping(args):
-    """Config 4: keyframe-sharded mapping, 2M Gaussians, 8 keyframes at 1200x680 over N GPUs."""
+    """Config 4: keyframe-sharded mapping, 2M Gaussians, 8 keyframes at 1200x680 over N GPUs (one
+    rank per GPU, NCCL). A step = one mapping iteration: every rank renders fwd + L1 + bwd of its
+    keyframes (8/N each), the gradient [14][n] is all-reduced, every rank runs the same Adam step,
+    then the Eq. 8 expansion (candidates all-gathered) and the opacity prune (BASELINE config 4)."""
+    import numpy as np
     import torch
 
     import gs_inputs as gi
@@ -587,40 +682,76 @@ def main_mapping(args):
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
     dist = init_dist(world, "nccl")
+    dev = torch.device("cuda", local)
     cfg = gi.CONFIGS[4]
     cam = cfg.cam
     n = cfg.n
     cap = int(n * 1.05) + 65536
-    P = torch.zeros(14, cap, device="cuda")
-    P[:, :n] = torch.as_tensor(cfg.scene(), device="cuda")
-    tgt = torch.as_tensor(gi.gaussians(n, cfg.target_seed), device="cuda")
-    probe = g.RenderPipeline(n, 1 << 28, cam.width, cam.height)
+    P = torch.zeros(14, cap, device=dev)
+    P[:, :n] = torch.as_tensor(cfg.scene(), device=dev)
+    tgt = torch.as_tensor(gi.gaussians(n, cfg.target_seed, cfg.lo, cfg.hi), device=dev)
+    probe = g.RenderPipeline(n, 1 << 28, cam.width, cam.height, dev)
     kfs, kmax = [], 0
     for s in gi.MAPPING_POSE_SEEDS:
-        V = torch.as_tensor(gi.room_view(s), device="cuda")
+        V = torch.as_tensor(gi.room_view(s), device=dev)
+        kmax = max(kmax, probe.forward(P, n, V, cam).n_keys)
         fr = probe.forward(tgt, n, V, cam)
-        kmax = max(kmax, fr.n_keys, probe.forward(P, n, V, cam).n_keys)
-        fr = probe.forward(tgt, n, V, cam)
+        kmax = max(kmax, fr.n_keys)
         kfs.append(Keyframe(V, fr.color.clone(), fr.depth.clone()))
     del probe
     torch.cuda.empty_cache()
-    mp = ShardedMapper(P, n, kfs, cam, int(kmax * 1.2) + (1 << 20), max_add_per_kf=8192, group=None)
+    mp = ShardedMapper(P, n, kfs, cam, int(kmax * 1.3) + (1 << 20), max_add_per_kf=8192, group=None)
     for _ in range(max(args.warmup, 3)):
         mp.step()
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    ms = _timed_events(mp.step, args.steps)
-    if dist:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    out = {"metric": "multi-keyframe mapping iters/s (config 4: 2M Gaussians, 8 keyframes 1200x680)",
-           "value": 1000.0 / ms, "unit": "iters/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-           "data": "synthetic", "config": {"workload": "config 4 mapping", "keyframes": len(kfs),
-                                           "keyframes_per_rank": len(mp.local), "n_gaussians_end": mp.n,
-                                           "parallelism": f"keyframe shards x{world}, NCCL all_reduce"}}
+    launches = count_own_kernels(mp.step)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    def timed(fn, steps):
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        ms = _timed_events(fn, steps)
+        barrier()
+        if dist:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    with ClockSampler(local) as clk:
+        ms = timed(mp.step, args.steps)
+    clocks = clk.summary()
+    # e2e: every step uploads its local keyframes' RGB-D targets and poses from pinned host memory
+    # and reads back the loss and the map size (the step's result)
+    mine = [kfs[k] for k in mp.local]
+    host = [(kf.view.cpu().pin_memory(), kf.color.cpu().pin_memory(), kf.depth.cpu().pin_memory()) for kf in mine]
+    res = torch.empty(2, dtype=torch.float64).pin_memory()
+
+    def e2e_step():
+        for kf, (hv, hc, hd) in zip(mine, host):
+            kf.view.copy_(hv, non_blocking=True)
+            kf.color.copy_(hc, non_blocking=True)
+            kf.depth.copy_(hd, non_blocking=True)
+        mp.step()
+        res.copy_(torch.stack([mp.pipe.loss.reshape(-1)[0], mp.n_dev[0].to(torch.float64)]), non_blocking=True)
+    ms_e2e = timed(e2e_step, args.steps)
+    h2d = sum(a.numel() * a.element_size() for t in host for a in t)
+    out = {"metric": METRIC, "value": 1000.0 / ms, "unit": "mapping iters/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic (seeded 2M-Gaussian room, 8 seeded keyframe poses, SURVEY.md §8(d))",
+           "config": {"workload": "config 4: mapping, 2M Gaussians, 8 keyframes 1200x680 (fwd + L1 + bwd per keyframe, "
+                                  "all-reduce of grad[14][n], Adam, Eq. 8 add + prune); value = box-wide mapping "
+                                  "iterations/s", "keyframes": len(kfs), "keyframes_per_rank": len(mp.local),
+                      "n_gaussians_start": n, "n_gaussians_end": mp.n,
+                      "parallelism": f"keyframe shards x{world}, NCCL all_reduce" if world > 1 else "1 GPU",
+                      "l2": "per-keyframe working set > L2; no flush"},
+           "keyframe_renders_per_s": len(kfs) * 1000.0 / ms, "clocks": clocks, "gpu_launches": launches,
+           "e2e": {"value": 1000.0 / ms_e2e, "unit": "mapping iters/s", "h2d_bytes_per_step": int(h2d),
+                   "d2h_bytes_per_step": 16}}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if dist:
@@ -628,8 +759,32 @@ def main_mapping(args):
     return 0
 
 
+def relaunch(args) -> int:
+    """`bench.py --gpus N` (N > 1) outside torchrun: re-run this script under torch.distributed.run with
+    one process per GPU on 127.0.0.1; NCCL prints its communicator set-up (NCCL_DEBUG=INFO, INIT)
+    on stderr so stdout keeps the one JSON line."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    under_launcher = "WORLD_SIZE" in os.environ
+    if args.impl == "ours" and args.gpus > 1 and not under_launcher:
+        return relaunch(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.config is None:   # 1 GPU: the headline frame (config 2); N GPUs: the sharded mapping (config 4)
+        args.config = 4 if world > 1 else 2
     if args.impl == "reference":
         return run_reference(args)
     if args.config == 3:

@@ -28,7 +28,7 @@ import threading
 import torch
 
 from . import gs_image_half
-from .mapping import Keyframe, ShardedMapper
+from .mapping import Keyframe, ShardedMapper, SplitClone
 from .tracking import Frontend, FrontendConfig, Tracker
 
 
@@ -42,6 +42,8 @@ class SlamConfig:
     seed: int = 0              # window sampling
     degenerate: tuple[float, float] | None = None   # Eq. 9 (eta, gamma) in the expansion step (NEXT-2)
     sh_degree: int = 0         # 1: the paper's degree-1 SH colour (23 parameter rows, NEXT-1)
+    ba: bool = True            # keyframe poses refined in the window's second half (Eq. 13)
+    split_clone: SplitClone | None = dataclasses.field(default_factory=SplitClone)
 
 
 class SlamSystem:
@@ -56,7 +58,8 @@ class SlamSystem:
         rows = 23 if cfg.sh_degree == 1 else 14
         with torch.cuda.stream(self.ms):
             self.mapper = ShardedMapper(torch.zeros(rows, n_cap, device=dev), 0, [], cam, key_cap_full,
-                                        max_add_per_kf=max_add, densify=True, degenerate=cfg.degenerate)
+                                        max_add_per_kf=max_add, densify=True, degenerate=cfg.degenerate,
+                                        split_clone=cfg.split_clone)
         with torch.cuda.stream(self.ts):
             self.tracker = Tracker(n_cap, key_cap_full, key_cap_half, cam, device)
             self.frontend = Frontend(self.tracker, cfg.frontend)
@@ -87,17 +90,25 @@ class SlamSystem:
         m = self.mapper
         with torch.cuda.stream(self.ms):
             self.ms.wait_event(produced)   # the keyframe's pose and images (tracking stream)
+            if not self.keyframes:
+                kf.fixed = True    # the first keyframe anchors the world frame (its pose is never moved)
             self.keyframes.append(kf)
             m.it = 0   # per-keyframe learning-rate schedule (PAPER.md:931-933 over the mapping iterations)
             m.densify = True
+            m.ba_iters = None
             m.set_keyframes([kf])   # expansion from the new keyframe only (Eq. 8, "at every keyframe")
             m.step()
             m.densify = False
             older = self.keyframes[:-1]
             window = [kf] + self.rng.sample(older, min(self.cfg.window - 1, len(older)))
             m.set_keyframes(window)
+            # bundle adjustment over the window (Eq. 13): the map alone in the first
+            # half of the iterations, map and keyframe poses in the second; the first-order SH
+            # coefficients are optimised only here
+            m.ba_iters = self.cfg.map_iters if self.cfg.ba else None
             for _ in range(self.cfg.map_iters - 1):
                 m.step()
+            m.ba_iters = None
             self._publish()
             self.map_rounds += 1
 
@@ -114,16 +125,19 @@ class SlamSystem:
             self.pending = b
 
     def _map_loop(self):
-        try:
-            while True:
-                job = self.jobs.get()
+        # the worker lives until the None sentinel and marks every job done, so join() never blocks;
+        # after a failure the remaining jobs are skipped and the error surfaces in process() / finish()
+        while True:
+            job = self.jobs.get()
+            try:
                 if job is None:
                     return
-                self._map_keyframe(*job)
+                if self.error is None:
+                    self._map_keyframe(*job)
+            except BaseException as e:
+                self.error = e
+            finally:
                 self.jobs.task_done()
-        except BaseException as e:   # surfaced to the caller by process() / finish()
-            self.error = e
-            self.jobs.task_done()
 
     # ------------------------------------------------------------------ tracking side (stream ts)
     def _take_snapshot(self):

@@ -33,7 +33,7 @@ def _mapping_module():
                          "GS_DENSIFY_DEGENERATE_FLAG"):
                 setattr(stub, name, 0)
             for name in ("densify_cfg", "gs_adam_step", "gs_adam_step_rows", "gs_densify_append", "gs_densify_prune",
-                         "make_camera"):
+                         "make_camera", "gs_densify_accum_grad", "gs_densify_split_clone", "gs_pose_step"):
                 setattr(stub, name, None)
             sys.modules["paper_2311_11700_b200"] = stub
             pl = types.ModuleType("paper_2311_11700_b200.pipeline")
@@ -42,6 +42,7 @@ def _mapping_module():
     spec = importlib.util.spec_from_file_location("paper_2311_11700_b200.mapping",
                                                   os.path.join(ROOT, "paper_2311_11700_b200", "mapping.py"))
     mod = importlib.util.module_from_spec(spec)
+    sys.modules[spec.name] = mod   # dataclasses resolve their module through sys.modules
     spec.loader.exec_module(mod)
     return mod
 
@@ -67,6 +68,19 @@ def test_learning_rate_schedule_endpoints():
     assert math.isclose(m.learning_rates(0)[0], 1.6e-5)
     assert math.isclose(m.learning_rates(100)[0], 1.7e-7, rel_tol=1e-9)
     assert m.learning_rates(50)[10] == 1e-2 and m.learning_rates(7)[11] == 5e-4
+    # first-order SH coefficients (rows 14-22) only in bundle adjustment
+    lr = m.learning_rates(3, rows=23, sh_linear=False)
+    assert lr[11:14] == [5e-4] * 3 and lr[14:] == [0.0] * 9
+    assert m.learning_rates(3, rows=23, sh_linear=True)[14:] == [5e-4] * 9
+
+
+def test_uneven_shards_pad_to_equal_exchange_sizes():
+    m = _mapping_module()
+    for nk, world in ((8, 3), (1, 2), (5, 4), (3, 8)):
+        per = m.shard_size(nk, world)
+        got = [m.shard(nk, world, r) for r in range(world)]
+        assert sum(got, []) == list(range(nk))
+        assert all(len(g) <= per for g in got)
 
 
 def _tiny_world(seed=0):
@@ -100,6 +114,57 @@ def _degen_flags(p, cam, views, k):
     return oracle.degenerate_mask(pr["mean2d"], pr["depth"], pr["tiles"], td, gamma=0.10)
 
 
+def _gather_worker(rank, world, port, nk, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = _mapping_module()
+        local = m.shard(nk, world, rank)
+        S = m.shard_size(nk, world)
+        cand = torch.zeros(S, 14, 4)
+        counts = torch.zeros(S, dtype=torch.int64)
+        for j, k in enumerate(local):
+            counts[j] = 1 + k % 4
+            cand[j, :, :1 + k % 4] = float(k)
+        allc, allk = m.gather_candidates(cand, counts)
+        g = torch.arange(5, dtype=torch.float32).repeat(3, 1) * (rank + 1)
+        m.allreduce_grads(g, 3)   # only the first 3 columns are summed
+        out[rank] = (allc.numpy().copy(), allk.numpy().copy(), g.numpy().copy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_gloo_world3_uneven_candidate_gather_and_partial_allreduce():
+    """8 keyframes over 3 ranks (3/3/2) and 1 keyframe over 2 ranks (1/0): equal-sized exchanges, the
+    sets arrive in global keyframe order with the padding sets empty; allreduce_grads(g, n) sums only
+    the n live columns of every row."""
+    ctx = mp.get_context("spawn")
+    for nk, world in ((8, 3), (1, 2)):
+        mgr = ctx.Manager()
+        out = mgr.dict()
+        port = _free_port()
+        procs = [ctx.Process(target=_gather_worker, args=(r, world, port, nk, out)) for r in range(world)]
+        for pr in procs:
+            pr.start()
+        for pr in procs:
+            pr.join(240)
+            assert pr.exitcode == 0
+        allc, allk, g = out[0]
+        for r in range(1, world):
+            np.testing.assert_array_equal(out[r][0], allc)
+            np.testing.assert_array_equal(out[r][1], allk)
+        got = [int(c) for c in allk if c > 0]
+        assert got == [1 + k % 4 for k in range(nk)]
+        live = [i for i, c in enumerate(allk) if c > 0]
+        for k, i in enumerate(live):
+            assert (allc[i, :, :1 + k % 4] == k).all()
+        tot = sum(range(1, world + 1))
+        np.testing.assert_array_equal(g[:, :3], np.arange(3, dtype=np.float32)[None].repeat(3, 0) * tot)
+        np.testing.assert_array_equal(g[:, 3:], np.arange(3, 5, dtype=np.float32)[None].repeat(3, 0))
+
+
 def _worker(rank, world, port, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -114,7 +179,7 @@ def _worker(rank, world, port, out):
         for k in local:
             dc, dd = gi.upstream(cam.width, cam.height, 100 + k)
             grad += torch.from_numpy(oracle.backward(p, views[k], cam, dc, dd, "f64")["grad_params"])
-        m.allreduce_grads(grad)
+        m.allreduce_grads(grad, grad.shape[1])
         # densify candidates: one padded set per local keyframe, count = k + 1, payload tagged by k
         max_add = 6
         cand = torch.zeros(len(local), 14, max_add)
