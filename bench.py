@@ -620,9 +620,22 @@ def main_tracking(args):
         V.copy_(torch.as_tensor(Vp, dtype=torch.float32))
         tr.reset()
         t_c = _timed_events(lambda: tr.coarse_iter(P, n, V, tch, tdh, tcfg), tcfg.iters_coarse)
+        e_c = pose_error(V.cpu().numpy(), view)
+        Vc = V.clone()
+        m6, v6, stp = tr.m6.clone(), tr.v6.clone(), tr.step
         tr.select(P, n, V, tdf, tcfg)
+        n_sel = int(tr.mask[:n].sum().item())
         t_f = _timed_events(lambda: tr.fine_iter(P, n, V, tcf, tdf, tcfg), tcfg.iters_fine)
         e1 = pose_error(V.cpu().numpy(), view)
+        # diagnostic: the same fine stage on every Gaussian (no Eq. 12 selection), from the coarse pose
+        V.copy_(Vc)
+        tr.m6.copy_(m6)
+        tr.v6.copy_(v6)
+        tr.step = stp
+        tr.mask[:n].fill_(1)
+        for _ in range(tcfg.iters_fine):
+            tr.fine_iter(P, n, V, tcf, tdf, tcfg)
+        e_all = pose_error(V.cpu().numpy(), view)
         # the same two stages as captured CUDA graphs (Tracker.stage_graphs): one replay per stage
         V.copy_(torch.as_tensor(Vp, dtype=torch.float32))
         g_c, g_f = tr.stage_graphs(P, n, V, tch, tdh, tcf, tdf, tcfg)
@@ -635,8 +648,10 @@ def main_tracking(args):
         tg_c, tg_f = tg_c / reps, tg_f / reps
         e2 = pose_error(V.cpu().numpy(), view)
         results[name] = {"coarse_iters_per_s": 1000.0 / t_c, "fine_iters_per_s": 1000.0 / t_f,
-                         "selected": int(tr.mask[:n].sum().item()), "err_init_cm": e0[0] * 100,
-                         "err_init_deg": e0[1], "err_final_cm": e1[0] * 100, "err_final_deg": e1[1],
+                         "selected": n_sel, "err_init_cm": e0[0] * 100,
+                         "err_init_deg": e0[1], "err_coarse_cm": e_c[0] * 100, "err_coarse_deg": e_c[1],
+                         "err_final_cm": e1[0] * 100, "err_final_deg": e1[1],
+                         "err_final_unselected_cm": e_all[0] * 100, "err_final_unselected_deg": e_all[1],
                          "track_ms_per_frame_eager": t_c * tcfg.iters_coarse + t_f * tcfg.iters_fine,
                          "coarse_iters_per_s_graph": 1000.0 * tcfg.iters_coarse / tg_c,
                          "fine_iters_per_s_graph": 1000.0 * tcfg.iters_fine / tg_f,

@@ -159,11 +159,30 @@ gs_status gs_render_bwd_l1(const float* params, int64_t n, int64_t ld, const flo
                            float* grad_params, double* grad_pose /*nullable*/, double* loss /*nullable*/,
                            uint32_t flags, void* stream);
 
-/* gs_pose_grad — pose-only backward (Eq. 11; tracking, Alg. 1): same inputs as
- * gs_render_bwd, ACCUMULATES dL/d(rho, phi) into grad_pose[6]; no per-Gaussian outputs. */
+/* gs_pose_grad — pose-only backward (Eq. 11; supplement P:626-729; tracking, Alg. 1
+ * PAPER.md:774-800): same inputs as gs_render_bwd, ACCUMULATES dL/d(rho, phi)
+ * into grad_pose[6] (GS_FLAG_GRAD_ASSIGN: overwrites); no per-Gaussian outputs.
+ *   Paper mode (no GS_FLAG_POSE_COV_PATH; P:168 drops Sigma' through the pose): ONE tile pass. Per
+ *   (tile, Gaussian) only the mean and depth sums (3 pixel moments + the depth sum) are formed and
+ *   turned into dL/dX^c = J^T dL/dm + e_z dL/dd with J and X^c rebuilt from the projected record;
+ *   rho += dL/dX^c, phi += X^c x dL/dX^c in fp64; per-tile partials are reduced in a fixed order by the
+ *   last tile block. No screen-space atomics, no per-Gaussian pass.
+ *   Covariance path (exact gradient, reading C7): a tile pass keeping the 6 quantities the chain
+ *   reads (mean, conic, depth; all 10 for degree-1 SH, whose colour reaches the pose through the
+ *   camera centre), then the per-Gaussian chain writing only the pose partials.
+ * Errors as gs_render_bwd. */
 gs_status gs_pose_grad(const float* params, int64_t n, int64_t ld, const float* viewmat, gs_ws* ws,
                        const gs_camera* cam /*(host)*/, const float* dL_dcolor, const float* dL_ddepth,
                        double* grad_pose /*[6] (rho_xyz, phi_xyz), +=*/, uint32_t flags, void* stream);
+
+/* gs_pose_grad_l1 — gs_loss_l1 fused into gs_pose_grad (as gs_render_bwd_l1 fuses it into the full
+ * backward): dL/dC, dL/dD of Eq. 6 (reading C20) are formed in the pose pass' pixel loads and never
+ * written; loss (nullable, device fp64 [1]) receives L. color, depth: the last gs_render_fwd's
+ * outputs. Other arguments, flags and errors as gs_pose_grad. */
+gs_status gs_pose_grad_l1(const float* params, int64_t n, int64_t ld, const float* viewmat, gs_ws* ws,
+                          const gs_camera* cam /*(host)*/, const float* color, const float* depth,
+                          const float* tgt_color, const float* tgt_depth, float w_color, float w_depth,
+                          double* grad_pose /*[6], +=*/, double* loss /*nullable*/, uint32_t flags, void* stream);
 
 /* gs_loss_l1 — Eq. 6 as means (reading C20):
  *   L = w_c/(3HW) sum|C - C*| + w_d/#valid sum_{D*>0}|D - D*|

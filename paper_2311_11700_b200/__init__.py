@@ -11,10 +11,12 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgs.so")
+# GS_DEBUG=1 loads the debug build (output invariant checks after every stage, csrc/debug.cu)
+DEBUG = os.environ.get("GS_DEBUG", "0") == "1"
+LIB_PATH = os.path.join(_HERE, "libgs_debug.so" if DEBUG else "libgs.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"libgs.so not built at {LIB_PATH}: run `python -m paper_2311_11700_b200.build` "
+    raise ImportError(f"{os.path.basename(LIB_PATH)} not built at {LIB_PATH}: run `python -m paper_2311_11700_b200.build` "
                       "(or __graft_entry__.build()); there is no fallback path")
 
 _lib = ctypes.CDLL(LIB_PATH)
@@ -77,6 +79,8 @@ _SIGS = {
                                               _P]),
     "gs_render_bwd_l1": (ctypes.c_int, [_P, _I64, _I64, _P, ctypes.POINTER(gs_ws), ctypes.POINTER(gs_camera), _P, _P,
                                         _P, _P, _F, _F, _P, _P, _P, _U32, _P]),
+    "gs_pose_grad_l1": (ctypes.c_int, [_P, _I64, _I64, _P, ctypes.POINTER(gs_ws), ctypes.POINTER(gs_camera), _P, _P,
+                                       _P, _P, _F, _F, _P, _P, _U32, _P]),
     "gs_pose_extrapolate": (ctypes.c_int, [_P, _P, _P, _P]),
     "gs_adam_step_rows": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I64, _I32, _P, _I32, _F, _F, _F, _P]),
     "gs_image_half": (ctypes.c_int, [_P, _P, _I32, _I32, _P, _P, _P]),
@@ -273,6 +277,13 @@ def gs_pose_grad(params, n, ld, viewmat, ws: Workspace, cam: gs_camera, dL_dcolo
     _check(_lib.gs_pose_grad(_ptr(params), n, ld, _ptr(viewmat), ctypes.byref(ws.state), ctypes.byref(cam),
                              _ptr(dL_dcolor), _ptr(dL_ddepth), _ptr(grad_pose), flags, _stream(stream)),
            "gs_pose_grad")
+
+
+def gs_pose_grad_l1(params, n, ld, viewmat, ws: Workspace, cam: gs_camera, color, depth, tgt_color, tgt_depth,
+                    w_color, w_depth, grad_pose, loss=None, flags: int = GS_FLAG_POSE_COV_PATH, stream=None):
+    _check(_lib.gs_pose_grad_l1(_ptr(params), n, ld, _ptr(viewmat), ctypes.byref(ws.state), ctypes.byref(cam),
+                                _ptr(color), _ptr(depth), _ptr(tgt_color), _ptr(tgt_depth), w_color, w_depth,
+                                _ptr(grad_pose), _ptr(loss), flags, _stream(stream)), "gs_pose_grad_l1")
 
 
 def gs_loss_l1(color, depth, tgt_color, tgt_depth, width, height, w_color, w_depth, dL_dcolor, dL_ddepth, loss,

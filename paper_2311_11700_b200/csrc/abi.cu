@@ -15,6 +15,8 @@ void set_cuda_error(cudaError_t e, const char* what) {
     g_last_cuda_error = std::string(what) + ": " + cudaGetErrorString(e);
 }
 
+void set_error_text(const char* msg) { g_last_cuda_error = msg; }
+
 gs_status check_launch(WsState*, const char* what) {
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -79,6 +81,7 @@ static void carve(WsState* s, Carver& c) {
     s->coop = c.take((uint64_t(kCoopPasses) * kCoopGridMax * kCoopBins + kCoopPasses * kCoopBins + kCoopGridMax +
                       uint64_t(tiles) * (1 + kCoopSegs)) * 4);
     s->tile_order = c.take(uint64_t(tiles) * 4);                     // backward LPT tile order
+    s->tile_pose = c.take(uint64_t(tiles) * 6 * 8);                  // pose-only pass: per-tile twist partials
 }
 
 static bool ws_ok(const gs_ws* ws) { return ws && state(ws)->magic == kMagic; }
@@ -165,15 +168,21 @@ gs_status gs_project_ex(const float* params, int64_t n, int64_t ld, int32_t sh_d
     s->cam_gy = (cam->height + kTile - 1) / kTile;
     s->gen_project += 1;
     launch_project(s, params, n, ld, mask, viewmat, *cam, static_cast<cudaStream_t>(stream));
-    return check_launch(s, "gs_project");
+    const gs_status rc = check_launch(s, "gs_project");
+    if (GS_DEBUG && rc == GS_OK) return dbg_after_project(s, static_cast<cudaStream_t>(stream));
+    return rc;
 }
 
 gs_status gs_bin_sort(gs_ws* ws, int64_t* n_keys, uint32_t flags, void* stream) {
     if (!ws_ok(ws)) return GS_ERR_INVALID_ARG;
     WsState* s = state(ws);
     if (s->gen_project == 0) return GS_ERR_STALE;
-    if (flags & GS_FLAG_BINSORT_KEYS) return run_bin_sort_keys(s, n_keys, flags, static_cast<cudaStream_t>(stream));
-    return run_bin_sort_bucket(s, n_keys, flags, static_cast<cudaStream_t>(stream));
+    const gs_status rc = (flags & GS_FLAG_BINSORT_KEYS)
+                             ? run_bin_sort_keys(s, n_keys, flags, static_cast<cudaStream_t>(stream))
+                             : run_bin_sort_bucket(s, n_keys, flags, static_cast<cudaStream_t>(stream));
+    if (GS_DEBUG && rc == GS_OK && !(flags & GS_FLAG_BINSORT_EMIT_ONLY))
+        return dbg_after_bin_sort(s, static_cast<cudaStream_t>(stream));
+    return rc;
 }
 
 gs_status gs_render_fwd(gs_ws* ws, const gs_camera* cam, float* color, float* depth, float* alpha, float* accum_weight,
@@ -185,12 +194,18 @@ gs_status gs_render_fwd(gs_ws* ws, const gs_camera* cam, float* color, float* de
     if (s->gen_project == 0) return GS_ERR_STALE;
     launch_render_fwd(s, *cam, color, depth, alpha, accum_weight, flags, static_cast<cudaStream_t>(stream));
     s->gen_fwd = s->gen_project;
-    return check_launch(s, "gs_render_fwd");
+    const gs_status rc = check_launch(s, "gs_render_fwd");
+    if (GS_DEBUG && rc == GS_OK) return dbg_after_fwd(s, static_cast<cudaStream_t>(stream), color, depth, alpha);
+    return rc;
 }
 
+// mode: BWD_FULL (gs_render_bwd[_l1]); gs_pose_grad[_l1] picks a pose-only tile pass (render.cu BwdMode):
+// the paper's gradient (no POSE_COV_PATH) needs only that pass; with the covariance path the pass keeps
+// the 6 quantities the per-Gaussian chain reads (degree-1 SH: all 10, the colour reaches the pose).
 static gs_status backward_common(const float* params, int64_t n, int64_t ld, const float* viewmat, gs_ws* ws,
                                  const gs_camera* cam, const float* dLdC, const float* dLdD, float* grad,
-                                 double* grad_pose, uint32_t flags, void* stream, const L1Fuse* fuse = nullptr) {
+                                 double* grad_pose, uint32_t flags, void* stream, const L1Fuse* fuse = nullptr,
+                                 bool pose_only = false) {
     if (!ws_ok(ws)) return GS_ERR_INVALID_ARG;
     WsState* s = state(ws);
     if (!cam_ok(s, cam) || (!fuse && (!dLdC || !dLdD)) || !viewmat || (n > 0 && !params) || ld < n)
@@ -199,18 +214,30 @@ static gs_status backward_common(const float* params, int64_t n, int64_t ld, con
         cam->height != s->cam_h)
         return GS_ERR_STALE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    // prologue: screen accumulators [10][V_s] (rank-indexed), LPT tile order, fused-L1 valid count
+    const int mode = !pose_only ? 0 : !(flags & GS_FLAG_POSE_COV_PATH) ? 2 : (s->sh_degree == 1 ? 0 : 1);
+    const int assign = (flags & GS_FLAG_GRAD_ASSIGN) ? 1 : 0;
+    // prologue: screen accumulators [10][V_s] (rank-indexed; not needed by the paper-mode pose pass),
+    // LPT tile order, fused-L1 valid count
     if (n > 0 || fuse)
-        launch_zero_sgrad(s, st, fuse ? fuse->td : nullptr, fuse ? int64_t(cam->width) * cam->height : 0);
+        launch_zero_sgrad(s, st, fuse ? fuse->td : nullptr, fuse ? int64_t(cam->width) * cam->height : 0, mode != 2);
+    if (mode == 2) {   // the pose-only pass is the whole backward (its last block writes twist and loss)
+        launch_render_bwd_tiles(s, *cam, nullptr, dLdC, dLdD, st, fuse, true, mode, grad_pose, assign);
+        s->gen_bwd = s->gen_fwd;
+        const gs_status rc = check_launch(s, "gs_pose_grad");
+        if (GS_DEBUG && rc == GS_OK) return dbg_after_bwd(s, st, nullptr, n, ld, grad_pose);
+        return rc;
+    }
     // fused L1 with a pose gradient: gaussian_bwd's last block (which exists then) writes the loss
     const bool fin_in_gbwd = fuse && fuse->loss && grad_pose && n > 0;
-    launch_render_bwd_tiles(s, *cam, nullptr, dLdC, dLdD, st, fuse, !fin_in_gbwd);
+    launch_render_bwd_tiles(s, *cam, nullptr, dLdC, dLdD, st, fuse, !fin_in_gbwd, mode);
     LossFin lf{nullptr, nullptr, 0.f, 0.f, 0};
     if (fin_in_gbwd)
         lf = LossFin{at<Misc>(s, s->misc)->loss_acc, fuse->loss, fuse->wc, fuse->wd, int64_t(cam->width) * cam->height};
     launch_gaussian_bwd(s, params, n, ld, viewmat, *cam, grad, grad_pose, flags, st, lf);
     s->gen_bwd = s->gen_fwd;
-    return check_launch(s, "gs_render_bwd");
+    const gs_status rc = check_launch(s, "gs_render_bwd");
+    if (GS_DEBUG && rc == GS_OK) return dbg_after_bwd(s, st, grad, n, ld, grad_pose);
+    return rc;
 }
 
 gs_status gs_render_bwd(const float* params, int64_t n, int64_t ld, const float* viewmat, gs_ws* ws,
@@ -235,7 +262,18 @@ gs_status gs_pose_grad(const float* params, int64_t n, int64_t ld, const float* 
                        const gs_camera* cam, const float* dL_dcolor, const float* dL_ddepth, double* grad_pose,
                        uint32_t flags, void* stream) {
     if (!grad_pose) return GS_ERR_INVALID_ARG;
-    return backward_common(params, n, ld, viewmat, ws, cam, dL_dcolor, dL_ddepth, nullptr, grad_pose, flags, stream);
+    return backward_common(params, n, ld, viewmat, ws, cam, dL_dcolor, dL_ddepth, nullptr, grad_pose, flags, stream,
+                           nullptr, true);
+}
+
+gs_status gs_pose_grad_l1(const float* params, int64_t n, int64_t ld, const float* viewmat, gs_ws* ws,
+                          const gs_camera* cam, const float* color, const float* depth, const float* tgt_color,
+                          const float* tgt_depth, float w_color, float w_depth, double* grad_pose, double* loss,
+                          uint32_t flags, void* stream) {
+    if (!grad_pose || !color || !depth || !tgt_color || !tgt_depth) return GS_ERR_INVALID_ARG;
+    const L1Fuse fuse{color, depth, tgt_color, tgt_depth, w_color, w_depth, loss};
+    return backward_common(params, n, ld, viewmat, ws, cam, nullptr, nullptr, nullptr, grad_pose, flags, stream, &fuse,
+                           true);
 }
 
 gs_status gs_loss_l1(const float* color, const float* depth, const float* tgt_color, const float* tgt_depth, int32_t W,
@@ -470,7 +508,7 @@ const char* gs_kernel_name(int32_t id) {
                                            "sort_pass", "tile_ranges", "render_fwd", "render_bwd_tiles",
                                            "gaussian_bwd", "pose_finalize", "loss_l1", "densify", "depth_sort",
                                            "chunk_hist", "chunk_scan", "bucket_emit", "bin_coop", "sgrad_clear",
-                                           "loss_count", "loss_finalize"};
+                                           "loss_count", "loss_finalize", "render_pose_tiles"};
     return (id >= 0 && id < KID_COUNT) ? names[id] : "unknown";
 }
 

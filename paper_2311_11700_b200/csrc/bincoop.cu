@@ -453,13 +453,12 @@ gs_status run_bin_coop(WsState* s, cudaStream_t st) {
     g.groups = int(std::min<size_t>(kCGroups, kSmemMax / std::max<size_t>(cells, 1)));
     if (g.groups < 1 || size_t(T) * 4 > kSmemMax) return GS_ERR_UNSUPPORTED;   // tile grid too large
     g.smem = std::max({size_t(kCW) * kCoopBins * 4, size_t(g.groups) * cells, size_t(T) * 4});
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(bin_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemMax)) !=
-            cudaSuccess)
-            return check_launch(s, "bin_coop attribute");
-        attr = true;
-    }
+    static PerDeviceOnce attr;
+    if (!attr.run([] {
+            return cudaFuncSetAttribute(bin_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemMax)) ==
+                   cudaSuccess;
+        }))
+        return check_launch(s, "bin_coop attribute");
     const int sms = coop_sm_count();
     if (sms <= 0) return check_launch(s, "bin_coop sm count");
     g.grid = std::min(sms, kCoopGridMax);

@@ -306,7 +306,7 @@ gs_status run_bin_sort_keys(WsState* s, int64_t* n_keys, uint32_t flags, cudaStr
     s->sorted_in_1 = which;
     const uint64_t* sk = which ? at<uint64_t>(s, s->keys1) : at<uint64_t>(s, s->keys0);
     if (Kgrid > 0) {
-        const int rblocks = int(std::min<int64_t>((Kgrid + 255) / 256, 148 * 16));
+        const int rblocks = int(std::min<int64_t>((Kgrid + 255) / 256, sm_count() * 16));
         KTimer kt(s, KID_RANGES, st);
         tile_ranges_kernel<<<rblocks, 256, 0, st>>>(sk, &misc->n_keys_eff, at<uint2>(s, s->ranges));
     }

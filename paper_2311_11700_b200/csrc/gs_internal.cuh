@@ -1,5 +1,6 @@
 // Internal declarations of libgs (B200 / sm_100a). Not part of the ABI; see include/gs.h.
 #pragma once
+#include <atomic>
 
 #include <cuda_runtime.h>
 #include <utility>
@@ -31,7 +32,7 @@ struct WsState {
     Region rec, depth_key, rect, radius, tiles, offsets, sgrad, scan_state,
         keys0, keys1, vals0, vals1, ranges, t_final, n_last, examined, sort_hist, sort_look,
         misc, scratch, scratch14, dkey_sorted, dval_sorted, chunk_hist, chunk_mat, srect, tile_tot, pose_part,
-        onlist, live_cnt, svals, coop, tile_order;
+        onlist, live_cnt, svals, coop, tile_order, tile_pose;
     // run state
     int64_t n;                     // Gaussians of the last gs_project
     int32_t sh_degree;             // colour model of the last gs_project_sh (0 = RGB, 1 = degree-1 SH)
@@ -78,6 +79,8 @@ struct Misc {
     unsigned int chunk_counter;
     unsigned int pose_done;        // gaussian_bwd last-block ticket (self-resetting)
     unsigned int prep_done;        // bwd_prep_kernel last-block ticket (self-resetting)
+    unsigned int tile_pose_done;   // pose-only tile pass last-block ticket (self-resetting)
+    unsigned int debug_flag;       // debug builds: violated checks (debug.cu), cleared when reported
     unsigned int pad;
 };
 
@@ -118,7 +121,35 @@ __device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int& goal)
     }
     __syncthreads();
 }
-int coop_sm_count();   // SMs of the current device (cached)
+// debug library (-DGS_DEBUG=1): output invariant checks after each stage (debug.cu)
+void set_error_text(const char* msg);
+gs_status dbg_after_project(WsState* s, cudaStream_t st);
+gs_status dbg_after_bin_sort(WsState* s, cudaStream_t st);
+gs_status dbg_after_fwd(WsState* s, cudaStream_t st, const float* color, const float* depth, const float* alpha);
+gs_status dbg_after_bwd(WsState* s, cudaStream_t st, const float* grad, int64_t n, int64_t ld, const double* pose);
+#ifndef GS_DEBUG
+#define GS_DEBUG 0
+#endif
+
+int coop_sm_count();   // SMs of the current device (cached per device; multiProcessorCount)
+inline int sm_count() { const int v = coop_sm_count(); return v > 0 ? v : 148; }
+
+// Per-device one-time initialisation: kernel attributes (max dynamic shared memory, carveout) are
+// per device, so a process using several GPUs sets them once on each. A bitmask of done devices,
+// updated atomically (the tracking and mapping threads of slam.py launch concurrently; setting an
+// attribute twice is harmless).
+struct PerDeviceOnce {
+    std::atomic<unsigned long long> done{0ull};
+    template <class F> bool run(F&& f) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+        const unsigned long long bit = 1ull << dev;
+        if (done.load(std::memory_order_acquire) & bit) return true;
+        if (!f()) return false;
+        done.fetch_or(bit, std::memory_order_acq_rel);
+        return true;
+    }
+};
 
 // ------------------------------------------------------------------ launch helpers
 // Kernel ids for the event log; names in gs_kernel_name (abi.cu). Keep in sync.
@@ -126,7 +157,7 @@ enum KernelId {
     KID_PROJECT = 0, KID_SCAN, KID_EMIT, KID_SORT_HIST, KID_SORT_DSCAN, KID_SORT_PASS, KID_RANGES,
     KID_FWD, KID_BWD_TILE, KID_BWD_GAUSS, KID_POSE_FIN, KID_LOSS, KID_DENSIFY,
     KID_DEPTH_SORT, KID_CHUNK_HIST, KID_CHUNK_SCAN, KID_BUCKET_EMIT, KID_BIN_COOP, KID_SGRAD_CLEAR,
-    KID_LOSS_COUNT, KID_LOSS_FINALIZE, KID_COUNT
+    KID_LOSS_COUNT, KID_LOSS_FINALIZE, KID_POSE_TILE, KID_COUNT
 };
 
 // RAII bracket around one kernel launch: counts it and, when an event log is attached, records
@@ -163,7 +194,7 @@ gs_status run_compact_onscreen(WsState* s, cudaStream_t st);   // path A
 gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t st);
 void launch_render_fwd(WsState* s, const gs_camera& cam, float* color, float* depth, float* alpha,
                        float* accum_weight, uint32_t flags, cudaStream_t st);
-void launch_zero_sgrad(WsState* s, cudaStream_t st, const float* td_l1 = nullptr, int64_t npx = 0);
+void launch_zero_sgrad(WsState* s, cudaStream_t st, const float* td_l1 = nullptr, int64_t npx = 0, bool clear = true);
 struct L1Fuse {   // gs_render_bwd_l1: the L1 loss formed inside the backward's pixel loads
     const float *color, *depth, *tc, *td;
     float wc, wd;
@@ -171,7 +202,8 @@ struct L1Fuse {   // gs_render_bwd_l1: the L1 loss formed inside the backward's 
 };
 void launch_render_bwd_tiles(WsState* s, const gs_camera& cam, const float* color_unused,
                              const float* dL_dcolor, const float* dL_ddepth, cudaStream_t st,
-                             const L1Fuse* fuse = nullptr, bool finalize_loss = true);
+                             const L1Fuse* fuse = nullptr, bool finalize_loss = true, int mode = 0,
+                             double* grad_pose = nullptr, int assign = 0);
 struct LossFin {   // the fused L1 loss scalar, written by gaussian_bwd's last block (loss == nullptr: none)
     const double* acc;
     double* loss;

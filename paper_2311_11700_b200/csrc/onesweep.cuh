@@ -180,16 +180,16 @@ gs_status onesweep_sort_pairs(WsState* s, KT* k0, uint32_t* v0, KT* k1, uint32_t
     cudaMemsetAsync(misc->sort_counter, 0, sizeof(misc->sort_counter), st);
     if (!hist_ready) {
         cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 256 * npass, st);
-        const int blocks = int(std::min<int64_t>((Kgrid + 255) / 256, 148 * 8));
+        const int blocks = int(std::min<int64_t>((Kgrid + 255) / 256, sm_count() * 8));
         KTimer kt(s, KID_SORT_HIST, st);
         onesweep_hist_kernel<KT><<<blocks, 256, 0, st>>>(k0, n_keys, npass, hist);
     }
     const size_t smem = sizeof(OnesweepSmem<KT, IPT>);
-    static bool attr_set = false;   // idempotent attribute; benign race
-    if (!attr_set) {
-        cudaFuncSetAttribute(onesweep_pass_kernel<KT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        attr_set = true;
-    }
+    static PerDeviceOnce attr;   // the attribute is per device
+    attr.run([smem] {
+        return cudaFuncSetAttribute(onesweep_pass_kernel<KT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(smem)) == cudaSuccess;
+    });
     const int64_t parts = (Kgrid + kSortThreads * IPT - 1) / (kSortThreads * IPT);
     if (parts > s->max_parts) return GS_ERR_CAPACITY;
     KT* kin = k0; uint32_t* vin = v0; KT* ko = k1; uint32_t* vo = v1;

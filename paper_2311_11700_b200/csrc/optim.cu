@@ -112,7 +112,7 @@ void launch_loss_l1(WsState* s, const float* color, const float* depth, const fl
     const bool v4 = npx % 4 == 0 && aligned(color) && aligned(depth) && aligned(tc) && aligned(td) && aligned(dc) &&
                     aligned(dd);
     const int64_t nv = v4 ? npx / 4 : npx;
-    const int blocks = int(std::min<int64_t>((nv + 255) / 256, 148 * 4));
+    const int blocks = int(std::min<int64_t>((nv + 255) / 256, sm_count() * 4));
     {
         KTimer kt(s, KID_LOSS, st);
         if (v4) loss_reduce_kernel<4><<<blocks, 256, 0, st>>>(color, depth, tc, td, npx, misc->loss_acc);
@@ -124,15 +124,15 @@ void launch_loss_l1(WsState* s, const float* color, const float* depth, const fl
 }
 
 int coop_sm_count() {
-    static int cached[64] = {0};
+    static std::atomic<int> cached[64];   // zero-initialised (static storage); per device
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
-    if (!cached[dev]) {
-        int v = 0;
+    int v = cached[dev].load(std::memory_order_relaxed);
+    if (!v) {
         if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
-        cached[dev] = v;
+        cached[dev].store(v, std::memory_order_relaxed);
     }
-    return cached[dev];
+    return v;
 }
 
 // ------------------------------------------------------------------ tracking front end (NEXT-4)
@@ -355,7 +355,7 @@ void launch_loss_l1_masked(WsState* s, const float* color, const float* depth, c
         cudaLaunchCooperativeKernel(reinterpret_cast<void*>(loss_robust_kernel), dim3(grid), dim3(1024), args, 0, st);
         return;
     }
-    const int blocks = int(std::min<int64_t>((npx + 255) / 256, 148 * 4));
+    const int blocks = int(std::min<int64_t>((npx + 255) / 256, sm_count() * 4));
     {
         KTimer kt(s, KID_LOSS, st);
         loss_masked_reduce_kernel<<<blocks, 256, 0, st>>>(color, depth, tc, td, alpha, amin, npx, misc->loss_acc);
@@ -395,7 +395,7 @@ void launch_frame_stats(const float* alpha, const float* depth, const float* td,
                         float tdep, uint32_t* counts, cudaStream_t st) {
     cudaMemsetAsync(counts, 0, 3 * sizeof(uint32_t), st);
     const int64_t npx = int64_t(W) * H;
-    frame_stats_kernel<<<int(std::min<int64_t>((npx + 255) / 256, 148 * 2)), 256, 0, st>>>(alpha, depth, td, npx, ta,
+    frame_stats_kernel<<<int(std::min<int64_t>((npx + 255) / 256, sm_count() * 2)), 256, 0, st>>>(alpha, depth, td, npx, ta,
                                                                                            tdep, counts);
 }
 
@@ -455,7 +455,7 @@ __global__ void image_half_kernel(const float* __restrict__ c, const float* __re
 void launch_image_half(const float* c, const float* d, int32_t W, int32_t H, float* ch, float* dh, cudaStream_t st) {
     const int64_t nh = int64_t(W / 2) * (H / 2);
     if (nh == 0) return;
-    const int blocks = int(std::min<int64_t>((nh + 255) / 256, 148 * 8));
+    const int blocks = int(std::min<int64_t>((nh + 255) / 256, sm_count() * 8));
     image_half_kernel<<<blocks, 256, 0, st>>>(c, d, W, H, ch, dh);
 }
 
@@ -494,7 +494,7 @@ void launch_adam(float* raw, float* act, const float* g, float* m, float* v, int
     Lr14 l{};
     for (int k = 0; k < rows; ++k) l.v[k] = lr[k];
     const float bc1 = float(1.0 - std::pow(double(b1), step)), bc2 = float(1.0 - std::pow(double(b2), step));
-    dim3 grid(unsigned(std::min<int64_t>((n + 255) / 256, 148 * 2)), unsigned(rows));
+    dim3 grid(unsigned(std::min<int64_t>((n + 255) / 256, sm_count() * 2)), unsigned(rows));
     adam_kernel<<<grid, 256, 0, st>>>(raw, act, g, m, v, n, ld, l, b1, b2, eps, bc1, bc2);
 }
 
@@ -773,7 +773,7 @@ __global__ void accum_grad_kernel(const uint32_t* __restrict__ onlist, const uns
 
 void launch_accum_grad(WsState* s, float* grad_accum, float* count, cudaStream_t st) {
     KTimer kt(s, KID_DENSIFY, st);
-    accum_grad_kernel<<<148 * 4, 256, 0, st>>>(at<uint32_t>(s, s->onlist), &at<Misc>(s, s->misc)->n_onscreen,
+    accum_grad_kernel<<<sm_count() * 4, 256, 0, st>>>(at<uint32_t>(s, s->onlist), &at<Misc>(s, s->misc)->n_onscreen,
                                                at<float>(s, s->sgrad), s->n_cap, 0.5f * float(s->cam_w),
                                                0.5f * float(s->cam_h), grad_accum, count);
 }
@@ -904,11 +904,11 @@ gs_status run_split_clone(WsState* s, float* params, float* raw, float* m, float
         if (!a) continue;
         scatter_kernel<<<nb2, kCmpThreads, 0, st>>>(capacity, ncols, keep,
                                                     GatherEmit{a, scratch, ld, s->n_cap, rows}, bcounts);
-        dim3 g(unsigned(std::min<int64_t>((capacity + 255) / 256, 148 * 4)), unsigned(rows));
+        dim3 g(unsigned(std::min<int64_t>((capacity + 255) / 256, sm_count() * 4)), unsigned(rows));
         copy_rows_kernel<<<g, 256, 0, st>>>(scratch, s->n_cap, a, ld, &misc->keep_count);
     }
     set_n_kernel<<<1, 1, 0, st>>>(n_dev, &misc->keep_count);
-    zero2_kernel<<<148 * 4, 256, 0, st>>>(accum, count, capacity);
+    zero2_kernel<<<sm_count() * 4, 256, 0, st>>>(accum, count, capacity);
     return check_launch(s, "densify_split_clone");
 }
 
@@ -986,14 +986,14 @@ gs_status run_densify(WsState* s, float* params, float* raw, int64_t* n_dev, int
     uint32_t* bcounts = at<uint32_t>(s, s->chunk_hist);
     const int rows = cfg.rows == 23 ? 23 : 14;   // 0 -> 14 (RGB)
     if (cfg.mode == GS_DENSIFY_SELECT) {
-        const int blocks = int(std::min<int64_t>((capacity + 255) / 256, 148 * 8));
+        const int blocks = int(std::min<int64_t>((capacity + 255) / 256, sm_count() * 8));
         GS_K((select_kernel<<<blocks, 256, 0, st>>>(capacity, n_dev, at<float4>(s, s->rec), at<uint32_t>(s, s->tiles),
                                                     accum, tdepth, cam.width, cam.height, cfg.sel_weight,
                                                     cfg.sel_depth, select_mask)));
         return check_launch(s, "densify_select");
     }
     if (cfg.mode == GS_DENSIFY_DEGENERATE || cfg.mode == GS_DENSIFY_DEGENERATE_FLAG) {
-        const int blocks = int(std::min<int64_t>((capacity + 255) / 256, 148 * 8));
+        const int blocks = int(std::min<int64_t>((capacity + 255) / 256, sm_count() * 8));
         GS_K((degenerate_kernel<<<blocks, 256, 0, st>>>(capacity, n_dev, at<float4>(s, s->rec), at<uint32_t>(s, s->tiles),
                                                         tdepth, cam.width, cam.height, cfg.gamma, cfg.eta,
                                                         params ? params + 10 * ld : nullptr,
@@ -1002,7 +1002,7 @@ gs_status run_densify(WsState* s, float* params, float* raw, int64_t* n_dev, int
         return check_launch(s, "densify_degenerate");
     }
     if (cfg.mode == GS_DENSIFY_DEGENERATE_APPLY) {
-        const int blocks = int(std::min<int64_t>((capacity + 255) / 256, 148 * 8));
+        const int blocks = int(std::min<int64_t>((capacity + 255) / 256, sm_count() * 8));
         GS_K((degenerate_apply_kernel<<<blocks, 256, 0, st>>>(capacity, n_dev, select_mask, cfg.eta, params + 10 * ld,
                                                               raw ? raw + 10 * ld : nullptr)));
         return check_launch(s, "densify_degenerate_apply");
@@ -1031,7 +1031,7 @@ gs_status run_densify(WsState* s, float* params, float* raw, int64_t* n_dev, int
             if (!a) continue;
             GS_K((scatter_kernel<<<nb, kCmpThreads, 0, st>>>(capacity, n_dev, pred,
                                                              GatherEmit{a, scratch, ld, s->n_cap, rows}, bcounts)));
-            dim3 g(unsigned(std::min<int64_t>((capacity + 255) / 256, 148 * 4)), unsigned(rows));
+            dim3 g(unsigned(std::min<int64_t>((capacity + 255) / 256, sm_count() * 4)), unsigned(rows));
             GS_K((copy_rows_kernel<<<g, 256, 0, st>>>(scratch, s->n_cap, a, ld, &misc->keep_count)));
         }
         GS_K((set_n_kernel<<<1, 1, 0, st>>>(n_dev, &misc->keep_count)));

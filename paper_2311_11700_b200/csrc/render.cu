@@ -592,13 +592,31 @@ struct FusedL1 {
 
 __device__ __forceinline__ float sgn1(float x) { return float((x > 0.f) - (x < 0.f)); }
 
-template <bool L1>
+// Tile-pass modes: the full backward (10 screen quantities per Gaussian), and the two pose-only
+// passes of gs_pose_grad (§8(a) a10): POSE_COV accumulates only the 6 quantities the pose chain reads
+// (mean, conic, depth) for the per-Gaussian pass; POSE_PAPER (the paper's gradient) needs only
+// the mean and depth paths, so each (tile, Gaussian) turns its sums directly into its share of the
+// twist (rho += dL/dX^c, phi += X^c x dL/dX^c, with J and X^c rebuilt from the record) in fp64, and
+// the last tile block reduces the per-tile partials in a fixed order: no screen atomics and no
+// per-Gaussian pass.
+enum BwdMode { BWD_FULL = 0, BWD_POSE_COV = 1, BWD_POSE_PAPER = 2 };
+
+struct PoseTile {              // BWD_POSE_PAPER only
+    float fx, fy, cx, cy;
+    double* part;              // [6][gridDim.x] per-tile twist partials
+    unsigned int* ticket;      // last-block ticket (self-resetting)
+    double* grad_pose;         // [6], += (or = with assign)
+    int assign;
+    LossFin lf;                // fused L1: the loss scalar, written by the last block
+};
+
+template <bool L1, int MODE>
 __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
     const float4* __restrict__ rec, const uint32_t* __restrict__ live_g, const uint32_t* __restrict__ live_j,
     const uint32_t* __restrict__ live_cnt, const uint2* __restrict__ ranges, int W, int H,
     int GX, const float* __restrict__ t_final, float bgr, float bgg, float bgb, const uint32_t* __restrict__ n_last,
     const float* __restrict__ dLdC, const float* __restrict__ dLdD, float* __restrict__ sgrad, int64_t sld,
-    FusedL1 l1, const uint32_t* __restrict__ order) {
+    FusedL1 l1, const uint32_t* __restrict__ order, PoseTile pt) {
     griddep_wait();   // PDL (gs_internal.cuh)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BwdSmem& sm = *reinterpret_cast<BwdSmem*>(smem_raw);
@@ -733,6 +751,7 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
     // bb's gradients run right after the NEXT batch's barrier [A] (or after the loop): part and the
     // slot are rewritten only after that batch's barrier [B] and two stagings later, so no barrier of
     // their own is needed (two barriers per batch).
+    double tw[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};   // BWD_POSE_PAPER: this thread's twist sums
     auto gradients = [&](int gbuf, int gbb) {
         const int cnt = min(kBB, int(len) - gbb * kBB);
         auto moment = [&](int c, int k) {
@@ -741,8 +760,34 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
             for (int p = 0; p < kBwdWarps; ++p) a += sm.part[p][c][k];
             return a;
         };
-        for (int t = tid; t < 10 * kBB; t += kBwdThreads) {
-            const int c = t / kBB, k = t % kBB;
+        if (MODE == BWD_POSE_PAPER) {
+            const int k = tid;
+            if (k >= cnt) return;
+            const float M0 = moment(0, k), Mx = moment(1, k), My = moment(2, k);
+            const float4 r0 = sm.rec[gbuf][k][0], r1 = sm.rec[gbuf][k][1];
+            const float o = r1.y;
+            const float X = r0.x - (float(tx * kTile) + 7.5f), Y = r0.y - (float(ty * kTile) + 7.5f);
+            const float gdx = X * M0 - Mx, gdy = Y * M0 - My;
+            const float dmx = o * (2.f * r0.z * gdx + r0.w * gdy);   // as the full pass' mean gradients
+            const float dmy = o * (r0.w * gdx + 2.f * r1.x * gdy);
+            const float dd = moment(9, k);
+            // X^c and J from the record: z = d, x = (m_x - c_x) z / f_x (C3 typo fixed)
+            const double z = double(r1.z), ux = double(r0.x - pt.cx), uy = double(r0.y - pt.cy);
+            const double x = ux * z / double(pt.fx), y = uy * z / double(pt.fy);
+            const double g0 = double(pt.fx) / z * double(dmx), g1 = double(pt.fy) / z * double(dmy);
+            const double g2 = -(ux / z) * double(dmx) - (uy / z) * double(dmy) + double(dd);
+            tw[0] += g0;
+            tw[1] += g1;
+            tw[2] += g2;
+            tw[3] += y * g2 - z * g1;
+            tw[4] += z * g0 - x * g2;
+            tw[5] += x * g1 - y * g0;
+            return;
+        }
+        constexpr int kComps = MODE == BWD_FULL ? 10 : 6;
+        for (int t = tid; t < kComps * kBB; t += kBwdThreads) {
+            const int ci = t / kBB, k = t % kBB;
+            const int c = (MODE == BWD_FULL || ci < 5) ? ci : 9;   // POSE_COV: mean, conic, depth
             if (k >= cnt) continue;
             float v;
             if (c >= 5) {
@@ -816,10 +861,12 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
                 const f32x2 w = pk2(v.x, v.y), g = pk2(v.z, v.w);
                 R0 = add2(R0, g);
                 Rx = fma2(g, bc2(float(x) - 7.5f), Rx);                               // exact constants
-                Rxx = fma2(g, bc2((float(x) - 7.5f) * (float(x) - 7.5f)), Rxx);
-                Sr = fma2(w, sm.dl[q][0], Sr);
-                Sg = fma2(w, sm.dl[q][1], Sg);
-                Sb = fma2(w, sm.dl[q][2], Sb);
+                if (MODE != BWD_POSE_PAPER) Rxx = fma2(g, bc2((float(x) - 7.5f) * (float(x) - 7.5f)), Rxx);
+                if (MODE == BWD_FULL) {
+                    Sr = fma2(w, sm.dl[q][0], Sr);
+                    Sg = fma2(w, sm.dl[q][1], Sg);
+                    Sb = fma2(w, sm.dl[q][2], Sb);
+                }
                 Sd = fma2(w, sm.dl[q][3], Sd);
             }
             const float fyA_ = float(gi) - 7.5f, fyB_ = float(gi + kGroups) - 7.5f;   // about the centre
@@ -836,16 +883,56 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
             m[9] = -(lo2(Sd) + hi2(Sd));
             // lanes l and l + 16 hold the same Gaussian for the warp's two row groups
 #pragma unroll
-            for (int c = 0; c < 10; ++c) m[c] += __shfl_xor_sync(0xffffffffu, m[c], 16);
-            if (lane < kBB) {
-#pragma unroll
-                for (int c = 0; c < 10; ++c) sm.part[warp][c][k2] = m[c];
+            for (int c = 0; c < 10; ++c) {
+                if (MODE == BWD_POSE_PAPER && c >= 3 && c < 9) continue;
+                if (MODE == BWD_POSE_COV && c >= 6 && c < 9) continue;
+                m[c] += __shfl_xor_sync(0xffffffffu, m[c], 16);
+                if (lane < kBB) sm.part[warp][c][k2] = m[c];
             }
         }
     }
     if (nbatch > 0) {
         __syncthreads();   // the last batch's partial sets are complete
         gradients((nbatch - 1) % kSlots, 0);
+    }
+    if (MODE == BWD_POSE_PAPER) {
+        // this tile's twist partial: the kBB gradient threads (warp 0) reduce in a fixed order
+        __shared__ bool s_last;
+        if (warp == 0) {
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+                double v = tw[c];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) pt.part[size_t(c) * gridDim.x + blockIdx.x] = v;
+            }
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) s_last = atomicAdd(pt.ticket, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+        // last block: fixed-order sums over the tiles, warp w sums component w (and w + 4)
+        __shared__ double acc6[6];
+        for (int c = warp; c < 6; c += kBwdWarps) {
+            double v = 0.0;
+            for (unsigned b = lane; b < gridDim.x; b += 32) v += __ldcg(pt.part + size_t(c) * gridDim.x + b);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) acc6[c] = v;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int c = 0; c < 6; ++c) pt.grad_pose[c] = (pt.assign ? 0.0 : pt.grad_pose[c]) + acc6[c];
+            if (pt.lf.loss) {   // fused L1: every block's loss sums are in (atomics before the ticket)
+                const double nvalid = __ldcg(pt.lf.acc + 2);
+                const float sc = float(double(pt.lf.wc) / (3.0 * double(pt.lf.npx)));
+                const float sd = nvalid > 0 ? float(double(pt.lf.wd) / nvalid) : 0.f;
+                *pt.lf.loss = double(sc) * __ldcg(pt.lf.acc) + (nvalid > 0 ? double(sd) * __ldcg(pt.lf.acc + 1) : 0.0);
+            }
+            *pt.ticket = 0u;
+        }
     }
 }
 
@@ -854,7 +941,7 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
 // (reading C20's depth mean): per-block counts, and the last block to finish (atomic ticket,
 // self-resetting) sums them in a fixed order into acc[2] and zeroes the loss sums acc[0..1] that
 // the tile pass accumulates. No memset and no second kernel.
-constexpr int kPrepBlocks = 148 * 4;
+inline int prep_blocks() { return std::min(sm_count() * 4, 1024); }   // <= chunk_hist rows
 __global__ void __launch_bounds__(256) zero_sgrad_kernel(float* __restrict__ sgrad, int64_t sld,
                                                          const unsigned int* __restrict__ n_on,
                                                          const uint32_t* __restrict__ live_cnt, int T,
@@ -864,7 +951,7 @@ __global__ void __launch_bounds__(256) zero_sgrad_kernel(float* __restrict__ sgr
     griddep_wait();   // PDL (gs_internal.cuh)
     // block 0 also builds the backward's LPT tile order from the forward's live-list lengths
     if (blockIdx.x == 0) lpt_tile_order<256>([&](int t) { return live_cnt[t]; }, T, order);
-    const int64_t V = int64_t(*n_on);
+    const int64_t V = n_on ? int64_t(*n_on) : 0;   // nullptr: no clear (the pose-only paper-mode pass)
     for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < V; t += int64_t(gridDim.x) * blockDim.x)
 #pragma unroll
         for (int c = 0; c < 10; ++c) sgrad[c * sld + t] = 0.f;
@@ -913,10 +1000,11 @@ __global__ void __launch_bounds__(256) zero_sgrad_kernel(float* __restrict__ sgr
     }
 }
 
-void launch_zero_sgrad(WsState* s, cudaStream_t st, const float* td_l1, int64_t npx) {
+void launch_zero_sgrad(WsState* s, cudaStream_t st, const float* td_l1, int64_t npx, bool clear) {
     KTimer kt(s, KID_SGRAD_CLEAR, st);
     Misc* misc = at<Misc>(s, s->misc);
-    launch_pdl(zero_sgrad_kernel, dim3(kPrepBlocks), dim3(256), 0, st, at<float>(s, s->sgrad), s->n_cap, &misc->n_onscreen,
+    launch_pdl(zero_sgrad_kernel, dim3(prep_blocks()), dim3(256), 0, st, at<float>(s, s->sgrad), s->n_cap,
+                                                   clear ? &misc->n_onscreen : nullptr,
                                                    at<uint32_t>(s, s->live_cnt), s->cam_gx * s->cam_gy,
                                                    at<uint32_t>(s, s->tile_order), td_l1, npx,
                                                    at<uint32_t>(s, s->chunk_hist), misc->loss_acc, &misc->prep_done);
@@ -930,30 +1018,46 @@ __global__ void loss_finalize_kernel(const double* acc, int64_t npx, float wc, f
 }
 
 void launch_render_bwd_tiles(WsState* s, const gs_camera& cam, const float*, const float* dL_dcolor,
-                             const float* dL_ddepth, cudaStream_t st, const L1Fuse* fuse, bool finalize_loss) {
+                             const float* dL_ddepth, cudaStream_t st, const L1Fuse* fuse, bool finalize_loss,
+                             int mode, double* grad_pose, int assign) {
     const int ntiles = s->cam_gx * s->cam_gy;
     if (ntiles == 0) return;
     const LiveBufs lb = live_bufs(s);
-    static bool attr = false;
-    if (!attr) {
-        for (auto k : {render_bwd_kernel<false>, render_bwd_kernel<true>}) {
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem)));
+    static PerDeviceOnce attr;
+    attr.run([] {
+        for (auto k : {render_bwd_kernel<false, BWD_FULL>, render_bwd_kernel<true, BWD_FULL>,
+                       render_bwd_kernel<false, BWD_POSE_COV>, render_bwd_kernel<true, BWD_POSE_COV>,
+                       render_bwd_kernel<false, BWD_POSE_PAPER>, render_bwd_kernel<true, BWD_POSE_PAPER>}) {
+            if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem))) != cudaSuccess)
+                return false;
             cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, int(cudaSharedmemCarveoutMaxShared));
         }
-        attr = true;
-    }
+        return true;
+    });
     FusedL1 l1{};
     double* acc = at<Misc>(s, s->misc)->loss_acc;
     const int64_t npx = int64_t(cam.width) * cam.height;
     if (fuse) l1 = FusedL1{fuse->color, fuse->depth, fuse->tc, fuse->td, fuse->wc, fuse->wd, acc};   // acc: zero_sgrad_kernel
+    PoseTile pt{cam.fx, cam.fy, cam.cx, cam.cy, at<double>(s, s->tile_pose), &at<Misc>(s, s->misc)->tile_pose_done,
+                grad_pose, assign, LossFin{nullptr, nullptr, 0.f, 0.f, 0}};
+    const bool paper = mode == BWD_POSE_PAPER;
+    if (paper && fuse && fuse->loss && finalize_loss) {   // the pose pass' last block writes the loss
+        pt.lf = LossFin{acc, fuse->loss, fuse->wc, fuse->wd, npx};
+        finalize_loss = false;
+    }
     {
-        KTimer kt(s, KID_BWD_TILE, st);
-        auto k = fuse ? render_bwd_kernel<true> : render_bwd_kernel<false>;
+        KTimer kt(s, paper ? KID_POSE_TILE : KID_BWD_TILE, st);
+        auto k = fuse ? (mode == BWD_FULL ? render_bwd_kernel<true, BWD_FULL>
+                         : mode == BWD_POSE_COV ? render_bwd_kernel<true, BWD_POSE_COV>
+                                                : render_bwd_kernel<true, BWD_POSE_PAPER>)
+                      : (mode == BWD_FULL ? render_bwd_kernel<false, BWD_FULL>
+                         : mode == BWD_POSE_COV ? render_bwd_kernel<false, BWD_POSE_COV>
+                                                : render_bwd_kernel<false, BWD_POSE_PAPER>);
         launch_pdl(k, dim3(ntiles), dim3(kBwdThreads), sizeof(BwdSmem), st,
             at<float4>(s, s->rec), lb.g, lb.j, lb.cnt, at<uint2>(s, s->ranges), cam.width, cam.height, s->cam_gx,
             at<float>(s, s->t_final), cam.bg[0], cam.bg[1], cam.bg[2], at<uint32_t>(s, s->n_last), dL_dcolor,
             dL_ddepth, at<float>(s, s->sgrad), s->n_cap, l1,
-            s->n > 0 ? at<uint32_t>(s, s->tile_order) : nullptr);
+            s->n > 0 ? at<uint32_t>(s, s->tile_order) : nullptr, pt);
     }
     if (fuse && fuse->loss && finalize_loss) {
         KTimer kt(s, KID_LOSS_FINALIZE, st);
@@ -1246,13 +1350,7 @@ void launch_gaussian_bwd(WsState* s, const float* params, int64_t n, int64_t ld,
                          LossFin lf) {
     if (n == 0) return;
     double* part = grad_pose ? at<double>(s, s->pose_part) : nullptr;
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        sms = std::max(sms, 1);
-    }
+    const int sms = sm_count();
     // grid sized without a host sync: at most 4 blocks per SM, at most ceil(n / 256)
     const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(sms) * kGbwdBlocksPerSM));
     KTimer kt(s, KID_BWD_GAUSS, st);

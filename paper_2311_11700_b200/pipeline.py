@@ -8,7 +8,7 @@ import dataclasses
 import torch
 
 from . import (GS_FLAG_EXAMINED, GS_FLAG_GRAD_ASSIGN, GS_FLAG_POSE_COV_PATH, Workspace, gs_bin_sort, gs_loss_l1, gs_pose_grad,
-               gs_project_ex, gs_render_bwd, gs_render_bwd_l1, gs_render_fwd, make_camera)
+               gs_pose_grad_l1, gs_project_ex, gs_render_bwd, gs_render_bwd_l1, gs_render_fwd, make_camera)
 
 
 @dataclasses.dataclass
@@ -74,6 +74,14 @@ class RenderPipeline:
                   stream=None):
         gs_pose_grad(params, n, params.shape[1], viewmat, self.ws, make_camera(cam), dL_dcolor, dL_ddepth, grad_pose,
                      flags, stream)
+
+    def pose_grad_l1(self, params, n, viewmat, cam, tgt_color, tgt_depth, grad_pose, w_color=0.9, w_depth=0.1,
+                     flags=GS_FLAG_POSE_COV_PATH, stream=None):
+        """gs_pose_grad_l1: the L1 loss of the last forward's images fused into the pose pass; self.loss
+        receives L."""
+        color, depth, _ = self._imgs(cam)
+        gs_pose_grad_l1(params, n, params.shape[1], viewmat, self.ws, make_camera(cam), color, depth, tgt_color,
+                        tgt_depth, w_color, w_depth, grad_pose, self.loss, flags, stream)
 
     def iteration(self, params, n, viewmat, cam, tgt_color, tgt_depth, grad_params, grad_pose=None, bin_flags=0,
                   fwd_flags=0, w_color=0.9, w_depth=0.1, stream=None, assign_grads=False, fused_loss=False,

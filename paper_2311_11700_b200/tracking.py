@@ -1,8 +1,8 @@
 """Coarse-to-fine camera tracking (Alg. 1; Eq. 10-12).
 
 Every step runs in libgs kernels; this module only sequences the calls:
-  coarse stage  T_c x [ gs_project (H/2 x W/2) -> gs_bin_sort -> gs_render_fwd -> gs_loss_l1
-                        -> gs_pose_grad -> gs_pose_step ]
+  coarse stage  T_c x [ gs_project (H/2 x W/2) -> gs_bin_sort -> gs_render_fwd
+                        -> gs_pose_grad_l1 (Eq. 6 fused into the pose-only pass) -> gs_pose_step ]
   selection     gs_render_fwd (full res, GS_FLAG_ACCUM_WEIGHT) -> gs_densify_prune(SELECT)  (Eq. 12)
   fine stage    T_f x [ same at full resolution, gs_project with the selection mask ]
 The pose lives on the device (world->camera 3x4) and is updated in place; no host sync inside
@@ -17,7 +17,8 @@ import math
 import numpy as np
 import torch
 
-from . import (GS_DENSIFY_SELECT, GS_FLAG_ACCUM_WEIGHT, GS_FLAG_NO_HOST_SYNC, GS_FLAG_POSE_COV_PATH, densify_cfg,
+from . import (GS_DENSIFY_SELECT, GS_FLAG_ACCUM_WEIGHT, GS_FLAG_GRAD_ASSIGN, GS_FLAG_NO_HOST_SYNC,
+               GS_FLAG_POSE_COV_PATH, densify_cfg,
                gs_densify_prune, gs_frame_stats, gs_loss_l1_masked, gs_pose_extrapolate, gs_pose_step, make_camera)
 from .pipeline import RenderPipeline
 
@@ -61,7 +62,9 @@ class Tracker:
     def _iter(self, pipe, cam, P, n, V, tc, td, cfg: TrackConfig, mask=None):
         pipe.forward(P, n, V, cam, mask=mask, bin_flags=GS_FLAG_NO_HOST_SYNC, fwd_flags=0)
         if cfg.observed_alpha is None and cfg.outlier_k == 0:
-            dc, dd = pipe.loss_l1(cam, tc, td, cfg.w_color, cfg.w_depth)
+            # Eq. 6 L1 fused into the pose-only pass (gs_pose_grad_l1): the gradient is assigned
+            pipe.pose_grad_l1(P, n, V, cam, tc, td, self.grad_pose, cfg.w_color, cfg.w_depth,
+                              flags=cfg.pose_flags | GS_FLAG_GRAD_ASSIGN)
         else:   # "only rendered at previously observed areas"
             color, depth, alpha = pipe._imgs(cam)
             npx = cam.width * cam.height
@@ -70,8 +73,7 @@ class Tracker:
             amin = cfg.observed_alpha if cfg.observed_alpha is not None else float("-inf")
             gs_loss_l1_masked(color, depth, tc, td, alpha, amin, cfg.outlier_k, cam.width, cam.height, cfg.w_color,
                               cfg.w_depth, dc, dd, pipe.loss, pipe.ws)
-        self.grad_pose.zero_()
-        pipe.pose_grad(P, n, V, cam, dc, dd, self.grad_pose, flags=cfg.pose_flags)
+            pipe.pose_grad(P, n, V, cam, dc, dd, self.grad_pose, flags=cfg.pose_flags | GS_FLAG_GRAD_ASSIGN)
         self.step += 1
         gs_pose_step(V, self.grad_pose, self.m6, self.v6, self.step, cfg.lr_rho, cfg.lr_phi)
 

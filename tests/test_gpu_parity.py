@@ -221,6 +221,35 @@ def test_pose_grad_parity(c):
         np.testing.assert_allclose(gp.cpu().numpy(), ref, rtol=2e-3, atol=1e-6)
 
 
+@pytest.mark.parametrize("c", [0, 1])
+@pytest.mark.parametrize("cov", [False, True])
+def test_pose_grad_l1_matches_unfused(c, cov):
+    """gs_pose_grad_l1 (the L1 loss fused into the pose-only pass) against gs_loss_l1 + gs_pose_grad on
+    the same forward: the same loss (1e-6 relative) and twist (atomics / partial-sum order only,
+    summation bound of the oracle); GS_FLAG_GRAD_ASSIGN overwrites instead of accumulating."""
+    import paper_2311_11700_b200 as g
+    cfg, p, v = scene(c)
+    n = p.shape[1]
+    pipe, P, V, fr = run_forward(p, v, cfg.cam)
+    tc, td = gi.random_images(cfg.cam.width, cfg.cam.height, 90 + c)
+    tcd, tdd = to_dev(tc), to_dev(td)
+    flags = g.GS_FLAG_POSE_COV_PATH if cov else 0
+    dc, dd = pipe.loss_l1(cfg.cam, tcd, tdd, 0.9, 0.1)
+    loss_ref = float(pipe.loss.item())
+    ref = torch.zeros(6, dtype=torch.float64, device="cuda")
+    pipe.pose_grad(P, n, V, cfg.cam, dc, dd, ref, flags=flags)
+    got = torch.full((6,), 5.0, dtype=torch.float64, device="cuda")
+    pipe.pose_grad_l1(P, n, V, cfg.cam, tcd, tdd, got, flags=flags | g.GS_FLAG_GRAD_ASSIGN)
+    torch.cuda.synchronize()
+    assert abs(float(pipe.loss.item()) - loss_ref) <= 1e-6 * abs(loss_ref)
+    nl = pipe.arrays(n)["n_last"].cpu().numpy()
+    ob = oracle.backward(p, v, cfg.cam, dc.cpu().numpy(), dd.cpu().numpy(), "f32", replay_nlast=nl, bound=True)
+    bnd = ob["pose_bound"] if cov else ob["pose_bound_paper"]
+    check_pose(got.cpu().numpy(), ref.cpu().numpy(), bnd, f"pose_grad_l1 cfg{c} cov={int(cov)}", k=bound_factor(nl))
+    check_pose(got.cpu().numpy(), ob["pose_twist"] if cov else ob["pose_twist_paper"], bnd,
+               f"pose_grad_l1 cfg{c} cov={int(cov)} vs oracle", k=bound_factor(nl))
+
+
 # ------------------------------------------------------------------ O5 loss / Adam / pose step
 @pytest.mark.parametrize("W,H", [(200, 120), (37, 21)])   # 16-B vector path and the ragged scalar path
 def test_loss_parity(W, H):
