@@ -618,6 +618,16 @@ def main_tracking(args):
         e0 = pose_error(Vp, view)
         tcfg = TrackConfig()
         V.copy_(torch.as_tensor(Vp, dtype=torch.float32))
+        # diagnostic: does the loss gradient at the start point toward the ground truth? The start is
+        # exp(d^) T_gt, so a descent step -lr g heads home iff g . d > 0 (per block: rho, phi)
+        gcos = {}
+        for nm_, pipe_, cam_, tc_, td_ in (("coarse", tr.half, cam.half(), tch, tdh), ("fine", tr.full, cam, tcf, tdf)):
+            pipe_.forward(P, n, V, cam_)
+            gq = torch.zeros(6, dtype=torch.float64, device="cuda")
+            pipe_.pose_grad_l1(P, n, V, cam_, tc_, td_, gq, tcfg.w_color, tcfg.w_depth, flags=tcfg.pose_flags)
+            gq = gq.cpu().numpy()
+            gcos[nm_] = [float(np.dot(gq[a:a + 3], d[a:a + 3]) / (np.linalg.norm(gq[a:a + 3]) * np.linalg.norm(d[a:a + 3])
+                                                                  + 1e-30)) for a in (0, 3)]
         tr.reset()
         t_c = _timed_events(lambda: tr.coarse_iter(P, n, V, tch, tdh, tcfg), tcfg.iters_coarse)
         e_c = pose_error(V.cpu().numpy(), view)
@@ -652,6 +662,7 @@ def main_tracking(args):
                          "err_init_deg": e0[1], "err_coarse_cm": e_c[0] * 100, "err_coarse_deg": e_c[1],
                          "err_final_cm": e1[0] * 100, "err_final_deg": e1[1],
                          "err_final_unselected_cm": e_all[0] * 100, "err_final_unselected_deg": e_all[1],
+                         "grad_cos_to_gt_rho_phi": gcos,
                          "track_ms_per_frame_eager": t_c * tcfg.iters_coarse + t_f * tcfg.iters_fine,
                          "coarse_iters_per_s_graph": 1000.0 * tcfg.iters_coarse / tg_c,
                          "fine_iters_per_s_graph": 1000.0 * tcfg.iters_fine / tg_f,

@@ -144,16 +144,19 @@ static bool cam_ok(const WsState* s, const gs_camera* cam) {
 
 gs_status gs_project(const float* params, int64_t n, int64_t ld, const uint8_t* mask, const float* viewmat,
                      const gs_camera* cam, gs_ws* ws, void* stream) {
+    GS_NVTX("gs_project");
     return gs_project_sh(params, n, ld, 0, mask, viewmat, cam, ws, stream);
 }
 
 gs_status gs_project_sh(const float* params, int64_t n, int64_t ld, int32_t sh_degree, const uint8_t* mask,
                         const float* viewmat, const gs_camera* cam, gs_ws* ws, void* stream) {
+    GS_NVTX("gs_project_sh");
     return gs_project_ex(params, n, ld, sh_degree, 0u, mask, viewmat, cam, ws, stream);
 }
 
 gs_status gs_project_ex(const float* params, int64_t n, int64_t ld, int32_t sh_degree, uint32_t flags,
                         const uint8_t* mask, const float* viewmat, const gs_camera* cam, gs_ws* ws, void* stream) {
+    GS_NVTX("gs_project_ex");
     if (!ws_ok(ws)) return GS_ERR_INVALID_ARG;
     WsState* s = state(ws);
     if (n < 0 || n > s->n_cap || ld < n || (n > 0 && !params) || !viewmat || !cam_ok(s, cam) ||
@@ -174,6 +177,7 @@ gs_status gs_project_ex(const float* params, int64_t n, int64_t ld, int32_t sh_d
 }
 
 gs_status gs_bin_sort(gs_ws* ws, int64_t* n_keys, uint32_t flags, void* stream) {
+    GS_NVTX("gs_bin_sort");
     if (!ws_ok(ws)) return GS_ERR_INVALID_ARG;
     WsState* s = state(ws);
     if (s->gen_project == 0) return GS_ERR_STALE;
@@ -187,6 +191,7 @@ gs_status gs_bin_sort(gs_ws* ws, int64_t* n_keys, uint32_t flags, void* stream) 
 
 gs_status gs_render_fwd(gs_ws* ws, const gs_camera* cam, float* color, float* depth, float* alpha, float* accum_weight,
                         uint32_t flags, void* stream) {
+    GS_NVTX("gs_render_fwd");
     if (!ws_ok(ws)) return GS_ERR_INVALID_ARG;
     WsState* s = state(ws);
     if (!cam_ok(s, cam) || !color || !depth || !alpha) return GS_ERR_INVALID_ARG;
@@ -243,6 +248,7 @@ static gs_status backward_common(const float* params, int64_t n, int64_t ld, con
 gs_status gs_render_bwd(const float* params, int64_t n, int64_t ld, const float* viewmat, gs_ws* ws,
                         const gs_camera* cam, const float* dL_dcolor, const float* dL_ddepth, float* grad_params,
                         double* grad_pose, uint32_t flags, void* stream) {
+    GS_NVTX("gs_render_bwd");
     if (!grad_params) return GS_ERR_INVALID_ARG;
     return backward_common(params, n, ld, viewmat, ws, cam, dL_dcolor, dL_ddepth, grad_params, grad_pose, flags,
                            stream);
@@ -252,6 +258,7 @@ gs_status gs_render_bwd_l1(const float* params, int64_t n, int64_t ld, const flo
                            const gs_camera* cam, const float* color, const float* depth, const float* tgt_color,
                            const float* tgt_depth, float w_color, float w_depth, float* grad_params,
                            double* grad_pose, double* loss, uint32_t flags, void* stream) {
+    GS_NVTX("gs_render_bwd_l1");
     if (!grad_params || !color || !depth || !tgt_color || !tgt_depth) return GS_ERR_INVALID_ARG;
     const L1Fuse fuse{color, depth, tgt_color, tgt_depth, w_color, w_depth, loss};
     return backward_common(params, n, ld, viewmat, ws, cam, nullptr, nullptr, grad_params, grad_pose, flags, stream,
@@ -261,6 +268,7 @@ gs_status gs_render_bwd_l1(const float* params, int64_t n, int64_t ld, const flo
 gs_status gs_pose_grad(const float* params, int64_t n, int64_t ld, const float* viewmat, gs_ws* ws,
                        const gs_camera* cam, const float* dL_dcolor, const float* dL_ddepth, double* grad_pose,
                        uint32_t flags, void* stream) {
+    GS_NVTX("gs_pose_grad");
     if (!grad_pose) return GS_ERR_INVALID_ARG;
     return backward_common(params, n, ld, viewmat, ws, cam, dL_dcolor, dL_ddepth, nullptr, grad_pose, flags, stream,
                            nullptr, true);
@@ -270,6 +278,7 @@ gs_status gs_pose_grad_l1(const float* params, int64_t n, int64_t ld, const floa
                           const gs_camera* cam, const float* color, const float* depth, const float* tgt_color,
                           const float* tgt_depth, float w_color, float w_depth, double* grad_pose, double* loss,
                           uint32_t flags, void* stream) {
+    GS_NVTX("gs_pose_grad_l1");
     if (!grad_pose || !color || !depth || !tgt_color || !tgt_depth) return GS_ERR_INVALID_ARG;
     const L1Fuse fuse{color, depth, tgt_color, tgt_depth, w_color, w_depth, loss};
     return backward_common(params, n, ld, viewmat, ws, cam, nullptr, nullptr, nullptr, grad_pose, flags, stream, &fuse,
@@ -279,6 +288,7 @@ gs_status gs_pose_grad_l1(const float* params, int64_t n, int64_t ld, const floa
 gs_status gs_loss_l1(const float* color, const float* depth, const float* tgt_color, const float* tgt_depth, int32_t W,
                      int32_t H, float w_color, float w_depth, float* dL_dcolor, float* dL_ddepth, double* loss,
                      gs_ws* ws, void* stream) {
+    GS_NVTX("gs_loss_l1");
     if (!ws_ok(ws) || !color || !depth || !tgt_color || !tgt_depth || !dL_dcolor || !dL_ddepth || W <= 0 || H <= 0)
         return GS_ERR_INVALID_ARG;
     WsState* s = state(ws);
@@ -290,6 +300,7 @@ gs_status gs_loss_l1(const float* color, const float* depth, const float* tgt_co
 gs_status gs_loss_l1_masked(const float* color, const float* depth, const float* tgt_color, const float* tgt_depth,
                             const float* alpha, float alpha_min, float outlier_k, int32_t W, int32_t H, float w_color,
                             float w_depth, float* dL_dcolor, float* dL_ddepth, double* loss, gs_ws* ws, void* stream) {
+    GS_NVTX("gs_loss_l1_masked");
     if (!ws_ok(ws) || !color || !depth || !tgt_color || !tgt_depth || !alpha || !dL_dcolor || !dL_ddepth || W <= 0 ||
         H <= 0 || !(outlier_k >= 0.f))
         return GS_ERR_INVALID_ARG;
@@ -301,12 +312,14 @@ gs_status gs_loss_l1_masked(const float* color, const float* depth, const float*
 
 gs_status gs_frame_stats(const float* alpha, const float* depth, const float* target_depth, int32_t W, int32_t H,
                          float tau_alpha, float tau_depth, uint32_t* counts, void* stream) {
+    GS_NVTX("gs_frame_stats");
     if (!alpha || !depth || !target_depth || !counts || W <= 0 || H <= 0) return GS_ERR_INVALID_ARG;
     launch_frame_stats(alpha, depth, target_depth, W, H, tau_alpha, tau_depth, counts, static_cast<cudaStream_t>(stream));
     return check_launch(nullptr, "gs_frame_stats");
 }
 
 gs_status gs_pose_extrapolate(const float* view_prev2, const float* view_prev, float* view_out, void* stream) {
+    GS_NVTX("gs_pose_extrapolate");
     if (!view_prev2 || !view_prev || !view_out || view_out == view_prev || view_out == view_prev2)
         return GS_ERR_INVALID_ARG;
     launch_pose_extrapolate(view_prev2, view_prev, view_out, static_cast<cudaStream_t>(stream));
@@ -315,6 +328,7 @@ gs_status gs_pose_extrapolate(const float* view_prev2, const float* view_prev, f
 
 gs_status gs_image_half(const float* color, const float* depth, int32_t W, int32_t H, float* color_half,
                         float* depth_half, void* stream) {
+    GS_NVTX("gs_image_half");
     if (!color || !depth || !color_half || !depth_half || W < 2 || H < 2) return GS_ERR_INVALID_ARG;
     launch_image_half(color, depth, W, H, color_half, depth_half, static_cast<cudaStream_t>(stream));
     return check_launch(nullptr, "gs_image_half");
@@ -322,6 +336,7 @@ gs_status gs_image_half(const float* color, const float* depth, int32_t W, int32
 
 gs_status gs_adam_step(float* params_raw, float* params_act, const float* grad_act, float* m, float* v, int64_t n,
                        int64_t ld, const float lr[14], int32_t step, float b1, float b2, float eps, void* stream) {
+    GS_NVTX("gs_adam_step");
     if ((n > 0 && (!params_raw || !params_act || !grad_act || !m || !v)) || !lr || n < 0 || ld < n || step < 1)
         return GS_ERR_INVALID_ARG;
     launch_adam(params_raw, params_act, grad_act, m, v, n, ld, lr, 14, step, b1, b2, eps,
@@ -332,6 +347,7 @@ gs_status gs_adam_step(float* params_raw, float* params_act, const float* grad_a
 gs_status gs_adam_step_rows(float* params_raw, float* params_act, const float* grad_act, float* m, float* v,
                             int64_t n, int64_t ld, int32_t rows, const float* lr, int32_t step, float b1, float b2,
                             float eps, void* stream) {
+    GS_NVTX("gs_adam_step_rows");
     if ((n > 0 && (!params_raw || !params_act || !grad_act || !m || !v)) || !lr || n < 0 || ld < n || step < 1 ||
         (rows != 14 && rows != 23))
         return GS_ERR_INVALID_ARG;
@@ -342,6 +358,7 @@ gs_status gs_adam_step_rows(float* params_raw, float* params_act, const float* g
 
 gs_status gs_pose_step(float* viewmat, const double* grad_pose, float* m6, float* v6, int32_t step, float lr_rho,
                        float lr_phi, void* stream) {
+    GS_NVTX("gs_pose_step");
     if (!viewmat || !grad_pose || !m6 || !v6 || step < 1) return GS_ERR_INVALID_ARG;
     launch_pose_step(viewmat, grad_pose, m6, v6, step, lr_rho, lr_phi, static_cast<cudaStream_t>(stream));
     return check_launch(nullptr, "gs_pose_step");
@@ -352,6 +369,7 @@ gs_status gs_densify_prune(float* params, float* params_raw, int64_t* n_dev, int
                            const float* target_rgb, const float* target_depth, const float* accum_weight,
                            const float* viewmat, const gs_camera* cam, const gs_densify_cfg* cfg,
                            uint8_t* select_mask, float* add_out, gs_ws* ws, void* stream) {
+    GS_NVTX("gs_densify_prune");
     if (!ws_ok(ws) || !cfg || !n_dev || capacity < 0 || ld < capacity) return GS_ERR_INVALID_ARG;
     WsState* s = state(ws);
     if (cfg->rows != 0 && cfg->rows != 14 && cfg->rows != 23) return GS_ERR_INVALID_ARG;
@@ -394,6 +412,7 @@ gs_status gs_densify_prune(float* params, float* params_raw, int64_t* n_dev, int
 gs_status gs_densify_append(float* params, float* params_raw, float* adam_m, float* adam_v, int64_t* n_dev,
                             int64_t capacity, int64_t ld, const float* cand, const int64_t* counts, int32_t n_sets,
                             int64_t max_add, int32_t rows, void* stream) {
+    GS_NVTX("gs_densify_append");
     if (!params || !n_dev || capacity < 0 || ld < capacity || n_sets < 0 || max_add < 0 ||
         (n_sets > 0 && (!cand || !counts)) || (rows != 14 && rows != 23))
         return GS_ERR_INVALID_ARG;
@@ -403,6 +422,7 @@ gs_status gs_densify_append(float* params, float* params_raw, float* adam_m, flo
 }
 
 gs_status gs_densify_accum_grad(gs_ws* ws, float* grad_accum, float* count, void* stream) {
+    GS_NVTX("gs_densify_accum_grad");
     if (!ws_ok(ws) || !grad_accum || !count) return GS_ERR_INVALID_ARG;
     WsState* s = state(ws);
     if (s->gen_fwd == 0 || s->gen_bwd != s->gen_fwd || s->gen_fwd != s->gen_project) return GS_ERR_STALE;
@@ -413,6 +433,7 @@ gs_status gs_densify_accum_grad(gs_ws* ws, float* grad_accum, float* count, void
 gs_status gs_densify_split_clone(float* params, float* params_raw, float* adam_m, float* adam_v, int64_t* n_dev,
                                  int64_t capacity, int64_t ld, float* grad_accum, float* count, const float* noise,
                                  float grad_thresh, float scale_thresh, int32_t rows, gs_ws* ws, void* stream) {
+    GS_NVTX("gs_densify_split_clone");
     if (!ws_ok(ws) || !params || !n_dev || !grad_accum || !count || !noise || capacity < 0 || ld < capacity ||
         !(grad_thresh >= 0.f) || !(scale_thresh >= 0.f) || (rows != 14 && rows != 23))
         return GS_ERR_INVALID_ARG;

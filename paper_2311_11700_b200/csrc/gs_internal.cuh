@@ -7,6 +7,16 @@
 #include <stdint.h>
 
 #include "../../include/gs.h"
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX 3: ranges cost a few ns unless a profiler attaches
+
+namespace gs {
+// NVTX range per ABI call (nsys / ncu --nvtx timelines name the library's stages)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace gs
+#define GS_NVTX(name) ::gs::NvtxRange gs_nvtx_range_(name)
 
 namespace gs {
 

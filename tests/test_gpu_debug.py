@@ -57,3 +57,32 @@ def test_debug_build_catches_nan_record():
     r = _run(0, "nan")
     assert r.returncode == 3, r.stdout + r.stderr
     assert "debug check failed" in r.stdout and "record finite" in (r.stdout + r.stderr)
+
+
+def test_second_device_after_first():
+    """Per-device kernel attributes and SM counts (PerDeviceOnce): the pipeline on cuda:1 after cuda:0
+    in one process gives the same lists and images (skipped on 1-GPU boxes)."""
+    import numpy as np
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    import gs_inputs as gi
+    import paper_2311_11700_b200 as g
+    cfg = gi.CONFIGS[1]
+    p, v, cam = cfg.scene(), cfg.view(), cfg.cam
+    out = []
+    for d in (0, 1):
+        dev = torch.device("cuda", d)
+        with torch.cuda.device(dev):
+            P, V = torch.as_tensor(p, device=dev), torch.as_tensor(v, device=dev)
+            pipe = g.RenderPipeline(p.shape[1], 1 << 23, cam.width, cam.height, dev)
+            fr = pipe.forward(P, p.shape[1], V, cam)
+            grad = torch.zeros_like(P)
+            tc, td = gi.random_images(cam.width, cam.height, 5)
+            pipe.iteration(P, p.shape[1], V, cam, torch.as_tensor(tc, device=dev), torch.as_tensor(td, device=dev),
+                           grad, None, fused_loss=True)
+            torch.cuda.synchronize(dev)
+            out.append((pipe.arrays()["vals"].cpu().numpy(), fr.color.cpu().numpy(), grad.cpu().numpy()))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])   # the forward is deterministic: same bits on both devices
+    assert np.isfinite(out[1][2]).all() and np.abs(out[1][2]).max() > 0
