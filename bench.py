@@ -63,6 +63,9 @@ def parse():
                                                              "replaying their CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="timed loop only (for ncu launch lists)")
+    ap.add_argument("--frame", action="store_true",
+                    help="with --config 4: time one keyframe's fwd+bwd iteration at config-4 size (2M Gaussians, "
+                         "~150M keys) instead of the sharded mapping (kernel rooflines at scale)")
     return ap.parse_args()
 
 
@@ -260,7 +263,7 @@ def main_ours(args):
     proj_flags = g.GS_FLAG_OPACITY_RADIUS if args.opacity_radius else 0
 
     # ---- setup (untimed): target = render of a second seeded scene at the same pose (config 2)
-    probe = g.RenderPipeline(n, 1 << 26, cam.width, cam.height, dev)
+    probe = g.RenderPipeline(n, 1 << 28 if n > 1_000_000 else 1 << 26, cam.width, cam.height, dev)
     tgt_seed = cfg.target_seed if cfg.target_seed is not None else cfg.scene_seed + 1
     Pt = torch.as_tensor(gi.gaussians(n, tgt_seed, cfg.lo, cfg.hi), device=dev)
     fr_t = probe.forward(Pt, n, V, cam, bin_flags=bin_flags, proj_flags=proj_flags)
@@ -815,7 +818,7 @@ def main():
         return run_reference(args)
     if args.config == 3:
         return main_tracking(args)
-    if args.config == 4:
+    if args.config == 4 and not args.frame:
         return main_mapping(args)
     return main_ours(args)
 

@@ -47,16 +47,7 @@ __device__ __forceinline__ void lpt_tile_order(Cost cost, int T, uint32_t* __res
     for (int b = threadIdx.x; b < kOrderBuckets; b += NT) hist[b] = 0;
     __syncthreads();
     auto bucket = [&](int t) { return kOrderBuckets - 1 - int(min(cost(t) >> 5, uint32_t(kOrderBuckets - 1))); };
-    // warp-aggregated shared atomics: most tiles share a few buckets, so lanes with the same bucket
-    // (match_any) add once per group (one atomic per distinct bucket per warp)
-    const unsigned lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
-    const int rounds = (T + NT - 1) / NT;   // warp-uniform trip count
-    for (int r = 0; r < rounds; ++r) {
-        const int t = r * NT + int(threadIdx.x);
-        const int b = t < T ? bucket(t) : -1;
-        const unsigned m = __match_any_sync(0xffffffffu, b);
-        if (b >= 0 && (m & lt) == 0u) atomicAdd(hist + b, uint32_t(__popc(m)));
-    }
+    for (int t = threadIdx.x; t < T; t += NT) atomicAdd(hist + bucket(t), 1u);
     __syncthreads();
     uint32_t v[PER];
 #pragma unroll
@@ -65,16 +56,7 @@ __device__ __forceinline__ void lpt_tile_order(Cost cost, int T, uint32_t* __res
 #pragma unroll
     for (int j = 0; j < PER; ++j) hist[threadIdx.x * PER + j] = v[j];
     __syncthreads();
-    for (int r = 0; r < rounds; ++r) {
-        const int t = r * NT + int(threadIdx.x);
-        const int b = t < T ? bucket(t) : -1;
-        const unsigned m = __match_any_sync(0xffffffffu, b);
-        const int leader = __ffs(m) - 1;
-        uint32_t base = 0;
-        if (b >= 0 && int(lane) == leader) base = atomicAdd(hist + b, uint32_t(__popc(m)));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        if (b >= 0) order[base + uint32_t(__popc(m & lt))] = uint32_t(t);
-    }
+    for (int t = threadIdx.x; t < T; t += NT) order[atomicAdd(hist + bucket(t), 1u)] = uint32_t(t);
 }
 
 // ------------------------------------------------------------------ forward

@@ -444,6 +444,30 @@ def test_capacity_error_and_stale():
     assert e.value.status == g.GS_ERR_STALE
 
 
+@pytest.mark.parametrize("c", [0, 1])
+def test_no_host_sync_overflow_is_safe(c):
+    """Key-capacity overflow in GS_FLAG_NO_HOST_SYNC mode (the mapper's and tracker's mode): the device
+    flag is set, every tile range is empty (no list entry past key_cap is read), the forward renders
+    the background and the backward writes zero gradients; nothing faults."""
+    import paper_2311_11700_b200 as g
+    cfg, p, v = scene(c)
+    n = p.shape[1]
+    pipe = g.RenderPipeline(n, 1024, cfg.cam.width, cfg.cam.height)   # far fewer keys than needed
+    P, V = to_dev(p), to_dev(v)
+    fr = pipe.forward(P, n, V, cfg.cam, bin_flags=g.GS_FLAG_NO_HOST_SYNC)
+    grad = torch.full_like(P, 7.0)
+    gp = torch.zeros(6, dtype=torch.float64, device="cuda")
+    dc = torch.ones(3, cfg.cam.height, cfg.cam.width, device="cuda")
+    dd = torch.ones(cfg.cam.height, cfg.cam.width, device="cuda")
+    pipe.backward(P, n, V, cfg.cam, dc, dd, grad, gp, flags=g.GS_FLAG_POSE_COV_PATH | g.GS_FLAG_GRAD_ASSIGN)
+    torch.cuda.synchronize()
+    a = pipe.arrays(n)
+    assert int(a["error_flag"].item()) != 0
+    assert int(a["ranges"].abs().sum().item()) == 0
+    assert float(fr.alpha.abs().max()) == 0.0 and float(fr.depth.abs().max()) == 0.0
+    assert float(grad.abs().max()) == 0.0 and float(gp.abs().max()) == 0.0
+
+
 def test_no_host_sync_mode_matches():
     import paper_2311_11700_b200 as g
     cfg, p, v = scene(1)

@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round-end evidence on the GPU box: bench line, ncu launch list, one --set full capture of a step.
+# Round evidence on the GPU box: bench line, ncu launch list, one --set full capture of a step.
 # usage (via gpurun): bash tools/capture_round.sh <tag>
 set -x
 TAG=$1
