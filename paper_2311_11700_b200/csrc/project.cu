@@ -12,21 +12,13 @@ __device__ __forceinline__ int clamp_tile(float v, int hi) {
     return int(v);
 }
 
-__global__ void __launch_bounds__(256) project_kernel(
-    const float* __restrict__ params, int64_t n, int64_t ld, const uint8_t* __restrict__ mask,
-    const float* __restrict__ viewmat, gs_camera cam, int GX, int GY, int sh, int orad,
-    float4* __restrict__ rec, uint32_t* __restrict__ depth_key, short4* __restrict__ rect,
-    int32_t* __restrict__ radius_out, uint32_t* __restrict__ tiles_out) {
-    griddep_wait();   // PDL: the previous kernel's writes (and its reads of what this one writes) are done
-    __shared__ float V[12];
-    if (threadIdx.x < 12) V[threadIdx.x] = viewmat[threadIdx.x];
-    __syncthreads();
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-
-    float p[14];
-#pragma unroll
-    for (int k = 0; k < 14; ++k) p[k] = __ldg(params + k * ld + i);   // rows 11-13: RGB or SH constant terms
+// One Gaussian: the DESIGN.md O1 steps on its 14 parameter values p (rows 11-13: RGB or SH constant
+// terms), writing its record, depth key, rect, radius and tile count.
+__device__ __forceinline__ void project_one(
+    const float (&p)[14], int64_t i, const float* __restrict__ params, int64_t ld, const uint8_t* __restrict__ mask,
+    const float* V, const gs_camera& cam, int GX, int GY, int sh, int orad, float4* __restrict__ rec,
+    uint32_t* __restrict__ depth_key, short4* __restrict__ rect, int32_t* __restrict__ radius_out,
+    uint32_t* __restrict__ tiles_out) {
 
     float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0;
     int radius = 0;
@@ -176,11 +168,40 @@ __global__ void __launch_bounds__(256) project_kernel(
     tiles_out[i] = tiles;
 }
 
+// kG Gaussians per thread (i, i + 256, ...): all their parameter loads are issued before any of the
+// (long, division-heavy) projection chains, so each warp keeps kG x 14 loads in flight.
+constexpr int kProjG = 2;
+__global__ void __launch_bounds__(256) project_kernel(
+    const float* __restrict__ params, int64_t n, int64_t ld, const uint8_t* __restrict__ mask,
+    const float* __restrict__ viewmat, gs_camera cam, int GX, int GY, int sh, int orad,
+    float4* __restrict__ rec, uint32_t* __restrict__ depth_key, short4* __restrict__ rect,
+    int32_t* __restrict__ radius_out, uint32_t* __restrict__ tiles_out) {
+    griddep_wait();   // PDL: the previous kernel's writes (and its reads of what this one writes) are done
+    __shared__ float V[12];
+    if (threadIdx.x < 12) V[threadIdx.x] = viewmat[threadIdx.x];
+    __syncthreads();
+    const int64_t i0 = int64_t(blockIdx.x) * blockDim.x * kProjG + threadIdx.x;
+    float p[kProjG][14];
+#pragma unroll
+    for (int g = 0; g < kProjG; ++g) {
+        const int64_t i = i0 + int64_t(g) * blockDim.x;
+#pragma unroll
+        for (int k = 0; k < 14; ++k) p[g][k] = i < n ? __ldg(params + k * ld + i) : 0.f;
+    }
+#pragma unroll
+    for (int g = 0; g < kProjG; ++g) {
+        const int64_t i = i0 + int64_t(g) * blockDim.x;
+        if (i < n)
+            project_one(p[g], i, params, ld, mask, V, cam, GX, GY, sh, orad, rec, depth_key, rect, radius_out,
+                        tiles_out);
+    }
+}
+
 void launch_project(WsState* s, const float* params, int64_t n, int64_t ld, const uint8_t* mask,
                     const float* viewmat, const gs_camera& cam, cudaStream_t st) {
     const int GX = (cam.width + kTile - 1) / kTile, GY = (cam.height + kTile - 1) / kTile;
     if (n == 0) return;
-    const int blocks = int((n + 255) / 256);
+    const int blocks = int((n + 256 * kProjG - 1) / (256 * kProjG));
     KTimer kt(s, KID_PROJECT, st);
     launch_pdl(project_kernel, dim3(blocks), dim3(256), 0, st, params, n, ld, mask, viewmat, cam, GX, GY, s->sh_degree,
                                            s->opacity_radius, at<float4>(s, s->rec),

@@ -906,8 +906,8 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
                 for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
                 if (lane == 0) pt.part[size_t(c) * gridDim.x + blockIdx.x] = v;
             }
+            if (lane == 0) __threadfence();   // the writer publishes the partials before the ticket
         }
-        __threadfence();
         __syncthreads();
         if (tid == 0) s_last = atomicAdd(pt.ticket, 1u) == gridDim.x - 1;
         __syncthreads();
@@ -1300,8 +1300,8 @@ __global__ void __launch_bounds__(256, kGbwdBlocksPerSM) gaussian_bwd_kernel(
 #pragma unroll
             for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
             pose_part[size_t(threadIdx.x) * gridDim.x + blockIdx.x] = v;
+            __threadfence();   // the writers publish their partials before the ticket (membar: writers only)
         }
-        __threadfence();
         __syncthreads();
         if (threadIdx.x == 0) s_last = atomicAdd(done_ctr, 1u) == gridDim.x - 1;
         __syncthreads();
