@@ -199,6 +199,69 @@ def test_backward_parity(c):
         check_pose(gpose2, ref, bnd, f"{tag} gs_pose_grad twist", k=kb)
 
 
+@pytest.mark.parametrize("c", [2, 4])
+def test_bench_iteration_matches_oracle(c):
+    """The iteration exactly as bench.py times it (config 2, and one keyframe at config-4 size: 2M
+    Gaussians, ~156M keys): GS_FLAG_NO_HOST_SYNC binning, the L1 loss fused into the backward,
+    gradients assigned, the whole iteration captured once as a CUDA graph and replayed. After three
+    replays: image within the tie rule, every one of the 14 x n gradients and the twist under the
+    §4.3 criterion, the loss within 1e-5 relative, all against the oracle on the oracle's own target
+    render. The L1 sign is a decision taken on the rendered image: where the oracle's |C - C*| (or
+    |D - D*|) is within twice the image tolerance of 0, the GPU's fp32 image may fall on the other
+    side, so there the oracle replays the GPU's sign (the tie rule's replay applied to the loss;
+    their number is printed)."""
+    import paper_2311_11700_b200 as g
+    cfg = gi.CONFIGS[c]
+    p, v, cam = cfg.scene(), cfg.view(), cfg.cam
+    n = p.shape[1]
+    t = oracle.forward(gi.gaussians(cfg.n, cfg.target_seed, cfg.lo, cfg.hi), v, cam, "f32")
+    tc, td = t["color"].astype(np.float32), t["depth"].astype(np.float32)
+    o_f = oracle.forward(p, v, cam, "f32")
+    key_cap, _ = key_cap_for(p, v, cam, slack=1.1)
+    pipe = g.RenderPipeline(n, key_cap, cam.width, cam.height)
+    P, V, TC, TD = to_dev(p), to_dev(v), to_dev(tc), to_dev(td)
+    grad = torch.full_like(P, 3.0)
+    gpose = torch.zeros(6, dtype=torch.float64, device="cuda")
+
+    def step():
+        pipe.iteration(P, n, V, cam, TC, TD, grad, gpose, bin_flags=g.GS_FLAG_NO_HOST_SYNC, fwd_flags=0,
+                       assign_grads=True, fused_loss=True)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        step()
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    a = pipe.arrays(n)
+    assert int(a["error_flag"].item()) == 0
+    gpu = dict(color=pipe.color, depth=pipe.depth, alpha=pipe.alpha, n_last=a["n_last"])
+    compare_images(gpu, o_f, cam, p, v, f"bench iteration cfg{c}")
+    nl = a["n_last"].cpu().numpy()
+    L = oracle.loss_l1(o_f["color"], o_f["depth"], tc, td, cfg.w_color, cfg.w_depth)
+    dc, dd = L["dL_dcolor"].copy(), L["dL_ddepth"].copy()
+    amb_c = np.abs(o_f["color"] - tc) <= 2 * ATOL_IMG
+    amb_d = (np.abs(o_f["depth"] - td) <= 2 * ATOL_IMG) & (td > 0)
+    if amb_c.any() or amb_d.any():   # replay the GPU's sign decision there (Eq. 6 scales as the oracle's)
+        gc, gd = pipe.color.cpu().numpy().astype(np.float64), pipe.depth.cpu().numpy().astype(np.float64)
+        sc = cfg.w_color / (3.0 * cam.width * cam.height)
+        sd = cfg.w_depth / L["n_valid"]
+        dc[amb_c] = (sc * np.sign(gc - tc))[amb_c]
+        dd[amb_d] = (sd * np.sign(gd - td))[amb_d]
+    print(f"cfg{c}: {int(amb_c.sum())} colour and {int(amb_d.sum())} depth L1 signs replayed")
+    ob = oracle.backward(p, v, cam, dc.astype(np.float32), dd.astype(np.float32), "f32", replay_nlast=nl,
+                         bound=True)
+    kb = bound_factor(nl)
+    check_grads(grad.cpu().numpy(), ob["grad_params"], ob["grad_bound"], f"bench iteration cfg{c} params", k=kb)
+    check_pose(gpose.cpu().numpy(), ob["pose_twist"], ob["pose_bound"], f"bench iteration cfg{c} twist", k=kb)
+    assert abs(float(pipe.loss.item()) - L["loss"]) <= 1e-5 * abs(L["loss"]), (float(pipe.loss.item()), L["loss"])
+
+
 @pytest.mark.parametrize("c", CFGS)
 def test_pose_grad_parity(c):
     """gs_pose_grad (§8(a) a10) against the oracle's twist directly (not against gs_render_bwd),
