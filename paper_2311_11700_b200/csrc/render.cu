@@ -523,13 +523,13 @@ void launch_render_fwd(WsState* s, const gs_camera& cam, float* color, float* de
 //   phase 2  lane = (Gaussian, row group): pixel moments with compile-time x
 //   combine  one thread per (component, Gaussian) sums the per-warp partial moments it needs, turns
 //            them into the screen-space gradient and issues its atomic.
-// The staged batches rotate through 3 slots, so a batch needs 2 block barriers and none at its end.
+// The staged batches rotate through 4 slots (gathered two ahead), so a batch needs 2 block barriers and none at its end.
 constexpr int kBB = 16;                          // Gaussians per backward batch
 constexpr int kBwdThreads = kTilePx / 2;         // 128
 constexpr int kBwdWarps = kBwdThreads / 32;
 constexpr int kGroups = kBwdWarps * (32 / kBB);  // phase-2 row groups (= partial sets)
 constexpr int kRowsPerGroup = kTile / kGroups;
-constexpr int kSlots = 3;
+constexpr int kSlots = 4;
 static_assert(kTile % kGroups == 0, "row groups must tile the 16 rows");
 
 static_assert(kRowsPerGroup == 2 && kGroups == 8, "phase 2 pairs rows ly and ly + 8 like phase 1");
@@ -745,7 +745,11 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
 
     // phase-2 lane roles: Gaussian k2 of the batch, row group gi (rows gi + kGroups r)
     const int k2 = lane & (kBB - 1), gi = warp * (32 / kBB) + lane / kBB;
+    // records are gathered two batches ahead (4 slots: staging it + 2, phase 1 on it, gradients of
+    // it - 1; the slot staged at iteration it was last read by batch it - 2's gradients, which every
+    // warp finished before the previous iteration's barrier [B])
     if (nbatch > 0) stage(nbatch - 1, 0);
+    if (nbatch > 1) stage(nbatch - 2, 1);
     // ---- moments -> screen-space gradients of batch bb (staged in slot gbuf); one thread and one
     // atomic per (component, Gaussian). Each thread sums the per-warp partial sets it needs. Batch
     // bb's gradients run right after the NEXT batch's barrier [A] (or after the loop): part and the
@@ -820,8 +824,10 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
     for (int it = 0; it < nbatch; ++it) {
         const int bb = nbatch - 1 - it;
         const int buf = it % kSlots;
-        if (it + 1 < nbatch) {
-            stage(bb - 1, (it + 1) % kSlots);
+        if (it + 2 < nbatch) {
+            stage(bb - 2, (it + 2) % kSlots);
+            cp_async_wait<2>();
+        } else if (it + 1 < nbatch) {
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
