@@ -46,7 +46,7 @@ __device__ __forceinline__ void lpt_tile_order(Cost cost, int T, uint32_t* __res
     constexpr int PER = kOrderBuckets / NT;
     for (int b = threadIdx.x; b < kOrderBuckets; b += NT) hist[b] = 0;
     __syncthreads();
-    auto bucket = [&](int t) { return kOrderBuckets - 1 - int(min(cost(t) >> 5, uint32_t(kOrderBuckets - 1))); };
+    auto bucket = [&](int t) { return kOrderBuckets - 1 - int(min(cost(t), uint32_t(kOrderBuckets - 1))); };
     for (int t = threadIdx.x; t < T; t += NT) atomicAdd(hist + bucket(t), 1u);
     __syncthreads();
     uint32_t v[PER];
