@@ -59,7 +59,7 @@ def kernels(rep):
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     idx = {h: i for i, h in enumerate(hdr)}
-    out, traffic = [], {}
+    out, traffic, pipes = [], {}, {}
     seen = collections.Counter()
     for r in data:
         name = short(r[idx["Kernel Name"]])
@@ -75,10 +75,15 @@ def kernels(rep):
             b = rd * scale.get(units[idx["dram__bytes_read.sum"]], 1) + wr * scale.get(units[idx["dram__bytes_write.sum"]], 1)
             key = NAMES.get(name, name)
             traffic[key] = b / 1e9   # GB per launch (same unit scale as roofline amounts)
+            pipes[key] = {"fma_pipe_active_pct": float(r[idx["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"]]),
+                          "issue_active_pct": float(r[idx["smsp__issue_active.avg.pct_of_peak_sustained_active"]]),
+                          "warps_active_pct": float(r[idx["sm__warps_active.avg.pct_of_peak_sustained_active"]]),
+                          "dram_gb_per_launch": b / 1e9,
+                          "source": os.path.basename(rep)}
         except (KeyError, ValueError):
             pass
         out.append("")
-    return "\n".join(out), traffic
+    return "\n".join(out), traffic, pipes
 
 
 if __name__ == "__main__":
@@ -87,9 +92,11 @@ if __name__ == "__main__":
     with open(prefix + "_launches.md", "w") as f:
         f.write(f"# ncu launch list ({os.path.basename(ll)}): `ncu --metrics gpu__time_duration.sum --clock-control "
                 "none` over `bench.py --quick` (cold-cache, serialised; compare shares)\n\n" + launches(ll) + "\n")
-    txt, traffic = kernels(rep)
+    txt, traffic, pipes = kernels(rep)
     with open(prefix + "_kernels.md", "w") as f:
         f.write(f"# ncu --set full ({os.path.basename(rep)}), bench.py config 2\n\n" + txt)
     with open(os.path.join(os.path.dirname(prefix), "ncu_traffic.json"), "w") as f:
         json.dump(traffic, f, indent=1)
+    with open(os.path.join(os.path.dirname(prefix), "ncu_metrics.json"), "w") as f:
+        json.dump(pipes, f, indent=1)   # bench.py roofline: the measured pipe activity next to the nominal count
     print(open(prefix + "_launches.md").read())
