@@ -1,6 +1,6 @@
 """Debug build (libgs_debug.so, GS_DEBUG=1): every stage's output invariants are
 checked after the call (compute-sanitizer is not available on this pool). -m gpu:
-- configs 0-1 run project -> bin_sort -> fwd -> L1 -> bwd and the pose-only passes clean;
+- configs 0-2 run project -> bin_sort -> fwd -> L1 -> bwd and the pose-only passes clean;
 - a NaN colour makes gs_project's record check fail with GS_ERR_CUDA naming the check."""
 import os
 import subprocess
@@ -22,7 +22,7 @@ cfg = gi.CONFIGS[c]; p = cfg.scene(); v = cfg.view(); cam = cfg.cam; n = p.shape
 if poison:
     p[11, 7] = np.nan
 P = torch.as_tensor(p, device="cuda"); V = torch.as_tensor(v, device="cuda")
-pipe = g.RenderPipeline(n, 1 << 23, cam.width, cam.height)
+pipe = g.RenderPipeline(n, 1 << 26 if c == 2 else 1 << 23, cam.width, cam.height)
 try:
     pipe.forward(P, n, V, cam)
 except g.GSError as e:
@@ -46,7 +46,7 @@ def _run(c, mode):
                           capture_output=True, text=True, timeout=600)
 
 
-@pytest.mark.parametrize("c", [0, 1])
+@pytest.mark.parametrize("c", [0, 1, 2])
 def test_debug_build_clean_on_configs(c):
     r = _run(c, "clean")
     assert r.returncode == 0, r.stdout + r.stderr
