@@ -649,6 +649,18 @@ def main_tracking(args):
         for _ in range(tcfg.iters_fine):
             tr.fine_iter(P, n, V, tcf, tdf, tcfg)
         e_all = pose_error(V.cpu().numpy(), view)
+        # the paper's tracking loss (readings C31/C32): observed area only, pixels
+        # above 10x the median loss ignored; both stages from the same start
+        rcfg = dataclasses.replace(tcfg, observed_alpha=0.5, outlier_k=10.0)
+        V.copy_(torch.as_tensor(Vp, dtype=torch.float32))
+        tr.reset()
+        for _ in range(rcfg.iters_coarse):
+            tr.coarse_iter(P, n, V, tch, tdh, rcfg)
+        e_rc = pose_error(V.cpu().numpy(), view)
+        tr.select(P, n, V, tdf, rcfg)
+        for _ in range(rcfg.iters_fine):
+            tr.fine_iter(P, n, V, tcf, tdf, rcfg)
+        e_r = pose_error(V.cpu().numpy(), view)
         # the same two stages as captured CUDA graphs (Tracker.stage_graphs): one replay per stage
         V.copy_(torch.as_tensor(Vp, dtype=torch.float32))
         g_c, g_f = tr.stage_graphs(P, n, V, tch, tdh, tcf, tdf, tcfg)
@@ -666,6 +678,8 @@ def main_tracking(args):
                          "err_final_cm": e1[0] * 100, "err_final_deg": e1[1],
                          "err_final_unselected_cm": e_all[0] * 100, "err_final_unselected_deg": e_all[1],
                          "grad_cos_to_gt_rho_phi": gcos,
+                         "robust_loss": {"err_coarse_cm": e_rc[0] * 100, "err_coarse_deg": e_rc[1],
+                                         "err_final_cm": e_r[0] * 100, "err_final_deg": e_r[1]},
                          "track_ms_per_frame_eager": t_c * tcfg.iters_coarse + t_f * tcfg.iters_fine,
                          "coarse_iters_per_s_graph": 1000.0 * tcfg.iters_coarse / tg_c,
                          "fine_iters_per_s_graph": 1000.0 * tcfg.iters_fine / tg_f,

@@ -48,9 +48,18 @@ def launches(path):
             agg[k][0] += 1
             agg[k][1] += float(d["Metric Value"])
     tot = sum(v[1] for v in agg.values())
-    lines = ["| kernel | launches | total us | share |", "|---|---|---|---|"]
+    lines = ["| kernel | launches | total us | us per launch | share |", "|---|---|---|---|---|"]
     for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
-        lines.append(f"| {k} | {v[0]} | {v[1] / 1e3:.1f} | {v[1] / tot:.3f} |")
+        lines.append(f"| {k} | {v[0]} | {v[1] / 1e3:.1f} | {v[1] / 1e3 / max(v[0], 1):.1f} | {v[1] / tot:.3f} |")
+    # the library's kernels per launch (the bench's setup runs extra forwards, so shares by total
+    # time over-weight the forward-side kernels): one iteration = one launch of each
+    own = {k: v[1] / 1e3 / max(v[0], 1) for k, v in agg.items() if k.endswith("_kernel") and not k.startswith("at")}
+    step = sum(own.values())
+    if step:
+        lines += ["", "Per iteration (one launch of each library kernel):", "",
+                  "| kernel | us | share of the iteration |", "|---|---|---|"]
+        for k, v in sorted(own.items(), key=lambda x: -x[1]):
+            lines.append(f"| {k} | {v:.1f} | {v / step:.3f} |")
     return "\n".join(lines)
 
 
