@@ -53,7 +53,7 @@ def launches(path):
         lines.append(f"| {k} | {v[0]} | {v[1] / 1e3:.1f} | {v[1] / 1e3 / max(v[0], 1):.1f} | {v[1] / tot:.3f} |")
     # the library's kernels per launch (the bench's setup runs extra forwards, so shares by total
     # time over-weight the forward-side kernels): one iteration = one launch of each
-    own = {k: v[1] / 1e3 / max(v[0], 1) for k, v in agg.items() if k.endswith("_kernel") and not k.startswith("at")}
+    own = {k: v[1] / 1e3 / max(v[0], 1) for k, v in agg.items() if k in NAMES}
     step = sum(own.values())
     if step:
         lines += ["", "Per iteration (one launch of each library kernel):", "",
