@@ -2,8 +2,8 @@
 
 One process per GPU; each rank holds a full replica of the map and renders ITS keyframes:
   per local keyframe:  gs_project -> gs_bin_sort -> gs_render_fwd -> gs_loss_l1 -> gs_render_bwd (+=)
-  exchange:            all_reduce(sum) of grad[rows][:n] over NCCL (NVLink 5 / NVSwitch), one coalesced
-                       group of row all-reduces
+  exchange:            all_reduce(sum) of grad[rows][:n] over NCCL (NVLink 5 / NVSwitch): the live columns
+                       packed into one contiguous buffer, one collective
   optimiser:           gs_adam_step (identical on every rank -> parameters stay bitwise equal)
   adaptive expansion:  gs_densify_prune(ADD, gather mode) per local keyframe (Eq. 8)
                        -> all_gather of candidate counts and padded candidates (rank order)
@@ -63,24 +63,25 @@ def _dist_on(group=None) -> bool:
     return dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
 
 
-def allreduce_grads(grad: torch.Tensor, n: int | None = None, group=None) -> None:
+def allreduce_grads(grad: torch.Tensor, n: int | None = None, group=None, packed: torch.Tensor | None = None) -> None:
     """Sum the gradient buffer [rows][ld] over ranks in place, only its first n columns (the live
-    Gaussians; each row slice is contiguous). NCCL on GPU (one coalesced group of row all-reduces),
-    gloo on CPU or CUDA tensors."""
+    Gaussians). The live block is packed into one contiguous buffer (rows x n, `packed` if given, of at
+    least that size) and reduced with ONE all_reduce (NCCL on GPU, gloo on CPU or CUDA tensors), then
+    copied back: 2 x 56 n bytes of HBM copies instead of 14 collective launches or reducing the unused
+    capacity columns."""
     if not _dist_on(group):
         return
     n = grad.shape[1] if n is None else n
     if n == grad.shape[1] or grad.dim() == 1:
         dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=group)
         return
-    rows = [grad[k, :n] for k in range(grad.shape[0])]
-    if grad.is_cuda and dist.get_backend(group) == "nccl":
-        with dist._coalescing_manager(group=group, device=grad.device):
-            for r in rows:
-                dist.all_reduce(r, op=dist.ReduceOp.SUM, group=group)
-    else:
-        for r in rows:
-            dist.all_reduce(r, op=dist.ReduceOp.SUM, group=group)
+    rows = grad.shape[0]
+    if packed is None or packed.numel() < rows * n:
+        packed = torch.empty(rows * n, dtype=grad.dtype, device=grad.device)
+    buf = packed[:rows * n].view(rows, n)
+    buf.copy_(grad[:, :n])
+    dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    grad[:, :n].copy_(buf)
 
 
 def allreduce_sum(t: torch.Tensor, group=None) -> None:
@@ -169,6 +170,7 @@ class ShardedMapper:
         self.m = torch.zeros_like(params)
         self.v = torch.zeros_like(params)
         self.grad = torch.zeros_like(params)
+        self.packed = torch.empty(params.numel(), device=params.device) if self.world > 1 else None
         self.n = n
         self.n_dev = torch.tensor([n], dtype=torch.int64, device=params.device)
         self.cam = cam
@@ -262,7 +264,7 @@ class ShardedMapper:
     def step(self):
         poses = self.poses_active()
         self.render_backward()
-        allreduce_grads(self.grad, self.n, self.group)
+        allreduce_grads(self.grad, self.n, self.group, self.packed)
         if self.degenerate is not None and self.densify:   # one Eq. 9 application per expansion step
             allreduce_mask(self.dmask, self.group)
             gs_densify_prune(self.P, self.raw, self.n_dev, self.n, self.cap, None, None, None, None, None, None,
