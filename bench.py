@@ -217,7 +217,8 @@ def run_reference(args):
     cpu = {"value": value, "unit": unit, "cores": oracle.num_threads(), "kind": "oracle", "sample": desc,
            "cpu_model": cpu_model(), "stage_s": {k: v_ / max(args.steps, 1) for k, v_ in stages.items()}}
     line = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "strong" if mapping else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Replica-shaped room scene, SURVEY.md §8(d))",
             "impl": "reference",
             "config": {"workload": f"config {cfg_index(cfg)}: {cfg.name} {cfg.cam.width}x{cfg.cam.height}, {cfg.n} "
