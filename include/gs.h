@@ -6,7 +6,8 @@
  *  - Every call is asynchronous on `stream` (a cudaStream_t passed as void*; NULL = legacy default
  *    stream) and never allocates device memory. The caller owns every buffer, including the
  *    device workspace and the host workspace state `gs_ws` (see gs_ws_init).
- *  - The library holds no global state; calls on distinct workspaces are independent.
+ *  - The library holds no global device state; calls on distinct workspaces are independent. Its only
+ *    process-wide state is a per-device host cache of kernel attributes and SM counts (thread-safe).
  *  - Argument errors are detected on the host before any launch (GS_ERR_INVALID_ARG);
  *    a failed launch returns GS_ERR_CUDA (gs_last_cuda_error() gives the CUDA error string).
  *  - Gaussian parameters are ACTIVATED values in a structure-of-arrays float32 buffer
