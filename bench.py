@@ -128,10 +128,20 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------------- dist
 def dist_env():
+    """(world, rank, local GPU index). GS_BENCH_BACKEND=gloo (testing the N-rank flow on a box with
+    fewer GPUs than ranks) maps ranks onto the visible GPUs round-robin; the default NCCL run uses
+    one GPU per rank."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if dist_backend() != "nccl":
+        import torch
+        local %= max(torch.cuda.device_count(), 1)
     return world, rank, local
+
+
+def dist_backend() -> str:
+    return os.environ.get("GS_BENCH_BACKEND", "nccl")
 
 
 def init_dist(world, backend):
@@ -247,7 +257,7 @@ def main_ours(args):
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
-    dist = init_dist(world, "nccl")
+    dist = init_dist(world, dist_backend())
     dev = torch.device("cuda", local)
     cfg = gi.CONFIGS[args.config]
     if args.pose_seed is not None:
@@ -725,7 +735,7 @@ def main_mapping(args):
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
-    dist = init_dist(world, "nccl")
+    dist = init_dist(world, dist_backend())
     dev = torch.device("cuda", local)
     cfg = gi.CONFIGS[4]
     cam = cfg.cam
@@ -791,7 +801,8 @@ def main_mapping(args):
                                   "all-reduce of grad[14][n], Adam, Eq. 8 add + prune); value = box-wide mapping "
                                   "iterations/s", "keyframes": len(kfs), "keyframes_per_rank": len(mp.local),
                       "n_gaussians_start": n, "n_gaussians_end": mp.n,
-                      "parallelism": f"keyframe shards x{world}, NCCL all_reduce" if world > 1 else "1 GPU",
+                      "parallelism": (f"keyframe shards x{world}, {dist_backend().upper()} all_reduce" if world > 1
+                                      else "1 GPU"),
                       "l2": "per-keyframe working set > L2; no flush"},
            "keyframe_renders_per_s": len(kfs) * 1000.0 / ms, "clocks": clocks, "gpu_launches": launches,
            "e2e": {"value": 1000.0 / ms_e2e, "unit": "mapping iters/s", "h2d_bytes_per_step": int(h2d),
