@@ -16,7 +16,7 @@
 
 namespace gs {
 
-constexpr int kSortThreads = 256, kSortItems = 16, kSortTile = kSortThreads * kSortItems;
+constexpr int kSortThreads = 256, kSortItems = 8, kSortTile = kSortThreads * kSortItems;
 constexpr int kSortItemsSmall = 4;   // 1024-key partitions for small sorts (more CTAs, shorter latency)
 
 template <class KT>
