@@ -59,7 +59,7 @@ static void carve(WsState* s, Carver& c) {
     s->n_last = c.take(uint64_t(px) * 4);
     s->examined = c.take(uint64_t(px) * 4);
     s->sort_hist = c.take(8 * 256 * 4);
-    // look-back rows: path A sorts key_cap keys in 4096-key partitions, path B n_cap keys in 1024-key ones
+    // look-back rows: path A sorts key_cap keys in kSortTile-key (2048) partitions, path B n_cap keys in 1024-key ones
     s->max_parts = std::max(sort_parts(s->key_cap), (std::max<int64_t>(s->n_cap, 1) + 1023) / 1024);
     s->sort_look = c.take(uint64_t(s->max_parts) * 256 * 8);
     s->misc = c.take(sizeof(Misc));

@@ -2,7 +2,7 @@
 //  1. one upfront pass builds the digit histograms of every pass (reads the keys once), or the
 //     producer of the keys accumulates them; each pass kernel scans its histogram in-CTA;
 //  2. each digit pass is ONE kernel: a CTA takes the next partition from an atomic ticket
-//     (forward progress for the look-back), ranks its 4096 keys stably with warp match_any,
+//     (forward progress for the look-back), ranks its kSortTile (2048) keys stably with warp match_any,
 //     publishes its per-digit counts, resolves its global digit offsets by decoupled look-back
 //     over its predecessors, and scatters through shared memory so stores are coalesced per digit.
 // Look-back words are [epoch:30 | flag:2 | count:32]; a fresh epoch per pass makes stale words
