@@ -186,7 +186,8 @@ def backward(params, view, cam, dL_dcolor, dL_ddepth, precision="f32", replay_nl
     pose_twist_paper: same without the Sigma'-through-pose term (P:168, paper mode);
     pose_qt: dL/d(q_r,q_i,q_j,q_k,t) via Eq. S1/S3 (independent path), plus the pose quaternion.
     bound=True adds grad_bound [rows][n], pose_bound[6], pose_bound_paper[6], screen_bound [10][n]
-    (the screen quantities' sums of term magnitudes): the error-bound scale
+    (the screen quantities' sums of term magnitudes), chain_scale [rows][n] (the per-Gaussian chain
+    evaluated on magnitudes: the rounding scale of the chain itself): the error-bound scale
     of each result, sum_j |d grad / d s_j| sum_p |c_pj| (the per-pixel terms' magnitudes carried
     through the linear per-Gaussian chain; oracle.cpp error_bound). |result| <= bound always.
     """
@@ -207,16 +208,17 @@ def backward(params, view, cam, dL_dcolor, dL_ddepth, precision="f32", replay_nl
     pb = np.zeros(6, np.float64) if bound else None
     pbp = np.zeros(6, np.float64) if bound else None
     sb = np.zeros((10, n), np.float64) if bound else None
+    cs = np.zeros((params.shape[0], n), np.float64) if bound else None
     c = _cam(cam)
     getattr(lib(), f"oracle_backward_{precision}")(
         _p(params), ctypes.c_int64(n), ctypes.c_int64(n), _p(view), ctypes.byref(c), _p(dc), _p(dd), _p(rp),
         _p(gp), _p(gs), _p(tw), _p(twp), _p(qt), ctypes.c_int32(1 if qt_cov else 0), _p(px),
         ctypes.c_int64(0 if px is None else px.shape[0]), ctypes.c_int32(_mode(params, opacity_radius)),
-        _p(gb), _p(pb), _p(pbp), _p(sb))
+        _p(gb), _p(pb), _p(pbp), _p(sb), _p(cs))
     out = dict(grad_params=gp, grad_screen=gs, pose_twist=tw, pose_twist_paper=twp,
                pose_q=qt[0:4], pose_t=qt[4:7], pose_quat=qt[7:11])
     if bound:
-        out.update(grad_bound=gb, pose_bound=pb, pose_bound_paper=pbp, screen_bound=sb)
+        out.update(grad_bound=gb, pose_bound=pb, pose_bound_paper=pbp, screen_bound=sb, chain_scale=cs)
     return out
 
 

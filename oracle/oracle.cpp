@@ -586,6 +586,120 @@ static GaussianBack gaussian_backward(const R* params, int64_t ld, int64_t i, co
     return out;
 }
 
+// Magnitude of the per-Gaussian chain (the rounding scale of any fp32 evaluation of it, DESIGN.md
+// §4.3): gaussian_backward's steps with every quantity replaced by its absolute value and every sum
+// of products by the sum of the products' magnitudes, applied to the screen magnitudes S (the
+// backward's sums of per-pixel term magnitudes). An evaluation of the chain in precision u differs
+// from the exact one by at most about (steps) u times this value; where the exact gradient cancels
+// to 0 (e.g. the rotation gradient of an isotropic Gaussian) the rounding is all that remains.
+template <class R>
+static void gaussian_chain_scale(const R* params, int64_t ld, int64_t i, const R* Vr, const Cam<R>& camr,
+                                 const ScreenGrad& s, const Proj<R>& pr, double* out) {
+    double p[MAXP], V[12];
+    const int rows = n_rows(camr.sh);
+    for (int k = 0; k < rows; ++k) p[k] = double(params[k * ld + i]);
+    for (int k = 0; k < 12; ++k) V[k] = double(Vr[k]);
+    const double fx = std::fabs(double(camr.fx)), fy = std::fabs(double(camr.fy));
+    double W[3][3], aW[3][3];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) {
+            W[a][b] = V[a * 4 + b];
+            aW[a][b] = std::fabs(W[a][b]);
+        }
+    double Xc[3];
+    for (int a = 0; a < 3; ++a) Xc[a] = W[a][0] * p[0] + W[a][1] * p[1] + W[a][2] * p[2] + V[a * 4 + 3];
+    const double x = std::fabs(Xc[0]), y = std::fabs(Xc[1]), z = std::fabs(Xc[2]);
+    const double nq = std::sqrt(p[6] * p[6] + p[7] * p[7] + p[8] * p[8] + p[9] * p[9]);
+    const double q[4] = {p[6] / nq, p[7] / nq, p[8] / nq, p[9] / nq};
+    double Rm[3][3];
+    rot_of(q, Rm);
+    double aR[3][3], aM[3][3], aS[3][3];
+    for (int a = 0; a < 3; ++a)
+        for (int k = 0; k < 3; ++k) {
+            aR[a][k] = std::fabs(Rm[a][k]);
+            aM[a][k] = aR[a][k] * std::fabs(p[3 + k]);
+        }
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) aS[a][b] = aM[a][0] * aM[b][0] + aM[a][1] * aM[b][1] + aM[a][2] * aM[b][2];
+    const double aJ[2][3] = {{fx / z, 0, fx * x / (z * z)}, {0, fy / z, fy * y / (z * z)}};
+    double aE[2][3];
+    for (int a = 0; a < 2; ++a)
+        for (int k = 0; k < 3; ++k) aE[a][k] = aJ[a][0] * aW[0][k] + aJ[a][1] * aW[1][k] + aJ[a][2] * aW[2][k];
+    const double aQ[2][2] = {{std::fabs(double(pr.ca)), std::fabs(double(pr.cb))},
+                             {std::fabs(double(pr.cb)), std::fabs(double(pr.cc))}};
+    const double aG[2][2] = {{s.a, 0.5 * s.b}, {0.5 * s.b, s.c}};
+    double aQG[2][2] = {{0, 0}, {0, 0}}, adSp[2][2] = {{0, 0}, {0, 0}};
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b)
+            for (int k = 0; k < 2; ++k) aQG[a][b] += aQ[a][k] * aG[k][b];
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b)
+            for (int k = 0; k < 2; ++k) adSp[a][b] += aQG[a][k] * aQ[k][b];
+    double adS[3][3], adE[2][3];
+    for (int k = 0; k < 3; ++k)
+        for (int l = 0; l < 3; ++l) {
+            double acc = 0;
+            for (int a = 0; a < 2; ++a)
+                for (int b = 0; b < 2; ++b) acc += aE[a][k] * adSp[a][b] * aE[b][l];
+            adS[k][l] = acc;
+        }
+    for (int a = 0; a < 2; ++a)
+        for (int l = 0; l < 3; ++l) {
+            double acc = 0;
+            for (int b = 0; b < 2; ++b)
+                for (int k = 0; k < 3; ++k) acc += adSp[a][b] * aE[b][k] * aS[k][l];
+            adE[a][l] = 2 * acc;
+        }
+    double adJ[2][3];
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 3; ++b) adJ[a][b] = adE[a][0] * aW[b][0] + adE[a][1] * aW[b][1] + adE[a][2] * aW[b][2];
+    const double z2 = z * z, z3 = z2 * z;
+    const double adXcJ[3] = {adJ[0][2] * fx / z2, adJ[1][2] * fy / z2,
+                             adJ[0][0] * fx / z2 + adJ[0][2] * 2 * fx * x / z3 + adJ[1][1] * fy / z2 +
+                                 adJ[1][2] * 2 * fy * y / z3};
+    const double adXcm[3] = {aJ[0][0] * s.mx, aJ[1][1] * s.my, aJ[0][2] * s.mx + aJ[1][2] * s.my + s.d};
+    double adXc[3];
+    for (int a = 0; a < 3; ++a) adXc[a] = adXcm[a] + adXcJ[a];
+    for (int k = 0; k < 3; ++k) out[k] = aW[0][k] * adXc[0] + aW[1][k] * adXc[1] + aW[2][k] * adXc[2];
+    double adM[3][3], adRm[3][3];
+    for (int a = 0; a < 3; ++a)
+        for (int k = 0; k < 3; ++k) adM[a][k] = 2 * (adS[a][0] * aM[0][k] + adS[a][1] * aM[1][k] + adS[a][2] * aM[2][k]);
+    for (int k = 0; k < 3; ++k) out[3 + k] = adM[0][k] * aR[0][k] + adM[1][k] * aR[1][k] + adM[2][k] * aR[2][k];
+    for (int a = 0; a < 3; ++a)
+        for (int k = 0; k < 3; ++k) adRm[a][k] = adM[a][k] * std::fabs(p[3 + k]);
+    double dR[3][3][4], adqh[4] = {0, 0, 0, 0};
+    dR_dq(q, dR);
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+            for (int m = 0; m < 4; ++m) adqh[m] += adRm[a][b] * std::fabs(dR[a][b][m]);
+    double adot = 0;
+    for (int m = 0; m < 4; ++m) adot += adqh[m] * std::fabs(q[m]);
+    for (int m = 0; m < 4; ++m) out[6 + m] = (adqh[m] + std::fabs(q[m]) * adot) / nq;
+    out[10] = s.o;
+    if (camr.sh == 1) {
+        double cw[3];
+        for (int k = 0; k < 3; ++k) cw[k] = -(W[0][k] * V[3] + W[1][k] * V[7] + W[2][k] * V[11]);
+        const double d[3] = {p[0] - cw[0], p[1] - cw[1], p[2] - cw[2]};
+        const double len = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+        const double au[3] = {std::fabs(d[0] / len), std::fabs(d[1] / len), std::fabs(d[2] / len)};
+        const double gc[3] = {pr.lit[0] ? s.r : 0.0, pr.lit[1] ? s.g : 0.0, pr.lit[2] ? s.bl : 0.0};
+        const double basis[4] = {SH_C0, SH_C1 * au[1], SH_C1 * au[2], SH_C1 * au[0]};
+        double adu[3] = {0, 0, 0};
+        for (int c = 0; c < 3; ++c) {
+            for (int k = 0; k < 4; ++k) out[11 + 3 * k + c] = gc[c] * basis[k];
+            adu[0] += gc[c] * SH_C1 * std::fabs(p[20 + c]);
+            adu[1] += gc[c] * SH_C1 * std::fabs(p[14 + c]);
+            adu[2] += gc[c] * SH_C1 * std::fabs(p[17 + c]);
+        }
+        const double aud = au[0] * adu[0] + au[1] * adu[1] + au[2] * adu[2];
+        for (int k = 0; k < 3; ++k) out[k] += (adu[k] + au[k] * aud) / len;
+    } else {
+        out[11] = s.r;
+        out[12] = s.g;
+        out[13] = s.bl;
+    }
+}
+
 // Error-bound scale of every gradient (parity tolerance): the sums over pixels of
 // the magnitudes of the per-pixel terms, S_j = sum_p |c_pj| for the 10 screen quantities j
 // (backward_pixel with `sa`), carried through the per-Gaussian chain, which is linear in the screen
@@ -597,7 +711,7 @@ static GaussianBack gaussian_backward(const R* params, int64_t ld, int64_t i, co
 template <class R>
 static void error_bound(const R* params, int64_t n, int64_t ld, const R* view, const Cam<R>& cam,
                         const std::vector<Proj<R>>& pj, const std::vector<ScreenGrad>& sabs, double* grad_bound,
-                        double* pose_bound, double* pose_bound_paper) {
+                        double* pose_bound, double* pose_bound_paper, double* chain_scale) {
     const int rows = n_rows(cam.sh);
     double W[3][3];
     for (int a = 0; a < 3; ++a)
@@ -610,6 +724,11 @@ static void error_bound(const R* params, int64_t n, int64_t ld, const R* view, c
         for (int64_t i = 0; i < n; ++i) {
             if (!pj[size_t(i)].in_front || pj[size_t(i)].tiles == 0) continue;
             const ScreenGrad& m = sabs[size_t(i)];
+            if (chain_scale) {
+                double cs[MAXP];
+                gaussian_chain_scale<R>(params, ld, i, view, cam, m, pj[size_t(i)], cs);
+                for (int k = 0; k < rows; ++k) chain_scale[k * n + i] = cs[k];
+            }
             const double v10[10] = {m.mx, m.my, m.a, m.b, m.c, m.o, m.r, m.g, m.bl, m.d};
             for (int j = 0; j < 10; ++j) {
                 if (v10[j] == 0) continue;
@@ -804,14 +923,15 @@ ORACLE_FORWARD(f64, double)
                               double* grad_params, double* grad_screen, double* pose_twist,                    \
                               double* pose_twist_paper, double* pose_qt, int32_t qt_cov,                       \
                               const int64_t* pixels, int64_t n_pix, int32_t mode, double* grad_bound,          \
-                              double* pose_bound, double* pose_bound_paper, double* screen_bound) {            \
+                              double* pose_bound, double* pose_bound_paper, double* screen_bound,              \
+                              double* chain_scale) {                                                           \
         Cam<R> cam(*oc, mode);                                                                            \
         auto pj = project_all<R>(params, n, ld, view, cam);                                                    \
         auto order = depth_order(pj);                                                                          \
         const int64_t P = int64_t(cam.W) * cam.H;                                                              \
         const int64_t NQ = pixels ? n_pix : P; /* optional pixel subset (bounded CPU-baseline sample) */       \
         std::vector<ScreenGrad> sg(size_t(n), ScreenGrad{0, 0, 0, 0, 0, 0, 0, 0, 0, 0});                       \
-        const bool want_bound = grad_bound || pose_bound || pose_bound_paper || screen_bound;                  \
+        const bool want_bound = grad_bound || pose_bound || pose_bound_paper || screen_bound || chain_scale;   \
         std::vector<ScreenGrad> sabs(want_bound ? size_t(n) : 0, ScreenGrad{0, 0, 0, 0, 0, 0, 0, 0, 0, 0});   \
         _Pragma("omp parallel for schedule(dynamic, 64)")                                                     \
         for (int64_t qi = 0; qi < NQ; ++qi) {                                                                  \
@@ -823,7 +943,8 @@ ORACLE_FORWARD(f64, double)
             const double dc[3] = {double(dLdC[q]), double(dLdC[P + q]), double(dLdC[2 * P + q])};             \
             backward_pixel<R>(r, pj, params, ld, cam, dc, double(dLdD[q]), sg, want_bound ? &sabs : nullptr);  \
         }                                                                                                      \
-        if (want_bound) error_bound<R>(params, n, ld, view, cam, pj, sabs, grad_bound, pose_bound, pose_bound_paper); \
+        if (want_bound) error_bound<R>(params, n, ld, view, cam, pj, sabs, grad_bound, pose_bound, pose_bound_paper, \
+                                       chain_scale);                                                           \
         if (screen_bound) for (int64_t i = 0; i < n; ++i) {                                                    \
             const ScreenGrad& m = sabs[size_t(i)];                                                             \
             const double v10[10] = {m.mx, m.my, m.a, m.b, m.c, m.o, m.r, m.g, m.bl, m.d};                      \

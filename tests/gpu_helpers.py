@@ -89,6 +89,11 @@ def grad_close(gpu, ref, rtol=RTOL_GRAD, atol=ATOL_GRAD):
 # a dropped term, a sign or an index error moves the element by O(bound). No element may fail.
 K_BOUND = 1e-4
 ULP2 = 2.384185791015625e-07   # 2 ulp of fp32 (2^-22)
+# The per-Gaussian chain itself is evaluated in fp32 by the kernel: its rounding is at most (depth of
+# the chain, < 64 operations) x 2^-24 of the chain evaluated on magnitudes (oracle chain_scale). This
+# matters only where the exact chain cancels completely, e.g. the rotation gradient of an isotropic
+# Gaussian (exactly 0; the kernel's fp32 terms leave ~1e-6).
+K_CHAIN = 64 * 2.0 ** -24
 
 
 def bound_factor(n_last) -> float:
@@ -97,13 +102,16 @@ def bound_factor(n_last) -> float:
     return max(K_BOUND, ULP2 * float(nl.max() if nl.size else 0))
 
 
-def check_grads(gpu, ref, bound, label="", rtol=RTOL_GRAD, atol=ATOL_GRAD, k=K_BOUND):
+def check_grads(gpu, ref, bound, label="", rtol=RTOL_GRAD, atol=ATOL_GRAD, k=K_BOUND, chain=None):
     gpu = np.asarray(gpu, np.float64)
     ref = np.asarray(ref, np.float64)
     bound = np.asarray(bound, np.float64)
     err = np.abs(gpu - ref)
     plain = err <= rtol * np.abs(ref) + atol
-    ok = plain | (err <= k * bound + atol)
+    lim = k * bound + atol
+    if chain is not None:
+        lim = lim + K_CHAIN * np.asarray(chain, np.float64)
+    ok = plain | (err <= lim)
     nb = int((~plain).sum())
     worst = float((err[~plain] / np.maximum(bound[~plain], 1e-300)).max()) if nb else 0.0
     print(f"{label}: {err.size} elements, {nb} outside 2e-3 rel / 1e-6 abs (cancelling sums), "

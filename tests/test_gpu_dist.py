@@ -117,14 +117,18 @@ def test_two_ranks_bitwise_equal_and_match_one_rank():
     # the first step's reduced gradient against the 1-rank sum over the same 4 keyframes
     p, tgt, views, kc = _world()
     bound = np.zeros((14, N))
+    chain = np.zeros((14, N))
     nl_max = 0
     for vv in views:   # the L1 upstream's magnitudes are the oracle's as well (sign(0) aside)
         t = oracle.forward(tgt, vv, CAM, "f32")
         f = oracle.forward(p, vv, CAM, "f32")
         L = oracle.loss_l1(f["color"], f["depth"], t["color"], t["depth"], 0.9, 0.1)
         nl_max = max(nl_max, int(f["n_last"].max()))
-        bound += oracle.backward(p, vv, CAM, L["dL_dcolor"], L["dL_ddepth"], "f32", bound=True)["grad_bound"]
-    check_grads(two[0]["grad1"], one[0]["grad1"], bound, "2-rank vs 1-rank reduced gradient", k=bound_factor(nl_max))
+        ob = oracle.backward(p, vv, CAM, L["dL_dcolor"], L["dL_ddepth"], "f32", bound=True)
+        bound += ob["grad_bound"]
+        chain += ob["chain_scale"]
+    check_grads(two[0]["grad1"], one[0]["grad1"], bound, "2-rank vs 1-rank reduced gradient", k=bound_factor(nl_max),
+                chain=chain)
 
 
 @pytest.mark.timeout(900)

@@ -89,6 +89,7 @@ def test_mapping_single_gpu_steps():
     acc = mp.grad[:, :n].clone()
     ref = torch.zeros_like(acc)
     bound = np.zeros((14, n))
+    chain = np.zeros((14, n))
     nl_max = 0
     for kf, vv in zip(kfs, views):
         gk = torch.zeros(14, cap, device="cuda")
@@ -99,12 +100,14 @@ def test_mapping_single_gpu_steps():
         torch.cuda.synchronize()
         nl = probe.arrays(n)["n_last"].cpu().numpy()
         nl_max = max(nl_max, int(nl.max()))
-        bound += oracle.backward(p, vv, cam, dc.cpu().numpy(), dd.cpu().numpy(), "f32", replay_nlast=nl,
-                                 bound=True)["grad_bound"]
+        ob = oracle.backward(p, vv, cam, dc.cpu().numpy(), dd.cpu().numpy(), "f32", replay_nlast=nl, bound=True)
+        bound += ob["grad_bound"]
+        chain += ob["chain_scale"]
     torch.cuda.synchronize()
     from gpu_helpers import bound_factor, check_grads
     # fp32 atomics: equal up to summation order, within the sums' error bound
-    check_grads(acc.cpu().numpy(), ref.cpu().numpy(), bound, "keyframe accumulation", k=bound_factor(nl_max))
+    check_grads(acc.cpu().numpy(), ref.cpu().numpy(), bound, "keyframe accumulation", k=bound_factor(nl_max),
+                chain=chain)
     # a few full mapping steps with densification: loss goes down, map stays finite and in capacity
     mp = ShardedMapper(P, n, kfs, cam, kc, max_add_per_kf=4096)
     losses = []

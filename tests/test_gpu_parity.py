@@ -192,7 +192,7 @@ def test_backward_parity(c):
     for cov in (True, False):
         gg, gpose, gpose2 = _gpu_backward(pipe, P, V, cfg, dc, dd, cov=cov)
         tag = f"cfg{c} cov={int(cov)}"
-        check_grads(gg, o["grad_params"], o["grad_bound"], f"{tag} params", k=kb)
+        check_grads(gg, o["grad_params"], o["grad_bound"], f"{tag} params", k=kb, chain=o["chain_scale"])
         ref = o["pose_twist"] if cov else o["pose_twist_paper"]
         bnd = o["pose_bound"] if cov else o["pose_bound_paper"]
         check_pose(gpose, ref, bnd, f"{tag} gs_render_bwd twist", k=kb)
@@ -257,7 +257,7 @@ def test_bench_iteration_matches_oracle(c):
     ob = oracle.backward(p, v, cam, dc.astype(np.float32), dd.astype(np.float32), "f32", replay_nlast=nl,
                          bound=True)
     kb = bound_factor(nl)
-    check_grads(grad.cpu().numpy(), ob["grad_params"], ob["grad_bound"], f"bench iteration cfg{c} params", k=kb)
+    check_grads(grad.cpu().numpy(), ob["grad_params"], ob["grad_bound"], f"bench iteration cfg{c} params", k=kb, chain=ob["chain_scale"])
     check_pose(gpose.cpu().numpy(), ob["pose_twist"], ob["pose_bound"], f"bench iteration cfg{c} twist", k=kb)
     assert abs(float(pipe.loss.item()) - L["loss"]) <= 1e-5 * abs(L["loss"]), (float(pipe.loss.item()), L["loss"])
 
@@ -489,6 +489,77 @@ def test_edge_empty_and_culled_and_ragged():
     assert np.abs(fr.color.cpu().numpy() - o["color"]).max() <= ATOL_IMG
 
 
+def _edge_scene(kind):
+    """Degenerate geometries of the method: a 1x1 image; a tile-aligned 32x32 image under one huge
+    Gaussian (every tile, the 0.99 clamp on most pixels); Gaussians straddling the 0.2 m near plane;
+    a half-culled mix with Gaussians far off-screen; coincident means and depths (index ties); an
+    image narrower than one tile (9x40); a degenerate quaternion (zero 4-vector: culled)."""
+    rng = np.random.default_rng({"one_px": 1, "huge": 2, "near_plane": 3, "offscreen": 4, "ties": 5,
+                                 "thin": 6, "zero_quat": 7}[kind])
+    W, H = {"one_px": (1, 1), "huge": (32, 32), "thin": (9, 40)}.get(kind, (48, 40))
+    cam = gi.Camera(40.0, 40.0, (W - 1) / 2, (H - 1) / 2, W, H, bg=(0.1, 0.2, 0.3))
+    n = {"one_px": 50, "huge": 3, "ties": 30}.get(kind, 60)
+    z = rng.uniform(1.0, 3.0, n)
+    p = np.zeros((14, n))
+    p[0] = rng.uniform(-0.4, 0.4, n) * z
+    p[1] = rng.uniform(-0.4, 0.4, n) * z
+    p[2] = z
+    p[3:6] = np.exp(rng.normal(np.log(0.1), 0.3, (3, n)))
+    q = rng.normal(size=(4, n))
+    p[6:10] = q / np.linalg.norm(q, axis=0)
+    p[10] = rng.uniform(0.2, 0.9, n)
+    p[11:14] = rng.uniform(0, 1, (3, n))
+    if kind == "huge":
+        p[0:3, 0] = [0.0, 0.0, 2.0]
+        p[3:6, 0] = 1.0
+        p[10, 0] = 0.999
+    elif kind == "near_plane":
+        p[2] = rng.uniform(0.15, 0.35, n)   # many within the footprint of the 0.2 m cull
+        p[3:6] = 0.02
+    elif kind == "offscreen":
+        p[0, ::2] = rng.choice([-1, 1], n // 2 + n % 2) * rng.uniform(5, 50, n // 2 + n % 2)
+    elif kind == "ties":
+        p[0:3, 10:20] = p[0:3, 0:1]          # ten copies of one mean (equal depth bits)
+        p[2, 20:30] = p[2, 0]                # ten more at that depth elsewhere
+    elif kind == "zero_quat":
+        p[6:10, ::3] = 0.0
+    return p.astype(np.float32), cam
+
+
+@pytest.mark.parametrize("kind", ["one_px", "huge", "near_plane", "offscreen", "ties", "thin", "zero_quat"])
+def test_edge_geometry_end_to_end(kind):
+    """Each degenerate geometry through project, both binning paths, forward and backward (both pose
+    modes) against the oracle: lists bit-exact, images under the tie rule, every gradient element
+    under the §4.3 criterion."""
+    import paper_2311_11700_b200 as g
+    p, cam = _edge_scene(kind)
+    v = gi.identity_view()
+    n = p.shape[1]
+    for path in (0, g.GS_FLAG_BINSORT_KEYS):
+        pipe, P, V, fr = run_forward(p, v, cam, flags_bin=path)
+        a = pipe.arrays(n)
+        o_p = oracle.project(p, v, cam, "f32")
+        assert np.array_equal(a["tiles"].cpu().numpy().view(np.uint32), o_p["tiles"])
+        ob = oracle.bin_sort(o_p["depth_bits"], o_p["rect"], o_p["tiles"], cam)
+        assert fr.n_keys == ob["n_keys"]
+        assert np.array_equal(a["vals"].cpu().numpy().view(np.uint32), ob["vals"])
+        assert np.array_equal(a["ranges"].cpu().numpy().view(np.uint32), ob["ranges"])
+    o = oracle.forward(p, v, cam, "f32")
+    compare_images(dict(color=fr.color, depth=fr.depth, alpha=fr.alpha, n_last=a["n_last"]), o, cam, p, v,
+                   f"edge {kind}")
+    dc, dd = gi.upstream(cam.width, cam.height, 44)
+    nl = a["n_last"].cpu().numpy()
+    ob = oracle.backward(p, v, cam, dc, dd, "f32", replay_nlast=nl, bound=True)
+    kb = bound_factor(nl)
+    for cov in (True, False):
+        gg, gpose, gpose2 = _gpu_backward(pipe, P, V, type("C", (), {"cam": cam})(), dc, dd, cov=cov)
+        check_grads(gg, ob["grad_params"], ob["grad_bound"], f"edge {kind} params", k=kb, chain=ob["chain_scale"])
+        ref = ob["pose_twist"] if cov else ob["pose_twist_paper"]
+        bnd = ob["pose_bound"] if cov else ob["pose_bound_paper"]
+        check_pose(gpose, ref, bnd, f"edge {kind} twist cov={int(cov)}", k=kb)
+        check_pose(gpose2, ref, bnd, f"edge {kind} gs_pose_grad cov={int(cov)}", k=kb)
+
+
 def test_capacity_error_and_stale():
     import paper_2311_11700_b200 as g
     cfg, p, v = scene(0)
@@ -623,7 +694,7 @@ def test_sh1_parity(c):
     ob = oracle.backward(p, v, cfg.cam, dc, dd, "f32", replay_nlast=nl, bound=True)
     assert gg.shape == (23, p.shape[1])
     kb = bound_factor(nl)
-    check_grads(gg, ob["grad_params"], ob["grad_bound"], f"sh1 cfg{c} params", k=kb)
+    check_grads(gg, ob["grad_params"], ob["grad_bound"], f"sh1 cfg{c} params", k=kb, chain=ob["chain_scale"])
     check_pose(gpose, ob["pose_twist"], ob["pose_bound"], f"sh1 cfg{c} twist", k=kb)
     check_pose(gpose2, ob["pose_twist"], ob["pose_bound"], f"sh1 cfg{c} gs_pose_grad twist", k=kb)
     _, gp_paper, gp_paper2 = _gpu_backward(pipe, P, V, cfg, dc, dd, cov=False)
@@ -750,7 +821,7 @@ def test_fused_l1_backward_equals_loss_then_backward(c):
     # fp32 atomics order only; the scale of each sum from the oracle on the same upstream
     nl = pipe.arrays(n)["n_last"].cpu().numpy()
     ob = oracle.backward(p, v, cfg.cam, dc.cpu().numpy(), dd.cpu().numpy(), "f32", replay_nlast=nl, bound=True)
-    check_grads(got.cpu().numpy(), ref.cpu().numpy(), ob["grad_bound"], f"fused L1 cfg{c}", k=bound_factor(nl))
+    check_grads(got.cpu().numpy(), ref.cpu().numpy(), ob["grad_bound"], f"fused L1 cfg{c}", k=bound_factor(nl), chain=ob["chain_scale"])
     check_pose(gp.cpu().numpy(), gp_ref.cpu().numpy(), ob["pose_bound"], f"fused L1 cfg{c} twist", k=bound_factor(nl))
 
 
@@ -842,7 +913,7 @@ def test_opacity_radius_parity(c):
     gp, gpose, _ = _gpu_backward(pipe, P, V, cfg, dc, dd)
     ob = oracle.backward(p, v, cfg.cam, dc, dd, "f32", replay_nlast=a["n_last"].cpu().numpy(),
                          opacity_radius=True, bound=True)
-    check_grads(gp, ob["grad_params"], ob["grad_bound"], f"orad cfg{c} params", k=bound_factor(a["n_last"].cpu().numpy()))
+    check_grads(gp, ob["grad_params"], ob["grad_bound"], f"orad cfg{c} params", k=bound_factor(a["n_last"].cpu().numpy()), chain=ob["chain_scale"])
     check_pose(gpose, ob["pose_twist"], ob["pose_bound"], f"orad cfg{c} twist", k=bound_factor(a["n_last"].cpu().numpy()))
 
 

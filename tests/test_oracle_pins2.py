@@ -4,6 +4,7 @@ other than itself.
 - accum_grad (reading C30): hand-computed NDC norms and a finite-difference NDC chain rule;
 - pose_adam_step (reading C23): torch.optim.Adam on a 6-vector twist, scipy.linalg.expm for SE(3);
 - the backward's error-bound scale (DESIGN.md §4.3): dominance and exactness on sign-definite sums;
+  the chain's magnitude scale: dominance, and the isotropic case it exists for;
 - the power's evaluation order (reading R1 against SURVEY.md §8(c) O3): both orders take the same
   decisions outside the oracle's tie band at configs 0-2.
 """
@@ -118,6 +119,27 @@ def test_error_bound_dominates_and_is_exact_on_sign_definite_sums():
     g, b = o1["grad_params"][:, 0], o1["grad_bound"][:, 0]
     np.testing.assert_allclose(g[10:14], b[10:14], rtol=1e-12)
     assert np.all(b[0:2] > np.abs(g[0:2]) * 1.01)
+
+
+def test_chain_scale_dominates_and_exposes_isotropic_rotation():
+    """chain_scale (the per-Gaussian chain on magnitudes) bounds the signed chain of the same
+    magnitudes: chain >= bound >= |grad| (up to the fp32 conic the scale reads: 1e-5 relative), with
+    equality on the rows the chain passes through unchanged (opacity, RGB). For an isotropic Gaussian
+    the exact rotation gradient is 0 (Sigma = s^2 I for every rotation) while the chain's magnitude is
+    not: exactly the case where an fp32 chain leaves rounding behind and the scale is needed."""
+    cfg = gi.CONFIGS[0]
+    p, v, cam = cfg.scene(), cfg.view(), cfg.cam
+    dc, dd = gi.upstream(cam.width, cam.height, gi.UPSTREAM_SEED_CFG0)
+    o = oracle.backward(p, v, cam, dc, dd, "f32", bound=True)
+    assert np.all(o["chain_scale"] >= o["grad_bound"] * (1 - 1e-5))
+    np.testing.assert_allclose(o["chain_scale"][10:14], o["grad_bound"][10:14], rtol=1e-12)
+    cam1 = gi.Camera(40.0, 40.0, 15.5, 15.5, 32, 32)
+    p1 = _one([0.05, -0.03, 2.0], [0.3, 0.3, 0.3], 0.7, [0.2, 0.5, 0.9], quat=(0.9, 0.1, -0.2, 0.3))
+    rng = np.random.default_rng(3)
+    o1 = oracle.backward(p1, gi.identity_view(), cam1, rng.normal(size=(3, 32, 32)).astype(np.float32),
+                         rng.normal(size=(32, 32)).astype(np.float32), "f64", bound=True)
+    gq, cq = o1["grad_params"][6:10, 0], o1["chain_scale"][6:10, 0]
+    assert np.all(np.abs(gq) <= 1e-12 * cq.max()) and cq.min() > 0
 
 
 # ------------------------------------------------------------------ power order (R1 vs O3)
