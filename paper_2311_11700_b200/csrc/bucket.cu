@@ -39,7 +39,9 @@ gs_status resolve_keys(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t
 // up to 4 chunks ahead of the slowest one instead of meeting it at a barrier every chunk.
 constexpr int kWX = 8, kWY = 4;        // consumer tile area (lane j = tile (j & 7, j >> 3))
 constexpr int kBX = 16, kBY = 16;      // block tile area: 2 x 4 consumer areas
-constexpr int kEmitChunkBlocks = 256;  // grid.x: chunk stride (measured: 96 -> 0.091 ms, 224-320 -> 0.081 ms)
+// grid.x (chunk stride): 256 up to ~1M Gaussians, 512 beyond (measured, round 2: config 2 with 128 /
+// 256 / 512 / 1024 -> 0.080 / 0.073 / 0.077 / 0.083 ms; config-4 size 0.384 / 0.349 / 0.333 / 0.340 ms)
+constexpr int kEmitChunkBlocksMin = 256, kEmitChunkBlocksMax = 512;
 constexpr int kRing = 4;               // chunk slots in flight
 constexpr int kConsumers = 8;
 constexpr int kProducers = 2;          // producer warps, alternating chunks (ring order kept)
@@ -211,7 +213,8 @@ gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaS
         if (rc != GS_OK) return rc;
         const int nch = int((n + kChunk - 1) / kChunk);
         KTimer kt(s, KID_BUCKET_EMIT, st);
-        const dim3 grid(unsigned(std::min(nch, kEmitChunkBlocks)), unsigned((s->cam_gx + kBX - 1) / kBX),
+        const int gx = std::min(kEmitChunkBlocksMax, std::max(kEmitChunkBlocksMin, nch / 8));
+        const dim3 grid(unsigned(std::min(nch, gx)), unsigned((s->cam_gx + kBX - 1) / kBX),
                         unsigned((s->cam_gy + kBY - 1) / kBY));
         launch_pdl(bucket_emit_kernel, grid, dim3((kConsumers + kProducers) * 32), 0, st, at<uint32_t>(s, s->svals), at<short4>(s, s->srect),
                                                  at<uint32_t>(s, s->chunk_mat), &misc->n_onscreen, &misc->n_keys_eff,
