@@ -1118,9 +1118,14 @@ __global__ void __launch_bounds__(256, kGbwdBlocksPerSM) gaussian_bwd_kernel(
             if (tiles[i] == 0u)
                 for (int k = 0; k < rows; ++k) grad[k * ld + i] = 0.f;
     }
-    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < Von && int(blockIdx.x) < compute_blocks;
-         t += int64_t(compute_blocks) * blockDim.x) {
-        const int64_t i = int64_t(onlist[t]);
+    // the next item's Gaussian index is loaded one item ahead, so an item's parameter loads do not
+    // wait for its index load first (one DRAM round trip per item instead of two)
+    const int64_t tstride = int64_t(compute_blocks) * blockDim.x;
+    int64_t t0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    uint32_t i_next = (t0 < Von && int(blockIdx.x) < compute_blocks) ? onlist[t0] : 0u;
+    for (int64_t t = t0; t < Von && int(blockIdx.x) < compute_blocks; t += tstride) {
+        const int64_t i = int64_t(i_next);
+        i_next = t + tstride < Von ? onlist[t + tstride] : 0u;
         if (i >= n) continue;
         float s[10];
 #pragma unroll
