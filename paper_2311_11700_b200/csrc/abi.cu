@@ -64,7 +64,8 @@ static void carve(WsState* s, Carver& c) {
     s->sort_look = c.take(uint64_t(s->max_parts) * 256 * 8);
     s->misc = c.take(sizeof(Misc));
     s->scratch = c.take(uint64_t(px) * 4 * 4);
-    s->scratch14 = c.take(uint64_t(n) * 4 * 23);   // compaction scratch: up to 23 parameter rows
+    // in-place compaction (prune, split/clone): per-256-column counts / offsets, ticket + read flags
+    s->cmp = c.take(uint64_t(2 * ((n + 255) / 256 + 2)) * 4);
     s->dkey_sorted = c.take(uint64_t(n) * 4 * 2);
     s->dval_sorted = c.take(uint64_t(n) * 4 * 2);
     // densify block counts; also the backward prologue's per-block valid counts (148 * 4 blocks)

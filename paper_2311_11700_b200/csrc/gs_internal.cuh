@@ -41,7 +41,7 @@ struct WsState {
     // carve
     Region rec, depth_key, rect, radius, tiles, offsets, sgrad, scan_state,
         keys0, keys1, vals0, vals1, ranges, t_final, n_last, examined, sort_hist, sort_look,
-        misc, scratch, scratch14, dkey_sorted, dval_sorted, chunk_hist, chunk_mat, srect, tile_tot, pose_part,
+        misc, scratch, cmp, dkey_sorted, dval_sorted, chunk_hist, chunk_mat, srect, tile_tot, pose_part,
         onlist, live_cnt, svals, coop, tile_order, tile_pose;
     // run state
     int64_t n;                     // Gaussians of the last gs_project
@@ -130,6 +130,14 @@ __device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int& goal)
         } while (v < goal);
     }
     __syncthreads();
+}
+__device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
 }
 // debug library (-DGS_DEBUG=1): output invariant checks after each stage (debug.cu)
 void set_error_text(const char* msg);

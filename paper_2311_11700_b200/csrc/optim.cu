@@ -738,25 +738,105 @@ struct KeepPred {
     __device__ bool operator()(int64_t i) const { return opacity[i] >= min_o; }
 };
 
-struct GatherEmit {
-    const float* src;
-    float* dst;
-    int64_t src_ld, dst_ld;
-    int rows;
-    __device__ void operator()(int64_t i, uint32_t o) const {
-        for (int k = 0; k < rows; ++k) dst[k * dst_ld + o] = src[k * src_ld + i];
-    }
-};
+__global__ void set_n_kernel(int64_t* n_dev, const unsigned long long* count) { *n_dev = int64_t(*count); }
 
-__global__ void copy_rows_kernel(const float* __restrict__ src, int64_t src_ld, float* __restrict__ dst, int64_t dst_ld,
-                                 const unsigned long long* __restrict__ count) {
-    const int64_t n = int64_t(*count);
-    const int k = blockIdx.y;
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
-        dst[k * dst_ld + i] = src[k * src_ld + i];
+// ------------------------------------------------------------------ in-place stable compaction
+// PRUNE and the split/clone removal keep the columns a predicate accepts, in index order, in up to
+// four [rows][ld] arrays at once. One CTA per 256-column tile: count -> exclusive scan of the tile
+// counts -> compact. The compaction is in place: tile t's destination [off_t, off_t + cnt_t) lies at
+// or below its own columns and spans at most two source tiles, so the CTA reads its tile (all rows
+// of all arrays) into registers, publishes "read" for t, waits for the "read" flag of the earlier
+// tiles its destination overlaps, then writes. Tiles are claimed through a ticket counter, so every
+// tile waited on belongs to a CTA that is already running and whose read phase waits on nothing.
+// A tile with no removal at or before it moves nothing and only publishes its flag; a map with
+// nothing to remove costs one read of the predicate's row. Traffic: the moved columns once read and
+// once written (the two-pass scratch scheme it replaces moved every column four times).
+constexpr int kCmp = 256;
+
+template <class Pred>
+__global__ void __launch_bounds__(kCmp) count256_kernel(const int64_t* n_dev, Pred pred, uint32_t* __restrict__ counts) {
+    using BR = cub::BlockReduce<uint32_t, kCmp>;
+    __shared__ typename BR::TempStorage tmp;
+    const int64_t nn = *n_dev;
+    const int64_t i = int64_t(blockIdx.x) * kCmp + threadIdx.x;
+    const uint32_t c = BR(tmp).Sum((i < nn && pred(i)) ? 1u : 0u);
+    if (threadIdx.x == 0) counts[blockIdx.x] = c;
 }
 
-__global__ void set_n_kernel(int64_t* n_dev, const unsigned long long* count) { *n_dev = int64_t(*count); }
+template <int ROWS, class Pred>
+__global__ void __launch_bounds__(kCmp) compact_inplace_kernel(float* a0, float* a1, float* a2, float* a3, int64_t ld,
+                                                               const int64_t* n_dev, Pred pred, int nt,
+                                                               const uint32_t* __restrict__ offs,
+                                                               const unsigned long long* __restrict__ total,
+                                                               uint32_t* ctl) {
+    using BS = cub::BlockScan<uint32_t, kCmp>;
+    __shared__ typename BS::TempStorage tmp;
+    __shared__ uint32_t s_t;
+    if (threadIdx.x == 0) s_t = atomicAdd(&ctl[0], 1u);
+    __syncthreads();
+    const int t = int(s_t);
+    const int64_t nn = *n_dev;
+    const int64_t base = int64_t(t) * kCmp, i = base + threadIdx.x;
+    const int64_t off = offs[t];
+    const int64_t end = t + 1 < nt ? int64_t(offs[t + 1]) : int64_t(*total);
+    const int64_t valid = base < nn ? (nn - base < kCmp ? nn - base : kCmp) : 0;
+    uint32_t* flag = ctl + 1;
+    if (off == base && end - off == valid) {   // nothing at or before this tile moves
+        if (threadIdx.x == 0) st_release_u32(&flag[t], 1u);
+        return;
+    }
+    const bool keep = i < nn && pred(i);
+    float* arr[4] = {a0, a1, a2, a3};
+    float v[4][ROWS];
+    if (keep) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+            if (arr[a])
+#pragma unroll
+                for (int k = 0; k < ROWS; ++k) v[a][k] = arr[a][k * ld + i];
+    }
+    uint32_t rank;
+    BS(tmp).ExclusiveSum(keep ? 1u : 0u, rank);
+    __syncthreads();   // every thread's reads of the tile precede the release below
+    if (threadIdx.x == 0) {
+        __threadfence();
+        st_release_u32(&flag[t], 1u);
+        // destination [off, end) overlaps source tiles off/256 .. (end-1)/256 (all <= t)
+        if (end > off) {
+            for (int64_t u = off / kCmp; u <= (end - 1) / kCmp && u < t; ++u)
+                while (ld_acquire_u32(&flag[u]) == 0u) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+    if (keep) {
+        const int64_t o = off + rank;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+            if (arr[a])
+#pragma unroll
+                for (int k = 0; k < ROWS; ++k) arr[a][k * ld + o] = v[a][k];
+    }
+}
+
+// count + scan + in-place compaction of arrays[4] (nullable) over columns [0, *n_dev) of [rows][ld];
+// the kept count lands in *kept (the caller sets n from it)
+template <class Pred>
+void compact_inplace(WsState* s, float* const arrays[4], int rows, int64_t ld, int64_t capacity, const int64_t* n_dev,
+                     Pred pred, unsigned long long* kept, cudaStream_t st) {
+    const int nt = int((std::max<int64_t>(capacity, 1) + kCmp - 1) / kCmp);
+    uint32_t* counts = at<uint32_t>(s, s->cmp);
+    uint32_t* ctl = counts + (nt + 2);
+    cudaMemsetAsync(ctl, 0, size_t(nt + 1) * 4, st);
+    count256_kernel<<<nt, kCmp, 0, st>>>(n_dev, pred, counts);
+    scan_blocks_kernel<<<1, 1024, 0, st>>>(counts, nt, kept);
+    if (rows == 23)
+        compact_inplace_kernel<23><<<nt, kCmp, 0, st>>>(arrays[0], arrays[1], arrays[2], arrays[3], ld, n_dev, pred,
+                                                        nt, counts, kept, ctl);
+    else
+        compact_inplace_kernel<14><<<nt, kCmp, 0, st>>>(arrays[0], arrays[1], arrays[2], arrays[3], ld, n_dev, pred,
+                                                        nt, counts, kept, ctl);
+}
 
 // ------------------------------------------------------------------ split / clone (reading C30)
 __global__ void accum_grad_kernel(const uint32_t* __restrict__ onlist, const unsigned int* __restrict__ n_on,
@@ -895,18 +975,8 @@ gs_status run_split_clone(WsState* s, float* params, float* raw, float* m, float
     split_clone_total_kernel<<<1, 1, 0, st>>>(ncols, n_dev, nclone, nsplit, capacity);
     const KeepSplitPred keep{accum, n_dev};
     // compaction over [0, ncols): n_dev stays the original n inside the predicate (appended columns kept)
-    const int nb2 = int((capacity + kCmpTile - 1) / kCmpTile);
-    count_kernel<<<nb2, kCmpThreads, 0, st>>>(capacity, ncols, keep, bcounts);
-    scan_blocks_kernel<<<1, 1024, 0, st>>>(bcounts, nb2, &misc->keep_count);
-    float* scratch = at<float>(s, s->scratch14);
-    float* arrays[4] = {raw, m, v, params};
-    for (float* a : arrays) {
-        if (!a) continue;
-        scatter_kernel<<<nb2, kCmpThreads, 0, st>>>(capacity, ncols, keep,
-                                                    GatherEmit{a, scratch, ld, s->n_cap, rows}, bcounts);
-        dim3 g(unsigned(std::min<int64_t>((capacity + 255) / 256, sm_count() * 4)), unsigned(rows));
-        copy_rows_kernel<<<g, 256, 0, st>>>(scratch, s->n_cap, a, ld, &misc->keep_count);
-    }
+    float* const arrays[4] = {raw, m, v, params};
+    compact_inplace(s, arrays, rows, ld, capacity, ncols, keep, &misc->keep_count, st);
     set_n_kernel<<<1, 1, 0, st>>>(n_dev, &misc->keep_count);
     zero2_kernel<<<sm_count() * 4, 256, 0, st>>>(accum, count, capacity);
     return check_launch(s, "densify_split_clone");
@@ -1021,19 +1091,9 @@ gs_status run_densify(WsState* s, float* params, float* raw, int64_t* n_dev, int
         return check_launch(s, "densify_add");
     }
     if (cfg.mode == GS_DENSIFY_PRUNE) {
-        const int nb = int((capacity + kCmpTile - 1) / kCmpTile);
         KeepPred pred{params + 10 * ld, cfg.min_opacity};
-        GS_K((count_kernel<<<nb, kCmpThreads, 0, st>>>(capacity, n_dev, pred, bcounts)));
-        GS_K((scan_blocks_kernel<<<1, 1024, 0, st>>>(bcounts, nb, &misc->keep_count)));
-        float* scratch = at<float>(s, s->scratch14);
-        float* arrays[4] = {raw, m, v, params};   // params last: the predicate reads its opacity row
-        for (float* a : arrays) {
-            if (!a) continue;
-            GS_K((scatter_kernel<<<nb, kCmpThreads, 0, st>>>(capacity, n_dev, pred,
-                                                             GatherEmit{a, scratch, ld, s->n_cap, rows}, bcounts)));
-            dim3 g(unsigned(std::min<int64_t>((capacity + 255) / 256, sm_count() * 4)), unsigned(rows));
-            GS_K((copy_rows_kernel<<<g, 256, 0, st>>>(scratch, s->n_cap, a, ld, &misc->keep_count)));
-        }
+        float* const arrays[4] = {raw, m, v, params};   // each column's predicate is read before it moves
+        GS_K((compact_inplace(s, arrays, rows, ld, capacity, n_dev, pred, &misc->keep_count, st)));
         GS_K((set_n_kernel<<<1, 1, 0, st>>>(n_dev, &misc->keep_count)));
         return check_launch(s, "densify_prune");
     }

@@ -419,6 +419,41 @@ def test_densify_add_and_prune_parity(rows):
     assert np.array_equal(Pc[:, :n2].cpu().numpy(), before[:, keep])
 
 
+@pytest.mark.parametrize("rows", [14, 23])
+@pytest.mark.parametrize("pattern", ["none", "all", "first", "last", "every_other", "long_run", "sparse", "dense"])
+def test_prune_in_place_compaction(rows, pattern):
+    """PRUNE's in-place compaction over all four arrays (params, raw, Adam m, v) against the stable
+    boolean selection the oracle's keep mask defines: removal patterns that make a tile's destination
+    reach far below it (a long removed run), empty results, nothing removed, ragged tail."""
+    import paper_2311_11700_b200 as g
+    n = 70_001
+    cap = n + 300
+    rng = np.random.default_rng(7)
+    o = rng.uniform(0.1, 1.0, n).astype(np.float32)
+    kill = {"none": np.zeros(n, bool), "all": np.ones(n, bool), "first": np.arange(n) == 0,
+            "last": np.arange(n) == n - 1, "every_other": np.arange(n) % 2 == 0,
+            "long_run": (np.arange(n) >= 1000) & (np.arange(n) < 41_000), "sparse": rng.random(n) < 0.002,
+            "dense": rng.random(n) < 0.9}[pattern]
+    o[kill] = 0.001
+    keep = oracle.densify_prune_mask(o)
+    pipe = g.RenderPipeline(cap, 1 << 16, 64, 64)
+    arrs = [torch.randn(rows, cap, device="cuda") for _ in range(4)]
+    arrs[0][10, :n] = torch.as_tensor(o, device="cuda")
+    before = [a[:, :n].cpu().numpy() for a in arrs]
+    tail = [a[:, n:].cpu().numpy() for a in arrs]
+    n_dev = torch.tensor([n], dtype=torch.int64, device="cuda")
+    P, raw, m, v = arrs
+    g.gs_densify_prune(P, raw, n_dev, cap, cap, m, v, None, None, None, None, None, None, None,
+                       g.densify_cfg(g.GS_DENSIFY_PRUNE, rows=rows), None, None, pipe.ws)
+    torch.cuda.synchronize()
+    k = int(keep.sum())
+    assert int(n_dev.item()) == k
+    for a, b, t in zip(arrs, before, tail):
+        got = a.cpu().numpy()
+        assert np.array_equal(got[:, :k], b[:, keep])
+        assert np.array_equal(got[:, n:], t)   # columns past n untouched
+
+
 def test_select_parity():
     import paper_2311_11700_b200 as g
     cfg, p, v = scene(1)
