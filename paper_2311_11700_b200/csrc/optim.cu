@@ -466,26 +466,58 @@ void launch_pose_extrapolate(const float* t1, const float* t2, float* out, cudaS
 // ------------------------------------------------------------------ Adam
 struct Lr14 { float v[23]; };   // per-row rates: 14 (RGB) or 23 (degree-1 SH) rows
 
+__device__ __forceinline__ float adam_one(float r, float gr, float& m, float& v, int k, float lrk, float b1, float b2,
+                                         float eps, float bc1, float bc2, float& act) {
+    if (k >= 3 && k < 6) gr *= expf(r);                       // d/dlog s = s d/ds
+    else if (k == 10) { const float s = 1.f / (1.f + expf(-r)); gr *= s * (1.f - s); }   // d/dlogit o
+    m = b1 * m + (1.f - b1) * gr;
+    v = b2 * v + (1.f - b2) * gr * gr;
+    const float nr = r - lrk * (m / bc1) / (sqrtf(v / bc2) + eps);
+    act = (k >= 3 && k < 6) ? expf(nr) : (k == 10 ? 1.f / (1.f + expf(-nr)) : nr);
+    return nr;
+}
+
+// One row per blockIdx.y. With 16-byte aligned arrays the row body moves float4s (the row's
+// unaligned head and tail go element by element): 4x the bytes in flight per load instruction, which
+// the elementwise update needs to approach HBM bandwidth (~0.9 GB per step at 2M x 14).
 __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ raw, float* __restrict__ act,
                                                    const float* __restrict__ g, float* __restrict__ m,
                                                    float* __restrict__ v, int64_t n, int64_t ld, Lr14 lr, float b1,
-                                                   float b2, float eps, float bc1, float bc2) {
+                                                   float b2, float eps, float bc1, float bc2, bool vec) {
     const int k = blockIdx.y;
     const float lrk = lr.v[k];
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t o = k * ld + i;
-        const float r = raw[o];
-        float gr = g[o];
-        if (k >= 3 && k < 6) gr *= expf(r);                       // d/dlog s = s d/ds
-        else if (k == 10) { const float s = 1.f / (1.f + expf(-r)); gr *= s * (1.f - s); }   // d/dlogit o
-        const float mm = b1 * m[o] + (1.f - b1) * gr;
-        const float vv = b2 * v[o] + (1.f - b2) * gr * gr;
+    const int64_t row = k * ld;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x, t0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    int64_t head = n, body_end = n;
+    if (vec) {
+        head = std::min<int64_t>(n, (4 - (row & 3)) & 3);
+        body_end = head + ((n - head) & ~int64_t(3));
+    }
+    auto one = [&](int64_t i) {
+        const int64_t o = row + i;
+        float mm = m[o], vv = v[o], a;
+        raw[o] = adam_one(raw[o], g[o], mm, vv, k, lrk, b1, b2, eps, bc1, bc2, a);
         m[o] = mm;
         v[o] = vv;
-        const float nr = r - lrk * (mm / bc1) / (sqrtf(vv / bc2) + eps);
-        raw[o] = nr;
-        act[o] = (k >= 3 && k < 6) ? expf(nr) : (k == 10 ? 1.f / (1.f + expf(-nr)) : nr);
+        act[o] = a;
+    };
+    for (int64_t i = t0; i < head; i += stride) one(i);
+    if (!vec) return;
+    for (int64_t q = t0; head + 4 * q < body_end; q += stride) {
+        const int64_t o = row + head + 4 * q;
+        const float4 r4 = *reinterpret_cast<const float4*>(raw + o), g4 = *reinterpret_cast<const float4*>(g + o);
+        float4 m4 = *reinterpret_cast<const float4*>(m + o), v4 = *reinterpret_cast<const float4*>(v + o);
+        float4 nr, a4;
+        nr.x = adam_one(r4.x, g4.x, m4.x, v4.x, k, lrk, b1, b2, eps, bc1, bc2, a4.x);
+        nr.y = adam_one(r4.y, g4.y, m4.y, v4.y, k, lrk, b1, b2, eps, bc1, bc2, a4.y);
+        nr.z = adam_one(r4.z, g4.z, m4.z, v4.z, k, lrk, b1, b2, eps, bc1, bc2, a4.z);
+        nr.w = adam_one(r4.w, g4.w, m4.w, v4.w, k, lrk, b1, b2, eps, bc1, bc2, a4.w);
+        *reinterpret_cast<float4*>(raw + o) = nr;
+        *reinterpret_cast<float4*>(m + o) = m4;
+        *reinterpret_cast<float4*>(v + o) = v4;
+        *reinterpret_cast<float4*>(act + o) = a4;
     }
+    for (int64_t i = body_end + t0; i < n; i += stride) one(i);
 }
 
 void launch_adam(float* raw, float* act, const float* g, float* m, float* v, int64_t n, int64_t ld, const float* lr,
@@ -494,8 +526,12 @@ void launch_adam(float* raw, float* act, const float* g, float* m, float* v, int
     Lr14 l{};
     for (int k = 0; k < rows; ++k) l.v[k] = lr[k];
     const float bc1 = float(1.0 - std::pow(double(b1), step)), bc2 = float(1.0 - std::pow(double(b2), step));
-    dim3 grid(unsigned(std::min<int64_t>((n + 255) / 256, sm_count() * 2)), unsigned(rows));
-    adam_kernel<<<grid, 256, 0, st>>>(raw, act, g, m, v, n, ld, l, b1, b2, eps, bc1, bc2);
+    const bool vec = ((reinterpret_cast<uintptr_t>(raw) | reinterpret_cast<uintptr_t>(act) |
+                       reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(m) |
+                       reinterpret_cast<uintptr_t>(v)) & 15) == 0;
+    const int64_t work = vec ? (n + 3) / 4 : n;
+    dim3 grid(unsigned(std::min<int64_t>((work + 255) / 256, sm_count() * 2)), unsigned(rows));
+    adam_kernel<<<grid, 256, 0, st>>>(raw, act, g, m, v, n, ld, l, b1, b2, eps, bc1, bc2, vec);
 }
 
 // ------------------------------------------------------------------ pose step (reading C23)

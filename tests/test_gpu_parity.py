@@ -332,27 +332,38 @@ def test_loss_parity(W, H):
     assert abs(pipe.loss.item() - o["loss"]) <= 1e-6 * abs(o["loss"])
 
 
+def _offset_dev(a, shift):
+    """a on the device, its data pointer shifted by `shift` floats from the allocation's alignment"""
+    buf = torch.zeros(a.size + shift, device="cuda")
+    t = buf[shift:].view(a.shape)
+    t.copy_(torch.as_tensor(a, device="cuda"))
+    return t
+
+
 @pytest.mark.parametrize("rows", [14, 23])
-def test_adam_parity(rows):
-    """gs_adam_step (14 rows) and gs_adam_step_rows (23: degree-1 SH layout) against the fp64 oracle."""
+@pytest.mark.parametrize("n,ld,shift", [(1000, 1024, 0), (1001, 1027, 0), (999, 1024, 1)])
+def test_adam_parity(rows, n, ld, shift):
+    """gs_adam_step (14 rows) and gs_adam_step_rows (23: degree-1 SH layout) against the fp64 oracle;
+    16-byte aligned rows (float4 body), rows with ragged heads (ld % 4 != 0) and unaligned arrays
+    (element path)."""
     import paper_2311_11700_b200 as g
     rng = np.random.default_rng(3)
-    n, ld = 1000, 1024
     raw = rng.normal(size=(rows, ld)).astype(np.float32)
     lr = [1.6e-5] * 3 + [2e-4] * 3 + [4e-5] * 4 + [1e-2] + [5e-4] * (rows - 11)
-    R = to_dev(raw)
-    A = torch.zeros_like(R)
-    M = torch.zeros_like(R)
-    Vv = torch.zeros_like(R)
+    R = _offset_dev(raw, shift)
+    A = _offset_dev(np.zeros_like(raw), shift)
+    M = _offset_dev(np.zeros_like(raw), shift)
+    Vv = _offset_dev(np.zeros_like(raw), shift)
     m = np.zeros((rows, n))
     vv = np.zeros((rows, n))
     r64 = raw[:, :n].astype(np.float64)
     for step in (1, 2, 3):
         gr = rng.normal(size=(rows, ld)).astype(np.float32)
+        G = _offset_dev(gr, shift)
         if rows == 14:
-            g.gs_adam_step(R, A, to_dev(gr), M, Vv, n, ld, lr, step)
+            g.gs_adam_step(R, A, G, M, Vv, n, ld, lr, step)
         else:
-            g.gs_adam_step_rows(R, A, to_dev(gr), M, Vv, n, ld, rows, lr, step)
+            g.gs_adam_step_rows(R, A, G, M, Vv, n, ld, rows, lr, step)
         out = oracle.adam_step(r64, gr[:, :n], m, vv, lr, step)
         r64, m, vv = out["raw"], out["m"], out["v"]
     torch.cuda.synchronize()
