@@ -14,6 +14,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # GS_DEBUG=1 loads the debug build (output invariant checks after every stage, csrc/debug.cu)
 DEBUG = os.environ.get("GS_DEBUG", "0") == "1"
 LIB_PATH = os.path.join(_HERE, "libgs_debug.so" if DEBUG else "libgs.so")
+# GS_LIB: an explicit library path (A/B experiments, tools/variant_build.py)
+LIB_PATH = os.environ.get("GS_LIB") or LIB_PATH
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{os.path.basename(LIB_PATH)} not built at {LIB_PATH}: run `python -m paper_2311_11700_b200.build` "

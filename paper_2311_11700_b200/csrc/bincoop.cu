@@ -270,9 +270,12 @@ __global__ void __launch_bounds__(kCT, 1) bin_coop_kernel(CoopArgs a) {
             }
             __syncthreads();
         }
+        // per-warp digit counts wh[warp][digit] are zero between rounds: the scan below rewrites only
+        // the non-zero entries and each warp's leader lanes clear their own entries after the
+        // scatter, so a round needs no clearing pass and two block barriers
+        for (int i = tid; i < (kCW << dbits); i += kCT) wh[(i >> dbits) * kCoopBins + (i & int(dmask))] = 0u;
+        __syncthreads();
         for (uint32_t r0 = s0; r0 < s1; r0 += kCT) {
-            for (int i = tid; i < (kCW << dbits); i += kCT) wh[(i >> dbits) * kCoopBins + (i & int(dmask))] = 0u;
-            __syncthreads();
             const uint32_t idx = r0 + tid;
             const bool ok = idx < s1;
             const uint32_t key = ok ? ldcg(kin + idx) : 0u;
@@ -280,19 +283,22 @@ __global__ void __launch_bounds__(kCT, 1) bin_coop_kernel(CoopArgs a) {
             const uint32_t dg = ok ? (key >> shift) & dmask : nbins;   // nbins: sentinel digit
             const uint32_t peers = __match_any_sync(0xffffffffu, dg);
             const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
-            if (ok && lane == __ffs(peers) - 1) wh[warp * kCoopBins + dg] = __popc(peers);
-            __syncthreads();
+            const bool leader = ok && lane == __ffs(peers) - 1;
+            if (leader) wh[warp * kCoopBins + dg] = __popc(peers);
+            __syncthreads();   // [R] counts complete (and the previous round's scatter done)
             for (uint32_t d = tid; d < nbins; d += kCT) {   // per digit: exclusive over warps + running
+                uint32_t c[kCW];
+#pragma unroll
+                for (int w = 0; w < kCW; ++w) c[w] = wh[w * kCoopBins + d];
                 uint32_t run = s_run[d];
-#pragma unroll 8
+#pragma unroll
                 for (int w = 0; w < kCW; ++w) {
-                    const uint32_t c = wh[w * kCoopBins + d];
-                    wh[w * kCoopBins + d] = run;
-                    run += c;
+                    if (c[w]) wh[w * kCoopBins + d] = run;
+                    run += c[w];
                 }
                 s_run[d] = run;
             }
-            __syncthreads();
+            __syncthreads();   // [S] offsets complete
             if (ok) {
                 const uint32_t pos = s_gpos[dg] + wh[warp * kCoopBins + dg] + rank;
                 if (last) {
@@ -305,7 +311,9 @@ __global__ void __launch_bounds__(kCT, 1) bin_coop_kernel(CoopArgs a) {
                     atomicAdd(a.H + (size_t(p + 1) * kCoopGridMax + pos / S2) * kCoopBins + dn, 1u);
                 }
             }
-            __syncthreads();
+            __syncwarp();   // every lane of the warp has read its entry
+            if (leader) wh[warp * kCoopBins + dg] = 0u;
+            // the next round's [R] orders these clears and this round's reads before the next scan
         }
         grid_sync(&misc->coop_bar, goal);
     }
