@@ -27,9 +27,10 @@ def main():
     flags = g.GS_FLAG_NO_HOST_SYNC
     hp = P.cpu().pin_memory()
     hv, htc, htd = V.cpu().pin_memory(), tc.cpu().pin_memory(), td.cpu().pin_memory()
-    hgrad = [torch.empty_like(grad, device="cpu").pin_memory() for _ in range(2)]
+    NB = int(os.environ.get("E2E_NB", "2"))   # buffer sets in rotation
+    hgrad = [torch.empty_like(grad, device="cpu").pin_memory() for _ in range(NB)]
     bufs = [(torch.empty_like(P), torch.empty_like(V), torch.empty_like(tc), torch.empty_like(td),
-             torch.empty_like(grad), torch.empty_like(gpose)) for _ in range(2)]
+             torch.empty_like(grad), torch.empty_like(gpose)) for _ in range(NB)]
     for b in bufs:
         b[0].copy_(P), b[1].copy_(V), b[2].copy_(tc), b[3].copy_(td)
     s_up, s_down = torch.cuda.Stream(), torch.cuda.Stream()
@@ -42,9 +43,9 @@ def main():
         d, s_ = dst.view(-1), src.view(-1)
         for o in range(0, d.numel(), CH):
             d[o:o + CH].copy_(s_[o:o + CH], non_blocking=True)
-    ev_c = [torch.cuda.Event() for _ in range(2)]
-    ev_d = [torch.cuda.Event() for _ in range(2)]
-    ev_r = [torch.cuda.Event() for _ in range(2)]
+    ev_c = [torch.cuda.Event() for _ in range(NB)]
+    ev_d = [torch.cuda.Event() for _ in range(NB)]
+    ev_r = [torch.cuda.Event() for _ in range(NB)]
 
     def graph_of(b):
         Pd, Vd, tcd, tdd, gd, gpd = b
@@ -70,27 +71,27 @@ def main():
             e.record(cur)
 
         def upload(i):
-            b = bufs[i % 2]
+            b = bufs[i % NB]
             with torch.cuda.stream(s_up):
-                s_up.wait_event(ev_d[i % 2])
+                s_up.wait_event(ev_d[i % NB])
                 if up:
                     for dst, src in zip(b[:4], (hp, hv, htc, htd)):
                         chunked(dst, src)
-                ev_c[i % 2].record(s_up)
+                ev_c[i % NB].record(s_up)
         upload(0)
         for i in range(steps):
             if i + 1 < steps:
                 upload(i + 1)
-            cur.wait_event(ev_c[i % 2])
-            cur.wait_event(ev_r[i % 2])
+            cur.wait_event(ev_c[i % NB])
+            cur.wait_event(ev_r[i % NB])
             if comp:
-                its[i % 2]()
-            ev_d[i % 2].record(cur)
+                its[i % NB]()
+            ev_d[i % NB].record(cur)
             with torch.cuda.stream(s_down):
-                s_down.wait_event(ev_d[i % 2])
+                s_down.wait_event(ev_d[i % NB])
                 if down:
-                    chunked(hgrad[i % 2], bufs[i % 2][4])
-                ev_r[i % 2].record(s_down)
+                    chunked(hgrad[i % NB], bufs[i % NB][4])
+                ev_r[i % NB].record(s_down)
         cur.wait_stream(s_down)
 
     for name, kw in (("full", {}), ("no read-back", {"down": False}), ("no upload", {"up": False}),
