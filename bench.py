@@ -779,19 +779,43 @@ def main_mapping(args):
         ms = timed(mp.step, args.steps)
     clocks = clk.summary()
     # e2e: every step uploads its local keyframes' RGB-D targets and poses from pinned host memory
-    # and reads back the loss and the map size (the step's result)
+    # and reads back the loss and the map size (the step's result). Two device sets of the keyframe
+    # inputs alternate: step i+1's upload (copy stream) overlaps step i's kernels; all of it inside
+    # the timed region.
     mine = [kfs[k] for k in mp.local]
     host = [(kf.view.cpu().pin_memory(), kf.color.cpu().pin_memory(), kf.depth.cpu().pin_memory()) for kf in mine]
+    sets = [[(torch.empty_like(kf.view), torch.empty_like(kf.color), torch.empty_like(kf.depth)) for kf in mine]
+            for _ in range(2)]
     res = torch.empty(2, dtype=torch.float64).pin_memory()
+    s_up = torch.cuda.Stream(device=dev)
+    ev_up = [torch.cuda.Event() for _ in range(2)]
+    ev_used = [torch.cuda.Event() for _ in range(2)]
+    for e in ev_used:
+        e.record()
 
-    def e2e_step():
-        for kf, (hv, hc, hd) in zip(mine, host):
-            kf.view.copy_(hv, non_blocking=True)
-            kf.color.copy_(hc, non_blocking=True)
-            kf.depth.copy_(hd, non_blocking=True)
-        mp.step()
-        res.copy_(torch.stack([mp.pipe.loss.reshape(-1)[0], mp.n_dev[0].to(torch.float64)]), non_blocking=True)
-    ms_e2e = timed(e2e_step, args.steps)
+    def upload(i):
+        with torch.cuda.stream(s_up):
+            s_up.wait_event(ev_used[i % 2])   # the step that last read this set is done
+            for dst, src in zip(sets[i % 2], host):
+                for d, h in zip(dst, src):
+                    d.copy_(h, non_blocking=True)
+            ev_up[i % 2].record(s_up)
+
+    def e2e_run(steps):
+        cur = torch.cuda.current_stream()
+        s_up.wait_stream(cur)   # the first upload starts inside the timed region
+        upload(0)
+        for i in range(steps):
+            if i + 1 < steps:
+                upload(i + 1)
+            cur.wait_event(ev_up[i % 2])
+            for kf, (dv, dc, dd) in zip(mine, sets[i % 2]):
+                kf.view, kf.color, kf.depth = dv, dc, dd
+            mp.step()
+            ev_used[i % 2].record(cur)
+            res.copy_(torch.stack([mp.pipe.loss.reshape(-1)[0], mp.n_dev[0].to(torch.float64)]), non_blocking=True)
+    e2e_run(2)
+    ms_e2e = timed(lambda: e2e_run(args.steps), 1) / args.steps
     h2d = sum(a.numel() * a.element_size() for t in host for a in t)
     out = {"metric": METRIC, "value": 1000.0 / ms, "unit": "mapping iters/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -805,8 +829,9 @@ def main_mapping(args):
                                       else "1 GPU"),
                       "l2": "per-keyframe working set > L2; no flush"},
            "keyframe_renders_per_s": len(kfs) * 1000.0 / ms, "clocks": clocks, "gpu_launches": launches,
-           "e2e": {"value": 1000.0 / ms_e2e, "unit": "mapping iters/s", "h2d_bytes_per_step": int(h2d),
-                   "d2h_bytes_per_step": 16}}
+           "e2e": {"value": 1000.0 / ms_e2e, "unit": "mapping iters/s",
+                   "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 16,
+                   "overlap": "two device sets of the keyframe inputs; step i+1's upload overlaps step i"}}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if dist:
