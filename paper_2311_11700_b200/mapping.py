@@ -1,7 +1,7 @@
 """Keyframe-sharded multi-GPU mapping (BASELINE config 4).
 
 One process per GPU; each rank holds a full replica of the map and renders ITS keyframes:
-  per local keyframe:  gs_project -> gs_bin_sort -> gs_render_fwd -> gs_loss_l1 -> gs_render_bwd (+=)
+  per local keyframe:  gs_project -> gs_bin_sort -> gs_render_fwd -> gs_render_bwd_l1 (+=; the L1 loss fused)
   exchange:            all_reduce(sum) of grad[rows][:n] over NCCL (NVLink 5 / NVSwitch): the live columns
                        packed into one contiguous buffer, one collective
   optimiser:           gs_adam_step (identical on every rank -> parameters stay bitwise equal)
@@ -29,8 +29,9 @@ import torch
 import torch.distributed as dist
 
 from . import (GS_DENSIFY_ADD, GS_DENSIFY_DEGENERATE_APPLY, GS_DENSIFY_DEGENERATE_FLAG, GS_DENSIFY_PRUNE,
-               GS_FLAG_NO_HOST_SYNC, densify_cfg, gs_adam_step, gs_adam_step_rows, gs_densify_accum_grad,
-               gs_densify_append, gs_densify_prune, gs_densify_split_clone, gs_pose_step, make_camera)
+               GS_FLAG_NO_HOST_SYNC, GS_FLAG_POSE_COV_PATH, densify_cfg, gs_adam_step, gs_adam_step_rows,
+               gs_densify_accum_grad, gs_densify_append, gs_densify_prune, gs_densify_split_clone, gs_pose_step,
+               gs_render_bwd_l1, make_camera)
 from .pipeline import RenderPipeline
 
 
@@ -246,12 +247,15 @@ class ShardedMapper:
                                  None, kf.view, self.cm, densify_cfg(GS_DENSIFY_DEGENERATE_FLAG,
                                                                      gamma=self.degenerate[1]),
                                  self.dmask, None, self.pipe.ws)
-            dc, dd = self.pipe.loss_l1(self.cam, kf.color, kf.depth, self.w_color, self.w_depth)
             gp = None
             if self.poses_active():
                 gp = self.gpose[j]
                 gp.zero_()
-            self.pipe.backward(self.P, self.n, kf.view, self.cam, dc, dd, self.grad, gp)
+            # L1 (Eq. 6) formed inside the backward's pixel loads (gs_render_bwd_l1): no dL/dC, dL/dD images
+            color, depth, _ = self.pipe._imgs(self.cam)
+            gs_render_bwd_l1(self.P, self.n, self.P.shape[1], kf.view, self.pipe.ws, self.cm, color, depth, kf.color,
+                             kf.depth, self.w_color, self.w_depth, self.grad, gp, self.pipe.loss,
+                             GS_FLAG_POSE_COV_PATH)
             if self.split is not None:   # reading C30 statistics of this view (NDC mean-gradient norm)
                 gs_densify_accum_grad(self.pipe.ws, self.acc, self.cnt)
             if self.densify:   # Eq. 8 candidates from this keyframe's render (gather mode)

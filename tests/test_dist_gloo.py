@@ -30,10 +30,11 @@ def _mapping_module():
             stub = types.ModuleType("paper_2311_11700_b200")
             stub.__path__ = [os.path.join(ROOT, "paper_2311_11700_b200")]
             for name in ("GS_DENSIFY_ADD", "GS_DENSIFY_PRUNE", "GS_FLAG_NO_HOST_SYNC", "GS_DENSIFY_DEGENERATE_APPLY",
-                         "GS_DENSIFY_DEGENERATE_FLAG"):
+                         "GS_DENSIFY_DEGENERATE_FLAG", "GS_FLAG_POSE_COV_PATH"):
                 setattr(stub, name, 0)
             for name in ("densify_cfg", "gs_adam_step", "gs_adam_step_rows", "gs_densify_append", "gs_densify_prune",
-                         "make_camera", "gs_densify_accum_grad", "gs_densify_split_clone", "gs_pose_step"):
+                         "make_camera", "gs_densify_accum_grad", "gs_densify_split_clone", "gs_pose_step",
+                         "gs_render_bwd_l1"):
                 setattr(stub, name, None)
             sys.modules["paper_2311_11700_b200"] = stub
             pl = types.ModuleType("paper_2311_11700_b200.pipeline")
