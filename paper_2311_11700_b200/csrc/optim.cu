@@ -107,7 +107,7 @@ void launch_loss_l1(WsState* s, const float* color, const float* depth, const fl
                     int32_t H, float wc, float wd, float* dc, float* dd, double* loss, cudaStream_t st) {
     Misc* misc = at<Misc>(s, s->misc);
     const int64_t npx = int64_t(W) * H;
-    cudaMemsetAsync(misc->loss_acc, 0, sizeof(misc->loss_acc), st);
+    launch_zero(misc->loss_acc, sizeof(misc->loss_acc), st);
     auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
     const bool v4 = npx % 4 == 0 && aligned(color) && aligned(depth) && aligned(tc) && aligned(td) && aligned(dc) &&
                     aligned(dd);
@@ -342,10 +342,10 @@ void launch_loss_l1_masked(WsState* s, const float* color, const float* depth, c
                            float* dc, float* dd, double* loss, cudaStream_t st) {
     Misc* misc = at<Misc>(s, s->misc);
     const int64_t npx = int64_t(W) * H;
-    cudaMemsetAsync(misc->loss_acc, 0, sizeof(misc->loss_acc), st);
+    launch_zero(misc->loss_acc, sizeof(misc->loss_acc), st);
     if (outlier_k > 0.f) {
         RobustScratch* rs = at<RobustScratch>(s, s->coop);
-        cudaMemsetAsync(rs, 0, sizeof(RobustScratch), st);
+        launch_zero(rs, sizeof(RobustScratch), st);
         const int grid = coop_sm_count();
         if (grid <= 0) return;   // check_launch reports the device error
         int64_t n = npx;
@@ -393,7 +393,7 @@ __global__ void frame_stats_kernel(const float* __restrict__ alpha, const float*
 
 void launch_frame_stats(const float* alpha, const float* depth, const float* td, int32_t W, int32_t H, float ta,
                         float tdep, uint32_t* counts, cudaStream_t st) {
-    cudaMemsetAsync(counts, 0, 3 * sizeof(uint32_t), st);
+    launch_zero(counts, 3 * sizeof(uint32_t), st);
     const int64_t npx = int64_t(W) * H;
     frame_stats_kernel<<<int(std::min<int64_t>((npx + 255) / 256, sm_count() * 2)), 256, 0, st>>>(alpha, depth, td, npx, ta,
                                                                                            tdep, counts);
@@ -461,6 +461,17 @@ void launch_image_half(const float* c, const float* d, int32_t W, int32_t H, flo
 
 void launch_pose_extrapolate(const float* t1, const float* t2, float* out, cudaStream_t st) {
     pose_extrapolate_kernel<<<1, 32, 0, st>>>(t1, t2, out);
+}
+
+__global__ void zero_u32_kernel(uint32_t* __restrict__ p, size_t nw) {
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nw; i += size_t(gridDim.x) * blockDim.x) p[i] = 0u;
+}
+
+void launch_zero(void* p, size_t bytes, cudaStream_t st) {
+    const size_t nw = bytes / 4;
+    if (nw == 0) return;
+    const int blocks = int(std::min<size_t>((nw + 255) / 256, 64));
+    zero_u32_kernel<<<blocks, 256, 0, st>>>(static_cast<uint32_t*>(p), nw);
 }
 
 // ------------------------------------------------------------------ Adam
@@ -863,7 +874,7 @@ void compact_inplace(WsState* s, float* const arrays[4], int rows, int64_t ld, i
     const int nt = int((std::max<int64_t>(capacity, 1) + kCmp - 1) / kCmp);
     uint32_t* counts = at<uint32_t>(s, s->cmp);
     uint32_t* ctl = counts + (nt + 2);
-    cudaMemsetAsync(ctl, 0, size_t(nt + 1) * 4, st);
+    launch_zero(ctl, size_t(nt + 1) * 4, st);
     count256_kernel<<<nt, kCmp, 0, st>>>(n_dev, pred, counts);
     scan_blocks_kernel<<<1, 1024, 0, st>>>(counts, nt, kept);
     if (rows == 23)
