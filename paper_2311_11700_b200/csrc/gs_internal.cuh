@@ -91,7 +91,7 @@ struct Misc {
     unsigned int prep_done;        // bwd_prep_kernel last-block ticket (self-resetting)
     unsigned int tile_pose_done;   // pose-only tile pass last-block ticket (self-resetting)
     unsigned int debug_flag;       // debug builds: violated checks (debug.cu), cleared when reported
-    unsigned int pad;
+    unsigned int gbwd_zero_chunk;  // gaussian_bwd: off-screen zeroing chunks claimed (reset by the bwd prologue)
 };
 
 // Programmatic dependent launch (PDL): kernels of the iteration are launched with programmatic

@@ -953,8 +953,9 @@ __global__ void __launch_bounds__(256) zero_sgrad_kernel(float* __restrict__ sgr
                                                          const uint32_t* __restrict__ live_cnt, int T,
                                                          uint32_t* __restrict__ order, const float* __restrict__ td,
                                                          int64_t npx, uint32_t* __restrict__ part, double* acc,
-                                                         unsigned int* ticket) {
+                                                         unsigned int* ticket, unsigned int* zero_chunk) {
     griddep_wait();   // PDL (gs_internal.cuh)
+    if (blockIdx.x == 0 && threadIdx.x == 0) *zero_chunk = 0u;   // gaussian_bwd's zeroing chunk counter
     // block 0 also builds the backward's LPT tile order from the forward's live-list lengths
     if (blockIdx.x == 0) lpt_tile_order<256>([&](int t) { return live_cnt[t]; }, T, order);
     const int64_t V = n_on ? int64_t(*n_on) : 0;   // nullptr: no clear (the pose-only paper-mode pass)
@@ -1013,7 +1014,8 @@ void launch_zero_sgrad(WsState* s, cudaStream_t st, const float* td_l1, int64_t 
                                                    clear ? &misc->n_onscreen : nullptr,
                                                    at<uint32_t>(s, s->live_cnt), s->cam_gx * s->cam_gy,
                                                    at<uint32_t>(s, s->tile_order), td_l1, npx,
-                                                   at<uint32_t>(s, s->chunk_hist), misc->loss_acc, &misc->prep_done);
+                                                   at<uint32_t>(s, s->chunk_hist), misc->loss_acc, &misc->prep_done,
+                                                   &misc->gbwd_zero_chunk);
 }
 
 __global__ void loss_finalize_kernel(const double* acc, int64_t npx, float wc, float wd, double* loss) {
@@ -1096,7 +1098,7 @@ __global__ void __launch_bounds__(256, kGbwdBlocksPerSM) gaussian_bwd_kernel(
     const uint32_t* __restrict__ onlist, const unsigned int* __restrict__ n_on, const float4* __restrict__ rec,
     const float* __restrict__ sgrad, int64_t sld, float* __restrict__ grad, int cov_path,
     double* __restrict__ pose_part, unsigned int* done_ctr, double* __restrict__ grad_pose, LossFin lf,
-    const uint32_t* __restrict__ tiles, int zero_blocks) {
+    const uint32_t* __restrict__ tiles, unsigned int* zero_chunk) {
     griddep_wait();   // PDL (gs_internal.cuh)
     constexpr bool assign = ASSIGN;
     __shared__ float V[12];
@@ -1108,16 +1110,8 @@ __global__ void __launch_bounds__(256, kGbwdBlocksPerSM) gaussian_bwd_kernel(
     for (int k = 0; k < kPoseSums; ++k) pose[k] = 0.f;
     const int64_t Von = int64_t(*n_on);
     // thread t handles the t-th on-screen Gaussians (index order); off-screen ones have zero gradient
-    // GS_FLAG_GRAD_ASSIGN: the last zero_blocks blocks write the off-screen columns' zero gradients,
-    // concurrently with the compute blocks (they then join the pose epilogue with zero partials)
-    const int compute_blocks = int(gridDim.x) - zero_blocks;
-    if (ASSIGN && int(blockIdx.x) >= compute_blocks) {
-        const int rows = SH == 1 ? 23 : 14;
-        for (int64_t i = int64_t(blockIdx.x - compute_blocks) * blockDim.x + threadIdx.x; i < n;
-             i += int64_t(zero_blocks) * blockDim.x)
-            if (tiles[i] == 0u)
-                for (int k = 0; k < rows; ++k) grad[k * ld + i] = 0.f;
-    }
+    // (GS_FLAG_GRAD_ASSIGN: written after the items, below)
+    const int compute_blocks = int(gridDim.x);
     // the next item's Gaussian index is loaded one item ahead, so an item's parameter loads do not
     // wait for its index load first (one DRAM round trip per item instead of two)
     const int64_t tstride = int64_t(compute_blocks) * blockDim.x;
@@ -1295,6 +1289,25 @@ __global__ void __launch_bounds__(256, kGbwdBlocksPerSM) gaussian_bwd_kernel(
             }
         }
     }
+    if (ASSIGN && grad) {
+        // off-screen columns get zero gradients: 2048-column chunks claimed from a counter, so blocks
+        // with fewer items above take more chunks (a second wave of zeroing-only blocks would run
+        // after the items: the grid is one wave at 2 blocks per SM)
+        constexpr int kZeroChunk = 2048;
+        const int rows = SH == 1 ? 23 : 14;
+        __shared__ unsigned int s_chunk;
+        for (;;) {
+            if (threadIdx.x == 0) s_chunk = atomicAdd(zero_chunk, 1u);
+            __syncthreads();
+            const int64_t c0 = int64_t(s_chunk) * kZeroChunk;
+            __syncthreads();   // s_chunk read by every thread before the next claim
+            if (c0 >= n) break;
+            const int64_t c1 = c0 + kZeroChunk < n ? c0 + kZeroChunk : n;
+            for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x)
+                if (tiles[i] == 0u)
+                    for (int k = 0; k < rows; ++k) grad[k * ld + i] = 0.f;
+        }
+    }
     if (pose_part) {   // per-block partial sums (fp64), reduced in a fixed order by the last block
         __shared__ double red[8][kPoseSums];
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1366,14 +1379,13 @@ void launch_gaussian_bwd(WsState* s, const float* params, int64_t n, int64_t ld,
     const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(sms) * kGbwdBlocksPerSM));
     KTimer kt(s, KID_BWD_GAUSS, st);
     const int assign = (flags & GS_FLAG_GRAD_ASSIGN) ? 1 : 0;
-    const int zero_blocks = (assign && grad_params) ? std::min(sms, int((n + 255) / 256)) : 0;
     auto kern = s->sh_degree == 1 ? (assign ? gaussian_bwd_kernel<1, true> : gaussian_bwd_kernel<1, false>)
                                   : (assign ? gaussian_bwd_kernel<0, true> : gaussian_bwd_kernel<0, false>);
-    launch_pdl(kern, dim3(blocks + zero_blocks), dim3(256), 0, st,
+    launch_pdl(kern, dim3(blocks), dim3(256), 0, st,
         params, n, ld, viewmat, cam, at<uint32_t>(s, s->onlist), &at<Misc>(s, s->misc)->n_onscreen,
         at<float4>(s, s->rec), at<float>(s, s->sgrad), s->n_cap, grad_params, (flags & GS_FLAG_POSE_COV_PATH) ? 1 : 0,
         part, &at<Misc>(s, s->misc)->pose_done, grad_pose, part ? lf : LossFin{}, at<uint32_t>(s, s->tiles),
-        zero_blocks);
+        &at<Misc>(s, s->misc)->gbwd_zero_chunk);
 }
 
 }  // namespace gs
