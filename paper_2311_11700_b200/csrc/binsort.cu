@@ -217,10 +217,10 @@ static int ceil_log2(uint32_t v) { int b = 0; while ((1u << b) < v) ++b; return 
 gs_status chained_scan(WsState* s, const uint32_t* in, uint32_t* out, int64_t n, unsigned long long* total,
                        cudaStream_t st, int64_t cap, unsigned long long* total_eff) {
     Misc* misc = at<Misc>(s, s->misc);
-    launch_zero(total, sizeof(*total), st);
-    if (total_eff) launch_zero(total_eff, sizeof(*total_eff), st);
+    launch_zero(total, sizeof(*total), st, s);
+    if (total_eff) launch_zero(total_eff, sizeof(*total_eff), st, s);
     if (n == 0) return GS_OK;
-    launch_zero(&misc->scan_counter, sizeof(misc->scan_counter), st);
+    launch_zero(&misc->scan_counter, sizeof(misc->scan_counter), st, s);
     const uint32_t epoch = uint32_t(++s->epoch) & 0x3fffffffu;
     const int parts = int((n + kScanTile - 1) / kScanTile);
     KTimer kt(s, KID_SCAN, st);
@@ -234,10 +234,10 @@ gs_status chained_scan(WsState* s, const uint32_t* in, uint32_t* out, int64_t n,
 // dkey_sorted / dval_sorted (first half); V_s in misc->n_onscreen and misc->n_items.
 gs_status run_compact_onscreen(WsState* s, cudaStream_t st) {
     Misc* misc = at<Misc>(s, s->misc);
-    launch_zero(&misc->n_onscreen, sizeof(misc->n_onscreen), st);
-    launch_zero(&misc->n_items, sizeof(misc->n_items), st);
+    launch_zero(&misc->n_onscreen, sizeof(misc->n_onscreen), st, s);
+    launch_zero(&misc->n_items, sizeof(misc->n_items), st, s);
     if (s->n == 0) return GS_OK;
-    launch_zero(&misc->scan_counter, sizeof(misc->scan_counter), st);
+    launch_zero(&misc->scan_counter, sizeof(misc->scan_counter), st, s);
     const uint32_t epoch = uint32_t(++s->epoch) & 0x3fffffffu;
     const int parts = int((s->n + kScanTile - 1) / kScanTile);
     KTimer kt(s, KID_DEPTH_SORT, st);
@@ -273,8 +273,8 @@ int ceil_log2_tiles(int64_t ntiles) { return ceil_log2(uint32_t(ntiles)); }
 gs_status run_bin_sort_keys(WsState* s, int64_t* n_keys, uint32_t flags, cudaStream_t st) {
     Misc* misc = at<Misc>(s, s->misc);
     const int64_t ntiles = int64_t(s->cam_gx) * s->cam_gy;
-    launch_zero(misc, offsetof(Misc, loss_acc), st);                 // K, flags, tickets
-    launch_zero(at<char>(s, s->ranges), size_t(ntiles) * sizeof(uint2), st);
+    launch_zero(misc, offsetof(Misc, loss_acc), st, s);                 // K, flags, tickets
+    launch_zero(at<char>(s, s->ranges), size_t(ntiles) * sizeof(uint2), st, s);
     gs_status rc = chained_scan(s, at<uint32_t>(s, s->tiles), at<uint32_t>(s, s->offsets), s->n, &misc->n_keys, st,
                                 s->key_cap, &misc->n_keys_eff);
     if (rc != GS_OK) return rc;

@@ -206,7 +206,7 @@ gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaS
     Misc* misc = at<Misc>(s, s->misc);
     const int T = s->cam_gx * s->cam_gy;
     const int64_t n = s->n;
-    launch_zero(misc, offsetof(Misc, loss_acc), st);   // K, flags, barrier, key range
+    launch_zero(misc, offsetof(Misc, loss_acc), st, s);   // K, flags, barrier, key range
     gs_status rc = GS_OK;
     if (n > 0) {
         rc = run_bin_coop(s, st);   // B1-B4: compaction, depth sort, chunk counts, tile scans
@@ -221,7 +221,7 @@ gs_status run_bin_sort_bucket(WsState* s, int64_t* n_keys, uint32_t flags, cudaS
                                                  &misc->n_keys, s->cam_gx, s->cam_gy, at<uint32_t>(s, s->vals0),
                                                  at<uint2>(s, s->ranges));
     } else {
-        launch_zero(at<char>(s, s->ranges), size_t(T) * sizeof(uint2), st);
+        launch_zero(at<char>(s, s->ranges), size_t(T) * sizeof(uint2), st, s);
     }
     s->sorted_in_1 = 0;
     s->keys_valid = 0;

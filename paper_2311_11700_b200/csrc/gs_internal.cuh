@@ -142,7 +142,7 @@ __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
 // Zero `bytes` (a multiple of 4, 4-byte aligned) on stream st with a small kernel rather than
 // cudaMemsetAsync: inside the iteration's CUDA graph a memset node measured ~3 us slower per
 // iteration than a kernel node (optim.cu)
-void launch_zero(void* p, size_t bytes, cudaStream_t st);
+void launch_zero(void* p, size_t bytes, cudaStream_t st, WsState* s = nullptr);   // s: counts the launch
 // debug library (-DGS_DEBUG=1): output invariant checks after each stage (debug.cu)
 void set_error_text(const char* msg);
 gs_status dbg_after_project(WsState* s, cudaStream_t st);

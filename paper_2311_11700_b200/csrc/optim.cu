@@ -107,7 +107,7 @@ void launch_loss_l1(WsState* s, const float* color, const float* depth, const fl
                     int32_t H, float wc, float wd, float* dc, float* dd, double* loss, cudaStream_t st) {
     Misc* misc = at<Misc>(s, s->misc);
     const int64_t npx = int64_t(W) * H;
-    launch_zero(misc->loss_acc, sizeof(misc->loss_acc), st);
+    launch_zero(misc->loss_acc, sizeof(misc->loss_acc), st, s);
     auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
     const bool v4 = npx % 4 == 0 && aligned(color) && aligned(depth) && aligned(tc) && aligned(td) && aligned(dc) &&
                     aligned(dd);
@@ -342,10 +342,10 @@ void launch_loss_l1_masked(WsState* s, const float* color, const float* depth, c
                            float* dc, float* dd, double* loss, cudaStream_t st) {
     Misc* misc = at<Misc>(s, s->misc);
     const int64_t npx = int64_t(W) * H;
-    launch_zero(misc->loss_acc, sizeof(misc->loss_acc), st);
+    launch_zero(misc->loss_acc, sizeof(misc->loss_acc), st, s);
     if (outlier_k > 0.f) {
         RobustScratch* rs = at<RobustScratch>(s, s->coop);
-        launch_zero(rs, sizeof(RobustScratch), st);
+        launch_zero(rs, sizeof(RobustScratch), st, s);
         const int grid = coop_sm_count();
         if (grid <= 0) return;   // check_launch reports the device error
         int64_t n = npx;
@@ -467,9 +467,10 @@ __global__ void zero_u32_kernel(uint32_t* __restrict__ p, size_t nw) {
     for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nw; i += size_t(gridDim.x) * blockDim.x) p[i] = 0u;
 }
 
-void launch_zero(void* p, size_t bytes, cudaStream_t st) {
+void launch_zero(void* p, size_t bytes, cudaStream_t st, WsState* s) {
     const size_t nw = bytes / 4;
     if (nw == 0) return;
+    if (s) s->launches += 1;
     const int blocks = int(std::min<size_t>((nw + 255) / 256, 64));
     zero_u32_kernel<<<blocks, 256, 0, st>>>(static_cast<uint32_t*>(p), nw);
 }
@@ -874,7 +875,7 @@ void compact_inplace(WsState* s, float* const arrays[4], int rows, int64_t ld, i
     const int nt = int((std::max<int64_t>(capacity, 1) + kCmp - 1) / kCmp);
     uint32_t* counts = at<uint32_t>(s, s->cmp);
     uint32_t* ctl = counts + (nt + 2);
-    launch_zero(ctl, size_t(nt + 1) * 4, st);
+    launch_zero(ctl, size_t(nt + 1) * 4, st, s);
     count256_kernel<<<nt, kCmp, 0, st>>>(n_dev, pred, counts);
     scan_blocks_kernel<<<1, 1024, 0, st>>>(counts, nt, kept);
     if (rows == 23)

@@ -33,7 +33,7 @@ def test_default_line_schema():
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "clocks", "gpu_launches", "e2e", "roofline"):
         assert k in d, k
-    assert d["n_gpus"] == 1 and d["steps"] == 5 and d["value"] > 0 and d["gpu_launches"] == 7
+    assert d["n_gpus"] == 1 and d["steps"] == 5 and d["value"] > 0 and d["gpu_launches"] == 8   # zero, project, bin_coop, emit, fwd, prologue, bwd tiles, gaussian_bwd
     assert d["config"]["workload"].startswith("config 2")
     for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
         assert k in d["roofline"], k
