@@ -2,8 +2,9 @@
 
 One process per GPU; each rank holds a full replica of the map and renders ITS keyframes:
   per local keyframe:  gs_project -> gs_bin_sort -> gs_render_fwd -> gs_render_bwd_l1 (+=; the L1 loss fused)
-  exchange:            all_reduce(sum) of grad[rows][:n] over NCCL (NVLink 5 / NVSwitch): the live columns
-                       packed into one contiguous buffer, one collective
+  exchange:            all_reduce(sum) of the live columns grad[rows][:n] over NCCL (NVLink 5 /
+                       NVSwitch) in 4 column buckets, each packed contiguously; each bucket's Adam step
+                       overlaps the next buckets' reductions (allreduce_adam)
   optimiser:           gs_adam_step (identical on every rank -> parameters stay bitwise equal)
   adaptive expansion:  gs_densify_prune(ADD, gather mode) per local keyframe (Eq. 8)
                        -> all_gather of candidate counts and padded candidates (rank order)
@@ -83,6 +84,43 @@ def allreduce_grads(grad: torch.Tensor, n: int | None = None, group=None, packed
     buf.copy_(grad[:, :n])
     dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
     grad[:, :n].copy_(buf)
+
+
+def column_chunks(n: int, chunks: int, align: int = 32) -> list[tuple[int, int]]:
+    """[0, n) split into <= chunks column ranges whose starts are multiples of `align` (16-byte aligned
+    rows for the Adam kernel's vector path)."""
+    if n <= 0:
+        return []
+    w = max(align, -(-((n + chunks - 1) // chunks) // align) * align)
+    return [(c0, min(n, c0 + w)) for c0 in range(0, n, w)]
+
+
+def allreduce_adam(grad: torch.Tensor, n: int, adam, group=None, packed: torch.Tensor | None = None,
+                   chunks: int = 4) -> None:
+    """The gradient exchange overlapped with the optimiser (bucketed overlap): the
+    live columns [0, n) in `chunks` column ranges; each range is packed into its own slice of `packed`
+    and its sum all_reduce issued asynchronously (the collectives run in issue order on the
+    communicator's stream), then, range by range, the step waits for that range's reduction, copies
+    it back and runs adam(c0, c1) on those columns while the next ranges are still being reduced.
+    Adam is per column, so the result is the reduction followed by one Adam step over [0, n). One
+    rank: adam(0, n)."""
+    if not _dist_on(group):
+        if n > 0:
+            adam(0, n)
+        return
+    rows = grad.shape[0]
+    if packed is None or packed.numel() < rows * n:
+        packed = torch.empty(rows * n, dtype=grad.dtype, device=grad.device)
+    pending, off = [], 0
+    for c0, c1 in column_chunks(n, chunks):
+        buf = packed[off:off + rows * (c1 - c0)].view(rows, c1 - c0)
+        off += rows * (c1 - c0)
+        buf.copy_(grad[:, c0:c1])
+        pending.append((c0, c1, buf, dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group, async_op=True)))
+    for c0, c1, buf, work in pending:
+        work.wait()
+        grad[:, c0:c1].copy_(buf)
+        adam(c0, c1)
 
 
 def allreduce_sum(t: torch.Tensor, group=None) -> None:
@@ -172,6 +210,7 @@ class ShardedMapper:
         self.v = torch.zeros_like(params)
         self.grad = torch.zeros_like(params)
         self.packed = torch.empty(params.numel(), device=params.device) if self.world > 1 else None
+        self.exchange_chunks = 4   # gradient buckets overlapped with Adam (allreduce_adam)
         self.n = n
         self.n_dev = torch.tensor([n], dtype=torch.int64, device=params.device)
         self.cam = cam
@@ -268,7 +307,6 @@ class ShardedMapper:
     def step(self):
         poses = self.poses_active()
         self.render_backward()
-        allreduce_grads(self.grad, self.n, self.group, self.packed)
         if self.degenerate is not None and self.densify:   # one Eq. 9 application per expansion step
             allreduce_mask(self.dmask, self.group)
             gs_densify_prune(self.P, self.raw, self.n_dev, self.n, self.cap, None, None, None, None, None, None,
@@ -284,11 +322,17 @@ class ShardedMapper:
         self.it += 1
         self.adam_t += 1
         lr = learning_rates(self.it - 1, self.iters, rows=self.rows, sh_linear=self.ba_iters is not None)
-        if self.rows == 14:
-            gs_adam_step(self.raw, self.P, self.grad, self.m, self.v, self.n, self.cap, lr, self.adam_t)
-        else:
-            gs_adam_step_rows(self.raw, self.P, self.grad, self.m, self.v, self.n, self.cap, self.rows, lr,
-                              self.adam_t)
+
+        def adam(c0: int, c1: int):   # columns [c0, c1): pointers offset by c0, the same row stride
+            a = (self.raw[:, c0:], self.P[:, c0:], self.grad[:, c0:], self.m[:, c0:], self.v[:, c0:], c1 - c0,
+                 self.cap)
+            if self.rows == 14:
+                gs_adam_step(*a, lr, self.adam_t)
+            else:
+                gs_adam_step_rows(*a, self.rows, lr, self.adam_t)
+        # all-reduce of grad[:, :n] in column buckets, each bucket's Adam step overlapping the next
+        # buckets' reductions (the Eq. 9 degeneration and the pose steps above read no map gradient)
+        allreduce_adam(self.grad, self.n, adam, self.group, self.packed, self.exchange_chunks)
         changed = False
         if self.split_due():
             # statistics summed over ranks before the decision: identical splits and clones everywhere

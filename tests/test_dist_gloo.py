@@ -234,3 +234,64 @@ def test_gloo_world2_allreduce_and_candidate_gather():
     assert k0.tolist() == [1, 2, 3, 4]                     # global keyframe order: rank 0's, then rank 1's
     for k in range(4):
         assert (c0[k, :, : k + 1] == k).all()
+
+
+def test_column_chunks_partition_and_alignment():
+    m = _mapping_module()
+    for n, c in ((0, 4), (1, 4), (31, 4), (32, 4), (1000, 4), (2_000_000, 4), (100, 1), (100, 7)):
+        ch = m.column_chunks(n, c)
+        assert len(ch) <= max(c, 1)
+        assert [a for a, _ in ch] == sorted(a for a, _ in ch)
+        covered = [i for a, b in ch for i in range(a, b)] if n <= 2000 else None
+        if covered is not None:
+            assert covered == list(range(n))
+        else:
+            assert ch[0][0] == 0 and ch[-1][1] == n and all(b == a2 for (_, b), (a2, _) in zip(ch, ch[1:]))
+        assert all(a % 32 == 0 for a, _ in ch)
+
+
+def _adam_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = _mapping_module()
+        rows, cap, n = 14, 300, 261
+        g = torch.arange(rows * cap, dtype=torch.float32).view(rows, cap) * (rank + 1)
+        res = torch.full((rows, cap), -1.0)
+        calls = []
+
+        def adam(c0, c1):   # a per-column stand-in for the optimiser: reads the reduced gradient
+            calls.append((c0, c1))
+            res[:, c0:c1] = 2.0 * g[:, c0:c1]
+        m.allreduce_adam(g, n, adam, packed=torch.empty(rows * cap), chunks=4)
+        out[rank] = (g.numpy().copy(), res.numpy().copy(), calls)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_gloo_bucketed_allreduce_overlapped_with_adam():
+    """allreduce_adam at world sizes 2 and 3: the live columns [0, n) reduced in 32-aligned buckets,
+    each bucket's optimiser call made on its reduced values in column order; columns >= n untouched."""
+    ctx = mp.get_context("spawn")
+    for world in (2, 3):
+        mgr = ctx.Manager()
+        out = mgr.dict()
+        port = _free_port()
+        procs = [ctx.Process(target=_adam_worker, args=(r, world, port, out)) for r in range(world)]
+        for pr in procs:
+            pr.start()
+        for pr in procs:
+            pr.join(240)
+            assert pr.exitcode == 0
+        rows, cap, n = 14, 300, 261
+        base = np.arange(rows * cap, dtype=np.float32).reshape(rows, cap)
+        tot = sum(range(1, world + 1))
+        for r in range(world):
+            g, res, calls = out[r]
+            np.testing.assert_array_equal(g[:, :n], base[:, :n] * tot)
+            np.testing.assert_array_equal(g[:, n:], base[:, n:] * (r + 1))
+            np.testing.assert_array_equal(res[:, :n], 2.0 * base[:, :n] * tot)
+            assert (res[:, n:] == -1.0).all()
+            assert calls == [(0, 96), (96, 192), (192, 261)]
