@@ -185,8 +185,11 @@ __global__ void __launch_bounds__(256) project_kernel(
 #pragma unroll
     for (int g = 0; g < kProjG; ++g) {
         const int64_t i = i0 + int64_t(g) * blockDim.x;
+        // a masked-out Gaussian (tracking's fine stage) needs only its position (its depth key is
+        // still written); the other 11 rows are not read
+        const bool on = i < n && (mask == nullptr || mask[i] != 0);
 #pragma unroll
-        for (int k = 0; k < 14; ++k) p[g][k] = i < n ? __ldg(params + k * ld + i) : 0.f;
+        for (int k = 0; k < 14; ++k) p[g][k] = (k < 3 ? i < n : on) ? __ldg(params + k * ld + i) : 0.f;
     }
 #pragma unroll
     for (int g = 0; g < kProjG; ++g) {

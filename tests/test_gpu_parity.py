@@ -391,6 +391,44 @@ def test_pose_step_parity():
     np.testing.assert_allclose(V.cpu().numpy(), vref, atol=2e-6)
 
 
+# ------------------------------------------------------------------ masked projection (tracking's fine stage)
+@pytest.mark.parametrize("c", [0, 2])
+def test_masked_projection_and_render(c):
+    """gs_project with a selection mask (Eq. 12's fine stage): masked-out Gaussians are culled
+    (no tiles, zero record, rect and radius; their depth key is still the projected depth), the kept
+    ones are bit-exact with the oracle's projection, and the masked render equals the oracle's
+    render of the kept subset (same relative index order, so the same tie order)."""
+    import paper_2311_11700_b200 as g
+    cfg, p, v = scene(c)
+    n = p.shape[1]
+    keep = np.random.default_rng(40 + c).random(n) < 0.4
+    key_cap, _ = key_cap_for(p, v, cfg.cam)
+    pipe = g.RenderPipeline(n, key_cap, cfg.cam.width, cfg.cam.height)
+    P, V = to_dev(p), to_dev(v)
+    fr = pipe.forward(P, n, V, cfg.cam, mask=torch.as_tensor(keep.astype(np.uint8), device="cuda"),
+                      fwd_flags=g.GS_FLAG_EXAMINED)
+    torch.cuda.synchronize()
+    a = pipe.arrays(n)
+    full = oracle.project(p, v, cfg.cam, "f32")
+    sub = oracle.project(p[:, keep], v, cfg.cam, "f32")
+    assert np.array_equal(a["depth_key"].cpu().numpy().view(np.uint32), full["depth_bits"])
+    tiles = a["tiles"].cpu().numpy().view(np.uint32)
+    radius = a["radius"].cpu().numpy()
+    rect = a["rect"].cpu().numpy().astype(np.int32).T
+    rec = a["records"].cpu().numpy()
+    assert (tiles[~keep] == 0).all() and (radius[~keep] == 0).all() and (rect[:, ~keep] == 0).all()
+    assert (rec[~keep] == 0).all()
+    assert np.array_equal(tiles[keep], sub["tiles"]) and np.array_equal(radius[keep], sub["radius"])
+    assert np.array_equal(rect[:, keep], sub["rect"])
+    on = sub["tiles"] > 0
+    rk = rec[keep]
+    assert np.array_equal(rk[on, 0], sub["mean2d"][0, on]) and np.array_equal(rk[on, 1], sub["mean2d"][1, on])
+    assert np.array_equal(-2 * rk[on, 2], sub["conic"][0, on]) and np.array_equal(-rk[on, 3], sub["conic"][1, on])
+    o = oracle.forward(p[:, keep], v, cfg.cam, "f32")
+    compare_images({"color": fr.color, "depth": fr.depth, "alpha": fr.alpha, "n_last": a["n_last"]}, o, cfg.cam,
+                   p[:, keep], v, f"masked config {c}")
+
+
 # ------------------------------------------------------------------ densify / prune / select
 @pytest.mark.parametrize("rows", [14, 23])
 def test_densify_add_and_prune_parity(rows):
