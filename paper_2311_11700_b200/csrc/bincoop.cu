@@ -243,14 +243,19 @@ __global__ void __launch_bounds__(kCT, 1) bin_coop_kernel(CoopArgs a) {
         const uint32_t s1 = p == 0 ? base_k + ldcg(a.cta_cnt + k) : min(Vs, s0 + S2);
         // global start of each digit for this CTA: digit base (scan of the pass totals) + the
         // preceding CTAs' counts. Thread (4-bin column c4, row set rs) sums rows k' = rs, rs + 8, ...
-        // < k with 16-B loads (rows are zero beyond nbins). (Keeping per-group row sums to shorten
+        // < k with 16-B loads (rows are zero beyond nbins); CTAs in the second half sum the rows
+        // k' >= k instead (preceding = total - following). (Keeping per-group row sums to shorten
         // this walk was measured slower: the extra scatter atomics contend.)
         const uint32_t* Hp = a.H + size_t(p) * kCoopGridMax * kCoopBins;
         {
             const int c4 = tid & (kCoopBins / 4 - 1), rs = tid / (kCoopBins / 4);   // 128 x 8
             uint4 acc = make_uint4(0u, 0u, 0u, 0u);
+            // the second half of the CTAs sums the rows AFTER theirs and subtracts from the digit
+            // total, so no CTA walks more than half of the rows (the walk is the pass' critical path)
+            const bool suffix = 2 * k >= G;
+            const int klo = suffix ? k : 0, khi = suffix ? G : k;
 #pragma unroll 4
-            for (int kk = rs; kk < k; kk += kCT / (kCoopBins / 4)) {
+            for (int kk = klo + rs; kk < khi; kk += kCT / (kCoopBins / 4)) {
                 const uint4 v = __ldcg(reinterpret_cast<const uint4*>(Hp + size_t(kk) * kCoopBins) + c4);
                 acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
             }
@@ -261,6 +266,7 @@ __global__ void __launch_bounds__(kCT, 1) bin_coop_kernel(CoopArgs a) {
 #pragma unroll
                 for (int q = 0; q < kCT / (kCoopBins / 4); ++q) pre += wh[q * kCoopBins + tid];
                 tot = ldcg(a.hist_all + p * kCoopBins + tid);
+                if (suffix) pre = tot - pre;
             }
             uint32_t dbase;
             BScan(bscan).ExclusiveSum(tot, dbase);
