@@ -198,7 +198,7 @@ class ShardedMapper:
                  max_add_per_kf: int = 8192, w_color: float = 0.9, w_depth: float = 0.1, group=None,
                  densify: bool = True, ba_iters: int | None = None, lr_rho: float = 1e-3, lr_phi: float = 1e-3,
                  degenerate: tuple[float, float] | None = None, split_clone: SplitClone | None = None,
-                 iters: int = 100):
+                 iters: int = 100, pipelines: int = 2):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if self.world > 1 else 0
@@ -215,7 +215,13 @@ class ShardedMapper:
         self.n_dev = torch.tensor([n], dtype=torch.int64, device=params.device)
         self.cam = cam
         self.cm = make_camera(cam)
-        self.pipe = RenderPipeline(self.cap, key_cap, cam.width, cam.height, params.device)
+        # `pipelines` render workspaces on as many streams: keyframe j renders on pipeline j % count,
+        # so one keyframe's projection, binning and forward overlap the previous keyframe's backward
+        # (the backward chains stay in keyframe order: render_backward)
+        self.pipes = [RenderPipeline(self.cap, key_cap, cam.width, cam.height, params.device)
+                      for _ in range(max(1, pipelines))]
+        self.pipe = self.pipes[0]
+        self.side = [torch.cuda.Stream(device=params.device) for _ in self.pipes[1:]]
         self.w_color, self.w_depth = w_color, w_depth
         self.max_add = max_add_per_kf
         self.densify = densify
@@ -237,9 +243,10 @@ class ShardedMapper:
         self.splits_done = 0
         self.split_log: list | None = None   # set to [] to record each split/clone decision's inputs
         self.key_cap = key_cap
-        # the workspace's key-capacity flag is reset by every gs_bin_sort: OR it over the renders here
-        self.err_flag = self.pipe.arrays(0)["error_flag"]
-        self.err_acc = torch.zeros(1, dtype=torch.int32, device=params.device)
+        # the workspaces' key-capacity flags are reset by every gs_bin_sort: OR them over the renders
+        # here (one accumulator per pipeline: each is written from its own stream)
+        self.err_flags = [pp.arrays(0)["error_flag"] for pp in self.pipes]
+        self.err_acc = torch.zeros(len(self.pipes), dtype=torch.int32, device=params.device)
         self.cand = None
         self.set_keyframes(keyframes)
 
@@ -272,37 +279,55 @@ class ShardedMapper:
         return s is not None and self.it % s.every == 0 and self.it < s.until
 
     def render_backward(self):
-        """fwd + L1 + bwd for every local keyframe, accumulating into grad."""
+        """fwd + L1 + bwd for every local keyframe, accumulating into grad.
+        Keyframe j runs on pipeline / stream j % len(pipes); its backward call (and the split/clone
+        statistics) waits for keyframe j-1's, so the gradient sums in keyframe order exactly as one
+        pipeline would (bitwise the same), while the next keyframe's projection, binning and forward
+        overlap it."""
         self.grad[:, :self.n].zero_()
         degen = self.degenerate is not None and self.densify
         if degen:
             self.dmask.zero_()
+        cur = torch.cuda.current_stream(self.P.device)
+        streams = [cur] + self.side
+        for st in self.side:
+            st.wait_stream(cur)
+        prev = None   # event: the previous keyframe's backward chain is done
         for j, k in enumerate(self.local):
+            q = j % len(streams)
+            pipe, st = self.pipes[q], streams[q]
             kf = self.keyframes[k]
-            self.pipe.forward(self.P, self.n, kf.view, self.cam, bin_flags=GS_FLAG_NO_HOST_SYNC, fwd_flags=0)
-            torch.bitwise_or(self.err_acc, self.err_flag, out=self.err_acc)
-            if degen:   # Eq. 9 flags from this keyframe's projection, ORed over the local keyframes
-                gs_densify_prune(None, None, self.n_dev, self.n, self.cap, None, None, None, None, None, kf.depth,
-                                 None, kf.view, self.cm, densify_cfg(GS_DENSIFY_DEGENERATE_FLAG,
-                                                                     gamma=self.degenerate[1]),
-                                 self.dmask, None, self.pipe.ws)
-            gp = None
-            if self.poses_active():
-                gp = self.gpose[j]
-                gp.zero_()
-            # L1 (Eq. 6) formed inside the backward's pixel loads (gs_render_bwd_l1): no dL/dC, dL/dD images
-            color, depth, _ = self.pipe._imgs(self.cam)
-            gs_render_bwd_l1(self.P, self.n, self.P.shape[1], kf.view, self.pipe.ws, self.cm, color, depth, kf.color,
-                             kf.depth, self.w_color, self.w_depth, self.grad, gp, self.pipe.loss,
-                             GS_FLAG_POSE_COV_PATH)
-            if self.split is not None:   # reading C30 statistics of this view (NDC mean-gradient norm)
-                gs_densify_accum_grad(self.pipe.ws, self.acc, self.cnt)
-            if self.densify:   # Eq. 8 candidates from this keyframe's render (gather mode)
-                cnt = self.counts[j:j + 1]
-                gs_densify_prune(self.P, None, cnt, self.cap, self.cap, None, None, self.pipe.alpha, self.pipe.depth,
-                                 kf.color, kf.depth, None, kf.view, self.cm,
-                                 densify_cfg(GS_DENSIFY_ADD, max_add=self.max_add, rows=self.rows), None, self.cand[j],
-                                 self.pipe.ws)
+            with torch.cuda.stream(st):
+                pipe.forward(self.P, self.n, kf.view, self.cam, bin_flags=GS_FLAG_NO_HOST_SYNC, fwd_flags=0)
+                torch.bitwise_or(self.err_acc[q:q + 1], self.err_flags[q], out=self.err_acc[q:q + 1])
+                if degen:   # Eq. 9 flags from this keyframe's projection, ORed over the local keyframes
+                    gs_densify_prune(None, None, self.n_dev, self.n, self.cap, None, None, None, None, None, kf.depth,
+                                     None, kf.view, self.cm, densify_cfg(GS_DENSIFY_DEGENERATE_FLAG,
+                                                                         gamma=self.degenerate[1]),
+                                     self.dmask, None, pipe.ws)
+                gp = None
+                if self.poses_active():
+                    gp = self.gpose[j]
+                    gp.zero_()
+                if prev is not None:
+                    st.wait_event(prev)
+                # L1 (Eq. 6) formed inside the backward's pixel loads (gs_render_bwd_l1): no dL/dC, dL/dD images
+                color, depth, _ = pipe._imgs(self.cam)
+                gs_render_bwd_l1(self.P, self.n, self.P.shape[1], kf.view, pipe.ws, self.cm, color, depth, kf.color,
+                                 kf.depth, self.w_color, self.w_depth, self.grad, gp, pipe.loss,
+                                 GS_FLAG_POSE_COV_PATH)
+                if self.split is not None:   # reading C30 statistics of this view (NDC mean-gradient norm)
+                    gs_densify_accum_grad(pipe.ws, self.acc, self.cnt)
+                prev = torch.cuda.Event()
+                prev.record(st)
+                if self.densify:   # Eq. 8 candidates from this keyframe's render (gather mode)
+                    cnt = self.counts[j:j + 1]
+                    gs_densify_prune(self.P, None, cnt, self.cap, self.cap, None, None, pipe.alpha, pipe.depth,
+                                     kf.color, kf.depth, None, kf.view, self.cm,
+                                     densify_cfg(GS_DENSIFY_ADD, max_add=self.max_add, rows=self.rows), None,
+                                     self.cand[j], pipe.ws)
+        for st in self.side:
+            cur.wait_stream(st)
 
     def step(self):
         poses = self.poses_active()
@@ -369,7 +394,7 @@ class ShardedMapper:
     def sync(self) -> int:
         """One host read: the map size after densification and the workspace's key-capacity flag
         (a NO_HOST_SYNC render that overflowed its key capacity produced no lists; raise)."""
-        both = torch.stack([self.n_dev[0], self.err_acc[0].to(torch.int64)]).cpu()
+        both = torch.stack([self.n_dev[0], self.err_acc.max().to(torch.int64)]).cpu()
         self.n = int(both[0])
         if int(both[1]) != 0:
             raise RuntimeError(f"key capacity overflow in a mapping render (key_cap {self.key_cap}); raise key_cap")
