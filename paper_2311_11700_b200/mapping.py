@@ -281,9 +281,10 @@ class ShardedMapper:
     def render_backward(self):
         """fwd + L1 + bwd for every local keyframe, accumulating into grad.
         Keyframe j runs on pipeline / stream j % len(pipes); its backward call (and the split/clone
-        statistics) waits for keyframe j-1's, so the gradient sums in keyframe order exactly as one
-        pipeline would (bitwise the same), while the next keyframe's projection, binning and forward
-        overlap it."""
+        statistics) waits for keyframe j-1's, so the backward calls accumulate into grad in keyframe
+        order as with one pipeline (no two touch grad at once), while the next keyframe's projection,
+        binning and forward overlap it. (The tile pass's screen-gradient atomics already make two
+        runs differ in the last bits, with one pipeline or two.)"""
         self.grad[:, :self.n].zero_()
         degen = self.degenerate is not None and self.densify
         if degen:
