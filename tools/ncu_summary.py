@@ -87,6 +87,9 @@ def kernels(rep):
             pipes[key] = {"fma_pipe_active_pct": float(r[idx["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"]]),
                           "issue_active_pct": float(r[idx["smsp__issue_active.avg.pct_of_peak_sustained_active"]]),
                           "warps_active_pct": float(r[idx["sm__warps_active.avg.pct_of_peak_sustained_active"]]),
+                          # L1 / shared-memory side: the co-limit of the render kernels
+                          "memory_pipes_pct": float(r[idx["gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed"]]),
+                          "lsu_issue_pct": float(r[idx["sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"]]),
                           "dram_gb_per_launch": b / 1e9,
                           "source": os.path.basename(rep)}
         except (KeyError, ValueError):
