@@ -69,8 +69,15 @@ enum {
                                      [0, n) of grad_params is written (zero for off-screen Gaussians) and
                                      grad_pose = the pose gradient; no zeroing pass needed by the caller */
     GS_FLAG_OPACITY_RADIUS = 64u, /* gs_project_ex: opacity-aware radius (reading C33) */
-    GS_FLAG_BINSORT_EMIT_ONLY = 256u  /* testing: with GS_FLAG_BINSORT_KEYS, stop after key emission (the
+    GS_FLAG_BINSORT_EMIT_ONLY = 256u, /* testing: with GS_FLAG_BINSORT_KEYS, stop after key emission (the
                                      view's keys/vals then hold the unsorted index-order emission) */
+    GS_FLAG_BWD_SCREEN_ONLY = 512u,   /* gs_render_bwd[_l1]: the tile pass only: screen-space gradients into
+                                     the workspace (and the fused L1 loss); grad_params / grad_pose untouched */
+    GS_FLAG_BWD_CHAIN_ONLY = 1024u    /* gs_render_bwd[_l1]: the per-Gaussian chain only, from the screen
+                                     gradients a SCREEN_ONLY call left for the same forward (else
+                                     GS_ERR_STALE): grad_params / grad_pose as a full call. The two halves
+                                     let a caller order the accumulating halves of several workspaces'
+                                     backward passes while their tile passes overlap */
 };
 
 /* ---------------------------------------------------------------------------------------------

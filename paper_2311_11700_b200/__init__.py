@@ -33,6 +33,8 @@ GS_FLAG_BINSORT_KEYS = 16
 GS_FLAG_GRAD_ASSIGN = 32
 GS_FLAG_OPACITY_RADIUS = 64
 GS_FLAG_BINSORT_EMIT_ONLY = 256
+GS_FLAG_BWD_SCREEN_ONLY = 512
+GS_FLAG_BWD_CHAIN_ONLY = 1024
 GS_DENSIFY_ADD, GS_DENSIFY_PRUNE, GS_DENSIFY_SELECT, GS_DENSIFY_DEGENERATE = 1, 2, 3, 4
 GS_DENSIFY_DEGENERATE_FLAG, GS_DENSIFY_DEGENERATE_APPLY = 5, 6
 

@@ -222,6 +222,18 @@ static gs_status backward_common(const float* params, int64_t n, int64_t ld, con
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int mode = !pose_only ? 0 : !(flags & GS_FLAG_POSE_COV_PATH) ? 2 : (s->sh_degree == 1 ? 0 : 1);
     const int assign = (flags & GS_FLAG_GRAD_ASSIGN) ? 1 : 0;
+    const bool screen_only = (flags & GS_FLAG_BWD_SCREEN_ONLY) != 0, chain_only = (flags & GS_FLAG_BWD_CHAIN_ONLY) != 0;
+    if ((screen_only || chain_only) && (pose_only || (screen_only && chain_only))) return GS_ERR_INVALID_ARG;
+    if (chain_only) {   // the per-Gaussian chain from the screen gradients of this forward's tile pass
+        if (s->gen_screen != s->gen_fwd) return GS_ERR_STALE;
+        launch_zero(&at<Misc>(s, s->misc)->gbwd_zero_chunk, sizeof(unsigned int), st, s);
+        launch_gaussian_bwd(s, params, n, ld, viewmat, *cam, grad, grad_pose, flags, st,
+                            LossFin{nullptr, nullptr, 0.f, 0.f, 0});
+        s->gen_bwd = s->gen_fwd;
+        const gs_status rc = check_launch(s, "gs_render_bwd (chain)");
+        if (GS_DEBUG && rc == GS_OK) return dbg_after_bwd(s, st, grad, n, ld, grad_pose);
+        return rc;
+    }
     // prologue: screen accumulators [10][V_s] (rank-indexed; not needed by the paper-mode pose pass),
     // LPT tile order, fused-L1 valid count
     if (n > 0 || fuse)
@@ -234,8 +246,13 @@ static gs_status backward_common(const float* params, int64_t n, int64_t ld, con
         return rc;
     }
     // fused L1 with a pose gradient: gaussian_bwd's last block (which exists then) writes the loss
-    const bool fin_in_gbwd = fuse && fuse->loss && grad_pose && n > 0;
+    const bool fin_in_gbwd = fuse && fuse->loss && grad_pose && n > 0 && !screen_only;
     launch_render_bwd_tiles(s, *cam, nullptr, dLdC, dLdD, st, fuse, !fin_in_gbwd, mode);
+    s->gen_screen = s->gen_fwd;
+    if (screen_only) {
+        s->gen_bwd = s->gen_fwd;   // the screen gradients are there (gs_densify_accum_grad reads them)
+        return check_launch(s, "gs_render_bwd (screen)");
+    }
     LossFin lf{nullptr, nullptr, 0.f, 0.f, 0};
     if (fin_in_gbwd)
         lf = LossFin{at<Misc>(s, s->misc)->loss_acc, fuse->loss, fuse->wc, fuse->wd, int64_t(cam->width) * cam->height};

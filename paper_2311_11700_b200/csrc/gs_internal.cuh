@@ -51,6 +51,7 @@ struct WsState {
     int32_t cam_w, cam_h, cam_gx, cam_gy;   // image of the last gs_project
     uint64_t gen_project, gen_fwd; // generation counters (GS_ERR_STALE)
     uint64_t gen_bwd;              // gen_fwd of the last gs_render_bwd / gs_pose_grad
+    uint64_t gen_screen;           // gen_fwd whose screen gradients the workspace holds (tile pass done)
     int32_t sorted_in_1;           // final sorted keys/vals live in buffer 1
     int32_t keys_valid;            // path A materialised the 64-bit keys (view.keys valid)
     int64_t n_keys_host;           // K of the last host-synced gs_bin_sort (-1 unknown)

@@ -30,7 +30,8 @@ import torch
 import torch.distributed as dist
 
 from . import (GS_DENSIFY_ADD, GS_DENSIFY_DEGENERATE_APPLY, GS_DENSIFY_DEGENERATE_FLAG, GS_DENSIFY_PRUNE,
-               GS_FLAG_NO_HOST_SYNC, GS_FLAG_POSE_COV_PATH, densify_cfg, gs_adam_step, gs_adam_step_rows,
+               GS_FLAG_BWD_CHAIN_ONLY, GS_FLAG_BWD_SCREEN_ONLY, GS_FLAG_NO_HOST_SYNC, GS_FLAG_POSE_COV_PATH,
+               densify_cfg, gs_adam_step, gs_adam_step_rows,
                gs_densify_accum_grad, gs_densify_append, gs_densify_prune, gs_densify_split_clone, gs_pose_step,
                gs_render_bwd_l1, make_camera)
 from .pipeline import RenderPipeline
@@ -280,10 +281,11 @@ class ShardedMapper:
 
     def render_backward(self):
         """fwd + L1 + bwd for every local keyframe, accumulating into grad.
-        Keyframe j runs on pipeline / stream j % len(pipes); its backward call (and the split/clone
-        statistics) waits for keyframe j-1's, so the backward calls accumulate into grad in keyframe
-        order as with one pipeline (no two touch grad at once), while the next keyframe's projection,
-        binning and forward overlap it. (The tile pass's screen-gradient atomics already make two
+        Keyframe j runs on pipeline / stream j % len(pipes); its backward is split in two
+        (GS_FLAG_BWD_SCREEN_ONLY / _CHAIN_ONLY): the tile pass runs at once, the per-Gaussian chain
+        (and the split/clone statistics) waits for keyframe j-1's chain, so the chains accumulate into
+        grad in keyframe order as with one pipeline (no two touch grad at once), while the next
+        keyframe's projection, binning, forward and tile pass overlap. (The tile pass's screen-gradient atomics already make two
         runs differ in the last bits, with one pipeline or two.)"""
         self.grad[:, :self.n].zero_()
         degen = self.degenerate is not None and self.densify
@@ -310,13 +312,16 @@ class ShardedMapper:
                 if self.poses_active():
                     gp = self.gpose[j]
                     gp.zero_()
+                # L1 (Eq. 6) formed inside the backward's pixel loads (gs_render_bwd_l1): no dL/dC, dL/dD
+                # images. The tile pass (screen gradients, in this pipeline's workspace) runs at once; the
+                # per-Gaussian chain, which accumulates into grad, waits for the previous keyframe's
+                color, depth, _ = pipe._imgs(self.cam)
+                args = (self.P, self.n, self.P.shape[1], kf.view, pipe.ws, self.cm, color, depth, kf.color, kf.depth,
+                        self.w_color, self.w_depth, self.grad, gp, pipe.loss)
+                gs_render_bwd_l1(*args, GS_FLAG_POSE_COV_PATH | GS_FLAG_BWD_SCREEN_ONLY)
                 if prev is not None:
                     st.wait_event(prev)
-                # L1 (Eq. 6) formed inside the backward's pixel loads (gs_render_bwd_l1): no dL/dC, dL/dD images
-                color, depth, _ = pipe._imgs(self.cam)
-                gs_render_bwd_l1(self.P, self.n, self.P.shape[1], kf.view, pipe.ws, self.cm, color, depth, kf.color,
-                                 kf.depth, self.w_color, self.w_depth, self.grad, gp, pipe.loss,
-                                 GS_FLAG_POSE_COV_PATH)
+                gs_render_bwd_l1(*args, GS_FLAG_POSE_COV_PATH | GS_FLAG_BWD_CHAIN_ONLY)
                 if self.split is not None:   # reading C30 statistics of this view (NDC mean-gradient norm)
                     gs_densify_accum_grad(pipe.ws, self.acc, self.cnt)
                 prev = torch.cuda.Event()

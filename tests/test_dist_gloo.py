@@ -30,7 +30,8 @@ def _mapping_module():
             stub = types.ModuleType("paper_2311_11700_b200")
             stub.__path__ = [os.path.join(ROOT, "paper_2311_11700_b200")]
             for name in ("GS_DENSIFY_ADD", "GS_DENSIFY_PRUNE", "GS_FLAG_NO_HOST_SYNC", "GS_DENSIFY_DEGENERATE_APPLY",
-                         "GS_DENSIFY_DEGENERATE_FLAG", "GS_FLAG_POSE_COV_PATH"):
+                         "GS_DENSIFY_DEGENERATE_FLAG", "GS_FLAG_POSE_COV_PATH", "GS_FLAG_BWD_SCREEN_ONLY",
+                         "GS_FLAG_BWD_CHAIN_ONLY"):
                 setattr(stub, name, 0)
             for name in ("densify_cfg", "gs_adam_step", "gs_adam_step_rows", "gs_densify_append", "gs_densify_prune",
                          "make_camera", "gs_densify_accum_grad", "gs_densify_split_clone", "gs_pose_step",

@@ -375,9 +375,11 @@ def test_mapper_two_pipelines_match_one():
     # chain scale from the oracle, summed over the 4 keyframes' L1 backward passes)
     from gpu_helpers import bound_factor, check_grads
     n = p.shape[1]
+    from gpu_helpers import check_pose
     bound = np.zeros((14, n))
     chain = np.zeros((14, n))
     nl_max = 0
+    pose_bounds = []
     for v, (tc, td) in zip(views, targets):
         f = oracle.forward(p, v, cam, "f32")
         L = oracle.loss_l1(f["color"], f["depth"], tc, td, 0.9, 0.1)
@@ -385,8 +387,9 @@ def test_mapper_two_pipelines_match_one():
         ob = oracle.backward(p, v, cam, L["dL_dcolor"], L["dL_ddepth"], "f32", bound=True)
         bound += ob["grad_bound"]
         chain += ob["chain_scale"]
+        pose_bounds.append(ob["pose_bound"])
     check_grads(b["grad"].numpy(), a["grad"].numpy(), bound, "2 pipelines vs 1", k=bound_factor(nl_max), chain=chain)
-    for k in ("acc", "gpose"):   # sums of per-Gaussian terms (atomics / per-block partials): relative to the row
-        x, y = a[k].double(), b[k].double()
-        scale = x.abs().amax(dim=-1, keepdim=True)
-        assert ((x - y).abs() <= 1e-3 * x.abs() + 1e-4 * scale).all(), (k, float(((x - y).abs() / scale).max()))
+    for j, pb in enumerate(pose_bounds):   # each keyframe's twist under its own summation bound
+        check_pose(b["gpose"][j].numpy(), a["gpose"][j].numpy(), pb, f"keyframe {j} twist", k=bound_factor(nl_max))
+    x, y = a["acc"].double(), b["acc"].double()   # split/clone statistics: sums of per-view norms
+    assert ((x - y).abs() <= 1e-3 * x.abs() + 1e-4 * x.abs().max()).all()

@@ -391,6 +391,57 @@ def test_pose_step_parity():
     np.testing.assert_allclose(V.cpu().numpy(), vref, atol=2e-6)
 
 
+# ------------------------------------------------------------------ split backward (tile pass | chain)
+@pytest.mark.parametrize("c", [0, 1])
+def test_split_backward_matches_full(c):
+    """gs_render_bwd_l1 with GS_FLAG_BWD_SCREEN_ONLY then GS_FLAG_BWD_CHAIN_ONLY (the mapper's
+    overlapped keyframes) against one full call on the same forward: gradients and twist within the
+    summation bound of DESIGN.md §4.3 (the tile pass's screen-gradient atomics differ run to run),
+    the loss within 1e-12; two chains from one tile pass identical bit for bit (assign); a chain
+    without its tile pass is stale; invalid flag combinations are rejected."""
+    import paper_2311_11700_b200 as g
+    cfg, p, v = scene(c)
+    n = p.shape[1]
+    pipe, P, V, fr = run_forward(p, v, cfg.cam, flags_bin=g.GS_FLAG_NO_HOST_SYNC, fwd_flags=0)
+    tc, td = (to_dev(x) for x in gi.random_images(cfg.cam.width, cfg.cam.height, 60 + c, 0.5, 3.0))
+    cm = g.make_camera(cfg.cam)
+    base = g.GS_FLAG_POSE_COV_PATH | g.GS_FLAG_GRAD_ASSIGN
+
+    def call(flags, grad, gp, loss):
+        g.gs_render_bwd_l1(P, n, n, V, pipe.ws, cm, fr.color, fr.depth, tc, td, 0.9, 0.1, grad, gp, loss, flags)
+
+    def bufs():
+        return torch.zeros_like(P), torch.zeros(6, dtype=torch.float64, device="cuda"), \
+            torch.zeros(1, dtype=torch.float64, device="cuda")
+    gf, pf, lf = bufs()
+    call(base, gf, pf, lf)
+    gs, ps, ls = bufs()
+    call(base | g.GS_FLAG_BWD_SCREEN_ONLY, gs, ps, ls)
+    assert not gs.any() and not ps.any()   # the tile pass alone writes no parameter or pose gradient
+    call(base | g.GS_FLAG_BWD_CHAIN_ONLY, gs, ps, ls)
+    g2, p2, l2 = bufs()
+    call(base | g.GS_FLAG_BWD_CHAIN_ONLY, g2, p2, l2)
+    torch.cuda.synchronize()
+    assert torch.equal(gs, g2) and torch.equal(ps, p2)
+    assert abs(ls.item() - lf.item()) <= 1e-12 * abs(lf.item()) and l2.item() == 0.0
+    t = oracle.forward(p, v, cfg.cam, "f32")
+    L = oracle.loss_l1(t["color"], t["depth"], tc.cpu().numpy(), td.cpu().numpy(), 0.9, 0.1)
+    ob = oracle.backward(p, v, cfg.cam, L["dL_dcolor"], L["dL_ddepth"], "f32", bound=True)
+    check_grads(gs.cpu().numpy(), gf.cpu().numpy(), ob["grad_bound"], f"split vs full, config {c}",
+                k=bound_factor(int(t["n_last"].max())), chain=ob["chain_scale"])
+    check_pose(ps.cpu().numpy(), pf.cpu().numpy(), ob["pose_bound"], f"split vs full twist, config {c}",
+               k=bound_factor(int(t["n_last"].max())))
+    # a new forward invalidates the tile pass: the chain alone is stale
+    pipe.forward(P, n, V, cfg.cam, bin_flags=g.GS_FLAG_NO_HOST_SYNC, fwd_flags=0)
+    with pytest.raises(g.GSError, match="STALE"):
+        call(base | g.GS_FLAG_BWD_CHAIN_ONLY, g2, p2, l2)
+    with pytest.raises(g.GSError):
+        call(base | g.GS_FLAG_BWD_CHAIN_ONLY | g.GS_FLAG_BWD_SCREEN_ONLY, g2, p2, l2)
+    with pytest.raises(g.GSError):
+        g.gs_pose_grad_l1(P, n, n, V, pipe.ws, cm, fr.color, fr.depth, tc, td, 0.9, 0.1, p2, l2,
+                          base | g.GS_FLAG_BWD_SCREEN_ONLY)
+
+
 # ------------------------------------------------------------------ masked projection (tracking's fine stage)
 @pytest.mark.parametrize("c", [0, 2])
 def test_masked_projection_and_render(c):
