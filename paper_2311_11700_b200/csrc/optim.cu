@@ -542,7 +542,7 @@ void launch_adam(float* raw, float* act, const float* g, float* m, float* v, int
                        reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(m) |
                        reinterpret_cast<uintptr_t>(v)) & 15) == 0;
     const int64_t work = vec ? (n + 3) / 4 : n;
-    dim3 grid(unsigned(std::min<int64_t>((work + 255) / 256, sm_count() * 2)), unsigned(rows));
+    dim3 grid(unsigned(std::min<int64_t>((work + 255) / 256, sm_count() * 8)), unsigned(rows));
     adam_kernel<<<grid, 256, 0, st>>>(raw, act, g, m, v, n, ld, l, b1, b2, eps, bc1, bc2, vec);
 }
 
