@@ -70,3 +70,17 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_flag_and_status_values_match_the_header(gslib):
+    """Every GS_FLAG_* / GS_DENSIFY_* / GS_OK / GS_ERR_* value the binding exports equals the header's."""
+    src = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    vals = {name: int(v) for name, v in re.findall(r"\b((?:GS_FLAG|GS_DENSIFY|GS_ERR|GS_OK)[A-Z0-9_]*)\s*=\s*(\d+)u?", src)}
+    assert len(vals) >= 10
+    for name, v in vals.items():
+        if hasattr(gslib, name):
+            assert getattr(gslib, name) == v, name
+    for name in ("GS_FLAG_BWD_SCREEN_ONLY", "GS_FLAG_BWD_CHAIN_ONLY", "GS_FLAG_GRAD_ASSIGN", "GS_FLAG_NO_HOST_SYNC"):
+        assert name in vals and getattr(gslib, name) == vals[name]
+    flags = [v for k, v in vals.items() if k.startswith("GS_FLAG")]
+    assert all(f & (f - 1) == 0 for f in flags) and len(set(flags)) == len(flags)   # distinct single bits
